@@ -1,0 +1,759 @@
+/* absim_oracle.c — TEST INFRASTRUCTURE ONLY: CPU restatement of the
+ * reference hot path, used solely as the checker by tests/, smoke() and
+ * bench.py's cpu_baseline leg. Never linked into the product.
+ *
+ * Pinned against (a) the unmodified reference compiled by oracle/Makefile
+ * (oracle/_ref/libabsim_ref.so; tests/test_oracle_vs_reference.py compares
+ * every output bit-for-bit) and (b) the golden fixtures in tests/golden/.
+ *
+ * Semantics follow the reference with ONE worker and ONE domain (the only
+ * bitwise-deterministic mode, test_scheduler.cpp:196-212):
+ *   grid build        uniform_grid.cpp:155-266 (pass 1, sizing, LIFO chains)
+ *   box_index_of      uniform_grid.cpp:124-133
+ *   for_each_neighbor uniform_grid.cpp:268-326 (z,y,x boxes; chain order)
+ *   pairwise force    mechanics.cpp:10-27
+ *   run_forces        simulation.cpp:463-489
+ *   integration       agent.hpp:115-133, simulation.cpp:491-500
+ *   staticness        simulation.cpp:334-386, flags agent.hpp:61-101
+ *   commit            commit.cpp:86-178 (5-step removal), :236-297 (appends),
+ *                     mark_new_agent_neighbors simulation.cpp:510-530
+ *   morton / offsets  morton.cpp:11-186
+ *   sort_and_balance  sort_balance.cpp:22-148 (single domain)
+ *   prefix sum        prefix_sum.cpp:11-51
+ *   schedule          simulation.cpp:222-322
+ * Model behaviours come from include/absim_models.h (shared definitions).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "absim_models.h"
+
+#define ORC_NIL UINT64_MAX
+#define F_STATIC 1u
+#define F_MOVED 2u
+#define F_GREW 4u
+#define F_NEWLY_ADDED 8u
+#define F_NVIOL 16u
+#define F_NNEW 32u
+#define F_SELF_FORCE 64u
+
+static char g_err[512];
+const char* orc_last_error(void) { return g_err; }
+static int fail(const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return -1;
+}
+
+typedef struct {
+  uint64_t seed;
+  int32_t threads, domains; /* ignored: always one worker, one domain */
+  double dt, k, max_disp, threshold, fixed_box;
+  uint64_t sorting_frequency;
+  int32_t detect_static;
+  int32_t model; /* 0 none, 1 volume grow/divide, 2 drive, 3 grow */
+  double mp[8];
+} orc_params;
+
+typedef struct {
+  orc_params p;
+  uint64_t n, cap;
+  uint64_t* uid;
+  double *x, *y, *z, *d;
+  double *tx, *ty, *tz, *tg; /* pending translation / growth */
+  double *fx, *fy, *fz;
+  uint32_t* partners;
+  uint8_t* flags;
+  uint8_t* beh;
+  double* vol;
+  uint64_t uid_counter, iteration;
+  uint64_t evals, skips, added, removed, sorted;
+  /* grid */
+  double origin[3], box, dmax;
+  uint32_t dims[3];
+  uint64_t indexed, nboxes, box_cap;
+  uint64_t* head;
+  uint64_t* succ;
+  uint32_t* count;
+  /* staged additions */
+  uint64_t nstage, stage_cap;
+  uint64_t* s_uid;
+  double *s_x, *s_y, *s_z, *s_d, *s_vol;
+  uint8_t* s_beh;
+} orc_sim;
+
+static void* xrealloc(void* p, size_t n) {
+  void* q = realloc(p, n ? n : 1);
+  if (!q) abort();
+  return q;
+}
+
+static void reserve(orc_sim* s, uint64_t want) {
+  if (want <= s->cap) return;
+  uint64_t c = s->cap ? s->cap : 16;
+  while (c < want) c *= 2;
+#define GROW(f) s->f = xrealloc(s->f, c * sizeof(*s->f))
+  GROW(uid); GROW(x); GROW(y); GROW(z); GROW(d); GROW(tx); GROW(ty); GROW(tz);
+  GROW(tg); GROW(fx); GROW(fy); GROW(fz); GROW(partners); GROW(flags); GROW(beh);
+  GROW(vol); GROW(succ);
+#undef GROW
+  s->cap = c;
+}
+
+static void init_slot(orc_sim* s, uint64_t i, uint64_t uid, double x, double y, double z,
+                      double d, uint8_t beh, double vol, uint8_t flags) {
+  s->uid[i] = uid;
+  s->x[i] = x; s->y[i] = y; s->z[i] = z; s->d[i] = d;
+  s->tx[i] = s->ty[i] = s->tz[i] = s->tg[i] = 0.0;
+  s->fx[i] = s->fy[i] = s->fz[i] = 0.0;
+  s->partners[i] = 0;
+  s->flags[i] = flags;
+  s->beh[i] = beh;
+  s->vol[i] = vol;
+}
+
+orc_sim* orc_create(const orc_params* p, uint64_t n, const double* x, const double* y,
+                    const double* z, const double* d, const uint8_t* mask) {
+  orc_sim* s = calloc(1, sizeof *s);
+  s->p = *p;
+  reserve(s, n);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!(d[i] > 0.0)) { /* agent.hpp:25 */
+      free(s);
+      fail("diameter must be > 0");
+      return NULL;
+    }
+    const uint8_t b = (mask == NULL || mask[i]) && p->model != 0;
+    init_slot(s, i, i, x[i], y[i], z[i], d[i], b,
+              p->model == 1 ? abs_volume_of_diameter(d[i]) : 0.0, 0);
+  }
+  s->n = n;
+  s->uid_counter = n;
+  s->dims[0] = s->dims[1] = s->dims[2] = 1;
+  return s;
+}
+
+void orc_destroy(orc_sim* s) {
+  if (!s) return;
+  free(s->uid); free(s->x); free(s->y); free(s->z); free(s->d); free(s->tx);
+  free(s->ty); free(s->tz); free(s->tg); free(s->fx); free(s->fy); free(s->fz);
+  free(s->partners); free(s->flags); free(s->beh); free(s->vol); free(s->succ);
+  free(s->head); free(s->count); free(s->s_uid); free(s->s_x); free(s->s_y);
+  free(s->s_z); free(s->s_d); free(s->s_vol); free(s->s_beh);
+  free(s);
+}
+
+/* ---- uniform grid ------------------------------------------------------ */
+
+/* uniform_grid.cpp:124-133 */
+static uint64_t box_index_of(const orc_sim* s, double px, double py, double pz) {
+  const double p[3] = {px, py, pz};
+  uint64_t c[3];
+  for (int k = 0; k < 3; ++k) {
+    const double rel = (p[k] - s->origin[k]) / s->box;
+    int64_t i = (int64_t)floor(rel);
+    if (i < 0) i = 0;
+    if (i > (int64_t)s->dims[k] - 1) i = (int64_t)s->dims[k] - 1;
+    c[k] = (uint64_t)i;
+  }
+  return c[0] + s->dims[0] * (c[1] + (uint64_t)s->dims[1] * c[2]);
+}
+
+/* std::min / std::max argument order (b < a ? b : a), uniform_grid.cpp:191-194 */
+static double smin(double a, double b) { return b < a ? b : a; }
+static double smax(double a, double b) { return a < b ? b : a; }
+
+/* uniform_grid.cpp:155-266 with one worker */
+int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) {
+  s->indexed = s->n;
+  if (s->n == 0) {
+    s->dims[0] = s->dims[1] = s->dims[2] = 1;
+    s->origin[0] = s->origin[1] = s->origin[2] = 0.0;
+    s->box = s->p.fixed_box > 0.0 ? s->p.fixed_box : 1.0;
+    s->dmax = 0.0;
+    s->nboxes = 1;
+  } else {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double dm = 0.0;
+    for (uint64_t i = 0; i < s->n; ++i) {
+      const double p[3] = {s->x[i], s->y[i], s->z[i]};
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = smin(lo[k], p[k]);
+        hi[k] = smax(hi[k], p[k]);
+      }
+      dm = smax(dm, s->d[i]);
+    }
+    for (int k = 0; k < 3; ++k)
+      if (!isfinite(lo[k]) || !isfinite(hi[k])) return fail("agent positions are not finite");
+    s->dmax = dm;
+    if (s->p.fixed_box > 0.0) {
+      if (dm > s->p.fixed_box) return fail("fixed box length is smaller than the largest agent diameter");
+      s->box = s->p.fixed_box;
+    } else {
+      s->box = dm;
+    }
+    uint64_t needed = 1;
+    for (int k = 0; k < 3; ++k) {
+      s->origin[k] = lo[k];
+      uint64_t nk = (uint64_t)floor((hi[k] - lo[k]) / s->box) + 1;
+      s->dims[k] = (uint32_t)(nk < 1 ? 1 : nk);
+      needed *= s->dims[k];
+    }
+    if (needed > (1ull << 31)) return fail("grid would exceed the box budget");
+    s->nboxes = needed;
+  }
+  if (s->nboxes > s->box_cap) {
+    s->head = xrealloc(s->head, s->nboxes * sizeof *s->head);
+    s->count = xrealloc(s->count, s->nboxes * sizeof *s->count);
+    s->box_cap = s->nboxes;
+  }
+  for (uint64_t b = 0; b < s->nboxes; ++b) {
+    s->head[b] = ORC_NIL;
+    s->count[b] = 0;
+  }
+  if (s->n) {
+    for (uint64_t i = 0; i < s->n; ++i) { /* :249-265, LIFO chains */
+      const uint64_t b = box_index_of(s, s->x[i], s->y[i], s->z[i]);
+      s->succ[i] = s->head[b];
+      s->head[b] = i;
+      s->count[b]++;
+    }
+  }
+  if (grid) {
+    grid[0] = s->origin[0]; grid[1] = s->origin[1]; grid[2] = s->origin[2];
+    grid[3] = s->box; grid[4] = s->dmax;
+  }
+  if (dims) { dims[0] = s->dims[0]; dims[1] = s->dims[1]; dims[2] = s->dims[2]; }
+  if (indexed) *indexed = s->indexed;
+  return 0;
+}
+
+typedef void (*visit_fn)(orc_sim* s, void* ctx, uint64_t j, double d2);
+
+/* uniform_grid.cpp:268-326; query == ORC_NIL means no exclusion */
+static int for_each_neighbor(orc_sim* s, uint64_t query, double cx, double cy, double cz,
+                             double r2, visit_fn fn, void* ctx) {
+  if (s->indexed == 0) return 0;
+  if (r2 > s->box * s->box * (1.0 + 1e-12)) return fail("query radius exceeds the grid box length");
+  const double radius = sqrt(r2);
+  const double c[3] = {cx, cy, cz};
+  int64_t lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) {
+    int64_t a = (int64_t)floor((c[k] - radius - s->origin[k]) / s->box);
+    int64_t b = (int64_t)floor((c[k] + radius - s->origin[k]) / s->box);
+    lo[k] = a > 0 ? a : 0;
+    hi[k] = b < (int64_t)s->dims[k] - 1 ? b : (int64_t)s->dims[k] - 1;
+  }
+  const double cull = r2 * (1.0 + 1e-12);
+  for (int64_t z = lo[2]; z <= hi[2]; ++z)
+    for (int64_t y = lo[1]; y <= hi[1]; ++y)
+      for (int64_t x = lo[0]; x <= hi[0]; ++x) {
+        double min_d2 = 0.0;
+        const int64_t at[3] = {x, y, z};
+        for (int k = 0; k < 3; ++k) {
+          const double b0 = s->origin[k] + (double)at[k] * s->box;
+          const double b1 = b0 + s->box;
+          const double gap = c[k] < b0 ? b0 - c[k] : (c[k] > b1 ? c[k] - b1 : 0.0);
+          min_d2 += gap * gap;
+        }
+        if (min_d2 > cull) continue;
+        uint64_t j = s->head[(uint64_t)x + s->dims[0] * ((uint64_t)y + (uint64_t)s->dims[1] * (uint64_t)z)];
+        while (j != ORC_NIL) {
+          if (j != query) {
+            const double dx = cx - s->x[j], dy = cy - s->y[j], dz = cz - s->z[j];
+            const double d2 = (dx * dx + dy * dy) + dz * dz; /* vec3.hpp:44 */
+            if (d2 <= r2) fn(s, ctx, j, d2);
+          }
+          j = s->succ[j];
+        }
+      }
+  return 0;
+}
+
+int orc_cell_ids(const orc_sim* s, uint64_t* out) {
+  for (uint64_t i = 0; i < s->n; ++i) out[i] = box_index_of(s, s->x[i], s->y[i], s->z[i]);
+  return 0;
+}
+
+typedef struct {
+  uint64_t* buf;
+  uint64_t n, cap;
+} uidvec;
+static void collect_uid(orc_sim* s, void* ctx, uint64_t j, double d2) {
+  (void)d2;
+  uidvec* v = ctx;
+  if (v->n == v->cap) {
+    v->cap = v->cap ? v->cap * 2 : 64;
+    v->buf = xrealloc(v->buf, v->cap * sizeof *v->buf);
+  }
+  v->buf[v->n++] = s->uid[j];
+}
+static int cmp_u64(const void* a, const void* b) {
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* Sorted force-query neighbour uids per agent (simulation.cpp:469). */
+int64_t orc_neighbors(orc_sim* s, uint64_t* offsets, uint64_t* uids, uint64_t cap) {
+  uidvec v = {0};
+  uint64_t pos = 0;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    v.n = 0;
+    const double r = 0.5 * (s->d[i] + s->dmax);
+    if (for_each_neighbor(s, i, s->x[i], s->y[i], s->z[i], r * r, collect_uid, &v)) {
+      free(v.buf);
+      return -1;
+    }
+    qsort(v.buf, v.n, sizeof(uint64_t), cmp_u64);
+    offsets[i] = pos;
+    for (uint64_t k = 0; k < v.n; ++k, ++pos)
+      if (pos < cap) uids[pos] = v.buf[k];
+  }
+  offsets[s->n] = pos;
+  free(v.buf);
+  return pos > cap ? -2 : (int64_t)pos;
+}
+
+/* ---- mechanics ----------------------------------------------------------- */
+
+/* random.hpp:47-52 unit_vector via RandomStream(seed=lo uid, stream=hi uid, counter 0) */
+static void coincident_dir(uint64_t lo, uint64_t hi, double out[3]) {
+  const double u0 = abs_u01(abs_rng_word(lo, hi, 0));
+  const double u1 = abs_u01(abs_rng_word(lo, hi, 1));
+  const double zz = -1.0 + (1.0 - -1.0) * u0;
+  const double phi = 0.0 + (2.0 * ABS_PI - 0.0) * u1;
+  const double r = sqrt(smax(0.0, 1.0 - zz * zz));
+  out[0] = r * cos(phi);
+  out[1] = r * sin(phi);
+  out[2] = zz;
+}
+
+/* mechanics.cpp:10-27 */
+static void pairwise_repulsion(const orc_sim* s, uint64_t a, uint64_t b, double k, double f[3]) {
+  const double dx = s->x[a] - s->x[b], dy = s->y[a] - s->y[b], dz = s->z[a] - s->z[b];
+  const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+  const double overlap = 0.5 * (s->d[a] + s->d[b]) - dist;
+  f[0] = f[1] = f[2] = 0.0;
+  if (overlap <= 0.0) return;
+  if (dist > 0.0) {
+    const double sc = k * overlap / dist;
+    f[0] = dx * sc; f[1] = dy * sc; f[2] = dz * sc;
+    return;
+  }
+  const uint64_t lo = s->uid[a] < s->uid[b] ? s->uid[a] : s->uid[b];
+  const uint64_t hi = s->uid[a] < s->uid[b] ? s->uid[b] : s->uid[a];
+  double dir[3];
+  coincident_dir(lo, hi, dir);
+  if (s->uid[a] != lo) { dir[0] *= -1.0; dir[1] *= -1.0; dir[2] *= -1.0; }
+  const double m = k * overlap;
+  f[0] = dir[0] * m; f[1] = dir[1] * m; f[2] = dir[2] * m;
+}
+
+typedef struct {
+  uint64_t a, evals;
+  uint32_t contributors;
+  double t[3];
+} force_ctx;
+static void force_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
+  (void)d2;
+  force_ctx* c = vctx;
+  c->evals++;
+  double f[3];
+  pairwise_repulsion(s, c->a, j, s->p.k, f);
+  if ((f[0] * f[0] + f[1] * f[1]) + f[2] * f[2] > 0.0) {
+    c->contributors++;
+    c->t[0] += f[0]; c->t[1] += f[1]; c->t[2] += f[2];
+  }
+}
+
+/* simulation.cpp:463-489 */
+static int run_forces(orc_sim* s, uint64_t i) {
+  if (s->p.detect_static && (s->flags[i] & F_STATIC)) {
+    s->skips++;
+    return 0;
+  }
+  const double r = 0.5 * (s->d[i] + s->dmax);
+  force_ctx c = {i, 0, 0, {0.0, 0.0, 0.0}};
+  if (for_each_neighbor(s, i, s->x[i], s->y[i], s->z[i], r * r, force_visit, &c)) return -1;
+  s->evals += c.evals;
+  s->fx[i] = c.t[0]; s->fy[i] = c.t[1]; s->fz[i] = c.t[2];
+  s->partners[i] = c.contributors;
+  const double n2 = (c.t[0] * c.t[0] + c.t[1] * c.t[1]) + c.t[2] * c.t[2];
+  if (n2 > s->p.threshold * s->p.threshold) {
+    s->tx[i] += c.t[0] * s->p.dt;
+    s->ty[i] += c.t[1] * s->p.dt;
+    s->tz[i] += c.t[2] * s->p.dt;
+  }
+  return 0;
+}
+
+/* agent.hpp:115-133 */
+static void apply_pending(orc_sim* s, uint64_t i) {
+  double tx = s->tx[i], ty = s->ty[i], tz = s->tz[i];
+  const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
+  if (disp > 0.0) {
+    if (disp > s->p.max_disp) {
+      const double sc = s->p.max_disp / disp;
+      tx *= sc; ty *= sc; tz *= sc;
+    }
+    s->x[i] += tx; s->y[i] += ty; s->z[i] += tz;
+    s->flags[i] |= F_MOVED;
+  }
+  if (s->tg[i] != 0.0) {
+    const double dd = s->d[i] + s->tg[i];
+    s->d[i] = dd > 1e-9 ? dd : 1e-9;
+    if (s->tg[i] > 0.0) s->flags[i] |= F_GREW;
+  }
+  s->tx[i] = s->ty[i] = s->tz[i] = s->tg[i] = 0.0;
+}
+
+/* ---- staticness (simulation.cpp:334-386) ------------------------------- */
+typedef struct {
+  uint8_t set;
+} mark_ctx;
+static void mark_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
+  (void)d2;
+  s->flags[j] |= ((mark_ctx*)vctx)->set;
+}
+
+static int run_staticness(orc_sim* s) {
+  const uint8_t reset = F_MOVED | F_GREW | F_SELF_FORCE | F_NEWLY_ADDED | F_NVIOL | F_NNEW;
+  if (s->iteration == 0) {
+    for (uint64_t i = 0; i < s->n; ++i) s->flags[i] &= (uint8_t)~(reset | F_STATIC);
+    return 0;
+  }
+  for (uint64_t i = 0; i < s->n; ++i) {
+    const int disturbs = (s->flags[i] & (F_MOVED | F_GREW)) != 0;
+    const int fresh = (s->flags[i] & F_NEWLY_ADDED) != 0;
+    if (!disturbs && !fresh) continue;
+    const double r = 0.5 * (s->d[i] + s->dmax);
+    mark_ctx m = {(uint8_t)((disturbs ? F_NVIOL : 0) | (fresh ? F_NNEW : 0))};
+    if (for_each_neighbor(s, i, s->x[i], s->y[i], s->z[i], r * r, mark_visit, &m)) return -1;
+  }
+  for (uint64_t i = 0; i < s->n; ++i) {
+    const int skip = !(s->flags[i] & (F_MOVED | F_GREW | F_SELF_FORCE | F_NEWLY_ADDED | F_NVIOL | F_NNEW)) &&
+                     s->partners[i] <= 1;
+    s->flags[i] = (uint8_t)((s->flags[i] & ~(reset | F_STATIC)) | (skip ? F_STATIC : 0));
+  }
+  return 0;
+}
+
+/* ---- behaviours (absim_models.h / models.hpp:69-83) -------------------- */
+static void stage_daughter(orc_sim* s, double x, double y, double z, double d, double vol) {
+  if (s->nstage == s->stage_cap) {
+    s->stage_cap = s->stage_cap ? 2 * s->stage_cap : 64;
+    s->s_uid = xrealloc(s->s_uid, s->stage_cap * sizeof *s->s_uid);
+    s->s_x = xrealloc(s->s_x, s->stage_cap * sizeof *s->s_x);
+    s->s_y = xrealloc(s->s_y, s->stage_cap * sizeof *s->s_y);
+    s->s_z = xrealloc(s->s_z, s->stage_cap * sizeof *s->s_z);
+    s->s_d = xrealloc(s->s_d, s->stage_cap * sizeof *s->s_d);
+    s->s_vol = xrealloc(s->s_vol, s->stage_cap * sizeof *s->s_vol);
+    s->s_beh = xrealloc(s->s_beh, s->stage_cap * sizeof *s->s_beh);
+  }
+  const uint64_t k = s->nstage++;
+  s->s_uid[k] = s->uid_counter++; /* resource_manager.hpp:44-46 at creation */
+  s->s_x[k] = x; s->s_y[k] = y; s->s_z[k] = z; s->s_d[k] = d;
+  s->s_vol[k] = vol;
+  s->s_beh[k] = 1;
+}
+
+static int run_behaviour(orc_sim* s, uint64_t i) {
+  if (!s->beh[i]) return 0;
+  const orc_params* p = &s->p;
+  if (p->model == 1) {
+    s->vol[i] += p->mp[0];
+    if (s->vol[i] > p->mp[1]) {
+      s->vol[i] *= 0.5;
+      double dir[3];
+      abs_unit_vector(p->seed, s->uid[i], ABS_RNG_DIVISION_BASE(s->iteration), dir);
+      const double half = 0.5 * s->d[i];
+      const double dd = abs_diameter_of_volume(s->vol[i]);
+      if (!(dd > 0.0)) return fail("diameter must be > 0");
+      stage_daughter(s, s->x[i] + dir[0] * half, s->y[i] + dir[1] * half,
+                     s->z[i] + dir[2] * half, dd, s->vol[i]);
+    }
+    s->tg[i] += abs_diameter_of_volume(s->vol[i]) - s->d[i];
+  } else if (p->model == 2) {
+    double dl[3];
+    abs_drive_delta(s->x[i], s->y[i], s->z[i], p->mp[0], p->mp[1], p->mp[2], p->mp[3],
+                    p->seed, s->uid[i], s->iteration, dl);
+    s->tx[i] += dl[0]; s->ty[i] += dl[1]; s->tz[i] += dl[2];
+  } else if (p->model == 3) { /* models::Grow (models.hpp:69-83) */
+    const double cap = p->mp[1];
+    if (s->d[i] < cap) {
+      const double rem = cap - s->d[i];
+      s->tg[i] += rem < p->mp[0] ? rem : p->mp[0];
+    }
+  }
+  return 0;
+}
+
+/* ---- commit ---------------------------------------------------------------- */
+
+static void nn_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
+  (void)vctx; (void)d2;
+  s->flags[j] |= F_NNEW;
+}
+
+/* simulation.cpp:510-530: start-of-step grid, live positions, no exclusion */
+static int mark_new_agent_neighbors(orc_sim* s) {
+  for (uint64_t k = 0; k < s->nstage; ++k) {
+    const double r = 0.5 * (s->s_d[k] + s->dmax);
+    if (r <= s->box) {
+      if (for_each_neighbor(s, ORC_NIL, s->s_x[k], s->s_y[k], s->s_z[k], r * r, nn_visit, NULL)) return -1;
+    } else {
+      for (uint64_t j = 0; j < s->n; ++j) {
+        const double dx = s->s_x[k] - s->x[j], dy = s->s_y[k] - s->y[j], dz = s->s_z[k] - s->z[j];
+        if ((dx * dx + dy * dy) + dz * dz <= r * r) s->flags[j] |= F_NNEW;
+      }
+    }
+  }
+  return 0;
+}
+
+static void move_slot(orc_sim* s, uint64_t dst, uint64_t src) {
+  s->uid[dst] = s->uid[src];
+  s->x[dst] = s->x[src]; s->y[dst] = s->y[src]; s->z[dst] = s->z[src]; s->d[dst] = s->d[src];
+  s->tx[dst] = s->tx[src]; s->ty[dst] = s->ty[src]; s->tz[dst] = s->tz[src]; s->tg[dst] = s->tg[src];
+  s->fx[dst] = s->fx[src]; s->fy[dst] = s->fy[src]; s->fz[dst] = s->fz[src];
+  s->partners[dst] = s->partners[src];
+  s->flags[dst] = s->flags[src];
+  s->beh[dst] = s->beh[src];
+  s->vol[dst] = s->vol[src];
+}
+
+/* commit.cpp:86-178 (five steps, slot semantics independent of workers) */
+int orc_remove(orc_sim* s, const uint32_t* removed, uint32_t r) {
+  if (r == 0) return 0;
+  if (r > s->n) return fail("more removals than agents");
+  const uint64_t new_size = s->n - r;
+  uint32_t* to_right = malloc(r * sizeof *to_right);
+  uint32_t* tail = calloc(r, sizeof *tail);
+  for (uint32_t k = 0; k < r; ++k) {
+    to_right[k] = UINT32_MAX;
+    if (removed[k] < new_size) to_right[k] = removed[k];
+    else tail[removed[k] - new_size] = 1;
+  }
+  uint32_t holes = 0, movers = 0;
+  for (uint32_t k = 0; k < r; ++k) {
+    if (to_right[k] != UINT32_MAX) to_right[holes++] = to_right[k];
+    if (tail[k] == 0) tail[movers++] = (uint32_t)(k + new_size);
+  }
+  if (holes != movers) {
+    free(to_right); free(tail);
+    return fail("removal bookkeeping out of balance");
+  }
+  for (uint32_t k = 0; k < holes; ++k) move_slot(s, to_right[k], tail[k]);
+  s->n = new_size;
+  s->removed += r;
+  free(to_right); free(tail);
+  return 0;
+}
+
+/* commit.cpp:236-297 with one staging slot */
+static int run_commit(orc_sim* s) {
+  if (s->nstage == 0) return 0;
+  if (s->p.detect_static && mark_new_agent_neighbors(s)) return -1;
+  reserve(s, s->n + s->nstage);
+  for (uint64_t k = 0; k < s->nstage; ++k)
+    init_slot(s, s->n + k, s->s_uid[k], s->s_x[k], s->s_y[k], s->s_z[k], s->s_d[k],
+              s->s_beh[k], s->s_vol[k], F_NEWLY_ADDED);
+  s->n += s->nstage;
+  s->added += s->nstage;
+  s->nstage = 0;
+  return 0;
+}
+
+/* ---- morton (morton.cpp:11-186) ---------------------------------------- */
+static uint64_t spread3(uint64_t v) {
+  uint64_t out = 0;
+  for (int i = 0; i < 21; ++i) out |= ((v >> i) & 1ull) << (3 * i);
+  return out;
+}
+static uint64_t compact3(uint64_t v) {
+  uint64_t out = 0;
+  for (int i = 0; i < 21; ++i) out |= ((v >> (3 * i)) & 1ull) << i;
+  return out;
+}
+int orc_morton_encode3(uint32_t x, uint32_t y, uint32_t z, uint64_t* out) {
+  if (x >= (1u << 21) || y >= (1u << 21) || z >= (1u << 21)) return fail("3D coordinates limited to 21 bits");
+  *out = spread3(x) | spread3(y) << 1 | spread3(z) << 2;
+  return 0;
+}
+void orc_morton_decode3(uint64_t c, uint32_t* out) {
+  out[0] = (uint32_t)compact3(c);
+  out[1] = (uint32_t)compact3(c >> 1);
+  out[2] = (uint32_t)compact3(c >> 2);
+}
+
+typedef struct {
+  uint32_t dims[3];
+  int d;
+  uint64_t counter, offset;
+  int found_gap;
+  uint64_t* start;
+  uint64_t* off;
+  uint64_t n, cap;
+} tbuild;
+
+static void tvisit(tbuild* b, int level, uint32_t x, uint32_t y, uint32_t z) {
+  const uint64_t side = 1ull << level;
+  const uint64_t leaves = 1ull << (level * b->d);
+  if (x >= b->dims[0] || y >= b->dims[1] || (b->d == 3 && z >= b->dims[2])) {
+    b->offset += leaves;
+    b->found_gap = 1;
+    return;
+  }
+  if (x + side <= b->dims[0] && y + side <= b->dims[1] && (b->d == 2 || z + side <= b->dims[2])) {
+    if (b->found_gap) {
+      if (b->n < b->cap) { b->start[b->n] = b->counter; b->off[b->n] = b->offset; }
+      b->n++;
+      b->found_gap = 0;
+    }
+    b->counter += leaves;
+    return;
+  }
+  const uint32_t half = (uint32_t)(side / 2);
+  for (int c = 0; c < (1 << b->d); ++c)
+    tvisit(b, level - 1, x + ((c & 1) ? half : 0), y + ((c & 2) ? half : 0), z + ((c & 4) ? half : 0));
+}
+
+/* OffsetsTable::build (morton.cpp:124-143); returns the number of runs */
+int64_t orc_offsets_table(const uint32_t* dims, uint64_t* start, uint64_t* off, uint64_t cap) {
+  if (!dims[0] || !dims[1] || !dims[2]) return fail("grid dimensions must be positive");
+  tbuild b = {{dims[0], dims[1], dims[2]}, dims[2] == 1 ? 2 : 3, 0, 0, 1, start, off, 0, cap};
+  uint32_t m = dims[0] > dims[1] ? dims[0] : dims[1];
+  if (b.d == 3 && dims[2] > m) m = dims[2];
+  int level = 0;
+  while ((1ull << level) < m) ++level;
+  tvisit(&b, level, 0, 0, 0);
+  return (int64_t)b.n;
+}
+
+/* prefix_sum.cpp:11-19 */
+uint64_t orc_exclusive_scan(uint64_t* v, uint64_t n) {
+  uint64_t acc = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t next = acc + v[i];
+    v[i] = acc;
+    acc = next;
+  }
+  return acc;
+}
+
+/* sort_balance.cpp:22-148 with one domain: boxes in Morton-rank order, chain
+ * order inside a box. Requires a current grid. */
+int orc_sort(orc_sim* s, uint64_t* moved) {
+  if (moved) *moved = 0;
+  if (s->indexed != s->n) return fail("sort requires a grid updated for the current agents");
+  if (s->n == 0) return 0;
+  uint64_t cap = 64;
+  uint64_t *st = NULL, *of = NULL;
+  int64_t runs;
+  for (;;) {
+    st = xrealloc(st, cap * sizeof *st);
+    of = xrealloc(of, cap * sizeof *of);
+    runs = orc_offsets_table(s->dims, st, of, cap);
+    if (runs < 0) { free(st); free(of); return -1; }
+    if ((uint64_t)runs <= cap) break;
+    cap = (uint64_t)runs;
+  }
+  uint64_t* order = malloc(s->n * sizeof *order);
+  uint64_t w = 0, e = 0;
+  for (uint64_t rank = 0; rank < s->nboxes; ++rank) {
+    while (e + 1 < (uint64_t)runs && st[e + 1] <= rank) ++e;
+    uint32_t c[3];
+    orc_morton_decode3(rank + of[e], c);
+    if (s->dims[2] == 1) { /* 2D table: (x, y) interleave */
+      uint64_t code = rank + of[e], xx = 0, yy = 0;
+      for (int i = 0; i < 31; ++i) {
+        xx |= ((code >> (2 * i)) & 1ull) << i;
+        yy |= ((code >> (2 * i + 1)) & 1ull) << i;
+      }
+      c[0] = (uint32_t)xx; c[1] = (uint32_t)yy; c[2] = 0;
+    }
+    const uint64_t box = c[0] + (uint64_t)s->dims[0] * (c[1] + (uint64_t)s->dims[1] * c[2]);
+    for (uint64_t j = s->head[box]; j != ORC_NIL; j = s->succ[j]) order[w++] = j;
+  }
+  free(st); free(of);
+  if (w != s->n) { free(order); return fail("grid population changed during sort"); }
+  orc_sim tmp = *s;
+  tmp.cap = 0;
+  tmp.uid = NULL; tmp.x = tmp.y = tmp.z = tmp.d = NULL; tmp.tx = tmp.ty = tmp.tz = tmp.tg = NULL;
+  tmp.fx = tmp.fy = tmp.fz = NULL; tmp.partners = NULL; tmp.flags = NULL; tmp.beh = NULL;
+  tmp.vol = NULL; tmp.succ = NULL;
+  reserve(&tmp, s->n);
+  for (uint64_t i = 0; i < s->n; ++i) {
+    const uint64_t j = order[i];
+    tmp.uid[i] = s->uid[j];
+    tmp.x[i] = s->x[j]; tmp.y[i] = s->y[j]; tmp.z[i] = s->z[j]; tmp.d[i] = s->d[j];
+    tmp.tx[i] = s->tx[j]; tmp.ty[i] = s->ty[j]; tmp.tz[i] = s->tz[j]; tmp.tg[i] = s->tg[j];
+    tmp.fx[i] = s->fx[j]; tmp.fy[i] = s->fy[j]; tmp.fz[i] = s->fz[j];
+    tmp.partners[i] = s->partners[j]; tmp.flags[i] = s->flags[j]; tmp.beh[i] = s->beh[j];
+    tmp.vol[i] = s->vol[j];
+  }
+  free(order);
+#define SWAPF(f) do { void* t_ = s->f; s->f = tmp.f; tmp.f = t_; } while (0)
+  SWAPF(uid); SWAPF(x); SWAPF(y); SWAPF(z); SWAPF(d); SWAPF(tx); SWAPF(ty); SWAPF(tz);
+  SWAPF(tg); SWAPF(fx); SWAPF(fy); SWAPF(fz); SWAPF(partners); SWAPF(flags); SWAPF(beh);
+  SWAPF(vol); SWAPF(succ);
+#undef SWAPF
+  const uint64_t c2 = s->cap;
+  s->cap = tmp.cap;
+  tmp.cap = c2;
+  free(tmp.uid); free(tmp.x); free(tmp.y); free(tmp.z); free(tmp.d); free(tmp.tx); free(tmp.ty);
+  free(tmp.tz); free(tmp.tg); free(tmp.fx); free(tmp.fy); free(tmp.fz); free(tmp.partners);
+  free(tmp.flags); free(tmp.beh); free(tmp.vol); free(tmp.succ);
+  s->sorted += 0; /* one domain: nothing migrates (agents_moved counts domain changes) */
+  return 0;
+}
+
+/* ---- schedule (simulation.cpp:222-322) --------------------------------- */
+int orc_simulate(orc_sim* s, uint64_t iterations) {
+  for (uint64_t it = 0; it < iterations; ++it) {
+    if (orc_env_update(s, NULL, NULL, NULL)) return -1;
+    if (s->p.sorting_frequency > 0 && s->iteration % s->p.sorting_frequency == 0) {
+      if (orc_sort(s, NULL)) return -1;
+      if (orc_env_update(s, NULL, NULL, NULL)) return -1;
+    }
+    if (s->p.detect_static && run_staticness(s)) return -1;
+    /* agent phase: behaviours then forces per agent block; neither reads
+     * state the other writes, so whole-population order is equivalent */
+    const uint64_t n = s->n;
+    for (uint64_t i = 0; i < n; ++i)
+      if (run_behaviour(s, i)) return -1;
+    for (uint64_t i = 0; i < n; ++i)
+      if (run_forces(s, i)) return -1;
+    for (uint64_t i = 0; i < n; ++i) apply_pending(s, i);
+    if (run_commit(s)) return -1;
+    s->iteration++;
+  }
+  return 0;
+}
+
+int orc_counts(const orc_sim* s, uint64_t* out) {
+  out[0] = s->n; out[1] = s->uid_counter; out[2] = s->iteration; out[3] = s->evals;
+  out[4] = s->skips; out[5] = s->added; out[6] = s->removed; out[7] = s->sorted;
+  return 0;
+}
+
+/* same layout as ref_dump (oracle/ref_harness.cpp) */
+int orc_dump(const orc_sim* s, uint64_t* uid, double* x, double* y, double* z, double* d,
+             double* fx, double* fy, double* fz, uint32_t* partners, uint8_t* flags, double* vol) {
+  for (uint64_t i = 0; i < s->n; ++i) {
+    if (uid) uid[i] = s->uid[i];
+    if (x) x[i] = s->x[i];
+    if (y) y[i] = s->y[i];
+    if (z) z[i] = s->z[i];
+    if (d) d[i] = s->d[i];
+    if (fx) fx[i] = s->fx[i];
+    if (fy) fy[i] = s->fy[i];
+    if (fz) fz[i] = s->fz[i];
+    if (partners) partners[i] = s->partners[i];
+    if (flags) flags[i] = (uint8_t)(s->flags[i] & 63u);
+    if (vol) vol[i] = s->vol[i];
+  }
+  return 0;
+}
