@@ -1,0 +1,294 @@
+"""bench.py — agent-iterations/s of the mechanical step on B200 (BASELINE.json metric).
+
+Default workload (N=1): BASELINE configs[3] ("c4"): 2^26 agents, uniform cube
+at 12 mean neighbours, lognormal(ln 10, 0.1) diameters, dt 0.01 — the
+largest single-GPU config and the one the north-star roofline target is
+stated on. Inputs (2.5 GB of state) are far larger than L2 (126 MB), so no
+explicit flush is needed between steps. `--config c1|c2|c3|c4` picks another.
+
+One "step" = one full iteration (grid rebuild + radius query + repulsion +
+displacement [+ staticness / behaviours / commit for c2/c3]).
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the unmodified absim engine with all host threads) on a bounded sample of
+the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "agent-iterations/sec for the mechanical step; achieved fraction of HBM roofline"
+UNIT = "agent-iterations/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _workload(name, n=None, seed=0):
+    from paper_2301_06984_b200 import configs as CF
+    if name == "c1":
+        return CF.c1_relaxation(n or 131_072, seed)
+    if name == "c2":
+        return CF.c2_proliferation(side=16 if n is None else round(n ** (1 / 3)), seed=seed)
+    if name == "c3":
+        return CF.c3_spheroid(n or (1 << 23), seed)
+    return CF.c4_large_uniform(n or (1 << 26), seed)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(k)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=None)
+    return dist, world, rank, local
+
+
+def cpu_baseline(wl_name, sample_n, steps, threads=None):
+    """The reference engine (oracle/_ref) on a bounded sample of the workload."""
+    from oracle import oracle as O
+    wl = _workload(wl_name, sample_n, seed=0)
+    prm = wl.params
+    threads = threads or os.cpu_count()
+    p = O.OracleParams(seed=prm.get("seed", 0), dt=prm.get("simulation_time_step", 0.1),
+                       detect_static=prm.get("detect_static_agents", False),
+                       model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
+                       sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0)
+    try:
+        sim = O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask)
+        kind = "reference"
+    except (FileNotFoundError, OSError):
+        p.threads = 1
+        sim = O.PortSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask)
+        kind, threads = "port", 1
+    agent_its = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        agent_its += sim.counts()["agents"]
+        sim.simulate(1)
+    wall = time.perf_counter() - t0
+    return {"value": agent_its / wall, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{wl.name} shape at {wl.n} agents x {steps} steps (same density/distributions), "
+                      f"{wall:.1f} s wall"}
+
+
+def run_reference(args):
+    _, world, rank, _ = _dist() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 1, 0, 0)
+    if rank != 0:
+        return
+    sample_n = {"c1": 131_072, "c2": None, "c3": 1 << 20, "c4": 1 << 20}[args.config]
+    per = []
+    for _ in range(args.warmup):
+        cpu_baseline(args.config, sample_n, 1)
+    for _ in range(args.steps):
+        per.append(cpu_baseline(args.config, sample_n, 2))
+    v = statistics.median([p["value"] for p in per])
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "sample_agents": sample_n},
+            "cpu_baseline": {**per[0], "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    import paper_2301_06984_b200 as E
+
+    dist, world, rank, local = _dist() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 1, 0, 0)
+    torch.cuda.set_device(local)
+    wl = _workload(args.config, args.n, seed=args.seed + rank)
+    prm = dict(wl.params)
+    prm["record_forces"] = False
+    prm["bins_per_box"] = args.bins
+    if wl.params.get("model") == E.MODEL_PROLIFERATION:
+        prm["capacity"] = 5 * wl.n * 2 ** 9
+    sim = E.Simulation(E.SimulationParams(**prm), device=local)
+    sim.add_agents(wl.x, wl.y, wl.z, wl.d, behaviour_mask=wl.mask)
+    stream = torch.cuda.ExternalStream(sim.stream)
+
+    sim.simulate(args.warmup)
+    sim.synchronize()
+    r0 = sim.report()
+    sim.reset_timers(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        sim.simulate(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    r1 = sim.report()
+    force_ms, force_launches = sim.force_kernel_time()
+    sim.reset_timers(False)
+    agent_its = None
+    # agent count per step (constant unless the model adds agents)
+    if r1.agents_added == r0.agents_added:
+        agent_its = r1.final_agent_count * args.steps
+    else:
+        agent_its = (r0.final_agent_count + r1.final_agent_count) / 2 * args.steps
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        a = torch.tensor([float(agent_its)], device="cuda")
+        dist.all_reduce(a)
+        agent_its = float(a.item())
+    value = agent_its / (ms_max / 1e3)
+
+    # end to end through the public API with host buffers: per step, upload
+    # the step's input state from host memory, run it, read the result back
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        x, y, z, d = (np.ascontiguousarray(a) for a in (wl.x, wl.y, wl.z, wl.d))
+        sim.add_agents(x, y, z, d, behaviour_mask=wl.mask)
+        sim.simulate(1)
+        sim.synchronize()
+        e2e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            sim.add_agents(x, y, z, d, behaviour_mask=wl.mask)
+            sim.simulate(1)
+            out = sim.agents()
+        dt = time.perf_counter() - t0
+        n_e = len(out["x"])
+        e2e = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0)),
+               "d2h_bytes_per_step": n_e * (8 * 8 + 4 + 1 + 8)}
+
+    hbm, peak_src = _peaks()
+    n_agents = r1.final_agent_count
+    avg_force_ms = force_ms / max(1, force_launches)
+    force_bytes = 56 * n_agents  # read {x,y,z,d} 32 B + write {x,y,z} 24 B per agent
+    achieved = force_bytes / (avg_force_ms / 1e3) / 1e9
+    step_bytes = wl.bytes_per_agent_iteration * agent_its / max(1, world)
+    step_achieved = step_bytes / (ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "force_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                tt = json.load(f)
+            if tt.get("config") == args.config:
+                traffic = tt.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "bins_per_box": args.bins, "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
+        "roofline": {"bound": "hbm", "kernel": "k_force", "achieved": achieved, "peak": hbm,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
+                     "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms},
+        "step_roofline": {"bytes_per_agent_iteration": wl.bytes_per_agent_iteration,
+                          "achieved": step_achieved, "frac": step_achieved / hbm, "unit": "GB/s"},
+        "clocks": clk.summary(),
+        "gpu_launches": int(r1.kernel_launches - r0.kernel_launches),
+        "force_evaluations_per_agent_step": (r1.force_evaluations - r0.force_evaluations) / max(1, agent_its / world),
+        "e2e": e2e,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args.config, {"c1": 131_072, "c2": None, "c3": 1 << 20,
+                                                          "c4": 1 << 20}[args.config], 2)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--bins", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/* absim_gpu.h — C ABI of the B200 (sm_100a) mechanical-step engine.
+ *
+ * Drop-in boundary for the reference's neighbour-search / mechanical-forces
+ * path. The reference has no C ABI (static C++ lib, proj/src/CMakeLists.txt:1-21)
+ * and its per-agent virtual visitor (environment.hpp:12-16) cannot cross to a
+ * GPU, so the boundary is batched at step granularity. Each entry point names
+ * the reference interface it replaces:
+ *
+ *   abs_gpu_create          Simulation::Simulation(SimulationParams)      simulation.hpp:91, params.hpp:17-52
+ *                           + make_environment(kUniformGrid)                simulation.cpp:40-53
+ *   abs_gpu_upload          Simulation::add_agent (+ Behavior attach)       simulation.hpp:107, simulation.cpp:131-141
+ *   abs_gpu_simulate        Simulation::simulate(iterations)                simulation.hpp:121, simulation.cpp:222-322
+ *                           = Environment::update → [staticness] → behaviours
+ *                             → run_forces → run_integration → run_commit
+ *   abs_gpu_stats           Simulation::report() counters                   report.hpp:32-40
+ *   abs_gpu_download        ResourceManager::for_each_agent + Agent getters resource_manager.hpp:346, agent.hpp:31-110
+ *   abs_gpu_env_update      Environment::update (UniformGrid::update)       environment.hpp:38, uniform_grid.cpp:155-266
+ *   abs_gpu_grid_info       UniformGrid::{origin, box_length, dims, largest_agent_diameter}  uniform_grid.hpp:40-49
+ *   abs_gpu_cell_ids        UniformGrid::box_index_of (per agent)           uniform_grid.cpp:124-133
+ *   abs_gpu_neighbors       Environment::for_each_neighbor (batched; force
+ *                           query radius 0.5 (d + dmax), simulation.cpp:469) uniform_grid.cpp:268-326
+ *   abs_gpu_sort            sort_and_balance (one domain)                   sort_balance.cpp:22-148
+ *   abs_gpu_remove          CommitBuffer removals / remove_agents_parallel  commit.cpp:86-178
+ *
+ * Conventions: int status (ABS_OK == 0), no exceptions across the ABI, one
+ * host thread per context, device memory owned by the context, host buffers
+ * borrowed for the duration of the call only. All work is ordered on the
+ * context's CUDA stream; calls that return host data synchronise it.
+ * Agent order in download/cell_ids/neighbors is the device storage order
+ * (cell order); identity is the uid.
+ */
+#ifndef ABSIM_GPU_H
+#define ABSIM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define ABS_OK 0
+#define ABS_ERR_INVALID_ARGUMENT 1  /* std::invalid_argument in the reference */
+#define ABS_ERR_CUDA 2
+#define ABS_ERR_NONFINITE 3          /* "agent positions are not finite"  uniform_grid.cpp:208-212 */
+#define ABS_ERR_FIXED_BOX 4          /* fixed box < largest diameter     uniform_grid.cpp:214-221 */
+#define ABS_ERR_BOX_BUDGET 5         /* > 2^31 boxes                      uniform_grid.cpp:235-237 */
+#define ABS_ERR_CAPACITY 6           /* device agent capacity exhausted */
+#define ABS_ERR_NO_DEVICE 7
+#define ABS_ERR_STATE 8              /* std::logic_error in the reference */
+
+/* agent flags (download), same bits as the oracles' dumps */
+#define ABS_FLAG_STATIC 1u
+#define ABS_FLAG_MOVED 2u
+#define ABS_FLAG_GREW 4u
+#define ABS_FLAG_NEWLY_ADDED 8u
+#define ABS_FLAG_NEIGHBOR_VIOLATION 16u
+#define ABS_FLAG_NEW_NEIGHBOR 32u
+
+/* device behaviour models (BASELINE configs; models.hpp:69-83 for GROW) */
+#define ABS_MODEL_NONE 0
+#define ABS_MODEL_PROLIFERATION 1 /* mp[0] volume rate, mp[1] division volume */
+#define ABS_MODEL_DRIVE 2         /* mp[0..2] centre, mp[3] max speed */
+#define ABS_MODEL_GROW 3          /* mp[0] growth rate, mp[1] diameter cap */
+
+typedef struct abs_gpu_ctx abs_gpu_ctx;
+
+/* SimulationParams (params.hpp:17-52), hot-path subset + device knobs */
+typedef struct {
+  uint64_t seed;                 /* 42 */
+  double simulation_time_step;   /* 0.1 */
+  double repulsion_coefficient;  /* 2.0 */
+  double max_displacement;       /* 3.0 */
+  double force_threshold;        /* 0.0 */
+  double fixed_box_length;       /* 0.0 = follow the largest diameter */
+  uint64_t sorting_frequency;    /* 0 = never (storage is re-binned every step) */
+  int32_t detect_static_agents;  /* 0 */
+  int32_t model;                 /* ABS_MODEL_* */
+  double model_params[8];
+  uint64_t capacity;             /* agent capacity hint; grows on demand */
+  int32_t record_forces;         /* keep Agent::last_force (parity); 0 skips the 24 B/agent write */
+  int32_t bins_per_box;          /* internal sub-bins per box edge: 0 auto, 1, 2 */
+} abs_gpu_config;
+
+/* SimulationReport counters (report.hpp:32-40) */
+typedef struct {
+  uint64_t agents;
+  uint64_t uid_count;
+  uint64_t iterations;
+  uint64_t force_evaluations;
+  uint64_t force_skips;
+  uint64_t agents_added;
+  uint64_t agents_removed;
+  uint64_t kernel_launches; /* kernels this context launched so far */
+} abs_step_stats;
+
+void abs_gpu_default_config(abs_gpu_config* cfg);
+int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out);
+int abs_gpu_destroy(abs_gpu_ctx* ctx);
+/* message of the last failure on ctx (or of the last failed create if ctx == NULL) */
+const char* abs_gpu_last_error(const abs_gpu_ctx* ctx);
+
+/* Replace the population with n agents copied from host arrays. uid == NULL
+ * assigns uids 0..n-1 in array order (Simulation::add_agent order);
+ * behaviour_mask == NULL attaches the model behaviour to every agent;
+ * volume/flags/partners may be NULL (volume defaults to the sphere volume). */
+int abs_gpu_upload(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
+                   const double* y, const double* z, const double* d,
+                   const uint8_t* behaviour_mask, const double* volume,
+                   const uint8_t* flags, const uint32_t* partners, uint64_t uid_count);
+
+/* Same, from device pointers already resident in HBM (no host copies). */
+int abs_gpu_upload_device(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
+                          const double* y, const double* z, const double* d,
+                          const uint8_t* behaviour_mask, uint64_t uid_count);
+
+/* Set the global iteration counter (checkpoint resume / teacher forcing;
+ * the counter drives frequency gating and the RNG counters, simulation.hpp:117-121). */
+int abs_gpu_set_iteration(abs_gpu_ctx* ctx, uint64_t iteration);
+
+/* Run `iterations` full iterations (stream-ordered). */
+int abs_gpu_simulate(abs_gpu_ctx* ctx, uint64_t iterations);
+int abs_gpu_stats(abs_gpu_ctx* ctx, abs_step_stats* out);
+int abs_gpu_synchronize(abs_gpu_ctx* ctx);
+
+/* Copy the population to host arrays (any pointer may be NULL); *n_out = agents. */
+int abs_gpu_download(abs_gpu_ctx* ctx, uint64_t* n_out, uint64_t* uid, double* x, double* y,
+                     double* z, double* d, double* fx, double* fy, double* fz,
+                     uint32_t* partners, uint8_t* flags, double* volume);
+
+/* Teacher-forced environment: build the grid for the current state. */
+int abs_gpu_env_update(abs_gpu_ctx* ctx);
+/* grid[0..2] origin, grid[3] box length, grid[4] largest diameter */
+int abs_gpu_grid_info(abs_gpu_ctx* ctx, double* grid, uint32_t* dims);
+/* reference box index per agent (download order); requires abs_gpu_env_update */
+int abs_gpu_cell_ids(abs_gpu_ctx* ctx, uint64_t* out);
+/* CSR of sorted neighbour uids per agent (download order) within the force
+ * query radius; offsets has n+1 entries. *total receives the number of uids;
+ * returns ABS_ERR_CAPACITY (and the needed total) when cap is too small. */
+int abs_gpu_neighbors(abs_gpu_ctx* ctx, uint64_t* offsets, uint64_t* uids, uint64_t cap,
+                      uint64_t* total);
+/* Reorder storage into sort_and_balance order: boxes by Morton rank, agents in
+ * a box by descending current storage index (sort_balance.cpp:88-128). */
+int abs_gpu_sort(abs_gpu_ctx* ctx);
+/* Remove agents by uid with the reference's five-step slot semantics. */
+int abs_gpu_remove(abs_gpu_ctx* ctx, const uint64_t* uids, uint64_t count);
+
+/* CUDA stream used by the context (cudaStream_t); may be replaced. */
+void* abs_gpu_stream(abs_gpu_ctx* ctx);
+int abs_gpu_set_stream(abs_gpu_ctx* ctx, void* stream);
+
+/* Timing of the dominant kernel (mechanical force) recorded with CUDA events
+ * on the context stream: cumulative ms and launch count since the last reset. */
+int abs_gpu_force_kernel_time(abs_gpu_ctx* ctx, double* total_ms, uint64_t* launches);
+int abs_gpu_reset_timers(abs_gpu_ctx* ctx, int enable);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ABSIM_GPU_H */

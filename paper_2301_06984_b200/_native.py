@@ -1,0 +1,134 @@
+"""ctypes binding of the C ABI in include/absim_gpu.h (libabsim_gpu.so).
+
+There is no fallback: if the sm_100a library is missing or cannot be loaded
+this module raises at import time of the engine, and every engine call goes
+through the CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libabsim_gpu.so")
+
+ABS_OK = 0
+ABS_ERR_INVALID_ARGUMENT = 1
+ABS_ERR_CUDA = 2
+ABS_ERR_NONFINITE = 3
+ABS_ERR_FIXED_BOX = 4
+ABS_ERR_BOX_BUDGET = 5
+ABS_ERR_CAPACITY = 6
+ABS_ERR_NO_DEVICE = 7
+ABS_ERR_STATE = 8
+
+MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW = 0, 1, 2, 3
+
+# every symbol include/absim_gpu.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "abs_gpu_default_config", "abs_gpu_create", "abs_gpu_destroy", "abs_gpu_last_error",
+    "abs_gpu_upload", "abs_gpu_upload_device", "abs_gpu_set_iteration", "abs_gpu_simulate", "abs_gpu_stats",
+    "abs_gpu_synchronize", "abs_gpu_download", "abs_gpu_env_update", "abs_gpu_grid_info",
+    "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
+    "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
+]
+
+
+class Config(C.Structure):
+    _fields_ = [
+        ("seed", C.c_uint64),
+        ("simulation_time_step", C.c_double),
+        ("repulsion_coefficient", C.c_double),
+        ("max_displacement", C.c_double),
+        ("force_threshold", C.c_double),
+        ("fixed_box_length", C.c_double),
+        ("sorting_frequency", C.c_uint64),
+        ("detect_static_agents", C.c_int32),
+        ("model", C.c_int32),
+        ("model_params", C.c_double * 8),
+        ("capacity", C.c_uint64),
+        ("record_forces", C.c_int32),
+        ("bins_per_box", C.c_int32),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("agents", C.c_uint64),
+        ("uid_count", C.c_uint64),
+        ("iterations", C.c_uint64),
+        ("force_evaluations", C.c_uint64),
+        ("force_skips", C.c_uint64),
+        ("agents_added", C.c_uint64),
+        ("agents_removed", C.c_uint64),
+        ("kernel_launches", C.c_uint64),
+    ]
+
+
+_D = C.POINTER(C.c_double)
+_U64 = C.POINTER(C.c_uint64)
+_U32 = C.POINTER(C.c_uint32)
+_U8 = C.POINTER(C.c_uint8)
+_CTX = C.c_void_p
+
+_lib = None
+
+
+def load():
+    """Load libabsim_gpu.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    sig = {
+        "abs_gpu_default_config": (None, [C.POINTER(Config)]),
+        "abs_gpu_create": (C.c_int, [C.POINTER(Config), C.c_int, C.POINTER(_CTX)]),
+        "abs_gpu_destroy": (C.c_int, [_CTX]),
+        "abs_gpu_last_error": (C.c_char_p, [_CTX]),
+        "abs_gpu_upload": (C.c_int, [_CTX, C.c_uint64, _U64, _D, _D, _D, _D, _U8, _D, _U8, _U32,
+                                     C.c_uint64]),
+        "abs_gpu_upload_device": (C.c_int, [_CTX, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]),
+        "abs_gpu_set_iteration": (C.c_int, [_CTX, C.c_uint64]),
+        "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
+        "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),
+        "abs_gpu_synchronize": (C.c_int, [_CTX]),
+        "abs_gpu_download": (C.c_int, [_CTX, _U64, _U64, _D, _D, _D, _D, _D, _D, _D, _U32, _U8, _D]),
+        "abs_gpu_env_update": (C.c_int, [_CTX]),
+        "abs_gpu_grid_info": (C.c_int, [_CTX, _D, _U32]),
+        "abs_gpu_cell_ids": (C.c_int, [_CTX, _U64]),
+        "abs_gpu_neighbors": (C.c_int, [_CTX, _U64, _U64, C.c_uint64, _U64]),
+        "abs_gpu_sort": (C.c_int, [_CTX]),
+        "abs_gpu_remove": (C.c_int, [_CTX, _U64, C.c_uint64]),
+        "abs_gpu_stream": (C.c_void_p, [_CTX]),
+        "abs_gpu_set_stream": (C.c_int, [_CTX, C.c_void_p]),
+        "abs_gpu_force_kernel_time": (C.c_int, [_CTX, _D, _U64]),
+        "abs_gpu_reset_timers": (C.c_int, [_CTX, C.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class AbsimError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+def check(rc: int, ctx=None):
+    """Map a status code to the reference's exception kinds (params.cpp:44-72,
+    uniform_grid.cpp:208-237): invalid_argument -> ValueError, others ->
+    RuntimeError subclasses carrying the code."""
+    if rc == ABS_OK:
+        return
+    msg = load().abs_gpu_last_error(ctx).decode(errors="replace")
+    if rc == ABS_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise AbsimError(rc, msg)

@@ -1,0 +1,1713 @@
+// absim_gpu.cu — device kernels + C ABI (include/absim_gpu.h) of the B200
+// mechanical-step engine. One iteration (Simulation::simulate body,
+// simulation.cpp:232-303) is:
+//
+//   k_reduce     bbox + largest diameter          uniform_grid.cpp:170-206
+//   k_finalize   box length, origin, dims, checks  uniform_grid.cpp:208-237
+//   k_key        bin of each agent + per-bin count (atomic slot = rank)
+//   scan         exclusive scan of bin counts -> cell table `start`
+//   k_scatter    permute state into cell order (coalesced SoA writes)
+//   k_mark       [static] disturbers flag neighbours  simulation.cpp:351-373
+//   k_force      behaviours + static skip + 27-box radius query + pairwise
+//                repulsion + force sum + integration     simulation.cpp:388-500
+//   commit       [additions] daughter uid ranks + append  commit.cpp:236-297
+//
+// Every kernel is a grid-stride loop over a device-resident agent count, so an
+// iteration needs no host synchronisation (counts change on the device).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "absim_gpu.h"
+#include "kernels.cuh"
+
+using namespace absgpu;
+
+namespace {
+
+constexpr unsigned long long kInfOrdLo = 0xFFF0000000000000ull;  // ord_enc(+inf)
+constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf)
+constexpr unsigned long long kZeroOrd = 0x8000000000000000ull;   // ord_enc(+0.0)
+
+// ---------------------------------------------------------------- reduce
+__global__ void __launch_bounds__(kThreads) k_reduce(const Pd* __restrict__ pos, DevGrid* g) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  double dm = 0.0;
+  unsigned int bad = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const double v[3] = {p.x, p.y, p.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bad |= !isfinite(v[k]);
+      lo[k] = v[k] < lo[k] ? v[k] : lo[k];
+      hi[k] = hi[k] < v[k] ? v[k] : hi[k];
+    }
+    dm = dm < p.d ? p.d : dm;
+  }
+  // warp then block reduction (min/max are order independent: bit-exact)
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double a = __shfl_xor_sync(0xffffffffu, lo[k], off);
+      const double b = __shfl_xor_sync(0xffffffffu, hi[k], off);
+      lo[k] = a < lo[k] ? a : lo[k];
+      hi[k] = hi[k] < b ? b : hi[k];
+    }
+    const double c = __shfl_xor_sync(0xffffffffu, dm, off);
+    dm = dm < c ? c : dm;
+    bad |= __shfl_xor_sync(0xffffffffu, bad, off);
+  }
+  __shared__ double sh[kThreads / 32][7];
+  __shared__ unsigned int sbad[kThreads / 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    for (int k = 0; k < 3; ++k) { sh[w][k] = lo[k]; sh[w][3 + k] = hi[k]; }
+    sh[w][6] = dm;
+    sbad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int k = threadIdx.x;
+    double v = sh[0][k];
+    for (int q = 1; q < kThreads / 32; ++q) {
+      const double u = sh[q][k];
+      v = k < 3 ? (u < v ? u : v) : (v < u ? u : v);
+    }
+    if (k < 3) atomicMin(&g->red[k], ord_enc(v));
+    else atomicMax(&g->red[k], ord_enc(v));
+  } else if (threadIdx.x == 7) {
+    unsigned int b = 0;
+    for (int q = 0; q < kThreads / 32; ++q) b |= sbad[q];
+    if (b) atomicOr(&g->nonfinite, 1u);
+  }
+}
+
+__device__ void reset_reduction(DevGrid* g) {
+  g->red[0] = g->red[1] = g->red[2] = kInfOrdLo;
+  g->red[3] = g->red[4] = g->red[5] = kInfOrdHi;
+  g->red[6] = kZeroOrd;
+  g->nonfinite = 0;
+}
+
+// uniform_grid.cpp:155-237 sizing; one thread.
+__global__ void k_finalize(DevGrid* g, double fixed_box, int bins_cfg, unsigned long long bins_cap,
+                           unsigned long long capacity, unsigned long long uid_cap, int may_add,
+                           unsigned long long iteration) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (g->err) {
+    reset_reduction(g);
+    return;
+  }
+  const unsigned long long n = g->n;
+  int err = kErrNone;
+  if (n == 0) {
+    g->dims[0] = g->dims[1] = g->dims[2] = 1;
+    g->origin[0] = g->origin[1] = g->origin[2] = 0.0;
+    g->box = fixed_box > 0.0 ? fixed_box : 1.0;
+    g->dmax = 0.0;
+  } else {
+    double lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = ord_dec(g->red[k]);
+      hi[k] = ord_dec(g->red[3 + k]);
+    }
+    const double dm = ord_dec(g->red[6]);
+    for (int k = 0; k < 3; ++k)
+      if (!isfinite(lo[k]) || !isfinite(hi[k])) err = kErrNonFinite;
+    if (g->nonfinite) err = kErrNonFinite;
+    g->dmax = dm;
+    if (err == kErrNone) {
+      if (fixed_box > 0.0) {
+        if (dm > fixed_box) err = kErrFixedBox;
+        g->box = fixed_box;
+      } else {
+        g->box = dm;
+      }
+    }
+    if (err == kErrNone) {
+      unsigned long long needed = 1;
+      for (int k = 0; k < 3; ++k) {
+        g->origin[k] = lo[k];
+        const unsigned long long nk =
+            static_cast<unsigned long long>(floor((hi[k] - lo[k]) / g->box)) + 1ull;
+        g->dims[k] = static_cast<unsigned int>(nk < 1 ? 1 : nk);
+        needed *= g->dims[k];
+      }
+      if (needed > (1ull << 31)) err = kErrBoxBudget;
+    }
+  }
+  if (err == kErrNone) {
+    unsigned int B = bins_cfg == 2 ? 2u : 1u;
+    const unsigned long long boxes = (unsigned long long)g->dims[0] * g->dims[1] * g->dims[2];
+    if (boxes * B * B * B + 1 > 0xFFFFFFFFull) B = 1;
+    const unsigned long long nbins = boxes * B * B * B;
+    if (nbins + 1 > bins_cap) {
+      err = kErrBinsRetry;
+      g->needed_bins = nbins + 1;
+    } else if (may_add && (2 * n > capacity || g->uid_count + n > uid_cap)) {
+      err = kErrCapRetry;
+    } else {
+      g->B = B;
+      g->s = B == 1 ? g->box : g->box / static_cast<double>(B);
+      for (int k = 0; k < 3; ++k) g->bd[k] = g->dims[k] * B;
+      g->nbins = nbins;
+      double mag = g->box;
+      for (int k = 0; k < 3; ++k) {
+        mag = fmax(mag, fabs(g->origin[k]));
+        mag = fmax(mag, fabs(g->origin[k] + g->dims[k] * g->box));
+      }
+      g->margin = 1e-9 * mag;
+    }
+  }
+  reset_reduction(g);
+  if (err != kErrNone) {
+    g->err = err;
+    g->failed_iteration = iteration;
+  }
+}
+
+// ---------------------------------------------------------------- binning
+__global__ void __launch_bounds__(kThreads) k_key(const Pd* __restrict__ pos, const DevGrid* g,
+                                                  unsigned int* __restrict__ count,
+                                                  unsigned int* __restrict__ key,
+                                                  unsigned int* __restrict__ rank) {
+  if (g->err) return;
+  const DevGrid G = *g;
+  const unsigned long long n = G.n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const unsigned int bx = bin_coord(p.x, G.origin[0], G, 0);
+    const unsigned int by = bin_coord(p.y, G.origin[1], G, 1);
+    const unsigned int bz = bin_coord(p.z, G.origin[2], G, 2);
+    const unsigned int b = bx + G.bd[0] * (by + G.bd[1] * bz);
+    key[i] = b;
+    rank[i] = atomicAdd(count + b, 1u);
+  }
+}
+
+// ------------------------------------------------------------ exclusive scan
+// In-place exclusive scan of data[0..len) (len read from *len_ptr), with
+// data[len] = total. Three passes: tile sums, scan of tile sums, tile scan.
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int l = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const T u = __shfl_up_sync(0xffffffffu, v, off);
+    if (l >= off) v += u;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* total) {
+  __shared__ T warp_sums[kThreads / 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const T inc = warp_incl_scan(v);
+  if (l == 31) warp_sums[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T ws = l < kThreads / 32 ? warp_sums[l] : T(0);
+    const T wi = warp_incl_scan(ws);
+    if (l < kThreads / 32) warp_sums[l] = wi - ws;
+    if (l == kThreads / 32 - 1) *total = wi;
+  }
+  __syncthreads();
+  const T r = inc - v + warp_sums[w];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_scan_tiles(const T* __restrict__ data,
+                                                         const unsigned long long* len_ptr,
+                                                         T* __restrict__ tile_sums, const int* err) {
+  if (err && *err) return;
+  const unsigned long long len = *len_ptr;
+  const unsigned long long base = (unsigned long long)blockIdx.x * kScanTile;
+  if (base >= len) return;
+  T sum = 0;
+  for (int q = 0; q < kScanTile / kThreads; ++q) {
+    const unsigned long long i = base + threadIdx.x * (kScanTile / kThreads) + q;
+    if (i < len) sum += data[i];
+  }
+  __shared__ T tot;
+  block_excl_scan(sum, &tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_scan_partials(T* __restrict__ tile_sums,
+                                                            const unsigned long long* len_ptr,
+                                                            const int* err) {
+  if (err && *err) return;
+  const unsigned long long len = *len_ptr;
+  const unsigned long long tiles = (len + kScanTile - 1) / kScanTile;
+  T carry = 0;
+  __shared__ T tot;
+  for (unsigned long long b = 0; b < tiles; b += kThreads) {
+    const unsigned long long i = b + threadIdx.x;
+    const T v = i < tiles ? tile_sums[i] : T(0);
+    const T e = block_excl_scan(v, &tot);
+    if (i < tiles) tile_sums[i] = e + carry;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_scan_apply(T* __restrict__ data,
+                                                         const unsigned long long* len_ptr,
+                                                         const T* __restrict__ tile_sums,
+                                                         const int* err) {
+  if (err && *err) return;
+  const unsigned long long len = *len_ptr;
+  const unsigned long long base = (unsigned long long)blockIdx.x * kScanTile;
+  if (base >= len) return;
+  constexpr int per = kScanTile / kThreads;
+  T v[per];
+  T sum = 0;
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    const unsigned long long i = base + threadIdx.x * per + q;
+    v[q] = i < len ? data[i] : T(0);
+    sum += v[q];
+  }
+  __shared__ T tot;
+  T run = block_excl_scan(sum, &tot) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    const unsigned long long i = base + threadIdx.x * per + q;
+    if (i < len) data[i] = run;
+    run += v[q];
+  }
+  if (base + kScanTile >= len && threadIdx.x == kThreads - 1) data[len] = run;
+}
+
+// ---------------------------------------------------------------- scatter
+struct Soa {
+  Pd* pd;
+  unsigned long long* uid;
+  unsigned char* flags;
+  unsigned int* partners;
+  double* vol;
+  unsigned char* beh;
+  double* force;  // [3][cap]
+};
+
+__global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos, Soa src, Soa dst,
+                                                      const unsigned int* __restrict__ start,
+                                                      const unsigned int* __restrict__ key,
+                                                      const unsigned int* __restrict__ rank,
+                                                      const DevGrid* g, unsigned long long cap,
+                                                      int carry_vol, int carry_force) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned int j = __ldg(start + key[i]) + rank[i];
+    const Pd p = load_pd(pos + i);
+    reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
+    reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
+    dst.uid[j] = src.uid[i];
+    dst.flags[j] = src.flags[i];
+    dst.partners[j] = src.partners[i];
+    dst.beh[j] = src.beh[i];
+    if (carry_vol) dst.vol[j] = src.vol[i];
+    if (carry_force) {
+      dst.force[j] = src.force[i];
+      dst.force[cap + j] = src.force[cap + i];
+      dst.force[2 * cap + j] = src.force[2 * cap + i];
+    }
+  }
+}
+
+__global__ void k_zero_u32(unsigned int* __restrict__ a, const unsigned long long* len_ptr, int plus_one,
+                           const int* err) {
+  if (err && *err) return;
+  const unsigned long long len = *len_ptr + (plus_one ? 1 : 0);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    a[i] = 0;
+}
+
+// ------------------------------------------------------------ staticness
+// Phase 1 of run_staticness_update (simulation.cpp:351-373), scatter form:
+// every disturber (moved|grew) or fresh agent flags the agents within its
+// radius 0.5 (d_a + dmax). Racing stores write the same value (1).
+__global__ void __launch_bounds__(kThreads) k_mark(Soa S, const DevGrid* g,
+                                                   const unsigned int* __restrict__ start,
+                                                   unsigned char* __restrict__ nv,
+                                                   unsigned char* __restrict__ nn) {
+  if (g->err) return;
+  const DevGrid G = *g;
+  const unsigned long long n = G.n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned char f = S.flags[i];
+    const bool disturbs = f & (ABS_FLAG_MOVED | ABS_FLAG_GREW);
+    const bool fresh = f & ABS_FLAG_NEWLY_ADDED;
+    if (!disturbs && !fresh) continue;
+    const Pd me = load_pd(S.pd + i);
+    const double r = 0.5 * (me.d + G.dmax);
+    for_each_neighbor(G, S.pd, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r * r,
+                      [&](unsigned int j, const Pd&, double, double, double, double) {
+                        if (disturbs) nv[j] = 1;
+                        if (fresh) nn[j] = 1;
+                      });
+  }
+}
+
+// ------------------------------------------------------------ force step
+// Behaviours, static skip, run_forces and apply_pending for one agent.
+__global__ void __launch_bounds__(kThreads) k_force(Soa S, Pd* __restrict__ out, const DevGrid* gp,
+                                                    DevGrid* gw, const unsigned int* __restrict__ start,
+                                                    unsigned char* __restrict__ nv,
+                                                    unsigned char* __restrict__ nn, StepArgs a,
+                                                    unsigned long long cap,
+                                                    unsigned long long* __restrict__ st_parent,
+                                                    Pd* __restrict__ st_pd, double* __restrict__ st_vol,
+                                                    unsigned int* __restrict__ div_mark) {
+  if (gp->err) return;
+  const DevGrid G = *gp;
+  const unsigned long long n = G.n;
+  const int lane = threadIdx.x & 31;
+  unsigned long long n_eval = 0, n_skip = 0;
+  for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n;
+       base += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = base + threadIdx.x;
+    const bool active = i < n;
+    bool divides = false;
+    double dpx = 0, dpy = 0, dpz = 0, dd = 0, dvol = 0;
+    unsigned long long my_uid = 0;
+    if (active) {
+      const Pd me = load_pd(S.pd + i);
+      unsigned char fl = S.flags[i];
+      my_uid = S.uid[i];
+      // --- staticness phase 2 (simulation.cpp:375-384) -----------------
+      if (a.detect_static) {
+        if (a.iteration == 0) {
+          fl = 0;  // :335-349 everyone participates, flags wiped
+        } else {
+          const bool skip = !(fl & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED |
+                                    ABS_FLAG_NEIGHBOR_VIOLATION | ABS_FLAG_NEW_NEIGHBOR)) &&
+                            !nv[i] && !nn[i] && S.partners[i] <= 1u;
+          fl = skip ? ABS_FLAG_STATIC : 0;
+          nv[i] = 0;
+          nn[i] = 0;
+        }
+      }
+      // --- behaviours (run before forces, simulation.cpp:389-394) -------
+      double tx = 0.0, ty = 0.0, tz = 0.0, tg = 0.0;
+      if (a.model != ABS_MODEL_NONE && S.beh[i]) {
+        if (a.model == ABS_MODEL_PROLIFERATION) {
+          double v = S.vol[i] + a.mp[0];
+          if (v > a.mp[1]) {
+            v *= 0.5;
+            double dir[3];
+            abs_unit_vector(a.seed, my_uid, ABS_RNG_DIVISION_BASE(a.iteration), dir);
+            const double half = 0.5 * me.d;
+            dpx = me.x + dir[0] * half;
+            dpy = me.y + dir[1] * half;
+            dpz = me.z + dir[2] * half;
+            dd = abs_diameter_of_volume(v);
+            dvol = v;
+            divides = true;
+          }
+          S.vol[i] = v;
+          tg += abs_diameter_of_volume(v) - me.d;
+        } else if (a.model == ABS_MODEL_DRIVE) {
+          double dl[3];
+          abs_drive_delta(me.x, me.y, me.z, a.mp[0], a.mp[1], a.mp[2], a.mp[3], a.seed, my_uid,
+                          a.iteration, dl);
+          tx += dl[0];
+          ty += dl[1];
+          tz += dl[2];
+        } else if (a.model == ABS_MODEL_GROW) {
+          if (me.d < a.mp[1]) {
+            const double rem = a.mp[1] - me.d;
+            tg += rem < a.mp[0] ? rem : a.mp[0];
+          }
+        }
+      }
+      // --- run_forces (simulation.cpp:463-489) --------------------------
+      if (a.detect_static && (fl & ABS_FLAG_STATIC)) {
+        ++n_skip;
+      } else {
+        const double r = 0.5 * (me.d + G.dmax);
+        double fx = 0.0, fy = 0.0, fz = 0.0;
+        unsigned int contributors = 0, evals = 0;
+        const double k = a.k;
+        for_each_neighbor(
+            G, S.pd, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r * r,
+            [&](unsigned int j, const Pd& q, double dx, double dy, double dz, double d2) {
+              ++evals;
+              // pairwise_repulsion (mechanics.cpp:10-27)
+              const double dist = sqrt(d2);
+              const double overlap = 0.5 * (me.d + q.d) - dist;
+              if (overlap <= 0.0) return;
+              double f0, f1, f2;
+              if (dist > 0.0) {
+                const double sc = k * overlap / dist;
+                f0 = dx * sc;
+                f1 = dy * sc;
+                f2 = dz * sc;
+              } else {
+                const unsigned long long ub = S.uid[j];
+                const unsigned long long lo = my_uid < ub ? my_uid : ub;
+                const unsigned long long hi = my_uid < ub ? ub : my_uid;
+                const double zz = -1.0 + 2.0 * abs_u01(abs_rng_word(lo, hi, 0));
+                const double phi = 2.0 * ABS_PI * abs_u01(abs_rng_word(lo, hi, 1));
+                const double rr = sqrt(fmax(0.0, 1.0 - zz * zz));
+                double d0 = rr * cos(phi), d1 = rr * sin(phi), d2v = zz;
+                if (my_uid != lo) { d0 *= -1.0; d1 *= -1.0; d2v *= -1.0; }
+                const double m = k * overlap;
+                f0 = d0 * m;
+                f1 = d1 * m;
+                f2 = d2v * m;
+              }
+              if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
+                ++contributors;
+                fx += f0;
+                fy += f1;
+                fz += f2;
+              }
+            });
+        n_eval += evals;
+        if (a.record_forces) {
+          S.force[i] = fx;
+          S.force[cap + i] = fy;
+          S.force[2 * cap + i] = fz;
+        }
+        S.partners[i] = contributors;
+        if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
+          tx += fx * a.dt;
+          ty += fy * a.dt;
+          tz += fz * a.dt;
+        }
+      }
+      // --- apply_pending (agent.hpp:115-133) -----------------------------
+      Pd np = me;
+      const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
+      if (disp > 0.0) {
+        if (disp > a.max_disp) {
+          const double sc = a.max_disp / disp;
+          tx *= sc;
+          ty *= sc;
+          tz *= sc;
+        }
+        np.x = me.x + tx;
+        np.y = me.y + ty;
+        np.z = me.z + tz;
+        fl |= ABS_FLAG_MOVED;
+      }
+      if (tg != 0.0) {
+        const double nd = me.d + tg;
+        np.d = nd > 1e-9 ? nd : 1e-9;
+        if (tg > 0.0) fl |= ABS_FLAG_GREW;
+      }
+      reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
+      reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
+      S.flags[i] = fl;
+    }
+    // --- stage daughters (warp-aggregated slot claim) ------------------
+    if (a.model == ABS_MODEL_PROLIFERATION) {
+      const unsigned int ballot = __ballot_sync(0xffffffffu, divides);
+      if (ballot) {
+        unsigned long long slot0 = 0;
+        if (lane == 0) slot0 = atomicAdd(&gw->staged, (unsigned long long)__popc(ballot));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+        if (divides) {
+          const unsigned long long slot = slot0 + __popc(ballot & ((1u << lane) - 1u));
+          st_parent[slot] = my_uid;
+          reinterpret_cast<double2*>(st_pd + slot)[0] = make_double2(dpx, dpy);
+          reinterpret_cast<double2*>(st_pd + slot)[1] = make_double2(dpz, dd);
+          st_vol[slot] = dvol;
+          div_mark[my_uid] = 1u;
+        }
+      }
+    }
+  }
+  // counters: warp reduce, one atomic per warp
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    n_eval += __shfl_xor_sync(0xffffffffu, n_eval, off);
+    n_skip += __shfl_xor_sync(0xffffffffu, n_skip, off);
+  }
+  if (lane == 0) {
+    if (n_eval) atomicAdd(&gw->evals, n_eval);
+    if (n_skip) atomicAdd(&gw->skips, n_skip);
+  }
+}
+
+// ------------------------------------------------------------ commit
+// mark_new_agent_neighbors (simulation.cpp:510-530): each staged daughter
+// flags new_neighbor on agents of the START-OF-STEP grid (reference boxes,
+// reference cull) using their CURRENT positions; no query exclusion.
+__global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
+                           const unsigned int* __restrict__ start, const Pd* __restrict__ st_pd) {
+  if (g->err) return;
+  const DevGrid G = *g;
+  const unsigned long long staged = G.staged, n = G.n;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < staged;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd c = load_pd(st_pd + k);
+    const double r = 0.5 * (c.d + G.dmax);
+    const double r2 = r * r;
+    if (r <= G.box) {
+      const double radius = sqrt(r2);
+      const double cc[3] = {c.x, c.y, c.z};
+      long long lo[3], hi[3];
+      for (int q = 0; q < 3; ++q) {
+        const long long a = static_cast<long long>(floor((cc[q] - radius - G.origin[q]) / G.box));
+        const long long b = static_cast<long long>(floor((cc[q] + radius - G.origin[q]) / G.box));
+        lo[q] = a > 0 ? a : 0;
+        hi[q] = b < (long long)G.dims[q] - 1 ? b : (long long)G.dims[q] - 1;
+      }
+      const double cull = r2 * (1.0 + 1e-12);
+      for (long long z = lo[2]; z <= hi[2]; ++z)
+        for (long long y = lo[1]; y <= hi[1]; ++y)
+          for (long long x = lo[0]; x <= hi[0]; ++x) {
+            double min_d2 = 0.0;
+            const long long at[3] = {x, y, z};
+            for (int q = 0; q < 3; ++q) {
+              const double b0 = G.origin[q] + static_cast<double>(at[q]) * G.box;
+              const double b1 = b0 + G.box;
+              const double gap = cc[q] < b0 ? b0 - cc[q] : (cc[q] > b1 ? cc[q] - b1 : 0.0);
+              min_d2 += gap * gap;
+            }
+            if (min_d2 > cull) continue;
+            // the box's sub-bins: B x B rows of B contiguous bins
+            for (unsigned int sz = 0; sz < G.B; ++sz)
+              for (unsigned int sy = 0; sy < G.B; ++sy) {
+                const unsigned int bz = (unsigned int)z * G.B + sz, by = (unsigned int)y * G.B + sy;
+                const unsigned int row = G.bd[0] * (by + G.bd[1] * bz) + (unsigned int)x * G.B;
+                for (unsigned int j = start[row]; j < start[row + G.B]; ++j) {
+                  const Pd q = load_pd(live + j);
+                  const double dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+                  if ((dx * dx + dy * dy) + dz * dz <= r2) S.flags[j] |= ABS_FLAG_NEW_NEIGHBOR;
+                }
+              }
+          }
+    } else {
+      for (unsigned long long j = 0; j < n; ++j) {
+        const Pd q = load_pd(live + j);
+        const double dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
+        if ((dx * dx + dy * dy) + dz * dz <= r2) S.flags[j] |= ABS_FLAG_NEW_NEIGHBOR;
+      }
+    }
+  }
+}
+
+// Daughters get uid = uid_count + rank of the parent among this iteration's
+// dividers in parent-uid order (= the reference's one-worker storage order
+// while storage order equals uid order, resource_manager.hpp:44-46), and are
+// appended at n + rank (commit.cpp:258-292: appends never move survivors).
+__global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
+                         const unsigned long long* __restrict__ st_parent,
+                         const Pd* __restrict__ st_pd, const double* __restrict__ st_vol,
+                         const unsigned int* __restrict__ div_rank, unsigned long long cap,
+                         int record_forces) {
+  if (g->err) return;
+  const unsigned long long staged = g->staged, n = g->n, uc = g->uid_count;
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < staged;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned int rk = div_rank[st_parent[k]];
+    const unsigned long long j = n + rk;
+    const Pd p = st_pd[k];
+    reinterpret_cast<double2*>(live + j)[0] = make_double2(p.x, p.y);
+    reinterpret_cast<double2*>(live + j)[1] = make_double2(p.z, p.d);
+    S.uid[j] = uc + rk;
+    S.flags[j] = ABS_FLAG_NEWLY_ADDED;
+    S.partners[j] = 0;
+    S.beh[j] = 1;
+    S.vol[j] = st_vol[k];
+    if (record_forces) S.force[j] = S.force[cap + j] = S.force[2 * cap + j] = 0.0;
+  }
+}
+
+__global__ void k_commit_fin(DevGrid* g) {
+  if (threadIdx.x || blockIdx.x || g->err) return;
+  const unsigned long long s = g->staged;
+  g->n += s;
+  g->uid_count += s;
+  g->added += s;
+  g->staged = 0;
+}
+
+__global__ void k_zero_marks(unsigned int* __restrict__ m, const DevGrid* g) {
+  if (g->err || g->staged == 0) return;
+  const unsigned long long len = g->uid_count + 1;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    m[i] = 0;
+}
+
+// ------------------------------------------------------------ parity helpers
+__global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* out) {
+  const DevGrid G = *g;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const unsigned long long c0 = box_coord(p.x, G.origin[0], G.box, G.dims[0]);
+    const unsigned long long c1 = box_coord(p.y, G.origin[1], G.box, G.dims[1]);
+    const unsigned long long c2 = box_coord(p.z, G.origin[2], G.box, G.dims[2]);
+    out[i] = c0 + G.dims[0] * (c1 + (unsigned long long)G.dims[1] * c2);
+  }
+}
+
+__global__ void k_nbr_count(const Pd* __restrict__ pd, const DevGrid* g,
+                            const unsigned int* __restrict__ start, unsigned long long* cnt) {
+  const DevGrid G = *g;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd me = load_pd(pd + i);
+    const double r = 0.5 * (me.d + G.dmax);
+    unsigned long long c = 0;
+    for_each_neighbor(G, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
+                      [&](unsigned int, const Pd&, double, double, double, double) { ++c; });
+    cnt[i] = c;
+  }
+}
+
+__global__ void k_nbr_fill(const Pd* __restrict__ pd, const unsigned long long* __restrict__ uid,
+                           const DevGrid* g, const unsigned int* __restrict__ start,
+                           const unsigned long long* __restrict__ off, unsigned long long* out) {
+  const DevGrid G = *g;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd me = load_pd(pd + i);
+    const double r = 0.5 * (me.d + G.dmax);
+    unsigned long long w = off[i];
+    for_each_neighbor(G, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
+                      [&](unsigned int j, const Pd&, double, double, double, double) { out[w++] = uid[j]; });
+    // insertion sort of this agent's uid list
+    const unsigned long long b = off[i], e = off[i + 1];
+    for (unsigned long long p = b + 1; p < e; ++p) {
+      const unsigned long long v = out[p];
+      unsigned long long q = p;
+      while (q > b && out[q - 1] > v) {
+        out[q] = out[q - 1];
+        --q;
+      }
+      out[q] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------ sort_and_balance
+// Morton code of a box (morton.cpp:11-29, 54-60).
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+// sort key = (morton code of the reference box) << 32 | (~storage index):
+// ascending key = curve order, descending index inside a box (chain order).
+__global__ void k_sort_keys(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* keyhi,
+                            unsigned int* __restrict__ idx) {
+  const DevGrid G = *g;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const unsigned long long c0 = box_coord(p.x, G.origin[0], G.box, G.dims[0]);
+    const unsigned long long c1 = box_coord(p.y, G.origin[1], G.box, G.dims[1]);
+    const unsigned long long c2 = box_coord(p.z, G.origin[2], G.box, G.dims[2]);
+    const unsigned long long code = G.dims[2] == 1 ? 0ull : (spread3(c0) | spread3(c1) << 1 | spread3(c2) << 2);
+    unsigned long long code2 = code;
+    if (G.dims[2] == 1) {  // 2-D table (morton.cpp:124-129): x bits 2i, y bits 2i+1
+      unsigned long long xx = c0, yy = c1, o = 0;
+      for (int b = 0; b < 31; ++b) o |= ((xx >> b) & 1ull) << (2 * b) | ((yy >> b) & 1ull) << (2 * b + 1);
+      code2 = o;
+    }
+    keyhi[i] = code2;
+    idx[i] = static_cast<unsigned int>(i);
+  }
+}
+
+__device__ __forceinline__ unsigned int radix_digit(unsigned long long code, unsigned int idx, int shift) {
+  return shift < 32 ? ((0xFFFFFFFFu - idx) >> shift) & 255u
+                    : static_cast<unsigned int>((code >> (shift - 32)) & 255ull);
+}
+
+// One LSD radix pass (8 bits) over (key, idx) pairs with a stable
+// counting sort per digit: histogram -> scan -> rank by prefix popcounts.
+__global__ void k_radix_hist(const unsigned long long* __restrict__ key, const unsigned int* __restrict__ idx,
+                             unsigned long long n, int shift, unsigned int* __restrict__ hist,
+                             unsigned long long chunk) {
+  __shared__ unsigned int h[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const unsigned long long b = blockIdx.x * chunk, e = min(n, b + chunk);
+  for (unsigned long long i = b + threadIdx.x; i < e; i += blockDim.x) {
+    atomicAdd(&h[radix_digit(key[i], idx[i], shift)], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) hist[t * gridDim.x + blockIdx.x] = h[t];
+}
+
+__global__ void k_radix_scatter(const unsigned long long* __restrict__ key, const unsigned int* __restrict__ idx,
+                                unsigned long long* __restrict__ key2, unsigned int* __restrict__ idx2,
+                                unsigned long long n, int shift, const unsigned int* __restrict__ hist,
+                                unsigned long long chunk) {
+  // one warp per block walks its chunk in order: stable by construction
+  __shared__ unsigned int base[256];
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) base[t] = hist[t * gridDim.x + blockIdx.x];
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const unsigned long long b = blockIdx.x * chunk, e = min(n, b + chunk);
+  const int lane = threadIdx.x;
+  for (unsigned long long i0 = b; i0 < e; i0 += 32) {
+    const unsigned long long i = i0 + lane;
+    const bool ok = i < e;
+    unsigned int dig = 0;
+    unsigned long long k = 0;
+    unsigned int ix = 0;
+    if (ok) {
+      k = key[i];
+      ix = idx[i];
+      dig = radix_digit(k, ix, shift);
+    }
+    const unsigned int peers = __match_any_sync(0xffffffffu, ok ? dig : 0x1000u);
+    const unsigned int before = __popc(peers & ((1u << lane) - 1u));
+    unsigned int pos = 0;
+    if (ok) pos = base[dig] + before;
+    __syncwarp();
+    const int leader = __ffs(peers) - 1;
+    if (ok && lane == leader) base[dig] += __popc(peers);
+    __syncwarp();
+    if (ok) {
+      key2[pos] = k;
+      idx2[pos] = ix;
+    }
+  }
+}
+
+__global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const unsigned int* __restrict__ perm,
+                         unsigned long long n, unsigned long long cap, int carry_vol, int carry_force) {
+  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < n;
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned int i = perm[j];
+    const Pd p = load_pd(pos + i);
+    reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
+    reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
+    dst.uid[j] = src.uid[i];
+    dst.flags[j] = src.flags[i];
+    dst.partners[j] = src.partners[i];
+    dst.beh[j] = src.beh[i];
+    if (carry_vol) dst.vol[j] = src.vol[i];
+    if (carry_force) {
+      dst.force[j] = src.force[i];
+      dst.force[cap + j] = src.force[cap + i];
+      dst.force[2 * cap + j] = src.force[2 * cap + i];
+    }
+  }
+}
+
+// ------------------------------------------------------------ removal
+// remove_agents_parallel (commit.cpp:86-178): holes left of the split are
+// filled, in removal-list order, by surviving tail agents in index order.
+__global__ void k_remove_plan(const unsigned long long* __restrict__ slots, unsigned long long r,
+                              unsigned long long new_size, unsigned int* __restrict__ to_right,
+                              unsigned int* __restrict__ tail_alive) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long idx = slots[k];
+    if (idx < new_size) to_right[k] = 1;
+    else tail_alive[idx - new_size] = 0;
+  }
+}
+
+__global__ void k_remove_move(const Pd* pos_in, Pd* pos, Soa S, const unsigned long long* __restrict__ slots,
+                              unsigned long long r, unsigned long long new_size,
+                              const unsigned int* __restrict__ hole_rank, const unsigned int* __restrict__ to_right,
+                              const unsigned int* __restrict__ mover_rank, const unsigned int* __restrict__ tail_alive,
+                              unsigned int* __restrict__ hole_at, unsigned long long cap, int phase) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    if (phase == 0) {
+      if (to_right[k]) hole_at[hole_rank[k]] = static_cast<unsigned int>(slots[k]);
+    } else if (tail_alive[k]) {
+      const unsigned long long src = new_size + k;
+      const unsigned long long dst = hole_at[mover_rank[k]];
+      const Pd p = pos_in[src];
+      pos[dst] = p;
+      S.uid[dst] = S.uid[src];
+      S.flags[dst] = S.flags[src];
+      S.partners[dst] = S.partners[src];
+      S.beh[dst] = S.beh[src];
+      S.vol[dst] = S.vol[src];
+      S.force[dst] = S.force[src];
+      S.force[cap + dst] = S.force[cap + src];
+      S.force[2 * cap + dst] = S.force[2 * cap + src];
+    }
+  }
+}
+
+__global__ void k_uid_to_slot(const unsigned long long* __restrict__ uid, unsigned long long n,
+                              unsigned long long* __restrict__ map) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    map[uid[i]] = i;
+}
+
+__global__ void k_set_u32(unsigned int* a, unsigned long long n, unsigned int v) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+}  // namespace
+
+// ====================================================================== host
+struct abs_gpu_ctx {
+  abs_gpu_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int sms = 148;
+
+  unsigned long long cap = 0;      // agent capacity
+  unsigned long long uid_cap = 0;  // uid-indexed arrays
+  unsigned long long bins_cap = 0;
+  unsigned long long n = 0;        // host mirror (refreshed on sync)
+  unsigned long long iteration = 0;
+  unsigned long long launches = 0;
+
+  Soa S[2]{};
+  int cur = 0;
+  Pd* newpd = nullptr;
+  bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
+  bool grid_valid = false; // `start` holds a scanned cell table for S[cur]
+
+  DevGrid* g = nullptr;
+  unsigned int* start = nullptr;  // bins_cap
+  unsigned int* key = nullptr;
+  unsigned int* rank = nullptr;
+  unsigned int* tiles = nullptr;  // scan tile sums (u32)
+  unsigned long long* tiles64 = nullptr;
+  unsigned char* nv = nullptr;
+  unsigned char* nn = nullptr;
+  unsigned long long* st_parent = nullptr;
+  Pd* st_pd = nullptr;
+  double* st_vol = nullptr;
+  unsigned int* div_mark = nullptr;  // uid_cap + 1
+
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t ev_used = 0;
+  double force_ms = 0.0;
+  unsigned long long force_launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int set_err(abs_gpu_ctx* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  else g_create_err = m;
+  return code;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(c, ABS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
+  const unsigned long long b = (work + kThreads - 1) / kThreads;
+  const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 8;
+  return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
+}
+
+template <class T>
+cudaError_t dalloc(T** p, unsigned long long count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+void free_soa(Soa& s) {
+  cudaFree(s.pd); cudaFree(s.uid); cudaFree(s.flags); cudaFree(s.partners);
+  cudaFree(s.vol); cudaFree(s.beh); cudaFree(s.force);
+  s = Soa{};
+}
+
+cudaError_t alloc_soa(Soa& s, unsigned long long cap) {
+  cudaError_t e;
+  if ((e = dalloc(&s.pd, cap))) return e;
+  if ((e = dalloc(&s.uid, cap))) return e;
+  if ((e = dalloc(&s.flags, cap))) return e;
+  if ((e = dalloc(&s.partners, cap))) return e;
+  if ((e = dalloc(&s.vol, cap))) return e;
+  if ((e = dalloc(&s.beh, cap))) return e;
+  if ((e = dalloc(&s.force, 3 * cap))) return e;
+  return cudaSuccess;
+}
+
+Pd* cur_pos(abs_gpu_ctx* c) { return c->pos_in_new ? c->newpd : c->S[c->cur].pd; }
+
+// (Re)allocate agent-sized buffers preserving the first `keep` agents.
+int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long keep) {
+  if (want <= c->cap && c->uid_cap >= 2 * want) return ABS_OK;
+  unsigned long long ncap = std::max<unsigned long long>(want, 1024);
+  Soa S2[2]{};
+  for (int b = 0; b < 2; ++b) CK(alloc_soa(S2[b], ncap));
+  Pd* np = nullptr;
+  CK(dalloc(&np, ncap));
+  if (keep) {
+    Soa& src = c->S[c->cur];
+    Soa& dst = S2[0];
+    CK(cudaMemcpyAsync(np, cur_pos(c), keep * sizeof(Pd), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.uid, src.uid, keep * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.flags, src.flags, keep, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.partners, src.partners, keep * 4, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.vol, src.vol, keep * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.beh, src.beh, keep, cudaMemcpyDeviceToDevice, c->stream));
+    for (int q = 0; q < 3; ++q)
+      CK(cudaMemcpyAsync(dst.force + q * ncap, src.force + q * c->cap, keep * 8, cudaMemcpyDeviceToDevice,
+                         c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  free_soa(c->S[0]);
+  free_soa(c->S[1]);
+  cudaFree(c->newpd);
+  c->S[0] = S2[0];
+  c->S[1] = S2[1];
+  c->cur = 0;
+  c->newpd = np;
+  c->pos_in_new = true;
+  c->grid_valid = false;
+  cudaFree(c->key); cudaFree(c->rank); cudaFree(c->nv); cudaFree(c->nn);
+  cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
+  cudaFree(c->tiles64);
+  CK(dalloc(&c->key, ncap));
+  CK(dalloc(&c->rank, ncap));
+  CK(dalloc(&c->nv, ncap));
+  CK(dalloc(&c->nn, ncap));
+  CK(cudaMemsetAsync(c->nv, 0, ncap, c->stream));
+  CK(cudaMemsetAsync(c->nn, 0, ncap, c->stream));
+  CK(dalloc(&c->st_parent, ncap));
+  CK(dalloc(&c->st_pd, ncap));
+  CK(dalloc(&c->st_vol, ncap));
+  c->uid_cap = 2 * ncap + 1;
+  CK(dalloc(&c->div_mark, c->uid_cap + 1));
+  CK(cudaMemsetAsync(c->div_mark, 0, (c->uid_cap + 1) * 4, c->stream));
+  CK(dalloc(&c->tiles64, (2 * ncap + kScanTile) / kScanTile + 1));
+  c->cap = ncap;
+  return ABS_OK;
+}
+
+int ensure_bins(abs_gpu_ctx* c, unsigned long long want) {
+  if (want <= c->bins_cap) return ABS_OK;
+  unsigned long long nb = std::max<unsigned long long>(want + want / 2, 4096);
+  cudaFree(c->start);
+  cudaFree(c->tiles);
+  CK(dalloc(&c->start, nb + 1));
+  CK(cudaMemsetAsync(c->start, 0, (nb + 1) * 4, c->stream));
+  CK(dalloc(&c->tiles, nb / kScanTile + 2));
+  c->bins_cap = nb;
+  c->grid_valid = false;
+  return ABS_OK;
+}
+
+template <typename T>
+void launch_scan(abs_gpu_ctx* c, T* data, const unsigned long long* len_dev, unsigned long long len_cap,
+                 T* tiles, const int* err) {
+  const unsigned int nt = static_cast<unsigned int>((len_cap + kScanTile - 1) / kScanTile);
+  const unsigned int blocks = std::max(1u, nt);
+  k_scan_tiles<T><<<blocks, kThreads, 0, c->stream>>>(data, len_dev, tiles, err);
+  k_scan_partials<T><<<1, kThreads, 0, c->stream>>>(tiles, len_dev, err);
+  k_scan_apply<T><<<blocks, kThreads, 0, c->stream>>>(data, len_dev, tiles, err);
+  c->launches += 3;
+}
+
+StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
+  StepArgs a{};
+  a.seed = c->cfg.seed;
+  a.iteration = iteration;
+  a.dt = c->cfg.simulation_time_step;
+  a.k = c->cfg.repulsion_coefficient;
+  a.max_disp = c->cfg.max_displacement;
+  a.threshold2 = c->cfg.force_threshold * c->cfg.force_threshold;
+  for (int q = 0; q < 8; ++q) a.mp[q] = c->cfg.model_params[q];
+  a.model = c->cfg.model;
+  a.detect_static = c->cfg.detect_static_agents;
+  a.record_forces = c->cfg.record_forces;
+  return a;
+}
+
+int bins_cfg(const abs_gpu_ctx* c) { return c->cfg.bins_per_box == 2 ? 2 : 1; }
+
+// Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
+void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
+  const int nb = grid_blocks(c, c->cap);
+  const unsigned long long* nbins_dev = &c->g->nbins;
+  if (c->grid_valid) {  // previous cell table still holds scanned offsets
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, nbins_dev, 1, &c->g->err);
+    ++c->launches;
+  }
+  const Pd* pos = cur_pos(c);
+  k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_cfg(c), c->bins_cap, c->cap,
+                                      c->uid_cap, may_add, iteration);
+  k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+  c->launches += 3;
+  launch_scan<unsigned int>(c, c->start, nbins_dev, c->bins_cap, c->tiles, &c->g->err);
+  const int nxt = c->cur ^ 1;
+  k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->start, c->key, c->rank, c->g,
+                                            c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
+                                            c->cfg.record_forces);
+  ++c->launches;
+  c->cur = nxt;
+  c->pos_in_new = false;
+  c->grid_valid = true;
+}
+
+void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
+  launch_env_update(c, iteration, c->cfg.model == ABS_MODEL_PROLIFERATION);
+  const int nb = grid_blocks(c, c->cap);
+  const StepArgs a = step_args(c, iteration);
+  Soa& S = c->S[c->cur];
+  if (c->cfg.detect_static_agents && iteration > 0) {
+    k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn);
+    ++c->launches;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    if (c->ev_used + 2 > c->ev.size()) {
+      for (int q = 0; q < 256; ++q) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev.push_back(e);
+      }
+    }
+    e0 = c->ev[c->ev_used++];
+    e1 = c->ev[c->ev_used++];
+    cudaEventRecord(e0, c->stream);
+  }
+  k_force<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap,
+                                          c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+  ++c->launches;
+  if (c->timing) cudaEventRecord(e1, c->stream);
+  c->pos_in_new = true;
+  if (c->cfg.model == ABS_MODEL_PROLIFERATION) {
+    if (c->cfg.detect_static_agents) {
+      k_mark_new<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->st_pd);
+      ++c->launches;
+    }
+    const unsigned long long* uc = &c->g->uid_count;
+    launch_scan<unsigned int>(c, c->div_mark, uc, c->uid_cap, reinterpret_cast<unsigned int*>(c->tiles64),
+                              &c->g->err);
+    k_append<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->st_parent, c->st_pd, c->st_vol,
+                                             c->div_mark, c->cap, c->cfg.record_forces);
+    k_zero_marks<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->div_mark, c->g);
+    k_commit_fin<<<1, 32, 0, c->stream>>>(c->g);
+    c->launches += 3;
+  }
+}
+
+int read_grid(abs_gpu_ctx* c, DevGrid* h) {
+  CK(cudaMemcpyAsync(h, c->g, sizeof(DevGrid), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->n = h->n;
+  return ABS_OK;
+}
+
+int map_dev_err(abs_gpu_ctx* c, const DevGrid& h) {
+  switch (h.err) {
+    case kErrNone: return ABS_OK;
+    case kErrNonFinite:
+      return set_err(c, ABS_ERR_NONFINITE, "operation 'environment update' failed at iteration " +
+                                               std::to_string(h.failed_iteration) + ": agent positions are not finite");
+    case kErrFixedBox:
+      return set_err(c, ABS_ERR_FIXED_BOX, "operation 'environment update' failed at iteration " +
+                                               std::to_string(h.failed_iteration) +
+                                               ": fixed box length is smaller than the largest agent diameter");
+    case kErrBoxBudget:
+      return set_err(c, ABS_ERR_BOX_BUDGET, "operation 'environment update' failed at iteration " +
+                                                std::to_string(h.failed_iteration) + ": grid would exceed the box budget");
+    default: return set_err(c, ABS_ERR_STATE, "internal retry state leaked");
+  }
+}
+
+int clear_dev_err(abs_gpu_ctx* c) {
+  CK(cudaMemsetAsync(&c->g->err, 0, sizeof(int), c->stream));
+  return ABS_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void abs_gpu_default_config(abs_gpu_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->seed = 42;
+  cfg->simulation_time_step = 0.1;
+  cfg->repulsion_coefficient = 2.0;
+  cfg->max_displacement = 3.0;
+  cfg->force_threshold = 0.0;
+  cfg->fixed_box_length = 0.0;
+  cfg->record_forces = 1;
+  cfg->bins_per_box = 0;
+}
+
+const char* abs_gpu_last_error(const abs_gpu_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
+  abs_gpu_ctx* c = nullptr;
+  if (!cfg || !out) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "null argument");
+  // SimulationParams::validate (params.cpp:44-72), hot-path fields
+  if (cfg->fixed_box_length < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "fixed_box_length must be >= 0");
+  if (!(cfg->simulation_time_step > 0.0))
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "simulation_time_step must be > 0");
+  if (cfg->repulsion_coefficient < 0.0)
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "repulsion_coefficient must be >= 0");
+  if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
+  if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
+  if (cfg->model < 0 || cfg->model > 3) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return set_err(nullptr, ABS_ERR_NO_DEVICE, "no CUDA device available");
+  if (device < 0 || device >= count) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "bad device index");
+  if (cudaSetDevice(device) != cudaSuccess) return set_err(nullptr, ABS_ERR_CUDA, "cudaSetDevice failed");
+  c = new abs_gpu_ctx();
+  c->cfg = *cfg;
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  CK(cudaMalloc(&c->g, sizeof(DevGrid)));
+  DevGrid h{};
+  h.red[0] = h.red[1] = h.red[2] = kInfOrdLo;
+  h.red[3] = h.red[4] = h.red[5] = kInfOrdHi;
+  h.red[6] = kZeroOrd;
+  h.dims[0] = h.dims[1] = h.dims[2] = 1;
+  h.B = 1;
+  CK(cudaMemcpy(c->g, &h, sizeof h, cudaMemcpyHostToDevice));
+  int rc = ensure_capacity(c, std::max<unsigned long long>(cfg->capacity, 1024), 0);
+  if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
+  rc = ensure_bins(c, 1 << 16);
+  if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
+  *out = c;
+  return ABS_OK;
+}
+
+int abs_gpu_destroy(abs_gpu_ctx* c) {
+  if (!c) return ABS_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_soa(c->S[0]);
+  free_soa(c->S[1]);
+  cudaFree(c->newpd); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
+  cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
+  cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return ABS_OK;
+}
+
+static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long long uid_count,
+                         cudaMemcpyKind kind, const uint64_t* uid, const double* x, const double* y,
+                         const double* z, const double* d, const uint8_t* mask, const double* volume,
+                         const uint8_t* flags, const uint32_t* partners) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (n && (!x || !y || !z || !d)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null coordinate array");
+  if (n >= 0xFFFFFFF0ull) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "too many agents");
+  cudaSetDevice(c->device);
+  int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * n + 1024), 0);
+  if (rc) return rc;
+  const bool host = kind == cudaMemcpyHostToDevice;
+  std::vector<Pd> hp;
+  std::vector<unsigned long long> hu;
+  std::vector<unsigned char> hb, hf;
+  std::vector<double> hv;
+  std::vector<unsigned int> hpart;
+  Soa& S = c->S[c->cur];
+  if (host) {
+    hp.resize(n);
+    hv.resize(n);
+    hb.resize(n);
+    for (unsigned long long i = 0; i < n; ++i) {
+      if (!(d[i] > 0.0)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "diameter must be > 0");
+      hp[i] = Pd{x[i], y[i], z[i], d[i]};
+      hv[i] = volume ? volume[i] : abs_volume_of_diameter(d[i]);
+      hb[i] = (c->cfg.model != ABS_MODEL_NONE && (!mask || mask[i])) ? 1 : 0;
+    }
+    unsigned long long maxuid = n;
+    if (uid) {
+      hu.assign(uid, uid + n);
+      for (unsigned long long u : hu) maxuid = std::max(maxuid, u + 1);
+    } else {
+      hu.resize(n);
+      for (unsigned long long i = 0; i < n; ++i) hu[i] = i;
+    }
+    uid_count = std::max(uid_count, maxuid);
+    if (uid_count + 1 > c->uid_cap) {
+      rc = ensure_capacity(c, uid_count, 0);
+      if (rc) return rc;
+    }
+    hf.assign(n, 0);
+    if (flags) hf.assign(flags, flags + n);
+    hpart.assign(n, 0);
+    if (partners) hpart.assign(partners, partners + n);
+    CK(cudaMemcpyAsync(c->newpd, hp.data(), n * sizeof(Pd), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(S.uid, hu.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(S.vol, hv.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(S.beh, hb.data(), n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(S.flags, hf.data(), n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(S.partners, hpart.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    // device-resident inputs: interleave on the device
+    std::vector<unsigned long long> dummy;
+    if (uid_count < n) uid_count = n;
+    if (uid_count + 1 > c->uid_cap) {
+      rc = ensure_capacity(c, uid_count, 0);
+      if (rc) return rc;
+    }
+    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 0, sizeof(Pd), x, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 8, sizeof(Pd), y, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 16, sizeof(Pd), z, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 24, sizeof(Pd), d, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
+    if (uid) {
+      CK(cudaMemcpyAsync(S.uid, uid, n * 8, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      hu.resize(n);
+      for (unsigned long long i = 0; i < n; ++i) hu[i] = i;
+      CK(cudaMemcpyAsync(S.uid, hu.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    if (mask) CK(cudaMemcpyAsync(S.beh, mask, n, cudaMemcpyDeviceToDevice, c->stream));
+    else CK(cudaMemsetAsync(S.beh, c->cfg.model != ABS_MODEL_NONE ? 1 : 0, n, c->stream));
+    CK(cudaMemsetAsync(S.flags, 0, n, c->stream));
+    CK(cudaMemsetAsync(S.partners, 0, n * 4, c->stream));
+    CK(cudaMemsetAsync(S.vol, 0, n * 8, c->stream));
+  }
+  CK(cudaMemsetAsync(S.force, 0, 3 * c->cap * 8, c->stream));
+  DevGrid h{};
+  h.red[0] = h.red[1] = h.red[2] = kInfOrdLo;
+  h.red[3] = h.red[4] = h.red[5] = kInfOrdHi;
+  h.red[6] = kZeroOrd;
+  h.dims[0] = h.dims[1] = h.dims[2] = 1;
+  h.B = 1;
+  h.n = n;
+  h.uid_count = uid_count;
+  CK(cudaMemcpyAsync(c->g, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->pos_in_new = true;
+  c->grid_valid = false;
+  c->n = n;
+  c->iteration = 0;
+  return ABS_OK;
+}
+
+int abs_gpu_upload(abs_gpu_ctx* c, uint64_t n, const uint64_t* uid, const double* x, const double* y,
+                   const double* z, const double* d, const uint8_t* mask, const double* volume,
+                   const uint8_t* flags, const uint32_t* partners, uint64_t uid_count) {
+  return upload_common(c, n, uid_count, cudaMemcpyHostToDevice, uid, x, y, z, d, mask, volume, flags, partners);
+}
+
+int abs_gpu_upload_device(abs_gpu_ctx* c, uint64_t n, const uint64_t* uid, const double* x, const double* y,
+                          const double* z, const double* d, const uint8_t* mask, uint64_t uid_count) {
+  return upload_common(c, n, uid_count, cudaMemcpyDeviceToDevice, uid, x, y, z, d, mask, nullptr, nullptr,
+                       nullptr);
+}
+
+int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  // Launch in chunks; a chunk whose finalize asked for more bins/capacity is
+  // rolled back to the failed iteration (no kernel touched state after it).
+  unsigned long long done = 0;
+  const unsigned long long chunk = 32;
+  while (done < iterations) {
+    const unsigned long long todo = std::min<unsigned long long>(chunk, iterations - done);
+    struct Snap { int cur; bool pos_in_new; bool grid_valid; };
+    std::vector<Snap> snaps;
+    snaps.reserve(todo);
+    for (unsigned long long t = 0; t < todo; ++t) {
+      snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
+      launch_iteration(c, c->iteration + t);
+    }
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) return set_err(c, ABS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+    DevGrid h{};
+    int rc = read_grid(c, &h);
+    if (rc) return rc;
+    if (h.err == kErrNone) {
+      c->iteration += todo;
+      done += todo;
+      continue;
+    }
+    const unsigned long long fi = h.failed_iteration;
+    const unsigned long long off = fi - c->iteration;
+    if (fi < c->iteration || off >= todo) return set_err(c, ABS_ERR_STATE, "bad failed iteration");
+    c->cur = snaps[off].cur;
+    c->pos_in_new = snaps[off].pos_in_new;
+    c->grid_valid = false;  // finalize may have left a partially filled count table
+    c->iteration = fi;
+    done += off;
+    if (h.err == kErrBinsRetry) {
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      rc = ensure_bins(c, h.needed_bins);
+      if (rc) return rc;
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+    } else if (h.err == kErrCapRetry) {
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      rc = ensure_capacity(c, 2 * c->cap, h.n);
+      if (rc) return rc;
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+    } else {
+      rc = map_dev_err(c, h);
+      clear_dev_err(c);
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      return rc;
+    }
+  }
+  return ABS_OK;
+}
+
+int abs_gpu_set_iteration(abs_gpu_ctx* c, uint64_t iteration) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  c->iteration = iteration;
+  return ABS_OK;
+}
+
+int abs_gpu_synchronize(abs_gpu_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
+int abs_gpu_stats(abs_gpu_ctx* c, abs_step_stats* out) {
+  if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  out->agents = h.n;
+  out->uid_count = h.uid_count;
+  out->iterations = c->iteration;
+  out->force_evaluations = h.evals;
+  out->force_skips = h.skips;
+  out->agents_added = h.added;
+  out->agents_removed = h.removed;
+  out->kernel_launches = c->launches;
+  return ABS_OK;
+}
+
+int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, double* y, double* z, double* d,
+                     double* fx, double* fy, double* fz, uint32_t* partners, uint8_t* flags, double* volume) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  const unsigned long long n = h.n;
+  if (n_out) *n_out = n;
+  Soa& S = c->S[c->cur];
+  if (x || y || z || d) {
+    std::vector<Pd> hp(n);
+    CK(cudaMemcpy(hp.data(), cur_pos(c), n * sizeof(Pd), cudaMemcpyDeviceToHost));
+    for (unsigned long long i = 0; i < n; ++i) {
+      if (x) x[i] = hp[i].x;
+      if (y) y[i] = hp[i].y;
+      if (z) z[i] = hp[i].z;
+      if (d) d[i] = hp[i].d;
+    }
+  }
+  if (uid) CK(cudaMemcpy(uid, S.uid, n * 8, cudaMemcpyDeviceToHost));
+  if (fx) CK(cudaMemcpy(fx, S.force, n * 8, cudaMemcpyDeviceToHost));
+  if (fy) CK(cudaMemcpy(fy, S.force + c->cap, n * 8, cudaMemcpyDeviceToHost));
+  if (fz) CK(cudaMemcpy(fz, S.force + 2 * c->cap, n * 8, cudaMemcpyDeviceToHost));
+  if (partners) CK(cudaMemcpy(partners, S.partners, n * 4, cudaMemcpyDeviceToHost));
+  if (flags) {
+    CK(cudaMemcpy(flags, S.flags, n, cudaMemcpyDeviceToHost));
+    for (unsigned long long i = 0; i < n; ++i) flags[i] &= 63u;
+  }
+  if (volume) {
+    CK(cudaMemcpy(volume, S.vol, n * 8, cudaMemcpyDeviceToHost));
+    if (c->cfg.model != ABS_MODEL_PROLIFERATION)
+      for (unsigned long long i = 0; i < n; ++i) volume[i] = 0.0;
+  }
+  return ABS_OK;
+}
+
+int abs_gpu_env_update(abs_gpu_ctx* c) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    const int cur0 = c->cur;
+    const bool pin0 = c->pos_in_new;
+    launch_env_update(c, c->iteration, 0);
+    DevGrid h{};
+    int rc = read_grid(c, &h);
+    if (rc) return rc;
+    if (h.err == kErrNone) return ABS_OK;
+    c->cur = cur0;  // the scatter did not run
+    c->pos_in_new = pin0;
+    c->grid_valid = false;
+    CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+    if (h.err == kErrBinsRetry) {
+      rc = ensure_bins(c, h.needed_bins);
+      if (rc) return rc;
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+      continue;
+    }
+    rc = map_dev_err(c, h);
+    clear_dev_err(c);
+    CK(cudaStreamSynchronize(c->stream));
+    return rc;
+  }
+  return set_err(c, ABS_ERR_STATE, "environment update did not converge");
+}
+
+int abs_gpu_grid_info(abs_gpu_ctx* c, double* grid, uint32_t* dims) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (grid) {
+    grid[0] = h.origin[0]; grid[1] = h.origin[1]; grid[2] = h.origin[2];
+    grid[3] = h.box; grid[4] = h.dmax;
+  }
+  if (dims) { dims[0] = h.dims[0]; dims[1] = h.dims[1]; dims[2] = h.dims[2]; }
+  return ABS_OK;
+}
+
+int abs_gpu_cell_ids(abs_gpu_ctx* c, uint64_t* out) {
+  if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c->grid_valid) return set_err(c, ABS_ERR_STATE, "cell ids require abs_gpu_env_update");
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  unsigned long long* d_out = nullptr;
+  CK(dalloc(&d_out, h.n));
+  k_cell_ids<<<grid_blocks(c, h.n), kThreads, 0, c->stream>>>(cur_pos(c), c->g, d_out);
+  ++c->launches;
+  CK(cudaMemcpyAsync(out, d_out, h.n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_out);
+  return ABS_OK;
+}
+
+int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_t cap, uint64_t* total) {
+  if (!c || !offsets) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c->grid_valid) return set_err(c, ABS_ERR_STATE, "neighbour queries require abs_gpu_env_update");
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  const unsigned long long n = h.n;
+  unsigned long long *cnt = nullptr, *len = nullptr, *t64 = nullptr, *out = nullptr;
+  CK(dalloc(&cnt, n + 1));
+  CK(dalloc(&len, 1));
+  CK(dalloc(&t64, (n + 1) / kScanTile + 2));
+  CK(cudaMemcpyAsync(len, &n, 8, cudaMemcpyHostToDevice, c->stream));
+  const Pd* pd = c->S[c->cur].pd;
+  k_nbr_count<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->g, c->start, cnt);
+  ++c->launches;
+  launch_scan<unsigned long long>(c, cnt, len, n + 1, t64, nullptr);
+  CK(cudaMemcpyAsync(offsets, cnt, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const unsigned long long tot = offsets[n];
+  if (total) *total = tot;
+  if (tot > cap || !uids) {
+    cudaFree(cnt); cudaFree(len); cudaFree(t64);
+    return tot > cap ? set_err(c, ABS_ERR_CAPACITY, "neighbour buffer too small") : ABS_OK;
+  }
+  CK(dalloc(&out, tot));
+  k_nbr_fill<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->S[c->cur].uid, c->g, c->start, cnt, out);
+  ++c->launches;
+  CK(cudaMemcpyAsync(uids, out, tot * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(cnt); cudaFree(len); cudaFree(t64); cudaFree(out);
+  return ABS_OK;
+}
+
+int abs_gpu_sort(abs_gpu_ctx* c) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  // grid for the current state WITHOUT re-binning (the sort order depends on
+  // the current storage order, sort_balance.cpp:88-128)
+  const Pd* pos = cur_pos(c);
+  if (c->grid_valid) {
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->nbins, 1, nullptr);
+    ++c->launches;
+    c->grid_valid = false;
+  }
+  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, ~0ull, ~0ull, ~0ull, 0, c->iteration);
+  c->launches += 2;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (h.err) {
+    rc = map_dev_err(c, h);
+    clear_dev_err(c);
+    return rc;
+  }
+  const unsigned long long n = h.n;
+  if (n == 0) return ABS_OK;
+  unsigned long long *k1, *k2;
+  unsigned int *i1, *i2, *hist;
+  const unsigned long long chunk = 4096;
+  const unsigned int blocks = static_cast<unsigned int>((n + chunk - 1) / chunk);
+  CK(dalloc(&k1, n)); CK(dalloc(&k2, n)); CK(dalloc(&i1, n)); CK(dalloc(&i2, n));
+  CK(dalloc(&hist, 256ull * blocks + 1));
+  unsigned int* tiles = nullptr;
+  CK(dalloc(&tiles, (256ull * blocks) / kScanTile + 2));
+  unsigned long long* hl = nullptr;
+  const unsigned long long hlen = 256ull * blocks;
+  CK(dalloc(&hl, 1));
+  CK(cudaMemcpyAsync(hl, &hlen, 8, cudaMemcpyHostToDevice, c->stream));
+  k_sort_keys<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
+  ++c->launches;
+  unsigned int maxdim = std::max(h.dims[0], std::max(h.dims[1], h.dims[2]));
+  int axis_bits = 0;
+  while ((1u << axis_bits) < maxdim) ++axis_bits;
+  const int code_bits = (h.dims[2] == 1 ? 2 : 3) * axis_bits;
+  // composite key (morton << 32 | ~idx): 8-bit LSD passes over its used bits
+  for (int shift = 0; shift < 32 + code_bits; shift += 8) {
+    k_radix_hist<<<blocks, kThreads, 0, c->stream>>>(k1, i1, n, shift, hist, chunk);
+    launch_scan<unsigned int>(c, hist, hl, hlen, tiles, nullptr);
+    k_radix_scatter<<<blocks, kThreads, 0, c->stream>>>(k1, i1, k2, i2, n, shift, hist, chunk);
+    c->launches += 2;
+    std::swap(k1, k2);
+    std::swap(i1, i2);
+  }
+  const int nxt = c->cur ^ 1;
+  k_gather<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, n, c->cap, 1, 1);
+  ++c->launches;
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(k1); cudaFree(k2); cudaFree(i1); cudaFree(i2); cudaFree(hist); cudaFree(tiles); cudaFree(hl);
+  c->cur = nxt;
+  c->pos_in_new = false;
+  c->grid_valid = false;
+  return ABS_OK;
+}
+
+int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (r == 0) return ABS_OK;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  const unsigned long long n = h.n;
+  if (r > n) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "more removals than agents");
+  Soa& S = c->S[c->cur];
+  // uid -> slot, then the slot list in the given order
+  std::vector<unsigned long long> hu(n);
+  CK(cudaMemcpy(hu.data(), S.uid, n * 8, cudaMemcpyDeviceToHost));
+  std::vector<long long> slot_of(h.uid_count + 1, -1);
+  for (unsigned long long i = 0; i < n; ++i) slot_of[hu[i]] = (long long)i;
+  std::vector<unsigned long long> slots(r);
+  std::vector<char> seen(n, 0);
+  for (unsigned long long k = 0; k < r; ++k) {
+    if (uids[k] >= slot_of.size() || slot_of[uids[k]] < 0)
+      return set_err(c, ABS_ERR_INVALID_ARGUMENT, "unknown uid");
+    slots[k] = (unsigned long long)slot_of[uids[k]];
+    if (seen[slots[k]]) return set_err(c, ABS_ERR_STATE, "agent staged for removal twice");
+    seen[slots[k]] = 1;
+  }
+  const unsigned long long new_size = n - r;
+  unsigned long long *dslots, *len;
+  unsigned int *to_right, *tail_alive, *hole_at, *tiles;
+  CK(dalloc(&dslots, r)); CK(dalloc(&len, 1));
+  CK(dalloc(&to_right, r + 1)); CK(dalloc(&tail_alive, r + 1)); CK(dalloc(&hole_at, r + 1));
+  CK(dalloc(&tiles, r / kScanTile + 2));
+  unsigned int* to_right_scan = nullptr;
+  unsigned int* tail_scan = nullptr;
+  CK(dalloc(&to_right_scan, r + 1)); CK(dalloc(&tail_scan, r + 1));
+  CK(cudaMemcpyAsync(dslots, slots.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(len, &r, 8, cudaMemcpyHostToDevice, c->stream));
+  const int nb = grid_blocks(c, r);
+  k_set_u32<<<nb, kThreads, 0, c->stream>>>(to_right, r + 1, 0u);
+  k_set_u32<<<nb, kThreads, 0, c->stream>>>(tail_alive, r + 1, 1u);
+  k_remove_plan<<<nb, kThreads, 0, c->stream>>>(dslots, r, new_size, to_right, tail_alive);
+  CK(cudaMemcpyAsync(to_right_scan, to_right, (r + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(tail_scan, tail_alive, (r + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
+  launch_scan<unsigned int>(c, to_right_scan, len, r, tiles, nullptr);
+  launch_scan<unsigned int>(c, tail_scan, len, r, tiles, nullptr);
+  Pd* pos = cur_pos(c);
+  k_remove_move<<<nb, kThreads, 0, c->stream>>>(pos, pos, S, dslots, r, new_size, to_right_scan, to_right, tail_scan,
+                                                tail_alive, hole_at, c->cap, 0);
+  k_remove_move<<<nb, kThreads, 0, c->stream>>>(pos, pos, S, dslots, r, new_size, to_right_scan, to_right, tail_scan,
+                                                tail_alive, hole_at, c->cap, 1);
+  c->launches += 5;
+  h.n = new_size;
+  h.removed += r;
+  CK(cudaMemcpyAsync(&c->g->n, &h.n, 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(&c->g->removed, &h.removed, 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(dslots); cudaFree(len); cudaFree(to_right); cudaFree(tail_alive); cudaFree(hole_at);
+  cudaFree(tiles); cudaFree(to_right_scan); cudaFree(tail_scan);
+  if (c->grid_valid) {
+    CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+    c->grid_valid = false;
+  }
+  c->n = new_size;
+  return ABS_OK;
+}
+
+void* abs_gpu_stream(abs_gpu_ctx* c) { return c ? c->stream : nullptr; }
+
+int abs_gpu_set_stream(abs_gpu_ctx* c, void* stream) {
+  if (!c || !stream) return ABS_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->own_stream = false;
+  return ABS_OK;
+}
+
+int abs_gpu_force_kernel_time(abs_gpu_ctx* c, double* total_ms, uint64_t* launches) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t q = 0; q + 1 < c->ev_used; q += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev[q], c->ev[q + 1]));
+    c->force_ms += ms;
+    ++c->force_launches;
+  }
+  c->ev_used = 0;
+  if (total_ms) *total_ms = c->force_ms;
+  if (launches) *launches = c->force_launches;
+  return ABS_OK;
+}
+
+int abs_gpu_reset_timers(abs_gpu_ctx* c, int enable) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(c->stream));
+  c->ev_used = 0;
+  c->force_ms = 0.0;
+  c->force_launches = 0;
+  c->timing = enable != 0;
+  return ABS_OK;
+}
+
+}  // extern "C"

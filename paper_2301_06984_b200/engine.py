@@ -1,0 +1,268 @@
+"""Reference-shaped host API over the B200 engine (include/absim_gpu.h).
+
+Mirrors the reference's public surface for the hot path so call sites read
+like the reference's own tests:
+
+* ``SimulationParams``  — params.hpp:17-52 (hot-path fields + device knobs)
+* ``Simulation``        — simulation.hpp:89-123: ``add_agents`` (batched
+  ``add_agent``), ``simulate(iterations)``, ``report()``, ``environment()``,
+  ``iteration``; failures raise like the reference (ValueError for
+  std::invalid_argument, AbsimError(RuntimeError) for runtime/logic errors).
+* ``UniformGrid``       — the Environment contract (environment.hpp:36-51):
+  ``update()``, ``largest_agent_diameter()``, ``max_query_radius()``,
+  ``name()``, plus UniformGrid's ``box_length/origin/dims/box_index_of``
+  (uniform_grid.hpp:40-57), batched: ``cell_ids()`` and ``neighbors()``.
+* ``SimulationReport``  — report.hpp:18-41 counters.
+
+All compute runs in the sm_100a kernels of libabsim_gpu.so; there is no CPU
+path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+
+
+@dataclass
+class SimulationParams:
+    seed: int = 42
+    simulation_time_step: float = 0.1
+    repulsion_coefficient: float = 2.0
+    max_displacement: float = 3.0
+    force_threshold: float = 0.0
+    fixed_box_length: float = 0.0
+    sorting_frequency: int = 0
+    detect_static_agents: bool = False
+    # device-side behaviour model (ABS_MODEL_*) and its parameters
+    model: int = N.MODEL_NONE
+    model_params: list = field(default_factory=lambda: [0.0] * 8)
+    capacity: int = 0
+    record_forces: bool = True
+    bins_per_box: int = 0
+
+    def validate(self):
+        """SimulationParams::validate (params.cpp:44-72), hot-path subset."""
+        if self.fixed_box_length < 0.0:
+            raise ValueError("fixed_box_length must be >= 0")
+        if not self.simulation_time_step > 0.0:
+            raise ValueError("simulation_time_step must be > 0")
+        if self.repulsion_coefficient < 0.0:
+            raise ValueError("repulsion_coefficient must be >= 0")
+        if not self.max_displacement > 0.0:
+            raise ValueError("max_displacement must be > 0")
+        if self.force_threshold < 0.0:
+            raise ValueError("force_threshold must be >= 0")
+
+    def to_c(self) -> N.Config:
+        c = N.Config()
+        N.load().abs_gpu_default_config(C.byref(c))
+        c.seed = self.seed
+        c.simulation_time_step = self.simulation_time_step
+        c.repulsion_coefficient = self.repulsion_coefficient
+        c.max_displacement = self.max_displacement
+        c.force_threshold = self.force_threshold
+        c.fixed_box_length = self.fixed_box_length
+        c.sorting_frequency = self.sorting_frequency
+        c.detect_static_agents = 1 if self.detect_static_agents else 0
+        c.model = self.model
+        mp = list(self.model_params) + [0.0] * (8 - len(self.model_params))
+        for i in range(8):
+            c.model_params[i] = float(mp[i])
+        c.capacity = self.capacity
+        c.record_forces = 1 if self.record_forces else 0
+        c.bins_per_box = self.bins_per_box
+        return c
+
+
+@dataclass
+class SimulationReport:
+    iterations: int = 0
+    final_agent_count: int = 0
+    uid_count: int = 0
+    force_evaluations: int = 0
+    force_skips: int = 0
+    agents_added: int = 0
+    agents_removed: int = 0
+    kernel_launches: int = 0
+
+
+def _p(a, ct):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ct))
+
+
+class UniformGrid:
+    """Environment contract over the device grid (uniform_grid.hpp:26-94)."""
+
+    def __init__(self, sim: "Simulation"):
+        self._sim = sim
+
+    def name(self) -> str:
+        return "uniform_grid"
+
+    def update(self) -> None:
+        N.check(N.load().abs_gpu_env_update(self._sim._ctx), self._sim._ctx)
+
+    def _info(self):
+        g = np.zeros(5)
+        dims = np.zeros(3, np.uint32)
+        N.check(N.load().abs_gpu_grid_info(self._sim._ctx, _p(g, C.c_double), _p(dims, C.c_uint32)),
+                self._sim._ctx)
+        return g, dims
+
+    def largest_agent_diameter(self) -> float:
+        return float(self._info()[0][4])
+
+    def box_length(self) -> float:
+        return float(self._info()[0][3])
+
+    def max_query_radius(self) -> float:
+        return self.box_length()
+
+    def origin(self) -> np.ndarray:
+        return self._info()[0][:3].copy()
+
+    def dims(self) -> np.ndarray:
+        return self._info()[1].copy()
+
+    def cell_ids(self) -> np.ndarray:
+        """box_index_of for every agent, in device storage order."""
+        n = self._sim.agent_count()
+        out = np.zeros(n, np.uint64)
+        N.check(N.load().abs_gpu_cell_ids(self._sim._ctx, _p(out, C.c_uint64)), self._sim._ctx)
+        return out
+
+    def neighbors(self):
+        """CSR (offsets[n+1], uids) of sorted neighbour uids within the force
+        query radius 0.5 (d + dmax) (simulation.cpp:469), storage order."""
+        lib, ctx = N.load(), self._sim._ctx
+        n = self._sim.agent_count()
+        offsets = np.zeros(n + 1, np.uint64)
+        total = C.c_uint64(0)
+        N.check(lib.abs_gpu_neighbors(ctx, _p(offsets, C.c_uint64), None, 0, C.byref(total)), ctx)
+        uids = np.zeros(max(1, total.value), np.uint64)
+        N.check(lib.abs_gpu_neighbors(ctx, _p(offsets, C.c_uint64), _p(uids, C.c_uint64),
+                                      total.value, C.byref(total)), ctx)
+        return offsets, uids[: total.value]
+
+
+class Simulation:
+    """Simulation-shaped front end (simulation.hpp:89-123) on one B200."""
+
+    def __init__(self, params: SimulationParams | None = None, device: int = 0):
+        self.params = params or SimulationParams()
+        self.params.validate()
+        lib = N.load()
+        self._cfg = self.params.to_c()
+        ctx = C.c_void_p()
+        N.check(lib.abs_gpu_create(C.byref(self._cfg), device, C.byref(ctx)), None)
+        self._ctx = ctx
+        self._env = UniformGrid(self)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            N.load().abs_gpu_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- population ------------------------------------------------------
+    def add_agents(self, x, y, z, d, behaviour_mask=None, uid=None, volume=None, flags=None,
+                   partners=None, uid_count: int = 0):
+        """Batched Simulation::add_agent: replaces the population (uids
+        0..n-1 in array order unless given)."""
+        x, y, z, d = (np.ascontiguousarray(a, np.float64) for a in (x, y, z, d))
+        m = None if behaviour_mask is None else np.ascontiguousarray(behaviour_mask, np.uint8)
+        u = None if uid is None else np.ascontiguousarray(uid, np.uint64)
+        v = None if volume is None else np.ascontiguousarray(volume, np.float64)
+        f = None if flags is None else np.ascontiguousarray(flags, np.uint8)
+        pa = None if partners is None else np.ascontiguousarray(partners, np.uint32)
+        N.check(N.load().abs_gpu_upload(self._ctx, len(x), _p(u, C.c_uint64), _p(x, C.c_double),
+                                        _p(y, C.c_double), _p(z, C.c_double), _p(d, C.c_double),
+                                        _p(m, C.c_uint8), _p(v, C.c_double), _p(f, C.c_uint8),
+                                        _p(pa, C.c_uint32), uid_count), self._ctx)
+
+    def add_agents_device(self, x_ptr, y_ptr, z_ptr, d_ptr, n, uid_ptr=None, mask_ptr=None):
+        """Population from device-resident arrays (e.g. torch CUDA tensors)."""
+        N.check(N.load().abs_gpu_upload_device(self._ctx, n, uid_ptr, x_ptr, y_ptr, z_ptr, d_ptr,
+                                               mask_ptr, n), self._ctx)
+
+    def remove_agents(self, uids):
+        u = np.ascontiguousarray(uids, np.uint64)
+        N.check(N.load().abs_gpu_remove(self._ctx, _p(u, C.c_uint64), len(u)), self._ctx)
+
+    # -- schedule --------------------------------------------------------
+    def simulate(self, iterations: int) -> None:
+        N.check(N.load().abs_gpu_simulate(self._ctx, iterations), self._ctx)
+
+    def set_iteration(self, iteration: int) -> None:
+        N.check(N.load().abs_gpu_set_iteration(self._ctx, iteration), self._ctx)
+
+    def synchronize(self):
+        N.check(N.load().abs_gpu_synchronize(self._ctx), self._ctx)
+
+    def sort(self):
+        """sort_and_balance (sort_balance.cpp:22-148) on the current storage."""
+        N.check(N.load().abs_gpu_sort(self._ctx), self._ctx)
+
+    def environment(self) -> UniformGrid:
+        return self._env
+
+    def _stats(self) -> N.Stats:
+        s = N.Stats()
+        N.check(N.load().abs_gpu_stats(self._ctx, C.byref(s)), self._ctx)
+        return s
+
+    @property
+    def iteration(self) -> int:
+        return int(self._stats().iterations)
+
+    def agent_count(self) -> int:
+        return int(self._stats().agents)
+
+    def report(self) -> SimulationReport:
+        s = self._stats()
+        return SimulationReport(iterations=s.iterations, final_agent_count=s.agents,
+                                uid_count=s.uid_count, force_evaluations=s.force_evaluations,
+                                force_skips=s.force_skips, agents_added=s.agents_added,
+                                agents_removed=s.agents_removed, kernel_launches=s.kernel_launches)
+
+    def agents(self) -> dict:
+        """Download the population (device storage order)."""
+        n = self.agent_count()
+        out = {"uid": np.zeros(n, np.uint64), "x": np.zeros(n), "y": np.zeros(n), "z": np.zeros(n),
+               "d": np.zeros(n), "fx": np.zeros(n), "fy": np.zeros(n), "fz": np.zeros(n),
+               "partners": np.zeros(n, np.uint32), "flags": np.zeros(n, np.uint8),
+               "volume": np.zeros(n)}
+        nn = C.c_uint64(0)
+        N.check(N.load().abs_gpu_download(
+            self._ctx, C.byref(nn), _p(out["uid"], C.c_uint64),
+            *(_p(out[k], C.c_double) for k in ("x", "y", "z", "d", "fx", "fy", "fz")),
+            _p(out["partners"], C.c_uint32), _p(out["flags"], C.c_uint8),
+            _p(out["volume"], C.c_double)), self._ctx)
+        return out
+
+    # -- timing of the dominant kernel --------------------------------------
+    def reset_timers(self, enable: bool = True):
+        N.check(N.load().abs_gpu_reset_timers(self._ctx, 1 if enable else 0), self._ctx)
+
+    def force_kernel_time(self):
+        ms = C.c_double(0)
+        launches = C.c_uint64(0)
+        N.check(N.load().abs_gpu_force_kernel_time(self._ctx, C.byref(ms), C.byref(launches)),
+                self._ctx)
+        return ms.value, launches.value
+
+    @property
+    def stream(self) -> int:
+        return N.load().abs_gpu_stream(self._ctx) or 0

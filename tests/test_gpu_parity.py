@@ -1,0 +1,354 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on
+identical seeded inputs.
+
+Bars: bit-exact for grid params, cell ids, neighbour sets
+(sorted uid lists), static flags, partners and agent counts; fp64 positions
+within |g-o| <= 1e-9 max(|o|, 1) and forces within 1e-9 max(|o|, k) per
+component. Integer outputs are also checked teacher-forced (both sides fed
+the oracle's step-t state) so a 1-ulp drift in free-running positions cannot
+flip a floor() or <= decision.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from _util import assert_close, by_uid
+from paper_2301_06984_b200 import configs as CF
+
+pytestmark = pytest.mark.gpu
+
+K = 2.0
+
+
+def _oparams(O, prm, **kw):
+    p = O.OracleParams(seed=prm.get("seed", 42), dt=prm.get("simulation_time_step", 0.1),
+                       detect_static=prm.get("detect_static_agents", False),
+                       model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
+                       sorting_frequency=prm.get("sorting_frequency", 0),
+                       threshold=prm.get("force_threshold", 0.0),
+                       fixed_box=prm.get("fixed_box_length", 0.0))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def _gpu(E, prm, wl=None, bins=1, **kw):
+    p = E.SimulationParams(**{**prm, **kw})
+    p.bins_per_box = bins
+    sim = E.Simulation(p)
+    if wl is not None:
+        sim.add_agents(wl.x, wl.y, wl.z, wl.d, behaviour_mask=wl.mask)
+    return sim
+
+
+def compare_state(g, o, ints=True, what=""):
+    g, o = by_uid(g), by_uid(o)
+    assert np.array_equal(g["uid"], o["uid"]), f"{what}: uid sets differ"
+    for k in ("x", "y", "z", "d", "volume"):
+        assert_close(g[k], o[k], 1e-9, 1.0, f"{what} {k}")
+    for k in ("fx", "fy", "fz"):
+        assert_close(g[k], o[k], 1e-9, K, f"{what} {k}")
+    if ints:
+        assert np.array_equal(g["partners"], o["partners"]), f"{what}: partners"
+        assert np.array_equal(g["flags"], o["flags"]), f"{what}: flags"
+
+
+def compare_env(sim, orc, what=""):
+    env = sim.environment()
+    env.update()
+    og = orc.env_update()
+    assert np.array_equal(env.origin(), og["origin"]), what
+    assert env.box_length() == og["box"] and env.largest_agent_diameter() == og["dmax"], what
+    assert np.array_equal(env.dims(), og["dims"]), what
+    ga = sim.agents()
+    gid = dict(zip(ga["uid"].tolist(), env.cell_ids().tolist()))
+    od = orc.dump()
+    oid = dict(zip(od["uid"].tolist(), orc.cell_ids().tolist()))
+    assert gid == oid, f"{what}: cell ids"
+    go, gu = env.neighbors()
+    oo, ou = orc.neighbors()
+    gn = {int(u): tuple(gu[go[i]:go[i + 1]].tolist()) for i, u in enumerate(ga["uid"])}
+    on = {int(u): tuple(ou[oo[i]:oo[i + 1]].tolist()) for i, u in enumerate(od["uid"])}
+    assert gn == on, f"{what}: neighbour sets"
+
+
+def teacher_force(sim, orc, mask_by_uid=None):
+    """Upload the oracle's current state into the GPU context."""
+    o = orc.dump()
+    c = orc.counts()
+    m = None if mask_by_uid is None else mask_by_uid(o["uid"])
+    sim.add_agents(o["x"], o["y"], o["z"], o["d"], behaviour_mask=m, uid=o["uid"], volume=o["volume"],
+                   flags=o["flags"], partners=o["partners"], uid_count=c["uid_count"])
+    sim.set_iteration(c["iterations"])
+
+
+# ---------------------------------------------------------------- configs
+@pytest.mark.parametrize("bins", [1, 2])
+def test_c1_free_running(engine, oracle_mod, bins):
+    wl = CF.c1_relaxation(4096, seed=0)
+    sim = _gpu(engine, wl.params, wl, bins)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    compare_env(sim, orc, "c1 t=0")
+    for step in range(3):
+        sim.simulate(4)
+        orc.simulate(4)
+        compare_state(sim.agents(), orc.dump(), what=f"c1 after {4 * (step + 1)}")
+        r, c = sim.report(), orc.counts()
+        assert r.force_evaluations == c["force_evaluations"]
+        assert r.final_agent_count == c["agents"]
+
+
+def test_c1_teacher_forced_integers(engine, oracle_mod):
+    wl = CF.c1_relaxation(3000, seed=5)
+    sim = _gpu(engine, wl.params, wl, 2)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    for step in range(8):
+        teacher_force(sim, orc)
+        compare_env(sim, orc, f"c1 tf step {step}")
+        e0 = orc.counts()["force_evaluations"]
+        sim.simulate(1)
+        orc.simulate(1)
+        compare_state(sim.agents(), orc.dump(), what=f"c1 tf step {step}")
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"] - e0
+
+
+def test_c2_proliferation(engine, oracle_mod):
+    wl = CF.c2_proliferation(side=4, seed=0)
+    sim = _gpu(engine, wl.params, wl, 1)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    for chunk in range(6):
+        sim.simulate(10)
+        orc.simulate(10)
+        r, c = sim.report(), orc.counts()
+        assert r.final_agent_count == c["agents"] and r.uid_count == c["uid_count"]
+        assert r.agents_added == c["agents_added"]
+        compare_state(sim.agents(), orc.dump(), what=f"c2 after {10 * (chunk + 1)}")
+    assert sim.report().final_agent_count == 64 * 4  # two synchronous doublings by step 60
+
+
+def test_c3_static_spheroid(engine, oracle_mod):
+    wl = CF.c3_spheroid(4000, seed=0)
+    sim = _gpu(engine, wl.params, wl, 1)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d, wl.mask)
+    for chunk in range(3):
+        sim.simulate(3)
+        orc.simulate(3)
+        r, c = sim.report(), orc.counts()
+        assert (r.force_evaluations, r.force_skips) == (c["force_evaluations"], c["force_skips"])
+        compare_state(sim.agents(), orc.dump(), what=f"c3 after {3 * (chunk + 1)}")
+    static = (sim.agents()["flags"] & 1).mean()
+    assert static > 0.85
+
+
+def test_c4_shape_small(engine, oracle_mod):
+    wl = CF.c4_large_uniform(6000, seed=3)
+    sim = _gpu(engine, wl.params, wl, 2)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    compare_env(sim, orc, "c4 t=0")
+    sim.simulate(12)
+    orc.simulate(12)
+    compare_state(sim.agents(), orc.dump(), what="c4 after 12")
+    assert sim.report().force_evaluations == orc.counts()["force_evaluations"]
+
+
+def test_against_reference_engine(engine, oracle_mod, have_ref):
+    """The GPU against the unmodified reference (not only the C port)."""
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    wl = CF.c1_relaxation(2048, seed=9)
+    sim = _gpu(engine, wl.params, wl, 1)
+    ref = oracle_mod.RefSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    compare_env(sim, ref, "ref t=0")
+    sim.simulate(5)
+    ref.simulate(5)
+    compare_state(sim.agents(), ref.dump(), what="vs reference")
+
+
+# ---------------------------------------------------------------- known answers
+def _lattice(s, spacing):
+    pts = [(x * spacing, y * spacing, z * spacing) for x in range(s) for y in range(s) for z in range(s)]
+    return [np.array(v, dtype=float) for v in zip(*pts)]
+
+
+def test_static_lattice_known_answer(engine):
+    """test_scheduler.cpp:464-488."""
+    x, y, z = _lattice(3, 10.0)
+    sim = engine.Simulation(engine.SimulationParams(detect_static_agents=True))
+    sim.add_agents(x, y, z, np.full(27, 10.0))
+    sim.simulate(1)
+    r = sim.report()
+    assert (r.force_evaluations, r.force_skips) == (108, 0)
+    sim.simulate(1)
+    r = sim.report()
+    assert (r.force_evaluations, r.force_skips) == (108, 27)
+    sim.simulate(1)
+    assert sim.report().force_skips == 54
+    assert (sim.agents()["flags"] & 1).sum() == 27
+
+
+def test_cancelling_triple_known_answer(engine):
+    """test_scheduler.cpp:490-519."""
+    sim = engine.Simulation(engine.SimulationParams(detect_static_agents=True, force_threshold=10.0))
+    sim.add_agents([0.0, 10.0, 20.0], [0.0] * 3, [0.0] * 3, [12.0] * 3)
+    sim.simulate(1)
+    assert (sim.report().force_evaluations, sim.report().force_skips) == (4, 0)
+    sim.simulate(2)
+    assert (sim.report().force_evaluations, sim.report().force_skips) == (8, 4)
+    a = by_uid(sim.agents())
+    assert [int(u) for u, f in zip(a["uid"], a["flags"]) if f & 1] == [0, 2]
+    assert list(a["x"]) == [0.0, 10.0, 20.0]
+
+
+def test_static_front_known_answer(engine):
+    """test_scheduler.cpp:521-534 (reference Grow behaviour on one column)."""
+    x, y, z = _lattice(3, 10.0)
+    mask = np.array([1 if (i // 9 == 0 and (i // 3) % 3 == 1) else 0 for i in range(27)], np.uint8)
+    sim = engine.Simulation(engine.SimulationParams(detect_static_agents=True, model=engine.MODEL_GROW,
+                                                    model_params=[0.5, 20.0]))
+    sim.add_agents(x, y, z, np.full(27, 10.0), behaviour_mask=mask)
+    sim.simulate(3)
+    a = by_uid(sim.agents())
+    assert [int(u) for u, f in zip(a["uid"], a["flags"]) if f & 1] == [18, 19, 20, 24, 25, 26]
+
+
+def test_static_on_off_same_trajectory(engine):
+    """test_scheduler.cpp:536-558: static skipping does not change positions."""
+    x, y, z = _lattice(3, 10.0)
+    mask = np.array([1 if (i // 9 == 0 and (i // 3) % 3 == 1) else 0 for i in range(27)], np.uint8)
+    out = []
+    for detect in (True, False):
+        sim = engine.Simulation(engine.SimulationParams(detect_static_agents=detect,
+                                                        model=engine.MODEL_GROW, model_params=[0.5, 20.0]))
+        sim.add_agents(x, y, z, np.full(27, 10.0), behaviour_mask=mask)
+        sim.simulate(6)
+        out.append((by_uid(sim.agents()), sim.report()))
+    (a, ra), (b, rb) = out
+    for k in "xyz":
+        assert np.max(np.abs(a[k] - b[k])) <= 1e-12
+    assert ra.force_skips > 0 and rb.force_skips == 0
+    assert ra.force_evaluations < rb.force_evaluations
+
+
+def test_grid_known_answers(engine):
+    """test_grid.cpp:163-181 floor/clamp; :203-215 inclusive radius; :309-322 box = dmax."""
+    sim = engine.Simulation(engine.SimulationParams(fixed_box_length=20.0))
+    sim.add_agents([0.0, 100.0, 19.999, 100.0], [0.0, 100.0, 20.0, 100.0], [0.0, 100.0, 39.9, 100.0],
+                   [10.0] * 4)
+    env = sim.environment()
+    env.update()
+    assert list(env.dims()) == [6, 6, 6] and list(env.origin()) == [0, 0, 0]
+    ids = dict(zip(sim.agents()["uid"].tolist(), env.cell_ids().tolist()))
+    assert ids[2] == 0 + 6 * (1 + 6 * 1) and ids[3] == 215 and ids[1] == 215
+    sim2 = engine.Simulation(engine.SimulationParams())
+    sim2.add_agents([0.0, 15.0], [0.0, 0.0], [0.0, 0.0], [15.0, 15.0])
+    sim2.environment().update()
+    off, u = sim2.environment().neighbors()  # r = 0.5 (15 + 15) = 15 = separation
+    assert list(off) == [0, 1, 2] and sorted(u.tolist()) == [0, 1]
+    sim3 = engine.Simulation(engine.SimulationParams())
+    sim3.add_agents([0.0, 40.0], [0.0, 0.0], [0.0, 0.0], [8.0, 17.5])
+    sim3.environment().update()
+    assert sim3.environment().box_length() == 17.5 == sim3.environment().largest_agent_diameter()
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_population(engine):
+    sim = engine.Simulation(engine.SimulationParams(detect_static_agents=True))
+    sim.simulate(10)
+    r = sim.report()
+    assert r.iterations == 10 and r.final_agent_count == 0 and r.force_evaluations == 0
+    sim.environment().update()
+    assert list(sim.environment().dims()) == [1, 1, 1]
+    sim.simulate(0)
+    assert sim.report().iterations == 10
+
+
+def test_single_agent_and_degenerate_volume(engine):
+    sim = engine.Simulation(engine.SimulationParams())
+    sim.add_agents([5.0], [5.0], [5.0], [10.0])
+    sim.simulate(2)
+    assert sim.report().force_evaluations == 0
+    a = sim.agents()
+    assert (a["x"][0], a["y"][0], a["z"][0]) == (5.0, 5.0, 5.0)
+    # three coincident agents (test_grid.cpp:183-194) and the coincident-centre
+    # force of magnitude k * overlap (test_mechanics.cpp:55-72)
+    sim = engine.Simulation(engine.SimulationParams(simulation_time_step=0.01))
+    sim.add_agents([3.0] * 3, [3.0] * 3, [3.0] * 3, [10.0] * 3)
+    env = sim.environment()
+    env.update()
+    off, u = env.neighbors()
+    assert list(np.diff(off)) == [2, 2, 2]
+    sim.simulate(1)
+    a = sim.agents()
+    for i in range(3):
+        f = math.sqrt(a["fx"][i] ** 2 + a["fy"][i] ** 2 + a["fz"][i] ** 2)
+        assert f > 0.0
+    sim2 = engine.Simulation(engine.SimulationParams())
+    sim2.add_agents([5.0, 5.0], [5.0, 5.0], [5.0, 5.0], [10.0, 10.0])
+    sim2.simulate(1)
+    b = by_uid(sim2.agents())
+    f0 = np.array([b["fx"][0], b["fy"][0], b["fz"][0]])
+    f1 = np.array([b["fx"][1], b["fy"][1], b["fz"][1]])
+    assert abs(np.linalg.norm(f0) - 20.0) < 1e-12 and np.array_equal(f0, -f1)
+
+
+def test_errors(engine):
+    with pytest.raises(ValueError):
+        engine.Simulation(engine.SimulationParams(simulation_time_step=0.0))
+    sim = engine.Simulation(engine.SimulationParams(fixed_box_length=5.0))
+    sim.add_agents([0.0, 1.0], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0])
+    with pytest.raises(engine.AbsimError, match="fixed box"):
+        sim.simulate(1)
+    sim = engine.Simulation(engine.SimulationParams())
+    sim.add_agents([0.0, math.inf], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0])
+    with pytest.raises(engine.AbsimError, match="not finite"):
+        sim.simulate(1)
+    sim = engine.Simulation(engine.SimulationParams())
+    with pytest.raises(ValueError, match="diameter"):
+        sim.add_agents([0.0], [0.0], [0.0], [0.0])
+
+
+def test_sort_matches_reference_order(engine, oracle_mod, have_ref):
+    """sort_and_balance order (sort_balance.cpp:88-128) from a storage order
+    equal to the reference's (fresh upload)."""
+    wl = CF.c1_relaxation(3000, seed=4)
+    sim = _gpu(engine, wl.params, wl, 1)
+    sim.sort()
+    got = sim.agents()["uid"]
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+    orc.env_update()
+    orc.sort()
+    assert np.array_equal(got, orc.dump()["uid"])
+    if have_ref:
+        ref = oracle_mod.RefSim(_oparams(oracle_mod, wl.params), wl.x, wl.y, wl.z, wl.d)
+        ref.sort()
+        assert np.array_equal(got, ref.dump()["uid"])
+
+
+def test_removal_worked_example(engine):
+    """test_commit.cpp:99-119 on a freshly uploaded (reference-ordered) store."""
+    sim = engine.Simulation(engine.SimulationParams())
+    sim.add_agents(np.arange(7, dtype=float) * 20, np.zeros(7), np.zeros(7), np.ones(7))
+    sim.remove_agents([1, 4, 6])
+    assert list(sim.agents()["uid"]) == [0, 5, 2, 3]
+    assert sim.report().agents_removed == 3
+    with pytest.raises(engine.AbsimError):
+        sim.remove_agents([1])  # no longer alive
+    sim.simulate(2)
+    assert sim.report().final_agent_count == 4
+
+
+def test_grid_growth_retry(engine, oracle_mod):
+    """Agents spreading far beyond the initial grid force a bin-table regrow
+    (device-side retry) without changing results."""
+    rng = np.random.default_rng(3)
+    n = 400
+    x, y, z = rng.uniform(0, 30, (3, n))
+    d = np.full(n, 10.0)
+    prm = dict(simulation_time_step=1.0, max_displacement=3.0)
+    sim = engine.Simulation(engine.SimulationParams(**prm))
+    sim.add_agents(x, y, z, d)
+    orc = oracle_mod.PortSim(oracle_mod.OracleParams(dt=1.0), x, y, z, d)
+    sim.simulate(60)
+    orc.simulate(60)
+    compare_state(sim.agents(), orc.dump(), ints=False, what="spreading")
