@@ -79,7 +79,8 @@ typedef struct {
   double model_params[8];
   uint64_t capacity;             /* agent capacity hint; grows on demand */
   int32_t record_forces;         /* keep Agent::last_force (parity); 0 skips the 24 B/agent write */
-  int32_t bins_per_box;          /* internal sub-bins per box edge: 0 auto, 1, 2 */
+  int32_t bins_per_box;          /* internal sub-bins per box edge along y and z: 0 auto, 1..4 */
+  int32_t bins_per_box_x;        /* internal sub-bins per box edge along x: 0 auto, 1..4 */
 } abs_gpu_config;
 
 /* SimulationReport counters (report.hpp:32-40) */
@@ -136,7 +137,8 @@ int abs_gpu_grid_info(abs_gpu_ctx* ctx, double* grid, uint32_t* dims);
 int abs_gpu_cell_ids(abs_gpu_ctx* ctx, uint64_t* out);
 /* CSR of sorted neighbour uids per agent (download order) within the force
  * query radius; offsets has n+1 entries. *total receives the number of uids;
- * returns ABS_ERR_CAPACITY (and the needed total) when cap is too small. */
+ * uids == NULL only sizes the result; returns ABS_ERR_CAPACITY (and the
+ * needed total) when cap is too small. */
 int abs_gpu_neighbors(abs_gpu_ctx* ctx, uint64_t* offsets, uint64_t* uids, uint64_t cap,
                       uint64_t* total);
 /* Reorder storage into sort_and_balance order: boxes by Morton rank, agents in

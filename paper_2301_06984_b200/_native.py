@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libabsim_gpu.so")
+LIB_PATH = os.environ.get("ABSIM_GPU_LIB") or os.path.join(HERE, "_lib", "libabsim_gpu.so")
 
 ABS_OK = 0
 ABS_ERR_INVALID_ARGUMENT = 1
@@ -49,6 +49,7 @@ class Config(C.Structure):
         ("capacity", C.c_uint64),
         ("record_forces", C.c_int32),
         ("bins_per_box", C.c_int32),
+        ("bins_per_box_x", C.c_int32),
     ]
 
 

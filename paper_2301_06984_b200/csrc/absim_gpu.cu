@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,6 +31,10 @@ using namespace absgpu;
 
 namespace {
 
+#ifndef ABS_FORCE_MIN_BLOCKS
+#define ABS_FORCE_MIN_BLOCKS 2
+#endif
+constexpr int kForceMinBlocks = ABS_FORCE_MIN_BLOCKS;
 constexpr unsigned long long kInfOrdLo = 0xFFF0000000000000ull;  // ord_enc(+inf)
 constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf)
 constexpr unsigned long long kZeroOrd = 0x8000000000000000ull;   // ord_enc(+0.0)
@@ -100,7 +105,8 @@ __device__ void reset_reduction(DevGrid* g) {
 }
 
 // uniform_grid.cpp:155-237 sizing; one thread.
-__global__ void k_finalize(DevGrid* g, double fixed_box, int bins_cfg, unsigned long long bins_cap,
+__global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, unsigned int bins_yz,
+                           unsigned long long bins_cap,
                            unsigned long long capacity, unsigned long long uid_cap, int may_add,
                            unsigned long long iteration) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -147,19 +153,21 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, int bins_cfg, unsigned 
     }
   }
   if (err == kErrNone) {
-    unsigned int B = bins_cfg == 2 ? 2u : 1u;
+    unsigned int B[3] = {bins_x, bins_yz, bins_yz};
     const unsigned long long boxes = (unsigned long long)g->dims[0] * g->dims[1] * g->dims[2];
-    if (boxes * B * B * B + 1 > 0xFFFFFFFFull) B = 1;
-    const unsigned long long nbins = boxes * B * B * B;
+    if (boxes * B[0] * B[1] * B[2] + 1 > 0xFFFFFFFFull) B[0] = B[1] = B[2] = 1;
+    const unsigned long long nbins = boxes * B[0] * B[1] * B[2];
     if (nbins + 1 > bins_cap) {
       err = kErrBinsRetry;
       g->needed_bins = nbins + 1;
     } else if (may_add && (2 * n > capacity || g->uid_count + n > uid_cap)) {
       err = kErrCapRetry;
     } else {
-      g->B = B;
-      g->s = B == 1 ? g->box : g->box / static_cast<double>(B);
-      for (int k = 0; k < 3; ++k) g->bd[k] = g->dims[k] * B;
+      for (int k = 0; k < 3; ++k) {
+        g->B[k] = B[k];
+        g->s[k] = B[k] == 1 ? g->box : g->box / static_cast<double>(B[k]);
+        g->bd[k] = g->dims[k] * B[k];
+      }
       g->nbins = nbins;
       double mag = g->box;
       for (int k = 0; k < 3; ++k) {
@@ -351,8 +359,11 @@ __global__ void __launch_bounds__(kThreads) k_mark(Soa S, const DevGrid* g,
                                                    unsigned char* __restrict__ nv,
                                                    unsigned char* __restrict__ nn) {
   if (g->err) return;
-  const DevGrid G = *g;
-  const unsigned long long n = G.n;
+  __shared__ QGrid Q;
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned char f = S.flags[i];
@@ -360,8 +371,8 @@ __global__ void __launch_bounds__(kThreads) k_mark(Soa S, const DevGrid* g,
     const bool fresh = f & ABS_FLAG_NEWLY_ADDED;
     if (!disturbs && !fresh) continue;
     const Pd me = load_pd(S.pd + i);
-    const double r = 0.5 * (me.d + G.dmax);
-    for_each_neighbor(G, S.pd, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r * r,
+    const double r = 0.5 * (me.d + dmax);
+    for_each_neighbor(Q, S.pd, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r * r,
                       [&](unsigned int j, const Pd&, double, double, double, double) {
                         if (disturbs) nv[j] = 1;
                         if (fresh) nn[j] = 1;
@@ -370,185 +381,572 @@ __global__ void __launch_bounds__(kThreads) k_mark(Soa S, const DevGrid* g,
 }
 
 // ------------------------------------------------------------ force step
-// Behaviours, static skip, run_forces and apply_pending for one agent.
-__global__ void __launch_bounds__(kThreads) k_force(Soa S, Pd* __restrict__ out, const DevGrid* gp,
-                                                    DevGrid* gw, const unsigned int* __restrict__ start,
-                                                    unsigned char* __restrict__ nv,
-                                                    unsigned char* __restrict__ nn, StepArgs a,
-                                                    unsigned long long cap,
-                                                    unsigned long long* __restrict__ st_parent,
-                                                    Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-                                                    unsigned int* __restrict__ div_mark) {
-  if (gp->err) return;
-  const DevGrid G = *gp;
-  const unsigned long long n = G.n;
-  const int lane = threadIdx.x & 31;
-  unsigned long long n_eval = 0, n_skip = 0;
-  for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n;
-       base += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long i = base + threadIdx.x;
-    const bool active = i < n;
-    bool divides = false;
-    double dpx = 0, dpy = 0, dpz = 0, dd = 0, dvol = 0;
-    unsigned long long my_uid = 0;
-    if (active) {
-      const Pd me = load_pd(S.pd + i);
-      unsigned char fl = S.flags[i];
-      my_uid = S.uid[i];
-      // --- staticness phase 2 (simulation.cpp:375-384) -----------------
-      if (a.detect_static) {
-        if (a.iteration == 0) {
-          fl = 0;  // :335-349 everyone participates, flags wiped
-        } else {
-          const bool skip = !(fl & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED |
-                                    ABS_FLAG_NEIGHBOR_VIOLATION | ABS_FLAG_NEW_NEIGHBOR)) &&
-                            !nv[i] && !nn[i] && S.partners[i] <= 1u;
-          fl = skip ? ABS_FLAG_STATIC : 0;
-          nv[i] = 0;
-          nn[i] = 0;
-        }
-      }
-      // --- behaviours (run before forces, simulation.cpp:389-394) -------
-      double tx = 0.0, ty = 0.0, tz = 0.0, tg = 0.0;
-      if (a.model != ABS_MODEL_NONE && S.beh[i]) {
-        if (a.model == ABS_MODEL_PROLIFERATION) {
-          double v = S.vol[i] + a.mp[0];
-          if (v > a.mp[1]) {
-            v *= 0.5;
-            double dir[3];
-            abs_unit_vector(a.seed, my_uid, ABS_RNG_DIVISION_BASE(a.iteration), dir);
-            const double half = 0.5 * me.d;
-            dpx = me.x + dir[0] * half;
-            dpy = me.y + dir[1] * half;
-            dpz = me.z + dir[2] * half;
-            dd = abs_diameter_of_volume(v);
-            dvol = v;
-            divides = true;
-          }
-          S.vol[i] = v;
-          tg += abs_diameter_of_volume(v) - me.d;
-        } else if (a.model == ABS_MODEL_DRIVE) {
-          double dl[3];
-          abs_drive_delta(me.x, me.y, me.z, a.mp[0], a.mp[1], a.mp[2], a.mp[3], a.seed, my_uid,
-                          a.iteration, dl);
-          tx += dl[0];
-          ty += dl[1];
-          tz += dl[2];
-        } else if (a.model == ABS_MODEL_GROW) {
-          if (me.d < a.mp[1]) {
-            const double rem = a.mp[1] - me.d;
-            tg += rem < a.mp[0] ? rem : a.mp[0];
-          }
-        }
-      }
-      // --- run_forces (simulation.cpp:463-489) --------------------------
-      if (a.detect_static && (fl & ABS_FLAG_STATIC)) {
-        ++n_skip;
-      } else {
-        const double r = 0.5 * (me.d + G.dmax);
-        double fx = 0.0, fy = 0.0, fz = 0.0;
-        unsigned int contributors = 0, evals = 0;
-        const double k = a.k;
-        for_each_neighbor(
-            G, S.pd, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r * r,
-            [&](unsigned int j, const Pd& q, double dx, double dy, double dz, double d2) {
-              ++evals;
-              // pairwise_repulsion (mechanics.cpp:10-27)
-              const double dist = sqrt(d2);
-              const double overlap = 0.5 * (me.d + q.d) - dist;
-              if (overlap <= 0.0) return;
-              double f0, f1, f2;
-              if (dist > 0.0) {
-                const double sc = k * overlap / dist;
-                f0 = dx * sc;
-                f1 = dy * sc;
-                f2 = dz * sc;
-              } else {
-                const unsigned long long ub = S.uid[j];
-                const unsigned long long lo = my_uid < ub ? my_uid : ub;
-                const unsigned long long hi = my_uid < ub ? ub : my_uid;
-                const double zz = -1.0 + 2.0 * abs_u01(abs_rng_word(lo, hi, 0));
-                const double phi = 2.0 * ABS_PI * abs_u01(abs_rng_word(lo, hi, 1));
-                const double rr = sqrt(fmax(0.0, 1.0 - zz * zz));
-                double d0 = rr * cos(phi), d1 = rr * sin(phi), d2v = zz;
-                if (my_uid != lo) { d0 *= -1.0; d1 *= -1.0; d2v *= -1.0; }
-                const double m = k * overlap;
-                f0 = d0 * m;
-                f1 = d1 * m;
-                f2 = d2v * m;
-              }
-              if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
-                ++contributors;
-                fx += f0;
-                fy += f1;
-                fz += f2;
-              }
-            });
-        n_eval += evals;
-        if (a.record_forces) {
-          S.force[i] = fx;
-          S.force[cap + i] = fy;
-          S.force[2 * cap + i] = fz;
-        }
-        S.partners[i] = contributors;
-        if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
-          tx += fx * a.dt;
-          ty += fy * a.dt;
-          tz += fz * a.dt;
-        }
-      }
-      // --- apply_pending (agent.hpp:115-133) -----------------------------
-      Pd np = me;
-      const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
-      if (disp > 0.0) {
-        if (disp > a.max_disp) {
-          const double sc = a.max_disp / disp;
-          tx *= sc;
-          ty *= sc;
-          tz *= sc;
-        }
-        np.x = me.x + tx;
-        np.y = me.y + ty;
-        np.z = me.z + tz;
-        fl |= ABS_FLAG_MOVED;
-      }
-      if (tg != 0.0) {
-        const double nd = me.d + tg;
-        np.d = nd > 1e-9 ? nd : 1e-9;
-        if (tg > 0.0) fl |= ABS_FLAG_GREW;
-      }
-      reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
-      reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
-      S.flags[i] = fl;
+// Coincident centres (mechanics.cpp:14-19): direction from
+// RandomStream(seed = min uid, stream = max uid).unit_vector() (random.hpp:47-52,
+// cos/sin — the one non-bit-portable term), negated for the larger uid.
+// Out of line: it is essentially never taken and its registers would
+// otherwise cap the occupancy of the force kernel.
+__device__ __noinline__ void coincident_force(unsigned long long ua, unsigned long long ub, double m,
+                                              double* f0, double* f1, double* f2) {
+  const unsigned long long lo = ua < ub ? ua : ub;
+  const unsigned long long hi = ua < ub ? ub : ua;
+  const double zz = -1.0 + 2.0 * abs_u01(abs_rng_word(lo, hi, 0));
+  const double phi = 2.0 * ABS_PI * abs_u01(abs_rng_word(lo, hi, 1));
+  const double rr = sqrt(fmax(0.0, 1.0 - zz * zz));
+  double d0 = rr * cos(phi), d1 = rr * sin(phi), d2 = zz;
+  if (ua != lo) {
+    d0 *= -1.0;
+    d1 *= -1.0;
+    d2 *= -1.0;
+  }
+  *f0 = d0 * m;
+  *f1 = d1 * m;
+  *f2 = d2 * m;
+}
+
+// Outputs of one agent's step that need warp-level cooperation afterwards.
+struct Daughter {
+  bool divides;
+  unsigned long long parent;
+  double x, y, z, d, vol;
+};
+
+// Behaviours, static skip, run_forces and apply_pending for agent i (storage
+// index). `walk(r, r2, visit)` enumerates every candidate j != i with exact
+// fp64 d2 <= r2 in a fixed order; `fetch(j)` returns candidate j's Pd;
+// `uid_of(j)` its uid. `ovl` is this thread's column of the contact list.
+template <int MODEL, bool STATIC, bool RECORD, class OvlT, class Walk, class Fetch, class UidOf>
+__device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, unsigned long long i, const Pd& me,
+                                               double dmax, unsigned char* __restrict__ nv,
+                                               unsigned char* __restrict__ nn, const StepArgs& a,
+                                               unsigned long long cap, OvlT* ovl, int ovl_stride,
+                                               unsigned long long& n_eval, unsigned long long& n_skip,
+                                               Walk&& walk, Fetch&& fetch, UidOf&& uid_of) {
+  Daughter dg{false, 0, 0, 0, 0, 0, 0};
+  unsigned char fl = S.flags[i];
+  const unsigned long long my_uid = S.uid[i];
+  dg.parent = my_uid;
+  // --- staticness phase 2 (simulation.cpp:375-384) -----------------------
+  if (STATIC) {
+    if (a.iteration == 0) {
+      fl = 0;  // :335-349 everyone participates, flags wiped
+    } else {
+      const bool skip = !(fl & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED |
+                                ABS_FLAG_NEIGHBOR_VIOLATION | ABS_FLAG_NEW_NEIGHBOR)) &&
+                        !nv[i] && !nn[i] && S.partners[i] <= 1u;
+      fl = skip ? ABS_FLAG_STATIC : 0;
+      nv[i] = 0;
+      nn[i] = 0;
     }
-    // --- stage daughters (warp-aggregated slot claim) ------------------
-    if (a.model == ABS_MODEL_PROLIFERATION) {
-      const unsigned int ballot = __ballot_sync(0xffffffffu, divides);
-      if (ballot) {
-        unsigned long long slot0 = 0;
-        if (lane == 0) slot0 = atomicAdd(&gw->staged, (unsigned long long)__popc(ballot));
-        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-        if (divides) {
-          const unsigned long long slot = slot0 + __popc(ballot & ((1u << lane) - 1u));
-          st_parent[slot] = my_uid;
-          reinterpret_cast<double2*>(st_pd + slot)[0] = make_double2(dpx, dpy);
-          reinterpret_cast<double2*>(st_pd + slot)[1] = make_double2(dpz, dd);
-          st_vol[slot] = dvol;
-          div_mark[my_uid] = 1u;
-        }
+  }
+  // --- behaviours (run before forces, simulation.cpp:389-394) -------------
+  double tx = 0.0, ty = 0.0, tz = 0.0, tg = 0.0;
+  if (MODEL != ABS_MODEL_NONE && S.beh[i]) {
+    if (MODEL == ABS_MODEL_PROLIFERATION) {
+      double v = S.vol[i] + a.mp[0];
+      if (v > a.mp[1]) {
+        v *= 0.5;
+        double dir[3];
+        abs_unit_vector(a.seed, my_uid, ABS_RNG_DIVISION_BASE(a.iteration), dir);
+        const double half = 0.5 * me.d;
+        dg.x = me.x + dir[0] * half;
+        dg.y = me.y + dir[1] * half;
+        dg.z = me.z + dir[2] * half;
+        dg.d = abs_diameter_of_volume(v);
+        dg.vol = v;
+        dg.divides = true;
+      }
+      S.vol[i] = v;
+      tg += abs_diameter_of_volume(v) - me.d;
+    } else if (MODEL == ABS_MODEL_DRIVE) {
+      double dl[3];
+      abs_drive_delta(me.x, me.y, me.z, a.mp[0], a.mp[1], a.mp[2], a.mp[3], a.seed, my_uid, a.iteration, dl);
+      tx += dl[0];
+      ty += dl[1];
+      tz += dl[2];
+    } else if (MODEL == ABS_MODEL_GROW) {
+      if (me.d < a.mp[1]) {
+        const double rem = a.mp[1] - me.d;
+        tg += rem < a.mp[0] ? rem : a.mp[0];
       }
     }
   }
-  // counters: warp reduce, one atomic per warp
+  // --- run_forces (simulation.cpp:463-489) --------------------------------
+  // Pass A streams every candidate through the exact fp64 radius test
+  // (d2 <= r^2 counts a force evaluation) and records the ones that may
+  // overlap; pass B runs pairwise_repulsion only on those, in stream order.
+  // A pair can only contribute if dist < h = 0.5 (d_a + d_b); the record test
+  // d2 < h^2 (1 + 2^-50) is a strict superset of that (sqrt is correctly
+  // rounded and monotone), so no contributor is missed and every decision in
+  // pass B is the reference's exact one.
+  if (STATIC && (fl & ABS_FLAG_STATIC)) {
+    ++n_skip;
+  } else {
+    const double r = 0.5 * (me.d + dmax);
+    unsigned int evals = 0, nov = 0;
+    walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
+      ++evals;
+      const double h = 0.5 * (me.d + q.d);
+      if (d2 < h * h * (1.0 + 0x1.0p-50)) {
+        if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+        ++nov;
+      }
+    });
+    n_eval += evals;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    unsigned int contributors = 0;
+    const double k = a.k;
+    auto contact = [&](unsigned int j) {
+      const Pd q = fetch(j);
+      const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+      // pairwise_repulsion (mechanics.cpp:10-27)
+      const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+      const double overlap = 0.5 * (me.d + q.d) - dist;
+      if (overlap <= 0.0) return;
+      double f0, f1, f2;
+      if (dist > 0.0) {
+        const double sc = k * overlap / dist;
+        f0 = dx * sc;
+        f1 = dy * sc;
+        f2 = dz * sc;
+      } else {
+        coincident_force(my_uid, uid_of(j), k * overlap, &f0, &f1, &f2);
+      }
+      if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
+        ++contributors;
+        fx += f0;
+        fy += f1;
+        fz += f2;
+      }
+    };
+    if (nov <= kMaxContacts) {
+      for (unsigned int c = 0; c < nov; ++c) contact(ovl[c * ovl_stride]);
+    } else {  // more contacts than the list holds: re-walk (rare)
+      walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
+        const double h = 0.5 * (me.d + q.d);
+        if (d2 < h * h * (1.0 + 0x1.0p-50)) contact(j);
+      });
+    }
+    if (RECORD) {
+      S.force[i] = fx;
+      S.force[cap + i] = fy;
+      S.force[2 * cap + i] = fz;
+    }
+    S.partners[i] = contributors;
+    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
+      tx += fx * a.dt;
+      ty += fy * a.dt;
+      tz += fz * a.dt;
+    }
+  }
+  // --- apply_pending (agent.hpp:115-133) -----------------------------------
+  Pd np = me;
+  const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
+  if (disp > 0.0) {
+    if (disp > a.max_disp) {
+      const double sc = a.max_disp / disp;
+      tx *= sc;
+      ty *= sc;
+      tz *= sc;
+    }
+    np.x = me.x + tx;
+    np.y = me.y + ty;
+    np.z = me.z + tz;
+    fl |= ABS_FLAG_MOVED;
+  }
+  if (tg != 0.0) {
+    const double nd = me.d + tg;
+    np.d = nd > 1e-9 ? nd : 1e-9;
+    if (tg > 0.0) fl |= ABS_FLAG_GREW;
+  }
+  reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
+  reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
+  S.flags[i] = fl;
+  return dg;
+}
+
+// Daughter staging: warp-ballot compaction into the stage buffers
+// (commit.cpp:186-222 appends; here slots are claimed with one atomic per warp).
+__device__ __forceinline__ void stage_daughter(const Daughter& dg, DevGrid* gw,
+                                               unsigned long long* __restrict__ st_parent,
+                                               Pd* __restrict__ st_pd, double* __restrict__ st_vol,
+                                               unsigned int* __restrict__ div_mark) {
+  const int lane = threadIdx.x & 31;
+  const unsigned int ballot = __ballot_sync(0xffffffffu, dg.divides);
+  if (!ballot) return;
+  unsigned long long slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(&gw->staged, (unsigned long long)__popc(ballot));
+  slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+  if (dg.divides) {
+    const unsigned long long slot = slot0 + __popc(ballot & ((1u << lane) - 1u));
+    st_parent[slot] = dg.parent;
+    reinterpret_cast<double2*>(st_pd + slot)[0] = make_double2(dg.x, dg.y);
+    reinterpret_cast<double2*>(st_pd + slot)[1] = make_double2(dg.z, dg.d);
+    st_vol[slot] = dg.vol;
+    div_mark[dg.parent] = 1u;
+  }
+}
+
+__device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsigned long long n_skip, DevGrid* gw) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
     n_eval += __shfl_xor_sync(0xffffffffu, n_eval, off);
     n_skip += __shfl_xor_sync(0xffffffffu, n_skip, off);
   }
-  if (lane == 0) {
+  if ((threadIdx.x & 31) == 0) {
     if (n_eval) atomicAdd(&gw->evals, n_eval);
     if (n_skip) atomicAdd(&gw->skips, n_skip);
   }
+}
+
+// Global-gather force kernel: one agent per thread, candidates fetched from
+// HBM/L2 through the per-lane flat window stream. Used for small tiles'
+// overflow and as the reference implementation of the tiled kernel below.
+template <int MODEL, bool STATIC, bool RECORD>
+__global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
+    k_force(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
+            unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
+            unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
+            unsigned int* __restrict__ div_mark) {
+  if (gp->err) return;
+  __shared__ QGrid Q;
+  __shared__ unsigned int wj0[kMaxRows][kForceThreads];
+  __shared__ unsigned int wj1[kMaxRows][kForceThreads];
+  __shared__ unsigned int ovl[kMaxContacts][kForceThreads];
+  if (threadIdx.x == 0) Q = make_qgrid(*gp);
+  __syncthreads();
+  const unsigned long long n = gp->n;
+  const double dmax = gp->dmax;
+  unsigned long long n_eval = 0, n_skip = 0;
+  for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n;
+       base += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = base + threadIdx.x;
+    Daughter dg{false, 0, 0, 0, 0, 0, 0};
+    if (i < n) {
+      const Pd me = load_pd(S.pd + i);
+      const unsigned int self = static_cast<unsigned int>(i);
+      dg = agent_step<MODEL, STATIC, RECORD>(
+          S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
+          [&](double r, double r2, auto&& visit) {
+            for_each_neighbor_flat(Q, S.pd, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
+                                   [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                                     visit(j, q, d2);
+                                   });
+          },
+          [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
+    }
+    if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+  }
+  flush_counters(n_eval, n_skip, gw);
+}
+
+// ------------------------------------------------------------ tiled force
+// One persistent CTA per SM walks tiles of kTB^3 reference boxes. For each
+// tile it stages the tile's halo — exactly the reference's 3x3x3-box
+// neighbourhood of every box in the tile (uniform_grid.cpp:199-201) — into
+// shared memory with one TMA bulk copy (cp.async.bulk) per bin row (a row
+// of the cell-ordered arrays is one contiguous byte range), builds a local
+// cell table, and then runs the same per-agent step as k_force with every
+// candidate read from shared memory. Tiles whose halo exceeds the staging
+// capacity fall back to the global walk.
+constexpr int kTileThreads = 512;
+constexpr int kTB = 4;                        // tile edge in reference boxes
+constexpr int kTileCap = 4096;                // staged agents per tile
+constexpr int kTileWinRows = 24;              // stored windows per query
+constexpr int kTileMaxHaloRows = 144;         // ((kTB + 2) * 2)^2 for B <= 2
+constexpr int kTileMaxHaloX = (kTB + 2) * 2 + 1;
+constexpr int kTileMaxCoreRows = (kTB * 2) * (kTB * 2);
+
+struct TileSmem {
+  Pd sp[kTileCap];
+  unsigned int lst[kTileMaxHaloRows][kTileMaxHaloX];  // local start of each halo bin (+ end)
+  unsigned int lrow[kTileMaxHaloRows + 1];            // local start of each halo row
+  unsigned int rowg0[kTileMaxHaloRows];               // global index of each row's first agent
+  unsigned int qpre[kTileMaxCoreRows + 1];            // query prefix over core rows
+  unsigned short qrow[kTileMaxCoreRows];              // halo row of each core row
+  unsigned short qoff[kTileMaxCoreRows];              // local bin offset of the core x range
+  unsigned short wj0[kTileWinRows][kTileThreads];
+  unsigned short wj1[kTileWinRows][kTileThreads];
+  unsigned short ovl[kMaxContacts][kTileThreads];
+  unsigned int ovl32[1];
+  unsigned long long bar;
+  int hx0, hx1, hy0, hy1, hz0, hz1, nhx, nhy, nrows, ncore, total, overflow;
+};
+
+__device__ __forceinline__ unsigned int smem_u32(const void* p) {
+  return static_cast<unsigned int>(__cvta_generic_to_shared(p));
+}
+
+template <int MODEL, bool STATIC, bool RECORD>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_force_tile(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
+                 unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
+                 unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
+                 unsigned int* __restrict__ div_mark) {
+  if (gp->err) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw);
+  __shared__ QGrid Q;
+  __shared__ DevGrid G;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    G = *gp;
+    Q = make_qgrid(G);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const double dmax = G.dmax;
+  const unsigned int Bx = G.B[0], By = G.B[1], Bz = G.B[2];
+  const unsigned int ntx = (G.dims[0] + kTB - 1) / kTB, nty = (G.dims[1] + kTB - 1) / kTB,
+                     ntz = (G.dims[2] + kTB - 1) / kTB;
+  const unsigned long long ntiles = (unsigned long long)ntx * nty * ntz;
+  unsigned long long n_eval = 0, n_skip = 0;
+  unsigned int phase = 0;
+  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // ---- tile geometry (boxes -> bins) ---------------------------------
+    if (tid == 0) {
+      const unsigned int tx = tile % ntx, ty = (tile / ntx) % nty, tz = tile / ((unsigned long long)ntx * nty);
+      const int bx0 = tx * kTB, by0 = ty * kTB, bz0 = tz * kTB;
+      T.hx0 = max(bx0 - 1, 0) * Bx;
+      T.hx1 = min(bx0 + kTB + 1, (int)G.dims[0]) * Bx;
+      T.hy0 = max(by0 - 1, 0) * By;
+      T.hy1 = min(by0 + kTB + 1, (int)G.dims[1]) * By;
+      T.hz0 = max(bz0 - 1, 0) * Bz;
+      T.hz1 = min(bz0 + kTB + 1, (int)G.dims[2]) * Bz;
+      T.nhx = T.hx1 - T.hx0;
+      T.nhy = T.hy1 - T.hy0;
+      T.nrows = T.nhy * (T.hz1 - T.hz0);
+      // core rows/bins
+      const int cy0 = by0 * By, cy1 = min(by0 + kTB, (int)G.dims[1]) * By;
+      const int cz0 = bz0 * Bz, cz1 = min(bz0 + kTB, (int)G.dims[2]) * Bz;
+      int nc = 0;
+      for (int bz = cz0; bz < cz1; ++bz)
+        for (int by = cy0; by < cy1; ++by) {
+          T.qrow[nc] = static_cast<unsigned short>((bz - T.hz0) * T.nhy + (by - T.hy0));
+          ++nc;
+        }
+      T.ncore = nc;
+      T.qoff[0] = static_cast<unsigned short>(bx0 * Bx - T.hx0);
+      T.qoff[1] = static_cast<unsigned short>(min(bx0 + kTB, (int)G.dims[0]) * Bx - T.hx0);
+    }
+    __syncthreads();
+    const int nrows = T.nrows, nhx = T.nhx, nhy = T.nhy;
+    // ---- halo cell table: global bin starts -> local offsets ------------
+    for (int idx = tid; idx < nrows * (nhx + 1); idx += kTileThreads) {
+      const int r = idx / (nhx + 1), e = idx % (nhx + 1);
+      const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
+      const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+      T.lst[r][e] = __ldg(start + row + T.hx0 + e);
+    }
+    __syncthreads();
+    if (tid < 32) {  // row lengths -> exclusive scan (one warp)
+      unsigned int carry = 0;
+      for (int r0 = 0; r0 < nrows; r0 += 32) {
+        const int r = r0 + tid;
+        const unsigned int len = r < nrows ? T.lst[r][nhx] - T.lst[r][0] : 0;
+        const unsigned int inc = warp_incl_scan(len);
+        if (r < nrows) {
+          T.lrow[r] = carry + inc - len;
+          T.rowg0[r] = T.lst[r][0];
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (tid == 0) {
+        T.lrow[nrows] = carry;
+        T.total = carry;
+        T.overflow = carry > kTileCap;
+      }
+    }
+    __syncthreads();
+    const bool overflow = T.overflow;
+    if (!overflow) {
+      for (int idx = tid; idx < nrows * (nhx + 1); idx += kTileThreads) {
+        const int r = idx / (nhx + 1), e = idx % (nhx + 1);
+        T.lst[r][e] = T.lst[r][e] - T.rowg0[r] + T.lrow[r];
+      }
+      // ---- TMA: one bulk copy per non-empty halo row ------------------
+      if (tid == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&T.bar)),
+                     "r"(T.total * (unsigned int)sizeof(Pd))
+                     : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      for (int r = tid; r < nrows; r += kTileThreads) {
+        const unsigned int len = T.lrow[r + 1] - T.lrow[r];
+        if (len) {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(&T.sp[T.lrow[r]])),
+              "l"(S.pd + T.rowg0[r]), "r"(len * (unsigned int)sizeof(Pd)), "r"(smem_u32(&T.bar))
+              : "memory");
+        }
+      }
+    }
+    // query prefix over core rows (local ranges)
+    if (tid < 32) {
+      unsigned int carry = 0;
+      for (int c0 = 0; c0 < T.ncore; c0 += 32) {
+        const int cr = c0 + tid;
+        unsigned int len = 0;
+        if (cr < T.ncore) {
+          const int r = T.qrow[cr];
+          len = overflow ? 0 : T.lst[r][T.qoff[1]] - T.lst[r][T.qoff[0]];
+          if (overflow) {  // global indices: recompute from start[]
+            const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
+            const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+            len = __ldg(start + row + T.hx0 + T.qoff[1]) - __ldg(start + row + T.hx0 + T.qoff[0]);
+          }
+        }
+        const unsigned int inc = warp_incl_scan(len);
+        if (cr < T.ncore) T.qpre[cr] = carry + inc - len;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (tid == 0) T.qpre[T.ncore] = carry;
+    }
+    __syncthreads();
+    if (!overflow) {  // wait for the staged halo
+      const unsigned int bar = smem_u32(&T.bar);
+      unsigned int done = 0;
+      while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+      }
+      phase ^= 1u;
+    }
+    // ---- queries ---------------------------------------------------------
+    const unsigned int nq = T.qpre[T.ncore];
+    for (unsigned int q0 = 0; q0 < nq; q0 += kTileThreads) {
+      const unsigned int q = q0 + tid;
+      Daughter dg{false, 0, 0, 0, 0, 0, 0};
+      if (q < nq) {
+        int lo = 0, hi = T.ncore - 1;  // core row holding query q
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (T.qpre[mid] <= q) lo = mid;
+          else hi = mid - 1;
+        }
+        const int r = T.qrow[lo];
+        const unsigned int off = q - T.qpre[lo];
+        unsigned long long gi;
+        unsigned int li = 0;
+        if (!overflow) {
+          li = T.lst[r][T.qoff[0]] + off;
+          gi = T.rowg0[r] + (li - T.lrow[r]);
+        } else {
+          const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
+          const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+          gi = __ldg(start + row + T.hx0 + T.qoff[0]) + off;
+        }
+        const Pd me = overflow ? load_pd(S.pd + gi) : T.sp[li];
+        if (!overflow) {
+          dg = agent_step<MODEL, STATIC, RECORD>(
+              S, out, gi, me, dmax, nv, nn, a, cap, &T.ovl[0][tid], kTileThreads, n_eval, n_skip,
+              [&](double rr, double r2, auto&& visit) {
+                const float fx = static_cast<float>(me.x - Q.ox);
+                const float fy = static_cast<float>(me.y - Q.oy);
+                const float fz = static_cast<float>(me.z - Q.oz);
+                const float rf = static_cast<float>(rr) * 1.000001f + Q.slack;
+                const float rf2 = rf * rf;
+                int bl[3], bh[3];
+                box_bin_range(Q, me.x, me.y, me.z, bl, bh);
+                const int z0 = max(fbin(fz - rf, Q.inv_s[2], Q.bd[2]), max(T.hz0, bl[2]));
+                const int z1 = min(fbin(fz + rf, Q.inv_s[2], Q.bd[2]), min(T.hz1 - 1, bh[2]));
+                const int y0 = max(fbin(fy - rf, Q.inv_s[1], Q.bd[1]), max(T.hy0, bl[1]));
+                const int y1 = min(fbin(fy + rf, Q.inv_s[1], Q.bd[1]), min(T.hy1 - 1, bh[1]));
+                int nw = 0;
+                for (int bz = z0; bz <= z1; ++bz) {
+                  const float zl = static_cast<float>(bz) * Q.s[2];
+                  const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + Q.s[2])), 0.0f);
+                  for (int by = y0; by <= y1; ++by) {
+                    const float yl = static_cast<float>(by) * Q.s[1];
+                    const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + Q.s[1])), 0.0f);
+                    const float rem = rf2 - (gy * gy + gz * gz);
+                    if (rem < 0.0f) continue;
+                    const float w = sqrtf(rem);
+                    const int x0 = max(fbin(fx - w, Q.inv_s[0], Q.bd[0]), max(T.hx0, bl[0])) - T.hx0;
+                    const int x1 = min(fbin(fx + w, Q.inv_s[0], Q.bd[0]), min(T.hx1 - 1, bh[0])) - T.hx0;
+                    const int hr = (bz - T.hz0) * nhy + (by - T.hy0);
+                    const unsigned int j0 = T.lst[hr][x0], j1 = T.lst[hr][x1 + 1];
+                    if (j1 <= j0) continue;
+                    if (nw < kTileWinRows) {
+                      T.wj0[nw][tid] = static_cast<unsigned short>(j0);
+                      T.wj1[nw][tid] = static_cast<unsigned short>(j1);
+                      ++nw;
+                    } else {
+                      for (unsigned int j = j0; j < j1; ++j) {
+                        if (j == li) continue;
+                        const Pd c = T.sp[j];
+                        const double dx = me.x - c.x, dy = me.y - c.y, dz = me.z - c.z;
+                        const double d2 = (dx * dx + dy * dy) + dz * dz;
+                        if (d2 <= r2) visit(j, c, d2);
+                      }
+                    }
+                  }
+                }
+                if (nw == 0) return;
+                int k = 0;
+                unsigned int j = T.wj0[0][tid], je = T.wj1[0][tid];
+                while (k < nw) {
+                  unsigned int idx[kBatch];
+#pragma unroll
+                  for (int u = 0; u < kBatch; ++u) {
+                    idx[u] = li;
+                    if (k < nw) {
+                      idx[u] = j;
+                      if (++j == je && ++k < nw) {
+                        j = T.wj0[k][tid];
+                        je = T.wj1[k][tid];
+                      }
+                    }
+                  }
+                  Pd c[kBatch];
+#pragma unroll
+                  for (int u = 0; u < kBatch; ++u) c[u] = T.sp[idx[u]];
+#pragma unroll
+                  for (int u = 0; u < kBatch; ++u) {
+                    if (idx[u] != li) {
+                      const double dx = me.x - c[u].x, dy = me.y - c[u].y, dz = me.z - c[u].z;
+                      const double d2 = (dx * dx + dy * dy) + dz * dz;
+                      if (d2 <= r2) visit(idx[u], c[u], d2);
+                    }
+                  }
+                }
+              },
+              [&](unsigned int j) { return T.sp[j]; },
+              [&](unsigned int j) {  // local -> global index of a staged agent
+                int lo2 = 0, hi2 = nrows - 1;
+                while (lo2 < hi2) {
+                  const int mid = (lo2 + hi2 + 1) >> 1;
+                  if (T.lrow[mid] <= j) lo2 = mid;
+                  else hi2 = mid - 1;
+                }
+                return S.uid[T.rowg0[lo2] + (j - T.lrow[lo2])];
+              });
+        } else {
+          const unsigned int self = static_cast<unsigned int>(gi);
+          // overflow tile: the staging area is free, carve a u32 contact list
+          unsigned int* ovl32 = reinterpret_cast<unsigned int*>(T.sp) + tid;
+          dg = agent_step<MODEL, STATIC, RECORD>(
+              S, out, gi, me, dmax, nv, nn, a, cap, ovl32, kTileThreads, n_eval, n_skip,
+              [&](double rr, double r2, auto&& visit) {
+                for_each_neighbor(Q, S.pd, start, self, me.x, me.y, me.z, rr, r2,
+                                  [&](unsigned int j, const Pd& c, double, double, double, double d2) {
+                                    visit(j, c, d2);
+                                  });
+              },
+              [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
+        }
+      }
+      if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+    }
+    __syncthreads();  // smem reused by the next tile
+  }
+  flush_counters(n_eval, n_skip, gw);
 }
 
 // ------------------------------------------------------------ commit
@@ -589,11 +987,11 @@ __global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
             }
             if (min_d2 > cull) continue;
             // the box's sub-bins: B x B rows of B contiguous bins
-            for (unsigned int sz = 0; sz < G.B; ++sz)
-              for (unsigned int sy = 0; sy < G.B; ++sy) {
-                const unsigned int bz = (unsigned int)z * G.B + sz, by = (unsigned int)y * G.B + sy;
-                const unsigned int row = G.bd[0] * (by + G.bd[1] * bz) + (unsigned int)x * G.B;
-                for (unsigned int j = start[row]; j < start[row + G.B]; ++j) {
+            for (unsigned int sz = 0; sz < G.B[2]; ++sz)
+              for (unsigned int sy = 0; sy < G.B[1]; ++sy) {
+                const unsigned int bz = (unsigned int)z * G.B[2] + sz, by = (unsigned int)y * G.B[1] + sy;
+                const unsigned int row = G.bd[0] * (by + G.bd[1] * bz) + (unsigned int)x * G.B[0];
+                for (unsigned int j = start[row]; j < start[row + G.B[0]]; ++j) {
                   const Pd q = load_pd(live + j);
                   const double dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
                   if ((dx * dx + dy * dy) + dz * dz <= r2) S.flags[j] |= ABS_FLAG_NEW_NEIGHBOR;
@@ -670,12 +1068,13 @@ __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigne
 __global__ void k_nbr_count(const Pd* __restrict__ pd, const DevGrid* g,
                             const unsigned int* __restrict__ start, unsigned long long* cnt) {
   const DevGrid G = *g;
+  const QGrid Q = make_qgrid(G);
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd me = load_pd(pd + i);
     const double r = 0.5 * (me.d + G.dmax);
     unsigned long long c = 0;
-    for_each_neighbor(G, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
+    for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
                       [&](unsigned int, const Pd&, double, double, double, double) { ++c; });
     cnt[i] = c;
   }
@@ -685,12 +1084,13 @@ __global__ void k_nbr_fill(const Pd* __restrict__ pd, const unsigned long long* 
                            const DevGrid* g, const unsigned int* __restrict__ start,
                            const unsigned long long* __restrict__ off, unsigned long long* out) {
   const DevGrid G = *g;
+  const QGrid Q = make_qgrid(G);
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd me = load_pd(pd + i);
     const double r = 0.5 * (me.d + G.dmax);
     unsigned long long w = off[i];
-    for_each_neighbor(G, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
+    for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
                       [&](unsigned int j, const Pd&, double, double, double, double) { out[w++] = uid[j]; });
     // insertion sort of this agent's uid list
     const unsigned long long b = off[i], e = off[i + 1];
@@ -860,12 +1260,6 @@ __global__ void k_remove_move(const Pd* pos_in, Pd* pos, Soa S, const unsigned l
   }
 }
 
-__global__ void k_uid_to_slot(const unsigned long long* __restrict__ uid, unsigned long long n,
-                              unsigned long long* __restrict__ map) {
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x)
-    map[uid[i]] = i;
-}
 
 __global__ void k_set_u32(unsigned int* a, unsigned long long n, unsigned int v) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
@@ -937,6 +1331,12 @@ int set_err(abs_gpu_ctx* c, int code, const std::string& m) {
 int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   const unsigned long long b = (work + kThreads - 1) / kThreads;
   const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 8;
+  return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
+}
+
+int force_blocks(const abs_gpu_ctx* c) {
+  const unsigned long long b = (c->cap + kForceThreads - 1) / kForceThreads;
+  const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 16;
   return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
 }
 
@@ -1057,7 +1457,16 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
   return a;
 }
 
-int bins_cfg(const abs_gpu_ctx* c) { return c->cfg.bins_per_box == 2 ? 2 : 1; }
+// Sub-bins per box edge: y/z rows finer than x (the x extent of a row is
+// trimmed to the sphere's cross-section, so x resolution matters less).
+unsigned int bins_yz(const abs_gpu_ctx* c) {
+  const int b = c->cfg.bins_per_box;
+  return b <= 0 ? 2u : static_cast<unsigned int>(std::min(b, 2));
+}
+unsigned int bins_x(const abs_gpu_ctx* c) {
+  const int b = c->cfg.bins_per_box_x;
+  return b <= 0 ? 1u : static_cast<unsigned int>(std::min(b, 2));
+}
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
@@ -1069,7 +1478,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   }
   const Pd* pos = cur_pos(c);
   k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_cfg(c), c->bins_cap, c->cap,
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_x(c), bins_yz(c), c->bins_cap, c->cap,
                                       c->uid_cap, may_add, iteration);
   k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
   c->launches += 3;
@@ -1082,6 +1491,60 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->cur = nxt;
   c->pos_in_new = false;
   c->grid_valid = true;
+}
+
+template <int MODEL, bool STATIC, bool RECORD>
+void launch_tile(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+  static bool configured = false;  // per template instance
+  const int smem = static_cast<int>(sizeof(TileSmem));
+  if (!configured) {
+    cudaFuncSetAttribute(k_force_tile<MODEL, STATIC, RECORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  k_force_tile<MODEL, STATIC, RECORD><<<c->sms, kTileThreads, smem, c->stream>>>(
+      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+}
+
+// ABSIM_FORCE_KERNEL=tile selects the TMA-staged tile kernel; the default
+// is the per-lane gather kernel (faster on the measured configs so far,
+// see DESIGN.md §Kernels).
+bool use_tile_kernel() {
+  static const int v = [] {
+    const char* e = std::getenv("ABSIM_FORCE_KERNEL");
+    return (e && std::strcmp(e, "tile") == 0) ? 1 : 0;
+  }();
+  return v != 0;
+}
+
+template <int MODEL, bool STATIC>
+void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
+  if (use_tile_kernel()) {
+    if (c->cfg.record_forces) launch_tile<MODEL, STATIC, true>(c, S, a);
+    else launch_tile<MODEL, STATIC, false>(c, S, a);
+    return;
+  }
+  const int nb = force_blocks(c);
+  if (c->cfg.record_forces)
+    k_force<MODEL, STATIC, true><<<nb, kForceThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a,
+                                                                c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+  else
+    k_force<MODEL, STATIC, false><<<nb, kForceThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a,
+                                                                 c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+}
+
+template <int MODEL>
+void launch_force_m(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
+  if (c->cfg.detect_static_agents) launch_force_t<MODEL, true>(c, nb, S, a);
+  else launch_force_t<MODEL, false>(c, nb, S, a);
+}
+
+void launch_force(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
+  switch (c->cfg.model) {
+    case ABS_MODEL_PROLIFERATION: launch_force_m<ABS_MODEL_PROLIFERATION>(c, nb, S, a); break;
+    case ABS_MODEL_DRIVE: launch_force_m<ABS_MODEL_DRIVE>(c, nb, S, a); break;
+    case ABS_MODEL_GROW: launch_force_m<ABS_MODEL_GROW>(c, nb, S, a); break;
+    default: launch_force_m<ABS_MODEL_NONE>(c, nb, S, a); break;
+  }
 }
 
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
@@ -1106,8 +1569,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
     e1 = c->ev[c->ev_used++];
     cudaEventRecord(e0, c->stream);
   }
-  k_force<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap,
-                                          c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+  launch_force(c, nb, S, a);
   ++c->launches;
   if (c->timing) cudaEventRecord(e1, c->stream);
   c->pos_in_new = true;
@@ -1204,7 +1666,7 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   h.red[3] = h.red[4] = h.red[5] = kInfOrdHi;
   h.red[6] = kZeroOrd;
   h.dims[0] = h.dims[1] = h.dims[2] = 1;
-  h.B = 1;
+  h.B[0] = h.B[1] = h.B[2] = 1;
   CK(cudaMemcpy(c->g, &h, sizeof h, cudaMemcpyHostToDevice));
   int rc = ensure_capacity(c, std::max<unsigned long long>(cfg->capacity, 1024), 0);
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
@@ -1311,7 +1773,7 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   h.red[3] = h.red[4] = h.red[5] = kInfOrdHi;
   h.red[6] = kZeroOrd;
   h.dims[0] = h.dims[1] = h.dims[2] = 1;
-  h.B = 1;
+  h.B[0] = h.B[1] = h.B[2] = 1;
   h.n = n;
   h.uid_count = uid_count;
   CK(cudaMemcpyAsync(c->g, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
@@ -1536,9 +1998,9 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
   CK(cudaStreamSynchronize(c->stream));
   const unsigned long long tot = offsets[n];
   if (total) *total = tot;
-  if (tot > cap || !uids) {
+  if (!uids || tot > cap) {
     cudaFree(cnt); cudaFree(len); cudaFree(t64);
-    return tot > cap ? set_err(c, ABS_ERR_CAPACITY, "neighbour buffer too small") : ABS_OK;
+    return uids ? set_err(c, ABS_ERR_CAPACITY, "neighbour buffer too small") : ABS_OK;
   }
   CK(dalloc(&out, tot));
   k_nbr_fill<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->S[c->cur].uid, c->g, c->start, cnt, out);
@@ -1561,7 +2023,7 @@ int abs_gpu_sort(abs_gpu_ctx* c) {
     c->grid_valid = false;
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, ~0ull, ~0ull, ~0ull, 0, c->iteration);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, ~0ull, ~0ull, ~0ull, 0, c->iteration);
   c->launches += 2;
   DevGrid h{};
   int rc = read_grid(c, &h);

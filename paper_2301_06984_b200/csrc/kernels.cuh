@@ -23,6 +23,10 @@ namespace absgpu {
 
 constexpr int kThreads = 256;
 constexpr int kScanTile = 2048;  // 256 threads x 8 values
+#ifndef ABS_UNROLL
+#define ABS_UNROLL 1
+#endif
+constexpr int kUnroll = ABS_UNROLL;  // candidate loads in flight per lane
 
 struct __align__(16) Pd {
   double x, y, z, d;
@@ -46,11 +50,11 @@ struct DevGrid {
   double origin[3];
   double box;
   double dmax;
-  double s;       // internal bin edge = box / B
+  double s[3];    // internal bin edge per axis = box / B[k]
   double margin;  // conservative culling slack (absolute)
   unsigned int dims[3];
-  unsigned int bd[3];  // bins per axis = B * dims
-  unsigned int B;
+  unsigned int bd[3];  // bins per axis = B[k] * dims[k]
+  unsigned int B[3];   // sub-bins per box edge per axis (x, y, z)
   unsigned int pad;
   unsigned long long nbins;
   unsigned long long needed_bins;
@@ -110,48 +114,199 @@ __device__ __forceinline__ unsigned int box_coord(double p, double o, double box
 // Internal bin along one axis: sub-bins nest exactly inside reference boxes.
 __device__ __forceinline__ unsigned int bin_coord(double p, double o, const DevGrid& g, int k) {
   const unsigned int c = box_coord(p, o, g.box, g.dims[k]);
-  if (g.B == 1) return c;
+  if (g.B[k] == 1) return c;
   const double t = (p - o) - static_cast<double>(c) * g.box;
-  return c * g.B + static_cast<unsigned int>(clamp_bin(t, g.s, g.B));
+  return c * g.B[k] + static_cast<unsigned int>(clamp_bin(t, g.s[k], g.B[k]));
+}
+
+// Culling geometry of the current grid, in fp32 relative to the origin.
+// Only used to choose WHICH bins to scan; every neighbour decision is the
+// exact fp64 test. `slack` bounds the fp32 rounding of coordinates and bin
+// edges, so the scanned set is a superset of the true neighbour set.
+struct QGrid {
+  double ox, oy, oz;
+  double box;
+  float inv_s[3];
+  float s[3];
+  float slack;
+  unsigned int bd[3];
+  unsigned int B[3];
+  unsigned int dims[3];
+};
+
+__device__ __forceinline__ QGrid make_qgrid(const DevGrid& g) {
+  QGrid q;
+  q.ox = g.origin[0];
+  q.oy = g.origin[1];
+  q.oz = g.origin[2];
+  q.box = g.box;
+  float ext = 1.0f;
+  for (int k = 0; k < 3; ++k) {
+    q.s[k] = static_cast<float>(g.s[k]);
+    q.inv_s[k] = 1.0f / q.s[k];
+    q.bd[k] = g.bd[k];
+    q.B[k] = g.B[k];
+    q.dims[k] = g.dims[k];
+    ext = fmaxf(ext, static_cast<float>(g.s[k] * g.bd[k]));
+  }
+  q.slack = 16.0f * ext * 5.96046448e-8f + 1e-5f;
+  return q;
+}
+
+__device__ __forceinline__ int fbin(float v, float inv_s, unsigned int nb) {
+  const int i = __float2int_rd(v * inv_s);
+  return min(max(i, 0), static_cast<int>(nb) - 1);
+}
+
+// Bin range (inclusive) of the 3x3x3 reference boxes around the box holding
+// c (uniform_grid.cpp:185-201): the reference never looks further, so
+// neither do we — this keeps the candidate universe identical to the
+// reference's even for agents that land exactly on a box boundary.
+__device__ __forceinline__ void box_bin_range(const QGrid& g, double cx, double cy, double cz, int lo[3],
+                                              int hi[3]) {
+  const double c[3] = {cx, cy, cz};
+  const double o[3] = {g.ox, g.oy, g.oz};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int b = static_cast<int>(box_coord(c[k], o[k], g.box, g.dims[k]));
+    lo[k] = (b > 0 ? b - 1 : 0) * static_cast<int>(g.B[k]);
+    hi[k] = min(b + 2, static_cast<int>(g.dims[k])) * static_cast<int>(g.B[k]) - 1;
+  }
 }
 
 // Visits every agent j != self whose exact fp64 squared distance to c is
 // <= r2 (inclusive, vec3.hpp:44 evaluation order). Bins are culled
-// conservatively (margin) row by row: for each (z, y) bin row the x extent
-// is trimmed to the sphere's cross-section, and a row is one contiguous
-// range of the cell-ordered arrays.
+// conservatively row by row: for each (z, y) bin row the x extent is trimmed
+// to the sphere's cross-section, and a row is one contiguous range of the
+// cell-ordered arrays.
 template <class F>
-__device__ __forceinline__ void for_each_neighbor(const DevGrid& g, const Pd* __restrict__ pd,
+__device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __restrict__ pd,
                                                   const unsigned int* __restrict__ start,
                                                   unsigned int self, double cx, double cy,
                                                   double cz, double r, double r2, F&& visit) {
-  const double rm = r + g.margin;
-  const double rm2 = rm * rm;
-  const double s = g.s;
-  const int z0 = clamp_bin(cz - rm - g.origin[2], s, g.bd[2]);
-  const int z1 = clamp_bin(cz + rm - g.origin[2], s, g.bd[2]);
-  const int y0 = clamp_bin(cy - rm - g.origin[1], s, g.bd[1]);
-  const int y1 = clamp_bin(cy + rm - g.origin[1], s, g.bd[1]);
+  const float fx = static_cast<float>(cx - g.ox);
+  const float fy = static_cast<float>(cy - g.oy);
+  const float fz = static_cast<float>(cz - g.oz);
+  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
+  const float rf2 = rf * rf;
+  int bl[3], bh[3];
+  box_bin_range(g, cx, cy, cz, bl, bh);
+  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
+  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
   for (int bz = z0; bz <= z1; ++bz) {
-    const double zl = g.origin[2] + bz * s;
-    const double gz = cz < zl ? zl - cz : (cz > zl + s ? cz - (zl + s) : 0.0);
+    const float zl = static_cast<float>(bz) * g.s[2];
+    const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
     for (int by = y0; by <= y1; ++by) {
-      const double yl = g.origin[1] + by * s;
-      const double gy = cy < yl ? yl - cy : (cy > yl + s ? cy - (yl + s) : 0.0);
-      const double rem = rm2 - (gy * gy + gz * gz);
-      if (rem < 0.0) continue;
-      const double w = sqrt(rem);
-      const int x0 = clamp_bin(cx - w - g.origin[0], s, g.bd[0]);
-      const int x1 = clamp_bin(cx + w - g.origin[0], s, g.bd[0]);
+      const float yl = static_cast<float>(by) * g.s[1];
+      const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
+      const float rem = rf2 - (gy * gy + gz * gz);
+      if (rem < 0.0f) continue;
+      const float w = sqrtf(rem);
+      const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
+      const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
       const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
-      const unsigned int j0 = __ldg(start + row + x0);
       const unsigned int j1 = __ldg(start + row + x1 + 1);
-      for (unsigned int j = j0; j < j1; ++j) {
+      for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) {
         if (j == self) continue;
         const Pd q = load_pd(pd + j);
         const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
         const double d2 = (dx * dx + dy * dy) + dz * dz;
         if (d2 <= r2) visit(j, q, dx, dy, dz, d2);
+      }
+    }
+  }
+}
+
+// Flat-stream variant used by the force kernel. Phase 1 computes this
+// lane's non-empty row windows (their `start` loads are independent, so they
+// are all in flight together) into shared memory laid out [row][thread];
+// phase 2 walks all windows as ONE candidate stream with a one-ahead
+// prefetch, so a warp costs max(total candidates) rather than the sum over
+// rows of the longest window. Rows beyond kMaxRows fall back to the nested
+// walk. Visits exactly the same set as for_each_neighbor.
+constexpr int kMaxRows = 32;
+constexpr int kMaxContacts = 16;  // recorded possible contacts per agent (pass B)
+constexpr int kForceThreads = 128;
+#ifndef ABS_BATCH
+#define ABS_BATCH 4
+#endif
+constexpr int kBatch = ABS_BATCH;
+
+template <class F>
+__device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd* __restrict__ pd,
+                                                       const unsigned int* __restrict__ start,
+                                                       unsigned int (*wj0)[kForceThreads],
+                                                       unsigned int (*wj1)[kForceThreads],
+                                                       unsigned int self, double cx, double cy,
+                                                       double cz, double r, double r2, F&& visit) {
+  const int t = threadIdx.x;
+  const float fx = static_cast<float>(cx - g.ox);
+  const float fy = static_cast<float>(cy - g.oy);
+  const float fz = static_cast<float>(cz - g.oz);
+  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
+  const float rf2 = rf * rf;
+  int bl[3], bh[3];
+  box_bin_range(g, cx, cy, cz, bl, bh);
+  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
+  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
+  int nw = 0;
+  for (int bz = z0; bz <= z1; ++bz) {
+    const float zl = static_cast<float>(bz) * g.s[2];
+    const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
+    for (int by = y0; by <= y1; ++by) {
+      const float yl = static_cast<float>(by) * g.s[1];
+      const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
+      const float rem = rf2 - (gy * gy + gz * gz);
+      if (rem < 0.0f) continue;
+      const float w = sqrtf(rem);
+      const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
+      const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
+      const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      const unsigned int j0 = __ldg(start + row + x0);
+      const unsigned int j1 = __ldg(start + row + x1 + 1);
+      if (j1 <= j0) continue;
+      if (nw < kMaxRows) {
+        wj0[nw][t] = j0;
+        wj1[nw][t] = j1;
+        ++nw;
+      } else {
+        for (unsigned int j = j0; j < j1; ++j) {  // overflow rows: nested walk
+          if (j == self) continue;
+          const Pd q = load_pd(pd + j);
+          const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          if (d2 <= r2) visit(j, q, dx, dy, dz, d2);
+        }
+      }
+    }
+  }
+  if (nw == 0) return;
+  int k = 0;
+  unsigned int j = wj0[0][t], je = wj1[0][t];
+  // kBatch candidates per lane per round: their loads are independent and in
+  // flight together; the exact tests are independent fp64 chains.
+  while (k < nw) {
+    unsigned int idx[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      idx[u] = self;  // sentinel: skipped below
+      if (k < nw) {
+        idx[u] = j;
+        if (++j == je && ++k < nw) {
+          j = wj0[k][t];
+          je = wj1[k][t];
+        }
+      }
+    }
+    Pd q[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + idx[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (idx[u] != self) {
+        const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
+        const double d2 = (dx * dx + dy * dy) + dz * dz;
+        if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
       }
     }
   }

@@ -42,7 +42,8 @@ class SimulationParams:
     model_params: list = field(default_factory=lambda: [0.0] * 8)
     capacity: int = 0
     record_forces: bool = True
-    bins_per_box: int = 0
+    bins_per_box: int = 0      # sub-bins per box edge along y, z (0 = auto)
+    bins_per_box_x: int = 0    # sub-bins per box edge along x (0 = auto)
 
     def validate(self):
         """SimulationParams::validate (params.cpp:44-72), hot-path subset."""
@@ -75,6 +76,7 @@ class SimulationParams:
         c.capacity = self.capacity
         c.record_forces = 1 if self.record_forces else 0
         c.bins_per_box = self.bins_per_box
+        c.bins_per_box_x = self.bins_per_box_x
         return c
 
 
