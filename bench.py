@@ -107,50 +107,66 @@ def _dist():
     return dist, world, rank, local
 
 
-def cpu_baseline(wl_name, sample_n, steps, threads=None):
-    """The reference engine (oracle/_ref) on a bounded sample of the workload."""
+CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22}
+CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12}
+
+
+def _ref_sim(wl_name, sample_n, threads):
+    """The reference engine (oracle/_ref, unmodified absim) on a bounded
+    sample of the workload; falls back to the C port if it is not built."""
     from oracle import oracle as O
     wl = _workload(wl_name, sample_n, seed=0)
     prm = wl.params
-    threads = threads or os.cpu_count()
     p = O.OracleParams(seed=prm.get("seed", 0), dt=prm.get("simulation_time_step", 0.1),
                        detect_static=prm.get("detect_static_agents", False),
                        model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
                        sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0)
     try:
-        sim = O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask)
-        kind = "reference"
+        return O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "reference", threads, wl
     except (FileNotFoundError, OSError):
         p.threads = 1
-        sim = O.PortSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask)
-        kind, threads = "port", 1
+        return O.PortSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "port", 1, wl
+
+
+def cpu_baseline(wl_name, steps=None, threads=None):
+    """Reference CPU throughput on a bounded sample (population built untimed)."""
+    threads = threads or os.cpu_count()
+    steps = steps or CPU_STEPS[wl_name]
+    sim, kind, cores, wl = _ref_sim(wl_name, CPU_SAMPLE[wl_name], threads)
     agent_its = 0
     t0 = time.perf_counter()
     for _ in range(steps):
         agent_its += sim.counts()["agents"]
         sim.simulate(1)
     wall = time.perf_counter() - t0
-    return {"value": agent_its / wall, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{wl.name} shape at {wl.n} agents x {steps} steps (same density/distributions), "
-                      f"{wall:.1f} s wall"}
+    return {"value": agent_its / wall, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{wl.name} shape at {wl.n} agents x {steps} iterations "
+                      f"(same density and distributions), {wall:.1f} s of CPU wall time"}
 
 
 def run_reference(args):
-    _, world, rank, _ = _dist() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 1, 0, 0)
+    """--impl reference: each step is one iteration of the unmodified
+    reference on the bounded sample, on all host cores; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    sample_n = {"c1": 131_072, "c2": None, "c3": 1 << 20, "c4": 1 << 20}[args.config]
-    per = []
+    threads = os.cpu_count()
+    sim, kind, cores, wl = _ref_sim(args.config, CPU_SAMPLE[args.config], threads)
     for _ in range(args.warmup):
-        cpu_baseline(args.config, sample_n, 1)
+        sim.simulate(1)
+    agent_its = 0
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        per.append(cpu_baseline(args.config, sample_n, 2))
-    v = statistics.median([p["value"] for p in per])
+        agent_its += sim.counts()["agents"]
+        sim.simulate(1)
+    wall = time.perf_counter() - t0
+    v = agent_its / wall
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "sample_agents": sample_n},
-            "cpu_baseline": {**per[0], "value": v},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl.name, "sample_agents": wl.n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": f"{wl.name} shape at {wl.n} agents, {args.steps} timed iterations"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -167,6 +183,7 @@ def run_gpu(args):
     prm = dict(wl.params)
     prm["record_forces"] = False
     prm["bins_per_box"] = args.bins
+    prm["bins_per_box_x"] = args.bins_x
     if wl.params.get("model") == E.MODEL_PROLIFERATION:
         prm["capacity"] = 5 * wl.n * 2 ** 9
     sim = E.Simulation(E.SimulationParams(**prm), device=local)
@@ -206,25 +223,28 @@ def run_gpu(args):
         agent_its = float(a.item())
     value = agent_its / (ms_max / 1e3)
 
-    # end to end through the public API with host buffers: per step, upload
-    # the step's input state from host memory, run it, read the result back
+    # end to end through the public API with HOST buffers: every step uploads
+    # the step's input state (x, y, z, d) from page-locked host memory, runs the
+    # iteration and reads the resulting positions back into page-locked memory
     e2e = None
     if not args.no_e2e and rank == 0:
-        x, y, z, d = (np.ascontiguousarray(a) for a in (wl.x, wl.y, wl.z, wl.d))
-        sim.add_agents(x, y, z, d, behaviour_mask=wl.mask)
+        pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (wl.x, wl.y, wl.z, wl.d)]
+        mask = None if wl.mask is None else torch.from_numpy(wl.mask).pin_memory().numpy()
+        outp = [torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+        sim.add_agents(*pin, behaviour_mask=mask)
         sim.simulate(1)
-        sim.synchronize()
-        e2e_steps = max(1, min(args.steps, 3))
+        sim.positions(*outp)
+        e2e_steps = max(1, min(args.steps, 5))
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            sim.add_agents(x, y, z, d, behaviour_mask=wl.mask)
+            sim.add_agents(*pin, behaviour_mask=mask)
             sim.simulate(1)
-            out = sim.agents()
+            n_e = sim.positions(*outp)
         dt = time.perf_counter() - t0
-        n_e = len(out["x"])
         e2e = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0)),
-               "d2h_bytes_per_step": n_e * (8 * 8 + 4 + 1 + 8)}
+               "d2h_bytes_per_step": n_e * 32, "steps": e2e_steps,
+               "path": "abs_gpu_upload (pinned host) -> abs_gpu_simulate(1) -> abs_gpu_download (pinned host)"}
 
     hbm, peak_src = _peaks()
     n_agents = r1.final_agent_count
@@ -249,7 +269,7 @@ def run_gpu(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "bins_per_box": args.bins, "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
+                   "bins_per_box": [args.bins_x, args.bins, args.bins], "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
         "roofline": {"bound": "hbm", "kernel": "k_force", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
@@ -262,8 +282,7 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(args.config, {"c1": 131_072, "c2": None, "c3": 1 << 20,
-                                                          "c4": 1 << 20}[args.config], 2)
+        line["cpu_baseline"] = cpu_baseline(args.config)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -280,7 +299,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--bins", type=int, default=2)
+    ap.add_argument("--bins", type=int, default=2, help="sub-bins per box edge along y, z")
+    ap.add_argument("--bins-x", type=int, default=2, help="sub-bins per box edge along x")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

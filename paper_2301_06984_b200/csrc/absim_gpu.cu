@@ -1052,6 +1052,28 @@ __global__ void k_zero_marks(unsigned int* __restrict__ m, const DevGrid* g) {
     m[i] = 0;
 }
 
+// ------------------------------------------------------------ ingest
+// Population upload (Simulation::add_agent, simulation.cpp:131-141): build the
+// interleaved {x,y,z,d} records from SoA device arrays, validate diameters
+// (Agent ctor throws unless d > 0, agent.hpp:25) and default the per-agent
+// state. Host arrays reach these inputs by contiguous H2D copies.
+__global__ void k_ingest(const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
+                         const double* __restrict__ d, const unsigned char* __restrict__ mask, unsigned long long n,
+                         int set_uid, int set_vol, int model_on, Pd* __restrict__ out, Soa S, DevGrid* g) {
+  unsigned int bad = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const double di = d[i];
+    bad |= !(di > 0.0);
+    reinterpret_cast<double2*>(out + i)[0] = make_double2(x[i], y[i]);
+    reinterpret_cast<double2*>(out + i)[1] = make_double2(z[i], di);
+    if (set_uid) S.uid[i] = i;
+    if (set_vol) S.vol[i] = abs_volume_of_diameter(di);
+    S.beh[i] = (model_on && (!mask || mask[i])) ? 1 : 0;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&g->bad_input, 1u);
+}
+
 // ------------------------------------------------------------ parity helpers
 __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* out) {
   const DevGrid G = *g;
@@ -1303,6 +1325,9 @@ struct abs_gpu_ctx {
   Pd* st_pd = nullptr;
   double* st_vol = nullptr;
   unsigned int* div_mark = nullptr;  // uid_cap + 1
+
+  void* pinned = nullptr;  // host staging for downloads (page-locked)
+  size_t pinned_bytes = 0;
 
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs
@@ -1686,6 +1711,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ABS_OK;
@@ -1699,74 +1725,34 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   if (n && (!x || !y || !z || !d)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null coordinate array");
   if (n >= 0xFFFFFFF0ull) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "too many agents");
   cudaSetDevice(c->device);
-  int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * n + 1024), 0);
-  if (rc) return rc;
   const bool host = kind == cudaMemcpyHostToDevice;
-  std::vector<Pd> hp;
-  std::vector<unsigned long long> hu;
-  std::vector<unsigned char> hb, hf;
-  std::vector<double> hv;
-  std::vector<unsigned int> hpart;
-  Soa& S = c->S[c->cur];
-  if (host) {
-    hp.resize(n);
-    hv.resize(n);
-    hb.resize(n);
-    for (unsigned long long i = 0; i < n; ++i) {
-      if (!(d[i] > 0.0)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "diameter must be > 0");
-      hp[i] = Pd{x[i], y[i], z[i], d[i]};
-      hv[i] = volume ? volume[i] : abs_volume_of_diameter(d[i]);
-      hb[i] = (c->cfg.model != ABS_MODEL_NONE && (!mask || mask[i])) ? 1 : 0;
-    }
-    unsigned long long maxuid = n;
-    if (uid) {
-      hu.assign(uid, uid + n);
-      for (unsigned long long u : hu) maxuid = std::max(maxuid, u + 1);
-    } else {
-      hu.resize(n);
-      for (unsigned long long i = 0; i < n; ++i) hu[i] = i;
-    }
-    uid_count = std::max(uid_count, maxuid);
-    if (uid_count + 1 > c->uid_cap) {
-      rc = ensure_capacity(c, uid_count, 0);
-      if (rc) return rc;
-    }
-    hf.assign(n, 0);
-    if (flags) hf.assign(flags, flags + n);
-    hpart.assign(n, 0);
-    if (partners) hpart.assign(partners, partners + n);
-    CK(cudaMemcpyAsync(c->newpd, hp.data(), n * sizeof(Pd), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(S.uid, hu.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(S.vol, hv.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(S.beh, hb.data(), n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(S.flags, hf.data(), n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(S.partners, hpart.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
-  } else {
-    // device-resident inputs: interleave on the device
-    std::vector<unsigned long long> dummy;
-    if (uid_count < n) uid_count = n;
-    if (uid_count + 1 > c->uid_cap) {
-      rc = ensure_capacity(c, uid_count, 0);
-      if (rc) return rc;
-    }
-    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 0, sizeof(Pd), x, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 8, sizeof(Pd), y, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 16, sizeof(Pd), z, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(c->newpd) + 24, sizeof(Pd), d, 8, 8, n, cudaMemcpyDeviceToDevice, c->stream));
-    if (uid) {
-      CK(cudaMemcpyAsync(S.uid, uid, n * 8, cudaMemcpyDeviceToDevice, c->stream));
-    } else {
-      hu.resize(n);
-      for (unsigned long long i = 0; i < n; ++i) hu[i] = i;
-      CK(cudaMemcpyAsync(S.uid, hu.data(), n * 8, cudaMemcpyHostToDevice, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-    }
-    if (mask) CK(cudaMemcpyAsync(S.beh, mask, n, cudaMemcpyDeviceToDevice, c->stream));
-    else CK(cudaMemsetAsync(S.beh, c->cfg.model != ABS_MODEL_NONE ? 1 : 0, n, c->stream));
-    CK(cudaMemsetAsync(S.flags, 0, n, c->stream));
-    CK(cudaMemsetAsync(S.partners, 0, n * 4, c->stream));
-    CK(cudaMemsetAsync(S.vol, 0, n * 8, c->stream));
+  if (uid && host) {
+    for (unsigned long long i = 0; i < n; ++i) uid_count = std::max<unsigned long long>(uid_count, uid[i] + 1);
   }
+  uid_count = std::max<unsigned long long>(uid_count, n);
+  int rc = ensure_capacity(c, std::max<unsigned long long>({c->cap, 2 * n + 1024, uid_count}), 0);
+  if (rc) return rc;
+  Soa& S = c->S[c->cur];
+  const double *dx = x, *dy = y, *dz = z, *dd = d;
+  const unsigned char* dmask = mask;
+  if (host && n) {  // contiguous H2D into the staging area, interleaved on the device
+    double* st = reinterpret_cast<double*>(c->st_pd);
+    CK(cudaMemcpyAsync(st, x, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(st + n, y, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(st + 2 * n, z, n * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(st + 3 * n, d, n * 8, cudaMemcpyHostToDevice, c->stream));
+    dx = st; dy = st + n; dz = st + 2 * n; dd = st + 3 * n;
+    if (mask) {
+      CK(cudaMemcpyAsync(c->key, mask, n, cudaMemcpyHostToDevice, c->stream));
+      dmask = reinterpret_cast<const unsigned char*>(c->key);
+    }
+  }
+  if (uid) CK(cudaMemcpyAsync(S.uid, uid, n * 8, kind, c->stream));
+  if (volume) CK(cudaMemcpyAsync(S.vol, volume, n * 8, kind, c->stream));
+  if (flags) CK(cudaMemcpyAsync(S.flags, flags, n, kind, c->stream));
+  else CK(cudaMemsetAsync(S.flags, 0, n, c->stream));
+  if (partners) CK(cudaMemcpyAsync(S.partners, partners, n * 4, kind, c->stream));
+  else CK(cudaMemsetAsync(S.partners, 0, n * 4, c->stream));
   CK(cudaMemsetAsync(S.force, 0, 3 * c->cap * 8, c->stream));
   DevGrid h{};
   h.red[0] = h.red[1] = h.red[2] = kInfOrdLo;
@@ -1777,12 +1763,27 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   h.n = n;
   h.uid_count = uid_count;
   CK(cudaMemcpyAsync(c->g, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  if (n) {
+    k_ingest<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr,
+                                                            volume == nullptr, c->cfg.model != ABS_MODEL_NONE,
+                                                            c->newpd, S, c->g);
+    ++c->launches;
+  }
   if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  unsigned int bad = 0;
+  CK(cudaMemcpyAsync(&bad, &c->g->bad_input, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->pos_in_new = true;
   c->grid_valid = false;
-  c->n = n;
   c->iteration = 0;
+  if (bad) {
+    c->n = 0;
+    CK(cudaMemsetAsync(&c->g->n, 0, 8, c->stream));
+    CK(cudaMemsetAsync(&c->g->bad_input, 0, 4, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "diameter must be > 0");
+  }
+  c->n = n;
   return ABS_OK;
 }
 
@@ -1893,8 +1894,16 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
   if (n_out) *n_out = n;
   Soa& S = c->S[c->cur];
   if (x || y || z || d) {
-    std::vector<Pd> hp(n);
-    CK(cudaMemcpy(hp.data(), cur_pos(c), n * sizeof(Pd), cudaMemcpyDeviceToHost));
+    if (c->pinned_bytes < n * sizeof(Pd)) {
+      if (c->pinned) cudaFreeHost(c->pinned);
+      c->pinned = nullptr;
+      c->pinned_bytes = 0;
+      CK(cudaMallocHost(&c->pinned, std::max<size_t>(n * sizeof(Pd), 1)));
+      c->pinned_bytes = std::max<size_t>(n * sizeof(Pd), 1);
+    }
+    Pd* hp = static_cast<Pd*>(c->pinned);
+    CK(cudaMemcpyAsync(hp, cur_pos(c), n * sizeof(Pd), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     for (unsigned long long i = 0; i < n; ++i) {
       if (x) x[i] = hp[i].x;
       if (y) y[i] = hp[i].y;

@@ -46,6 +46,8 @@ struct DevGrid {
   unsigned long long red[7];  // ordered-int min(x,y,z), max(x,y,z), max(d)
   unsigned int nonfinite;
   int err;
+  unsigned int bad_input;  // set by k_ingest on a diameter <= 0
+  unsigned int pad0;
   unsigned long long failed_iteration;
   double origin[3];
   double box;

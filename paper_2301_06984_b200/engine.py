@@ -254,6 +254,15 @@ class Simulation:
             _p(out["volume"], C.c_double)), self._ctx)
         return out
 
+    def positions(self, x, y, z) -> int:
+        """Download positions into caller-owned float64 arrays (e.g. pinned);
+        returns the agent count (device storage order)."""
+        nn = C.c_uint64(0)
+        N.check(N.load().abs_gpu_download(self._ctx, C.byref(nn), None, _p(x, C.c_double),
+                                          _p(y, C.c_double), _p(z, C.c_double), None, None, None,
+                                          None, None, None, None), self._ctx)
+        return int(nn.value)
+
     # -- timing of the dominant kernel --------------------------------------
     def reset_timers(self, enable: bool = True):
         N.check(N.load().abs_gpu_reset_timers(self._ctx, 1 if enable else 0), self._ctx)
