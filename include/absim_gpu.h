@@ -56,6 +56,7 @@ extern "C" {
 #define ABS_FLAG_NEWLY_ADDED 8u
 #define ABS_FLAG_NEIGHBOR_VIOLATION 16u
 #define ABS_FLAG_NEW_NEIGHBOR 32u
+#define ABS_FLAG_GHOST 128u /* multi-domain halo copy: a candidate, never stepped */
 
 /* device behaviour models (BASELINE configs; models.hpp:69-83 for GROW) */
 #define ABS_MODEL_NONE 0
@@ -114,6 +115,14 @@ int abs_gpu_upload(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const doub
 int abs_gpu_upload_device(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
                           const double* y, const double* z, const double* d,
                           const uint8_t* behaviour_mask, uint64_t uid_count);
+
+/* Multi-domain: force the grid computed over all ranks
+ * (grid[0..2] origin, grid[3] box length, grid[4] largest diameter; dims)
+ * instead of the local bounds; grid == NULL restores the local grid. */
+int abs_gpu_set_grid_override(abs_gpu_ctx* ctx, const double* grid, const uint32_t* dims);
+/* Local bounds of the current population: out[0..2] min xyz, out[3..5]
+ * max xyz, out[6] largest diameter (uniform_grid.cpp:170-206 pass 1). */
+int abs_gpu_local_bounds(abs_gpu_ctx* ctx, double* out7);
 
 /* Set the global iteration counter (checkpoint resume / teacher forcing;
  * the counter drives frequency gating and the RNG counters, simulation.hpp:117-121). */

@@ -39,6 +39,7 @@
 #define F_NVIOL 16u
 #define F_NNEW 32u
 #define F_SELF_FORCE 64u
+#define F_GHOST 128u /* halo copy owned by another rank: candidate only */
 
 static char g_err[512];
 const char* orc_last_error(void) { return g_err; }
@@ -77,6 +78,9 @@ typedef struct {
   uint64_t* head;
   uint64_t* succ;
   uint32_t* count;
+  int grid_override;
+  double ov_grid[5];
+  uint32_t ov_dims[3];
   /* staged additions */
   uint64_t nstage, stage_cap;
   uint64_t* s_uid;
@@ -135,6 +139,26 @@ orc_sim* orc_create(const orc_params* p, uint64_t n, const double* x, const doub
   return s;
 }
 
+/* Replace the population with a full state (uids, flags incl. F_GHOST,
+ * partners, volume, behaviour mask) — teacher forcing and multi-domain. */
+int orc_load(orc_sim* s, uint64_t n, const uint64_t* uid, const double* x, const double* y,
+             const double* z, const double* d, const uint8_t* flags, const uint32_t* partners,
+             const double* vol, const uint8_t* beh, uint64_t uid_count, uint64_t iteration) {
+  reserve(s, n);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!(d[i] > 0.0)) return fail("diameter must be > 0");
+    init_slot(s, i, uid[i], x[i], y[i], z[i], d[i], beh ? beh[i] : 0, vol ? vol[i] : 0.0,
+              flags ? flags[i] : 0);
+    if (partners) s->partners[i] = partners[i];
+  }
+  s->n = n;
+  s->uid_counter = uid_count;
+  s->iteration = iteration;
+  s->indexed = 0;
+  s->nstage = 0;
+  return 0;
+}
+
 void orc_destroy(orc_sim* s) {
   if (!s) return;
   free(s->uid); free(s->x); free(s->y); free(s->z); free(s->d); free(s->tx);
@@ -165,6 +189,17 @@ static uint64_t box_index_of(const orc_sim* s, double px, double py, double pz) 
 static double smin(double a, double b) { return b < a ? b : a; }
 static double smax(double a, double b) { return a < b ? b : a; }
 
+/* Multi-domain support: force the global grid (origin[3], box, dmax) and
+ * dims computed over all ranks; grid == NULL clears it. */
+int orc_set_grid_override(orc_sim* s, const double* grid, const uint32_t* dims) {
+  s->grid_override = grid != NULL;
+  if (grid) {
+    for (int k = 0; k < 5; ++k) s->ov_grid[k] = grid[k];
+    for (int k = 0; k < 3; ++k) s->ov_dims[k] = dims[k];
+  }
+  return 0;
+}
+
 /* uniform_grid.cpp:155-266 with one worker */
 int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) {
   s->indexed = s->n;
@@ -187,8 +222,17 @@ int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) 
     }
     for (int k = 0; k < 3; ++k)
       if (!isfinite(lo[k]) || !isfinite(hi[k])) return fail("agent positions are not finite");
+    if (s->grid_override) { /* multi-domain: the global grid of all ranks */
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = s->ov_grid[k];
+        s->dims[k] = s->ov_dims[k];
+      }
+      dm = s->ov_grid[4];
+    }
     s->dmax = dm;
-    if (s->p.fixed_box > 0.0) {
+    if (s->grid_override) {
+      s->box = s->ov_grid[3];
+    } else if (s->p.fixed_box > 0.0) {
       if (dm > s->p.fixed_box) return fail("fixed box length is smaller than the largest agent diameter");
       s->box = s->p.fixed_box;
     } else {
@@ -197,8 +241,10 @@ int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) 
     uint64_t needed = 1;
     for (int k = 0; k < 3; ++k) {
       s->origin[k] = lo[k];
-      uint64_t nk = (uint64_t)floor((hi[k] - lo[k]) / s->box) + 1;
-      s->dims[k] = (uint32_t)(nk < 1 ? 1 : nk);
+      if (!s->grid_override) {
+        uint64_t nk = (uint64_t)floor((hi[k] - lo[k]) / s->box) + 1;
+        s->dims[k] = (uint32_t)(nk < 1 ? 1 : nk);
+      }
       needed *= s->dims[k];
     }
     if (needed > (1ull << 31)) return fail("grid would exceed the box budget");
@@ -370,6 +416,7 @@ static void force_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
 
 /* simulation.cpp:463-489 */
 static int run_forces(orc_sim* s, uint64_t i) {
+  if (s->flags[i] & F_GHOST) return 0;
   if (s->p.detect_static && (s->flags[i] & F_STATIC)) {
     s->skips++;
     return 0;
@@ -391,6 +438,7 @@ static int run_forces(orc_sim* s, uint64_t i) {
 
 /* agent.hpp:115-133 */
 static void apply_pending(orc_sim* s, uint64_t i) {
+  if (s->flags[i] & F_GHOST) return;
   double tx = s->tx[i], ty = s->ty[i], tz = s->tz[i];
   const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
   if (disp > 0.0) {
@@ -421,7 +469,8 @@ static void mark_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
 static int run_staticness(orc_sim* s) {
   const uint8_t reset = F_MOVED | F_GREW | F_SELF_FORCE | F_NEWLY_ADDED | F_NVIOL | F_NNEW;
   if (s->iteration == 0) {
-    for (uint64_t i = 0; i < s->n; ++i) s->flags[i] &= (uint8_t)~(reset | F_STATIC);
+    for (uint64_t i = 0; i < s->n; ++i)
+      if (!(s->flags[i] & F_GHOST)) s->flags[i] &= (uint8_t)~(reset | F_STATIC);
     return 0;
   }
   for (uint64_t i = 0; i < s->n; ++i) {
@@ -433,6 +482,7 @@ static int run_staticness(orc_sim* s) {
     if (for_each_neighbor(s, i, s->x[i], s->y[i], s->z[i], r * r, mark_visit, &m)) return -1;
   }
   for (uint64_t i = 0; i < s->n; ++i) {
+    if (s->flags[i] & F_GHOST) continue;
     const int skip = !(s->flags[i] & (F_MOVED | F_GREW | F_SELF_FORCE | F_NEWLY_ADDED | F_NVIOL | F_NNEW)) &&
                      s->partners[i] <= 1;
     s->flags[i] = (uint8_t)((s->flags[i] & ~(reset | F_STATIC)) | (skip ? F_STATIC : 0));
@@ -460,7 +510,7 @@ static void stage_daughter(orc_sim* s, double x, double y, double z, double d, d
 }
 
 static int run_behaviour(orc_sim* s, uint64_t i) {
-  if (!s->beh[i]) return 0;
+  if (!s->beh[i] || (s->flags[i] & F_GHOST)) return 0;
   const orc_params* p = &s->p;
   if (p->model == 1) {
     s->vol[i] += p->mp[0];
@@ -752,7 +802,7 @@ int orc_dump(const orc_sim* s, uint64_t* uid, double* x, double* y, double* z, d
     if (fy) fy[i] = s->fy[i];
     if (fz) fz[i] = s->fz[i];
     if (partners) partners[i] = s->partners[i];
-    if (flags) flags[i] = (uint8_t)(s->flags[i] & 63u);
+    if (flags) flags[i] = (uint8_t)(s->flags[i] & (63u | F_GHOST));
     if (vol) vol[i] = s->vol[i];
   }
   return 0;

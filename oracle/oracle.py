@@ -26,6 +26,7 @@ REFERENCE_SRC = "/root/reference/proj/src"
 MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW = 0, 1, 2, 3
 
 F_STATIC, F_MOVED, F_GREW, F_NEWLY_ADDED, F_NVIOL, F_NNEW = 1, 2, 4, 8, 16, 32
+F_GHOST = 128
 
 
 class _Params(C.Structure):
@@ -268,6 +269,9 @@ class PortSim(_Sim):
             d = _LibDict(C.CDLL(PORT_SO))
             _bind(d, "orc_", False)
             d["orc_remove"].argtypes = [C.c_void_p, _U32, C.c_uint32]
+            d["orc_set_grid_override"].argtypes = [C.c_void_p, _D, _U32]
+            d["orc_load"].argtypes = [C.c_void_p, C.c_uint64, _U64, _D, _D, _D, _D, _U8, _U32, _D, _U8,
+                                      C.c_uint64, C.c_uint64]
             d["orc_morton_encode3"].argtypes = [C.c_uint32] * 3 + [_U64]
             d["orc_morton_decode3"].argtypes = [C.c_uint64, _U32]
             d["orc_offsets_table"].restype = C.c_int64
@@ -279,6 +283,29 @@ class PortSim(_Sim):
 
     def _counts(self, out):
         self._check(self.lib()["orc_counts"](self.h, _ptr(out, C.c_uint64)))
+
+    def set_grid_override(self, grid=None, dims=None):
+        """Force the global grid (origin[3], box, dmax) + dims; None clears."""
+        if grid is None:
+            self._check(self.lib()["orc_set_grid_override"](self.h, None, None))
+            return
+        g = np.ascontiguousarray(grid, np.float64)
+        dm = np.ascontiguousarray(dims, np.uint32)
+        self._check(self.lib()["orc_set_grid_override"](self.h, _ptr(g, C.c_double), _ptr(dm, C.c_uint32)))
+
+    def load(self, st: dict, uid_count: int, iteration: int):
+        """Replace the population with a full state dict (dump() layout + 'beh')."""
+        n = len(st["x"])
+        a = {k: np.ascontiguousarray(st[k]) for k in ("x", "y", "z", "d")}
+        uid = np.ascontiguousarray(st["uid"], np.uint64)
+        fl = np.ascontiguousarray(st["flags"], np.uint8)
+        pa = np.ascontiguousarray(st["partners"], np.uint32)
+        vo = np.ascontiguousarray(st["volume"], np.float64)
+        be = np.ascontiguousarray(st.get("beh", np.zeros(n, np.uint8)), np.uint8)
+        self._check(self.lib()["orc_load"](self.h, n, _ptr(uid, C.c_uint64),
+                                           *(_ptr(a[k], C.c_double) for k in ("x", "y", "z", "d")),
+                                           _ptr(fl, C.c_uint8), _ptr(pa, C.c_uint32), _ptr(vo, C.c_double),
+                                           _ptr(be, C.c_uint8), uid_count, iteration))
 
     def remove(self, slots):
         s = np.ascontiguousarray(slots, dtype=np.uint32)

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -127,13 +128,19 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
       lo[k] = ord_dec(g->red[k]);
       hi[k] = ord_dec(g->red[3 + k]);
     }
-    const double dm = ord_dec(g->red[6]);
+    double dm = ord_dec(g->red[6]);
     for (int k = 0; k < 3; ++k)
       if (!isfinite(lo[k]) || !isfinite(hi[k])) err = kErrNonFinite;
     if (g->nonfinite) err = kErrNonFinite;
+    if (g->ov_on) {  // multi-domain: grid of all ranks
+      for (int k = 0; k < 3; ++k) lo[k] = g->ov_grid[k];
+      dm = g->ov_grid[4];
+    }
     g->dmax = dm;
     if (err == kErrNone) {
-      if (fixed_box > 0.0) {
+      if (g->ov_on) {
+        g->box = g->ov_grid[3];
+      } else if (fixed_box > 0.0) {
         if (dm > fixed_box) err = kErrFixedBox;
         g->box = fixed_box;
       } else {
@@ -146,7 +153,7 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
         g->origin[k] = lo[k];
         const unsigned long long nk =
             static_cast<unsigned long long>(floor((hi[k] - lo[k]) / g->box)) + 1ull;
-        g->dims[k] = static_cast<unsigned int>(nk < 1 ? 1 : nk);
+        g->dims[k] = g->ov_on ? g->ov_dims[k] : static_cast<unsigned int>(nk < 1 ? 1 : nk);
         needed *= g->dims[k];
       }
       if (needed > (1ull << 31)) err = kErrBoxBudget;
@@ -404,6 +411,8 @@ __device__ __noinline__ void coincident_force(unsigned long long ua, unsigned lo
   *f2 = d2 * m;
 }
 
+constexpr unsigned char kFlagGhost = 128u;  // ABS_FLAG_GHOST
+
 // Outputs of one agent's step that need warp-level cooperation afterwards.
 struct Daughter {
   bool divides;
@@ -426,6 +435,15 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
   dg.parent = my_uid;
+  if (fl & kFlagGhost) {  // halo copy of another rank's agent: candidate only
+    if (STATIC) {
+      nv[i] = 0;
+      nn[i] = 0;
+    }
+    reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
+    reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
+    return dg;
+  }
   // --- staticness phase 2 (simulation.cpp:375-384) -----------------------
   if (STATIC) {
     if (a.iteration == 0) {
@@ -1762,7 +1780,7 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   h.B[0] = h.B[1] = h.B[2] = 1;
   h.n = n;
   h.uid_count = uid_count;
-  CK(cudaMemcpyAsync(c->g, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->g, &h, offsetof(DevGrid, ov_on), cudaMemcpyHostToDevice, c->stream));
   if (n) {
     k_ingest<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr,
                                                             volume == nullptr, c->cfg.model != ABS_MODEL_NONE,
@@ -1857,6 +1875,46 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   return ABS_OK;
 }
 
+int abs_gpu_set_grid_override(abs_gpu_ctx* c, const double* grid, const uint32_t* dims) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  struct { int on; int pad; double g[5]; unsigned int d[3]; } ov{};
+  ov.on = grid != nullptr;
+  if (grid) {
+    if (!dims) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "grid override needs dims");
+    for (int k = 0; k < 5; ++k) ov.g[k] = grid[k];
+    for (int k = 0; k < 3; ++k) ov.d[k] = dims[k];
+    if (!(grid[3] > 0.0) || !dims[0] || !dims[1] || !dims[2])
+      return set_err(c, ABS_ERR_INVALID_ARGUMENT, "bad grid override");
+  }
+  CK(cudaMemcpyAsync(&c->g->ov_on, &ov.on, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->g->ov_grid, ov.g, sizeof ov.g, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->g->ov_dims, ov.d, sizeof ov.d, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
+int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
+  if (!c || !out7) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
+  ++c->launches;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  for (int k = 0; k < 7; ++k) {
+    const unsigned long long o = h.red[k];
+    const unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+    std::memcpy(&out7[k], &b, 8);
+  }
+  const unsigned long long reset[7] = {kInfOrdLo, kInfOrdLo, kInfOrdLo, kInfOrdHi, kInfOrdHi, kInfOrdHi, kZeroOrd};
+  CK(cudaMemcpyAsync(c->g->red, reset, sizeof reset, cudaMemcpyHostToDevice, c->stream));
+  const unsigned int zero = 0;
+  CK(cudaMemcpyAsync(&c->g->nonfinite, &zero, 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (h.nonfinite) return set_err(c, ABS_ERR_NONFINITE, "agent positions are not finite");
+  return ABS_OK;
+}
+
 int abs_gpu_set_iteration(abs_gpu_ctx* c, uint64_t iteration) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   c->iteration = iteration;
@@ -1918,7 +1976,7 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
   if (partners) CK(cudaMemcpy(partners, S.partners, n * 4, cudaMemcpyDeviceToHost));
   if (flags) {
     CK(cudaMemcpy(flags, S.flags, n, cudaMemcpyDeviceToHost));
-    for (unsigned long long i = 0; i < n; ++i) flags[i] &= 63u;
+    for (unsigned long long i = 0; i < n; ++i) flags[i] &= (63u | ABS_FLAG_GHOST);
   }
   if (volume) {
     CK(cudaMemcpy(volume, S.vol, n * 8, cudaMemcpyDeviceToHost));

@@ -47,7 +47,10 @@ struct DevGrid {
   unsigned int nonfinite;
   int err;
   unsigned int bad_input;  // set by k_ingest on a diameter <= 0
-  unsigned int pad0;
+  int ov_on;               // multi-domain: use the global grid below
+  double ov_grid[5];       // origin[3], box, dmax over all ranks
+  unsigned int ov_dims[3];
+  unsigned int pad1;
   unsigned long long failed_iteration;
   double origin[3];
   double box;

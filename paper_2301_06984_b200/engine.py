@@ -207,6 +207,22 @@ class Simulation:
     def simulate(self, iterations: int) -> None:
         N.check(N.load().abs_gpu_simulate(self._ctx, iterations), self._ctx)
 
+    def set_grid_override(self, grid=None, dims=None) -> None:
+        """Multi-domain: force the grid of all ranks (origin[3], box, dmax; dims)."""
+        if grid is None:
+            N.check(N.load().abs_gpu_set_grid_override(self._ctx, None, None), self._ctx)
+            return
+        g = np.ascontiguousarray(grid, np.float64)
+        dm = np.ascontiguousarray(dims, np.uint32)
+        N.check(N.load().abs_gpu_set_grid_override(self._ctx, _p(g, C.c_double), _p(dm, C.c_uint32)),
+                self._ctx)
+
+    def local_bounds(self) -> np.ndarray:
+        """[min x, min y, min z, max x, max y, max z, max d] of the population."""
+        out = np.zeros(7)
+        N.check(N.load().abs_gpu_local_bounds(self._ctx, _p(out, C.c_double)), self._ctx)
+        return out
+
     def set_iteration(self, iteration: int) -> None:
         N.check(N.load().abs_gpu_set_iteration(self._ctx, iteration), self._ctx)
 
