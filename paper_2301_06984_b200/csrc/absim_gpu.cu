@@ -185,6 +185,7 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
     }
   }
   reset_reduction(g);
+  g->work = 0;
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kThreads) k_key(const Pd* __restrict__ pos, co
     const unsigned int by = bin_coord(p.y, G.origin[1], G, 1);
     const unsigned int bz = bin_coord(p.z, G.origin[2], G, 2);
     const unsigned int b = bx + G.bd[0] * (by + G.bd[1] * bz);
+    ABS_ASSERT(b < G.nbins);
     key[i] = b;
     rank[i] = atomicAdd(count + b, 1u);
   }
@@ -332,6 +334,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned int j = __ldg(start + key[i]) + rank[i];
+    ABS_ASSERT(j < n);
     const Pd p = load_pd(pos + i);
     reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
@@ -636,8 +639,15 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
   const unsigned long long n = gp->n;
   const double dmax = gp->dmax;
   unsigned long long n_eval = 0, n_skip = 0;
-  for (unsigned long long base = blockIdx.x * (unsigned long long)blockDim.x; base < n;
-       base += (unsigned long long)gridDim.x * blockDim.x) {
+  __shared__ unsigned long long chunk;
+  // Persistent CTAs claim consecutive chunks: the agent array (cell order) is
+  // swept once, front to back, so each neighbourhood is fetched from HBM once.
+  while (true) {
+    if (threadIdx.x == 0) chunk = atomicAdd(&gw->work, 1ull);
+    __syncthreads();
+    const unsigned long long base = chunk * blockDim.x;
+    __syncthreads();
+    if (base >= n) break;
     const unsigned long long i = base + threadIdx.x;
     Daughter dg{false, 0, 0, 0, 0, 0, 0};
     if (i < n) {
@@ -1377,10 +1387,10 @@ int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
 }
 
-int force_blocks(const abs_gpu_ctx* c) {
-  const unsigned long long b = (c->cap + kForceThreads - 1) / kForceThreads;
-  const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 16;
-  return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
+int force_blocks(const abs_gpu_ctx* c) {  // persistent: the resident CTAs only
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<ABS_MODEL_NONE, false, false>, kForceThreads, 0);
+  return c->sms * std::max(per_sm, 1);
 }
 
 template <class T>
@@ -1431,6 +1441,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
       CK(cudaMemcpyAsync(dst.force + q * ncap, src.force + q * c->cap, keep * 8, cudaMemcpyDeviceToDevice,
                          c->stream));
   }
+  if (c->grid_valid && c->start) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   free_soa(c->S[0]);
   free_soa(c->S[1]);
@@ -1787,7 +1798,8 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
                                                             c->newpd, S, c->g);
     ++c->launches;
   }
-  if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  // the cell table is a counter array between iterations: always start clean
+  CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
   unsigned int bad = 0;
   CK(cudaMemcpyAsync(&bad, &c->g->bad_input, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));

@@ -19,6 +19,13 @@
 
 #include "absim_models.h"
 
+#ifdef ABS_DEBUG
+#include <cassert>
+#define ABS_ASSERT(c) assert(c)
+#else
+#define ABS_ASSERT(c) ((void)0)
+#endif
+
 namespace absgpu {
 
 constexpr int kThreads = 256;
@@ -47,10 +54,7 @@ struct DevGrid {
   unsigned int nonfinite;
   int err;
   unsigned int bad_input;  // set by k_ingest on a diameter <= 0
-  int ov_on;               // multi-domain: use the global grid below
-  double ov_grid[5];       // origin[3], box, dmax over all ranks
-  unsigned int ov_dims[3];
-  unsigned int pad1;
+  unsigned long long work;  // chunk counter of the persistent force kernel (reset by k_finalize)
   unsigned long long failed_iteration;
   double origin[3];
   double box;
@@ -70,6 +74,12 @@ struct DevGrid {
   unsigned long long skips;
   unsigned long long added;
   unsigned long long removed;
+  // --- kept across uploads (abs_gpu_upload copies everything above) ---
+  int ov_on;               // multi-domain: use the global grid below
+  int pad1;
+  double ov_grid[5];       // origin[3], box, dmax over all ranks
+  unsigned int ov_dims[3];
+  unsigned int pad2;
 };
 
 struct StepArgs {
@@ -267,8 +277,10 @@ __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd*
       const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
       const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
       const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      ABS_ASSERT(x0 >= 0 && x1 + 1 <= (int)g.bd[0] && by >= 0 && bz >= 0 && by < (int)g.bd[1] && bz < (int)g.bd[2]);
       const unsigned int j0 = __ldg(start + row + x0);
       const unsigned int j1 = __ldg(start + row + x1 + 1);
+      ABS_ASSERT(j0 <= j1);
       if (j1 <= j0) continue;
       if (nw < kMaxRows) {
         wj0[nw][t] = j0;

@@ -357,3 +357,16 @@ def test_grid_growth_retry(engine, oracle_mod):
         orc.simulate(10)
         compare_state(sim.agents(), orc.dump(), ints=False, what="spreading")
     assert sim.environment().dims().prod() > 4 * 4 * 4
+
+
+def test_reupload_with_growing_population(engine, oracle_mod):
+    """Re-uploading a larger population (capacity regrowth) after a step must
+    not leak the previous cell table into the next binning."""
+    wl = CF.c1_relaxation(3000, seed=1)
+    sim = _gpu(engine, wl.params, None, 2)
+    for n in (600, 1500, 3000):
+        sim.add_agents(wl.x[:n], wl.y[:n], wl.z[:n], wl.d[:n])
+        sim.simulate(2)
+        orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x[:n], wl.y[:n], wl.z[:n], wl.d[:n])
+        orc.simulate(2)
+        compare_state(sim.agents(), orc.dump(), what=f"reupload n={n}")
