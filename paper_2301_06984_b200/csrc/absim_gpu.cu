@@ -631,24 +631,25 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
             unsigned int* __restrict__ div_mark) {
   if (gp->err) return;
   __shared__ QGrid Q;
-  __shared__ unsigned int wj0[kMaxRows][kForceThreads];
-  __shared__ unsigned int wj1[kMaxRows][kForceThreads];
-  __shared__ unsigned int ovl[kMaxContacts][kForceThreads];
+  extern __shared__ __align__(16) unsigned int force_smem[];
+  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
+  auto wj1 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + 2 * kMaxRows * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
   const unsigned long long n = gp->n;
   const double dmax = gp->dmax;
   unsigned long long n_eval = 0, n_skip = 0;
-  __shared__ unsigned long long chunk;
-  // Persistent CTAs claim consecutive chunks: the agent array (cell order) is
-  // swept once, front to back, so each neighbourhood is fetched from HBM once.
+  // Persistent warps claim consecutive 32-agent chunks: the agent array (cell
+  // order) is swept once, front to back, and no warp waits for another.
+  const int lane = threadIdx.x & 31;
   while (true) {
-    if (threadIdx.x == 0) chunk = atomicAdd(&gw->work, 1ull);
-    __syncthreads();
-    const unsigned long long base = chunk * blockDim.x;
-    __syncthreads();
+    unsigned long long chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&gw->work, 1ull);
+    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+    const unsigned long long base = chunk * 32ull;
     if (base >= n) break;
-    const unsigned long long i = base + threadIdx.x;
+    const unsigned long long i = base + lane;
     Daughter dg{false, 0, 0, 0, 0, 0, 0};
     if (i < n) {
       const Pd me = load_pd(S.pd + i);
@@ -1389,7 +1390,10 @@ int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
 
 int force_blocks(const abs_gpu_ctx* c) {  // persistent: the resident CTAs only
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<ABS_MODEL_NONE, false, false>, kForceThreads, 0);
+  cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<ABS_MODEL_NONE, false, false>, kForceThreads,
+                                                (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
   return c->sms * std::max(per_sm, 1);
 }
 
@@ -1570,6 +1574,19 @@ bool use_tile_kernel() {
   return v != 0;
 }
 
+constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
+
+template <int MODEL, bool STATIC, bool RECORD>
+void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+  static bool configured = false;  // per template instance
+  if (!configured) {
+    cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kForceSmem);
+    configured = true;
+  }
+  k_force<MODEL, STATIC, RECORD><<<force_blocks(c), kForceThreads, kForceSmem, c->stream>>>(
+      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+}
+
 template <int MODEL, bool STATIC>
 void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
   if (use_tile_kernel()) {
@@ -1577,13 +1594,8 @@ void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
     else launch_tile<MODEL, STATIC, false>(c, S, a);
     return;
   }
-  const int nb = force_blocks(c);
-  if (c->cfg.record_forces)
-    k_force<MODEL, STATIC, true><<<nb, kForceThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a,
-                                                                c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
-  else
-    k_force<MODEL, STATIC, false><<<nb, kForceThreads, 0, c->stream>>>(S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a,
-                                                                 c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+  if (c->cfg.record_forces) launch_gather<MODEL, STATIC, true>(c, S, a);
+  else launch_gather<MODEL, STATIC, false>(c, S, a);
 }
 
 template <int MODEL>
