@@ -49,6 +49,8 @@ def _workload(name, n=None, seed=0):
         return CF.c2_proliferation(side=16 if n is None else round(n ** (1 / 3)), seed=seed)
     if name == "c3":
         return CF.c3_spheroid(n or (1 << 23), seed)
+    if name == "c5":
+        return CF.c5_sir(n or 10_000_000, seed)
     return CF.c4_large_uniform(n or (1 << 26), seed)
 
 
@@ -107,8 +109,8 @@ def _dist():
     return dist, world, rank, local
 
 
-CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22}
-CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12}
+CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22, "c5": 1 << 21}
+CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12, "c5": 10}
 
 
 def _ref_sim(wl_name, sample_n, threads):
@@ -122,6 +124,8 @@ def _ref_sim(wl_name, sample_n, threads):
                        model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
                        sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0)
     try:
+        if prm.get("model", 0) == 4:  # SIR: the reference has no periodic boundaries
+            raise FileNotFoundError("no reference path for config 5")
         return O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "reference", threads, wl
     except (FileNotFoundError, OSError):
         p.threads = 1
@@ -296,7 +300,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--bins", type=int, default=2, help="sub-bins per box edge along y, z")

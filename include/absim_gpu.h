@@ -63,6 +63,7 @@ extern "C" {
 #define ABS_MODEL_PROLIFERATION 1 /* mp[0] volume rate, mp[1] division volume */
 #define ABS_MODEL_DRIVE 2         /* mp[0..2] centre, mp[3] max speed */
 #define ABS_MODEL_GROW 3          /* mp[0] growth rate, mp[1] diameter cap */
+#define ABS_MODEL_SIR 4           /* mp[0] L (periodic cube), mp[1] radius, mp[2] step, mp[3] recovery, mp[4] p */
 
 typedef struct abs_gpu_ctx abs_gpu_ctx;
 
@@ -123,6 +124,11 @@ int abs_gpu_set_grid_override(abs_gpu_ctx* ctx, const double* grid, const uint32
 /* Local bounds of the current population: out[0..2] min xyz, out[3..5]
  * max xyz, out[6] largest diameter (uniform_grid.cpp:170-206 pass 1). */
 int abs_gpu_local_bounds(abs_gpu_ctx* ctx, double* out7);
+
+/* Config 5 (SIR): S/I/R counts after the last iteration, and the per-agent
+ * state (0 S, 1 I, 2 R) + infection iteration in download order. */
+int abs_gpu_sir_counts(abs_gpu_ctx* ctx, uint64_t* out3);
+int abs_gpu_sir_state(abs_gpu_ctx* ctx, uint8_t* state, uint32_t* t_infected);
 
 /* Set the global iteration counter (checkpoint resume / teacher forcing;
  * the counter drives frequency gating and the RNG counters, simulation.hpp:117-121). */

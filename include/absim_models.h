@@ -121,6 +121,44 @@ ABS_HD void abs_drive_delta(double px, double py, double pz, double cx, double c
   }
 }
 
+/* ---- config 5: SIR epidemic on a periodic cube (BASELINE configs[4]) ---
+ * The reference has no periodic boundaries; this model is
+ * defined here and checked between the C oracle and the kernels only.
+ * Per iteration, from the START-of-iteration states (double-buffered, so the
+ * agent loop order cannot leak into results):
+ *   k = #neighbours b != a in state I with minimum-image distance^2 <= r^2
+ *       (dx wrapped once into [-L/2, L/2], d2 = ((dx^2 + dy^2) + dz^2))
+ *   S -> I  if k > 0 and rng_word(seed, uid, SIR_INFECT(it)) < thr(k)
+ *           thr(k) = (u64)((1 - (1 - p)^k) * 2^64), (1-p)^k by repeated *
+ *   I -> R  if it - t_infected >= recovery
+ *   walk:   p += unit_vector(seed, uid, SIR_WALK(it)) * step, wrapped into [0, L)
+ * Initial state: I (t_infected = 0) iff u01(rng_word(seed, uid, 20)) < 0.01. */
+#define ABS_SIR_S 0
+#define ABS_SIR_I 1
+#define ABS_SIR_R 2
+#define ABS_RNG_SIR_INFECT(it) (((uint64_t)(it) << 8) | 0xfeull)
+#define ABS_RNG_SIR_WALK(it) ((uint64_t)(it) << 8)
+#define ABS_RNG_SIR_INIT 20ull
+
+ABS_HD uint64_t abs_sir_threshold(double p, unsigned int k) {
+  double q = 1.0;
+  for (unsigned int i = 0; i < k; ++i) q = q * (1.0 - p);
+  const double v = (1.0 - q) * 18446744073709551616.0;
+  return v >= 18446744073709551615.0 ? 0xFFFFFFFFFFFFFFFFull : (uint64_t)v;
+}
+
+ABS_HD double abs_min_image(double d, double L) {
+  if (d > 0.5 * L) return d - L;
+  if (d < -0.5 * L) return d + L;
+  return d;
+}
+
+ABS_HD double abs_wrap(double v, double L) {
+  if (v >= L) return v - L;
+  if (v < 0.0) return v + L;
+  return v;
+}
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,7 +129,9 @@ orc_sim* orc_create(const orc_params* p, uint64_t n, const double* x, const doub
       fail("diameter must be > 0");
       return NULL;
     }
-    const uint8_t b = (mask == NULL || mask[i]) && p->model != 0;
+    uint8_t b = (mask == NULL || mask[i]) && p->model != 0;
+    if (p->model == 4)  /* SIR: beh holds the state (absim_models.h) */
+      b = abs_u01(abs_rng_word(p->seed, i, ABS_RNG_SIR_INIT)) < 0.01 ? ABS_SIR_I : ABS_SIR_S;
     init_slot(s, i, i, x[i], y[i], z[i], d[i], b,
               p->model == 1 ? abs_volume_of_diameter(d[i]) : 0.0, 0);
   }
@@ -760,8 +762,96 @@ int orc_sort(orc_sim* s, uint64_t* moved) {
   return 0;
 }
 
+/* ---- config 5: SIR on a periodic cube (absim_models.h) -------------------
+ * States live in beh (0 S, 1 I, 2 R), infection iteration in partners.
+ * All decisions read start-of-iteration states and positions. */
+static uint64_t sir_counts[3];
+int orc_sir_counts(const orc_sim* s, uint64_t* out) {
+  (void)s;
+  out[0] = sir_counts[0]; out[1] = sir_counts[1]; out[2] = sir_counts[2];
+  return 0;
+}
+
+static int sir_step(orc_sim* s) {
+  const double L = s->p.mp[0], r = s->p.mp[1], step = s->p.mp[2], prob = s->p.mp[4];
+  const uint64_t rec = (uint64_t)s->p.mp[3];
+  uint32_t dims = (uint32_t)floor(L / r);
+  if (dims < 3) dims = 3;
+  const double box = L / (double)dims;
+  const uint64_t nb = (uint64_t)dims * dims * dims;
+  if (nb > s->box_cap) {
+    s->head = xrealloc(s->head, nb * sizeof *s->head);
+    s->count = xrealloc(s->count, nb * sizeof *s->count);
+    s->box_cap = nb;
+  }
+  for (uint64_t b = 0; b < nb; ++b) s->head[b] = ORC_NIL;
+  uint32_t* cb = malloc(3 * s->n * sizeof *cb + 1);
+  for (uint64_t i = 0; i < s->n; ++i) {
+    const double p[3] = {s->x[i], s->y[i], s->z[i]};
+    for (int k = 0; k < 3; ++k) {
+      int64_t c = (int64_t)floor(p[k] / box);
+      if (c < 0) c = 0;
+      if (c > (int64_t)dims - 1) c = dims - 1;
+      cb[3 * i + k] = (uint32_t)c;
+    }
+    const uint64_t b = cb[3 * i] + (uint64_t)dims * (cb[3 * i + 1] + (uint64_t)dims * cb[3 * i + 2]);
+    s->succ[i] = s->head[b];
+    s->head[b] = i;
+  }
+  uint8_t* ns = malloc(s->n + 1);
+  uint32_t* nt = malloc((s->n + 1) * sizeof *nt);
+  const double r2 = r * r;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    uint8_t st = s->beh[i];
+    uint32_t ti = s->partners[i];
+    if (st == ABS_SIR_I && s->iteration - ti >= rec) st = ABS_SIR_R;
+    if (st == ABS_SIR_S) {
+      unsigned int k = 0;
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            const uint64_t bx = (cb[3 * i] + dims + dx) % dims, by = (cb[3 * i + 1] + dims + dy) % dims,
+                           bz = (cb[3 * i + 2] + dims + dz) % dims;
+            for (uint64_t j = s->head[bx + dims * (by + (uint64_t)dims * bz)]; j != ORC_NIL; j = s->succ[j]) {
+              if (j == i || s->beh[j] != ABS_SIR_I) continue;
+              const double ddx = abs_min_image(s->x[i] - s->x[j], L);
+              const double ddy = abs_min_image(s->y[i] - s->y[j], L);
+              const double ddz = abs_min_image(s->z[i] - s->z[j], L);
+              if ((ddx * ddx + ddy * ddy) + ddz * ddz <= r2) ++k;
+            }
+          }
+      if (k > 0 && abs_rng_word(s->p.seed, s->uid[i], ABS_RNG_SIR_INFECT(s->iteration)) < abs_sir_threshold(prob, k)) {
+        st = ABS_SIR_I;
+        ti = (uint32_t)s->iteration;
+      }
+    }
+    ns[i] = st;
+    nt[i] = ti;
+  }
+  sir_counts[0] = sir_counts[1] = sir_counts[2] = 0;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    double dir[3];
+    abs_unit_vector(s->p.seed, s->uid[i], ABS_RNG_SIR_WALK(s->iteration), dir);
+    s->x[i] = abs_wrap(s->x[i] + dir[0] * step, L);
+    s->y[i] = abs_wrap(s->y[i] + dir[1] * step, L);
+    s->z[i] = abs_wrap(s->z[i] + dir[2] * step, L);
+    s->beh[i] = ns[i];
+    s->partners[i] = nt[i];
+    sir_counts[ns[i]]++;
+  }
+  free(cb); free(ns); free(nt);
+  return 0;
+}
+
 /* ---- schedule (simulation.cpp:222-322) --------------------------------- */
 int orc_simulate(orc_sim* s, uint64_t iterations) {
+  if (s->p.model == 4) {
+    for (uint64_t it = 0; it < iterations; ++it) {
+      if (sir_step(s)) return -1;
+      s->iteration++;
+    }
+    return 0;
+  }
   for (uint64_t it = 0; it < iterations; ++it) {
     if (orc_env_update(s, NULL, NULL, NULL)) return -1;
     if (s->p.sorting_frequency > 0 && s->iteration % s->p.sorting_frequency == 0) {
@@ -786,6 +876,14 @@ int orc_simulate(orc_sim* s, uint64_t iterations) {
 int orc_counts(const orc_sim* s, uint64_t* out) {
   out[0] = s->n; out[1] = s->uid_counter; out[2] = s->iteration; out[3] = s->evals;
   out[4] = s->skips; out[5] = s->added; out[6] = s->removed; out[7] = s->sorted;
+  return 0;
+}
+
+int orc_dump_beh(const orc_sim* s, uint8_t* beh, uint32_t* partners) {
+  for (uint64_t i = 0; i < s->n; ++i) {
+    beh[i] = s->beh[i];
+    partners[i] = s->partners[i];
+  }
   return 0;
 }
 

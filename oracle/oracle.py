@@ -23,7 +23,7 @@ REF_SO = os.path.join(HERE, "_ref", "libabsim_ref.so")
 PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
 REFERENCE_SRC = "/root/reference/proj/src"
 
-MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW = 0, 1, 2, 3
+MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3, 4
 
 F_STATIC, F_MOVED, F_GREW, F_NEWLY_ADDED, F_NVIOL, F_NNEW = 1, 2, 4, 8, 16, 32
 F_GHOST = 128
@@ -270,6 +270,8 @@ class PortSim(_Sim):
             _bind(d, "orc_", False)
             d["orc_remove"].argtypes = [C.c_void_p, _U32, C.c_uint32]
             d["orc_set_grid_override"].argtypes = [C.c_void_p, _D, _U32]
+            d["orc_dump_beh"].argtypes = [C.c_void_p, _U8, _U32]
+            d["orc_sir_counts"].argtypes = [C.c_void_p, _U64]
             d["orc_load"].argtypes = [C.c_void_p, C.c_uint64, _U64, _D, _D, _D, _D, _U8, _U32, _D, _U8,
                                       C.c_uint64, C.c_uint64]
             d["orc_morton_encode3"].argtypes = [C.c_uint32] * 3 + [_U64]
@@ -306,6 +308,19 @@ class PortSim(_Sim):
                                            *(_ptr(a[k], C.c_double) for k in ("x", "y", "z", "d")),
                                            _ptr(fl, C.c_uint8), _ptr(pa, C.c_uint32), _ptr(vo, C.c_double),
                                            _ptr(be, C.c_uint8), uid_count, iteration))
+
+    def sir_state(self):
+        """(state per agent [0 S, 1 I, 2 R], infection iteration), storage order."""
+        n = self.counts()["agents"]
+        st = np.zeros(n, np.uint8)
+        ti = np.zeros(n, np.uint32)
+        self._check(self.lib()["orc_dump_beh"](self.h, _ptr(st, C.c_uint8), _ptr(ti, C.c_uint32)))
+        return st, ti
+
+    def sir_counts(self):
+        out = np.zeros(3, np.uint64)
+        self._check(self.lib()["orc_sir_counts"](self.h, _ptr(out, C.c_uint64)))
+        return [int(v) for v in out]
 
     def remove(self, slots):
         s = np.ascontiguousarray(slots, dtype=np.uint32)

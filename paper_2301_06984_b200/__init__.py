@@ -6,4 +6,4 @@ include/absim_gpu.h for the C ABI every call goes through.
 """
 from .engine import Simulation, SimulationParams, SimulationReport, UniformGrid  # noqa: F401
 from ._native import (MODEL_DRIVE, MODEL_GROW, MODEL_NONE, MODEL_PROLIFERATION,  # noqa: F401
-                      AbsimError)
+                      MODEL_SIR, AbsimError)

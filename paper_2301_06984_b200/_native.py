@@ -22,14 +22,14 @@ ABS_ERR_CAPACITY = 6
 ABS_ERR_NO_DEVICE = 7
 ABS_ERR_STATE = 8
 
-MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW = 0, 1, 2, 3
+MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3, 4
 FLAG_GHOST = 128
 
 # every symbol include/absim_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "abs_gpu_default_config", "abs_gpu_create", "abs_gpu_destroy", "abs_gpu_last_error",
     "abs_gpu_upload", "abs_gpu_upload_device", "abs_gpu_set_grid_override", "abs_gpu_local_bounds",
-    "abs_gpu_set_iteration", "abs_gpu_simulate", "abs_gpu_stats",
+    "abs_gpu_set_iteration", "abs_gpu_sir_counts", "abs_gpu_sir_state", "abs_gpu_simulate", "abs_gpu_stats",
     "abs_gpu_synchronize", "abs_gpu_download", "abs_gpu_env_update", "abs_gpu_grid_info",
     "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
@@ -98,6 +98,8 @@ def load():
         "abs_gpu_set_grid_override": (C.c_int, [_CTX, _D, _U32]),
         "abs_gpu_local_bounds": (C.c_int, [_CTX, _D]),
         "abs_gpu_set_iteration": (C.c_int, [_CTX, C.c_uint64]),
+        "abs_gpu_sir_counts": (C.c_int, [_CTX, _U64]),
+        "abs_gpu_sir_state": (C.c_int, [_CTX, _U8, _U32]),
         "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),
         "abs_gpu_synchronize": (C.c_int, [_CTX]),

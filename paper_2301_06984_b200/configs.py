@@ -131,9 +131,24 @@ def c4_large_uniform(n: int = 1 << 26, seed: int = 0) -> Workload:
                     steps=50)
 
 
+def c5_sir(n: int = 10_000_000, seed: int = 0) -> Workload:
+    """configs[4]: n point agents uniform in a periodic cube at ~5 agents
+    within the infection radius 2 (rho = 0.1492 => L = (n / rho)^(1/3),
+    406.2 at 10^7), unit random-walk steps, p = 0.1 per infected neighbour,
+    recovery after 20 iterations, 1 % initially infected (absim_models.h)."""
+    rho = 5.0 / (4.0 / 3.0 * math.pi * 8.0)
+    L = (n / rho) ** (1.0 / 3.0)
+    uid = np.arange(n, dtype=np.uint64)
+    x, y, z = (u01(rng_word(seed, uid, j)) * L for j in range(3))
+    return Workload("c5_sir", x, y, z, np.ones(n), None,
+                    dict(seed=seed, model=N.MODEL_SIR, model_params=[L, 2.0, 1.0, 20.0, 0.1]),
+                    steps=300, bytes_per_agent_iteration=120)
+
+
 CONFIGS = {
     "c1": c1_relaxation,
     "c2": c2_proliferation,
     "c3": c3_spheroid,
     "c4": c4_large_uniform,
+    "c5": c5_sir,
 }

@@ -186,6 +186,7 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
   }
   reset_reduction(g);
   g->work = 0;
+  g->sir[0] = g->sir[1] = g->sir[2] = 0;
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
@@ -324,6 +325,7 @@ struct Soa {
 };
 
 __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos, Soa src, Soa dst,
+                                                      float4* __restrict__ pf,
                                                       const unsigned int* __restrict__ start,
                                                       const unsigned int* __restrict__ key,
                                                       const unsigned int* __restrict__ rank,
@@ -338,6 +340,9 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
     const Pd p = load_pd(pos + i);
     reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
+    if (ABS_PREFILTER)
+      pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
+                          static_cast<float>(p.z - g->origin[2]), static_cast<float>(p.d));
     dst.uid[j] = src.uid[i];
     dst.flags[j] = src.flags[i];
     dst.partners[j] = src.partners[i];
@@ -625,7 +630,7 @@ __device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsign
 // overflow and as the reference implementation of the tiled kernel below.
 template <int MODEL, bool STATIC, bool RECORD>
 __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
-    k_force(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
+    k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
             unsigned int* __restrict__ div_mark) {
@@ -657,7 +662,7 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
           [&](double r, double r2, auto&& visit) {
-            for_each_neighbor_flat(Q, S.pd, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
+            for_each_neighbor_flat(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
                                    [&](unsigned int j, const Pd& q, double, double, double, double d2) {
                                      visit(j, q, d2);
                                    });
@@ -978,6 +983,87 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   flush_counters(n_eval, n_skip, gw);
 }
 
+// ------------------------------------------------------------ config 5: SIR
+// absim_models.h: from start-of-iteration states, S -> I with probability
+// 1 - (1-p)^k (k infected neighbours within r, minimum image on the periodic
+// cube), I -> R after `recovery` iterations, then a unit random-walk step
+// wrapped into [0, L). Bins are the periodic boxes (box = L / floor(L / r) >= r),
+// so the 27 wrapped neighbour boxes hold every candidate.
+__global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, const DevGrid* g,
+                                                  const unsigned int* __restrict__ start,
+                                                  unsigned char* __restrict__ next_state,
+                                                  unsigned int* __restrict__ next_t, StepArgs a) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  const double L = a.mp[0], r = a.mp[1], step = a.mp[2], prob = a.mp[4];
+  const unsigned long long rec = static_cast<unsigned long long>(a.mp[3]);
+  const double box = g->box, r2 = r * r;
+  const unsigned int D0 = g->dims[0], D1 = g->dims[1], D2 = g->dims[2];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd me = load_pd(S.pd + i);
+    unsigned char st = S.beh[i];
+    unsigned int ti = S.partners[i];
+    if (st == ABS_SIR_I && a.iteration - ti >= rec) st = ABS_SIR_R;
+    if (st == ABS_SIR_S) {
+      const unsigned int cx = box_coord(me.x, 0.0, box, D0), cy = box_coord(me.y, 0.0, box, D1),
+                         cz = box_coord(me.z, 0.0, box, D2);
+      unsigned int k = 0;
+      for (int dz = -1; dz <= 1; ++dz) {
+        const unsigned int bz = (cz + D2 + dz) % D2;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const unsigned int by = (cy + D1 + dy) % D1;
+          const unsigned int row = D0 * (by + D1 * bz);
+          for (int dx = -1; dx <= 1; ++dx) {
+            const unsigned int bx = (cx + D0 + dx) % D0;
+            const unsigned int j1 = __ldg(start + row + bx + 1);
+            for (unsigned int j = __ldg(start + row + bx); j < j1; ++j) {
+              if (j == i || S.beh[j] != ABS_SIR_I) continue;
+              const Pd q = load_pd(S.pd + j);
+              const double ex = abs_min_image(me.x - q.x, L), ey = abs_min_image(me.y - q.y, L),
+                           ez = abs_min_image(me.z - q.z, L);
+              if ((ex * ex + ey * ey) + ez * ez <= r2) ++k;
+            }
+          }
+        }
+      }
+      if (k > 0 && abs_rng_word(a.seed, S.uid[i], ABS_RNG_SIR_INFECT(a.iteration)) < abs_sir_threshold(prob, k)) {
+        st = ABS_SIR_I;
+        ti = static_cast<unsigned int>(a.iteration);
+      }
+    }
+    double dir[3];
+    abs_unit_vector(a.seed, S.uid[i], ABS_RNG_SIR_WALK(a.iteration), dir);
+    reinterpret_cast<double2*>(out + i)[0] =
+        make_double2(abs_wrap(me.x + dir[0] * step, L), abs_wrap(me.y + dir[1] * step, L));
+    reinterpret_cast<double2*>(out + i)[1] = make_double2(abs_wrap(me.z + dir[2] * step, L), me.d);
+    next_state[i] = st;
+    next_t[i] = ti;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_sir_commit(Soa S, DevGrid* g,
+                                                         const unsigned char* __restrict__ next_state,
+                                                         const unsigned int* __restrict__ next_t) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  unsigned long long c[3] = {0, 0, 0};
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned char st = next_state[i];
+    S.beh[i] = st;
+    S.partners[i] = next_t[i];
+    c[0] += st == ABS_SIR_S;
+    c[1] += st == ABS_SIR_I;
+    c[2] += st == ABS_SIR_R;
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    for (int off = 16; off; off >>= 1) c[q] += __shfl_xor_sync(0xffffffffu, c[q], off);
+    if ((threadIdx.x & 31) == 0 && c[q]) atomicAdd(&g->sir[q], c[q]);
+  }
+}
+
 // ------------------------------------------------------------ commit
 // mark_new_agent_neighbors (simulation.cpp:510-530): each staged daughter
 // flags new_neighbor on agents of the START-OF-STEP grid (reference boxes,
@@ -1088,7 +1174,8 @@ __global__ void k_zero_marks(unsigned int* __restrict__ m, const DevGrid* g) {
 // state. Host arrays reach these inputs by contiguous H2D copies.
 __global__ void k_ingest(const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
                          const double* __restrict__ d, const unsigned char* __restrict__ mask, unsigned long long n,
-                         int set_uid, int set_vol, int model_on, Pd* __restrict__ out, Soa S, DevGrid* g) {
+                         int set_uid, int set_vol, int model_on, Pd* __restrict__ out, Soa S, DevGrid* g,
+                         int sir, unsigned long long seed) {
   unsigned int bad = 0;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
@@ -1098,7 +1185,12 @@ __global__ void k_ingest(const double* __restrict__ x, const double* __restrict_
     reinterpret_cast<double2*>(out + i)[1] = make_double2(z[i], di);
     if (set_uid) S.uid[i] = i;
     if (set_vol) S.vol[i] = abs_volume_of_diameter(di);
-    S.beh[i] = (model_on && (!mask || mask[i])) ? 1 : 0;
+    if (sir) {  // absim_models.h: 1 % initially infected, from the seed (or given states)
+      const unsigned long long u = set_uid ? i : S.uid[i];
+      S.beh[i] = mask ? mask[i] : (abs_u01(abs_rng_word(seed, u, ABS_RNG_SIR_INIT)) < 0.01 ? ABS_SIR_I : ABS_SIR_S);
+    } else {
+      S.beh[i] = (model_on && (!mask || mask[i])) ? 1 : 0;
+    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&g->bad_input, 1u);
 }
@@ -1339,6 +1431,7 @@ struct abs_gpu_ctx {
   Soa S[2]{};
   int cur = 0;
   Pd* newpd = nullptr;
+  float4* pf = nullptr;  // fp32 copy of pd relative to the grid origin (ABS_PREFILTER)
   bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
   bool grid_valid = false; // `start` holds a scanned cell table for S[cur]
 
@@ -1459,6 +1552,9 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   cudaFree(c->key); cudaFree(c->rank); cudaFree(c->nv); cudaFree(c->nn);
   cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
   cudaFree(c->tiles64);
+  cudaFree(c->pf);
+  c->pf = nullptr;
+  if (ABS_PREFILTER) CK(dalloc(&c->pf, ncap));
   CK(dalloc(&c->key, ncap));
   CK(dalloc(&c->rank, ncap));
   CK(dalloc(&c->nv, ncap));
@@ -1518,10 +1614,12 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
 // Sub-bins per box edge: y/z rows finer than x (the x extent of a row is
 // trimmed to the sphere's cross-section, so x resolution matters less).
 unsigned int bins_yz(const abs_gpu_ctx* c) {
+  if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box;
   return b <= 0 ? 2u : static_cast<unsigned int>(std::min(b, 2));
 }
 unsigned int bins_x(const abs_gpu_ctx* c) {
+  if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box_x;
   return b <= 0 ? 1u : static_cast<unsigned int>(std::min(b, 2));
 }
@@ -1542,7 +1640,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->launches += 3;
   launch_scan<unsigned int>(c, c->start, nbins_dev, c->bins_cap, c->tiles, &c->g->err);
   const int nxt = c->cur ^ 1;
-  k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->start, c->key, c->rank, c->g,
+  k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
                                             c->cfg.record_forces);
   ++c->launches;
@@ -1584,7 +1682,7 @@ void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     configured = true;
   }
   k_force<MODEL, STATIC, RECORD><<<force_blocks(c), kForceThreads, kForceSmem, c->stream>>>(
-      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
 }
 
 template <int MODEL, bool STATIC>
@@ -1615,6 +1713,16 @@ void launch_force(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
 
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
   launch_env_update(c, iteration, c->cfg.model == ABS_MODEL_PROLIFERATION);
+  if (c->cfg.model == ABS_MODEL_SIR) {
+    const int nb = grid_blocks(c, c->cap);
+    const StepArgs a = step_args(c, iteration);
+    Soa& S = c->S[c->cur];
+    k_sir<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->nv, c->key, a);
+    k_sir_commit<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->nv, c->key);
+    c->launches += 2;
+    c->pos_in_new = true;
+    return;
+  }
   const int nb = grid_blocks(c, c->cap);
   const StepArgs a = step_args(c, iteration);
   Soa& S = c->S[c->cur];
@@ -1714,7 +1822,10 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "repulsion_coefficient must be >= 0");
   if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
   if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
-  if (cfg->model < 0 || cfg->model > 3) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->model < 0 || cfg->model > 4) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->model == ABS_MODEL_SIR && !(cfg->model_params[0] > 0.0 && cfg->model_params[1] > 0.0 &&
+                                       cfg->model_params[0] >= 3.0 * cfg->model_params[1]))
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "SIR needs L >= 3 r > 0");
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     return set_err(nullptr, ABS_ERR_NO_DEVICE, "no CUDA device available");
@@ -1738,6 +1849,15 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
   rc = ensure_bins(c, 1 << 16);
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
+  if (cfg->model == ABS_MODEL_SIR) {  // periodic cube [0, L)^3 in boxes of L / floor(L / r)
+    const double L = cfg->model_params[0], r = cfg->model_params[1];
+    unsigned int D = static_cast<unsigned int>(std::floor(L / r));
+    if (D < 3) D = 3;
+    const double grid[5] = {0.0, 0.0, 0.0, L / static_cast<double>(D), r};
+    const unsigned int dims[3] = {D, D, D};
+    rc = abs_gpu_set_grid_override(c, grid, dims);
+    if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "grid setup failed"); }
+  }
   *out = c;
   return ABS_OK;
 }
@@ -1748,7 +1868,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_soa(c->S[0]);
   free_soa(c->S[1]);
-  cudaFree(c->newpd); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
+  cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
@@ -1807,7 +1927,8 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   if (n) {
     k_ingest<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr,
                                                             volume == nullptr, c->cfg.model != ABS_MODEL_NONE,
-                                                            c->newpd, S, c->g);
+                                                            c->newpd, S, c->g, c->cfg.model == ABS_MODEL_SIR,
+                                                            c->cfg.seed);
     ++c->launches;
   }
   // the cell table is a counter array between iterations: always start clean
@@ -1936,6 +2057,26 @@ int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
   CK(cudaMemcpyAsync(&c->g->nonfinite, &zero, 4, cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (h.nonfinite) return set_err(c, ABS_ERR_NONFINITE, "agent positions are not finite");
+  return ABS_OK;
+}
+
+int abs_gpu_sir_counts(abs_gpu_ctx* c, uint64_t* out3) {
+  if (!c || !out3) return ABS_ERR_INVALID_ARGUMENT;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  for (int q = 0; q < 3; ++q) out3[q] = h.sir[q];
+  return ABS_OK;
+}
+
+int abs_gpu_sir_state(abs_gpu_ctx* c, uint8_t* state, uint32_t* t_infected) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  Soa& S = c->S[c->cur];
+  if (state) CK(cudaMemcpy(state, S.beh, h.n, cudaMemcpyDeviceToHost));
+  if (t_infected) CK(cudaMemcpy(t_infected, S.partners, h.n * 4, cudaMemcpyDeviceToHost));
   return ABS_OK;
 }
 

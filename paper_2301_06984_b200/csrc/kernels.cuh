@@ -74,6 +74,7 @@ struct DevGrid {
   unsigned long long skips;
   unsigned long long added;
   unsigned long long removed;
+  unsigned long long sir[3];  // S/I/R counts after the last SIR iteration
   // --- kept across uploads (abs_gpu_upload copies everything above) ---
   int ov_on;               // multi-domain: use the global grid below
   int pad1;
@@ -242,6 +243,9 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
 constexpr int kMaxRows = 32;
 constexpr int kMaxContacts = 16;  // recorded possible contacts per agent (pass B)
 constexpr int kForceThreads = 128;
+#ifndef ABS_PREFILTER
+#define ABS_PREFILTER 0
+#endif
 #ifndef ABS_BATCH
 #define ABS_BATCH 4
 #endif
@@ -249,6 +253,7 @@ constexpr int kBatch = ABS_BATCH;
 
 template <class F>
 __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd* __restrict__ pd,
+                                                       const float4* __restrict__ pf,
                                                        const unsigned int* __restrict__ start,
                                                        unsigned int (*wj0)[kForceThreads],
                                                        unsigned int (*wj1)[kForceThreads],
@@ -315,6 +320,31 @@ __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd*
         }
       }
     }
+#if ABS_PREFILTER
+    // conservative fp32 reject on the float4 copy (|error| < slack), then the
+    // exact fp64 test only for the survivors
+    float4 qf[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pf + idx[u]);
+    bool pass[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const float ex = fx - qf[u].x, ey = fy - qf[u].y, ez = fz - qf[u].z;
+      pass[u] = idx[u] != self && __fmaf_rn(ez, ez, __fmaf_rn(ey, ey, ex * ex)) <= rf2;
+    }
+    Pd q[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (pass[u]) q[u] = load_pd(pd + idx[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (pass[u]) {
+        const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
+        const double d2 = (dx * dx + dy * dy) + dz * dz;
+        if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
+      }
+    }
+#else
     Pd q[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + idx[u]);
@@ -326,6 +356,7 @@ __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd*
         if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
       }
     }
+#endif
   }
 }
 

@@ -223,6 +223,20 @@ class Simulation:
         N.check(N.load().abs_gpu_local_bounds(self._ctx, _p(out, C.c_double)), self._ctx)
         return out
 
+    def sir_counts(self):
+        """Config 5: [S, I, R] after the last iteration."""
+        out = np.zeros(3, np.uint64)
+        N.check(N.load().abs_gpu_sir_counts(self._ctx, _p(out, C.c_uint64)), self._ctx)
+        return [int(v) for v in out]
+
+    def sir_state(self):
+        """Config 5: (state per agent, infection iteration), storage order."""
+        n = self.agent_count()
+        st = np.zeros(n, np.uint8)
+        ti = np.zeros(n, np.uint32)
+        N.check(N.load().abs_gpu_sir_state(self._ctx, _p(st, C.c_uint8), _p(ti, C.c_uint32)), self._ctx)
+        return st, ti
+
     def set_iteration(self, iteration: int) -> None:
         N.check(N.load().abs_gpu_set_iteration(self._ctx, iteration), self._ctx)
 
