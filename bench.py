@@ -253,8 +253,11 @@ def run_gpu(args):
     hbm, peak_src = _peaks()
     n_agents = r1.final_agent_count
     avg_force_ms = force_ms / max(1, force_launches)
-    force_bytes = 56 * n_agents  # read {x,y,z,d} 32 B + write {x,y,z} 24 B per agent
-    achieved = force_bytes / (avg_force_ms / 1e3) / 1e9
+    sir = wl.params.get("model") == E.MODEL_SIR
+    # k_force: read {x,y,z,d} 32 B + write {x,y,z} 24 B per agent;
+    # k_sir (config 5): read {x,y,z,state} 28 B + write {x,y,z,state} 28 B
+    force_bytes = 56 * n_agents
+    achieved = force_bytes / (avg_force_ms / 1e3) / 1e9 if avg_force_ms > 0 else 0.0
     step_bytes = wl.bytes_per_agent_iteration * agent_its / max(1, world)
     step_achieved = step_bytes / (ms / 1e3) / 1e9
     traffic = None
@@ -274,7 +277,7 @@ def run_gpu(args):
         "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "bins_per_box": [args.bins_x, args.bins, args.bins], "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
-        "roofline": {"bound": "hbm", "kernel": "k_force", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else "k_force", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
                      "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms},
@@ -303,8 +306,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--bins", type=int, default=2, help="sub-bins per box edge along y, z")
-    ap.add_argument("--bins-x", type=int, default=2, help="sub-bins per box edge along x")
+    ap.add_argument("--bins", type=int, default=0, help="sub-bins per box edge along y, z (0 = auto)")
+    ap.add_argument("--bins-x", type=int, default=0, help="sub-bins per box edge along x (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -644,6 +644,7 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
   __syncthreads();
   const unsigned long long n = gp->n;
   const double dmax = gp->dmax;
+  const bool box_mode = Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1;  // bins are the reference boxes
   unsigned long long n_eval = 0, n_skip = 0;
   // Persistent warps claim consecutive 32-agent chunks: the agent array (cell
   // order) is swept once, front to back, and no warp waits for another.
@@ -662,10 +663,17 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
           [&](double r, double r2, auto&& visit) {
-            for_each_neighbor_flat(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
-                                   [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                                     visit(j, q, d2);
-                                   });
+            if (box_mode) {
+              for_each_neighbor_box(Q, S.pd, start, self, me.x, me.y, me.z, r2,
+                                    [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                                      visit(j, q, d2);
+                                    });
+            } else {
+              for_each_neighbor_flat(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
+                                     [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                                       visit(j, q, d2);
+                                     });
+            }
           },
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
     }
@@ -1421,6 +1429,7 @@ struct abs_gpu_ctx {
   std::string err;
   int sms = 148;
 
+  unsigned int auto_bins = 2;      // sub-bins per box edge chosen at upload (bins_per_box == 0)
   unsigned long long cap = 0;      // agent capacity
   unsigned long long uid_cap = 0;  // uid-indexed arrays
   unsigned long long bins_cap = 0;
@@ -1613,15 +1622,19 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
 
 // Sub-bins per box edge: y/z rows finer than x (the x extent of a row is
 // trimmed to the sphere's cross-section, so x resolution matters less).
+// Auto (bins_per_box == 0): when the typical query radius 0.5 (d + dmax) is
+// close to the box (mean d / dmax > 0.75, e.g. config 1) all 27 boxes are
+// needed anyway and the box-lockstep walk (bins == boxes) wins; with a wide
+// diameter spread (config 4) 2x2x2 sub-bins cut the candidates 2x.
 unsigned int bins_yz(const abs_gpu_ctx* c) {
   if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box;
-  return b <= 0 ? 2u : static_cast<unsigned int>(std::min(b, 2));
+  return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 2));
 }
 unsigned int bins_x(const abs_gpu_ctx* c) {
   if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box_x;
-  return b <= 0 ? 1u : static_cast<unsigned int>(std::min(b, 2));
+  return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 2));
 }
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
@@ -1717,7 +1730,21 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
     const int nb = grid_blocks(c, c->cap);
     const StepArgs a = step_args(c, iteration);
     Soa& S = c->S[c->cur];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {  // the dominant kernel of config 5
+      if (c->ev_used + 2 > c->ev.size()) {
+        for (int q = 0; q < 256; ++q) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          c->ev.push_back(e);
+        }
+      }
+      e0 = c->ev[c->ev_used++];
+      e1 = c->ev[c->ev_used++];
+      cudaEventRecord(e0, c->stream);
+    }
     k_sir<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->nv, c->key, a);
+    if (c->timing) cudaEventRecord(e1, c->stream);
     k_sir_commit<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->nv, c->key);
     c->launches += 2;
     c->pos_in_new = true;
@@ -1896,6 +1923,14 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   Soa& S = c->S[c->cur];
   const double *dx = x, *dy = y, *dz = z, *dd = d;
   const unsigned char* dmask = mask;
+  if (host && n) {
+    double sum = 0.0, mx = 0.0;
+    for (unsigned long long i = 0; i < n; ++i) {
+      sum += d[i];
+      mx = d[i] > mx ? d[i] : mx;
+    }
+    c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
+  }
   if (host && n) {  // contiguous H2D into the staging area, interleaved on the device
     double* st = reinterpret_cast<double*>(c->st_pd);
     CK(cudaMemcpyAsync(st, x, n * 8, cudaMemcpyHostToDevice, c->stream));

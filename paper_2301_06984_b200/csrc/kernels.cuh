@@ -251,6 +251,41 @@ constexpr int kForceThreads = 128;
 #endif
 constexpr int kBatch = ABS_BATCH;
 
+// Box-lockstep variant (requires bins == reference boxes). Every lane walks
+// the 3x3x3 reference boxes around ITS box as 9 contiguous x-runs
+// (uniform_grid.cpp:199-201 without the per-lane trimming), so the lanes of a
+// warp whose agents share a box fetch the same candidate at the same time:
+// their loads coalesce into one broadcast instead of one L1 line per lane.
+template <class F>
+__device__ __forceinline__ void for_each_neighbor_box(const QGrid& g, const Pd* __restrict__ pd,
+                                                      const unsigned int* __restrict__ start, unsigned int self,
+                                                      double cx, double cy, double cz, double r2, F&& visit) {
+  const int bx = static_cast<int>(box_coord(cx, g.ox, g.box, g.dims[0]));
+  const int by = static_cast<int>(box_coord(cy, g.oy, g.box, g.dims[1]));
+  const int bz = static_cast<int>(box_coord(cz, g.oz, g.box, g.dims[2]));
+  const int x0 = max(bx - 1, 0), x1 = min(bx + 1, static_cast<int>(g.dims[0]) - 1);
+  const int y0 = max(by - 1, 0), y1 = min(by + 1, static_cast<int>(g.dims[1]) - 1);
+  const int z0 = max(bz - 1, 0), z1 = min(bz + 1, static_cast<int>(g.dims[2]) - 1);
+  for (int z = z0; z <= z1; ++z)
+    for (int y = y0; y <= y1; ++y) {
+      const unsigned int row = g.dims[0] * (static_cast<unsigned int>(y) + g.dims[1] * static_cast<unsigned int>(z));
+      const unsigned int j0 = __ldg(start + row + x0), j1 = __ldg(start + row + x1 + 1);
+      for (unsigned int j = j0; j < j1; j += kBatch) {
+        Pd q[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + min(j + u, j1 - 1));
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const unsigned int jj = j + u;
+          const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          if (jj < j1 && jj != self && d2 <= r2) visit(jj, q[u], dx, dy, dz, d2);
+        }
+      }
+    }
+}
+
+
 template <class F>
 __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd* __restrict__ pd,
                                                        const float4* __restrict__ pf,
