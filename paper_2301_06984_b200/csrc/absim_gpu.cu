@@ -646,13 +646,13 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
   const double dmax = gp->dmax;
   const bool box_mode = Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1;  // bins are the reference boxes
   unsigned long long n_eval = 0, n_skip = 0;
-  // Persistent warps claim consecutive 32-agent chunks: the agent array (cell
-  // order) is swept once, front to back, and no warp waits for another.
+  // Persistent warps sweep 32-agent chunks in a static warp-strided order:
+  // the resident warps cover a contiguous window of the agent array (cell
+  // order) that advances front to back, with no shared counter to contend on.
   const int lane = threadIdx.x & 31;
-  while (true) {
-    unsigned long long chunk = 0;
-    if (lane == 0) chunk = atomicAdd(&gw->work, 1ull);
-    chunk = __shfl_sync(0xffffffffu, chunk, 0);
+  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
     const unsigned long long base = chunk * 32ull;
     if (base >= n) break;
     const unsigned long long i = base + lane;

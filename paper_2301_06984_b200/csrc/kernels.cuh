@@ -35,7 +35,7 @@ constexpr int kScanTile = 2048;  // 256 threads x 8 values
 #endif
 constexpr int kUnroll = ABS_UNROLL;  // candidate loads in flight per lane
 
-struct __align__(16) Pd {
+struct __align__(32) Pd {
   double x, y, z, d;
 };
 
@@ -104,10 +104,14 @@ __device__ __forceinline__ double ord_dec(unsigned long long o) {
   return __longlong_as_double(static_cast<long long>(b));
 }
 
+// One 256-bit read-only load per record (sm_100: LDG.E.ENL2.256): half the
+// L1 requests of two 128-bit loads on the gather-bound neighbour walks.
 __device__ __forceinline__ Pd load_pd(const Pd* __restrict__ p) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  return Pd{a.x, a.y, b.x, b.y};
+  Pd r;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.d)
+               : "l"(p));
+  return r;
 }
 
 __device__ __forceinline__ int clamp_bin(double v, double s, unsigned int nb) {
