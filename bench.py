@@ -266,7 +266,7 @@ def run_gpu(args):
         try:
             with open(tp) as f:
                 tt = json.load(f)
-            if tt.get("config") == args.config:
+            if tt.get("config") == args.config and tt.get("agents") == n_agents:
                 traffic = tt.get("dram_bytes_per_launch")
         except Exception:
             pass
