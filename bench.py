@@ -175,6 +175,105 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def _slab_workload(n_per, world, rank, seed=0):
+    """Weak-scaling c4 (configs[3]): world * n_per agents uniform in one cube at
+    12 mean neighbours; rank r generates the agents of its z-slab (uids
+    r * n_per + i), lognormal(ln 10, 0.1) diameters from rng_word."""
+    import numpy as np
+    from paper_2301_06984_b200 import configs as CF
+    L = (n_per * world / CF.DENSITY) ** (1.0 / 3.0)
+    uid = np.arange(n_per, dtype=np.uint64) + np.uint64(rank * n_per)
+    x = CF.u01(CF.rng_word(seed, uid, 0)) * L
+    y = CF.u01(CF.rng_word(seed, uid, 1)) * L
+    z = (rank + CF.u01(CF.rng_word(seed, uid, 2))) * (L / world)
+    u1 = 1.0 - CF.u01(CF.rng_word(seed, uid, 4))
+    u2 = CF.u01(CF.rng_word(seed, uid, 5))
+    d = np.exp(math.log(10.0) + 0.1 * (np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * math.pi * u2)))
+    return x, y, z, d, uid, L
+
+
+def run_decomposed(args, dist, world, rank, local):
+    """N GPUs: slab decomposition with the device-resident exchange over NCCL."""
+    import torch
+
+    import paper_2301_06984_b200 as E
+    from paper_2301_06984_b200 import distributed as D
+    n_per = args.n or (1 << 26)
+    x, y, z, d, uid, L = _slab_workload(n_per, world, rank, args.seed)
+    prm = dict(seed=args.seed, simulation_time_step=0.01, record_forces=False,
+               bins_per_box=args.bins, bins_per_box_x=args.bins_x, capacity=int(n_per * 1.3))
+    sim = E.Simulation(E.SimulationParams(**prm), device=local)
+    sim.add_agents(x, y, z, d, uid=uid, uid_count=n_per * world)
+    dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="nccl",
+                                    cap=int(0.06 * n_per) + (1 << 20))
+    dec.simulate(args.warmup)
+    stream = torch.cuda.ExternalStream(sim.stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = sim.report().kernel_launches
+    with Clocks(local) as clk:
+        e0.record(stream)
+        dec.simulate(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = torch.tensor([float(sim.report().kernel_launches - l0)], device="cuda")
+    dist.all_reduce(launches)
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    owned = torch.tensor([float(sim.agent_count())], device="cuda")
+    dist.all_reduce(owned)
+    total = float(owned.item())
+    value = total * args.steps / (ms_max / 1e3)
+
+    # end to end per rank through the public API with HOST buffers: upload the
+    # rank's slab from page-locked memory, one decomposed iteration (bounds
+    # all-reduce, migration + halo over NCCL), positions back to page-locked
+    # memory; wall time between barriers, max over ranks
+    e2e = None
+    if not args.no_e2e:
+        import numpy as np
+        pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (x, y, z, d, uid)]
+        outp = [torch.empty(int(n_per * 1.3), dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+        e2e_steps = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        n_e = 0
+        for _ in range(e2e_steps):
+            sim.add_agents(*pin[:4], uid=pin[4], uid_count=n_per * world)
+            dec.simulate(1)
+            n_e = sim.positions(*outp)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_per * world * e2e_steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": n_per * 40 * world, "d2h_bytes_per_step": n_e * 24 * world,
+               "steps": e2e_steps, "timing": "wall clock between barriers, max over ranks",
+               "path": "per rank: abs_gpu_upload (pinned) -> decomposed iteration -> abs_gpu_download (pinned)"}
+    if rank == 0:
+        hbm, _ = _peaks()
+        step_bytes = 128 * n_per * args.steps
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c4_large_uniform (weak scaling)", "agents_per_gpu": n_per,
+                       "global_agents": int(total), "cube_side": L,
+                       "parallelism": f"slab{world} (z box layers, NCCL halo + migration)",
+                       "l2": "inputs >> 126 MB L2, no flush"},
+            "step_roofline": {"bytes_per_agent_iteration": 128, "unit": "GB/s",
+                              "achieved_per_gpu": step_bytes / (ms_max / 1e3) / 1e9,
+                              "frac": step_bytes / (ms_max / 1e3) / 1e9 / hbm},
+            "clocks": clk.summary(),
+            "force_evaluations_per_agent_step": dec.evals / max(1.0, total * (args.steps + args.warmup)),
+            "e2e": e2e, "gpu_launches": int(launches.item()),
+            "gpu_launches_note": "all ranks: engine kernels + export/import/compaction",
+        }))
+
+
 def run_gpu(args):
     import numpy as np
     import torch
@@ -183,6 +282,19 @@ def run_gpu(args):
 
     dist, world, rank, local = _dist() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 1, 0, 0)
     torch.cuda.set_device(local)
+    if world > 1 or args.decompose:
+        if args.config != "c4":
+            raise SystemExit("multi-GPU bench runs config c4 (slab decomposition)")
+        if dist is None:
+            import torch.distributed as dist0
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            dist0.init_process_group("nccl", rank=0, world_size=1)
+            dist = dist0
+        run_decomposed(args, dist, world, rank, local)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     wl = _workload(args.config, args.n, seed=args.seed + rank)
     prm = dict(wl.params)
     prm["record_forces"] = False
@@ -304,11 +416,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--agents", "--n", dest="n", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--bins", type=int, default=0, help="sub-bins per box edge along y, z (0 = auto)")
     ap.add_argument("--bins-x", type=int, default=0, help="sub-bins per box edge along x (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--decompose", action="store_true", help="use the slab decomposition even at N=1")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

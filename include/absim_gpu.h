@@ -125,6 +125,22 @@ int abs_gpu_set_grid_override(abs_gpu_ctx* ctx, const double* grid, const uint32
  * max xyz, out[6] largest diameter (uniform_grid.cpp:170-206 pass 1). */
 int abs_gpu_local_bounds(abs_gpu_ctx* ctx, double* out7);
 
+/* Device-resident multi-domain exchange. Agents travel as
+ * packed 96-byte records (ABS_RECORD_BYTES) in caller-owned DEVICE buffers.
+ * abs_gpu_export_layers classifies agents by reference-box z-layer under the
+ * given global grid (grid[0..2] origin, grid[3] box; dims):
+ *   mode 0 (migrate): owned agents with layer < lo -> out_lo, >= hi -> out_hi,
+ *                     removed from this context;
+ *   mode 1 (halo):    owned agents with layer == lo -> out_lo, == hi-1 -> out_hi.
+ * Returns ABS_ERR_CAPACITY when a count exceeds cap (counts are still set). */
+#define ABS_RECORD_BYTES 96
+int abs_gpu_export_layers(abs_gpu_ctx* ctx, const double* grid, const uint32_t* dims, int64_t lo, int64_t hi,
+                          int mode, void* out_lo, void* out_hi, uint64_t cap, uint64_t* n_lo, uint64_t* n_hi);
+/* Append count records (device pointer) as owned agents or as ghosts. */
+int abs_gpu_import(abs_gpu_ctx* ctx, const void* records, uint64_t count, int as_ghost);
+/* Remove every ghost agent (order-preserving compaction). */
+int abs_gpu_drop_ghosts(abs_gpu_ctx* ctx);
+
 /* Config 5 (SIR): S/I/R counts after the last iteration, and the per-agent
  * state (0 S, 1 I, 2 R) + infection iteration in download order. */
 int abs_gpu_sir_counts(abs_gpu_ctx* ctx, uint64_t* out3);

@@ -29,7 +29,8 @@ FLAG_GHOST = 128
 EXPORTS = [
     "abs_gpu_default_config", "abs_gpu_create", "abs_gpu_destroy", "abs_gpu_last_error",
     "abs_gpu_upload", "abs_gpu_upload_device", "abs_gpu_set_grid_override", "abs_gpu_local_bounds",
-    "abs_gpu_set_iteration", "abs_gpu_sir_counts", "abs_gpu_sir_state", "abs_gpu_simulate", "abs_gpu_stats",
+    "abs_gpu_set_iteration", "abs_gpu_sir_counts", "abs_gpu_sir_state",
+    "abs_gpu_export_layers", "abs_gpu_import", "abs_gpu_drop_ghosts", "abs_gpu_simulate", "abs_gpu_stats",
     "abs_gpu_synchronize", "abs_gpu_download", "abs_gpu_env_update", "abs_gpu_grid_info",
     "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
@@ -99,6 +100,10 @@ def load():
         "abs_gpu_local_bounds": (C.c_int, [_CTX, _D]),
         "abs_gpu_set_iteration": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_sir_counts": (C.c_int, [_CTX, _U64]),
+        "abs_gpu_export_layers": (C.c_int, [_CTX, _D, _U32, C.c_int64, C.c_int64, C.c_int, C.c_void_p,
+                                            C.c_void_p, C.c_uint64, _U64, _U64]),
+        "abs_gpu_import": (C.c_int, [_CTX, C.c_void_p, C.c_uint64, C.c_int]),
+        "abs_gpu_drop_ghosts": (C.c_int, [_CTX]),
         "abs_gpu_sir_state": (C.c_int, [_CTX, _U8, _U32]),
         "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),

@@ -1203,6 +1203,95 @@ __global__ void k_ingest(const double* __restrict__ x, const double* __restrict_
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&g->bad_input, 1u);
 }
 
+// ------------------------------------------------------------ multi-domain exchange
+// Packed agent record exchanged between ranks: 96 bytes.
+struct __align__(16) Rec {
+  double x, y, z, d, vol, fx, fy, fz;
+  unsigned long long uid;
+  unsigned int partners;
+  unsigned char flags, beh, pad0, pad1;
+  unsigned long long pad2;
+};
+static_assert(sizeof(Rec) == 96, "record layout");
+
+// mode 0 (migrate): owned agents with box z-layer < lo -> out_lo, >= hi -> out_hi,
+//                   keep[i] = 0 for them. mode 1 (halo): layer == lo -> out_lo,
+//                   layer == hi - 1 -> out_hi, kept. Ghosts are never exported.
+__global__ void k_export(const Pd* __restrict__ pos, Soa S, unsigned long long cap, unsigned long long n,
+                         double oz, double box, unsigned int dimz, long long lo, long long hi, int mode,
+                         Rec* __restrict__ out_lo, Rec* __restrict__ out_hi, unsigned long long out_cap,
+                         unsigned long long* __restrict__ counts, unsigned int* __restrict__ keep) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const unsigned char fl = S.flags[i];
+    const long long layer = static_cast<long long>(box_coord(p.z, oz, box, dimz));
+    int dest = -1;  // 0 -> lo, 1 -> hi
+    if (!(fl & ABS_FLAG_GHOST)) {
+      if (mode == 0) dest = layer < lo ? 0 : (layer >= hi ? 1 : -1);
+      else dest = layer == lo ? 0 : (layer == hi - 1 ? 1 : -1);
+    }
+    if (keep) keep[i] = (mode == 0 && dest >= 0) ? 0u : 1u;
+    if (dest < 0) continue;
+    const unsigned long long slot = atomicAdd(counts + dest, 1ull);
+    if (slot >= out_cap) continue;  // caller sees count > cap and retries larger
+    Rec r;
+    r.x = p.x; r.y = p.y; r.z = p.z; r.d = p.d;
+    r.vol = S.vol[i];
+    r.fx = S.force[i]; r.fy = S.force[cap + i]; r.fz = S.force[2 * cap + i];
+    r.uid = S.uid[i];
+    r.partners = S.partners[i];
+    r.flags = fl;
+    r.beh = S.beh[i];
+    r.pad0 = r.pad1 = 0;
+    r.pad2 = 0;
+    (dest ? out_hi : out_lo)[slot] = r;
+  }
+}
+
+__global__ void k_import(const Rec* __restrict__ in, unsigned long long count, unsigned long long base,
+                         Pd* __restrict__ pos, Soa S, unsigned long long cap, int as_ghost) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < count;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const Rec r = in[k];
+    const unsigned long long j = base + k;
+    pos[j] = Pd{r.x, r.y, r.z, r.d};
+    S.vol[j] = r.vol;
+    S.force[j] = r.fx; S.force[cap + j] = r.fy; S.force[2 * cap + j] = r.fz;
+    S.uid[j] = r.uid;
+    S.partners[j] = r.partners;
+    S.flags[j] = as_ghost ? (r.flags | ABS_FLAG_GHOST) : static_cast<unsigned char>(r.flags & ~ABS_FLAG_GHOST);
+    S.beh[j] = r.beh;
+  }
+}
+
+__global__ void k_keep_ghostless(const Soa S, unsigned long long n, unsigned int* __restrict__ keep) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    keep[i] = (S.flags[i] & ABS_FLAG_GHOST) ? 0u : 1u;
+}
+
+// Order-preserving stream compaction of the population by keep[] (exclusive
+// scan in `dst_index`): survivors move to S[dst] / dst_pos.
+__global__ void k_compact(const Pd* __restrict__ pos, Soa src, Pd* __restrict__ dst_pos, Soa dst,
+                          const unsigned int* __restrict__ keep, const unsigned int* __restrict__ dst_index,
+                          unsigned long long n, unsigned long long cap) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    const unsigned long long j = dst_index[i];
+    dst_pos[j] = load_pd(pos + i);
+    dst.uid[j] = src.uid[i];
+    dst.flags[j] = src.flags[i];
+    dst.partners[j] = src.partners[i];
+    dst.beh[j] = src.beh[i];
+    dst.vol[j] = src.vol[i];
+    dst.force[j] = src.force[i];
+    dst.force[cap + j] = src.force[cap + i];
+    dst.force[2 * cap + j] = src.force[2 * cap + i];
+  }
+}
+
 // ------------------------------------------------------------ parity helpers
 __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* out) {
   const DevGrid G = *g;
@@ -2093,6 +2182,99 @@ int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
   CK(cudaStreamSynchronize(c->stream));
   if (h.nonfinite) return set_err(c, ABS_ERR_NONFINITE, "agent positions are not finite");
   return ABS_OK;
+}
+
+// Keep only agents with keep[i] (already filled for the current population).
+static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
+  unsigned int* keep = c->rank;  // scratch: rank[] is rewritten by the next k_key
+  unsigned int* idx = c->key;
+  CK(cudaMemcpyAsync(idx, keep, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  unsigned long long* len = nullptr;
+  CK(dalloc(&len, 1));
+  CK(cudaMemcpyAsync(len, &n, 8, cudaMemcpyHostToDevice, c->stream));
+  unsigned int* tiles = nullptr;
+  CK(dalloc(&tiles, n / kScanTile + 2));
+  launch_scan<unsigned int>(c, idx, len, n, tiles, nullptr);  // idx[n] = survivors
+  const int nxt = c->cur ^ 1;
+  k_compact<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur], c->S[nxt].pd, c->S[nxt], keep,
+                                                           idx, n, c->cap);
+  ++c->launches;
+  unsigned int kept = 0;
+  CK(cudaMemcpyAsync(&kept, idx + n, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(len);
+  cudaFree(tiles);
+  const unsigned long long nn = kept;
+  CK(cudaMemcpyAsync(&c->g->n, &nn, 8, cudaMemcpyHostToDevice, c->stream));
+  if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->cur = nxt;
+  c->pos_in_new = false;
+  c->grid_valid = false;
+  c->n = nn;
+  return ABS_OK;
+}
+
+int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* dims, int64_t lo, int64_t hi, int mode,
+                          void* out_lo, void* out_hi, uint64_t cap, uint64_t* n_lo, uint64_t* n_hi) {
+  if (!c || !grid || !dims || (mode != 0 && mode != 1)) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  const unsigned long long n = h.n;
+  unsigned long long* counts = nullptr;
+  CK(dalloc(&counts, 2));
+  CK(cudaMemsetAsync(counts, 0, 16, c->stream));
+  if (n) {
+    k_export<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(
+        cur_pos(c), c->S[c->cur], c->cap, n, grid[2], grid[3], dims[2], lo, hi, mode, static_cast<Rec*>(out_lo),
+        static_cast<Rec*>(out_hi), cap, counts, mode == 0 ? c->rank : nullptr);
+    ++c->launches;
+  }
+  unsigned long long hc[2] = {0, 0};
+  CK(cudaMemcpyAsync(hc, counts, 16, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(counts);
+  if (n_lo) *n_lo = hc[0];
+  if (n_hi) *n_hi = hc[1];
+  if (hc[0] > cap || hc[1] > cap) return set_err(c, ABS_ERR_CAPACITY, "export buffer too small");
+  if (mode == 0 && (hc[0] || hc[1])) return compact_population(c, n);
+  return ABS_OK;
+}
+
+int abs_gpu_import(abs_gpu_ctx* c, const void* records, uint64_t count, int as_ghost) {
+  if (!c || (count && !records)) return ABS_ERR_INVALID_ARGUMENT;
+  if (!count) return ABS_OK;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  const unsigned long long n = h.n;
+  rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * (n + count) + 1024), n);
+  if (rc) return rc;
+  k_import<<<grid_blocks(c, count), kThreads, 0, c->stream>>>(static_cast<const Rec*>(records), count, n, cur_pos(c),
+                                                              c->S[c->cur], c->cap, as_ghost);
+  ++c->launches;
+  const unsigned long long nn = n + count;
+  CK(cudaMemcpyAsync(&c->g->n, &nn, 8, cudaMemcpyHostToDevice, c->stream));
+  if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->grid_valid = false;
+  c->n = nn;
+  return ABS_OK;
+}
+
+int abs_gpu_drop_ghosts(abs_gpu_ctx* c) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (!h.n) return ABS_OK;
+  k_keep_ghostless<<<grid_blocks(c, h.n), kThreads, 0, c->stream>>>(c->S[c->cur], h.n, c->rank);
+  ++c->launches;
+  return compact_population(c, h.n);
 }
 
 int abs_gpu_sir_counts(abs_gpu_ctx* c, uint64_t* out3) {

@@ -274,3 +274,138 @@ def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, m
     L = layer_bounds(int(g.dims[2]), world)
     lay = box_layer(st["z"], g)
     return _take(st, np.nonzero((lay >= L[rank]) & (lay < L[rank + 1]))[0])
+
+
+class DeviceSlabDecomposition:
+    """The same decomposition with a device-resident population: agents stay
+    in the rank's HBM; per iteration only the 7-double bounds, migrants and
+    the two boundary layers (packed 96-byte records, ABS_RECORD_BYTES) move.
+    transport="nccl": CUDA tensors straight through torch.distributed (NCCL
+    over NVLink); transport="host": staged through host tensors (gloo) — used
+    to test several ranks sharing one GPU."""
+
+    RECORD = 96
+
+    def __init__(self, sim, dist, rank: int, world: int, fixed_box_length: float = 0.0,
+                 transport: str = "nccl", cap: int = 1 << 20):
+        import torch
+        self.sim, self.dist, self.rank, self.world = sim, dist, rank, world
+        self.fixed_box_length = fixed_box_length
+        self.transport = transport
+        self.torch = torch
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self._alloc(cap)
+        self.evals = 0
+        self.skips = 0
+        self.iteration = 0
+
+    def _alloc(self, cap):
+        t = self.torch
+        self.cap = cap
+        self.buf = {k: t.empty(cap * self.RECORD, dtype=t.uint8, device=self.dev)
+                    for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
+
+    # -- collectives -----------------------------------------------------------
+    def _coll_tensor(self, a):
+        t = self.torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(self.dev) if self.transport == "nccl" else t
+
+    def _allreduce(self, a, op):
+        t = self._coll_tensor(a)
+        self.dist.all_reduce(t, op=op)
+        return t.cpu().numpy()
+
+    def _exchange(self, n_lo: int, n_hi: int):
+        """Send send_lo[:n_lo] to r-1 and send_hi[:n_hi] to r+1; returns the
+        received record counts (from r-1, from r+1) into recv_lo / recv_hi."""
+        t, d, r, w = self.torch, self.dist, self.rank, self.world
+        peers = [(p, n, sk, rk) for p, n, sk, rk in ((r - 1, n_lo, "send_lo", "recv_lo"),
+                                                   (r + 1, n_hi, "send_hi", "recv_hi")) if 0 <= p < w]
+        ops, cnt = [], {}
+        for p, n, _, _ in peers:
+            cs = self._coll_tensor(np.array([n], np.int64))
+            cr = self._coll_tensor(np.zeros(1, np.int64))
+            ops += [d.isend(cs, p), d.irecv(cr, p)]
+            cnt[p] = cr
+        for o in ops:
+            o.wait()
+        got = {p: int(cnt[p].cpu().item()) for p, *_ in peers}
+        need = max([n for _, n, _, _ in peers] + list(got.values()) + [0])
+        if need > self.cap:
+            raise RuntimeError("halo larger than the exchange buffers")
+        ops, staged = [], []
+        for p, n, sk, rk in peers:
+            nb, mb = n * self.RECORD, got[p] * self.RECORD
+            if self.transport == "nccl":
+                if nb:
+                    ops.append(d.isend(self.buf[sk][:nb], p))
+                if mb:
+                    ops.append(d.irecv(self.buf[rk][:mb], p))
+            else:
+                if nb:
+                    ops.append(d.isend(self.buf[sk][:nb].cpu(), p))
+                if mb:
+                    host = t.empty(mb, dtype=t.uint8)
+                    ops.append(d.irecv(host, p))
+                    staged.append((rk, host))
+        for o in ops:
+            o.wait()
+        for rk, host in staged:
+            self.buf[rk][:host.numel()].copy_(host.to(self.dev))
+        # the engine consumes the buffers on its own CUDA stream: make the
+        # received bytes (NCCL / staging copies on torch's stream) visible first
+        t.cuda.current_stream().synchronize()
+        return (got.get(r - 1, 0), got.get(r + 1, 0))
+
+    # -- one iteration -------------------------------------------------------------
+    def _export(self, g, lo, hi, mode):
+        from . import _native as N
+        import ctypes as C
+        grid, dims = g.as_override()
+        grid = np.ascontiguousarray(grid)
+        dims = np.ascontiguousarray(dims, np.uint32)
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        rc = N.load().abs_gpu_export_layers(self.sim._ctx, grid.ctypes.data_as(C.POINTER(C.c_double)),
+                                            dims.ctypes.data_as(C.POINTER(C.c_uint32)), int(lo), int(hi), mode,
+                                            self.buf["send_lo"].data_ptr(), self.buf["send_hi"].data_ptr(),
+                                            self.cap, C.byref(a), C.byref(b))
+        N.check(rc, self.sim._ctx)
+        return int(a.value), int(b.value)
+
+    def _import(self, key, count, ghost):
+        from . import _native as N
+        if count:
+            N.check(N.load().abs_gpu_import(self.sim._ctx, self.buf[key].data_ptr(), count, 1 if ghost else 0),
+                    self.sim._ctx)
+
+    def step(self):
+        from . import _native as N
+        b = self.sim.local_bounds()
+        red = self._allreduce(np.concatenate([-b[:3], b[3:]]), self.dist.ReduceOp.MAX)
+        g = global_grid(np.concatenate([-red[:3], red[3:]]), self.fixed_box_length)
+        L = layer_bounds(int(g.dims[2]), self.world)
+        lo, hi = L[self.rank], L[self.rank + 1]
+        n_lo, n_hi = self._export(g, lo, hi, 0)            # migrants leave
+        got_lo, got_hi = self._exchange(n_lo, n_hi)
+        self._import("recv_lo", got_lo, False)
+        self._import("recv_hi", got_hi, False)
+        n_lo, n_hi = self._export(g, lo, hi, 1)            # boundary layers
+        got_lo, got_hi = self._exchange(n_lo, n_hi)
+        self._import("recv_lo", got_lo, True)
+        self._import("recv_hi", got_hi, True)
+        grid, dims = g.as_override()
+        self.sim.set_grid_override(grid, dims)
+        r0 = self.sim.report()
+        self.sim.simulate(1)
+        r1 = self.sim.report()
+        N.check(N.load().abs_gpu_drop_ghosts(self.sim._ctx), self.sim._ctx)
+        tot = self._allreduce(np.array([r1.force_evaluations - r0.force_evaluations,
+                                        r1.force_skips - r0.force_skips], np.int64), self.dist.ReduceOp.SUM)
+        self.evals += int(tot[0])
+        self.skips += int(tot[1])
+        self.iteration += 1
+        return g
+
+    def simulate(self, iterations: int):
+        for _ in range(iterations):
+            self.step()

@@ -159,3 +159,47 @@ def test_gpu_ranks_match_single_domain(oracle_mod, world, case):
     assert np.array_equal(got["flags"], o["flags"])
     c = ref.counts()
     assert (int(parts[0]["evals"]), int(parts[0]["skips"])) == (c["force_evaluations"], c["force_skips"])
+
+
+def _dev_worker(rank, world, port, case, outdir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2301_06984_b200 as E
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    wl, steps = _make(case)
+    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=wl.mask)
+    sim = E.Simulation(E.SimulationParams(**wl.params), device=0)
+    sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=st["beh"], uid=st["uid"], uid_count=wl.n)
+    dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="host", cap=1 << 14)
+    dec.simulate(steps)
+    a = sim.agents()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), evals=dec.evals, skips=dec.skips, **a)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3")])
+def test_device_exchange_matches_single_domain(oracle_mod, world, case):
+    """Device-resident exchange (export/import kernels, packed records): the
+    union of the ranks' populations equals the single-domain run."""
+    O = oracle_mod
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_dev_worker, args=(world, _free_port(), case, tmp), nprocs=world, join=True)
+        parts = [dict(np.load(os.path.join(tmp, f"r{r}.npz"))) for r in range(world)]
+    keys = ["uid", "x", "y", "z", "d", "partners", "flags"]
+    got = by_uid({k: np.concatenate([p[k] for p in parts]) for k in keys})
+    wl, steps = _make(case)
+    ref = O.PortSim(_oparams(O, wl), wl.x, wl.y, wl.z, wl.d, wl.mask)
+    ref.simulate(steps)
+    o = by_uid(ref.dump())
+    assert np.array_equal(got["uid"], o["uid"])
+    for k in ("x", "y", "z", "d"):
+        assert_close(got[k], o[k], 1e-9, 1.0, k)
+    assert np.array_equal(got["partners"], o["partners"])
+    assert np.array_equal(got["flags"], o["flags"])
+    c = ref.counts()
+    assert (int(parts[0]["evals"]), int(parts[0]["skips"])) == (c["force_evaluations"], c["force_skips"])
