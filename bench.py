@@ -227,6 +227,7 @@ def run_decomposed(args, dist, world, rank, local):
     dist.all_reduce(owned)
     total = float(owned.item())
     value = total * args.steps / (ms_max / 1e3)
+    evals_per_agent_step = dec.evals / max(1.0, total * (args.steps + args.warmup))
 
     # end to end per rank through the public API with HOST buffers: upload the
     # rank's slab from page-locked memory, one decomposed iteration (bounds
@@ -268,7 +269,7 @@ def run_decomposed(args, dist, world, rank, local):
                               "achieved_per_gpu": step_bytes / (ms_max / 1e3) / 1e9,
                               "frac": step_bytes / (ms_max / 1e3) / 1e9 / hbm},
             "clocks": clk.summary(),
-            "force_evaluations_per_agent_step": dec.evals / max(1.0, total * (args.steps + args.warmup)),
+            "force_evaluations_per_agent_step": evals_per_agent_step,
             "e2e": e2e, "gpu_launches": int(launches.item()),
             "gpu_launches_note": "all ranks: engine kernels + export/import/compaction",
         }))

@@ -75,7 +75,9 @@ typedef struct {
   double max_displacement;       /* 3.0 */
   double force_threshold;        /* 0.0 */
   double fixed_box_length;       /* 0.0 = follow the largest diameter */
-  uint64_t sorting_frequency;    /* 0 = never (storage is re-binned every step) */
+  uint64_t sorting_frequency;    /* 0 = never; f > 0: the reference's Morton sort_and_balance order is
+                                    applied before every iteration with iteration % f == 0
+                                    (simulation.cpp:246-247); storage is re-binned every step anyway */
   int32_t detect_static_agents;  /* 0 */
   int32_t model;                 /* ABS_MODEL_* */
   double model_params[8];

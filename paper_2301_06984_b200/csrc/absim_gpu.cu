@@ -340,8 +340,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
     const Pd p = load_pd(pos + i);
     reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
-    if (ABS_PREFILTER)
-      pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
+    pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
                           static_cast<float>(p.z - g->origin[2]), static_cast<float>(p.d));
     dst.uid[j] = src.uid[i];
     dst.flags[j] = src.flags[i];
@@ -432,27 +431,42 @@ struct Daughter {
 // index). `walk(r, r2, visit)` enumerates every candidate j != i with exact
 // fp64 d2 <= r2 in a fixed order; `fetch(j)` returns candidate j's Pd;
 // `uid_of(j)` its uid. `ovl` is this thread's column of the contact list.
-template <int MODEL, bool STATIC, bool RECORD, class OvlT, class Walk, class Fetch, class UidOf>
+// LPA > 1: the LPA lanes of an aligned group run this together for the same
+// agent — every lane walks its share of the candidates (the walk deals them
+// out), the partial forces / partner counts are combined with a butterfly
+// (commutative pairwise adds: every lane ends with the same bits, and the
+// result is a fixed function of the storage order), and only the group's
+// leader lane writes agent state. All other decisions are group-uniform.
+// F32: `walk` is the fp32-classified walker (visit(j, df2, qd) for exactly
+// the candidates with fp64 d2 <= r^2); the contact record test is then the
+// conservative fp32 superset df2 < (h + slack)^2 (pass B decides exactly).
+template <int MODEL, bool STATIC, bool RECORD, int LPA = 1, bool F32 = false, class OvlT, class Walk, class Fetch,
+          class UidOf>
 __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, unsigned long long i, const Pd& me,
                                                double dmax, unsigned char* __restrict__ nv,
                                                unsigned char* __restrict__ nn, const StepArgs& a,
                                                unsigned long long cap, OvlT* ovl, int ovl_stride,
                                                unsigned long long& n_eval, unsigned long long& n_skip,
-                                               Walk&& walk, Fetch&& fetch, UidOf&& uid_of) {
+                                               Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f) {
   Daughter dg{false, 0, 0, 0, 0, 0, 0};
+  const bool leader = LPA == 1 || (threadIdx.x & (LPA - 1)) == 0;
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
   dg.parent = my_uid;
   if (fl & kFlagGhost) {  // halo copy of another rank's agent: candidate only
-    if (STATIC) {
-      nv[i] = 0;
-      nn[i] = 0;
+    if (leader) {
+      if (STATIC) {
+        nv[i] = 0;
+        nn[i] = 0;
+      }
+      reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
+      reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
     }
-    reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
-    reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
     return dg;
   }
   // --- staticness phase 2 (simulation.cpp:375-384) -----------------------
+  // (the nv / nn resets and the volume update are written at the end, by the
+  // leader, after every lane of the group has read them)
   if (STATIC) {
     if (a.iteration == 0) {
       fl = 0;  // :335-349 everyone participates, flags wiped
@@ -461,12 +475,12 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
                                 ABS_FLAG_NEIGHBOR_VIOLATION | ABS_FLAG_NEW_NEIGHBOR)) &&
                         !nv[i] && !nn[i] && S.partners[i] <= 1u;
       fl = skip ? ABS_FLAG_STATIC : 0;
-      nv[i] = 0;
-      nn[i] = 0;
     }
   }
   // --- behaviours (run before forces, simulation.cpp:389-394) -------------
   double tx = 0.0, ty = 0.0, tz = 0.0, tg = 0.0;
+  double new_vol = 0.0;
+  bool vol_changed = false;
   if (MODEL != ABS_MODEL_NONE && S.beh[i]) {
     if (MODEL == ABS_MODEL_PROLIFERATION) {
       double v = S.vol[i] + a.mp[0];
@@ -480,9 +494,10 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         dg.z = me.z + dir[2] * half;
         dg.d = abs_diameter_of_volume(v);
         dg.vol = v;
-        dg.divides = true;
+        dg.divides = leader;
       }
-      S.vol[i] = v;
+      new_vol = v;
+      vol_changed = true;
       tg += abs_diameter_of_volume(v) - me.d;
     } else if (MODEL == ABS_MODEL_DRIVE) {
       double dl[3];
@@ -505,22 +520,35 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
   // d2 < h^2 (1 + 2^-50) is a strict superset of that (sqrt is correctly
   // rounded and monotone), so no contributor is missed and every decision in
   // pass B is the reference's exact one.
+  bool wrote_partners = false;
+  unsigned int contributors = 0;
+  double fx = 0.0, fy = 0.0, fz = 0.0;
   if (STATIC && (fl & ABS_FLAG_STATIC)) {
-    ++n_skip;
+    if (leader) ++n_skip;
   } else {
     const double r = 0.5 * (me.d + dmax);
     unsigned int evals = 0, nov = 0;
-    walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
-      ++evals;
-      const double h = 0.5 * (me.d + q.d);
-      if (d2 < h * h * (1.0 + 0x1.0p-50)) {
-        if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
-        ++nov;
-      }
-    });
+    const float dif = static_cast<float>(me.d);
+    if constexpr (F32) {
+      walk(r, r * r, [&](unsigned int j, float df2, float qd) {
+        ++evals;
+        const float hp = 0.5f * (dif + qd) + slack;
+        if (df2 < hp * hp * 1.0000005f) {
+          if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+          ++nov;
+        }
+      });
+    } else {
+      walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
+        ++evals;
+        const double h = 0.5 * (me.d + q.d);
+        if (d2 < h * h * (1.0 + 0x1.0p-50)) {
+          if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+          ++nov;
+        }
+      });
+    }
     n_eval += evals;
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    unsigned int contributors = 0;
     const double k = a.k;
     auto contact = [&](unsigned int j) {
       const Pd q = fetch(j);
@@ -545,20 +573,36 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         fz += f2;
       }
     };
-    if (nov <= kMaxContacts) {
+    bool overflow = nov > kMaxContacts;
+    if (LPA > 1) overflow = (__ballot_sync(group_mask<LPA>(), overflow) & group_mask<LPA>()) != 0u;
+#if defined(ABS_ABLATE) && ABS_ABLATE >= 2
+    if (nov > 1000000u) overflow = false;  // timing ablation: no pass B
+    else nov = 0;
+#endif
+    if (!overflow) {
       for (unsigned int c = 0; c < nov; ++c) contact(ovl[c * ovl_stride]);
-    } else {  // more contacts than the list holds: re-walk (rare)
+    } else if constexpr (F32) {  // more contacts than the list holds: re-walk (rare)
+      walk(r, r * r, [&](unsigned int j, float df2, float qd) {
+        const float hp = 0.5f * (dif + qd) + slack;
+        if (df2 < hp * hp * 1.0000005f) contact(j);
+      });
+    } else {
       walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
         const double h = 0.5 * (me.d + q.d);
         if (d2 < h * h * (1.0 + 0x1.0p-50)) contact(j);
       });
     }
-    if (RECORD) {
-      S.force[i] = fx;
-      S.force[cap + i] = fy;
-      S.force[2 * cap + i] = fz;
+    if (LPA > 1) {
+      const unsigned int gm = group_mask<LPA>();
+#pragma unroll
+      for (int off = LPA / 2; off; off >>= 1) {
+        fx += __shfl_xor_sync(gm, fx, off, LPA);
+        fy += __shfl_xor_sync(gm, fy, off, LPA);
+        fz += __shfl_xor_sync(gm, fz, off, LPA);
+        contributors += __shfl_xor_sync(gm, contributors, off, LPA);
+      }
     }
-    S.partners[i] = contributors;
+    wrote_partners = true;
     if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
       tx += fx * a.dt;
       ty += fy * a.dt;
@@ -585,9 +629,24 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     np.d = nd > 1e-9 ? nd : 1e-9;
     if (tg > 0.0) fl |= ABS_FLAG_GREW;
   }
-  reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
-  reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
-  S.flags[i] = fl;
+  if (leader) {
+    if (STATIC && a.iteration != 0) {
+      nv[i] = 0;
+      nn[i] = 0;
+    }
+    if (vol_changed) S.vol[i] = new_vol;
+    if (wrote_partners) {
+      if (RECORD) {
+        S.force[i] = fx;
+        S.force[cap + i] = fy;
+        S.force[2 * cap + i] = fz;
+      }
+      S.partners[i] = contributors;
+    }
+    reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
+    reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
+    S.flags[i] = fl;
+  }
   return dg;
 }
 
@@ -628,7 +687,7 @@ __device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsign
 // Global-gather force kernel: one agent per thread, candidates fetched from
 // HBM/L2 through the per-lane flat window stream. Used for small tiles'
 // overflow and as the reference implementation of the tiled kernel below.
-template <int MODEL, bool STATIC, bool RECORD>
+template <int MODEL, bool STATIC, bool RECORD, bool F32>
 __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
@@ -660,6 +719,14 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
     if (i < n) {
       const Pd me = load_pd(S.pd + i);
       const unsigned int self = static_cast<unsigned int>(i);
+      if (F32 && !box_mode) {
+        dg = agent_step<MODEL, STATIC, RECORD, 1, true>(
+            S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
+            [&](double r, double r2, auto&& visit) {
+              for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2, visit);
+            },
+            [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, Q.slack);
+      } else
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
           [&](double r, double r2, auto&& visit) {
@@ -674,6 +741,55 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
                                        visit(j, q, d2);
                                      });
             }
+          },
+          [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
+    }
+    if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+  }
+  flush_counters(n_eval, n_skip, gw);
+}
+
+// Group-cooperative force kernel: LPA lanes per agent (for_each_neighbor_group).
+// A warp runs 32 / LPA consecutive agents (cell order) at a time; candidate
+// loads of a group are consecutive records of one bin row, so a warp load
+// touches ~32/LPA row segments instead of 32 unrelated lines (the per-lane
+// kernel above is L1-wavefront bound on exactly that). Persistent warps
+// sweep the agent array in a static warp-strided order, as in k_force.
+template <int MODEL, bool STATIC, bool RECORD, int LPA>
+__global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
+    k_force_g(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
+              unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
+              unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
+              unsigned int* __restrict__ div_mark) {
+  if (gp->err) return;
+  __shared__ QGrid Q;
+  __shared__ unsigned int rows[kForceThreads / LPA][kGroupRowWords];
+  __shared__ unsigned int ovl[kMaxContacts][kForceThreads];
+  if (threadIdx.x == 0) Q = make_qgrid(*gp);
+  __syncthreads();
+  const unsigned long long n = gp->n;
+  const double dmax = gp->dmax;
+  constexpr int G = 32 / LPA;  // agents per warp per sweep step
+  unsigned long long n_eval = 0, n_skip = 0;
+  const int lane = threadIdx.x & 31;
+  unsigned int* my_rows = rows[threadIdx.x / LPA];
+  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
+    const unsigned long long base = chunk * G;
+    if (base >= n) break;
+    const unsigned long long i = base + lane / LPA;
+    Daughter dg{false, 0, 0, 0, 0, 0, 0};
+    if (i < n) {  // group-uniform
+      const Pd me = load_pd(S.pd + i);
+      const unsigned int self = static_cast<unsigned int>(i);
+      dg = agent_step<MODEL, STATIC, RECORD, LPA>(
+          S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
+          [&](double r, double r2, auto&& visit) {
+            for_each_neighbor_group<LPA>(Q, S.pd, start, my_rows, self, me.x, me.y, me.z, r, r2,
+                                         [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                                           visit(j, q, d2);
+                                         });
           },
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
     }
@@ -1360,9 +1476,17 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
 
 // sort key = (morton code of the reference box) << 32 | (~storage index):
 // ascending key = curve order, descending index inside a box (chain order).
-__global__ void k_sort_keys(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* keyhi,
+__global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned long long* keyhi,
                             unsigned int* __restrict__ idx) {
   const DevGrid G = *g;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // passes over the used key bits, rounded up to even
+    const unsigned int maxdim = max(G.dims[0], max(G.dims[1], G.dims[2]));
+    unsigned int axis_bits = 0;
+    while ((1u << axis_bits) < maxdim) ++axis_bits;
+    const unsigned int code_bits = (G.dims[2] == 1 ? 2u : 3u) * axis_bits;
+    unsigned int passes = (32u + code_bits + 7u) / 8u;
+    g->sort_passes = passes + (passes & 1u);
+  }
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd p = load_pd(pos + i);
@@ -1388,9 +1512,13 @@ __device__ __forceinline__ unsigned int radix_digit(unsigned long long code, uns
 
 // One LSD radix pass (8 bits) over (key, idx) pairs with a stable
 // counting sort per digit: histogram -> scan -> rank by prefix popcounts.
+// Passes at or beyond g->sort_passes are skipped (they come in pairs, so the
+// host's ping-pong buffer order stays right without reading the grid back).
 __global__ void k_radix_hist(const unsigned long long* __restrict__ key, const unsigned int* __restrict__ idx,
-                             unsigned long long n, int shift, unsigned int* __restrict__ hist,
+                             const DevGrid* g, int shift, unsigned int* __restrict__ hist,
                              unsigned long long chunk) {
+  if (shift / 8 >= static_cast<int>(g->sort_passes)) return;
+  const unsigned long long n = g->n;
   __shared__ unsigned int h[256];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) h[t] = 0;
   __syncthreads();
@@ -1404,8 +1532,10 @@ __global__ void k_radix_hist(const unsigned long long* __restrict__ key, const u
 
 __global__ void k_radix_scatter(const unsigned long long* __restrict__ key, const unsigned int* __restrict__ idx,
                                 unsigned long long* __restrict__ key2, unsigned int* __restrict__ idx2,
-                                unsigned long long n, int shift, const unsigned int* __restrict__ hist,
+                                const DevGrid* g, int shift, const unsigned int* __restrict__ hist,
                                 unsigned long long chunk) {
+  if (shift / 8 >= static_cast<int>(g->sort_passes)) return;
+  const unsigned long long n = g->n;
   // one warp per block walks its chunk in order: stable by construction
   __shared__ unsigned int base[256];
   for (int t = threadIdx.x; t < 256; t += blockDim.x) base[t] = hist[t * gridDim.x + blockIdx.x];
@@ -1440,7 +1570,9 @@ __global__ void k_radix_scatter(const unsigned long long* __restrict__ key, cons
 }
 
 __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const unsigned int* __restrict__ perm,
-                         unsigned long long n, unsigned long long cap, int carry_vol, int carry_force) {
+                         const DevGrid* g, unsigned long long cap, int carry_vol, int carry_force) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
   for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < n;
        j += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned int i = perm[j];
@@ -1529,7 +1661,7 @@ struct abs_gpu_ctx {
   Soa S[2]{};
   int cur = 0;
   Pd* newpd = nullptr;
-  float4* pf = nullptr;  // fp32 copy of pd relative to the grid origin (ABS_PREFILTER)
+  float4* pf = nullptr;  // fp32 copy of pd relative to the grid origin (candidate classification)
   bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
   bool grid_valid = false; // `start` holds a scanned cell table for S[cur]
 
@@ -1545,6 +1677,13 @@ struct abs_gpu_ctx {
   Pd* st_pd = nullptr;
   double* st_vol = nullptr;
   unsigned int* div_mark = nullptr;  // uid_cap + 1
+  // Morton sort scratch (capacity-sized, allocated on first use)
+  unsigned long long sort_cap = 0;
+  unsigned long long *sort_k[2] = {nullptr, nullptr};
+  unsigned int *sort_i[2] = {nullptr, nullptr};
+  unsigned int* sort_hist = nullptr;
+  unsigned int* sort_tiles = nullptr;
+  unsigned long long* sort_hlen = nullptr;
 
   void* pinned = nullptr;  // host staging for downloads (page-locked)
   size_t pinned_bytes = 0;
@@ -1579,11 +1718,12 @@ int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
 }
 
-int force_blocks(const abs_gpu_ctx* c) {  // persistent: the resident CTAs only
+template <class K>
+int force_blocks(const abs_gpu_ctx* c, K kernel) {  // persistent: the resident CTAs only
   int per_sm = 0;
-  cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<ABS_MODEL_NONE, false, false>, kForceThreads,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kForceThreads,
                                                 (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
   return c->sms * std::max(per_sm, 1);
 }
@@ -1652,7 +1792,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   cudaFree(c->tiles64);
   cudaFree(c->pf);
   c->pf = nullptr;
-  if (ABS_PREFILTER) CK(dalloc(&c->pf, ncap));
+  CK(dalloc(&c->pf, ncap));
   CK(dalloc(&c->key, ncap));
   CK(dalloc(&c->rank, ncap));
   CK(dalloc(&c->nv, ncap));
@@ -1714,16 +1854,17 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
 // Auto (bins_per_box == 0): when the typical query radius 0.5 (d + dmax) is
 // close to the box (mean d / dmax > 0.75, e.g. config 1) all 27 boxes are
 // needed anyway and the box-lockstep walk (bins == boxes) wins; with a wide
-// diameter spread (config 4) 2x2x2 sub-bins cut the candidates 2x.
+// diameter spread (config 4) 2x2 sub-bins in y/z and 3 along x cut the
+// candidates ~2x (c4 @ 2^24: 2x2x2 7.77 ms, 3 along x 7.50 ms, 2x3x3 8.55 ms).
 unsigned int bins_yz(const abs_gpu_ctx* c) {
   if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box;
-  return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 2));
+  return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 4));
 }
-unsigned int bins_x(const abs_gpu_ctx* c) {
+unsigned int bins_x(const abs_gpu_ctx* c) {  // auto: 3 along x with 2x2 in y/z (c4 sweep)
   if (c->cfg.model == ABS_MODEL_SIR) return 1u;
   const int b = c->cfg.bins_per_box_x;
-  return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 2));
+  return b <= 0 ? (c->auto_bins == 2u ? 3u : c->auto_bins) : static_cast<unsigned int>(std::min(b, 4));
 }
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
@@ -1776,19 +1917,81 @@ bool use_tile_kernel() {
 
 constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
 
+// ABSIM_F32=0 disables the fp32-classified candidate walk (A/B switch).
+bool use_f32_walk() {
+  static const int v = [] {
+    const char* e = std::getenv("ABSIM_F32");
+    return (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+template <int MODEL, bool STATIC, bool RECORD, bool F32>
+void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+  static int blocks = 0;  // per template instance
+  if (!blocks) {
+    cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kForceSmem);
+    blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, F32>);
+  }
+  k_force<MODEL, STATIC, RECORD, F32><<<blocks, kForceThreads, kForceSmem, c->stream>>>(
+      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+}
+
 template <int MODEL, bool STATIC, bool RECORD>
 void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  static bool configured = false;  // per template instance
-  if (!configured) {
-    cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kForceSmem);
-    configured = true;
+  if (use_f32_walk()) launch_gather_f<MODEL, STATIC, RECORD, true>(c, S, a);
+  else launch_gather_f<MODEL, STATIC, RECORD, false>(c, S, a);
+}
+
+// Lanes per agent of the group kernel: ABSIM_LPA in {1 (per-lane k_force), 2,
+// 4, 8, 16, 32}; default 1 (measured fastest on c4).
+// Box mode (bins == boxes) keeps the lockstep walk.
+#ifndef ABS_GROUP_KERNEL
+#define ABS_GROUP_KERNEL 0  // -DABS_GROUP_KERNEL=1 builds the LPA > 1 variants
+#endif
+int lanes_per_agent() {
+  static const int v = [] {
+    const char* e = std::getenv("ABSIM_LPA");
+    const int x = e ? std::atoi(e) : 1;
+    return (ABS_GROUP_KERNEL && (x == 2 || x == 4 || x == 8 || x == 16 || x == 32)) ? x : 1;
+  }();
+  return v;
+}
+
+template <int MODEL, bool STATIC, bool RECORD, int LPA>
+void launch_group_l(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+  static int blocks = 0;  // per template instance: resident CTAs
+  if (!blocks) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_g<MODEL, STATIC, RECORD, LPA>, kForceThreads, 0);
+    blocks = c->sms * std::max(per_sm, 1);
   }
-  k_force<MODEL, STATIC, RECORD><<<force_blocks(c), kForceThreads, kForceSmem, c->stream>>>(
-      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+  k_force_g<MODEL, STATIC, RECORD, LPA><<<blocks, kForceThreads, 0, c->stream>>>(
+      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+}
+
+template <int MODEL, bool STATIC, bool RECORD>
+void launch_group(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+#if ABS_GROUP_KERNEL
+  switch (lanes_per_agent()) {
+    case 2: launch_group_l<MODEL, STATIC, RECORD, 2>(c, S, a); break;
+    case 4: launch_group_l<MODEL, STATIC, RECORD, 4>(c, S, a); break;
+    case 16: launch_group_l<MODEL, STATIC, RECORD, 16>(c, S, a); break;
+    case 32: launch_group_l<MODEL, STATIC, RECORD, 32>(c, S, a); break;
+    default: launch_group_l<MODEL, STATIC, RECORD, 8>(c, S, a); break;
+  }
+#endif
 }
 
 template <int MODEL, bool STATIC>
 void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
+  const bool box_mode = bins_x(c) == 1u && bins_yz(c) == 1u;
+  if (!use_tile_kernel() && !box_mode && lanes_per_agent() > 1) {
+    if (c->cfg.record_forces) launch_group<MODEL, STATIC, true>(c, S, a);
+    else launch_group<MODEL, STATIC, false>(c, S, a);
+    return;
+  }
   if (use_tile_kernel()) {
     if (c->cfg.record_forces) launch_tile<MODEL, STATIC, true>(c, S, a);
     else launch_tile<MODEL, STATIC, false>(c, S, a);
@@ -1978,6 +2181,8 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   return ABS_OK;
 }
 
+static void free_sort_scratch(abs_gpu_ctx* c);
+
 int abs_gpu_destroy(abs_gpu_ctx* c) {
   if (!c) return ABS_OK;
   cudaSetDevice(c->device);
@@ -1987,6 +2192,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
+  free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -2086,6 +2292,73 @@ int abs_gpu_upload_device(abs_gpu_ctx* c, uint64_t n, const uint64_t* uid, const
                        nullptr);
 }
 
+static void free_sort_scratch(abs_gpu_ctx* c) {
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->sort_k[b]);
+    cudaFree(c->sort_i[b]);
+    c->sort_k[b] = nullptr;
+    c->sort_i[b] = nullptr;
+  }
+  cudaFree(c->sort_hist); cudaFree(c->sort_tiles); cudaFree(c->sort_hlen);
+  c->sort_hist = nullptr;
+  c->sort_tiles = nullptr;
+  c->sort_hlen = nullptr;
+  c->sort_cap = 0;
+}
+
+constexpr unsigned long long kSortChunk = 4096;
+
+// sort_and_balance (sort_balance.cpp:22-148) on the device, stream-ordered and
+// without host synchronisation: grid of the current state (no re-binning),
+// (Morton code << 32 | ~index) keys, 12 8-bit LSD pass slots of which the
+// device runs sort_passes, gather into the other state buffer. Callable
+// inside the iteration loop (sorting_frequency, simulation.cpp:246-247).
+static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
+  if (c->sort_cap != c->cap) {
+    free_sort_scratch(c);
+    const unsigned long long blocks = (c->cap + kSortChunk - 1) / kSortChunk;
+    for (int b = 0; b < 2; ++b) {
+      CK(dalloc(&c->sort_k[b], c->cap));
+      CK(dalloc(&c->sort_i[b], c->cap));
+    }
+    const unsigned long long hlen = 256ull * blocks;
+    CK(dalloc(&c->sort_hist, hlen + 1));
+    CK(dalloc(&c->sort_tiles, hlen / kScanTile + 2));
+    CK(dalloc(&c->sort_hlen, 1));
+    CK(cudaMemcpyAsync(c->sort_hlen, &hlen, 8, cudaMemcpyHostToDevice, c->stream));
+    c->sort_cap = c->cap;
+  }
+  const Pd* pos = cur_pos(c);
+  if (c->grid_valid) {  // the sort leaves no valid cell table behind
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->nbins, 1, nullptr);
+    ++c->launches;
+    c->grid_valid = false;
+  }
+  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, ~0ull, ~0ull, ~0ull, 0, iteration);
+  const unsigned int blocks = static_cast<unsigned int>((c->cap + kSortChunk - 1) / kSortChunk);
+  unsigned long long* k1 = c->sort_k[0];
+  unsigned long long* k2 = c->sort_k[1];
+  unsigned int* i1 = c->sort_i[0];
+  unsigned int* i2 = c->sort_i[1];
+  k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
+  c->launches += 3;
+  for (int shift = 0; shift < 96; shift += 8) {
+    k_radix_hist<<<blocks, kThreads, 0, c->stream>>>(k1, i1, c->g, shift, c->sort_hist, kSortChunk);
+    launch_scan<unsigned int>(c, c->sort_hist, c->sort_hlen, 256ull * blocks, c->sort_tiles, nullptr);
+    k_radix_scatter<<<blocks, kThreads, 0, c->stream>>>(k1, i1, k2, i2, c->g, shift, c->sort_hist, kSortChunk);
+    c->launches += 2;
+    std::swap(k1, k2);
+    std::swap(i1, i2);
+  }
+  const int nxt = c->cur ^ 1;
+  k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap, 1, 1);
+  ++c->launches;
+  c->cur = nxt;
+  c->pos_in_new = false;
+  return ABS_OK;
+}
+
 int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
@@ -2100,7 +2373,12 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     snaps.reserve(todo);
     for (unsigned long long t = 0; t < todo; ++t) {
       snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
-      launch_iteration(c, c->iteration + t);
+      const unsigned long long it = c->iteration + t;
+      if (c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0) {
+        const int rc = launch_sort(c, it);
+        if (rc) return rc;
+      }
+      launch_iteration(c, it);
     }
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return set_err(c, ABS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
@@ -2463,62 +2741,20 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
 int abs_gpu_sort(abs_gpu_ctx* c) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
-  // grid for the current state WITHOUT re-binning (the sort order depends on
-  // the current storage order, sort_balance.cpp:88-128)
-  const Pd* pos = cur_pos(c);
-  if (c->grid_valid) {
-    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->nbins, 1, nullptr);
-    ++c->launches;
-    c->grid_valid = false;
-  }
-  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, ~0ull, ~0ull, ~0ull, 0, c->iteration);
-  c->launches += 2;
   DevGrid h{};
   int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (h.n == 0) return ABS_OK;
+  rc = launch_sort(c, c->iteration);
+  if (rc) return rc;
+  CK(cudaGetLastError());
+  rc = read_grid(c, &h);
   if (rc) return rc;
   if (h.err) {
     rc = map_dev_err(c, h);
     clear_dev_err(c);
     return rc;
   }
-  const unsigned long long n = h.n;
-  if (n == 0) return ABS_OK;
-  unsigned long long *k1, *k2;
-  unsigned int *i1, *i2, *hist;
-  const unsigned long long chunk = 4096;
-  const unsigned int blocks = static_cast<unsigned int>((n + chunk - 1) / chunk);
-  CK(dalloc(&k1, n)); CK(dalloc(&k2, n)); CK(dalloc(&i1, n)); CK(dalloc(&i2, n));
-  CK(dalloc(&hist, 256ull * blocks + 1));
-  unsigned int* tiles = nullptr;
-  CK(dalloc(&tiles, (256ull * blocks) / kScanTile + 2));
-  unsigned long long* hl = nullptr;
-  const unsigned long long hlen = 256ull * blocks;
-  CK(dalloc(&hl, 1));
-  CK(cudaMemcpyAsync(hl, &hlen, 8, cudaMemcpyHostToDevice, c->stream));
-  k_sort_keys<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
-  ++c->launches;
-  unsigned int maxdim = std::max(h.dims[0], std::max(h.dims[1], h.dims[2]));
-  int axis_bits = 0;
-  while ((1u << axis_bits) < maxdim) ++axis_bits;
-  const int code_bits = (h.dims[2] == 1 ? 2 : 3) * axis_bits;
-  // composite key (morton << 32 | ~idx): 8-bit LSD passes over its used bits
-  for (int shift = 0; shift < 32 + code_bits; shift += 8) {
-    k_radix_hist<<<blocks, kThreads, 0, c->stream>>>(k1, i1, n, shift, hist, chunk);
-    launch_scan<unsigned int>(c, hist, hl, hlen, tiles, nullptr);
-    k_radix_scatter<<<blocks, kThreads, 0, c->stream>>>(k1, i1, k2, i2, n, shift, hist, chunk);
-    c->launches += 2;
-    std::swap(k1, k2);
-    std::swap(i1, i2);
-  }
-  const int nxt = c->cur ^ 1;
-  k_gather<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, n, c->cap, 1, 1);
-  ++c->launches;
-  CK(cudaStreamSynchronize(c->stream));
-  cudaFree(k1); cudaFree(k2); cudaFree(i1); cudaFree(i2); cudaFree(hist); cudaFree(tiles); cudaFree(hl);
-  c->cur = nxt;
-  c->pos_in_new = false;
-  c->grid_valid = false;
   return ABS_OK;
 }
 

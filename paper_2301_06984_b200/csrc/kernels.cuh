@@ -64,7 +64,7 @@ struct DevGrid {
   unsigned int dims[3];
   unsigned int bd[3];  // bins per axis = B[k] * dims[k]
   unsigned int B[3];   // sub-bins per box edge per axis (x, y, z)
-  unsigned int pad;
+  unsigned int sort_passes;  // 8-bit radix passes the last k_sort_keys needs (even)
   unsigned long long nbins;
   unsigned long long needed_bins;
   unsigned long long n;
@@ -396,6 +396,239 @@ __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd*
       }
     }
 #endif
+  }
+}
+
+// fp32-classified variant of for_each_neighbor_flat. Candidates are read
+// from `pf` (float4 {x, y, z, d} relative to the grid origin, 16 B) and
+// classified against the exact fp64 test with a proven margin: the fp32
+// distance differs from the fp64 one by less than `g.slack` (rounding of two
+// relative coordinates of magnitude <= grid extent, their difference and the
+// fp32 norm: < 7 ext 2^-24; slack = 16 ext 2^-24 + 1e-5). So
+//   df2 <= (r - slack)^2  => the reference's d2 <= r^2 holds   (visit)
+//   df2 >  (r + slack)^2  => it fails                           (skip)
+// and only the thin band between re-reads the exact fp64 record and applies
+// the reference's own test. The visited set is identical to
+// for_each_neighbor's; visit(j, df2, qd) gets the fp32 squared distance and
+// diameter (for the caller's conservative contact test).
+template <class F>
+__device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const Pd* __restrict__ pd,
+                                                         const float4* __restrict__ pf,
+                                                         const unsigned int* __restrict__ start,
+                                                         unsigned int (*wj0)[kForceThreads],
+                                                         unsigned int (*wj1)[kForceThreads],
+                                                         unsigned int self, double cx, double cy,
+                                                         double cz, double r, double r2, F&& visit) {
+  const int t = threadIdx.x;
+  const float fx = static_cast<float>(cx - g.ox);
+  const float fy = static_cast<float>(cy - g.oy);
+  const float fz = static_cast<float>(cz - g.oz);
+  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
+  const float rf2 = rf * rf;
+  const double sl = static_cast<double>(g.slack);
+  const double rin = r - sl;
+  const float rin2 = rin > 0.0 ? __double2float_rd(rin * rin * (1.0 - 0x1.0p-40)) : -1.0f;
+  const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
+  int bl[3], bh[3];
+  box_bin_range(g, cx, cy, cz, bl, bh);
+  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
+  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
+  auto test = [&](unsigned int j, const float4& qf) {
+    const float ex = fx - qf.x, ey = fy - qf.y, ez = fz - qf.z;
+    const float df2 = (ex * ex + ey * ey) + ez * ez;
+    if (j == self || df2 > rout2) return;
+    if (df2 > rin2) {  // margin band: the reference's exact fp64 test
+      const Pd q = load_pd(pd + j);
+      const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
+      if (!((dx * dx + dy * dy) + dz * dz <= r2)) return;
+    }
+    visit(j, df2, qf.w);
+  };
+  // Phase 1a: row geometry only — the cell-table slots of each row's x range
+  // [start[a0], start[a1]) go to the window arrays, no loads yet.
+  int nr = 0;
+  for (int bz = z0; bz <= z1; ++bz) {
+    const float zl = static_cast<float>(bz) * g.s[2];
+    const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
+    for (int by = y0; by <= y1; ++by) {
+      const float yl = static_cast<float>(by) * g.s[1];
+      const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
+      const float rem = rf2 - (gy * gy + gz * gz);
+      if (rem < 0.0f) continue;
+      const float w = sqrtf(rem);
+      const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
+      const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
+      const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      if (nr < kMaxRows) {
+        wj0[nr][t] = row + x0;
+        wj1[nr][t] = row + x1 + 1;
+        ++nr;
+      } else {  // overflow rows: nested walk
+        const unsigned int j1 = __ldg(start + row + x1 + 1);
+        for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) test(j, __ldg(pf + j));
+      }
+    }
+  }
+  // Phase 1b: the cell-table loads, kRowBatch rows in flight at a time; empty
+  // windows are compacted out in place (write index <= read index).
+#ifndef ABS_ROW_BATCH
+#define ABS_ROW_BATCH 4
+#endif
+  constexpr int kRowBatch = ABS_ROW_BATCH;
+  int nw = 0;
+  for (int r0 = 0; r0 < nr; r0 += kRowBatch) {
+    unsigned int lo[kRowBatch], hi[kRowBatch];
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      const int q = min(r0 + u, nr - 1);
+      lo[u] = __ldg(start + wj0[q][t]);
+      hi[u] = __ldg(start + wj1[q][t]);
+    }
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      if (r0 + u < nr && hi[u] > lo[u]) {
+        wj0[nw][t] = lo[u];
+        wj1[nw][t] = hi[u];
+        ++nw;
+      }
+    }
+  }
+#if defined(ABS_ABLATE) && ABS_ABLATE == 1
+  if (nw > 1000) visit(self, 0.0f, 0.0f);  // timing ablation: rows only
+  return;
+#endif
+  if (nw == 0) return;
+  int k = 0;
+  unsigned int j = wj0[0][t], je = wj1[0][t];
+  while (k < nw) {
+    unsigned int idx[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      idx[u] = self;  // sentinel: skipped by test()
+      if (k < nw) {
+        idx[u] = j;
+        if (++j == je && ++k < nw) {
+          j = wj0[k][t];
+          je = wj1[k][t];
+        }
+      }
+    }
+    float4 qf[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pf + idx[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) test(idx[u], qf[u]);
+  }
+}
+
+// Group-cooperative variant: the LPA lanes of a group (aligned lane block)
+// share ONE agent. The agent's candidate stream — exactly the rows and order
+// of for_each_neighbor — is dealt round-robin to the group's lanes (lane l
+// gets flat positions l, l + LPA, ...), so one group load is LPA consecutive
+// records of a row (coalesced) instead of LPA unrelated ones. Rows are
+// enumerated in chunks of 32: lane l computes rows [l*R, (l+1)*R) of the
+// chunk, a group scan of the row lengths gives each row's flat offset, and
+// `rj0`/`rpre` (this group's shared-memory slice, 2*32+1 words) hold them for
+// the walk. Each lane visits its candidates in increasing flat order.
+constexpr int kGroupRows = 32;
+constexpr int kGroupRowWords = 2 * kGroupRows + 1;
+
+template <int LPA>
+__device__ __forceinline__ unsigned int group_mask() {
+  return LPA == 32 ? 0xffffffffu : (((1u << LPA) - 1u) << ((threadIdx.x & 31) & ~(LPA - 1)));
+}
+
+template <int LPA, class F>
+__device__ __forceinline__ void for_each_neighbor_group(const QGrid& g, const Pd* __restrict__ pd,
+                                                        const unsigned int* __restrict__ start,
+                                                        unsigned int* __restrict__ rows, unsigned int self,
+                                                        double cx, double cy, double cz, double r, double r2,
+                                                        F&& visit) {
+  constexpr int R = kGroupRows / LPA;
+  const unsigned int mask = group_mask<LPA>();
+  const int l = threadIdx.x & (LPA - 1);
+  unsigned int* rj0 = rows;
+  unsigned int* rpre = rows + kGroupRows;
+  const float fx = static_cast<float>(cx - g.ox);
+  const float fy = static_cast<float>(cy - g.oy);
+  const float fz = static_cast<float>(cz - g.oz);
+  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
+  const float rf2 = rf * rf;
+  int bl[3], bh[3];
+  box_bin_range(g, cx, cy, cz, bl, bh);
+  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
+  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
+  const int ny = y1 - y0 + 1;
+  const int nq = (z1 >= z0 && ny > 0) ? (z1 - z0 + 1) * ny : 0;
+  for (int qb = 0; qb < nq; qb += kGroupRows) {
+    unsigned int j0[R], len[R], tot = 0;
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      const int q = qb + l * R + m;
+      j0[m] = 0;
+      len[m] = 0;
+      if (q < nq) {
+        const int bz = z0 + q / ny, by = y0 + q % ny;
+        const float zl = static_cast<float>(bz) * g.s[2];
+        const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
+        const float yl = static_cast<float>(by) * g.s[1];
+        const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
+        const float rem = rf2 - (gy * gy + gz * gz);
+        if (rem >= 0.0f) {
+          const float w = sqrtf(rem);
+          const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
+          const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
+          const unsigned int row =
+              g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+          const unsigned int a0 = __ldg(start + row + x0);
+          const unsigned int a1 = __ldg(start + row + x1 + 1);
+          j0[m] = a0;
+          len[m] = a1 > a0 ? a1 - a0 : 0u;
+        }
+      }
+      tot += len[m];
+    }
+    unsigned int inc = tot;
+#pragma unroll
+    for (int off = 1; off < LPA; off <<= 1) {
+      const unsigned int v = __shfl_up_sync(mask, inc, off, LPA);
+      if (l >= off) inc += v;
+    }
+    const unsigned int total = __shfl_sync(mask, inc, LPA - 1, LPA);
+    unsigned int run = inc - tot;
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+      rj0[l * R + m] = j0[m];
+      rpre[l * R + m] = run;
+      run += len[m];
+    }
+    if (l == LPA - 1) rpre[kGroupRows] = total;
+    __syncwarp(mask);
+    int k = 0;
+    for (unsigned int p0 = 0; p0 < total; p0 += LPA * kBatch) {
+      unsigned int idx[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const unsigned int p = p0 + u * LPA + l;
+        idx[u] = self;  // sentinel: skipped below
+        if (p < total) {
+          while (rpre[k + 1] <= p) ++k;
+          idx[u] = rj0[k] + (p - rpre[k]);
+        }
+      }
+      Pd q[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + idx[u]);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        if (idx[u] != self) {
+          const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
+        }
+      }
+    }
+    __syncwarp(mask);  // the next chunk overwrites rj0 / rpre
   }
 }
 

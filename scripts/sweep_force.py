@@ -43,6 +43,7 @@ def child(args):
     r1 = sim.report()
     n = r1.final_agent_count
     print(json.dumps({"lib": os.path.basename(os.environ.get("ABSIM_GPU_LIB", "default")), "bins": args.bin,
+                      "lpa": os.environ.get("ABSIM_LPA", "default"),
                       "n": n, "ms_per_step": ms, "force_ms": fms / max(fl, 1),
                       "agent_it_per_s": n / (ms / 1e3),
                       "evals_per_agent": (r1.force_evaluations - r0.force_evaluations) / (n * args.steps)}),
@@ -58,6 +59,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cache", default="/tmp/sweep_wl.npz")
+    ap.add_argument("--lpas", nargs="*", default=[""])
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--bin", default="2x1")
     args = ap.parse_args()
@@ -73,8 +75,10 @@ def main():
     print(f"# workload {wl.name} n={wl.n} generated in {time.time() - t0:.1f}s", flush=True)
     libs = args.libs or [""]
     for lib in libs:
-        for b in args.bins:
+        for b, lpa in [(b, q) for b in args.bins for q in args.lpas]:
             env = dict(os.environ)
+            if lpa:
+                env["ABSIM_LPA"] = lpa
             if lib:
                 env["ABSIM_GPU_LIB"] = os.path.abspath(lib)
             subprocess.run([sys.executable, __file__, "--child", "--bin", b, "--cache", args.cache,

@@ -325,6 +325,37 @@ def test_sort_matches_reference_order(engine, oracle_mod, have_ref):
         assert np.array_equal(got, ref.dump()["uid"])
 
 
+def test_inloop_sort_frequency(engine, oracle_mod):
+    """sorting_frequency (simulation.cpp:246-247): the Morton sort runs inside
+    the iteration loop on the device; results match the oracle that sorts at
+    the same iterations."""
+    wl = CF.c1_relaxation(2500, seed=6)
+    prm = {**wl.params, "sorting_frequency": 2}
+    sim = _gpu(engine, prm, wl, 2)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, prm), wl.x, wl.y, wl.z, wl.d)
+    for step in range(3):
+        sim.simulate(3)
+        orc.simulate(3)
+        compare_state(sim.agents(), orc.dump(), what=f"sorted c1 after {3 * (step + 1)}")
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"]
+
+
+def test_sort_order_flat_layout(engine, oracle_mod):
+    """2-D Morton table (morton.cpp:124-129, dims[2] == 1): a flat sheet."""
+    rng = np.random.default_rng(11)
+    n = 1500
+    x, y = rng.uniform(0, 300, n), rng.uniform(0, 120, n)
+    z, d = np.zeros(n), rng.uniform(8, 12, n)
+    prm = dict(seed=1, simulation_time_step=0.01)
+    sim = _gpu(engine, prm)
+    sim.add_agents(x, y, z, d)
+    sim.sort()
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, prm), x, y, z, d)
+    orc.env_update()
+    orc.sort()
+    assert np.array_equal(sim.agents()["uid"], orc.dump()["uid"])
+
+
 def test_removal_worked_example(engine):
     """test_commit.cpp:99-119 on a freshly uploaded (reference-ordered) store."""
     sim = engine.Simulation(engine.SimulationParams())
