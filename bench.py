@@ -360,7 +360,7 @@ def run_gpu(args):
         dt = time.perf_counter() - t0
         e2e = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0)),
-               "d2h_bytes_per_step": n_e * 32, "steps": e2e_steps,
+               "d2h_bytes_per_step": n_e * 24, "steps": e2e_steps,
                "path": "abs_gpu_upload (pinned host) -> abs_gpu_simulate(1) -> abs_gpu_download (pinned host)"}
 
     hbm, peak_src = _peaks()

@@ -108,13 +108,17 @@ const char* abs_gpu_last_error(const abs_gpu_ctx* ctx);
 /* Replace the population with n agents copied from host arrays. uid == NULL
  * assigns uids 0..n-1 in array order (Simulation::add_agent order);
  * behaviour_mask == NULL attaches the model behaviour to every agent;
- * volume/flags/partners may be NULL (volume defaults to the sphere volume). */
+ * volume/flags/partners may be NULL (volume defaults to the sphere volume).
+ * uid_count: uids ever assigned (every uid < uid_count, checked on the
+ * device -> ABS_ERR_INVALID_ARGUMENT); 0 with explicit uids = derive it from
+ * the uids on the host. Page-locked host arrays are copied by plain DMA. */
 int abs_gpu_upload(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
                    const double* y, const double* z, const double* d,
                    const uint8_t* behaviour_mask, const double* volume,
                    const uint8_t* flags, const uint32_t* partners, uint64_t uid_count);
 
-/* Same, from device pointers already resident in HBM (no host copies). */
+/* Same, from device pointers already resident in HBM (no host copies);
+ * explicit uids need uid_count > 0. */
 int abs_gpu_upload_device(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
                           const double* y, const double* z, const double* d,
                           const uint8_t* behaviour_mask, uint64_t uid_count);

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
                                                       const unsigned int* __restrict__ key,
                                                       const unsigned int* __restrict__ rank,
                                                       const DevGrid* g, unsigned long long cap,
-                                                      int carry_vol, int carry_force) {
+                                                      int carry_vol, int carry_force, int write_pf) {
   if (g->err) return;
   const unsigned long long n = g->n;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
@@ -340,7 +340,8 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
     const Pd p = load_pd(pos + i);
     reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
-    pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
+    if (write_pf)
+      pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
                           static_cast<float>(p.z - g->origin[2]), static_cast<float>(p.d));
     dst.uid[j] = src.uid[i];
     dst.flags[j] = src.flags[i];
@@ -1296,18 +1297,29 @@ __global__ void k_zero_marks(unsigned int* __restrict__ m, const DevGrid* g) {
 // interleaved {x,y,z,d} records from SoA device arrays, validate diameters
 // (Agent ctor throws unless d > 0, agent.hpp:25) and default the per-agent
 // state. Host arrays reach these inputs by contiguous H2D copies.
-__global__ void k_ingest(const double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ z,
-                         const double* __restrict__ d, const unsigned char* __restrict__ mask, unsigned long long n,
-                         int set_uid, int set_vol, int model_on, Pd* __restrict__ out, Soa S, DevGrid* g,
-                         int sir, unsigned long long seed) {
+// Population upload. Also produces, per block, the sum and max of the
+// diameters in a fixed order (thread grid-stride sums, then a fixed tree), so
+// the host's auto-bin decision is deterministic for a given grid, and checks
+// uids against the caller's uid_count (uid_limit > 0). bad_input: bit 0 a
+// diameter <= 0, bit 1 a uid >= uid_count.
+__global__ void __launch_bounds__(kThreads) k_ingest(const double* __restrict__ x, const double* __restrict__ y,
+                                                     const double* __restrict__ z, const double* __restrict__ d,
+                                                     const unsigned char* __restrict__ mask, unsigned long long n,
+                                                     int set_uid, int set_vol, int model_on, Pd* __restrict__ out,
+                                                     Soa S, DevGrid* g, int sir, unsigned long long seed,
+                                                     double* __restrict__ part, unsigned long long uid_limit) {
   unsigned int bad = 0;
+  double sum = 0.0, mx = 0.0;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const double di = d[i];
     bad |= !(di > 0.0);
+    sum += di;
+    mx = di > mx ? di : mx;
     reinterpret_cast<double2*>(out + i)[0] = make_double2(x[i], y[i]);
     reinterpret_cast<double2*>(out + i)[1] = make_double2(z[i], di);
     if (set_uid) S.uid[i] = i;
+    else if (uid_limit && S.uid[i] >= uid_limit) bad |= 2u;
     if (set_vol) S.vol[i] = abs_volume_of_diameter(di);
     if (sir) {  // absim_models.h: 1 % initially infected, from the seed (or given states)
       const unsigned long long u = set_uid ? i : S.uid[i];
@@ -1316,7 +1328,52 @@ __global__ void k_ingest(const double* __restrict__ x, const double* __restrict_
       S.beh[i] = (model_on && (!mask || mask[i])) ? 1 : 0;
     }
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&g->bad_input, 1u);
+  const unsigned int anybad = __reduce_or_sync(0xffffffffu, bad);
+  if (anybad && (threadIdx.x & 31) == 0) atomicOr(&g->bad_input, anybad);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    const double m = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = m > mx ? m : mx;
+  }
+  __shared__ double ws[kThreads / 32][2];
+  if ((threadIdx.x & 31) == 0) {
+    ws[threadIdx.x >> 5][0] = sum;
+    ws[threadIdx.x >> 5][1] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0, m2 = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      s2 += ws[w][0];
+      m2 = ws[w][1] > m2 ? ws[w][1] : m2;
+    }
+    part[2 * blockIdx.x] = s2;
+    part[2 * blockIdx.x + 1] = m2;
+  }
+}
+
+// Positions/diameters of the current state as four contiguous fp64 arrays
+// (x | y | z | d) for direct device-to-host copies into caller arrays.
+__global__ void k_split_pd(const Pd* __restrict__ pos, const DevGrid* g, double* __restrict__ out,
+                           unsigned long long stride) {
+  const unsigned long long n = g->n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    out[i] = p.x;
+    out[stride + i] = p.y;
+    out[2 * stride + i] = p.z;
+    out[3 * stride + i] = p.d;
+  }
+}
+
+__global__ void k_mask_flags(const unsigned char* __restrict__ in, unsigned char* __restrict__ out,
+                             const DevGrid* g) {
+  const unsigned long long n = g->n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    out[i] = in[i] & (63u | ABS_FLAG_GHOST);
 }
 
 // ------------------------------------------------------------ multi-domain exchange
@@ -1474,8 +1531,11 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
   return v;
 }
 
-// sort key = (morton code of the reference box) << 32 | (~storage index):
-// ascending key = curve order, descending index inside a box (chain order).
+// Sort keys: the Morton code of each agent's reference box, listed in
+// DESCENDING storage index (element t = agent n-1-t). A stable LSD sort on the
+// code alone then gives curve order with descending index inside a box — the
+// reference's chain order (sort_balance.cpp:88-128) — without radix passes
+// over the index bits.
 __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned long long* keyhi,
                             unsigned int* __restrict__ idx) {
   const DevGrid G = *g;
@@ -1484,11 +1544,12 @@ __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned lon
     unsigned int axis_bits = 0;
     while ((1u << axis_bits) < maxdim) ++axis_bits;
     const unsigned int code_bits = (G.dims[2] == 1 ? 2u : 3u) * axis_bits;
-    unsigned int passes = (32u + code_bits + 7u) / 8u;
+    unsigned int passes = (code_bits + 7u) / 8u;
     g->sort_passes = passes + (passes & 1u);
   }
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
+  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < G.n;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = G.n - 1 - t;
     const Pd p = load_pd(pos + i);
     const unsigned long long c0 = box_coord(p.x, G.origin[0], G.box, G.dims[0]);
     const unsigned long long c1 = box_coord(p.y, G.origin[1], G.box, G.dims[1]);
@@ -1500,14 +1561,13 @@ __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned lon
       for (int b = 0; b < 31; ++b) o |= ((xx >> b) & 1ull) << (2 * b) | ((yy >> b) & 1ull) << (2 * b + 1);
       code2 = o;
     }
-    keyhi[i] = code2;
-    idx[i] = static_cast<unsigned int>(i);
+    keyhi[t] = code2;
+    idx[t] = static_cast<unsigned int>(i);
   }
 }
 
-__device__ __forceinline__ unsigned int radix_digit(unsigned long long code, unsigned int idx, int shift) {
-  return shift < 32 ? ((0xFFFFFFFFu - idx) >> shift) & 255u
-                    : static_cast<unsigned int>((code >> (shift - 32)) & 255ull);
+__device__ __forceinline__ unsigned int radix_digit(unsigned long long code, unsigned int, int shift) {
+  return static_cast<unsigned int>((code >> shift) & 255ull);
 }
 
 // One LSD radix pass (8 bits) over (key, idx) pairs with a stable
@@ -1677,6 +1737,7 @@ struct abs_gpu_ctx {
   Pd* st_pd = nullptr;
   double* st_vol = nullptr;
   unsigned int* div_mark = nullptr;  // uid_cap + 1
+  double* ingest_part = nullptr;     // per-block (sum d, max d) of the last upload
   // Morton sort scratch (capacity-sized, allocated on first use)
   unsigned long long sort_cap = 0;
   unsigned long long *sort_k[2] = {nullptr, nullptr};
@@ -1685,8 +1746,6 @@ struct abs_gpu_ctx {
   unsigned int* sort_tiles = nullptr;
   unsigned long long* sort_hlen = nullptr;
 
-  void* pinned = nullptr;  // host staging for downloads (page-locked)
-  size_t pinned_bytes = 0;
 
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs
@@ -1867,6 +1926,21 @@ unsigned int bins_x(const abs_gpu_ctx* c) {  // auto: 3 along x with 2x2 in y/z 
   return b <= 0 ? (c->auto_bins == 2u ? 3u : c->auto_bins) : static_cast<unsigned int>(std::min(b, 4));
 }
 
+// ABSIM_F32=0 disables the fp32-classified candidate walk (A/B switch).
+bool use_f32_walk() {
+  static const int v = [] {
+    const char* e = std::getenv("ABSIM_F32");
+    return (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }();
+  return v != 0;
+}
+
+// The fp32 copy `pf` is written by the re-bin only when the force kernel's
+// fp32-classified walk will read it (sub-binned grids; not SIR, not box mode).
+bool uses_f32_walk(const abs_gpu_ctx* c) {
+  return use_f32_walk() && c->cfg.model != ABS_MODEL_SIR && !(bins_x(c) == 1u && bins_yz(c) == 1u);
+}
+
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
   const int nb = grid_blocks(c, c->cap);
@@ -1885,7 +1959,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   const int nxt = c->cur ^ 1;
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                            c->cfg.record_forces);
+                                            c->cfg.record_forces, uses_f32_walk(c));
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -1916,15 +1990,6 @@ bool use_tile_kernel() {
 }
 
 constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
-
-// ABSIM_F32=0 disables the fp32-classified candidate walk (A/B switch).
-bool use_f32_walk() {
-  static const int v = [] {
-    const char* e = std::getenv("ABSIM_F32");
-    return (e && std::strcmp(e, "0") == 0) ? 0 : 1;
-  }();
-  return v != 0;
-}
 
 template <int MODEL, bool STATIC, bool RECORD, bool F32>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
@@ -2191,10 +2256,9 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
-  cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
+  cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark); cudaFree(c->ingest_part);
   free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
-  if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ABS_OK;
@@ -2209,23 +2273,20 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   if (n >= 0xFFFFFFF0ull) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "too many agents");
   cudaSetDevice(c->device);
   const bool host = kind == cudaMemcpyHostToDevice;
-  if (uid && host) {
+  // uid_count == 0 with explicit uids: derive it (host scan); otherwise the
+  // device checks every uid < uid_count during ingest
+  const unsigned long long uid_limit = (uid && uid_count) ? uid_count : 0;
+  if (uid && host && !uid_count) {
     for (unsigned long long i = 0; i < n; ++i) uid_count = std::max<unsigned long long>(uid_count, uid[i] + 1);
   }
+  if (uid && !host && !uid_count) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "device upload with uids needs uid_count");
   uid_count = std::max<unsigned long long>(uid_count, n);
   int rc = ensure_capacity(c, std::max<unsigned long long>({c->cap, 2 * n + 1024, uid_count}), 0);
   if (rc) return rc;
   Soa& S = c->S[c->cur];
   const double *dx = x, *dy = y, *dz = z, *dd = d;
   const unsigned char* dmask = mask;
-  if (host && n) {
-    double sum = 0.0, mx = 0.0;
-    for (unsigned long long i = 0; i < n; ++i) {
-      sum += d[i];
-      mx = d[i] > mx ? d[i] : mx;
-    }
-    c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
-  }
+  if (!c->ingest_part) CK(dalloc(&c->ingest_part, 2ull * c->sms * 8 + 2));
   if (host && n) {  // contiguous H2D into the staging area, interleaved on the device
     double* st = reinterpret_cast<double*>(c->st_pd);
     CK(cudaMemcpyAsync(st, x, n * 8, cudaMemcpyHostToDevice, c->stream));
@@ -2254,18 +2315,28 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   h.n = n;
   h.uid_count = uid_count;
   CK(cudaMemcpyAsync(c->g, &h, offsetof(DevGrid, ov_on), cudaMemcpyHostToDevice, c->stream));
+  const int ib = grid_blocks(c, n);
   if (n) {
-    k_ingest<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr,
-                                                            volume == nullptr, c->cfg.model != ABS_MODEL_NONE,
-                                                            c->newpd, S, c->g, c->cfg.model == ABS_MODEL_SIR,
-                                                            c->cfg.seed);
+    k_ingest<<<ib, kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr, volume == nullptr,
+                                             c->cfg.model != ABS_MODEL_NONE, c->newpd, S, c->g,
+                                             c->cfg.model == ABS_MODEL_SIR, c->cfg.seed, c->ingest_part, uid_limit);
     ++c->launches;
   }
   // the cell table is a counter array between iterations: always start clean
   CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
   unsigned int bad = 0;
+  std::vector<double> part(2ull * ib);
   CK(cudaMemcpyAsync(&bad, &c->g->bad_input, 4, cudaMemcpyDeviceToHost, c->stream));
+  if (n) CK(cudaMemcpyAsync(part.data(), c->ingest_part, part.size() * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (n) {  // Sub-bins: bins == boxes when the typical radius is close to the box (see bins_yz)
+    double sum = 0.0, mx = 0.0;
+    for (int b = 0; b < ib; ++b) {
+      sum += part[2 * b];
+      mx = part[2 * b + 1] > mx ? part[2 * b + 1] : mx;
+    }
+    c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
+  }
   c->pos_in_new = true;
   c->grid_valid = false;
   c->iteration = 0;
@@ -2274,7 +2345,7 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
     CK(cudaMemsetAsync(&c->g->n, 0, 8, c->stream));
     CK(cudaMemsetAsync(&c->g->bad_input, 0, 4, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "diameter must be > 0");
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, (bad & 1u) ? "diameter must be > 0" : "uid >= uid_count");
   }
   c->n = n;
   return ABS_OK;
@@ -2310,8 +2381,8 @@ constexpr unsigned long long kSortChunk = 4096;
 
 // sort_and_balance (sort_balance.cpp:22-148) on the device, stream-ordered and
 // without host synchronisation: grid of the current state (no re-binning),
-// (Morton code << 32 | ~index) keys, 12 8-bit LSD pass slots of which the
-// device runs sort_passes, gather into the other state buffer. Callable
+// Morton-code keys in descending index order, 8 8-bit LSD pass slots of which
+// the device runs sort_passes, gather into the other state buffer. Callable
 // inside the iteration loop (sorting_frequency, simulation.cpp:246-247).
 static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
   if (c->sort_cap != c->cap) {
@@ -2343,16 +2414,20 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
   unsigned int* i2 = c->sort_i[1];
   k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
   c->launches += 3;
-  for (int shift = 0; shift < 96; shift += 8) {
+  for (int shift = 0; shift < 64; shift += 8) {
     k_radix_hist<<<blocks, kThreads, 0, c->stream>>>(k1, i1, c->g, shift, c->sort_hist, kSortChunk);
     launch_scan<unsigned int>(c, c->sort_hist, c->sort_hlen, 256ull * blocks, c->sort_tiles, nullptr);
-    k_radix_scatter<<<blocks, kThreads, 0, c->stream>>>(k1, i1, k2, i2, c->g, shift, c->sort_hist, kSortChunk);
+    // one warp per chunk (stable by construction): 32-thread blocks keep the
+    // SM full of independent chunk walkers
+    k_radix_scatter<<<blocks, 32, 0, c->stream>>>(k1, i1, k2, i2, c->g, shift, c->sort_hist, kSortChunk);
     c->launches += 2;
     std::swap(k1, k2);
     std::swap(i1, i2);
   }
   const int nxt = c->cur ^ 1;
-  k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap, 1, 1);
+  k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
+                                                              c->cfg.model == ABS_MODEL_PROLIFERATION,
+                                                              c->cfg.record_forces);
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2611,38 +2686,34 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
   const unsigned long long n = h.n;
   if (n_out) *n_out = n;
   Soa& S = c->S[c->cur];
-  if (x || y || z || d) {
-    if (c->pinned_bytes < n * sizeof(Pd)) {
-      if (c->pinned) cudaFreeHost(c->pinned);
-      c->pinned = nullptr;
-      c->pinned_bytes = 0;
-      CK(cudaMallocHost(&c->pinned, std::max<size_t>(n * sizeof(Pd), 1)));
-      c->pinned_bytes = std::max<size_t>(n * sizeof(Pd), 1);
-    }
-    Pd* hp = static_cast<Pd*>(c->pinned);
-    CK(cudaMemcpyAsync(hp, cur_pos(c), n * sizeof(Pd), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    for (unsigned long long i = 0; i < n; ++i) {
-      if (x) x[i] = hp[i].x;
-      if (y) y[i] = hp[i].y;
-      if (z) z[i] = hp[i].z;
-      if (d) d[i] = hp[i].d;
-    }
+  // Components are split on the device into the staging area and copied
+  // straight into the caller's arrays (page-locked arrays: plain DMA).
+  if (n && (x || y || z || d)) {
+    double* st = reinterpret_cast<double*>(c->st_pd);
+    k_split_pd<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->g, st, n);
+    ++c->launches;
+    double* dst[4] = {x, y, z, d};
+    for (int q = 0; q < 4; ++q)
+      if (dst[q]) CK(cudaMemcpyAsync(dst[q], st + q * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
   }
-  if (uid) CK(cudaMemcpy(uid, S.uid, n * 8, cudaMemcpyDeviceToHost));
-  if (fx) CK(cudaMemcpy(fx, S.force, n * 8, cudaMemcpyDeviceToHost));
-  if (fy) CK(cudaMemcpy(fy, S.force + c->cap, n * 8, cudaMemcpyDeviceToHost));
-  if (fz) CK(cudaMemcpy(fz, S.force + 2 * c->cap, n * 8, cudaMemcpyDeviceToHost));
-  if (partners) CK(cudaMemcpy(partners, S.partners, n * 4, cudaMemcpyDeviceToHost));
-  if (flags) {
-    CK(cudaMemcpy(flags, S.flags, n, cudaMemcpyDeviceToHost));
-    for (unsigned long long i = 0; i < n; ++i) flags[i] &= (63u | ABS_FLAG_GHOST);
+  if (n && uid) CK(cudaMemcpyAsync(uid, S.uid, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (n && fx) CK(cudaMemcpyAsync(fx, S.force, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (n && fy) CK(cudaMemcpyAsync(fy, S.force + c->cap, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (n && fz) CK(cudaMemcpyAsync(fz, S.force + 2 * c->cap, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (n && partners) CK(cudaMemcpyAsync(partners, S.partners, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (n && flags) {
+    unsigned char* fb = reinterpret_cast<unsigned char*>(c->key);
+    k_mask_flags<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(S.flags, fb, c->g);
+    ++c->launches;
+    CK(cudaMemcpyAsync(flags, fb, n, cudaMemcpyDeviceToHost, c->stream));
   }
-  if (volume) {
-    CK(cudaMemcpy(volume, S.vol, n * 8, cudaMemcpyDeviceToHost));
-    if (c->cfg.model != ABS_MODEL_PROLIFERATION)
-      for (unsigned long long i = 0; i < n; ++i) volume[i] = 0.0;
+  if (n && volume) {
+    if (c->cfg.model == ABS_MODEL_PROLIFERATION)
+      CK(cudaMemcpyAsync(volume, S.vol, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    else
+      std::fill(volume, volume + n, 0.0);
   }
+  CK(cudaStreamSynchronize(c->stream));
   return ABS_OK;
 }
 

@@ -194,10 +194,11 @@ class Simulation:
                                         _p(m, C.c_uint8), _p(v, C.c_double), _p(f, C.c_uint8),
                                         _p(pa, C.c_uint32), uid_count), self._ctx)
 
-    def add_agents_device(self, x_ptr, y_ptr, z_ptr, d_ptr, n, uid_ptr=None, mask_ptr=None):
-        """Population from device-resident arrays (e.g. torch CUDA tensors)."""
+    def add_agents_device(self, x_ptr, y_ptr, z_ptr, d_ptr, n, uid_ptr=None, mask_ptr=None, uid_count: int = 0):
+        """Population from device-resident arrays (e.g. torch CUDA tensors).
+        With explicit uids, uid_count (> every uid) is required."""
         N.check(N.load().abs_gpu_upload_device(self._ctx, n, uid_ptr, x_ptr, y_ptr, z_ptr, d_ptr,
-                                               mask_ptr, n), self._ctx)
+                                               mask_ptr, uid_count if uid_ptr else n), self._ctx)
 
     def remove_agents(self, uids):
         u = np.ascontiguousarray(uids, np.uint64)

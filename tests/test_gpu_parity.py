@@ -306,6 +306,25 @@ def test_errors(engine):
     sim = engine.Simulation(engine.SimulationParams())
     with pytest.raises(ValueError, match="diameter"):
         sim.add_agents([0.0], [0.0], [0.0], [0.0])
+    with pytest.raises(ValueError, match="uid_count"):
+        sim.add_agents([0.0, 20.0], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0], uid=[3, 7], uid_count=5)
+    sim.add_agents([0.0, 20.0], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0], uid=[3, 7], uid_count=8)
+    sim.add_agents([0.0, 20.0], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0], uid=[3, 7])  # derived
+    assert sorted(sim.agents()["uid"].tolist()) == [3, 7]
+    assert sim.report().uid_count == 8
+
+
+def test_download_components_pinned(engine):
+    """abs_gpu_download straight into page-locked caller arrays, any subset."""
+    import torch
+    wl = CF.c1_relaxation(5000, seed=2)
+    sim = _gpu(engine, wl.params, wl, 1)
+    sim.simulate(2)
+    a = sim.agents()
+    out = [torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+    assert sim.positions(*out) == wl.n
+    for k, arr in zip("xyz", out):
+        assert np.array_equal(arr, a[k])
 
 
 def test_sort_matches_reference_order(engine, oracle_mod, have_ref):
