@@ -227,7 +227,7 @@ def run_decomposed(args, dist, world, rank, local):
     dist.all_reduce(owned)
     total = float(owned.item())
     value = total * args.steps / (ms_max / 1e3)
-    evals_per_agent_step = dec.evals / max(1.0, total * (args.steps + args.warmup))
+    evals_per_agent_step = dec.totals()[0] / max(1.0, total * (args.steps + args.warmup))
 
     # end to end per rank through the public API with HOST buffers: upload the
     # rank's slab from page-locked memory, one decomposed iteration (bounds
@@ -243,8 +243,10 @@ def run_decomposed(args, dist, world, rank, local):
         dist.barrier()
         t0 = time.perf_counter()
         n_e = 0
-        for _ in range(e2e_steps):
+        it = args.warmup + args.steps
+        for k in range(e2e_steps):
             sim.add_agents(*pin[:4], uid=pin[4], uid_count=n_per * world)
+            sim.set_iteration(it + k)
             dec.simulate(1)
             n_e = sim.positions(*outp)
         torch.cuda.synchronize()
@@ -348,13 +350,18 @@ def run_gpu(args):
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (wl.x, wl.y, wl.z, wl.d)]
         mask = None if wl.mask is None else torch.from_numpy(wl.mask).pin_memory().numpy()
         outp = [torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+        # a host-driven loop continues the step numbering after each upload
+        # (set_iteration), so periodic work (sorting_frequency) keeps its cadence
+        it = args.warmup + args.steps
         sim.add_agents(*pin, behaviour_mask=mask)
+        sim.set_iteration(it)
         sim.simulate(1)
         sim.positions(*outp)
         e2e_steps = max(1, min(args.steps, 5))
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
+        for k in range(e2e_steps):
             sim.add_agents(*pin, behaviour_mask=mask)
+            sim.set_iteration(it + 1 + k)
             sim.simulate(1)
             n_e = sim.positions(*outp)
         dt = time.perf_counter() - t0

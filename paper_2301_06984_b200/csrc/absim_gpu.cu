@@ -33,9 +33,13 @@ using namespace absgpu;
 namespace {
 
 #ifndef ABS_FORCE_MIN_BLOCKS
-#define ABS_FORCE_MIN_BLOCKS 2
+#define ABS_FORCE_MIN_BLOCKS 4
+#endif
+#ifndef ABS_FORCE_MIN_BLOCKS_F32
+#define ABS_FORCE_MIN_BLOCKS_F32 5
 #endif
 constexpr int kForceMinBlocks = ABS_FORCE_MIN_BLOCKS;
+constexpr int kForceMinBlocksF32 = ABS_FORCE_MIN_BLOCKS_F32;
 constexpr unsigned long long kInfOrdLo = 0xFFF0000000000000ull;  // ord_enc(+inf)
 constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf)
 constexpr unsigned long long kZeroOrd = 0x8000000000000000ull;   // ord_enc(+0.0)
@@ -688,8 +692,10 @@ __device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsign
 // Global-gather force kernel: one agent per thread, candidates fetched from
 // HBM/L2 through the per-lane flat window stream. Used for small tiles'
 // overflow and as the reference implementation of the tiled kernel below.
+// Resident CTAs per SM the register budget is sized for (c4 @ 2^24 sweep:
+// fp32 walk 5 -> 6.27 ms vs 2 -> 6.96 ms; box mode c3 4 -> 0.68 vs 2 -> 0.77).
 template <int MODEL, bool STATIC, bool RECORD, bool F32>
-__global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
+__global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kForceMinBlocks)
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
@@ -1738,6 +1744,7 @@ struct abs_gpu_ctx {
   double* st_vol = nullptr;
   unsigned int* div_mark = nullptr;  // uid_cap + 1
   double* ingest_part = nullptr;     // per-block (sum d, max d) of the last upload
+  unsigned long long ghosts = 0;     // upper bound on ghost agents present (0 -> drop_ghosts is a no-op)
   // Morton sort scratch (capacity-sized, allocated on first use)
   unsigned long long sort_cap = 0;
   unsigned long long *sort_k[2] = {nullptr, nullptr};
@@ -2340,6 +2347,7 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   c->pos_in_new = true;
   c->grid_valid = false;
   c->iteration = 0;
+  c->ghosts = flags ? n : 0;  // uploaded flags may carry ABS_FLAG_GHOST
   if (bad) {
     c->n = 0;
     CK(cudaMemsetAsync(&c->g->n, 0, 8, c->stream));
@@ -2615,11 +2623,13 @@ int abs_gpu_import(abs_gpu_ctx* c, const void* records, uint64_t count, int as_g
   CK(cudaStreamSynchronize(c->stream));
   c->grid_valid = false;
   c->n = nn;
+  if (as_ghost) c->ghosts += count;
   return ABS_OK;
 }
 
 int abs_gpu_drop_ghosts(abs_gpu_ctx* c) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c->ghosts) return ABS_OK;  // nothing imported as ghost since the last drop
   cudaSetDevice(c->device);
   DevGrid h{};
   int rc = read_grid(c, &h);
@@ -2627,7 +2637,9 @@ int abs_gpu_drop_ghosts(abs_gpu_ctx* c) {
   if (!h.n) return ABS_OK;
   k_keep_ghostless<<<grid_blocks(c, h.n), kThreads, 0, c->stream>>>(c->S[c->cur], h.n, c->rank);
   ++c->launches;
-  return compact_population(c, h.n);
+  rc = compact_population(c, h.n);
+  if (rc == ABS_OK) c->ghosts = 0;
+  return rc;
 }
 
 int abs_gpu_sir_counts(abs_gpu_ctx* c, uint64_t* out3) {

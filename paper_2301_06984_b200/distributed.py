@@ -295,8 +295,7 @@ class DeviceSlabDecomposition:
         self.torch = torch
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self._alloc(cap)
-        self.evals = 0
-        self.skips = 0
+        self._r0 = sim.report()
         self.iteration = 0
 
     def _alloc(self, cap):
@@ -395,16 +394,18 @@ class DeviceSlabDecomposition:
         self._import("recv_hi", got_hi, True)
         grid, dims = g.as_override()
         self.sim.set_grid_override(grid, dims)
-        r0 = self.sim.report()
         self.sim.simulate(1)
-        r1 = self.sim.report()
         N.check(N.load().abs_gpu_drop_ghosts(self.sim._ctx), self.sim._ctx)
-        tot = self._allreduce(np.array([r1.force_evaluations - r0.force_evaluations,
-                                        r1.force_skips - r0.force_skips], np.int64), self.dist.ReduceOp.SUM)
-        self.evals += int(tot[0])
-        self.skips += int(tot[1])
         self.iteration += 1
         return g
+
+    def totals(self):
+        """Force evaluations and static skips summed over ranks since this
+        decomposition was created (one all-reduce; ghosts never count)."""
+        r = self.sim.report()
+        tot = self._allreduce(np.array([r.force_evaluations - self._r0.force_evaluations,
+                                        r.force_skips - self._r0.force_skips], np.int64), self.dist.ReduceOp.SUM)
+        return int(tot[0]), int(tot[1])
 
     def simulate(self, iterations: int):
         for _ in range(iterations):

@@ -176,7 +176,8 @@ def _dev_worker(rank, world, port, case, outdir):
     dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="host", cap=1 << 14)
     dec.simulate(steps)
     a = sim.agents()
-    np.savez(os.path.join(outdir, f"r{rank}.npz"), evals=dec.evals, skips=dec.skips, **a)
+    evals, skips = dec.totals()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), evals=evals, skips=skips, **a)
     dist.barrier()
     dist.destroy_process_group()
 
