@@ -39,6 +39,10 @@ namespace {
 #define ABS_FORCE_MIN_BLOCKS_F32 5
 #endif
 constexpr int kForceMinBlocks = ABS_FORCE_MIN_BLOCKS;
+#ifndef ABS_PASSB
+#define ABS_PASSB 1  // 2 or 4 measured slower (c4 @ 2^24: 6.27 / 6.38 / 6.56 ms)
+#endif
+constexpr int kPassB = ABS_PASSB;  // contact records fetched together in pass B
 constexpr int kForceMinBlocksF32 = ABS_FORCE_MIN_BLOCKS_F32;
 constexpr unsigned long long kInfOrdLo = 0xFFF0000000000000ull;  // ord_enc(+inf)
 constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf)
@@ -555,8 +559,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     }
     n_eval += evals;
     const double k = a.k;
-    auto contact = [&](unsigned int j) {
-      const Pd q = fetch(j);
+    auto contact_q = [&](unsigned int j, const Pd& q) {
       const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
       // pairwise_repulsion (mechanics.cpp:10-27)
       const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
@@ -578,6 +581,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         fz += f2;
       }
     };
+    auto contact = [&](unsigned int j) { contact_q(j, fetch(j)); };
     bool overflow = nov > kMaxContacts;
     if (LPA > 1) overflow = (__ballot_sync(group_mask<LPA>(), overflow) & group_mask<LPA>()) != 0u;
 #if defined(ABS_ABLATE) && ABS_ABLATE >= 2
@@ -585,7 +589,20 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     else nov = 0;
 #endif
     if (!overflow) {
-      for (unsigned int c = 0; c < nov; ++c) contact(ovl[c * ovl_stride]);
+      // contact records fetched kPassB at a time (independent loads in
+      // flight), applied in list order
+      unsigned int c = 0;
+      for (; c + kPassB <= nov; c += kPassB) {
+        unsigned int jj[kPassB];
+        Pd qq[kPassB];
+#pragma unroll
+        for (int u = 0; u < kPassB; ++u) jj[u] = ovl[(c + u) * ovl_stride];
+#pragma unroll
+        for (int u = 0; u < kPassB; ++u) qq[u] = fetch(jj[u]);
+#pragma unroll
+        for (int u = 0; u < kPassB; ++u) contact_q(jj[u], qq[u]);
+      }
+      for (; c < nov; ++c) contact(ovl[c * ovl_stride]);
     } else if constexpr (F32) {  // more contacts than the list holds: re-walk (rare)
       walk(r, r * r, [&](unsigned int j, float df2, float qd) {
         const float hp = 0.5f * (dif + qd) + slack;

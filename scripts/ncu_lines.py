@@ -5,6 +5,7 @@ import sys
 
 
 def main(path, top=45):
+    top = int(top)
     rows = list(csv.reader(open(path)))
     fname, agg, cur = "?", {}, None
     hdr = None
