@@ -338,8 +338,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
                                                       const unsigned int* __restrict__ key,
                                                       const unsigned int* __restrict__ rank,
                                                       const DevGrid* g, unsigned long long cap,
-                                                      int carry_vol, int carry_force, int write_pf) {
+                                                      int carry_vol, int carry_force, int write_pf,
+                                                      int only_sort_mode = -1) {
   if (g->err) return;
+  if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
@@ -1554,6 +1556,47 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long morton_code_of(const DevGrid& G, double px, double py, double pz) {
+  const unsigned long long c0 = box_coord(px, G.origin[0], G.box, G.dims[0]);
+  const unsigned long long c1 = box_coord(py, G.origin[1], G.box, G.dims[1]);
+  if (G.dims[2] == 1) {  // 2-D table (morton.cpp:124-129): x bits 2i, y bits 2i+1
+    unsigned long long o = 0;
+    for (int b = 0; b < 31; ++b) o |= ((c0 >> b) & 1ull) << (2 * b) | ((c1 >> b) & 1ull) << (2 * b + 1);
+    return o;
+  }
+  const unsigned long long c2 = box_coord(pz, G.origin[2], G.box, G.dims[2]);
+  return spread3(c0) | spread3(c1) << 1 | spread3(c2) << 2;
+}
+
+// In-loop sort mode (one thread, after the sort-mode finalize): counting sort
+// by Morton code when the code space fits the cell table (the in-box order is
+// unobservable there: the iteration's re-bin re-orders by cell right after),
+// else the exact radix path. mode == 0 always for abs_gpu_sort.
+__global__ void k_sort_mode(DevGrid* g, unsigned long long table_cap, int allow_counting) {
+  const unsigned int maxdim = max(g->dims[0], max(g->dims[1], g->dims[2]));
+  unsigned int axis_bits = 0;
+  while ((1u << axis_bits) < maxdim) ++axis_bits;
+  const unsigned int code_bits = (g->dims[2] == 1 ? 2u : 3u) * axis_bits;
+  const bool fits = code_bits < 40 && (1ull << code_bits) <= table_cap;
+  g->sort_mode = (allow_counting && fits && !g->err) ? 1u : 0u;
+  g->sort_len = g->sort_mode ? (1ull << code_bits) : 0ull;
+  if (g->sort_mode) g->sort_passes = 0;
+}
+
+// Counting-sort keys: Morton code + slot claimed by an atomic (k_key's form).
+__global__ void k_mkey(const Pd* __restrict__ pos, const DevGrid* g, unsigned int* __restrict__ count,
+                       unsigned int* __restrict__ key, unsigned int* __restrict__ rank) {
+  if (g->err || g->sort_mode != 1u) return;
+  const DevGrid G = *g;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    const unsigned int code = static_cast<unsigned int>(morton_code_of(G, p.x, p.y, p.z));
+    key[i] = code;
+    rank[i] = atomicAdd(count + code, 1u);
+  }
+}
+
 // Sort keys: the Morton code of each agent's reference box, listed in
 // DESCENDING storage index (element t = agent n-1-t). A stable LSD sort on the
 // code alone then gives curve order with descending index inside a box — the
@@ -1562,6 +1605,7 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
 __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned long long* keyhi,
                             unsigned int* __restrict__ idx) {
   const DevGrid G = *g;
+  if (G.sort_mode == 1u) return;  // in-loop counting sort selected (k_sort_mode)
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // passes over the used key bits, rounded up to even
     const unsigned int maxdim = max(G.dims[0], max(G.dims[1], G.dims[2]));
     unsigned int axis_bits = 0;
@@ -1653,8 +1697,10 @@ __global__ void k_radix_scatter(const unsigned long long* __restrict__ key, cons
 }
 
 __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const unsigned int* __restrict__ perm,
-                         const DevGrid* g, unsigned long long cap, int carry_vol, int carry_force) {
+                         const DevGrid* g, unsigned long long cap, int carry_vol, int carry_force,
+                         int only_sort_mode = -1) {
   if (g->err) return;
+  if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
   for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < n;
        j += (unsigned long long)gridDim.x * blockDim.x) {
@@ -2409,7 +2455,7 @@ constexpr unsigned long long kSortChunk = 4096;
 // Morton-code keys in descending index order, 8 8-bit LSD pass slots of which
 // the device runs sort_passes, gather into the other state buffer. Callable
 // inside the iteration loop (sorting_frequency, simulation.cpp:246-247).
-static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
+static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_order) {
   if (c->sort_cap != c->cap) {
     free_sort_scratch(c);
     const unsigned long long blocks = (c->cap + kSortChunk - 1) / kSortChunk;
@@ -2432,6 +2478,19 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
   k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, ~0ull, ~0ull, ~0ull, 0, iteration);
+  k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, exact_order ? 0 : 1);
+  c->launches += 1;
+  const int nxt = c->cur ^ 1;
+  // counting path (device-selected): Morton key + atomic slot, scan, scatter
+  k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+  launch_scan<unsigned int>(c, c->start, &c->g->sort_len, c->bins_cap, c->tiles, &c->g->err);
+  k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
+                                                               c->key, c->rank, c->g, c->cap,
+                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
+                                                               c->cfg.record_forces, 0, 1);
+  k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, nullptr);
+  c->launches += 3;
+  // exact path (device-selected otherwise): radix passes + gather
   const unsigned int blocks = static_cast<unsigned int>((c->cap + kSortChunk - 1) / kSortChunk);
   unsigned long long* k1 = c->sort_k[0];
   unsigned long long* k2 = c->sort_k[1];
@@ -2449,10 +2508,9 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration) {
     std::swap(k1, k2);
     std::swap(i1, i2);
   }
-  const int nxt = c->cur ^ 1;
   k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                                              c->cfg.record_forces);
+                                                              c->cfg.record_forces, 0);
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2475,7 +2533,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
       const unsigned long long it = c->iteration + t;
       if (c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0) {
-        const int rc = launch_sort(c, it);
+        const int rc = launch_sort(c, it, false);
         if (rc) return rc;
       }
       launch_iteration(c, it);
@@ -2845,7 +2903,7 @@ int abs_gpu_sort(abs_gpu_ctx* c) {
   int rc = read_grid(c, &h);
   if (rc) return rc;
   if (h.n == 0) return ABS_OK;
-  rc = launch_sort(c, c->iteration);
+  rc = launch_sort(c, c->iteration, true);
   if (rc) return rc;
   CK(cudaGetLastError());
   rc = read_grid(c, &h);

@@ -81,6 +81,10 @@ struct DevGrid {
   double ov_grid[5];       // origin[3], box, dmax over all ranks
   unsigned int ov_dims[3];
   unsigned int pad2;
+  // --- in-loop Morton sort (set by k_sort_mode each sort) ---
+  unsigned long long sort_len;  // counting mode: Morton code space (cell-table entries used)
+  unsigned int sort_mode;       // 1 counting sort by code (in-box order free), 0 exact radix path
+  unsigned int pad3;
 };
 
 struct StepArgs {
