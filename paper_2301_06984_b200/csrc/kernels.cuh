@@ -182,6 +182,18 @@ __device__ __forceinline__ int fbin(float v, float inv_s, unsigned int nb) {
   return min(max(i, 0), static_cast<int>(nb) - 1);
 }
 
+// Row chord half-width for culling: MUFU sqrt (relative error < 2^-22)
+// inflated outward, so the chosen x range stays a superset.
+__device__ __forceinline__ float cull_sqrt(float v) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r * 1.000001f;
+}
+
+// Unclamped floor bin: callers clamp to the reference box range [lo, hi],
+// which already lies inside [0, nb).
+__device__ __forceinline__ int fbin_raw(float v, float inv_s) { return __float2int_rd(v * inv_s); }
+
 // Bin range (inclusive) of the 3x3x3 reference boxes around the box holding
 // c (uniform_grid.cpp:185-201): the reference never looks further, so
 // neither do we — this keeps the candidate universe identical to the
@@ -225,7 +237,7 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
       const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
       const float rem = rf2 - (gy * gy + gz * gz);
       if (rem < 0.0f) continue;
-      const float w = sqrtf(rem);
+      const float w = cull_sqrt(rem);
       const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
       const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
       const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
@@ -435,8 +447,8 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
   const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
   int bl[3], bh[3];
   box_bin_range(g, cx, cy, cz, bl, bh);
-  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
-  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
+  const int z0 = max(fbin_raw(fz - rf, g.inv_s[2]), bl[2]), z1 = min(fbin_raw(fz + rf, g.inv_s[2]), bh[2]);
+  const int y0 = max(fbin_raw(fy - rf, g.inv_s[1]), bl[1]), y1 = min(fbin_raw(fy + rf, g.inv_s[1]), bh[1]);
   auto test = [&](unsigned int j, const float4& qf) {
     const float ex = fx - qf.x, ey = fy - qf.y, ez = fz - qf.z;
     const float df2 = (ex * ex + ey * ey) + ez * ez;
@@ -459,9 +471,9 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
       const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
       const float rem = rf2 - (gy * gy + gz * gz);
       if (rem < 0.0f) continue;
-      const float w = sqrtf(rem);
-      const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
-      const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
+      const float w = cull_sqrt(rem);
+      const int x0 = max(fbin_raw(fx - w, g.inv_s[0]), bl[0]);
+      const int x1 = min(fbin_raw(fx + w, g.inv_s[0]), bh[0]);
       const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
       if (nr < kMaxRows) {
         wj0[nr][t] = row + x0;

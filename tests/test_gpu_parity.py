@@ -152,6 +152,44 @@ def test_c4_shape_small(engine, oracle_mod):
     assert sim.report().force_evaluations == orc.counts()["force_evaluations"]
 
 
+@pytest.mark.parametrize("byz,bx", [(1, 2), (2, 1), (2, 2), (2, 3), (2, 4), (3, 3), (4, 4)])
+def test_bin_geometries_exact(engine, oracle_mod, byz, bx):
+    """Every sub-bin geometry (fp32-classified walk) visits exactly the
+    reference's candidates: force evaluations, partners and positions."""
+    wl = CF.c4_large_uniform(5000, seed=8)
+    prm = {**wl.params, "sorting_frequency": 0}
+    sim = _gpu(engine, prm, wl, byz, bins_per_box_x=bx)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, prm), wl.x, wl.y, wl.z, wl.d)
+    for step in range(2):
+        teacher_force(sim, orc)
+        e0 = orc.counts()["force_evaluations"]
+        sim.simulate(2)
+        orc.simulate(2)
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"] - e0
+        compare_state(sim.agents(), orc.dump(), what=f"bins {byz}x{bx} step {step}")
+
+
+def test_large_extent_margin_band(engine, oracle_mod):
+    """A domain with a large extent (slack ~ 16 E 2^-24 grows) and clusters of
+    touching agents: the fp32 margin band falls back to the exact fp64 test."""
+    rng = np.random.default_rng(21)
+    centres = rng.uniform(0, 1.0, size=(60, 3)) * np.array([2.0e5, 150.0, 150.0])  # within the box budget
+    pts = centres[rng.integers(0, 60, 6000)] + rng.normal(0, 9.0, size=(6000, 3))
+    d = np.exp(np.log(10.0) + 0.1 * rng.standard_normal(6000))
+    prm = dict(seed=3, simulation_time_step=0.01)
+    sim = _gpu(engine, prm, None, 2, bins_per_box_x=3)
+    sim.add_agents(pts[:, 0], pts[:, 1], pts[:, 2], d)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, prm), pts[:, 0], pts[:, 1], pts[:, 2], d)
+    compare_env(sim, orc, "large extent t=0")
+    for step in range(3):
+        teacher_force(sim, orc)
+        e0 = orc.counts()["force_evaluations"]
+        sim.simulate(1)
+        orc.simulate(1)
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"] - e0
+        compare_state(sim.agents(), orc.dump(), what=f"large extent step {step}")
+
+
 def test_against_reference_engine(engine, oracle_mod, have_ref):
     """The GPU against the unmodified reference (not only the C port)."""
     if not have_ref:
