@@ -21,6 +21,12 @@
  *                           query radius 0.5 (d + dmax), simulation.cpp:469) uniform_grid.cpp:268-326
  *   abs_gpu_sort            sort_and_balance (one domain)                   sort_balance.cpp:22-148
  *   abs_gpu_remove          CommitBuffer removals / remove_agents_parallel  commit.cpp:86-178
+ *   abs_gpu_set_defer_commit / abs_gpu_division_marks / abs_gpu_commit
+ *                           CommitBuffer::commit additions, split so ranks
+ *                           agree on daughter uids                          commit.cpp:186-222, simulation.cpp:64-91
+ *   abs_gpu_export_layers / abs_gpu_import / abs_gpu_drop_ghosts / abs_gpu_set_grid_override
+ *                           multi-domain slab exchange (no reference
+ *                           counterpart: the reference is one process)
  *
  * Conventions: int status (ABS_OK == 0), no exceptions across the ABI, one
  * host thread per context, device memory owned by the context, host buffers
@@ -122,6 +128,20 @@ int abs_gpu_upload(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const doub
 int abs_gpu_upload_device(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
                           const double* y, const double* z, const double* d,
                           const uint8_t* behaviour_mask, uint64_t uid_count);
+
+/* Multi-domain additions (commit.cpp:186-222). With defer != 0
+ * a proliferation context's abs_gpu_simulate(ctx, 1) stops with the
+ * iteration's daughters staged. The caller copies this rank's uid-indexed
+ * division marks (uid_count entries, 1 = that uid divided here) with
+ * abs_gpu_division_marks into a device buffer, sums the buffers of all ranks
+ * (e.g. an NCCL all-reduce) and passes the sum to abs_gpu_commit: daughter
+ * uids are then uid_count + the parent's rank among ALL dividing parents,
+ * exactly the single-domain numbering. global_marks == NULL commits with
+ * this rank's marks alone. Static detection with deferred additions is
+ * rejected (new-neighbour marks would stay local). */
+int abs_gpu_set_defer_commit(abs_gpu_ctx* ctx, int defer);
+int abs_gpu_division_marks(abs_gpu_ctx* ctx, uint32_t* out_device, uint64_t cap, uint64_t* len);
+int abs_gpu_commit(abs_gpu_ctx* ctx, const uint32_t* global_marks_device, uint64_t len);
 
 /* Multi-domain: force the grid computed over all ranks
  * (grid[0..2] origin, grid[3] box length, grid[4] largest diameter; dims)

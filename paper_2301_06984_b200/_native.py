@@ -34,6 +34,7 @@ EXPORTS = [
     "abs_gpu_synchronize", "abs_gpu_download", "abs_gpu_env_update", "abs_gpu_grid_info",
     "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
+    "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
 ]
 
 
@@ -104,6 +105,9 @@ def load():
                                             C.c_void_p, C.c_uint64, _U64, _U64]),
         "abs_gpu_import": (C.c_int, [_CTX, C.c_void_p, C.c_uint64, C.c_int]),
         "abs_gpu_drop_ghosts": (C.c_int, [_CTX]),
+        "abs_gpu_set_defer_commit": (C.c_int, [_CTX, C.c_int]),
+        "abs_gpu_division_marks": (C.c_int, [_CTX, C.c_void_p, C.c_uint64, _U64]),
+        "abs_gpu_commit": (C.c_int, [_CTX, C.c_void_p, C.c_uint64]),
         "abs_gpu_sir_state": (C.c_int, [_CTX, _U8, _U32]),
         "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),

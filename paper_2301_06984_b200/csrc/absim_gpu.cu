@@ -1280,14 +1280,15 @@ __global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
 __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
                          const unsigned long long* __restrict__ st_parent,
                          const Pd* __restrict__ st_pd, const double* __restrict__ st_vol,
-                         const unsigned int* __restrict__ div_rank, unsigned long long cap,
-                         int record_forces) {
+                         const unsigned int* __restrict__ div_rank, const unsigned int* __restrict__ div_rank_g,
+                         unsigned long long cap, int record_forces) {
   if (g->err) return;
   const unsigned long long staged = g->staged, n = g->n, uc = g->uid_count;
   for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < staged;
        k += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned int rk = div_rank[st_parent[k]];
-    const unsigned long long j = n + rk;
+    const unsigned long long parent = st_parent[k];
+    const unsigned long long j = n + div_rank[parent];  // local append slot
+    const unsigned int rk = div_rank_g[parent];         // rank among all dividers
     const Pd p = st_pd[k];
     reinterpret_cast<double2*>(live + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(live + j)[1] = make_double2(p.z, p.d);
@@ -1300,17 +1301,21 @@ __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
   }
 }
 
-__global__ void k_commit_fin(DevGrid* g) {
+// grank: the scanned (global) division marks; grank[uid_count] is the total
+// number of daughters created this iteration over all ranks.
+__global__ void k_commit_fin(DevGrid* g, const unsigned int* __restrict__ grank) {
   if (threadIdx.x || blockIdx.x || g->err) return;
   const unsigned long long s = g->staged;
   g->n += s;
-  g->uid_count += s;
+  g->uid_count += grank[g->uid_count];
   g->added += s;
   g->staged = 0;
 }
 
+// After the commit: zero the scanned marks, indices [0, uid_count] (the
+// grown uid_count covers the old range and the old total slot).
 __global__ void k_zero_marks(unsigned int* __restrict__ m, const DevGrid* g) {
-  if (g->err || g->staged == 0) return;
+  if (g->err) return;
   const unsigned long long len = g->uid_count + 1;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
        i += (unsigned long long)gridDim.x * blockDim.x)
@@ -1805,7 +1810,10 @@ struct abs_gpu_ctx {
   unsigned long long* st_parent = nullptr;
   Pd* st_pd = nullptr;
   double* st_vol = nullptr;
-  unsigned int* div_mark = nullptr;  // uid_cap + 1
+  unsigned int* div_mark = nullptr;  // uid_cap + 1: this context's dividing parents (then their local ranks)
+  unsigned int* div_mark_g = nullptr;  // uid_cap + 1: all ranks' dividing parents (deferred commit only)
+  bool defer_commit = false;         // multi-domain additions: stop before the commit
+  bool pending_commit = false;
   double* ingest_part = nullptr;     // per-block (sum d, max d) of the last upload
   unsigned long long ghosts = 0;     // upper bound on ghost agents present (0 -> drop_ghosts is a no-op)
   // Morton sort scratch (capacity-sized, allocated on first use)
@@ -1886,7 +1894,7 @@ Pd* cur_pos(abs_gpu_ctx* c) { return c->pos_in_new ? c->newpd : c->S[c->cur].pd;
 
 // (Re)allocate agent-sized buffers preserving the first `keep` agents.
 int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long keep) {
-  if (want <= c->cap && c->uid_cap >= 2 * want) return ABS_OK;
+  if (want <= c->cap) return ABS_OK;
   unsigned long long ncap = std::max<unsigned long long>(want, 1024);
   Soa S2[2]{};
   for (int b = 0; b < 2; ++b) CK(alloc_soa(S2[b], ncap));
@@ -1917,8 +1925,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   c->pos_in_new = true;
   c->grid_valid = false;
   cudaFree(c->key); cudaFree(c->rank); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark);
-  cudaFree(c->tiles64);
+  cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol);
   cudaFree(c->pf);
   c->pf = nullptr;
   CK(dalloc(&c->pf, ncap));
@@ -1931,11 +1938,30 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   CK(dalloc(&c->st_parent, ncap));
   CK(dalloc(&c->st_pd, ncap));
   CK(dalloc(&c->st_vol, ncap));
-  c->uid_cap = 2 * ncap + 1;
-  CK(dalloc(&c->div_mark, c->uid_cap + 1));
-  CK(cudaMemsetAsync(c->div_mark, 0, (c->uid_cap + 1) * 4, c->stream));
-  CK(dalloc(&c->tiles64, (2 * ncap + kScanTile) / kScanTile + 1));
   c->cap = ncap;
+  return ABS_OK;
+}
+
+// uid-indexed arrays (division marks + their scan tiles), sized by the uid
+// space, not by the agent capacity: in a multi-domain run every rank holds
+// the global uid space but only its own agents. Zero between iterations.
+int ensure_uid_space(abs_gpu_ctx* c, unsigned long long want) {
+  if (want <= c->uid_cap && c->div_mark && (!c->defer_commit || c->div_mark_g)) return ABS_OK;
+  const unsigned long long ncap = std::max<unsigned long long>({want + want / 2, c->uid_cap, 1024});
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(c->div_mark);
+  cudaFree(c->div_mark_g);
+  cudaFree(c->tiles64);
+  c->div_mark = nullptr;
+  c->div_mark_g = nullptr;
+  CK(dalloc(&c->div_mark, ncap + 1));
+  CK(cudaMemsetAsync(c->div_mark, 0, (ncap + 1) * 4, c->stream));
+  if (c->defer_commit) {
+    CK(dalloc(&c->div_mark_g, ncap + 1));
+    CK(cudaMemsetAsync(c->div_mark_g, 0, (ncap + 1) * 4, c->stream));
+  }
+  CK(dalloc(&c->tiles64, (ncap + kScanTile) / kScanTile + 2));
+  c->uid_cap = ncap;
   return ABS_OK;
 }
 
@@ -2010,6 +2036,8 @@ bool use_f32_walk() {
 bool uses_f32_walk(const abs_gpu_ctx* c) {
   return use_f32_walk() && c->cfg.model != ABS_MODEL_SIR && !(bins_x(c) == 1u && bins_yz(c) == 1u);
 }
+
+void launch_commit(abs_gpu_ctx* c);
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
@@ -2206,15 +2234,32 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
       k_mark_new<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->st_pd);
       ++c->launches;
     }
-    const unsigned long long* uc = &c->g->uid_count;
-    launch_scan<unsigned int>(c, c->div_mark, uc, c->uid_cap, reinterpret_cast<unsigned int*>(c->tiles64),
-                              &c->g->err);
-    k_append<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->st_parent, c->st_pd, c->st_vol,
-                                             c->div_mark, c->cap, c->cfg.record_forces);
-    k_zero_marks<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->div_mark, c->g);
-    k_commit_fin<<<1, 32, 0, c->stream>>>(c->g);
-    c->launches += 3;
+    if (!c->defer_commit) launch_commit(c);
   }
+}
+
+// CommitBuffer::commit for additions (commit.cpp:186-222): daughter uids
+// uid_count + rank of the parent uid among all dividing parents (the
+// single-thread creation order), appended in that order. Deferred commit
+// (multi-domain): div_mark_g holds every rank's dividers (the caller summed
+// the ranks' div_mark into it), giving global uid ranks, while this rank's
+// own div_mark gives the local append slots.
+void launch_commit(abs_gpu_ctx* c) {
+  const int nb = grid_blocks(c, c->cap);
+  Soa& S = c->S[c->cur];
+  const unsigned long long* uc = &c->g->uid_count;
+  unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
+  launch_scan<unsigned int>(c, c->div_mark, uc, c->uid_cap, tiles, &c->g->err);
+  if (c->defer_commit) launch_scan<unsigned int>(c, c->div_mark_g, uc, c->uid_cap, tiles, &c->g->err);
+  const unsigned int* grank = c->defer_commit ? c->div_mark_g : c->div_mark;
+  k_append<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
+                                           grank, c->cap, c->cfg.record_forces);
+  // counts first (reads the scan total grank[uid_count]), then clear the
+  // marks over the grown range [0, uid_count]
+  k_commit_fin<<<1, 32, 0, c->stream>>>(c->g, grank);
+  k_zero_marks<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->div_mark, c->g);
+  if (c->defer_commit) k_zero_marks<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->div_mark_g, c->g);
+  c->launches += c->defer_commit ? 4 : 3;
 }
 
 int read_grid(abs_gpu_ctx* c, DevGrid* h) {
@@ -2300,6 +2345,7 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   h.B[0] = h.B[1] = h.B[2] = 1;
   CK(cudaMemcpy(c->g, &h, sizeof h, cudaMemcpyHostToDevice));
   int rc = ensure_capacity(c, std::max<unsigned long long>(cfg->capacity, 1024), 0);
+  if (!rc) rc = ensure_uid_space(c, 1024);
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
   rc = ensure_bins(c, 1 << 16);
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
@@ -2351,8 +2397,13 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   }
   if (uid && !host && !uid_count) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "device upload with uids needs uid_count");
   uid_count = std::max<unsigned long long>(uid_count, n);
-  int rc = ensure_capacity(c, std::max<unsigned long long>({c->cap, 2 * n + 1024, uid_count}), 0);
+  int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * n + 1024), 0);
   if (rc) return rc;
+  if (c->cfg.model == ABS_MODEL_PROLIFERATION) {  // uid-indexed division marks
+    rc = ensure_uid_space(c, 2 * uid_count + 1024);
+    if (rc) return rc;
+  }
+  c->pending_commit = false;
   Soa& S = c->S[c->cur];
   const double *dx = x, *dy = y, *dz = z, *dd = d;
   const unsigned char* dmask = mask;
@@ -2520,6 +2571,11 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
 int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
+  const bool deferred = c->defer_commit && c->cfg.model == ABS_MODEL_PROLIFERATION;
+  if (deferred && c->pending_commit)
+    return set_err(c, ABS_ERR_STATE, "abs_gpu_commit is pending for the previous iteration");
+  if (deferred && iterations > 1)
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "deferred commit runs one iteration per call");
   // Launch in chunks; a chunk whose finalize asked for more bins/capacity is
   // rolled back to the failed iteration (no kernel touched state after it).
   unsigned long long done = 0;
@@ -2546,6 +2602,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     if (h.err == kErrNone) {
       c->iteration += todo;
       done += todo;
+      if (deferred && todo) c->pending_commit = true;
       continue;
     }
     const unsigned long long fi = h.failed_iteration;
@@ -2565,7 +2622,9 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       if (rc) return rc;
     } else if (h.err == kErrCapRetry) {
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
-      rc = ensure_capacity(c, 2 * c->cap, h.n);
+      if (2 * h.n > c->cap) rc = ensure_capacity(c, 2 * c->cap, h.n);
+      if (rc) return rc;
+      rc = ensure_uid_space(c, 2 * (h.uid_count + h.n) + 1024);
       if (rc) return rc;
       rc = clear_dev_err(c);
       if (rc) return rc;
@@ -2576,6 +2635,57 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       CK(cudaStreamSynchronize(c->stream));
       return rc;
     }
+  }
+  return ABS_OK;
+}
+
+int abs_gpu_set_defer_commit(abs_gpu_ctx* c, int defer) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (c->pending_commit) return set_err(c, ABS_ERR_STATE, "abs_gpu_commit is pending");
+  if (defer && c->cfg.model == ABS_MODEL_PROLIFERATION && c->cfg.detect_static_agents)
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT,
+                   "static detection with multi-domain additions is not supported (new-neighbour marks stay local)");
+  cudaSetDevice(c->device);
+  c->defer_commit = defer != 0;
+  return ensure_uid_space(c, c->uid_cap);
+}
+
+int abs_gpu_division_marks(abs_gpu_ctx* c, uint32_t* out, uint64_t cap, uint64_t* len) {
+  if (!c || !len) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  *len = h.uid_count;
+  if (!c->pending_commit) return set_err(c, ABS_ERR_STATE, "no deferred iteration to commit");
+  if (!out || cap < h.uid_count) return set_err(c, ABS_ERR_CAPACITY, "division mark buffer too small");
+  if (h.uid_count) CK(cudaMemcpyAsync(out, c->div_mark, h.uid_count * 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
+int abs_gpu_commit(abs_gpu_ctx* c, const uint32_t* global_marks, uint64_t len) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c->pending_commit) return ABS_OK;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (global_marks) {
+    if (len != h.uid_count) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "division marks length != uid_count");
+    if (len) CK(cudaMemcpyAsync(c->div_mark_g, global_marks, len * 4, cudaMemcpyDeviceToDevice, c->stream));
+  } else if (h.uid_count) {  // single domain: this rank's marks are everyone's
+    CK(cudaMemcpyAsync(c->div_mark_g, c->div_mark, h.uid_count * 4, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  launch_commit(c);
+  c->pending_commit = false;
+  CK(cudaGetLastError());
+  rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (h.err) {
+    rc = map_dev_err(c, h);
+    clear_dev_err(c);
+    return rc;
   }
   return ABS_OK;
 }

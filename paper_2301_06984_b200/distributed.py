@@ -297,6 +297,13 @@ class DeviceSlabDecomposition:
         self._alloc(cap)
         self._r0 = sim.report()
         self.iteration = 0
+        # additions (config 2): daughters are committed only after the ranks
+        # have summed their division marks, so uids match the single domain
+        from ._native import MODEL_PROLIFERATION
+        self.additions = sim.params.model == MODEL_PROLIFERATION
+        self._marks = None
+        if self.additions:
+            sim.set_defer_commit(True)
 
     def _alloc(self, cap):
         t = self.torch
@@ -395,9 +402,30 @@ class DeviceSlabDecomposition:
         grid, dims = g.as_override()
         self.sim.set_grid_override(grid, dims)
         self.sim.simulate(1)
+        if self.additions:
+            self._commit_additions()
         N.check(N.load().abs_gpu_drop_ghosts(self.sim._ctx), self.sim._ctx)
         self.iteration += 1
         return g
+
+    def _commit_additions(self):
+        """Sum the ranks' uid-indexed division marks (every uid divides on at
+        most one rank) and commit: daughter uid = uid_count + rank of the
+        parent among all dividers (commit.cpp:186-222)."""
+        t = self.torch
+        length = self.sim.division_marks()  # uid_count: identical on every rank
+        if self._marks is None or self._marks.numel() < max(length, 1):
+            self._marks = t.zeros(max(int(length * 1.5), 1024), dtype=t.int32, device=self.dev)
+        self.sim.division_marks(self._marks.data_ptr(), self._marks.numel())
+        view = self._marks[:length]
+        if self.transport == "nccl":
+            self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM)
+        else:
+            host = view.cpu()
+            self.dist.all_reduce(host, op=self.dist.ReduceOp.SUM)
+            view.copy_(host.to(self.dev))
+        t.cuda.current_stream().synchronize()  # the engine reads the sum on its own stream
+        self.sim.commit(view.data_ptr(), length)
 
     def totals(self):
         """Force evaluations and static skips summed over ranks since this

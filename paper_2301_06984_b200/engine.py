@@ -238,6 +238,24 @@ class Simulation:
         N.check(N.load().abs_gpu_sir_state(self._ctx, _p(st, C.c_uint8), _p(ti, C.c_uint32)), self._ctx)
         return st, ti
 
+    # -- multi-domain additions (deferred commit) ---------------------------
+    def set_defer_commit(self, defer: bool) -> None:
+        N.check(N.load().abs_gpu_set_defer_commit(self._ctx, 1 if defer else 0), self._ctx)
+
+    def division_marks(self, out_ptr=None, cap: int = 0) -> int:
+        """Copy this context's uid-indexed division marks of the pending
+        iteration into a device buffer (uint32, >= uid_count entries);
+        returns uid_count (call with out_ptr=None to size the buffer)."""
+        n = C.c_uint64(0)
+        rc = N.load().abs_gpu_division_marks(self._ctx, out_ptr, cap, C.byref(n))
+        if out_ptr is not None:
+            N.check(rc, self._ctx)
+        return int(n.value)
+
+    def commit(self, global_marks_ptr=None, length: int = 0) -> None:
+        """Finish the pending iteration's additions with the rank-summed marks."""
+        N.check(N.load().abs_gpu_commit(self._ctx, global_marks_ptr, length), self._ctx)
+
     def set_iteration(self, iteration: int) -> None:
         N.check(N.load().abs_gpu_set_iteration(self._ctx, iteration), self._ctx)
 

@@ -49,6 +49,8 @@ def _oparams(O, wl):
 def _make(case):
     if case == "c1":
         return CF.c1_relaxation(3000, seed=1), 6
+    if case == "c2":
+        return CF.c2_proliferation(side=6, seed=0), 50
     if case == "c3":
         return CF.c3_spheroid(3000, seed=2), 5
     return CF.c4_large_uniform(3000, seed=3), 4
@@ -170,7 +172,8 @@ def _dev_worker(rank, world, port, case, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     wl, steps = _make(case)
-    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=wl.mask)
+    mask = wl.mask if wl.mask is not None else np.ones(wl.n, np.uint8)  # None = behaviour on every agent
+    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=mask)
     sim = E.Simulation(E.SimulationParams(**wl.params), device=0)
     sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=st["beh"], uid=st["uid"], uid_count=wl.n)
     dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="host", cap=1 << 14)
@@ -183,7 +186,7 @@ def _dev_worker(rank, world, port, case, outdir):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3")])
+@pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3"), (2, "c2"), (3, "c2")])
 def test_device_exchange_matches_single_domain(oracle_mod, world, case):
     """Device-resident exchange (export/import kernels, packed records): the
     union of the ranks' populations equals the single-domain run."""
@@ -191,14 +194,14 @@ def test_device_exchange_matches_single_domain(oracle_mod, world, case):
     with tempfile.TemporaryDirectory() as tmp:
         mp.spawn(_dev_worker, args=(world, _free_port(), case, tmp), nprocs=world, join=True)
         parts = [dict(np.load(os.path.join(tmp, f"r{r}.npz"))) for r in range(world)]
-    keys = ["uid", "x", "y", "z", "d", "partners", "flags"]
+    keys = ["uid", "x", "y", "z", "d", "volume", "partners", "flags"]
     got = by_uid({k: np.concatenate([p[k] for p in parts]) for k in keys})
     wl, steps = _make(case)
     ref = O.PortSim(_oparams(O, wl), wl.x, wl.y, wl.z, wl.d, wl.mask)
     ref.simulate(steps)
     o = by_uid(ref.dump())
     assert np.array_equal(got["uid"], o["uid"])
-    for k in ("x", "y", "z", "d"):
+    for k in ("x", "y", "z", "d", "volume"):
         assert_close(got[k], o[k], 1e-9, 1.0, k)
     assert np.array_equal(got["partners"], o["partners"])
     assert np.array_equal(got["flags"], o["flags"])
