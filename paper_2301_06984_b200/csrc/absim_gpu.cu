@@ -1726,6 +1726,32 @@ __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const uns
   }
 }
 
+// Removal lookup with O(removed) scratch: every agent binary-searches its uid
+// in the sorted removal list; a hit records the agent's slot at the list's
+// original position (perm) and counts it.
+__global__ void k_find_slots(const unsigned long long* __restrict__ uid, const DevGrid* g,
+                             const unsigned long long* __restrict__ sorted_uids,
+                             const unsigned long long* __restrict__ perm, unsigned long long r,
+                             unsigned long long* __restrict__ slots, unsigned long long* __restrict__ found) {
+  const unsigned long long n = g->n;
+  unsigned long long hits = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long u = uid[i];
+    unsigned long long lo = 0, hi = r;
+    while (lo < hi) {
+      const unsigned long long mid = (lo + hi) >> 1;
+      if (sorted_uids[mid] < u) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < r && sorted_uids[lo] == u) {
+      slots[perm[lo]] = i;
+      ++hits;
+    }
+  }
+  if (hits) atomicAdd(found, hits);
+}
+
 // ------------------------------------------------------------ removal
 // remove_agents_parallel (commit.cpp:86-178): holes left of the split are
 // filled, in removal-list order, by surviving tail agents in index order.
@@ -3035,30 +3061,40 @@ int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   const unsigned long long n = h.n;
   if (r > n) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "more removals than agents");
   Soa& S = c->S[c->cur];
-  // uid -> slot, then the slot list in the given order
-  std::vector<unsigned long long> hu(n);
-  CK(cudaMemcpy(hu.data(), S.uid, n * 8, cudaMemcpyDeviceToHost));
-  std::vector<long long> slot_of(h.uid_count + 1, -1);
-  for (unsigned long long i = 0; i < n; ++i) slot_of[hu[i]] = (long long)i;
-  std::vector<unsigned long long> slots(r);
-  std::vector<char> seen(n, 0);
-  for (unsigned long long k = 0; k < r; ++k) {
-    if (uids[k] >= slot_of.size() || slot_of[uids[k]] < 0)
-      return set_err(c, ABS_ERR_INVALID_ARGUMENT, "unknown uid");
-    slots[k] = (unsigned long long)slot_of[uids[k]];
-    if (seen[slots[k]]) return set_err(c, ABS_ERR_STATE, "agent staged for removal twice");
-    seen[slots[k]] = 1;
+  // the removal list sorted on the host (O(r log r)); duplicates are the
+  // reference's double-staging error (agent.hpp:136-141)
+  std::vector<unsigned long long> perm(r);
+  for (unsigned long long k = 0; k < r; ++k) perm[k] = k;
+  std::sort(perm.begin(), perm.end(), [&](unsigned long long a, unsigned long long b) { return uids[a] < uids[b]; });
+  std::vector<unsigned long long> su(r);
+  for (unsigned long long k = 0; k < r; ++k) su[k] = uids[perm[k]];
+  for (unsigned long long k = 1; k < r; ++k)
+    if (su[k] == su[k - 1]) return set_err(c, ABS_ERR_STATE, "agent staged for removal twice");
+  unsigned long long *d_su, *d_perm, *d_found, *d_slots;
+  CK(dalloc(&d_su, r)); CK(dalloc(&d_perm, r)); CK(dalloc(&d_found, 1)); CK(dalloc(&d_slots, r));
+  CK(cudaMemcpyAsync(d_su, su.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(d_perm, perm.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(d_found, 0, 8, c->stream));
+  k_find_slots<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(S.uid, c->g, d_su, d_perm, r, d_slots, d_found);
+  ++c->launches;
+  unsigned long long found = 0;
+  CK(cudaMemcpyAsync(&found, d_found, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_su); cudaFree(d_perm); cudaFree(d_found);
+  if (found != r) {
+    cudaFree(d_slots);
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "unknown uid");
   }
   const unsigned long long new_size = n - r;
   unsigned long long *dslots, *len;
   unsigned int *to_right, *tail_alive, *hole_at, *tiles;
-  CK(dalloc(&dslots, r)); CK(dalloc(&len, 1));
+  dslots = d_slots;
+  CK(dalloc(&len, 1));
   CK(dalloc(&to_right, r + 1)); CK(dalloc(&tail_alive, r + 1)); CK(dalloc(&hole_at, r + 1));
   CK(dalloc(&tiles, r / kScanTile + 2));
   unsigned int* to_right_scan = nullptr;
   unsigned int* tail_scan = nullptr;
   CK(dalloc(&to_right_scan, r + 1)); CK(dalloc(&tail_scan, r + 1));
-  CK(cudaMemcpyAsync(dslots, slots.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(len, &r, 8, cudaMemcpyHostToDevice, c->stream));
   const int nb = grid_blocks(c, r);
   k_set_u32<<<nb, kThreads, 0, c->stream>>>(to_right, r + 1, 0u);

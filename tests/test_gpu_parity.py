@@ -426,6 +426,26 @@ def test_removal_worked_example(engine):
     assert sim.report().final_agent_count == 4
 
 
+def test_removal_large_unordered(engine, oracle_mod):
+    """remove_agents_parallel survivor order (commit.cpp:86-178) for a large
+    unordered removal list; slots are looked up on the device."""
+    rng = np.random.default_rng(5)
+    n = 20000
+    x = rng.uniform(0, 400, n)
+    y = rng.uniform(0, 400, n)
+    z = rng.uniform(0, 400, n)
+    d = rng.uniform(8, 12, n)
+    rem = rng.choice(n, 3000, replace=False)
+    sim = engine.Simulation(engine.SimulationParams())
+    sim.add_agents(x, y, z, d)
+    sim.remove_agents(rem.astype(np.uint64))
+    orc = oracle_mod.PortSim(oracle_mod.OracleParams(), x, y, z, d)
+    orc.remove(rem.astype(np.uint32))  # fresh upload: slot == uid
+    assert np.array_equal(sim.agents()["uid"], orc.dump()["uid"])
+    with pytest.raises(engine.AbsimError, match="twice"):
+        sim.remove_agents([int(sim.agents()["uid"][0])] * 2)
+
+
 def test_grid_growth_retry(engine, oracle_mod):
     """Agents spreading far beyond the initial grid force a bin-table regrow
     (device-side retry) without changing results."""
