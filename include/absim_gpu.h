@@ -158,6 +158,8 @@ int abs_gpu_local_bounds(abs_gpu_ctx* ctx, double* out7);
  *   mode 0 (migrate): owned agents with layer < lo -> out_lo, >= hi -> out_hi,
  *                     removed from this context;
  *   mode 1 (halo):    owned agents with layer == lo -> out_lo, == hi-1 -> out_hi.
+ *   mode | 2:         periodic z (a ring of layers, config 5): a migrant
+ *                     leaves through the nearer side modulo dims[2].
  * Returns ABS_ERR_CAPACITY when a count exceeds cap (counts are still set). */
 #define ABS_RECORD_BYTES 96
 int abs_gpu_export_layers(abs_gpu_ctx* ctx, const double* grid, const uint32_t* dims, int64_t lo, int64_t hi,

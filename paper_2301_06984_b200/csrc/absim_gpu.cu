@@ -1154,6 +1154,13 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
     const Pd me = load_pd(S.pd + i);
     unsigned char st = S.beh[i];
     unsigned int ti = S.partners[i];
+    if (S.flags[i] & kFlagGhost) {  // another rank's agent: start-of-step state, candidate only
+      reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
+      reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
+      next_state[i] = st;
+      next_t[i] = ti;
+      continue;
+    }
     if (st == ABS_SIR_I && a.iteration - ti >= rec) st = ABS_SIR_R;
     if (st == ABS_SIR_S) {
       const unsigned int cx = box_coord(me.x, 0.0, box, D0), cy = box_coord(me.y, 0.0, box, D1),
@@ -1203,6 +1210,7 @@ __global__ void __launch_bounds__(kThreads) k_sir_commit(Soa S, DevGrid* g,
     const unsigned char st = next_state[i];
     S.beh[i] = st;
     S.partners[i] = next_t[i];
+    if (S.flags[i] & kFlagGhost) continue;  // counted by its owner
     c[0] += st == ABS_SIR_S;
     c[1] += st == ABS_SIR_I;
     c[2] += st == ABS_SIR_R;
@@ -1420,10 +1428,14 @@ static_assert(sizeof(Rec) == 96, "record layout");
 // mode 0 (migrate): owned agents with box z-layer < lo -> out_lo, >= hi -> out_hi,
 //                   keep[i] = 0 for them. mode 1 (halo): layer == lo -> out_lo,
 //                   layer == hi - 1 -> out_hi, kept. Ghosts are never exported.
+// periodic (ring of z layers, config 5): a migrant goes to the nearer side
+// modulo dimz (a wrapped step from layer 0 to dimz-1 leaves through lo).
 __global__ void k_export(const Pd* __restrict__ pos, Soa S, unsigned long long cap, unsigned long long n,
                          double oz, double box, unsigned int dimz, long long lo, long long hi, int mode,
-                         Rec* __restrict__ out_lo, Rec* __restrict__ out_hi, unsigned long long out_cap,
-                         unsigned long long* __restrict__ counts, unsigned int* __restrict__ keep) {
+                         int periodic, Rec* __restrict__ out_lo, Rec* __restrict__ out_hi,
+                         unsigned long long out_cap, unsigned long long* __restrict__ counts,
+                         unsigned int* __restrict__ keep) {
+  const long long D = static_cast<long long>(dimz);
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd p = load_pd(pos + i);
@@ -1431,8 +1443,14 @@ __global__ void k_export(const Pd* __restrict__ pos, Soa S, unsigned long long c
     const long long layer = static_cast<long long>(box_coord(p.z, oz, box, dimz));
     int dest = -1;  // 0 -> lo, 1 -> hi
     if (!(fl & ABS_FLAG_GHOST)) {
-      if (mode == 0) dest = layer < lo ? 0 : (layer >= hi ? 1 : -1);
-      else dest = layer == lo ? 0 : (layer == hi - 1 ? 1 : -1);
+      if (mode == 0) {
+        if (layer < lo || layer >= hi) {
+          if (periodic) dest = ((lo - layer + D) % D) <= ((layer - (hi - 1) + D) % D) ? 0 : 1;
+          else dest = layer < lo ? 0 : 1;
+        }
+      } else {
+        dest = layer == lo ? 0 : (layer == hi - 1 ? 1 : -1);
+      }
     }
     if (keep) keep[i] = (mode == 0 && dest >= 0) ? 0u : 1u;
     if (dest < 0) continue;
@@ -2789,7 +2807,8 @@ static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
 
 int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* dims, int64_t lo, int64_t hi, int mode,
                           void* out_lo, void* out_hi, uint64_t cap, uint64_t* n_lo, uint64_t* n_hi) {
-  if (!c || !grid || !dims || (mode != 0 && mode != 1)) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c || !grid || !dims || mode < 0 || mode > 3) return ABS_ERR_INVALID_ARGUMENT;
+  const int halo = mode & 1, periodic = (mode >> 1) & 1;
   cudaSetDevice(c->device);
   DevGrid h{};
   int rc = read_grid(c, &h);
@@ -2800,8 +2819,8 @@ int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* di
   CK(cudaMemsetAsync(counts, 0, 16, c->stream));
   if (n) {
     k_export<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(
-        cur_pos(c), c->S[c->cur], c->cap, n, grid[2], grid[3], dims[2], lo, hi, mode, static_cast<Rec*>(out_lo),
-        static_cast<Rec*>(out_hi), cap, counts, mode == 0 ? c->rank : nullptr);
+        cur_pos(c), c->S[c->cur], c->cap, n, grid[2], grid[3], dims[2], lo, hi, halo, periodic,
+        static_cast<Rec*>(out_lo), static_cast<Rec*>(out_hi), cap, counts, halo == 0 ? c->rank : nullptr);
     ++c->launches;
   }
   unsigned long long hc[2] = {0, 0};
@@ -2811,7 +2830,7 @@ int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* di
   if (n_lo) *n_lo = hc[0];
   if (n_hi) *n_hi = hc[1];
   if (hc[0] > cap || hc[1] > cap) return set_err(c, ABS_ERR_CAPACITY, "export buffer too small");
-  if (mode == 0 && (hc[0] || hc[1])) return compact_population(c, n);
+  if (halo == 0 && (hc[0] || hc[1])) return compact_population(c, n);
   return ABS_OK;
 }
 

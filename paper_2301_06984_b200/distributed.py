@@ -260,17 +260,28 @@ class GpuRankEngine:
     beh_by_uid = None
 
 
-def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, mask=None):
-    """The owned slice of a population for `rank` (box layers of the initial grid)."""
+def sir_grid(L: float, r: float) -> GlobalGrid:
+    """Config 5's periodic grid, as abs_gpu_create builds it: D = max(3,
+    floor(L / r)) boxes of L / D per axis, origin 0."""
+    D = max(3, int(math.floor(L / r)))
+    return GlobalGrid(np.zeros(3), L / D, r, np.array([D, D, D], np.int64))
+
+
+def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, mask=None, grid=None):
+    """The owned slice of a population for `rank` (box layers of the initial
+    grid, or of `grid` when given — e.g. the periodic grid of config 5)."""
     n = len(x)
     st = {"x": np.asarray(x, np.float64), "y": np.asarray(y, np.float64), "z": np.asarray(z, np.float64),
           "d": np.asarray(d, np.float64), "volume": np.zeros(n), "fx": np.zeros(n), "fy": np.zeros(n),
           "fz": np.zeros(n), "uid": np.arange(n, dtype=np.uint64), "flags": np.zeros(n, np.uint8),
           "partners": np.zeros(n, np.uint32),
           "beh": np.zeros(n, np.uint8) if mask is None else np.asarray(mask, np.uint8)}
-    b = np.array([st["x"].min(), st["y"].min(), st["z"].min(), st["x"].max(), st["y"].max(),
-                  st["z"].max(), st["d"].max()])
-    g = global_grid(b, fixed_box_length)
+    if grid is None:
+        b = np.array([st["x"].min(), st["y"].min(), st["z"].min(), st["x"].max(), st["y"].max(),
+                      st["z"].max(), st["d"].max()])
+        g = global_grid(b, fixed_box_length)
+    else:
+        g = grid
     L = layer_bounds(int(g.dims[2]), world)
     lay = box_layer(st["z"], g)
     return _take(st, np.nonzero((lay >= L[rank]) & (lay < L[rank + 1]))[0])
@@ -299,11 +310,18 @@ class DeviceSlabDecomposition:
         self.iteration = 0
         # additions (config 2): daughters are committed only after the ranks
         # have summed their division marks, so uids match the single domain
-        from ._native import MODEL_PROLIFERATION
+        from ._native import MODEL_PROLIFERATION, MODEL_SIR
         self.additions = sim.params.model == MODEL_PROLIFERATION
         self._marks = None
         if self.additions:
             sim.set_defer_commit(True)
+        # config 5: the periodic cube's fixed grid (abs_gpu_create: box L / D,
+        # D = max(3, floor(L / r))); slabs form a ring of z layers
+        self.periodic = sim.params.model == MODEL_SIR
+        if self.periodic:
+            self._fixed = sir_grid(float(sim.params.model_params[0]), float(sim.params.model_params[1]))
+        # NCCL: the first P2P batch must not be a communicator's first call
+        self.dist.barrier()
 
     def _alloc(self, cap):
         t = self.torch
@@ -321,52 +339,85 @@ class DeviceSlabDecomposition:
         self.dist.all_reduce(t, op=op)
         return t.cpu().numpy()
 
+    def _peers(self):
+        """(lo peer, hi peer); None at an open slab end. Periodic: a ring."""
+        r, w = self.rank, self.world
+        if w == 1:
+            return None, None
+        if self.periodic:
+            return (r - 1) % w, (r + 1) % w
+        return (r - 1 if r > 0 else None), (r + 1 if r < w - 1 else None)
+
+    def _p2p(self, sends, recvs):
+        """One batched round of point-to-point transfers (a single NCCL group,
+        so paired sends/receives cannot deadlock). sends/recvs: lists of
+        (tensor, peer, tag). Messages to one peer are posted lo-side first and
+        received hi-side first on every rank, so at world 2 on a ring (both
+        peers the same rank) the in-order matching of NCCL pairs each message
+        with the right buffer; the tags do the same for gloo."""
+        d = self.dist
+        ops = [d.P2POp(d.isend, t, p, tag=tag) for t, p, tag in sends]
+        ops += [d.P2POp(d.irecv, t, p, tag=tag) for t, p, tag in recvs]
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+
     def _exchange(self, n_lo: int, n_hi: int):
-        """Send send_lo[:n_lo] to r-1 and send_hi[:n_hi] to r+1; returns the
-        received record counts (from r-1, from r+1) into recv_lo / recv_hi."""
-        t, d, r, w = self.torch, self.dist, self.rank, self.world
-        peers = [(p, n, sk, rk) for p, n, sk, rk in ((r - 1, n_lo, "send_lo", "recv_lo"),
-                                                   (r + 1, n_hi, "send_hi", "recv_hi")) if 0 <= p < w]
-        ops, cnt = [], {}
-        for p, n, _, _ in peers:
-            cs = self._coll_tensor(np.array([n], np.int64))
-            cr = self._coll_tensor(np.zeros(1, np.int64))
-            ops += [d.isend(cs, p), d.irecv(cr, p)]
-            cnt[p] = cr
-        for o in ops:
-            o.wait()
-        got = {p: int(cnt[p].cpu().item()) for p, *_ in peers}
-        need = max([n for _, n, _, _ in peers] + list(got.values()) + [0])
+        """Send send_lo[:n_lo] to the lo peer and send_hi[:n_hi] to the hi peer;
+        returns the received record counts (from lo peer, from hi peer) into
+        recv_lo / recv_hi. Tag 1: travels to the receiver's hi side, tag 0: to
+        its lo side."""
+        t = self.torch
+        lo_p, hi_p = self._peers()
+        sends, recvs, cnt = [], [], {}
+        if lo_p is not None:
+            sends.append((self._coll_tensor(np.array([n_lo], np.int64)), lo_p, 1))
+        if hi_p is not None:
+            sends.append((self._coll_tensor(np.array([n_hi], np.int64)), hi_p, 0))
+        if hi_p is not None:
+            cnt["hi"] = self._coll_tensor(np.zeros(1, np.int64))
+            recvs.append((cnt["hi"], hi_p, 1))
+        if lo_p is not None:
+            cnt["lo"] = self._coll_tensor(np.zeros(1, np.int64))
+            recvs.append((cnt["lo"], lo_p, 0))
+        self._p2p(sends, recvs)
+        got = {k: int(v.cpu().item()) for k, v in cnt.items()}
+        need = max([n_lo if lo_p is not None else 0, n_hi if hi_p is not None else 0] + list(got.values()) + [0])
         if need > self.cap:
             raise RuntimeError("halo larger than the exchange buffers")
-        ops, staged = [], []
-        for p, n, sk, rk in peers:
-            nb, mb = n * self.RECORD, got[p] * self.RECORD
+        staged = []
+
+        def buf(key, nbytes, incoming):
             if self.transport == "nccl":
-                if nb:
-                    ops.append(d.isend(self.buf[sk][:nb], p))
-                if mb:
-                    ops.append(d.irecv(self.buf[rk][:mb], p))
-            else:
-                if nb:
-                    ops.append(d.isend(self.buf[sk][:nb].cpu(), p))
-                if mb:
-                    host = t.empty(mb, dtype=t.uint8)
-                    ops.append(d.irecv(host, p))
-                    staged.append((rk, host))
-        for o in ops:
-            o.wait()
-        for rk, host in staged:
-            self.buf[rk][:host.numel()].copy_(host.to(self.dev))
+                return self.buf[key][:nbytes]
+            if not incoming:
+                return self.buf[key][:nbytes].cpu()
+            host = t.empty(nbytes, dtype=t.uint8)
+            staged.append((key, host))
+            return host
+        sends, recvs = [], []
+        if lo_p is not None and n_lo:
+            sends.append((buf("send_lo", n_lo * self.RECORD, False), lo_p, 1))
+        if hi_p is not None and n_hi:
+            sends.append((buf("send_hi", n_hi * self.RECORD, False), hi_p, 0))
+        if got.get("hi", 0):
+            recvs.append((buf("recv_hi", got["hi"] * self.RECORD, True), hi_p, 1))
+        if got.get("lo", 0):
+            recvs.append((buf("recv_lo", got["lo"] * self.RECORD, True), lo_p, 0))
+        self._p2p(sends, recvs)
+        for key, host in staged:
+            self.buf[key][:host.numel()].copy_(host.to(self.dev))
         # the engine consumes the buffers on its own CUDA stream: make the
         # received bytes (NCCL / staging copies on torch's stream) visible first
         t.cuda.current_stream().synchronize()
-        return (got.get(r - 1, 0), got.get(r + 1, 0))
+        return got.get("lo", 0), got.get("hi", 0)
 
     # -- one iteration -------------------------------------------------------------
     def _export(self, g, lo, hi, mode):
         from . import _native as N
         import ctypes as C
+        if self.periodic:
+            mode |= 2
         grid, dims = g.as_override()
         grid = np.ascontiguousarray(grid)
         dims = np.ascontiguousarray(dims, np.uint32)
@@ -386,9 +437,12 @@ class DeviceSlabDecomposition:
 
     def step(self):
         from . import _native as N
-        b = self.sim.local_bounds()
-        red = self._allreduce(np.concatenate([-b[:3], b[3:]]), self.dist.ReduceOp.MAX)
-        g = global_grid(np.concatenate([-red[:3], red[3:]]), self.fixed_box_length)
+        if self.periodic:  # fixed grid, already forced at context creation
+            g = self._fixed
+        else:
+            b = self.sim.local_bounds()
+            red = self._allreduce(np.concatenate([-b[:3], b[3:]]), self.dist.ReduceOp.MAX)
+            g = global_grid(np.concatenate([-red[:3], red[3:]]), self.fixed_box_length)
         L = layer_bounds(int(g.dims[2]), self.world)
         lo, hi = L[self.rank], L[self.rank + 1]
         n_lo, n_hi = self._export(g, lo, hi, 0)            # migrants leave
@@ -399,8 +453,9 @@ class DeviceSlabDecomposition:
         got_lo, got_hi = self._exchange(n_lo, n_hi)
         self._import("recv_lo", got_lo, True)
         self._import("recv_hi", got_hi, True)
-        grid, dims = g.as_override()
-        self.sim.set_grid_override(grid, dims)
+        if not self.periodic:
+            grid, dims = g.as_override()
+            self.sim.set_grid_override(grid, dims)
         self.sim.simulate(1)
         if self.additions:
             self._commit_additions()
@@ -426,6 +481,11 @@ class DeviceSlabDecomposition:
             view.copy_(host.to(self.dev))
         t.cuda.current_stream().synchronize()  # the engine reads the sum on its own stream
         self.sim.commit(view.data_ptr(), length)
+
+    def sir_counts(self):
+        """Config 5: S/I/R over all ranks after the last iteration."""
+        c = self._allreduce(np.array(self.sim.sir_counts(), np.int64), self.dist.ReduceOp.SUM)
+        return [int(v) for v in c]
 
     def totals(self):
         """Force evaluations and static skips summed over ranks since this

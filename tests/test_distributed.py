@@ -51,6 +51,8 @@ def _make(case):
         return CF.c1_relaxation(3000, seed=1), 6
     if case == "c2":
         return CF.c2_proliferation(side=6, seed=0), 50
+    if case == "c5":
+        return CF.c5_sir(4000, seed=1), 26
     if case == "c3":
         return CF.c3_spheroid(3000, seed=2), 5
     return CF.c4_large_uniform(3000, seed=3), 4
@@ -161,6 +163,14 @@ def test_gpu_ranks_match_single_domain(oracle_mod, world, case):
     assert np.array_equal(got["flags"], o["flags"])
     c = ref.counts()
     assert (int(parts[0]["evals"]), int(parts[0]["skips"])) == (c["force_evaluations"], c["force_skips"])
+    if case == "c5":  # SIR on the periodic ring: states and counts bit-exact
+        gs = by_uid({"uid": got["uid"], "state": np.concatenate([p["state"] for p in parts]),
+                     "t": np.concatenate([p["t"] for p in parts])})
+        os_, ot = ref.sir_state()
+        od = by_uid({"uid": ref.dump()["uid"], "state": os_, "t": ot})
+        assert np.array_equal(gs["state"], od["state"]) and np.array_equal(gs["t"], od["t"])
+        assert list(parts[0]["sir"]) == list(ref.sir_counts())
+        assert ref.sir_counts()[1] + ref.sir_counts()[2] > 40  # the epidemic spread
 
 
 def _dev_worker(rank, world, port, case, outdir):
@@ -172,21 +182,29 @@ def _dev_worker(rank, world, port, case, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     wl, steps = _make(case)
+    sir = wl.params.get("model") == E.MODEL_SIR
     mask = wl.mask if wl.mask is not None else np.ones(wl.n, np.uint8)  # None = behaviour on every agent
-    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=mask)
+    grid = D.sir_grid(wl.params["model_params"][0], wl.params["model_params"][1]) if sir else None
+    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=mask, grid=grid)
     sim = E.Simulation(E.SimulationParams(**wl.params), device=0)
-    sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=st["beh"], uid=st["uid"], uid_count=wl.n)
+    sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=None if sir else st["beh"], uid=st["uid"],
+                   uid_count=wl.n)  # SIR: initial states from (seed, uid), as in one domain
     dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="host", cap=1 << 14)
     dec.simulate(steps)
     a = sim.agents()
     evals, skips = dec.totals()
-    np.savez(os.path.join(outdir, f"r{rank}.npz"), evals=evals, skips=skips, **a)
+    extra = {}
+    if dec.periodic:
+        extra["state"], extra["t"] = sim.sir_state()
+        extra["sir"] = np.array(dec.sir_counts())
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), evals=evals, skips=skips, **a, **extra)
     dist.barrier()
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3"), (2, "c2"), (3, "c2")])
+@pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3"), (2, "c2"), (3, "c2"), (2, "c5"),
+                                        (3, "c5")])
 def test_device_exchange_matches_single_domain(oracle_mod, world, case):
     """Device-resident exchange (export/import kernels, packed records): the
     union of the ranks' populations equals the single-domain run."""
