@@ -54,7 +54,8 @@ typedef struct {
   double dt, k, max_disp, threshold, fixed_box;
   uint64_t sorting_frequency;
   int32_t detect_static;
-  int32_t model; /* 0 none, 1 volume grow/divide, 2 drive, 3 grow */
+  int32_t model; /* 0 none, 1 volume grow/divide, 2 drive, 3 grow, 4 SIR,
+                    5 models::GrowDivide, 6 models::Cohere */
   double mp[8];
 } orc_params;
 
@@ -69,6 +70,8 @@ typedef struct {
   uint8_t* flags;
   uint8_t* beh;
   double* vol;
+  uint32_t* tag;   /* Agent::tag (agent.hpp:35-36) */
+  uint64_t* rngc;  /* Agent::rng_counter (agent.hpp:145, 188) */
   uint64_t uid_counter, iteration;
   uint64_t evals, skips, added, removed, sorted;
   /* grid */
@@ -86,6 +89,7 @@ typedef struct {
   uint64_t* s_uid;
   double *s_x, *s_y, *s_z, *s_d, *s_vol;
   uint8_t* s_beh;
+  uint32_t* s_tag;
 } orc_sim;
 
 static void* xrealloc(void* p, size_t n) {
@@ -101,7 +105,7 @@ static void reserve(orc_sim* s, uint64_t want) {
 #define GROW(f) s->f = xrealloc(s->f, c * sizeof(*s->f))
   GROW(uid); GROW(x); GROW(y); GROW(z); GROW(d); GROW(tx); GROW(ty); GROW(tz);
   GROW(tg); GROW(fx); GROW(fy); GROW(fz); GROW(partners); GROW(flags); GROW(beh);
-  GROW(vol); GROW(succ);
+  GROW(vol); GROW(succ); GROW(tag); GROW(rngc);
 #undef GROW
   s->cap = c;
 }
@@ -116,6 +120,8 @@ static void init_slot(orc_sim* s, uint64_t i, uint64_t uid, double x, double y, 
   s->flags[i] = flags;
   s->beh[i] = beh;
   s->vol[i] = vol;
+  s->tag[i] = 0;
+  s->rngc[i] = 0;
 }
 
 orc_sim* orc_create(const orc_params* p, uint64_t n, const double* x, const double* y,
@@ -166,8 +172,9 @@ void orc_destroy(orc_sim* s) {
   free(s->uid); free(s->x); free(s->y); free(s->z); free(s->d); free(s->tx);
   free(s->ty); free(s->tz); free(s->tg); free(s->fx); free(s->fy); free(s->fz);
   free(s->partners); free(s->flags); free(s->beh); free(s->vol); free(s->succ);
+  free(s->tag); free(s->rngc);
   free(s->head); free(s->count); free(s->s_uid); free(s->s_x); free(s->s_y);
-  free(s->s_z); free(s->s_d); free(s->s_vol); free(s->s_beh);
+  free(s->s_z); free(s->s_d); free(s->s_vol); free(s->s_beh); free(s->s_tag);
   free(s);
 }
 
@@ -493,7 +500,12 @@ static int run_staticness(orc_sim* s) {
 }
 
 /* ---- behaviours (absim_models.h / models.hpp:69-83) -------------------- */
+static void stage_daughter_tag(orc_sim* s, double x, double y, double z, double d, double vol, uint32_t tag);
 static void stage_daughter(orc_sim* s, double x, double y, double z, double d, double vol) {
+  stage_daughter_tag(s, x, y, z, d, vol, 0);
+}
+
+static void stage_daughter_tag(orc_sim* s, double x, double y, double z, double d, double vol, uint32_t tag) {
   if (s->nstage == s->stage_cap) {
     s->stage_cap = s->stage_cap ? 2 * s->stage_cap : 64;
     s->s_uid = xrealloc(s->s_uid, s->stage_cap * sizeof *s->s_uid);
@@ -503,12 +515,42 @@ static void stage_daughter(orc_sim* s, double x, double y, double z, double d, d
     s->s_d = xrealloc(s->s_d, s->stage_cap * sizeof *s->s_d);
     s->s_vol = xrealloc(s->s_vol, s->stage_cap * sizeof *s->s_vol);
     s->s_beh = xrealloc(s->s_beh, s->stage_cap * sizeof *s->s_beh);
+    s->s_tag = xrealloc(s->s_tag, s->stage_cap * sizeof *s->s_tag);
   }
   const uint64_t k = s->nstage++;
   s->s_uid[k] = s->uid_counter++; /* resource_manager.hpp:44-46 at creation */
   s->s_x[k] = x; s->s_y[k] = y; s->s_z[k] = z; s->s_d[k] = d;
   s->s_vol[k] = vol;
   s->s_beh[k] = 1;
+  s->s_tag[k] = tag;
+}
+
+/* RandomStream::unit_vector (random.hpp:47-52) on the agent's own stream:
+ * two draws at the agent's counter (advanced), cos/sin from libm. */
+static void orc_unit_vector(uint64_t seed, uint64_t uid, uint64_t* counter, double out[3]) {
+  const double u1 = abs_u01(abs_rng_word(seed, uid, (*counter)++));
+  const double zz = -1.0 + (1.0 - -1.0) * u1;
+  const double two_pi = 2.0 * 3.14159265358979323846;
+  const double u2 = abs_u01(abs_rng_word(seed, uid, (*counter)++));
+  const double phi = 0.0 + (two_pi - 0.0) * u2;
+  const double r = sqrt(smax(0.0, 1.0 - zz * zz));
+  out[0] = r * cos(phi);
+  out[1] = r * sin(phi);
+  out[2] = zz;
+}
+
+typedef struct {
+  double sx, sy, sz;
+  uint64_t count;
+  uint32_t tag;
+} cohere_ctx;
+
+static void cohere_visit(orc_sim* s, void* vctx, uint64_t j, double d2) {
+  (void)d2;
+  cohere_ctx* c = (cohere_ctx*)vctx;
+  if (s->tag[j] != c->tag) return;
+  c->sx += s->x[j]; c->sy += s->y[j]; c->sz += s->z[j];
+  ++c->count;
 }
 
 static int run_behaviour(orc_sim* s, uint64_t i) {
@@ -537,6 +579,28 @@ static int run_behaviour(orc_sim* s, uint64_t i) {
     if (s->d[i] < cap) {
       const double rem = cap - s->d[i];
       s->tg[i] += rem < p->mp[0] ? rem : p->mp[0];
+    }
+  } else if (p->model == 5) { /* models::GrowDivide (models.hpp:15-37): mp rate, threshold, initial d */
+    if (s->d[i] >= p->mp[1]) {
+      double dir[3];
+      orc_unit_vector(p->seed, s->uid[i], &s->rngc[i], dir); /* ctx.random(), random.hpp:47-52 */
+      const double half = 0.5 * s->d[i];
+      stage_daughter_tag(s, s->x[i] + dir[0] * half, s->y[i] + dir[1] * half, s->z[i] + dir[2] * half,
+                         p->mp[2], 0.0, s->tag[i]);
+      s->tg[i] += p->mp[2] - s->d[i];
+    } else {
+      s->tg[i] += p->mp[0];
+    }
+  } else if (p->model == 6) { /* models::Cohere (models.hpp:42-64): mp attraction radius, speed */
+    cohere_ctx cc = {0.0, 0.0, 0.0, 0, s->tag[i]};
+    if (for_each_neighbor(s, i, s->x[i], s->y[i], s->z[i], p->mp[0] * p->mp[0], cohere_visit, &cc)) return -1;
+    if (cc.count == 0) return 0;
+    const double inv = 1.0 / (double)cc.count;
+    const double tx = cc.sx * inv - s->x[i], ty = cc.sy * inv - s->y[i], tz = cc.sz * inv - s->z[i];
+    const double dist = sqrt((tx * tx + ty * ty) + tz * tz);
+    if (dist > 0.0) {
+      const double f = p->mp[1] / dist;
+      s->tx[i] += tx * f; s->ty[i] += ty * f; s->tz[i] += tz * f;
     }
   }
   return 0;
@@ -574,6 +638,26 @@ static void move_slot(orc_sim* s, uint64_t dst, uint64_t src) {
   s->flags[dst] = s->flags[src];
   s->beh[dst] = s->beh[src];
   s->vol[dst] = s->vol[src];
+  s->tag[dst] = s->tag[src];
+  s->rngc[dst] = s->rngc[src];
+}
+
+/* Agent::tag / rng_counter in storage order (models.hpp, agent.hpp:35-36, 145) */
+int orc_set_tags(orc_sim* s, const uint32_t* tags) {
+  for (uint64_t i = 0; i < s->n; ++i) s->tag[i] = tags[i];
+  return 0;
+}
+int orc_tags(const orc_sim* s, uint32_t* out) {
+  for (uint64_t i = 0; i < s->n; ++i) out[i] = s->tag[i];
+  return 0;
+}
+int orc_set_rng_counters(orc_sim* s, const uint64_t* c) {
+  for (uint64_t i = 0; i < s->n; ++i) s->rngc[i] = c[i];
+  return 0;
+}
+int orc_rng_counters(const orc_sim* s, uint64_t* out) {
+  for (uint64_t i = 0; i < s->n; ++i) out[i] = s->rngc[i];
+  return 0;
 }
 
 /* commit.cpp:86-178 (five steps, slot semantics independent of workers) */
@@ -609,9 +693,11 @@ static int run_commit(orc_sim* s) {
   if (s->nstage == 0) return 0;
   if (s->p.detect_static && mark_new_agent_neighbors(s)) return -1;
   reserve(s, s->n + s->nstage);
-  for (uint64_t k = 0; k < s->nstage; ++k)
+  for (uint64_t k = 0; k < s->nstage; ++k) {
     init_slot(s, s->n + k, s->s_uid[k], s->s_x[k], s->s_y[k], s->s_z[k], s->s_d[k],
               s->s_beh[k], s->s_vol[k], F_NEWLY_ADDED);
+    s->tag[s->n + k] = s->s_tag[k]; /* daughter.set_tag(a.tag()), models.hpp:27 */
+  }
   s->n += s->nstage;
   s->added += s->nstage;
   s->nstage = 0;
@@ -735,7 +821,7 @@ int orc_sort(orc_sim* s, uint64_t* moved) {
   tmp.cap = 0;
   tmp.uid = NULL; tmp.x = tmp.y = tmp.z = tmp.d = NULL; tmp.tx = tmp.ty = tmp.tz = tmp.tg = NULL;
   tmp.fx = tmp.fy = tmp.fz = NULL; tmp.partners = NULL; tmp.flags = NULL; tmp.beh = NULL;
-  tmp.vol = NULL; tmp.succ = NULL;
+  tmp.vol = NULL; tmp.succ = NULL; tmp.tag = NULL; tmp.rngc = NULL;
   reserve(&tmp, s->n);
   for (uint64_t i = 0; i < s->n; ++i) {
     const uint64_t j = order[i];
@@ -745,19 +831,21 @@ int orc_sort(orc_sim* s, uint64_t* moved) {
     tmp.fx[i] = s->fx[j]; tmp.fy[i] = s->fy[j]; tmp.fz[i] = s->fz[j];
     tmp.partners[i] = s->partners[j]; tmp.flags[i] = s->flags[j]; tmp.beh[i] = s->beh[j];
     tmp.vol[i] = s->vol[j];
+    tmp.tag[i] = s->tag[j];
+    tmp.rngc[i] = s->rngc[j];
   }
   free(order);
 #define SWAPF(f) do { void* t_ = s->f; s->f = tmp.f; tmp.f = t_; } while (0)
   SWAPF(uid); SWAPF(x); SWAPF(y); SWAPF(z); SWAPF(d); SWAPF(tx); SWAPF(ty); SWAPF(tz);
   SWAPF(tg); SWAPF(fx); SWAPF(fy); SWAPF(fz); SWAPF(partners); SWAPF(flags); SWAPF(beh);
-  SWAPF(vol); SWAPF(succ);
+  SWAPF(vol); SWAPF(succ); SWAPF(tag); SWAPF(rngc);
 #undef SWAPF
   const uint64_t c2 = s->cap;
   s->cap = tmp.cap;
   tmp.cap = c2;
   free(tmp.uid); free(tmp.x); free(tmp.y); free(tmp.z); free(tmp.d); free(tmp.tx); free(tmp.ty);
   free(tmp.tz); free(tmp.tg); free(tmp.fx); free(tmp.fy); free(tmp.fz); free(tmp.partners);
-  free(tmp.flags); free(tmp.beh); free(tmp.vol); free(tmp.succ);
+  free(tmp.flags); free(tmp.beh); free(tmp.vol); free(tmp.succ); free(tmp.tag); free(tmp.rngc);
   s->sorted += 0; /* one domain: nothing migrates (agents_moved counts domain changes) */
   return 0;
 }

@@ -196,6 +196,22 @@ class _Sim:
         self._check(self.lib()[f"{self.prefix}sort"](self.h, C.byref(moved)))
         return int(moved.value)
 
+    def set_tags(self, tags):
+        """Agent::set_tag per agent, storage order (agent.hpp:35-36)."""
+        t = np.ascontiguousarray(tags, np.uint32)
+        self._check(self.lib()[f"{self.prefix}set_tags"](self.h, _ptr(t, C.c_uint32)))
+
+    def tags(self) -> np.ndarray:
+        out = np.zeros(self.counts()["agents"], np.uint32)
+        self._check(self.lib()[f"{self.prefix}tags"](self.h, _ptr(out, C.c_uint32)))
+        return out
+
+    def rng_counters(self) -> np.ndarray:
+        """Agent::rng_counter per agent, storage order (agent.hpp:145)."""
+        out = np.zeros(self.counts()["agents"], np.uint64)
+        self._check(self.lib()[f"{self.prefix}rng_counters"](self.h, _ptr(out, C.c_uint64)))
+        return out
+
 
 def _bind(lib, prefix, ref_style):
     lib[f"{prefix}last_error"].restype = C.c_char_p
@@ -209,6 +225,9 @@ def _bind(lib, prefix, ref_style):
     lib[f"{prefix}neighbors"].restype = C.c_int64
     lib[f"{prefix}neighbors"].argtypes = [C.c_void_p, _U64, _U64, C.c_uint64]
     lib[f"{prefix}sort"].argtypes = [C.c_void_p, _U64]
+    lib[f"{prefix}set_tags"].argtypes = [C.c_void_p, _U32]
+    lib[f"{prefix}tags"].argtypes = [C.c_void_p, _U32]
+    lib[f"{prefix}rng_counters"].argtypes = [C.c_void_p, _U64]
     if ref_style:
         lib[f"{prefix}counts"].argtypes = [C.c_void_p, _U64, _D]
     else:
@@ -269,6 +288,7 @@ class PortSim(_Sim):
             d = _LibDict(C.CDLL(PORT_SO))
             _bind(d, "orc_", False)
             d["orc_remove"].argtypes = [C.c_void_p, _U32, C.c_uint32]
+            d["orc_set_rng_counters"].argtypes = [C.c_void_p, _U64]
             d["orc_set_grid_override"].argtypes = [C.c_void_p, _D, _U32]
             d["orc_dump_beh"].argtypes = [C.c_void_p, _U8, _U32]
             d["orc_sir_counts"].argtypes = [C.c_void_p, _U64]
@@ -325,6 +345,10 @@ class PortSim(_Sim):
     def remove(self, slots):
         s = np.ascontiguousarray(slots, dtype=np.uint32)
         self._check(self.lib()["orc_remove"](self.h, _ptr(s, C.c_uint32), len(s)))
+
+    def set_rng_counters(self, c):
+        v = np.ascontiguousarray(c, np.uint64)
+        self._check(self.lib()["orc_set_rng_counters"](self.h, _ptr(v, C.c_uint64)))
 
 
 def morton_encode3(x: int, y: int, z: int) -> int:

@@ -154,6 +154,12 @@ void* ref_create(const RefParams* rp, std::uint64_t n, const double* x, const do
       } else if (rp->model == 3) {
         models::Grow proto(rp->mp[0], rp->mp[1]);
         a.add_behavior(rm.clone_behavior(proto, dom));
+      } else if (rp->model == 5) {  // the reference's own models (models.hpp:15-64)
+        models::GrowDivide proto(rp->mp[0], rp->mp[1], rp->mp[2]);
+        a.add_behavior(rm.clone_behavior(proto, dom));
+      } else if (rp->model == 6) {
+        models::Cohere proto(rp->mp[0], rp->mp[1]);
+        a.add_behavior(rm.clone_behavior(proto, dom));
       }
     }
     r = h.release();
@@ -179,6 +185,8 @@ void* ref_create_builtin(const RefParams* rp, const char* name, std::uint64_t n)
       models::build_static_front(*h->sim, n, cfg);
     } else if (which == "clustering") {
       models::build_clustering(*h->sim, n);
+    } else if (which == "proliferation") {
+      models::build_proliferation(*h->sim, n);
     } else {
       throw std::invalid_argument("unknown builtin population: " + which);
     }
@@ -242,6 +250,28 @@ int ref_dump(void* h, std::uint64_t* uid, double* x, double* y, double* z, doubl
         }
       }
     }
+  });
+}
+
+// Agent::tag and rng_counter in storage order (agent.hpp:35-36, 145).
+int ref_set_tags(void* h, const std::uint32_t* tags) {
+  return guarded([&] {
+    const auto agents = storage_order(static_cast<Ref*>(h)->sim->resource_manager());
+    for (std::size_t i = 0; i < agents.size(); ++i) agents[i]->set_tag(tags[i]);
+  });
+}
+
+int ref_tags(void* h, std::uint32_t* out) {
+  return guarded([&] {
+    const auto agents = storage_order(static_cast<Ref*>(h)->sim->resource_manager());
+    for (std::size_t i = 0; i < agents.size(); ++i) out[i] = agents[i]->tag();
+  });
+}
+
+int ref_rng_counters(void* h, std::uint64_t* out) {
+  return guarded([&] {
+    const auto agents = storage_order(static_cast<Ref*>(h)->sim->resource_manager());
+    for (std::size_t i = 0; i < agents.size(); ++i) out[i] = *agents[i]->rng_counter();
   });
 }
 

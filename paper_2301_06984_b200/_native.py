@@ -23,6 +23,7 @@ ABS_ERR_NO_DEVICE = 7
 ABS_ERR_STATE = 8
 
 MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3, 4
+MODEL_GROW_DIVIDE, MODEL_COHERE = 5, 6  # the reference's own models::GrowDivide / models::Cohere
 FLAG_GHOST = 128
 
 # every symbol include/absim_gpu.h declares (checked by tests/test_abi.py)

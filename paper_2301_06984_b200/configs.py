@@ -59,6 +59,8 @@ class Workload:
     params: dict = field(default_factory=dict)  # SimulationParams fields
     steps: int = 1
     bytes_per_agent_iteration: int = 128
+    tags: np.ndarray | None = None          # Agent::tag (reference models)
+    rng_counters: np.ndarray | None = None  # Agent::rng_counter after population build
 
     @property
     def n(self) -> int:
@@ -143,6 +145,42 @@ def c5_sir(n: int = 10_000_000, seed: int = 0) -> Workload:
     return Workload("c5_sir", x, y, z, np.ones(n), None,
                     dict(seed=seed, model=N.MODEL_SIR, model_params=[L, 2.0, 1.0, 20.0, 0.1]),
                     steps=300, bytes_per_agent_iteration=120)
+
+
+def _cube_side(n: int) -> int:
+    s = 1
+    while s * s * s < n:
+        s += 1
+    return s
+
+
+def ref_proliferation(n: int = 4096) -> Workload:
+    """The reference's own build_proliferation (models.cpp:21-38): a cubic
+    lattice of ceil(n^(1/3))^3 cells (x-major), spacing 20, d 10, each with
+    models::GrowDivide(rate 2, threshold 14, initial 10) (models.hpp:15-37)."""
+    s = _cube_side(n)
+    g = np.arange(s, dtype=np.float64) * 20.0
+    x, y, z = (a.ravel() for a in np.meshgrid(g, g, g, indexing="ij"))
+    m = len(x)
+    return Workload("ref_proliferation", x.copy(), y.copy(), z.copy(), np.full(m, 10.0), None,
+                    dict(seed=42, model=N.MODEL_GROW_DIVIDE, model_params=[2.0, 14.0, 10.0]),
+                    steps=40, bytes_per_agent_iteration=128, tags=np.zeros(m, np.uint32),
+                    rng_counters=np.zeros(m, np.uint64))
+
+
+def ref_clustering(n: int = 10_000, seed: int = 42) -> Workload:
+    """The reference's own build_clustering (models.cpp:40-61): n cells of
+    two interleaved types (tag = uid % 2) uniformly in a cube of side
+    cbrt(n) * 20, positions from each agent's own stream (counters 0..2, so
+    its rng_counter is 3 afterwards), d 10, models::Cohere(30, 1)
+    (models.hpp:42-64); tune_clustering_params pins the box length to 30."""
+    side = math.cbrt(float(n)) * 20.0
+    uid = np.arange(n, dtype=np.uint64)
+    x, y, z = (0.0 + (side - 0.0) * u01(rng_word(seed, uid, j)) for j in range(3))
+    return Workload("ref_clustering", x, y, z, np.full(n, 10.0), None,
+                    dict(seed=seed, model=N.MODEL_COHERE, model_params=[30.0, 1.0], fixed_box_length=30.0),
+                    steps=40, bytes_per_agent_iteration=128, tags=(uid % np.uint64(2)).astype(np.uint32),
+                    rng_counters=np.full(n, 3, np.uint64))
 
 
 CONFIGS = {

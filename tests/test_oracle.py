@@ -224,3 +224,57 @@ def test_errors_match_reference(oracle_mod):
         s.simulate(1)
     with pytest.raises(RuntimeError, match="diameter"):
         O.PortSim(O.OracleParams(), np.zeros(1), np.zeros(1), np.zeros(1), np.zeros(1))
+
+
+# ---- the reference's own behaviour models ---------------------
+def _port_from(O, wl, **kw):
+    prm = wl.params
+    p = O.OracleParams(seed=prm["seed"], model=prm["model"], mp=prm["model_params"],
+                       fixed_box=prm.get("fixed_box_length", 0.0), **kw)
+    s = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+    s.set_tags(wl.tags)
+    s.set_rng_counters(wl.rng_counters)
+    return s, p
+
+
+def _same_state(a, b, what):
+    da, db = a.dump(), b.dump()
+    for k in ("uid", "x", "y", "z", "d", "partners", "flags"):
+        assert np.array_equal(da[k], db[k]), f"{what}: {k}"
+    assert np.array_equal(a.tags(), b.tags()), f"{what}: tags"
+    assert np.array_equal(a.rng_counters(), b.rng_counters()), f"{what}: rng counters"
+    assert a.counts() == b.counts(), f"{what}: counts"
+
+
+def test_growdivide_matches_reference_builder(oracle_mod, have_ref):
+    """models::GrowDivide on the reference's own build_proliferation lattice:
+    daughters from the agent's RandomStream (cos/sin), tags and counters."""
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    O = oracle_mod
+    wl = CF.ref_proliferation(64)
+    port, p = _port_from(O, wl)
+    ref = O.RefSim.builtin(p, "proliferation", 64)
+    for chunk in range(4):
+        ref.simulate(6)
+        port.simulate(6)
+        _same_state(ref, port, f"grow-divide after {6 * (chunk + 1)}")
+    assert ref.counts()["agents"] > 64
+
+
+def test_cohere_matches_reference_builder(oracle_mod, have_ref):
+    """models::Cohere on the reference's own build_clustering population
+    (tags uid % 2, box pinned to the attraction radius)."""
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    O = oracle_mod
+    wl = CF.ref_clustering(600, seed=7)
+    port, p = _port_from(O, wl)
+    ref = O.RefSim.builtin(p, "clustering", 600)
+    d0 = ref.dump()
+    assert np.array_equal(d0["x"], wl.x) and np.array_equal(ref.tags(), wl.tags)
+    assert np.array_equal(ref.rng_counters(), wl.rng_counters)
+    for chunk in range(3):
+        ref.simulate(4)
+        port.simulate(4)
+        _same_state(ref, port, f"cohere after {4 * (chunk + 1)}")
