@@ -70,6 +70,12 @@ extern "C" {
 #define ABS_MODEL_DRIVE 2         /* mp[0..2] centre, mp[3] max speed */
 #define ABS_MODEL_GROW 3          /* mp[0] growth rate, mp[1] diameter cap */
 #define ABS_MODEL_SIR 4           /* mp[0] L (periodic cube), mp[1] radius, mp[2] step, mp[3] recovery, mp[4] p */
+#define ABS_MODEL_GROW_DIVIDE 5   /* the reference's models::GrowDivide (models.hpp:15-37): mp[0] growth rate,
+                                     mp[1] division threshold, mp[2] initial diameter; daughters from the
+                                     agent's own RandomStream (tag copied, counter advanced by 2) */
+#define ABS_MODEL_COHERE 6        /* the reference's models::Cohere (models.hpp:42-64): mp[0] attraction
+                                     radius (<= box length, e.g. fixed_box_length), mp[1] speed; same-tag
+                                     neighbours only */
 
 typedef struct abs_gpu_ctx abs_gpu_ctx;
 
@@ -128,6 +134,13 @@ int abs_gpu_upload(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const doub
 int abs_gpu_upload_device(abs_gpu_ctx* ctx, uint64_t n, const uint64_t* uid, const double* x,
                           const double* y, const double* z, const double* d,
                           const uint8_t* behaviour_mask, uint64_t uid_count);
+
+/* Agent::tag and the per-agent RandomStream counter (agent.hpp:35-36, 145;
+ * used by ABS_MODEL_GROW_DIVIDE / ABS_MODEL_COHERE), host arrays in the
+ * current storage order (after abs_gpu_upload: upload order); either
+ * pointer may be NULL. Uploads reset both to 0. */
+int abs_gpu_set_agent_ext(abs_gpu_ctx* ctx, const uint32_t* tags, const uint64_t* rng_counters);
+int abs_gpu_download_ext(abs_gpu_ctx* ctx, uint32_t* tags, uint64_t* rng_counters);
 
 /* Multi-domain additions (commit.cpp:186-222). With defer != 0
  * a proliferation context's abs_gpu_simulate(ctx, 1) stops with the

@@ -330,6 +330,8 @@ struct Soa {
   double* vol;
   unsigned char* beh;
   double* force;  // [3][cap]
+  unsigned int* tag;          // Agent::tag (agent.hpp:35-36)
+  unsigned long long* rngc;   // Agent::rng_counter (agent.hpp:145)
 };
 
 __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos, Soa src, Soa dst,
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
                                                       const unsigned int* __restrict__ rank,
                                                       const DevGrid* g, unsigned long long cap,
                                                       int carry_vol, int carry_force, int write_pf,
-                                                      int only_sort_mode = -1) {
+                                                      int only_sort_mode = -1, int carry_ext = 0) {
   if (g->err) return;
   if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
@@ -362,6 +364,10 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
       dst.force[j] = src.force[i];
       dst.force[cap + j] = src.force[cap + i];
       dst.force[2 * cap + j] = src.force[2 * cap + i];
+    }
+    if (carry_ext) {
+      dst.tag[j] = src.tag[i];
+      dst.rngc[j] = src.rngc[i];
     }
   }
 }
@@ -436,6 +442,30 @@ struct Daughter {
   bool divides;
   unsigned long long parent;
   double x, y, z, d, vol;
+  unsigned int tag;
+};
+
+// RandomStream::unit_vector (random.hpp:47-52) on an agent's own stream:
+// two draws at its counter (advanced by 2); cos/sin are the non-bit-portable
+// terms (values within tolerance, as in coincident_force).
+__device__ __forceinline__ void stream_unit_vector(unsigned long long seed, unsigned long long uid,
+                                                   unsigned long long& ctr, double out[3]) {
+  const double u1 = abs_u01(abs_rng_word(seed, uid, ctr++));
+  const double zz = -1.0 + (1.0 - -1.0) * u1;
+  const double u2 = abs_u01(abs_rng_word(seed, uid, ctr++));
+  const double phi = 0.0 + (2.0 * ABS_PI - 0.0) * u2;
+  const double q = 1.0 - zz * zz;
+  const double r = sqrt(0.0 < q ? q : 0.0);
+  out[0] = r * cos(phi);
+  out[1] = r * sin(phi);
+  out[2] = zz;
+}
+
+// Behaviour-side radius query (AgentContext::for_each_neighbor,
+// simulation.hpp:213-218) for kernels that do not provide one.
+struct NoQuery {
+  template <class F>
+  __device__ void operator()(double, double, F&&) const {}
 };
 
 // Behaviours, static skip, run_forces and apply_pending for agent i (storage
@@ -452,14 +482,15 @@ struct Daughter {
 // the candidates with fp64 d2 <= r^2); the contact record test is then the
 // conservative fp32 superset df2 < (h + slack)^2 (pass B decides exactly).
 template <int MODEL, bool STATIC, bool RECORD, int LPA = 1, bool F32 = false, class OvlT, class Walk, class Fetch,
-          class UidOf>
+          class UidOf, class Query = NoQuery>
 __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, unsigned long long i, const Pd& me,
                                                double dmax, unsigned char* __restrict__ nv,
                                                unsigned char* __restrict__ nn, const StepArgs& a,
                                                unsigned long long cap, OvlT* ovl, int ovl_stride,
                                                unsigned long long& n_eval, unsigned long long& n_skip,
-                                               Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f) {
-  Daughter dg{false, 0, 0, 0, 0, 0, 0};
+                                               Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f,
+                                               const Query& query = Query{}) {
+  Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u};
   const bool leader = LPA == 1 || (threadIdx.x & (LPA - 1)) == 0;
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
@@ -492,6 +523,8 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
   double tx = 0.0, ty = 0.0, tz = 0.0, tg = 0.0;
   double new_vol = 0.0;
   bool vol_changed = false;
+  unsigned long long new_rngc = 0;
+  bool rngc_changed = false;
   if (MODEL != ABS_MODEL_NONE && S.beh[i]) {
     if (MODEL == ABS_MODEL_PROLIFERATION) {
       double v = S.vol[i] + a.mp[0];
@@ -520,6 +553,48 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       if (me.d < a.mp[1]) {
         const double rem = a.mp[1] - me.d;
         tg += rem < a.mp[0] ? rem : a.mp[0];
+      }
+    } else if (MODEL == ABS_MODEL_GROW_DIVIDE) {  // models::GrowDivide (models.hpp:15-37)
+      if (me.d >= a.mp[1]) {
+        unsigned long long ctr = S.rngc[i];
+        double dir[3];
+        stream_unit_vector(a.seed, my_uid, ctr, dir);  // ctx.random().unit_vector()
+        new_rngc = ctr;
+        rngc_changed = true;
+        const double half = 0.5 * me.d;
+        dg.x = me.x + dir[0] * half;
+        dg.y = me.y + dir[1] * half;
+        dg.z = me.z + dir[2] * half;
+        dg.d = a.mp[2];
+        dg.vol = 0.0;
+        dg.tag = S.tag[i];  // daughter.set_tag(a.tag())
+        dg.divides = leader;
+        tg += a.mp[2] - me.d;
+      } else {
+        tg += a.mp[0];
+      }
+    } else if (MODEL == ABS_MODEL_COHERE) {  // models::Cohere (models.hpp:42-64)
+      const unsigned int my_tag = S.tag[i];
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+      unsigned long long cnt = 0;
+      query(a.mp[0], a.mp[0] * a.mp[0], [&](unsigned int j, const Pd& q) {
+        if (S.tag[j] == my_tag) {
+          sx += q.x;
+          sy += q.y;
+          sz += q.z;
+          ++cnt;
+        }
+      });
+      if (cnt) {
+        const double inv = 1.0 / static_cast<double>(cnt);
+        const double cx = sx * inv - me.x, cy = sy * inv - me.y, cz = sz * inv - me.z;
+        const double dist = sqrt((cx * cx + cy * cy) + cz * cz);
+        if (dist > 0.0) {
+          const double f = a.mp[1] / dist;
+          tx += cx * f;
+          ty += cy * f;
+          tz += cz * f;
+        }
       }
     }
   }
@@ -659,6 +734,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       nn[i] = 0;
     }
     if (vol_changed) S.vol[i] = new_vol;
+    if (rngc_changed) S.rngc[i] = new_rngc;
     if (wrote_partners) {
       if (RECORD) {
         S.force[i] = fx;
@@ -679,7 +755,8 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
 __device__ __forceinline__ void stage_daughter(const Daughter& dg, DevGrid* gw,
                                                unsigned long long* __restrict__ st_parent,
                                                Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-                                               unsigned int* __restrict__ div_mark) {
+                                               unsigned int* __restrict__ div_mark,
+                                               unsigned int* __restrict__ st_tag) {
   const int lane = threadIdx.x & 31;
   const unsigned int ballot = __ballot_sync(0xffffffffu, dg.divides);
   if (!ballot) return;
@@ -692,6 +769,7 @@ __device__ __forceinline__ void stage_daughter(const Daughter& dg, DevGrid* gw,
     reinterpret_cast<double2*>(st_pd + slot)[0] = make_double2(dg.x, dg.y);
     reinterpret_cast<double2*>(st_pd + slot)[1] = make_double2(dg.z, dg.d);
     st_vol[slot] = dg.vol;
+    st_tag[slot] = dg.tag;
     div_mark[dg.parent] = 1u;
   }
 }
@@ -718,7 +796,7 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-            unsigned int* __restrict__ div_mark) {
+            unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
   if (gp->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
@@ -727,6 +805,14 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
   auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + 2 * kMaxRows * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
+  if (MODEL == ABS_MODEL_COHERE && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
+    // uniform_grid.cpp:176-181: the query radius must not exceed the box
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      gw->err = kErrQueryRadius;
+      gw->failed_iteration = a.iteration;
+    }
+    return;
+  }
   const unsigned long long n = gp->n;
   const double dmax = gp->dmax;
   const bool box_mode = Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1;  // bins are the reference boxes
@@ -745,13 +831,19 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
     if (i < n) {
       const Pd me = load_pd(S.pd + i);
       const unsigned int self = static_cast<unsigned int>(i);
+      // behaviour-side exact radius query (models::Cohere)
+      auto query = [&](double rq, double rq2, auto&& v) {
+        for_each_neighbor(Q, S.pd, start, self, me.x, me.y, me.z, rq, rq2,
+                          [&](unsigned int j, const Pd& q, double, double, double, double) { v(j, q); });
+      };
       if (F32 && !box_mode) {
         dg = agent_step<MODEL, STATIC, RECORD, 1, true>(
             S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
             [&](double r, double r2, auto&& visit) {
               for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2, visit);
             },
-            [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, Q.slack);
+            [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, Q.slack,
+            query);
       } else
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
@@ -768,9 +860,11 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
                                      });
             }
           },
-          [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
+          [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, 0.0f,
+          query);
     }
-    if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+    if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
+      stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
   }
   flush_counters(n_eval, n_skip, gw);
 }
@@ -786,7 +880,7 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
     k_force_g(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
               unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
               unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-              unsigned int* __restrict__ div_mark) {
+              unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
   if (gp->err) return;
   __shared__ QGrid Q;
   __shared__ unsigned int rows[kForceThreads / LPA][kGroupRowWords];
@@ -819,7 +913,8 @@ __global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
           },
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
     }
-    if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+    if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
+      stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
   }
   flush_counters(n_eval, n_skip, gw);
 }
@@ -866,7 +961,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     k_force_tile(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
                  unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
                  unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-                 unsigned int* __restrict__ div_mark) {
+                 unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
   if (gp->err) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw);
@@ -1126,7 +1221,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
               [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
         }
       }
-      if (MODEL == ABS_MODEL_PROLIFERATION) stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark);
+      if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
+        stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
     }
     __syncthreads();  // smem reused by the next tile
   }
@@ -1288,6 +1384,7 @@ __global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
 __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
                          const unsigned long long* __restrict__ st_parent,
                          const Pd* __restrict__ st_pd, const double* __restrict__ st_vol,
+                         const unsigned int* __restrict__ st_tag,
                          const unsigned int* __restrict__ div_rank, const unsigned int* __restrict__ div_rank_g,
                          unsigned long long cap, int record_forces) {
   if (g->err) return;
@@ -1305,6 +1402,8 @@ __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
     S.partners[j] = 0;
     S.beh[j] = 1;
     S.vol[j] = st_vol[k];
+    S.tag[j] = st_tag[k];
+    S.rngc[j] = 0;  // a new Agent's stream starts at counter 0
     if (record_forces) S.force[j] = S.force[cap + j] = S.force[2 * cap + j] = 0.0;
   }
 }
@@ -1358,6 +1457,8 @@ __global__ void __launch_bounds__(kThreads) k_ingest(const double* __restrict__ 
     reinterpret_cast<double2*>(out + i)[1] = make_double2(z[i], di);
     if (set_uid) S.uid[i] = i;
     else if (uid_limit && S.uid[i] >= uid_limit) bad |= 2u;
+    S.tag[i] = 0;   // set with abs_gpu_set_agent_ext
+    S.rngc[i] = 0;
     if (set_vol) S.vol[i] = abs_volume_of_diameter(di);
     if (sir) {  // absim_models.h: 1 % initially infected, from the seed (or given states)
       const unsigned long long u = set_uid ? i : S.uid[i];
@@ -1421,7 +1522,8 @@ struct __align__(16) Rec {
   unsigned long long uid;
   unsigned int partners;
   unsigned char flags, beh, pad0, pad1;
-  unsigned long long pad2;
+  unsigned long long rngc;
+  unsigned int tag, pad3;
 };
 static_assert(sizeof(Rec) == 96, "record layout");
 
@@ -1465,7 +1567,9 @@ __global__ void k_export(const Pd* __restrict__ pos, Soa S, unsigned long long c
     r.flags = fl;
     r.beh = S.beh[i];
     r.pad0 = r.pad1 = 0;
-    r.pad2 = 0;
+    r.rngc = S.rngc[i];
+    r.tag = S.tag[i];
+    r.pad3 = 0;
     (dest ? out_hi : out_lo)[slot] = r;
   }
 }
@@ -1483,6 +1587,8 @@ __global__ void k_import(const Rec* __restrict__ in, unsigned long long count, u
     S.partners[j] = r.partners;
     S.flags[j] = as_ghost ? (r.flags | ABS_FLAG_GHOST) : static_cast<unsigned char>(r.flags & ~ABS_FLAG_GHOST);
     S.beh[j] = r.beh;
+    S.tag[j] = r.tag;
+    S.rngc[j] = r.rngc;
   }
 }
 
@@ -1510,6 +1616,8 @@ __global__ void k_compact(const Pd* __restrict__ pos, Soa src, Pd* __restrict__ 
     dst.force[j] = src.force[i];
     dst.force[cap + j] = src.force[cap + i];
     dst.force[2 * cap + j] = src.force[2 * cap + i];
+    dst.tag[j] = src.tag[i];
+    dst.rngc[j] = src.rngc[i];
   }
 }
 
@@ -1721,7 +1829,7 @@ __global__ void k_radix_scatter(const unsigned long long* __restrict__ key, cons
 
 __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const unsigned int* __restrict__ perm,
                          const DevGrid* g, unsigned long long cap, int carry_vol, int carry_force,
-                         int only_sort_mode = -1) {
+                         int only_sort_mode = -1, int carry_ext = 1) {
   if (g->err) return;
   if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
@@ -1740,6 +1848,10 @@ __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const uns
       dst.force[j] = src.force[i];
       dst.force[cap + j] = src.force[cap + i];
       dst.force[2 * cap + j] = src.force[2 * cap + i];
+    }
+    if (carry_ext) {
+      dst.tag[j] = src.tag[i];
+      dst.rngc[j] = src.rngc[i];
     }
   }
 }
@@ -1806,6 +1918,8 @@ __global__ void k_remove_move(const Pd* pos_in, Pd* pos, Soa S, const unsigned l
       S.force[dst] = S.force[src];
       S.force[cap + dst] = S.force[cap + src];
       S.force[2 * cap + dst] = S.force[2 * cap + src];
+      S.tag[dst] = S.tag[src];
+      S.rngc[dst] = S.rngc[src];
     }
   }
 }
@@ -1854,6 +1968,7 @@ struct abs_gpu_ctx {
   unsigned long long* st_parent = nullptr;
   Pd* st_pd = nullptr;
   double* st_vol = nullptr;
+  unsigned int* st_tag = nullptr;    // staged daughters' tags
   unsigned int* div_mark = nullptr;  // uid_cap + 1: this context's dividing parents (then their local ranks)
   unsigned int* div_mark_g = nullptr;  // uid_cap + 1: all ranks' dividing parents (deferred commit only)
   bool defer_commit = false;         // multi-domain additions: stop before the commit
@@ -1893,6 +2008,15 @@ int set_err(abs_gpu_ctx* c, int code, const std::string& m) {
       return set_err(c, ABS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Models whose behaviour creates agents (daughter staging, uid-indexed marks).
+bool adds_agents(const abs_gpu_config& cfg) {
+  return cfg.model == ABS_MODEL_PROLIFERATION || cfg.model == ABS_MODEL_GROW_DIVIDE;
+}
+// Models that read Agent::tag / rng_counter.
+bool uses_ext(const abs_gpu_config& cfg) {
+  return cfg.model == ABS_MODEL_GROW_DIVIDE || cfg.model == ABS_MODEL_COHERE;
+}
+
 int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   const unsigned long long b = (work + kThreads - 1) / kThreads;
   const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 8;
@@ -1918,7 +2042,7 @@ cudaError_t dalloc(T** p, unsigned long long count) {
 
 void free_soa(Soa& s) {
   cudaFree(s.pd); cudaFree(s.uid); cudaFree(s.flags); cudaFree(s.partners);
-  cudaFree(s.vol); cudaFree(s.beh); cudaFree(s.force);
+  cudaFree(s.vol); cudaFree(s.beh); cudaFree(s.force); cudaFree(s.tag); cudaFree(s.rngc);
   s = Soa{};
 }
 
@@ -1931,6 +2055,8 @@ cudaError_t alloc_soa(Soa& s, unsigned long long cap) {
   if ((e = dalloc(&s.vol, cap))) return e;
   if ((e = dalloc(&s.beh, cap))) return e;
   if ((e = dalloc(&s.force, 3 * cap))) return e;
+  if ((e = dalloc(&s.tag, cap))) return e;
+  if ((e = dalloc(&s.rngc, cap))) return e;
   return cudaSuccess;
 }
 
@@ -1953,6 +2079,8 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
     CK(cudaMemcpyAsync(dst.partners, src.partners, keep * 4, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(dst.vol, src.vol, keep * 8, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(dst.beh, src.beh, keep, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.tag, src.tag, keep * 4, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.rngc, src.rngc, keep * 8, cudaMemcpyDeviceToDevice, c->stream));
     for (int q = 0; q < 3; ++q)
       CK(cudaMemcpyAsync(dst.force + q * ncap, src.force + q * c->cap, keep * 8, cudaMemcpyDeviceToDevice,
                          c->stream));
@@ -1969,7 +2097,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   c->pos_in_new = true;
   c->grid_valid = false;
   cudaFree(c->key); cudaFree(c->rank); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol);
+  cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag);
   cudaFree(c->pf);
   c->pf = nullptr;
   CK(dalloc(&c->pf, ncap));
@@ -1982,6 +2110,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   CK(dalloc(&c->st_parent, ncap));
   CK(dalloc(&c->st_pd, ncap));
   CK(dalloc(&c->st_vol, ncap));
+  CK(dalloc(&c->st_tag, ncap));
   c->cap = ncap;
   return ABS_OK;
 }
@@ -2101,7 +2230,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   const int nxt = c->cur ^ 1;
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                            c->cfg.record_forces, uses_f32_walk(c));
+                                            c->cfg.record_forces, uses_f32_walk(c), -1, uses_ext(c->cfg));
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2117,7 +2246,7 @@ void launch_tile(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     configured = true;
   }
   k_force_tile<MODEL, STATIC, RECORD><<<c->sms, kTileThreads, smem, c->stream>>>(
-      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
 }
 
 // ABSIM_FORCE_KERNEL=tile selects the TMA-staged tile kernel; the default
@@ -2142,7 +2271,7 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, F32>);
   }
   k_force<MODEL, STATIC, RECORD, F32><<<blocks, kForceThreads, kForceSmem, c->stream>>>(
-      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
@@ -2175,7 +2304,7 @@ void launch_group_l(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     blocks = c->sms * std::max(per_sm, 1);
   }
   k_force_g<MODEL, STATIC, RECORD, LPA><<<blocks, kForceThreads, 0, c->stream>>>(
-      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark);
+      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
@@ -2194,6 +2323,11 @@ void launch_group(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
 template <int MODEL, bool STATIC>
 void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
   const bool box_mode = bins_x(c) == 1u && bins_yz(c) == 1u;
+  if (MODEL == ABS_MODEL_COHERE) {  // its behaviour query lives in the gather kernel
+    if (c->cfg.record_forces) launch_gather<MODEL, STATIC, true>(c, S, a);
+    else launch_gather<MODEL, STATIC, false>(c, S, a);
+    return;
+  }
   if (!use_tile_kernel() && !box_mode && lanes_per_agent() > 1) {
     if (c->cfg.record_forces) launch_group<MODEL, STATIC, true>(c, S, a);
     else launch_group<MODEL, STATIC, false>(c, S, a);
@@ -2219,12 +2353,14 @@ void launch_force(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
     case ABS_MODEL_PROLIFERATION: launch_force_m<ABS_MODEL_PROLIFERATION>(c, nb, S, a); break;
     case ABS_MODEL_DRIVE: launch_force_m<ABS_MODEL_DRIVE>(c, nb, S, a); break;
     case ABS_MODEL_GROW: launch_force_m<ABS_MODEL_GROW>(c, nb, S, a); break;
+    case ABS_MODEL_GROW_DIVIDE: launch_force_m<ABS_MODEL_GROW_DIVIDE>(c, nb, S, a); break;
+    case ABS_MODEL_COHERE: launch_force_m<ABS_MODEL_COHERE>(c, nb, S, a); break;
     default: launch_force_m<ABS_MODEL_NONE>(c, nb, S, a); break;
   }
 }
 
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
-  launch_env_update(c, iteration, c->cfg.model == ABS_MODEL_PROLIFERATION);
+  launch_env_update(c, iteration, adds_agents(c->cfg));
   if (c->cfg.model == ABS_MODEL_SIR) {
     const int nb = grid_blocks(c, c->cap);
     const StepArgs a = step_args(c, iteration);
@@ -2273,7 +2409,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
   ++c->launches;
   if (c->timing) cudaEventRecord(e1, c->stream);
   c->pos_in_new = true;
-  if (c->cfg.model == ABS_MODEL_PROLIFERATION) {
+  if (adds_agents(c->cfg)) {
     if (c->cfg.detect_static_agents) {
       k_mark_new<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->st_pd);
       ++c->launches;
@@ -2296,8 +2432,8 @@ void launch_commit(abs_gpu_ctx* c) {
   launch_scan<unsigned int>(c, c->div_mark, uc, c->uid_cap, tiles, &c->g->err);
   if (c->defer_commit) launch_scan<unsigned int>(c, c->div_mark_g, uc, c->uid_cap, tiles, &c->g->err);
   const unsigned int* grank = c->defer_commit ? c->div_mark_g : c->div_mark;
-  k_append<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
-                                           grank, c->cap, c->cfg.record_forces);
+  k_append<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->st_parent, c->st_pd, c->st_vol, c->st_tag,
+                                           c->div_mark, grank, c->cap, c->cfg.record_forces);
   // counts first (reads the scan total grank[uid_count]), then clear the
   // marks over the grown range [0, uid_count]
   k_commit_fin<<<1, 32, 0, c->stream>>>(c->g, grank);
@@ -2323,6 +2459,10 @@ int map_dev_err(abs_gpu_ctx* c, const DevGrid& h) {
       return set_err(c, ABS_ERR_FIXED_BOX, "operation 'environment update' failed at iteration " +
                                                std::to_string(h.failed_iteration) +
                                                ": fixed box length is smaller than the largest agent diameter");
+    case kErrQueryRadius:
+      return set_err(c, ABS_ERR_INVALID_ARGUMENT, "operation 'behaviours' failed at iteration " +
+                                                      std::to_string(h.failed_iteration) +
+                                                      ": query radius exceeds the grid box length");
     case kErrBoxBudget:
       return set_err(c, ABS_ERR_BOX_BUDGET, "operation 'environment update' failed at iteration " +
                                                 std::to_string(h.failed_iteration) + ": grid would exceed the box budget");
@@ -2365,7 +2505,11 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "repulsion_coefficient must be >= 0");
   if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
   if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
-  if (cfg->model < 0 || cfg->model > 4) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->model < 0 || cfg->model > 6) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->model == ABS_MODEL_GROW_DIVIDE && !(cfg->model_params[2] > 0.0))
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "GrowDivide needs an initial diameter > 0");
+  if (cfg->model == ABS_MODEL_COHERE && !(cfg->model_params[0] > 0.0))
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "Cohere needs an attraction radius > 0");
   if (cfg->model == ABS_MODEL_SIR && !(cfg->model_params[0] > 0.0 && cfg->model_params[1] > 0.0 &&
                                        cfg->model_params[0] >= 3.0 * cfg->model_params[1]))
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "SIR needs L >= 3 r > 0");
@@ -2416,7 +2560,8 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
-  cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->div_mark); cudaFree(c->ingest_part);
+  cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
+  cudaFree(c->ingest_part);
   free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -2443,7 +2588,7 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   uid_count = std::max<unsigned long long>(uid_count, n);
   int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * n + 1024), 0);
   if (rc) return rc;
-  if (c->cfg.model == ABS_MODEL_PROLIFERATION) {  // uid-indexed division marks
+  if (adds_agents(c->cfg)) {  // uid-indexed division marks
     rc = ensure_uid_space(c, 2 * uid_count + 1024);
     if (rc) return rc;
   }
@@ -2582,7 +2727,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
                                                                c->key, c->rank, c->g, c->cap,
                                                                c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                                               c->cfg.record_forces, 0, 1);
+                                                               c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
   k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, nullptr);
   c->launches += 3;
   // exact path (device-selected otherwise): radix passes + gather
@@ -2605,7 +2750,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   }
   k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                                              c->cfg.record_forces, 0);
+                                                              c->cfg.record_forces, 0, uses_ext(c->cfg));
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2615,7 +2760,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
 int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
-  const bool deferred = c->defer_commit && c->cfg.model == ABS_MODEL_PROLIFERATION;
+  const bool deferred = c->defer_commit && adds_agents(c->cfg);
   if (deferred && c->pending_commit)
     return set_err(c, ABS_ERR_STATE, "abs_gpu_commit is pending for the previous iteration");
   if (deferred && iterations > 1)
@@ -2683,10 +2828,36 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   return ABS_OK;
 }
 
+int abs_gpu_set_agent_ext(abs_gpu_ctx* c, const uint32_t* tags, const uint64_t* rng_counters) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  Soa& S = c->S[c->cur];
+  if (h.n && tags) CK(cudaMemcpyAsync(S.tag, tags, h.n * 4, cudaMemcpyHostToDevice, c->stream));
+  if (h.n && rng_counters) CK(cudaMemcpyAsync(S.rngc, rng_counters, h.n * 8, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
+int abs_gpu_download_ext(abs_gpu_ctx* c, uint32_t* tags, uint64_t* rng_counters) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  Soa& S = c->S[c->cur];
+  if (h.n && tags) CK(cudaMemcpyAsync(tags, S.tag, h.n * 4, cudaMemcpyDeviceToHost, c->stream));
+  if (h.n && rng_counters) CK(cudaMemcpyAsync(rng_counters, S.rngc, h.n * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
 int abs_gpu_set_defer_commit(abs_gpu_ctx* c, int defer) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (c->pending_commit) return set_err(c, ABS_ERR_STATE, "abs_gpu_commit is pending");
-  if (defer && c->cfg.model == ABS_MODEL_PROLIFERATION && c->cfg.detect_static_agents)
+  if (defer && adds_agents(c->cfg) && c->cfg.detect_static_agents)
     return set_err(c, ABS_ERR_INVALID_ARGUMENT,
                    "static detection with multi-domain additions is not supported (new-neighbour marks stay local)");
   cudaSetDevice(c->device);

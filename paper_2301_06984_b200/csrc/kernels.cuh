@@ -46,6 +46,7 @@ enum DevErr : int {
   kErrBoxBudget = 3,
   kErrBinsRetry = 4,  // internal: grow the bin table and re-run the iteration
   kErrCapRetry = 5,   // internal: grow agent capacity and re-run the iteration
+  kErrQueryRadius = 6,  // a behaviour's query radius exceeds the box (uniform_grid.cpp:176-181)
 };
 
 // Grid + bookkeeping living in device memory (one per context).

@@ -310,8 +310,8 @@ class DeviceSlabDecomposition:
         self.iteration = 0
         # additions (config 2): daughters are committed only after the ranks
         # have summed their division marks, so uids match the single domain
-        from ._native import MODEL_PROLIFERATION, MODEL_SIR
-        self.additions = sim.params.model == MODEL_PROLIFERATION
+        from ._native import MODEL_GROW_DIVIDE, MODEL_PROLIFERATION, MODEL_SIR
+        self.additions = sim.params.model in (MODEL_PROLIFERATION, MODEL_GROW_DIVIDE)
         self._marks = None
         if self.additions:
             sim.set_defer_commit(True)

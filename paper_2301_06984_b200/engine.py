@@ -238,6 +238,21 @@ class Simulation:
         N.check(N.load().abs_gpu_sir_state(self._ctx, _p(st, C.c_uint8), _p(ti, C.c_uint32)), self._ctx)
         return st, ti
 
+    # -- Agent::tag / rng_counter (reference models) -------------------------
+    def set_agent_ext(self, tags=None, rng_counters=None) -> None:
+        """Per-agent tags / RandomStream counters in the current storage order."""
+        t = None if tags is None else np.ascontiguousarray(tags, np.uint32)
+        r = None if rng_counters is None else np.ascontiguousarray(rng_counters, np.uint64)
+        N.check(N.load().abs_gpu_set_agent_ext(self._ctx, _p(t, C.c_uint32), _p(r, C.c_uint64)), self._ctx)
+
+    def agent_ext(self):
+        """(tags, rng_counters) in the device storage order."""
+        n = self.report().final_agent_count
+        t = np.zeros(n, np.uint32)
+        r = np.zeros(n, np.uint64)
+        N.check(N.load().abs_gpu_download_ext(self._ctx, _p(t, C.c_uint32), _p(r, C.c_uint64)), self._ctx)
+        return t, r
+
     # -- multi-domain additions (deferred commit) ---------------------------
     def set_defer_commit(self, defer: bool) -> None:
         N.check(N.load().abs_gpu_set_defer_commit(self._ctx, 1 if defer else 0), self._ctx)

@@ -53,6 +53,8 @@ def _make(case):
         return CF.c2_proliferation(side=6, seed=0), 50
     if case == "c5":
         return CF.c5_sir(4000, seed=1), 26
+    if case == "gd":  # the reference's own GrowDivide lattice
+        return CF.ref_proliferation(343), 12
     if case == "c3":
         return CF.c3_spheroid(3000, seed=2), 5
     return CF.c4_large_uniform(3000, seed=3), 4
@@ -96,8 +98,17 @@ def test_slab_decomposition_matches_single_domain(oracle_mod, world, case):
 
     wl, steps = _make(case)
     ref = O.PortSim(_oparams(O, wl), wl.x, wl.y, wl.z, wl.d, wl.mask)
+    if wl.tags is not None:
+        ref.set_tags(wl.tags)
+        ref.set_rng_counters(wl.rng_counters)
     ref.simulate(steps)
     o = by_uid(ref.dump())
+    if wl.tags is not None:  # tags and RandomStream counters travel with the agents
+        ge = by_uid({"uid": np.concatenate([p["uid"] for p in parts]),
+                     "tag": np.concatenate([p["tag"] for p in parts]),
+                     "rngc": np.concatenate([p["rngc"] for p in parts])})
+        oe = by_uid({"uid": ref.dump()["uid"], "tag": ref.tags(), "rngc": ref.rng_counters()})
+        assert np.array_equal(ge["tag"], oe["tag"]) and np.array_equal(ge["rngc"], oe["rngc"])
     assert np.array_equal(got["uid"], o["uid"])
     for k in ("x", "y", "z", "d"):
         assert_close(got[k], o[k], 1e-9, 1.0, k)
@@ -189,11 +200,14 @@ def _dev_worker(rank, world, port, case, outdir):
     sim = E.Simulation(E.SimulationParams(**wl.params), device=0)
     sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=None if sir else st["beh"], uid=st["uid"],
                    uid_count=wl.n)  # SIR: initial states from (seed, uid), as in one domain
+    if wl.tags is not None:
+        sim.set_agent_ext(wl.tags[st["uid"]], wl.rng_counters[st["uid"]])
     dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="host", cap=1 << 14)
     dec.simulate(steps)
     a = sim.agents()
     evals, skips = dec.totals()
     extra = {}
+    extra["tag"], extra["rngc"] = sim.agent_ext()
     if dec.periodic:
         extra["state"], extra["t"] = sim.sir_state()
         extra["sir"] = np.array(dec.sir_counts())
@@ -204,7 +218,7 @@ def _dev_worker(rank, world, port, case, outdir):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,case", [(2, "c1"), (3, "c4"), (2, "c3"), (2, "c2"), (3, "c2"), (2, "c5"),
-                                        (3, "c5")])
+                                        (3, "c5"), (2, "gd")])
 def test_device_exchange_matches_single_domain(oracle_mod, world, case):
     """Device-resident exchange (export/import kernels, packed records): the
     union of the ranks' populations equals the single-domain run."""

@@ -1,0 +1,91 @@
+"""The reference's own behaviour models on the device:
+models::GrowDivide and models::Cohere (models.hpp:15-64) on the reference's
+own population builders (models.cpp:21-61), against the C oracle (pinned
+bit-exact to the unmodified reference in test_oracle.py) and the reference
+itself when its build is present. Integer state (agent/uid counts, tags,
+RandomStream counters, force evaluations) is exact; positions within
+1e-9 (cos/sin of the division axis and the Cohere centroid sum order are
+the non-bit-portable terms)."""
+import numpy as np
+import pytest
+
+from _util import assert_close, by_uid
+from paper_2301_06984_b200 import configs as CF
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(O, wl):
+    prm = wl.params
+    p = O.OracleParams(seed=prm["seed"], model=prm["model"], mp=prm["model_params"],
+                       fixed_box=prm.get("fixed_box_length", 0.0))
+    s = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+    s.set_tags(wl.tags)
+    s.set_rng_counters(wl.rng_counters)
+    return s, p
+
+
+def _gpu(E, wl):
+    sim = E.Simulation(E.SimulationParams(**wl.params))
+    sim.add_agents(wl.x, wl.y, wl.z, wl.d)
+    sim.set_agent_ext(wl.tags, wl.rng_counters)
+    return sim
+
+
+def _compare(sim, orc, what):
+    g = sim.agents()
+    g["tag"], g["rngc"] = sim.agent_ext()
+    o = orc.dump()
+    o["tag"], o["rngc"] = orc.tags(), orc.rng_counters()
+    g, o = by_uid(g), by_uid(o)
+    assert np.array_equal(g["uid"], o["uid"]), f"{what}: uid sets"
+    for k in ("tag", "rngc"):
+        assert np.array_equal(g[k], o[k]), f"{what}: {k}"
+    for k in ("x", "y", "z", "d"):
+        assert_close(g[k], o[k], 1e-9, 1.0, f"{what} {k}")
+    r, c = sim.report(), orc.counts()
+    assert (r.final_agent_count, r.uid_count, r.agents_added) == (c["agents"], c["uid_count"], c["agents_added"])
+    assert r.force_evaluations == c["force_evaluations"], what
+
+
+def test_growdivide_reference_lattice(engine, oracle_mod, have_ref):
+    O = oracle_mod
+    wl = CF.ref_proliferation(216)
+    sim = _gpu(engine, wl)
+    orc, p = _oracle(O, wl)
+    ref = O.RefSim.builtin(p, "proliferation", 216) if have_ref else None
+    for chunk in range(4):
+        sim.simulate(5)
+        orc.simulate(5)
+        _compare(sim, orc, f"grow-divide after {5 * (chunk + 1)}")
+        if ref is not None:
+            ref.simulate(5)
+            assert ref.counts()["agents"] == sim.report().final_agent_count
+    assert sim.report().final_agent_count > 216
+
+
+def test_cohere_reference_clustering(engine, oracle_mod, have_ref):
+    O = oracle_mod
+    wl = CF.ref_clustering(3000, seed=7)
+    sim = _gpu(engine, wl)
+    orc, p = _oracle(O, wl)
+    for chunk in range(3):
+        sim.simulate(4)
+        orc.simulate(4)
+        _compare(sim, orc, f"cohere after {4 * (chunk + 1)}")
+    if have_ref:  # the reference's own builder gives the same start state
+        ref = O.RefSim.builtin(p, "clustering", 3000)
+        ref.simulate(12)
+        g, r = by_uid(sim.agents()), by_uid(ref.dump())
+        assert np.array_equal(g["uid"], r["uid"])
+        assert_close(g["x"], r["x"], 1e-9, 1.0, "cohere vs reference x")
+
+
+def test_cohere_radius_exceeds_box(engine):
+    """uniform_grid.cpp:176-181: a query radius above the box length fails."""
+    wl = CF.ref_clustering(500, seed=1)
+    prm = {**wl.params, "fixed_box_length": 0.0}  # box = largest diameter (10) < 30
+    sim = engine.Simulation(engine.SimulationParams(**prm))
+    sim.add_agents(wl.x, wl.y, wl.z, wl.d)
+    with pytest.raises(ValueError, match="query radius"):
+        sim.simulate(1)
