@@ -51,6 +51,10 @@ def _workload(name, n=None, seed=0):
         return CF.c3_spheroid(n or (1 << 23), seed)
     if name == "c5":
         return CF.c5_sir(n or 10_000_000, seed)
+    if name == "rclust":  # the reference's own clustering benchmark (models::Cohere)
+        return CF.ref_clustering(n or (1 << 22), seed=42 + seed)
+    if name == "rprolif":  # the reference's own proliferation benchmark (models::GrowDivide)
+        return CF.ref_proliferation(n or 32768)
     return CF.c4_large_uniform(n or (1 << 26), seed)
 
 
@@ -109,8 +113,10 @@ def _dist():
     return dist, world, rank, local
 
 
-CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22, "c5": 1 << 21}
-CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12, "c5": 10}
+CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22, "c5": 1 << 21, "rclust": 1 << 18,
+              "rprolif": 4096}
+CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12, "c5": 10, "rclust": 10, "rprolif": 18}
+REF_BUILDERS = {"ref_clustering": "clustering", "ref_proliferation": "proliferation"}
 
 
 def _ref_sim(wl_name, sample_n, threads):
@@ -122,14 +128,21 @@ def _ref_sim(wl_name, sample_n, threads):
     p = O.OracleParams(seed=prm.get("seed", 0), dt=prm.get("simulation_time_step", 0.1),
                        detect_static=prm.get("detect_static_agents", False),
                        model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
-                       sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0)
+                       sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0,
+                       fixed_box=prm.get("fixed_box_length", 0.0))
     try:
         if prm.get("model", 0) == 4:  # SIR: the reference has no periodic boundaries
             raise FileNotFoundError("no reference path for config 5")
+        if wl.name in REF_BUILDERS:  # the reference's own population builder and models
+            return O.RefSim.builtin(p, REF_BUILDERS[wl.name], wl.n), "reference", threads, wl
         return O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "reference", threads, wl
     except (FileNotFoundError, OSError):
         p.threads = 1
-        return O.PortSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "port", 1, wl
+        s = O.PortSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask)
+        if wl.tags is not None:
+            s.set_tags(wl.tags)
+            s.set_rng_counters(wl.rng_counters)
+        return s, "port", 1, wl
 
 
 def cpu_baseline(wl_name, steps=None, threads=None):
@@ -305,8 +318,12 @@ def run_gpu(args):
     prm["bins_per_box_x"] = args.bins_x
     if wl.params.get("model") == E.MODEL_PROLIFERATION:
         prm["capacity"] = 5 * wl.n * 2 ** 9
+    if wl.params.get("model") == E.MODEL_GROW_DIVIDE:  # doubles every 3 iterations
+        prm["capacity"] = 3 * wl.n * 2 ** ((args.warmup + args.steps + 8) // 3)
     sim = E.Simulation(E.SimulationParams(**prm), device=local)
     sim.add_agents(wl.x, wl.y, wl.z, wl.d, behaviour_mask=wl.mask)
+    if wl.tags is not None:
+        sim.set_agent_ext(wl.tags, wl.rng_counters)
     stream = torch.cuda.ExternalStream(sim.stream)
 
     sim.simulate(args.warmup)
@@ -353,7 +370,12 @@ def run_gpu(args):
         # a host-driven loop continues the step numbering after each upload
         # (set_iteration), so periodic work (sorting_frequency) keeps its cadence
         it = args.warmup + args.steps
+        ext = None
+        if wl.tags is not None:  # per-agent tags / stream counters travel with the state
+            ext = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (wl.tags, wl.rng_counters)]
         sim.add_agents(*pin, behaviour_mask=mask)
+        if ext:
+            sim.set_agent_ext(*ext)
         sim.set_iteration(it)
         sim.simulate(1)
         sim.positions(*outp)
@@ -361,12 +383,14 @@ def run_gpu(args):
         t0 = time.perf_counter()
         for k in range(e2e_steps):
             sim.add_agents(*pin, behaviour_mask=mask)
+            if ext:
+                sim.set_agent_ext(*ext)
             sim.set_iteration(it + 1 + k)
             sim.simulate(1)
             n_e = sim.positions(*outp)
         dt = time.perf_counter() - t0
         e2e = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
-               "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0)),
+               "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0) + (12 if ext else 0)),
                "d2h_bytes_per_step": n_e * 24, "steps": e2e_steps,
                "path": "abs_gpu_upload (pinned host) -> abs_gpu_simulate(1) -> abs_gpu_download (pinned host)"}
 
@@ -423,7 +447,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "rclust", "rprolif"])
     ap.add_argument("--agents", "--n", dest="n", type=int, default=None)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--bins", type=int, default=0, help="sub-bins per box edge along y, z (0 = auto)")

@@ -2140,7 +2140,7 @@ int ensure_uid_space(abs_gpu_ctx* c, unsigned long long want) {
 
 int ensure_bins(abs_gpu_ctx* c, unsigned long long want) {
   if (want <= c->bins_cap) return ABS_OK;
-  unsigned long long nb = std::max<unsigned long long>(want + want / 2, 4096);
+  unsigned long long nb = std::max<unsigned long long>(2 * want, 4096);  // growing domains: few retries
   cudaFree(c->start);
   cudaFree(c->tiles);
   CK(dalloc(&c->start, nb + 1));
@@ -2588,8 +2588,9 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   uid_count = std::max<unsigned long long>(uid_count, n);
   int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * n + 1024), 0);
   if (rc) return rc;
-  if (adds_agents(c->cfg)) {  // uid-indexed division marks
-    rc = ensure_uid_space(c, 2 * uid_count + 1024);
+  if (adds_agents(c->cfg)) {  // uid-indexed division marks: uids cannot outgrow
+    // uid_count + capacity before a capacity retry, so no uid-space retry either
+    rc = ensure_uid_space(c, std::max<unsigned long long>(2 * uid_count, uid_count + c->cap) + 1024);
     if (rc) return rc;
   }
   c->pending_commit = false;
@@ -2813,7 +2814,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
       if (2 * h.n > c->cap) rc = ensure_capacity(c, 2 * c->cap, h.n);
       if (rc) return rc;
-      rc = ensure_uid_space(c, 2 * (h.uid_count + h.n) + 1024);
+      rc = ensure_uid_space(c, std::max<unsigned long long>(2 * (h.uid_count + h.n), h.uid_count + c->cap) + 1024);
       if (rc) return rc;
       rc = clear_dev_err(c);
       if (rc) return rc;
