@@ -226,6 +226,13 @@ int abs_gpu_set_stream(abs_gpu_ctx* ctx, void* stream);
 /* Timing of the dominant kernel (mechanical force) recorded with CUDA events
  * on the context stream: cumulative ms and launch count since the last reset. */
 int abs_gpu_force_kernel_time(abs_gpu_ctx* ctx, double* total_ms, uint64_t* launches);
+/* SimulationReport wall-time categories (report.hpp:12-23) as device time
+ * of the iterations run while timing is enabled (abs_gpu_reset_timers(ctx, 1)):
+ * out4 = {environment update, sorting, agent operations (staticness marking,
+ * behaviours, forces, integration), setup/teardown (commit of additions)} ms;
+ * per_iteration_ms[0 .. min(cap, *n)) with *n = iterations recorded (a
+ * rolled-back attempt counts as one). */
+int abs_gpu_phase_times(abs_gpu_ctx* ctx, double* out4, double* per_iteration_ms, uint64_t cap, uint64_t* n);
 int abs_gpu_reset_timers(abs_gpu_ctx* ctx, int enable);
 
 #ifdef __cplusplus

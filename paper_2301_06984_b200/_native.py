@@ -36,7 +36,7 @@ EXPORTS = [
     "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
     "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
-    "abs_gpu_set_agent_ext", "abs_gpu_download_ext",
+    "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times",
 ]
 
 
@@ -112,6 +112,7 @@ def load():
         "abs_gpu_commit": (C.c_int, [_CTX, C.c_void_p, C.c_uint64]),
         "abs_gpu_set_agent_ext": (C.c_int, [_CTX, _U32, _U64]),
         "abs_gpu_download_ext": (C.c_int, [_CTX, _U32, _U64]),
+        "abs_gpu_phase_times": (C.c_int, [_CTX, _D, _D, C.c_uint64, _U64]),
         "abs_gpu_sir_state": (C.c_int, [_CTX, _U8, _U32]),
         "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),

@@ -1987,6 +1987,12 @@ struct abs_gpu_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
+  // SimulationReport categories (report.hpp:12-23): five marks per iteration
+  // [start | after sort | after environment update | after agent ops | after commit]
+  std::vector<cudaEvent_t> pev;
+  size_t pev_used = 0;
+  double phase_ms[4] = {0.0, 0.0, 0.0, 0.0};  // env update, sorting, agent ops, setup/teardown
+  std::vector<double> iter_ms;
   double force_ms = 0.0;
   unsigned long long force_launches = 0;
 };
@@ -2359,8 +2365,21 @@ void launch_force(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
   }
 }
 
+void phase_mark(abs_gpu_ctx* c) {
+  if (!c->timing) return;
+  if (c->pev_used + 1 > c->pev.size()) {
+    for (int q = 0; q < 320; ++q) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->pev.push_back(e);
+    }
+  }
+  cudaEventRecord(c->pev[c->pev_used++], c->stream);
+}
+
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
   launch_env_update(c, iteration, adds_agents(c->cfg));
+  phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
     const int nb = grid_blocks(c, c->cap);
     const StepArgs a = step_args(c, iteration);
@@ -2383,6 +2402,8 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
     k_sir_commit<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->nv, c->key);
     c->launches += 2;
     c->pos_in_new = true;
+    phase_mark(c);  // after agent ops
+    phase_mark(c);  // no commit
     return;
   }
   const int nb = grid_blocks(c, c->cap);
@@ -2409,6 +2430,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
   ++c->launches;
   if (c->timing) cudaEventRecord(e1, c->stream);
   c->pos_in_new = true;
+  phase_mark(c);  // after agent ops (staticness marking, behaviours, forces, integration)
   if (adds_agents(c->cfg)) {
     if (c->cfg.detect_static_agents) {
       k_mark_new<<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->start, c->st_pd);
@@ -2416,6 +2438,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
     }
     if (!c->defer_commit) launch_commit(c);
   }
+  phase_mark(c);  // after commit
 }
 
 // CommitBuffer::commit for additions (commit.cpp:186-222): daughter uids
@@ -2564,6 +2587,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->ingest_part);
   free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ABS_OK;
@@ -2778,10 +2802,12 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     for (unsigned long long t = 0; t < todo; ++t) {
       snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
       const unsigned long long it = c->iteration + t;
+      phase_mark(c);  // iteration start
       if (c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0) {
         const int rc = launch_sort(c, it, false);
         if (rc) return rc;
       }
+      phase_mark(c);  // after sort
       launch_iteration(c, it);
     }
     cudaError_t le = cudaGetLastError();
@@ -3342,12 +3368,36 @@ int abs_gpu_force_kernel_time(abs_gpu_ctx* c, double* total_ms, uint64_t* launch
   return ABS_OK;
 }
 
+int abs_gpu_phase_times(abs_gpu_ctx* c, double* out4, double* per_iteration_ms, uint64_t cap, uint64_t* n) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t q = 0; q + 4 < c->pev_used; q += 5) {
+    float t[4];
+    for (int k = 0; k < 4; ++k) CK(cudaEventElapsedTime(&t[k], c->pev[q + k], c->pev[q + k + 1]));
+    c->phase_ms[1] += t[0];  // sorting
+    c->phase_ms[0] += t[1];  // environment update
+    c->phase_ms[2] += t[2];  // agent ops
+    c->phase_ms[3] += t[3];  // setup/teardown
+    c->iter_ms.push_back(static_cast<double>(t[0]) + t[1] + t[2] + t[3]);
+  }
+  c->pev_used = 0;
+  if (out4)
+    for (int k = 0; k < 4; ++k) out4[k] = c->phase_ms[k];
+  if (per_iteration_ms)
+    for (size_t k = 0; k < c->iter_ms.size() && k < cap; ++k) per_iteration_ms[k] = c->iter_ms[k];
+  if (n) *n = c->iter_ms.size();
+  return ABS_OK;
+}
+
 int abs_gpu_reset_timers(abs_gpu_ctx* c, int enable) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   CK(cudaStreamSynchronize(c->stream));
   c->ev_used = 0;
   c->force_ms = 0.0;
   c->force_launches = 0;
+  c->pev_used = 0;
+  for (double& v : c->phase_ms) v = 0.0;
+  c->iter_ms.clear();
   c->timing = enable != 0;
   return ABS_OK;
 }

@@ -20,11 +20,24 @@ path.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native as N
+
+
+def peak_rss_bytes() -> int:
+    """High-water-mark RSS of this process (report.cpp: VmHWM), 0 if unavailable."""
+    try:
+        with open("/proc/self/status") as f:
+            for line in f:
+                if line.startswith("VmHWM:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
 
 
 @dataclass
@@ -82,6 +95,10 @@ class SimulationParams:
 
 @dataclass
 class SimulationReport:
+    """SimulationReport (report.hpp:18-41). Counters are cumulative. The wall
+    buckets are device time of the iterations run while timing is enabled
+    (Simulation.reset_timers(True)); total_wall_ms is the host wall time of
+    simulate() calls, as in the reference."""
     iterations: int = 0
     final_agent_count: int = 0
     uid_count: int = 0
@@ -90,6 +107,18 @@ class SimulationReport:
     agents_added: int = 0
     agents_removed: int = 0
     kernel_launches: int = 0
+    total_wall_ms: float = 0.0
+    agent_ops_ms: float = 0.0
+    env_update_ms: float = 0.0
+    sorting_ms: float = 0.0
+    setup_teardown_ms: float = 0.0
+    per_iteration_ms: list = field(default_factory=list)
+    per_operation_ms: dict = field(default_factory=dict)
+    agents_sorted: int = 0           # cross-domain migrations during sorting: one domain per device
+    same_domain_steals: int = 0      # no work stealing on the device (grid scheduler)
+    cross_domain_steals: int = 0
+    allocator_batch_migrations: int = 0
+    peak_rss_bytes: int = 0
 
 
 def _p(a, ct):
@@ -158,6 +187,7 @@ class Simulation:
         self.params = params or SimulationParams()
         self.params.validate()
         lib = N.load()
+        self._wall_ms = 0.0  # host wall time of simulate() (report.total_wall_ms)
         self._cfg = self.params.to_c()
         ctx = C.c_void_p()
         N.check(lib.abs_gpu_create(C.byref(self._cfg), device, C.byref(ctx)), None)
@@ -206,7 +236,9 @@ class Simulation:
 
     # -- schedule --------------------------------------------------------
     def simulate(self, iterations: int) -> None:
+        t0 = time.perf_counter()
         N.check(N.load().abs_gpu_simulate(self._ctx, iterations), self._ctx)
+        self._wall_ms += (time.perf_counter() - t0) * 1e3
 
     def set_grid_override(self, grid=None, dims=None) -> None:
         """Multi-domain: force the grid of all ranks (origin[3], box, dmax; dims)."""
@@ -301,7 +333,23 @@ class Simulation:
         return SimulationReport(iterations=s.iterations, final_agent_count=s.agents,
                                 uid_count=s.uid_count, force_evaluations=s.force_evaluations,
                                 force_skips=s.force_skips, agents_added=s.agents_added,
-                                agents_removed=s.agents_removed, kernel_launches=s.kernel_launches)
+                                agents_removed=s.agents_removed, kernel_launches=s.kernel_launches,
+                                total_wall_ms=self._wall_ms, peak_rss_bytes=peak_rss_bytes())
+
+    def phase_report(self) -> SimulationReport:
+        """report() plus the device-time categories of the timed iterations."""
+        r = self.report()
+        out4 = np.zeros(4)
+        n = C.c_uint64(0)
+        N.check(N.load().abs_gpu_phase_times(self._ctx, _p(out4, C.c_double), None, 0, C.byref(n)), self._ctx)
+        per = np.zeros(max(int(n.value), 1))
+        N.check(N.load().abs_gpu_phase_times(self._ctx, _p(out4, C.c_double), _p(per, C.c_double), len(per),
+                                             C.byref(n)), self._ctx)
+        r.env_update_ms, r.sorting_ms, r.agent_ops_ms, r.setup_teardown_ms = (float(v) for v in out4)
+        r.per_iteration_ms = per[:int(n.value)].tolist()
+        r.per_operation_ms = {"environment_update": r.env_update_ms, "sorting": r.sorting_ms,
+                              "agent_operations": r.agent_ops_ms, "commit": r.setup_teardown_ms}
+        return r
 
     def agents(self) -> dict:
         """Download the population (device storage order)."""

@@ -57,3 +57,19 @@ def test_models_header_compiles_as_c(tmp_path):
                    "int main(void){ return abs_rng_word(1,2,3) == 0; }\n")
     rc = os.system(f"gcc -std=c11 -I{ROOT}/include {src} -o {tmp_path}/t -lm")
     assert rc == 0
+
+
+def test_report_schema_matches_reference_bench():
+    """CSV header / JSON keys of tools/bench_main.cpp:24-28, 398-434."""
+    from paper_2301_06984_b200 import report as R
+    from paper_2301_06984_b200.engine import SimulationReport
+    r = SimulationReport(iterations=3, final_agent_count=10, force_evaluations=7, total_wall_ms=1.5)
+    o = R.RunOptions(model="clustering", agents=10, iterations=3)
+    row = R.csv_row(o, r, 2)
+    assert len(row.split(",")) == len(R.CSV_HEADER.split(","))
+    assert row.startswith("clustering,10,3,1,1,uniform_grid,device_pool,0,0,1.500,")
+    j = R.report_json(o, r)
+    assert set(j) == {"model", "agents", "iterations", "threads", "domain_count", "env", "allocator",
+                      "sorting_frequency", "static_detection", "seed", "report"}
+    assert {"wall_ms_total", "per_iteration_ms", "per_operation_ms", "force_evaluations",
+            "allocator_batch_migrations"} <= set(j["report"])

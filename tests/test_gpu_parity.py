@@ -478,3 +478,23 @@ def test_reupload_with_growing_population(engine, oracle_mod):
         orc = oracle_mod.PortSim(_oparams(oracle_mod, wl.params), wl.x[:n], wl.y[:n], wl.z[:n], wl.d[:n])
         orc.simulate(2)
         compare_state(sim.agents(), orc.dump(), what=f"reupload n={n}")
+
+
+def test_phase_report_categories(engine):
+    """SimulationReport wall-time categories (report.hpp:12-23) from device
+    events; they add up to the per-iteration times and export in the
+    reference bench's schema."""
+    from paper_2301_06984_b200 import report as R
+    wl = CF.c1_relaxation(4000, seed=3)
+    sim = _gpu(engine, {**wl.params, "sorting_frequency": 2}, wl, 1)
+    sim.simulate(1)
+    sim.reset_timers(True)
+    sim.simulate(5)
+    r = sim.phase_report()
+    assert len(r.per_iteration_ms) == 5
+    parts = r.env_update_ms + r.sorting_ms + r.agent_ops_ms + r.setup_teardown_ms
+    assert abs(parts - sum(r.per_iteration_ms)) < 1e-3 * max(parts, 1.0)
+    assert r.env_update_ms > 0 and r.agent_ops_ms > 0 and r.sorting_ms > 0
+    assert r.total_wall_ms > 0 and r.peak_rss_bytes > 0
+    j = R.report_json(R.RunOptions(model="c1", agents=wl.n, iterations=6, sorting_frequency=2), r)
+    assert j["report"]["per_iteration_ms"] == r.per_iteration_ms
