@@ -363,6 +363,7 @@ def run_gpu(args):
     # the step's input state (x, y, z, d) from page-locked host memory, runs the
     # iteration and reads the resulting positions back into page-locked memory
     e2e = None
+    sir_model = wl.params.get("model") == E.MODEL_SIR
     if not args.no_e2e and rank == 0:
         pin = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (wl.x, wl.y, wl.z, wl.d)]
         mask = None if wl.mask is None else torch.from_numpy(wl.mask).pin_memory().numpy()
@@ -389,10 +390,30 @@ def run_gpu(args):
             sim.simulate(1)
             n_e = sim.positions(*outp)
         dt = time.perf_counter() - t0
-        e2e = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
+        seq = {"value": wl.n * e2e_steps / dt, "unit": UNIT,
                "h2d_bytes_per_step": wl.n * (32 + (1 if wl.mask is not None else 0) + (12 if ext else 0)),
                "d2h_bytes_per_step": n_e * 24, "steps": e2e_steps,
                "path": "abs_gpu_upload (pinned host) -> abs_gpu_simulate(1) -> abs_gpu_download (pinned host)"}
+        e2e = seq
+        if mask is None and ext is None and not sir_model:
+            # the same per-step work through abs_gpu_run_frames: every frame
+            # uploads its inputs from page-locked memory, runs one iteration
+            # and downloads the positions, with the next frame's H2D and the
+            # previous frame's D2H overlapping this frame's compute
+            frames = max(5, min(args.steps, 20))
+            outs = [outp, [torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]]
+            it2 = it + 1 + e2e_steps
+            sim.run_frames([pin] * 2, outs, iterations=1, first_iteration=it2)  # staging allocated untimed
+            it2 += 2
+            t0 = time.perf_counter()
+            counts = sim.run_frames([pin] * frames, [outs[f % 2] for f in range(frames)], iterations=1,
+                                    first_iteration=it2)
+            dt = time.perf_counter() - t0
+            e2e = {"value": wl.n * frames / dt, "unit": UNIT, "h2d_bytes_per_step": wl.n * 32,
+                   "d2h_bytes_per_step": counts[-1] * 24, "steps": frames,
+                   "path": "abs_gpu_run_frames: per step H2D x,y,z,d (pinned) -> ingest -> 1 iteration -> "
+                           "D2H x,y,z (pinned); copies of neighbouring steps overlap on two copy streams",
+                   "sequential": seq}
 
     hbm, peak_src = _peaks()
     n_agents = r1.final_agent_count

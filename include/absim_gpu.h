@@ -14,6 +14,8 @@
  *                             → run_forces → run_integration → run_commit
  *   abs_gpu_stats           Simulation::report() counters                   report.hpp:32-40
  *   abs_gpu_download        ResourceManager::for_each_agent + Agent getters resource_manager.hpp:346, agent.hpp:31-110
+ *   abs_gpu_run_frames      add_agent -> simulate -> read agents, repeated over
+ *                           independent host frames with copy/compute overlap simulation.hpp:107-121
  *   abs_gpu_env_update      Environment::update (UniformGrid::update)       environment.hpp:38, uniform_grid.cpp:155-266
  *   abs_gpu_grid_info       UniformGrid::{origin, box_length, dims, largest_agent_diameter}  uniform_grid.hpp:40-49
  *   abs_gpu_cell_ids        UniformGrid::box_index_of (per agent)           uniform_grid.cpp:124-133
@@ -200,6 +202,25 @@ int abs_gpu_synchronize(abs_gpu_ctx* ctx);
 int abs_gpu_download(abs_gpu_ctx* ctx, uint64_t* n_out, uint64_t* uid, double* x, double* y,
                      double* z, double* d, double* fx, double* fy, double* fz,
                      uint32_t* partners, uint8_t* flags, double* volume);
+
+/* Host-boundary pipeline (end-to-end use with host buffers). Each frame is
+ * exactly abs_gpu_upload (uids 0..n-1, no mask) + abs_gpu_set_iteration(
+ * first_iteration + f * iterations) + abs_gpu_simulate(iterations) +
+ * abs_gpu_download(x, y, z); frames run in order on this context. The H2D of
+ * frame f+1 and the D2H of frame f-1 run on two copy streams while frame f
+ * computes (double-buffered device staging), so PCIe and HBM work overlap.
+ * Host arrays should be page-locked (plain DMA). Output order is the device
+ * storage order (cell order), as abs_gpu_download. */
+typedef struct {
+  uint64_t n;                    /* agents in this frame */
+  const double *x, *y, *z, *d;   /* host inputs */
+  double *out_x, *out_y, *out_z; /* host outputs: positions after the iterations */
+  uint64_t out_cap;              /* entries each output array holds (>= n unless a model adds agents) */
+  uint64_t* n_out;               /* agents after the iterations (may be NULL) */
+  uint64_t* out_uid;             /* uids in output order (may be NULL; out_cap entries) */
+} abs_frame;
+int abs_gpu_run_frames(abs_gpu_ctx* ctx, const abs_frame* frames, uint64_t count, uint64_t iterations,
+                       uint64_t first_iteration);
 
 /* Teacher-forced environment: build the grid for the current state. */
 int abs_gpu_env_update(abs_gpu_ctx* ctx);

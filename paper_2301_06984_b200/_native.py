@@ -36,7 +36,7 @@ EXPORTS = [
     "abs_gpu_cell_ids", "abs_gpu_neighbors", "abs_gpu_sort", "abs_gpu_remove",
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
     "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
-    "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times",
+    "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times", "abs_gpu_run_frames",
 ]
 
 
@@ -69,6 +69,20 @@ class Stats(C.Structure):
         ("agents_added", C.c_uint64),
         ("agents_removed", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+    ]
+
+
+class Frame(C.Structure):
+    """abs_frame: one host frame of abs_gpu_run_frames."""
+    _fields_ = [
+        ("n", C.c_uint64),
+        ("x", C.POINTER(C.c_double)), ("y", C.POINTER(C.c_double)),
+        ("z", C.POINTER(C.c_double)), ("d", C.POINTER(C.c_double)),
+        ("out_x", C.POINTER(C.c_double)), ("out_y", C.POINTER(C.c_double)),
+        ("out_z", C.POINTER(C.c_double)),
+        ("out_cap", C.c_uint64),
+        ("n_out", C.POINTER(C.c_uint64)),
+        ("out_uid", C.POINTER(C.c_uint64)),
     ]
 
 
@@ -114,6 +128,7 @@ def load():
         "abs_gpu_download_ext": (C.c_int, [_CTX, _U32, _U64]),
         "abs_gpu_phase_times": (C.c_int, [_CTX, _D, _D, C.c_uint64, _U64]),
         "abs_gpu_sir_state": (C.c_int, [_CTX, _U8, _U32]),
+        "abs_gpu_run_frames": (C.c_int, [_CTX, C.POINTER(Frame), C.c_uint64, C.c_uint64, C.c_uint64]),
         "abs_gpu_simulate": (C.c_int, [_CTX, C.c_uint64]),
         "abs_gpu_stats": (C.c_int, [_CTX, C.POINTER(Stats)]),
         "abs_gpu_synchronize": (C.c_int, [_CTX]),

@@ -1515,6 +1515,61 @@ __global__ void k_mask_flags(const unsigned char* __restrict__ in, unsigned char
     out[i] = in[i] & (63u | ABS_FLAG_GHOST);
 }
 
+// Host-visible mirror of the device grid record: one warp copies it into
+// mapped page-locked memory, so reading it back never queues behind bulk
+// DMA on the copy engines (abs_gpu_run_frames overlaps those with compute).
+__global__ void k_grid_out(const DevGrid* __restrict__ g, DevGrid* out) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(g);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(out);
+  for (unsigned int w = threadIdx.x; w < sizeof(DevGrid) / 8; w += blockDim.x) d[w] = s[w];
+}
+
+// Population reset at upload: everything before ov_on as a fresh record with
+// the reduction identities (the host-built DevGrid of the synchronous path).
+__global__ void k_grid_reset(DevGrid* g, unsigned long long n, unsigned long long uid_count) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(g);
+  for (unsigned int q = threadIdx.x; q < offsetof(DevGrid, ov_on) / 8; q += blockDim.x) w[q] = 0ull;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    g->red[0] = g->red[1] = g->red[2] = kInfOrdLo;
+    g->red[3] = g->red[4] = g->red[5] = kInfOrdHi;
+    g->red[6] = kZeroOrd;
+    g->dims[0] = g->dims[1] = g->dims[2] = 1;
+    g->B[0] = g->B[1] = g->B[2] = 1;
+    g->n = n;
+    g->uid_count = uid_count;
+  }
+}
+static_assert(offsetof(DevGrid, ov_on) % 8 == 0 && sizeof(DevGrid) % 8 == 0, "grid record layout");
+
+// Zero `bytes` bytes on the compute engine (16-byte stores + tail).
+__global__ void k_zero_bytes(unsigned char* __restrict__ p, unsigned long long bytes) {
+  const unsigned long long n16 = bytes / 16;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n16; i += stride)
+    reinterpret_cast<uint4*>(p)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (unsigned long long i = n16 * 16 + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < bytes;
+       i += stride)
+    p[i] = 0;
+}
+
+// Frame input x | y | z | d (stride n) -> interleaved staging consumed by k_ingest
+// is not needed: k_ingest reads the four arrays directly. Frame output: the
+// positions of the current state as x | y | z (stride n).
+__global__ void k_split_xyz(const Pd* __restrict__ pos, const unsigned long long* __restrict__ uid,
+                            const DevGrid* g, double* __restrict__ out, unsigned long long stride) {
+  const unsigned long long n = g->n;
+  unsigned long long* ou = reinterpret_cast<unsigned long long*>(out + 3 * stride);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd p = load_pd(pos + i);
+    out[i] = p.x;
+    out[stride + i] = p.y;
+    out[2 * stride + i] = p.z;
+    if (uid) ou[i] = uid[i];
+  }
+}
+
 // ------------------------------------------------------------ multi-domain exchange
 // Packed agent record exchanged between ranks: 96 bytes.
 struct __align__(16) Rec {
@@ -1973,7 +2028,15 @@ struct abs_gpu_ctx {
   unsigned int* div_mark_g = nullptr;  // uid_cap + 1: all ranks' dividing parents (deferred commit only)
   bool defer_commit = false;         // multi-domain additions: stop before the commit
   bool pending_commit = false;
-  double* ingest_part = nullptr;     // per-block (sum d, max d) of the last upload
+  double* ingest_part = nullptr;     // mapped page-locked: per-block (sum d, max d) of the last upload
+  DevGrid* hgrid = nullptr;          // mapped page-locked mirror of *g (read_grid)
+  // host-boundary pipeline (abs_gpu_run_frames): two copy streams, double-buffered
+  // device staging of frame inputs (x|y|z|d) and outputs (x|y|z)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  double* fin[2] = {nullptr, nullptr};
+  double* fout[2] = {nullptr, nullptr};
+  unsigned long long fcap = 0, fout_cap = 0;  // agents per input / output slot
+  cudaEvent_t in_ready[2] = {}, in_free[2] = {}, out_ready[2] = {}, out_free[2] = {};
   unsigned long long ghosts = 0;     // upper bound on ghost agents present (0 -> drop_ghosts is a no-op)
   // Morton sort scratch (capacity-sized, allocated on first use)
   unsigned long long sort_cap = 0;
@@ -2466,9 +2529,23 @@ void launch_commit(abs_gpu_ctx* c) {
 }
 
 int read_grid(abs_gpu_ctx* c, DevGrid* h) {
-  CK(cudaMemcpyAsync(h, c->g, sizeof(DevGrid), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  if (c->hgrid) {  // mapped mirror: no copy-engine work (see k_grid_out)
+    k_grid_out<<<1, 64, 0, c->stream>>>(c->g, c->hgrid);
+    ++c->launches;
+    CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(h, c->hgrid, sizeof(DevGrid));
+  } else {
+    CK(cudaMemcpyAsync(h, c->g, sizeof(DevGrid), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
   c->n = h->n;
+  return ABS_OK;
+}
+
+int dzero(abs_gpu_ctx* c, void* p, unsigned long long bytes) {
+  if (!bytes) return ABS_OK;
+  k_zero_bytes<<<grid_blocks(c, (bytes + 15) / 16), kThreads, 0, c->stream>>>(static_cast<unsigned char*>(p), bytes);
+  ++c->launches;
   return ABS_OK;
 }
 
@@ -2555,6 +2632,14 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   h.dims[0] = h.dims[1] = h.dims[2] = 1;
   h.B[0] = h.B[1] = h.B[2] = 1;
   CK(cudaMemcpy(c->g, &h, sizeof h, cudaMemcpyHostToDevice));
+  // small host-visible results (grid record, ingest partials) through mapped
+  // page-locked memory; on failure read_grid falls back to cudaMemcpy
+  if (cudaHostAlloc(reinterpret_cast<void**>(&c->hgrid), sizeof(DevGrid), cudaHostAllocMapped) != cudaSuccess) {
+    c->hgrid = nullptr;
+    cudaGetLastError();
+  }
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&c->ingest_part), (2ull * c->sms * 8 + 2) * sizeof(double),
+                   cudaHostAllocMapped));
   int rc = ensure_capacity(c, std::max<unsigned long long>(cfg->capacity, 1024), 0);
   if (!rc) rc = ensure_uid_space(c, 1024);
   if (rc) { abs_gpu_destroy(c); return set_err(nullptr, rc, "allocation failed"); }
@@ -2584,7 +2669,16 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
-  cudaFree(c->ingest_part);
+  if (c->ingest_part) cudaFreeHost(c->ingest_part);
+  if (c->hgrid) cudaFreeHost(c->hgrid);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->fin[b]);
+    cudaFree(c->fout[b]);
+    for (cudaEvent_t e : {c->in_ready[b], c->in_free[b], c->out_ready[b], c->out_free[b]})
+      if (e) cudaEventDestroy(e);
+  }
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
@@ -2593,10 +2687,15 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   return ABS_OK;
 }
 
-static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long long uid_count,
-                         cudaMemcpyKind kind, const uint64_t* uid, const double* x, const double* y,
-                         const double* z, const double* d, const uint8_t* mask, const double* volume,
-                         const uint8_t* flags, const uint32_t* partners) {
+// Upload, stage 1: everything stream-ordered (no host synchronisation).
+// Host coordinate arrays are DMA'd into the staging area; device arrays
+// (kind == cudaMemcpyDeviceToDevice) are read in place by k_ingest. Only
+// kernels touch the compute stream besides the caller's own host copies, so a
+// frame upload never waits behind another stream's bulk DMA.
+static int upload_enqueue(abs_gpu_ctx* c, unsigned long long n, unsigned long long uid_count,
+                          cudaMemcpyKind kind, const uint64_t* uid, const double* x, const double* y,
+                          const double* z, const double* d, const uint8_t* mask, const double* volume,
+                          const uint8_t* flags, const uint32_t* partners, int* blocks_out) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (n && (!x || !y || !z || !d)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null coordinate array");
   if (n >= 0xFFFFFFF0ull) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "too many agents");
@@ -2621,7 +2720,6 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   Soa& S = c->S[c->cur];
   const double *dx = x, *dy = y, *dz = z, *dd = d;
   const unsigned char* dmask = mask;
-  if (!c->ingest_part) CK(dalloc(&c->ingest_part, 2ull * c->sms * 8 + 2));
   if (host && n) {  // contiguous H2D into the staging area, interleaved on the device
     double* st = reinterpret_cast<double*>(c->st_pd);
     CK(cudaMemcpyAsync(st, x, n * 8, cudaMemcpyHostToDevice, c->stream));
@@ -2637,19 +2735,12 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   if (uid) CK(cudaMemcpyAsync(S.uid, uid, n * 8, kind, c->stream));
   if (volume) CK(cudaMemcpyAsync(S.vol, volume, n * 8, kind, c->stream));
   if (flags) CK(cudaMemcpyAsync(S.flags, flags, n, kind, c->stream));
-  else CK(cudaMemsetAsync(S.flags, 0, n, c->stream));
+  else dzero(c, S.flags, n);
   if (partners) CK(cudaMemcpyAsync(S.partners, partners, n * 4, kind, c->stream));
-  else CK(cudaMemsetAsync(S.partners, 0, n * 4, c->stream));
-  CK(cudaMemsetAsync(S.force, 0, 3 * c->cap * 8, c->stream));
-  DevGrid h{};
-  h.red[0] = h.red[1] = h.red[2] = kInfOrdLo;
-  h.red[3] = h.red[4] = h.red[5] = kInfOrdHi;
-  h.red[6] = kZeroOrd;
-  h.dims[0] = h.dims[1] = h.dims[2] = 1;
-  h.B[0] = h.B[1] = h.B[2] = 1;
-  h.n = n;
-  h.uid_count = uid_count;
-  CK(cudaMemcpyAsync(c->g, &h, offsetof(DevGrid, ov_on), cudaMemcpyHostToDevice, c->stream));
+  else dzero(c, S.partners, n * 4);
+  if (c->cfg.record_forces) dzero(c, S.force, 3 * c->cap * 8);
+  k_grid_reset<<<1, 64, 0, c->stream>>>(c->g, n, uid_count);
+  ++c->launches;
   const int ib = grid_blocks(c, n);
   if (n) {
     k_ingest<<<ib, kThreads, 0, c->stream>>>(dx, dy, dz, dd, dmask, n, uid == nullptr, volume == nullptr,
@@ -2658,24 +2749,30 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
     ++c->launches;
   }
   // the cell table is a counter array between iterations: always start clean
-  CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
-  unsigned int bad = 0;
-  std::vector<double> part(2ull * ib);
-  CK(cudaMemcpyAsync(&bad, &c->g->bad_input, 4, cudaMemcpyDeviceToHost, c->stream));
-  if (n) CK(cudaMemcpyAsync(part.data(), c->ingest_part, part.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (n) {  // Sub-bins: bins == boxes when the typical radius is close to the box (see bins_yz)
-    double sum = 0.0, mx = 0.0;
-    for (int b = 0; b < ib; ++b) {
-      sum += part[2 * b];
-      mx = part[2 * b + 1] > mx ? part[2 * b + 1] : mx;
-    }
-    c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
-  }
+  dzero(c, c->start, (c->bins_cap + 1) * 4);
   c->pos_in_new = true;
   c->grid_valid = false;
   c->iteration = 0;
   c->ghosts = flags ? n : 0;  // uploaded flags may carry ABS_FLAG_GHOST
+  c->n = n;
+  *blocks_out = ib;
+  return ABS_OK;
+}
+
+// Upload, stage 2: wait for the ingest, check the inputs, pick the sub-bins.
+static int upload_finish(abs_gpu_ctx* c, unsigned long long n, int ib) {
+  DevGrid h{};
+  int rc = read_grid(c, &h);  // synchronises the stream
+  if (rc) return rc;
+  const unsigned int bad = h.bad_input;
+  if (n && !bad) {  // Sub-bins: bins == boxes when the typical radius is close to the box (see bins_yz)
+    double sum = 0.0, mx = 0.0;
+    for (int b = 0; b < ib; ++b) {
+      sum += c->ingest_part[2 * b];
+      mx = c->ingest_part[2 * b + 1] > mx ? c->ingest_part[2 * b + 1] : mx;
+    }
+    c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
+  }
   if (bad) {
     c->n = 0;
     CK(cudaMemsetAsync(&c->g->n, 0, 8, c->stream));
@@ -2685,6 +2782,16 @@ static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long lon
   }
   c->n = n;
   return ABS_OK;
+}
+
+static int upload_common(abs_gpu_ctx* c, unsigned long long n, unsigned long long uid_count,
+                         cudaMemcpyKind kind, const uint64_t* uid, const double* x, const double* y,
+                         const double* z, const double* d, const uint8_t* mask, const double* volume,
+                         const uint8_t* flags, const uint32_t* partners) {
+  int ib = 0;
+  int rc = upload_enqueue(c, n, uid_count, kind, uid, x, y, z, d, mask, volume, flags, partners, &ib);
+  if (rc) return rc;
+  return upload_finish(c, n, ib);
 }
 
 int abs_gpu_upload(abs_gpu_ctx* c, uint64_t n, const uint64_t* uid, const double* x, const double* y,
@@ -3137,9 +3244,12 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
       if (dst[q]) CK(cudaMemcpyAsync(dst[q], st + q * n, n * 8, cudaMemcpyDeviceToHost, c->stream));
   }
   if (n && uid) CK(cudaMemcpyAsync(uid, S.uid, n * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (n && fx) CK(cudaMemcpyAsync(fx, S.force, n * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (n && fy) CK(cudaMemcpyAsync(fy, S.force + c->cap, n * 8, cudaMemcpyDeviceToHost, c->stream));
-  if (n && fz) CK(cudaMemcpyAsync(fz, S.force + 2 * c->cap, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  double* fdst[3] = {fx, fy, fz};
+  for (int q = 0; q < 3; ++q) {
+    if (!n || !fdst[q]) continue;
+    if (c->cfg.record_forces) CK(cudaMemcpyAsync(fdst[q], S.force + q * c->cap, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    else std::fill(fdst[q], fdst[q] + n, 0.0);  // last_force is not kept (record_forces == 0)
+  }
   if (n && partners) CK(cudaMemcpyAsync(partners, S.partners, n * 4, cudaMemcpyDeviceToHost, c->stream));
   if (n && flags) {
     unsigned char* fb = reinterpret_cast<unsigned char*>(c->key);
@@ -3154,6 +3264,133 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
       std::fill(volume, volume + n, 0.0);
   }
   CK(cudaStreamSynchronize(c->stream));
+  return ABS_OK;
+}
+
+// Host-boundary pipeline. Per frame: H2D of the frame's x|y|z|d into device
+// staging slot f%2 (stream h2d), ingest + `iterations` iterations (compute
+// stream), positions split into output slot f%2 and D2H into the frame's
+// host arrays (stream d2h). Events order the slots: the H2D of frame f+1 is
+// issued before frame f computes, so it overlaps frame f's iterations, and
+// the D2H of frame f overlaps frame f+1. Each frame is exactly
+// abs_gpu_upload (uids 0..n-1) + abs_gpu_set_iteration + abs_gpu_simulate +
+// abs_gpu_download (x, y, z).
+int abs_gpu_run_frames(abs_gpu_ctx* c, const abs_frame* frames, uint64_t count, uint64_t iterations,
+                       uint64_t first_iteration) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (count && !frames) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null frames");
+  if (c->defer_commit && adds_agents(c->cfg))
+    return set_err(c, ABS_ERR_STATE, "frames need the commit inside the iteration (defer_commit is set)");
+  if (c->cfg.model == ABS_MODEL_SIR) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "frames carry no SIR state");
+  unsigned long long mx = 0;
+  for (uint64_t f = 0; f < count; ++f) {
+    const abs_frame& F = frames[f];
+    if (F.n && (!F.x || !F.y || !F.z || !F.d || !F.out_x || !F.out_y || !F.out_z))
+      return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null frame array");
+    mx = std::max<unsigned long long>(mx, F.n);
+  }
+  if (!count) return ABS_OK;
+  cudaSetDevice(c->device);
+  if (!c->h2d) {
+    CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t* e : {&c->in_ready[b], &c->in_free[b], &c->out_ready[b], &c->out_free[b]})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if (mx > c->fcap) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(c->fin[b]);
+      c->fin[b] = nullptr;
+    }
+    c->fcap = 0;
+    for (int b = 0; b < 2; ++b) CK(dalloc(&c->fin[b], 4 * mx));
+    c->fcap = mx;
+  }
+  if (mx > c->fout_cap) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(c->fout[b]);
+      c->fout[b] = nullptr;
+    }
+    c->fout_cap = 0;
+    for (int b = 0; b < 2; ++b) CK(dalloc(&c->fout[b], 4 * mx));
+    c->fout_cap = mx;
+  }
+  // capacity for the largest frame up front (allocation synchronises)
+  int rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * mx + 1024), 0);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < 2; ++b) {  // slots start free
+    CK(cudaEventRecord(c->in_free[b], c->stream));
+    CK(cudaEventRecord(c->out_free[b], c->d2h));
+  }
+  auto stage_in = [&](uint64_t f) -> int {
+    const abs_frame& F = frames[f];
+    const int b = static_cast<int>(f & 1);
+    double* st = c->fin[b];
+    CK(cudaStreamWaitEvent(c->h2d, c->in_free[b], 0));
+    const double* src[4] = {F.x, F.y, F.z, F.d};
+    for (int q = 0; q < 4; ++q)
+      if (F.n) CK(cudaMemcpyAsync(st + q * F.n, src[q], F.n * 8, cudaMemcpyHostToDevice, c->h2d));
+    CK(cudaEventRecord(c->in_ready[b], c->h2d));
+    return ABS_OK;
+  };
+  rc = stage_in(0);
+  if (rc) return rc;
+  for (uint64_t f = 0; f < count; ++f) {
+    const abs_frame& F = frames[f];
+    const int b = static_cast<int>(f & 1);
+    if (f + 1 < count) {
+      rc = stage_in(f + 1);  // overlaps this frame's iterations
+      if (rc) return rc;
+    }
+    CK(cudaStreamWaitEvent(c->stream, c->in_ready[b], 0));
+    const double* st = c->fin[b];
+    int ib = 0;
+    rc = upload_enqueue(c, F.n, 0, cudaMemcpyDeviceToDevice, nullptr, st, st + F.n, st + 2 * F.n, st + 3 * F.n,
+                        nullptr, nullptr, nullptr, nullptr, &ib);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->in_free[b], c->stream));  // k_ingest has consumed the slot
+    rc = upload_finish(c, F.n, ib);
+    if (rc) return rc;
+    c->iteration = first_iteration + f * iterations;
+    rc = abs_gpu_simulate(c, iterations);
+    if (rc) return rc;
+    // positions -> output slot (after the slot's previous D2H), then D2H
+    if (c->n > c->fout_cap) {  // a model added agents beyond the output staging: regrow it
+      CK(cudaStreamSynchronize(c->d2h));
+      c->fout_cap = 0;
+      for (int q = 0; q < 2; ++q) {
+        cudaFree(c->fout[q]);
+        c->fout[q] = nullptr;
+      }
+      for (int q = 0; q < 2; ++q) CK(dalloc(&c->fout[q], 4 * c->n));
+      c->fout_cap = c->n;
+    }
+    CK(cudaStreamWaitEvent(c->stream, c->out_free[b], 0));
+    if (c->n) {
+      k_split_xyz<<<grid_blocks(c, c->n), kThreads, 0, c->stream>>>(cur_pos(c), F.out_uid ? c->S[c->cur].uid : nullptr,
+                                                                      c->g, c->fout[b], c->n);
+      ++c->launches;
+    }
+    CK(cudaEventRecord(c->out_ready[b], c->stream));
+    CK(cudaStreamWaitEvent(c->d2h, c->out_ready[b], 0));
+    double* dst[3] = {F.out_x, F.out_y, F.out_z};
+    const unsigned long long m = c->n;
+    if (F.n_out) *F.n_out = m;
+    if (m > F.out_cap) {
+      cudaStreamSynchronize(c->d2h);
+      cudaStreamSynchronize(c->h2d);
+      return set_err(c, ABS_ERR_CAPACITY, "frame " + std::to_string(f) + ": " + std::to_string(m) +
+                                              " agents exceed out_cap " + std::to_string(F.out_cap));
+    }
+    for (int q = 0; q < 3; ++q)
+      if (m) CK(cudaMemcpyAsync(dst[q], c->fout[b] + q * m, m * 8, cudaMemcpyDeviceToHost, c->d2h));
+    if (m && F.out_uid) CK(cudaMemcpyAsync(F.out_uid, c->fout[b] + 3 * m, m * 8, cudaMemcpyDeviceToHost, c->d2h));
+    CK(cudaEventRecord(c->out_free[b], c->d2h));
+  }
+  CK(cudaStreamSynchronize(c->d2h));
+  CK(cudaStreamSynchronize(c->h2d));
   return ABS_OK;
 }
 

@@ -375,6 +375,41 @@ class Simulation:
                                           None, None, None, None), self._ctx)
         return int(nn.value)
 
+    def run_frames(self, inputs, outputs, iterations: int = 1, first_iteration: int = 0, uids=None) -> list:
+        """Host-boundary pipeline (abs_gpu_run_frames): for each frame f,
+        upload inputs[f] = (x, y, z, d), run `iterations` iterations from
+        iteration first_iteration + f * iterations, and write the positions
+        into outputs[f] = (x, y, z) (float64 arrays, ideally page-locked);
+        uids[f] (uint64, optional) receives the uid of each output row.
+        The next frame's upload and the previous frame's download overlap
+        the current frame's iterations. Returns the agent count per frame."""
+        if len(inputs) != len(outputs):
+            raise ValueError("one output triple per input frame")
+        frames = (N.Frame * len(inputs))()
+        keep, counts = [], (C.c_uint64 * max(1, len(inputs)))()
+        for f, (inp, out) in enumerate(zip(inputs, outputs)):
+            a = [np.ascontiguousarray(v, np.float64) for v in inp]
+            o = list(out)
+            for v in o:
+                if v.dtype != np.float64 or not v.flags.c_contiguous:
+                    raise ValueError("outputs must be contiguous float64 arrays")
+            keep += a
+            n = len(a[0])
+            if any(len(v) != n for v in a):
+                raise ValueError("frame arrays differ in length")
+            u = None if uids is None else uids[f]
+            if u is not None and (u.dtype != np.uint64 or not u.flags.c_contiguous):
+                raise ValueError("uids must be contiguous uint64 arrays")
+            cap = min(len(v) for v in o + ([u] if u is not None else []))
+            frames[f] = N.Frame(n, *(_p(v, C.c_double) for v in a), *(_p(v, C.c_double) for v in o), cap,
+                                C.cast(C.byref(counts, 8 * f), C.POINTER(C.c_uint64)), _p(u, C.c_uint64))
+        t0 = time.perf_counter()
+        N.check(N.load().abs_gpu_run_frames(self._ctx, frames, len(inputs), iterations, first_iteration),
+                self._ctx)
+        self._wall_ms += (time.perf_counter() - t0) * 1e3
+        del keep
+        return [int(counts[f]) for f in range(len(inputs))]
+
     # -- timing of the dominant kernel --------------------------------------
     def reset_timers(self, enable: bool = True):
         N.check(N.load().abs_gpu_reset_timers(self._ctx, 1 if enable else 0), self._ctx)
