@@ -615,14 +615,16 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     const double r = 0.5 * (me.d + dmax);
     unsigned int evals = 0, nov = 0;
     const float dif = static_cast<float>(me.d);
+    // contact superset threshold: (0.5 (d_a + d_b) + slack)^2 (1 + 5e-7), the
+    // half diameter of this agent and the slack folded in once
+    const float hme = 0.5f * dif + slack;
     if constexpr (F32) {
-      walk(r, r * r, [&](unsigned int j, float df2, float qd) {
-        ++evals;
-        const float hp = 0.5f * (dif + qd) + slack;
-        if (df2 < hp * hp * 1.0000005f) {
-          if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
-          ++nov;
-        }
+      walk(r, r * r, [&](unsigned int j, float df2, float qd, bool in) {
+        evals += in;
+        const float hp = __fmaf_rn(0.5f, qd, hme);
+        const bool ct = in && df2 < hp * hp * 1.0000005f;
+        if (ct && nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+        nov += ct;
       });
     } else {
       walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {
@@ -681,9 +683,9 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       }
       for (; c < nov; ++c) contact(ovl[c * ovl_stride]);
     } else if constexpr (F32) {  // more contacts than the list holds: re-walk (rare)
-      walk(r, r * r, [&](unsigned int j, float df2, float qd) {
-        const float hp = 0.5f * (dif + qd) + slack;
-        if (df2 < hp * hp * 1.0000005f) contact(j);
+      walk(r, r * r, [&](unsigned int j, float df2, float qd, bool in) {
+        const float hp = __fmaf_rn(0.5f, qd, hme);
+        if (in && df2 < hp * hp * 1.0000005f) contact(j);
       });
     } else {
       walk(r, r * r, [&](unsigned int j, const Pd& q, double d2) {

@@ -450,16 +450,21 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
   box_bin_range(g, cx, cy, cz, bl, bh);
   const int z0 = max(fbin_raw(fz - rf, g.inv_s[2]), bl[2]), z1 = min(fbin_raw(fz + rf, g.inv_s[2]), bh[2]);
   const int y0 = max(fbin_raw(fy - rf, g.inv_s[1]), bl[1]), y1 = min(fbin_raw(fy + rf, g.inv_s[1]), bh[1]);
-  auto test = [&](unsigned int j, const float4& qf) {
+  // Classification of one candidate: `in` is exactly the reference's
+  // j != self && fp64 d2 <= r2 (fp32 decides outside the margin band, fp64
+  // inside it). Branch-free apart from the rare band reload; the visitor is
+  // called for every slot with the decision (visit(j, df2, qd, in)).
+  auto test = [&](unsigned int j, const float4& qf, bool valid) {
     const float ex = fx - qf.x, ey = fy - qf.y, ez = fz - qf.z;
-    const float df2 = (ex * ex + ey * ey) + ez * ez;
-    if (j == self || df2 > rout2) return;
-    if (df2 > rin2) {  // margin band: the reference's exact fp64 test
+    // fused: fewer roundings than the unfused sum, inside the same slack bound
+    const float df2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
+    bool in = valid && j != self && df2 <= rout2;
+    if (in && df2 > rin2) {  // margin band: the reference's exact fp64 test
       const Pd q = load_pd(pd + j);
       const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
-      if (!((dx * dx + dy * dy) + dz * dz <= r2)) return;
+      in = (dx * dx + dy * dy) + dz * dz <= r2;
     }
-    visit(j, df2, qf.w);
+    visit(j, df2, qf.w, in);
   };
   // Phase 1a: row geometry only — the cell-table slots of each row's x range
   // [start[a0], start[a1]) go to the window arrays, no loads yet.
@@ -482,17 +487,21 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
         ++nr;
       } else {  // overflow rows: nested walk
         const unsigned int j1 = __ldg(start + row + x1 + 1);
-        for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) test(j, __ldg(pf + j));
+        for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) test(j, __ldg(pf + j), true);
       }
     }
   }
-  // Phase 1b: the cell-table loads, kRowBatch rows in flight at a time; empty
-  // windows are compacted out in place (write index <= read index).
+  // Phase 1b: the cell-table loads, kRowBatch rows in flight at a time. Empty
+  // windows are compacted out in place (write index <= read index) and the
+  // rest are stored as one flat stream: window k covers flat positions
+  // [P_k, P_{k+1}) and candidate index = flat position + off_k, with
+  // off_k = start_k - P_k in wj0 and the bound P_{k+1} in wj1.
 #ifndef ABS_ROW_BATCH
 #define ABS_ROW_BATCH 4
 #endif
   constexpr int kRowBatch = ABS_ROW_BATCH;
   int nw = 0;
+  unsigned int total = 0;
   for (int r0 = 0; r0 < nr; r0 += kRowBatch) {
     unsigned int lo[kRowBatch], hi[kRowBatch];
 #pragma unroll
@@ -504,37 +513,70 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
 #pragma unroll
     for (int u = 0; u < kRowBatch; ++u) {
       if (r0 + u < nr && hi[u] > lo[u]) {
-        wj0[nw][t] = lo[u];
-        wj1[nw][t] = hi[u];
+        wj0[nw][t] = lo[u] - total;
+        total += hi[u] - lo[u];
+        wj1[nw][t] = total;
         ++nw;
       }
     }
   }
 #if defined(ABS_ABLATE) && ABS_ABLATE == 1
-  if (nw > 1000) visit(self, 0.0f, 0.0f);  // timing ablation: rows only
+  if (nw > 1000) visit(self, 0.0f, 0.0f, true);  // timing ablation: rows only
   return;
 #endif
   if (nw == 0) return;
+  // Phase 2: the flat stream, kBatch candidates per step. Advancing a window
+  // is a predicated reload (windows are non-empty), no per-candidate branch.
   int k = 0;
-  unsigned int j = wj0[0][t], je = wj1[0][t];
-  while (k < nw) {
+  unsigned int off = wj0[0][t], bnd = wj1[0][t];
+  for (unsigned int p = 0; p < total;) {
     unsigned int idx[kBatch];
+    bool val[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
-      idx[u] = self;  // sentinel: skipped by test()
-      if (k < nw) {
-        idx[u] = j;
-        if (++j == je && ++k < nw) {
-          j = wj0[k][t];
-          je = wj1[k][t];
-        }
+      val[u] = p < total;
+      idx[u] = val[u] ? p + off : self;
+      ++p;
+      if (p == bnd) {
+        k = min(k + 1, nw - 1);
+        off = wj0[k][t];
+        bnd = wj1[k][t];
       }
     }
     float4 qf[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pf + idx[u]);
+#ifndef ABS_BAND_BATCH
+#define ABS_BAND_BATCH 0  // c4 @ 2^26: 25.8 ms per-candidate vs 26.9 batched (2^24: 5.63 vs 5.50)
+#endif
+#if !ABS_BAND_BATCH
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) test(idx[u], qf[u]);
+    for (int u = 0; u < kBatch; ++u) test(idx[u], qf[u], val[u]);
+    continue;
+#endif
+    // classify the batch; one branch covers the (rare) margin-band reloads
+    float df2[kBatch];
+    bool in[kBatch];
+    bool band = false;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const float ex = fx - qf[u].x, ey = fy - qf[u].y, ez = fz - qf[u].z;
+      df2[u] = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
+      in[u] = val[u] && idx[u] != self && df2[u] <= rout2;
+      band |= in[u] && df2[u] > rin2;
+    }
+    if (band) {
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        if (in[u] && df2[u] > rin2) {  // the reference's exact fp64 test
+          const Pd q = load_pd(pd + idx[u]);
+          const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
+          in[u] = (dx * dx + dy * dy) + dz * dz <= r2;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) visit(idx[u], df2[u], qf[u].w, in[u]);
   }
 }
 
