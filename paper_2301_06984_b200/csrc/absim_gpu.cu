@@ -115,7 +115,7 @@ __device__ void reset_reduction(DevGrid* g) {
 
 // uniform_grid.cpp:155-237 sizing; one thread.
 __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, unsigned int bins_yz,
-                           unsigned long long bins_cap,
+                           unsigned int row_block_shift, unsigned long long bins_cap,
                            unsigned long long capacity, unsigned long long uid_cap, int may_add,
                            unsigned long long iteration) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -169,10 +169,27 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
   }
   if (err == kErrNone) {
     unsigned int B[3] = {bins_x, bins_yz, bins_yz};
-    const unsigned long long boxes = (unsigned long long)g->dims[0] * g->dims[1] * g->dims[2];
-    if (boxes * B[0] * B[1] * B[2] + 1 > 0xFFFFFFFFull) B[0] = B[1] = B[2] = 1;
-    const unsigned long long nbins = boxes * B[0] * B[1] * B[2];
-    if (nbins + 1 > bins_cap) {
+    // rows in y-blocks of 2^ysh (row_of); ~0u = one block (z-major rows)
+    auto rows_shift = [&](unsigned int by) {
+      unsigned int sh = 0;
+      if (row_block_shift == ~0u) {
+        while ((1u << sh) < by) ++sh;
+      } else {
+        sh = row_block_shift;
+      }
+      return sh;
+    };
+    auto padded = [&](const unsigned int* Bk) {
+      const unsigned long long by = (unsigned long long)g->dims[1] * Bk[1];
+      const unsigned int sh = rows_shift(static_cast<unsigned int>(by));
+      const unsigned long long byp = ((by + (1ull << sh) - 1) >> sh) << sh;
+      return (unsigned long long)g->dims[0] * Bk[0] * byp * ((unsigned long long)g->dims[2] * Bk[2]);
+    };
+    if (padded(B) + 1 > 0xFFFFFFFFull) B[0] = B[1] = B[2] = 1;
+    const unsigned long long nbins = padded(B);
+    if (nbins + 1 > 0xFFFFFFFFull) {  // padded bin rows exceed the u32 cell table
+      err = kErrBoxBudget;
+    } else if (nbins + 1 > bins_cap) {
       err = kErrBinsRetry;
       g->needed_bins = nbins + 1;
     } else if (may_add && (2 * n > capacity || g->uid_count + n > uid_cap)) {
@@ -183,6 +200,8 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
         g->s[k] = B[k] == 1 ? g->box : g->box / static_cast<double>(B[k]);
         g->bd[k] = g->dims[k] * B[k];
       }
+      g->ysh = rows_shift(g->bd[1]);
+      g->bd1p = ((g->bd[1] + (1u << g->ysh) - 1u) >> g->ysh) << g->ysh;
       g->nbins = nbins;
       double mag = g->box;
       for (int k = 0; k < 3; ++k) {
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_key(const Pd* __restrict__ pos, co
     const unsigned int bx = bin_coord(p.x, G.origin[0], G, 0);
     const unsigned int by = bin_coord(p.y, G.origin[1], G, 1);
     const unsigned int bz = bin_coord(p.z, G.origin[2], G, 2);
-    const unsigned int b = bx + G.bd[0] * (by + G.bd[1] * bz);
+    const unsigned int b = bx + G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
     ABS_ASSERT(b < G.nbins);
     key[i] = b;
     rank[i] = atomicAdd(count + b, 1u);
@@ -1017,7 +1036,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     for (int idx = tid; idx < nrows * (nhx + 1); idx += kTileThreads) {
       const int r = idx / (nhx + 1), e = idx % (nhx + 1);
       const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-      const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+      const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
       T.lst[r][e] = __ldg(start + row + T.hx0 + e);
     }
     __syncthreads();
@@ -1076,7 +1095,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
           len = overflow ? 0 : T.lst[r][T.qoff[1]] - T.lst[r][T.qoff[0]];
           if (overflow) {  // global indices: recompute from start[]
             const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-            const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+            const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
             len = __ldg(start + row + T.hx0 + T.qoff[1]) - __ldg(start + row + T.hx0 + T.qoff[0]);
           }
         }
@@ -1120,7 +1139,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
           gi = T.rowg0[r] + (li - T.lrow[r]);
         } else {
           const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-          const unsigned int row = G.bd[0] * (by + G.bd[1] * bz);
+          const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
           gi = __ldg(start + row + T.hx0 + T.qoff[0]) + off;
         }
         const Pd me = overflow ? load_pd(S.pd + gi) : T.sp[li];
@@ -1246,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
   const double L = a.mp[0], r = a.mp[1], step = a.mp[2], prob = a.mp[4];
   const unsigned long long rec = static_cast<unsigned long long>(a.mp[3]);
   const double box = g->box, r2 = r * r;
-  const unsigned int D0 = g->dims[0], D1 = g->dims[1], D2 = g->dims[2];
+  const unsigned int D0 = g->dims[0], D1 = g->dims[1], D2 = g->dims[2], ysh = g->ysh;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd me = load_pd(S.pd + i);
@@ -1268,7 +1287,7 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
         const unsigned int bz = (cz + D2 + dz) % D2;
         for (int dy = -1; dy <= 1; ++dy) {
           const unsigned int by = (cy + D1 + dy) % D1;
-          const unsigned int row = D0 * (by + D1 * bz);
+          const unsigned int row = D0 * row_of(by, bz, ysh, D2);
           for (int dx = -1; dx <= 1; ++dx) {
             const unsigned int bx = (cx + D0 + dx) % D0;
             const unsigned int j1 = __ldg(start + row + bx + 1);
@@ -1361,7 +1380,7 @@ __global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
             for (unsigned int sz = 0; sz < G.B[2]; ++sz)
               for (unsigned int sy = 0; sy < G.B[1]; ++sy) {
                 const unsigned int bz = (unsigned int)z * G.B[2] + sz, by = (unsigned int)y * G.B[1] + sy;
-                const unsigned int row = G.bd[0] * (by + G.bd[1] * bz) + (unsigned int)x * G.B[0];
+                const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]) + (unsigned int)x * G.B[0];
                 for (unsigned int j = start[row]; j < start[row + G.B[0]]; ++j) {
                   const Pd q = load_pd(live + j);
                   const double dx = c.x - q.x, dy = c.y - q.y, dz = c.z - q.z;
@@ -2248,6 +2267,22 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
   return a;
 }
 
+// Bin rows are stored in y-blocks of 2^shift rows (row_of, kernels.cuh).
+// ABSIM_ROW_BLOCK = rows per block (power of two; 0 = one block, i.e.
+// z-major rows); default 32 (c4 @ 2^26 k_force: z-major 25.9 ms, 8: 25.8,
+// 16: 26.1, 32: 25.3, 64: 28.9; c3 step 1.67 -> 1.54 ms at 16).
+unsigned int row_block_shift() {
+  static const unsigned int v = [] {
+    const char* e = std::getenv("ABSIM_ROW_BLOCK");
+    const long x = e ? std::atol(e) : 32;
+    if (x <= 0) return ~0u;
+    unsigned int sh = 0;
+    while ((1l << (sh + 1)) <= x && sh < 12) ++sh;
+    return sh;
+  }();
+  return v;
+}
+
 // Sub-bins per box edge: y/z rows finer than x (the x extent of a row is
 // trimmed to the sphere's cross-section, so x resolution matters less).
 // Auto (bins_per_box == 0): when the typical query radius 0.5 (d + dmax) is
@@ -2293,7 +2328,8 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   }
   const Pd* pos = cur_pos(c);
   k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_x(c), bins_yz(c), c->bins_cap, c->cap,
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_x(c), bins_yz(c), row_block_shift(),
+                                      c->bins_cap, c->cap,
                                       c->uid_cap, may_add, iteration);
   k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
   c->launches += 3;
@@ -2851,7 +2887,8 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     c->grid_valid = false;
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, ~0ull, ~0ull, ~0ull, 0, iteration);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, row_block_shift(), ~0ull, ~0ull, ~0ull,
+                                      0, iteration);
   k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, exact_order ? 0 : 1);
   c->launches += 1;
   const int nxt = c->cur ^ 1;

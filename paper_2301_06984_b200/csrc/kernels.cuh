@@ -66,6 +66,8 @@ struct DevGrid {
   unsigned int bd[3];  // bins per axis = B[k] * dims[k]
   unsigned int B[3];   // sub-bins per box edge per axis (x, y, z)
   unsigned int sort_passes;  // 8-bit radix passes the last k_sort_keys needs (even)
+  unsigned int ysh;   // bin rows are stored in y-blocks of 2^ysh rows (row_of)
+  unsigned int bd1p;  // bd[1] padded to a multiple of 2^ysh
   unsigned long long nbins;
   unsigned long long needed_bins;
   unsigned long long n;
@@ -157,7 +159,19 @@ struct QGrid {
   unsigned int bd[3];
   unsigned int B[3];
   unsigned int dims[3];
+  unsigned int ysh;
 };
+
+// Storage position of bin row (by, bz): rows are x-contiguous runs of the
+// cell-ordered arrays, ordered by (y-block, z, y within the block). A
+// front-to-back sweep over storage then walks one y-block column along z, so
+// the rows its neighbour queries touch span (2^ysh + a few) x (a few) rows
+// instead of whole z-layers: the candidate working set stays in L2 at any
+// population size (bin index = x + bd[0] * row_of(...)).
+__device__ __forceinline__ unsigned int row_of(unsigned int by, unsigned int bz, unsigned int ysh,
+                                               unsigned int bd2) {
+  return (((by >> ysh) * bd2 + bz) << ysh) + (by & ((1u << ysh) - 1u));
+}
 
 __device__ __forceinline__ QGrid make_qgrid(const DevGrid& g) {
   QGrid q;
@@ -174,6 +188,7 @@ __device__ __forceinline__ QGrid make_qgrid(const DevGrid& g) {
     q.dims[k] = g.dims[k];
     ext = fmaxf(ext, static_cast<float>(g.s[k] * g.bd[k]));
   }
+  q.ysh = g.ysh;
   q.slack = 16.0f * ext * 5.96046448e-8f + 1e-5f;
   return q;
 }
@@ -241,7 +256,7 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
       const float w = cull_sqrt(rem);
       const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
       const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
-      const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
       const unsigned int j1 = __ldg(start + row + x1 + 1);
       for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) {
         if (j == self) continue;
@@ -289,7 +304,8 @@ __device__ __forceinline__ void for_each_neighbor_box(const QGrid& g, const Pd* 
   const int z0 = max(bz - 1, 0), z1 = min(bz + 1, static_cast<int>(g.dims[2]) - 1);
   for (int z = z0; z <= z1; ++z)
     for (int y = y0; y <= y1; ++y) {
-      const unsigned int row = g.dims[0] * (static_cast<unsigned int>(y) + g.dims[1] * static_cast<unsigned int>(z));
+      const unsigned int row =
+          g.dims[0] * row_of(static_cast<unsigned int>(y), static_cast<unsigned int>(z), g.ysh, g.dims[2]);
       const unsigned int j0 = __ldg(start + row + x0), j1 = __ldg(start + row + x1 + 1);
       for (unsigned int j = j0; j < j1; j += kBatch) {
         Pd q[kBatch];
@@ -337,7 +353,7 @@ __device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd*
       const float w = sqrtf(rem);
       const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
       const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
-      const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
       ABS_ASSERT(x0 >= 0 && x1 + 1 <= (int)g.bd[0] && by >= 0 && bz >= 0 && by < (int)g.bd[1] && bz < (int)g.bd[2]);
       const unsigned int j0 = __ldg(start + row + x0);
       const unsigned int j1 = __ldg(start + row + x1 + 1);
@@ -480,7 +496,7 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
       const float w = cull_sqrt(rem);
       const int x0 = max(fbin_raw(fx - w, g.inv_s[0]), bl[0]);
       const int x1 = min(fbin_raw(fx + w, g.inv_s[0]), bh[0]);
-      const unsigned int row = g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+      const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
       if (nr < kMaxRows) {
         wj0[nr][t] = row + x0;
         wj1[nr][t] = row + x1 + 1;
@@ -638,7 +654,7 @@ __device__ __forceinline__ void for_each_neighbor_group(const QGrid& g, const Pd
           const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
           const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
           const unsigned int row =
-              g.bd[0] * (static_cast<unsigned int>(by) + g.bd[1] * static_cast<unsigned int>(bz));
+              g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
           const unsigned int a0 = __ldg(start + row + x0);
           const unsigned int a1 = __ldg(start + row + x1 + 1);
           j0[m] = a0;
