@@ -199,6 +199,28 @@ class Simulation {
     return out;
   }
 
+  // Host-boundary pipeline (abs_gpu_run_frames): independent host frames, each
+  // = add the frame's agents -> simulate(iterations) -> read positions back,
+  // with the next frame's upload and the previous frame's download overlapping
+  // the current frame on the device. Replaces the staged population.
+  struct Frame {
+    const double *x, *y, *z, *d;  // n agents (page-locked memory: plain DMA)
+    std::uint64_t n;
+    double *out_x, *out_y, *out_z;  // out_cap entries each
+    std::uint64_t out_cap;
+    std::uint64_t* out_uid = nullptr;  // optional
+    std::uint64_t n_out = 0;           // filled: agents after the iterations
+  };
+  void run_frames(std::vector<Frame>& frames, std::uint64_t iterations, std::uint64_t first_iteration = 0) {
+    std::vector<abs_frame> f(frames.size());
+    for (std::size_t i = 0; i < frames.size(); ++i) {
+      const Frame& F = frames[i];
+      f[i] = abs_frame{F.n, F.x, F.y, F.z, F.d, F.out_x, F.out_y, F.out_z, F.out_cap, &frames[i].n_out, F.out_uid};
+    }
+    uploaded_ = true;  // the frames replace any staged population
+    check(abs_gpu_run_frames(ctx_, f.data(), f.size(), iterations, first_iteration), ctx_);
+  }
+
   void flush() {
     if (uploaded_) return;
     uploaded_ = true;

@@ -151,6 +151,31 @@ int main() {
     sim.simulate(10);
     CHECK(sim.report().iterations == 10 && sim.report().final_agent_count == 0);
   }
+  {  // mechanics.cpp:10-27 through the frame pipeline: each frame is a pair at
+     // distance 8 with diameters 10 -> overlap 2, |F| = 4 (test_mechanics.cpp:11-30),
+     // displaced by F dt; frames are independent populations
+    std::printf("frames\n");
+    SimulationParams p;
+    p.simulation_time_step = 0.01;
+    Simulation sim(p);
+    std::vector<double> x = {0.0, 8.0}, y = {0.0, 0.0}, z = {0.0, 0.0}, d = {10.0, 10.0};
+    std::vector<double> x2 = {100.0, 108.0};
+    std::vector<std::vector<double>> ox(2, std::vector<double>(2)), oy = ox, oz = ox;
+    std::vector<std::vector<std::uint64_t>> ou(2, std::vector<std::uint64_t>(2));
+    std::vector<Simulation::Frame> fr(2);
+    for (int f = 0; f < 2; ++f)
+      fr[f] = Simulation::Frame{f ? x2.data() : x.data(), y.data(), z.data(), d.data(), 2,
+                                ox[f].data(), oy[f].data(), oz[f].data(), 2, ou[f].data()};
+    sim.run_frames(fr, 1);
+    for (int f = 0; f < 2; ++f) {
+      CHECK(fr[f].n_out == 2);
+      const double base = f ? 100.0 : 0.0;
+      for (int i = 0; i < 2; ++i) {
+        const double want = base + (ou[f][i] == 0 ? -0.04 : 8.04);  // F dt = 4 * 0.01
+        CHECK(std::fabs(ox[f][i] - want) < 1e-12);
+      }
+    }
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
   return failures;
 }
