@@ -44,6 +44,12 @@ constexpr int kForceMinBlocks = ABS_FORCE_MIN_BLOCKS;
 #endif
 constexpr int kPassB = ABS_PASSB;  // contact records fetched together in pass B
 constexpr int kForceMinBlocksF32 = ABS_FORCE_MIN_BLOCKS_F32;
+// box-lockstep walk (bins == boxes): no row windows in shared memory, so the
+// register budget alone sets residency
+#ifndef ABS_FORCE_MIN_BLOCKS_BOX
+#define ABS_FORCE_MIN_BLOCKS_BOX 8  // c3 k_force 0.685 (shared 96-reg build) -> 0.496 ms; c1 0.083 -> 0.059 ms (7: 0.530 / 0.057)
+#endif
+constexpr int kForceMinBlocksBox = ABS_FORCE_MIN_BLOCKS_BOX;
 constexpr unsigned long long kInfOrdLo = 0xFFF0000000000000ull;  // ord_enc(+inf)
 constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf)
 constexpr unsigned long long kZeroOrd = 0x8000000000000000ull;   // ord_enc(+0.0)
@@ -812,8 +818,12 @@ __device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsign
 // overflow and as the reference implementation of the tiled kernel below.
 // Resident CTAs per SM the register budget is sized for (c4 @ 2^24 sweep:
 // fp32 walk 5 -> 6.27 ms vs 2 -> 6.96 ms; box mode c3 4 -> 0.68 vs 2 -> 0.77).
-template <int MODEL, bool STATIC, bool RECORD, bool F32>
-__global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kForceMinBlocks)
+// WALK: 0 flat fp64 walk, 1 fp32-classified flat walk, 2 box-lockstep walk
+// (bins == boxes, decided on the host; 0/1 also fall back to it when the
+// device grid has no sub-bins).
+template <int MODEL, bool STATIC, bool RECORD, int WALK>
+__global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
+                                                           : (WALK == 1 ? kForceMinBlocksF32 : kForceMinBlocks))
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
@@ -821,9 +831,10 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
   if (gp->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
+  constexpr bool F32 = WALK == 1;
   auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
   auto wj1 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
-  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + 2 * kMaxRows * kForceThreads);
+  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + (WALK == 2 ? 0 : 2 * kMaxRows) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
   if (MODEL == ABS_MODEL_COHERE && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
@@ -836,7 +847,8 @@ __global__ void __launch_bounds__(kForceThreads, F32 ? kForceMinBlocksF32 : kFor
   }
   const unsigned long long n = gp->n;
   const double dmax = gp->dmax;
-  const bool box_mode = Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1;  // bins are the reference boxes
+  // bins are the reference boxes
+  const bool box_mode = WALK == 2 || (Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1);
   unsigned long long n_eval = 0, n_skip = 0;
   // Persistent warps sweep 32-agent chunks in a static warp-strided order:
   // the resident warps cover a contiguous window of the agent array (cell
@@ -2114,12 +2126,10 @@ int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
 }
 
 template <class K>
-int force_blocks(const abs_gpu_ctx* c, K kernel) {  // persistent: the resident CTAs only
-  int per_sm = 0;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kForceThreads,
-                                                (2 * kMaxRows + kMaxContacts) * kForceThreads * 4);
+int force_blocks(const abs_gpu_ctx* c, K kernel, int smem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4) {
+  int per_sm = 0;  // persistent: the resident CTAs only
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kForceThreads, smem);
   return c->sms * std::max(per_sm, 1);
 }
 
@@ -2369,22 +2379,25 @@ bool use_tile_kernel() {
 
 constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
 
-template <int MODEL, bool STATIC, bool RECORD, bool F32>
+constexpr int kForceSmemBox = kMaxContacts * kForceThreads * 4;  // contact lists only
+
+template <int MODEL, bool STATIC, bool RECORD, int WALK>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   static int blocks = 0;  // per template instance
+  constexpr int smem = WALK == 2 ? kForceSmemBox : kForceSmem;
   if (!blocks) {
-    cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, F32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kForceSmem);
-    blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, F32>);
+    cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, WALK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, WALK>, smem);
   }
-  k_force<MODEL, STATIC, RECORD, F32><<<blocks, kForceThreads, kForceSmem, c->stream>>>(
+  k_force<MODEL, STATIC, RECORD, WALK><<<blocks, kForceThreads, smem, c->stream>>>(
       S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
 void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  if (use_f32_walk()) launch_gather_f<MODEL, STATIC, RECORD, true>(c, S, a);
-  else launch_gather_f<MODEL, STATIC, RECORD, false>(c, S, a);
+  if (bins_x(c) == 1u && bins_yz(c) == 1u) launch_gather_f<MODEL, STATIC, RECORD, 2>(c, S, a);
+  else if (use_f32_walk()) launch_gather_f<MODEL, STATIC, RECORD, 1>(c, S, a);
+  else launch_gather_f<MODEL, STATIC, RECORD, 0>(c, S, a);
 }
 
 // Lanes per agent of the group kernel: ABSIM_LPA in {1 (per-lane k_force), 2,

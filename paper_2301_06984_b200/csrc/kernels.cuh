@@ -276,8 +276,14 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
 // prefetch, so a warp costs max(total candidates) rather than the sum over
 // rows of the longest window. Rows beyond kMaxRows fall back to the nested
 // walk. Visits exactly the same set as for_each_neighbor.
-constexpr int kMaxRows = 32;
-constexpr int kMaxContacts = 16;  // recorded possible contacts per agent (pass B)
+#ifndef ABS_MAX_ROWS
+#define ABS_MAX_ROWS 32
+#endif
+#ifndef ABS_MAX_CONTACTS
+#define ABS_MAX_CONTACTS 16
+#endif
+constexpr int kMaxRows = ABS_MAX_ROWS;
+constexpr int kMaxContacts = ABS_MAX_CONTACTS;  // recorded possible contacts per agent (pass B)
 constexpr int kForceThreads = 128;
 #ifndef ABS_PREFILTER
 #define ABS_PREFILTER 0

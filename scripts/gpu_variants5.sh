@@ -1,0 +1,12 @@
+#!/bin/bash
+# box-walk residency variants: parity subset, then c3 (static spheroid) and c1 step/k_force times
+mkdir -p gpurun_out
+TAG=${TAG:-v5}
+for L in variants/*.so; do ABSIM_GPU_LIB=$PWD/$L timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -m gpu -q -x 2>&1 | tail -1 | sed "s#^#$L #" >> gpurun_out/${TAG}_pytest.log; done
+timeout 900 python scripts/sweep_force.py --config c3 --libs variants/*.so --bins 0x0 --steps 10 > gpurun_out/${TAG}_sweep_c3.log 2>&1
+timeout 900 python scripts/sweep_force.py --config c1 --libs variants/*.so --bins 0x0 --steps 50 --warmup 5 > gpurun_out/${TAG}_sweep_c1.log 2>&1
+timeout 900 python scripts/sweep_force.py --config c4 --libs variants/box_m7.so --bins 0x0 > gpurun_out/${TAG}_sweep_c4.log 2>&1
+cat gpurun_out/${TAG}_pytest.log; grep -h force_ms gpurun_out/${TAG}_sweep_*.log | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['lib'], d['n'], round(d['ms_per_step'],4), round(d['force_ms'],4))"
