@@ -834,7 +834,10 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
   constexpr bool F32 = WALK == 1;
   auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
   auto wj1 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
-  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + (WALK == 2 ? 0 : 2 * kMaxRows) * kForceThreads);
+  // fp32 walk: 16-bit stream bounds, so its contact lists start after 1.5 row arrays
+  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(
+      force_smem + (WALK == 2 ? 0 : (WALK == 1 ? kMaxRows + kMaxRows / 2 : 2 * kMaxRows)) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
   if (MODEL == ABS_MODEL_COHERE && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
@@ -873,7 +876,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
         dg = agent_step<MODEL, STATIC, RECORD, 1, true>(
             S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
             [&](double r, double r2, auto&& visit) {
-              for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2, visit);
+              for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wb16, self, me.x, me.y, me.z, r, r2, visit);
             },
             [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, Q.slack,
             query);
@@ -2380,11 +2383,13 @@ bool use_tile_kernel() {
 constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
 
 constexpr int kForceSmemBox = kMaxContacts * kForceThreads * 4;  // contact lists only
+constexpr int kForceSmemF32 = (kMaxRows + kMaxRows / 2 + kMaxContacts) * kForceThreads * 4;
+static_assert(kMaxRows % 2 == 0, "16-bit bound array packs two rows per word");
 
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   static int blocks = 0;  // per template instance
-  constexpr int smem = WALK == 2 ? kForceSmemBox : kForceSmem;
+  constexpr int smem = WALK == 2 ? kForceSmemBox : (WALK == 1 ? kForceSmemF32 : kForceSmem);
   if (!blocks) {
     cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, WALK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, WALK>, smem);

@@ -455,7 +455,7 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
                                                          const float4* __restrict__ pf,
                                                          const unsigned int* __restrict__ start,
                                                          unsigned int (*wj0)[kForceThreads],
-                                                         unsigned int (*wj1)[kForceThreads],
+                                                         unsigned short (*wj1)[kForceThreads],
                                                          unsigned int self, double cx, double cy,
                                                          double cz, double r, double r2, F&& visit) {
   const int t = threadIdx.x;
@@ -503,9 +503,9 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
       const int x0 = max(fbin_raw(fx - w, g.inv_s[0]), bl[0]);
       const int x1 = min(fbin_raw(fx + w, g.inv_s[0]), bh[0]);
       const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
-      if (nr < kMaxRows) {
+      if (nr < kMaxRows) {  // first bin and bin count of the row window
         wj0[nr][t] = row + x0;
-        wj1[nr][t] = row + x1 + 1;
+        wj1[nr][t] = static_cast<unsigned short>(x1 + 1 - x0);
         ++nr;
       } else {  // overflow rows: nested walk
         const unsigned int j1 = __ldg(start + row + x1 + 1);
@@ -517,7 +517,9 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
   // windows are compacted out in place (write index <= read index) and the
   // rest are stored as one flat stream: window k covers flat positions
   // [P_k, P_{k+1}) and candidate index = flat position + off_k, with
-  // off_k = start_k - P_k in wj0 and the bound P_{k+1} in wj1.
+  // off_k = start_k - P_k in wj0 and the bound P_{k+1} in wj1 (16 bits: a
+  // window that would push the stream past 65535 candidates is walked
+  // directly instead).
 #ifndef ABS_ROW_BATCH
 #define ABS_ROW_BATCH 4
 #endif
@@ -529,15 +531,20 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
 #pragma unroll
     for (int u = 0; u < kRowBatch; ++u) {
       const int q = min(r0 + u, nr - 1);
-      lo[u] = __ldg(start + wj0[q][t]);
-      hi[u] = __ldg(start + wj1[q][t]);
+      const unsigned int b0 = wj0[q][t];
+      lo[u] = __ldg(start + b0);
+      hi[u] = __ldg(start + b0 + wj1[q][t]);
     }
 #pragma unroll
     for (int u = 0; u < kRowBatch; ++u) {
       if (r0 + u < nr && hi[u] > lo[u]) {
+        if (total + (hi[u] - lo[u]) > 0xFFFFu) {  // stream bound would not fit 16 bits
+          for (unsigned int j = lo[u]; j < hi[u]; ++j) test(j, __ldg(pf + j), true);
+          continue;
+        }
         wj0[nw][t] = lo[u] - total;
         total += hi[u] - lo[u];
-        wj1[nw][t] = total;
+        wj1[nw][t] = static_cast<unsigned short>(total);
         ++nw;
       }
     }

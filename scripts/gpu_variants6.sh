@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+TAG=${TAG:-v6}
+for L in variants/*.so; do ABSIM_GPU_LIB=$PWD/$L timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py tests/test_frames.py -m gpu -q -x 2>&1 | tail -1 | sed "s#^#$L #" >> gpurun_out/${TAG}_pytest.log; done
+timeout 1500 python scripts/sweep_force.py --config c4 --libs variants/*.so --bins 0x0 > gpurun_out/${TAG}_sweep_c4_26.log 2>&1
+timeout 1200 python scripts/sweep_force.py --config c4 --n 16777216 --libs variants/*.so --bins 0x0 > gpurun_out/${TAG}_sweep_c4_24.log 2>&1
+cat gpurun_out/${TAG}_pytest.log; grep -h force_ms gpurun_out/${TAG}_sweep_*.log | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['lib'], d['n'], round(d['ms_per_step'],4), round(d['force_ms'],4))"
