@@ -119,7 +119,10 @@ CPU_STEPS = {"c1": 200, "c2": 60, "c3": 20, "c4": 12, "c5": 10, "rclust": 10, "r
 REF_BUILDERS = {"ref_clustering": "clustering", "ref_proliferation": "proliferation"}
 
 
-def _ref_sim(wl_name, sample_n, threads):
+ENV_IDS = {"uniform_grid": 0, "brute_force": 1}
+
+
+def _ref_sim(wl_name, sample_n, threads, env="uniform_grid"):
     """The reference engine (oracle/_ref, unmodified absim) on a bounded
     sample of the workload; falls back to the C port if it is not built."""
     from oracle import oracle as O
@@ -129,7 +132,7 @@ def _ref_sim(wl_name, sample_n, threads):
                        detect_static=prm.get("detect_static_agents", False),
                        model=prm.get("model", 0), mp=prm.get("model_params", [0.0] * 8),
                        sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0,
-                       fixed_box=prm.get("fixed_box_length", 0.0))
+                       fixed_box=prm.get("fixed_box_length", 0.0), env=ENV_IDS[env])
     try:
         if prm.get("model", 0) == 4:  # SIR: the reference has no periodic boundaries
             raise FileNotFoundError("no reference path for config 5")
@@ -145,11 +148,15 @@ def _ref_sim(wl_name, sample_n, threads):
         return s, "port", 1, wl
 
 
-def cpu_baseline(wl_name, steps=None, threads=None):
+BRUTE_SAMPLE, BRUTE_STEPS = 16384, 4  # O(N^2) reference: a smaller bounded sample
+
+
+def cpu_baseline(wl_name, steps=None, threads=None, env="uniform_grid"):
     """Reference CPU throughput on a bounded sample (population built untimed)."""
     threads = threads or os.cpu_count()
-    steps = steps or CPU_STEPS[wl_name]
-    sim, kind, cores, wl = _ref_sim(wl_name, CPU_SAMPLE[wl_name], threads)
+    brute = env != "uniform_grid"
+    steps = steps or (BRUTE_STEPS if brute else CPU_STEPS[wl_name])
+    sim, kind, cores, wl = _ref_sim(wl_name, BRUTE_SAMPLE if brute else CPU_SAMPLE[wl_name], threads, env)
     agent_its = 0
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -168,7 +175,9 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count()
-    sim, kind, cores, wl = _ref_sim(args.config, CPU_SAMPLE[args.config], threads)
+    brute = args.env != "uniform_grid"
+    sim, kind, cores, wl = _ref_sim(args.config, BRUTE_SAMPLE if brute else CPU_SAMPLE[args.config], threads,
+                                    args.env)
     for _ in range(args.warmup):
         sim.simulate(1)
     agent_its = 0
@@ -181,7 +190,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": wl.name, "sample_agents": wl.n},
+            "data": "synthetic", "config": {"workload": wl.name, "sample_agents": wl.n, "environment": args.env},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{wl.name} shape at {wl.n} agents, {args.steps} timed iterations"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -314,6 +323,7 @@ def run_gpu(args):
     wl = _workload(args.config, args.n, seed=args.seed + rank)
     prm = dict(wl.params)
     prm["record_forces"] = False
+    prm["environment"] = args.env
     prm["bins_per_box"] = args.bins
     prm["bins_per_box_x"] = args.bins_x
     if wl.params.get("model") == E.MODEL_PROLIFERATION:
@@ -440,7 +450,7 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": f"replicas{world}" if world > 1 else "single", "environment": args.env,
                    "bins_per_box": [args.bins_x, args.bins, args.bins], "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
         "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else "k_force", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
@@ -454,7 +464,7 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(args.config)
+        line["cpu_baseline"] = cpu_baseline(args.config, env=args.env)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
@@ -476,6 +486,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--decompose", action="store_true", help="use the slab decomposition even at N=1")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force"],
+                    help="EnvironmentKind (params.hpp:9); brute_force = the O(N^2) comparison baseline")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

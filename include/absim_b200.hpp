@@ -18,6 +18,7 @@
 #pragma once
 
 #include <array>
+#include <limits>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -61,11 +62,15 @@ struct SimulationParams {
   int model = ABS_MODEL_NONE;
   std::array<double, 8> model_params{};
   bool record_forces = true;
+  // EnvironmentKind (params.hpp:9): ABS_ENV_UNIFORM_GRID or ABS_ENV_BRUTE_FORCE
+  int environment_kind = ABS_ENV_UNIFORM_GRID;
 
   // SimulationParams::validate (params.cpp:44-72), hot-path fields
   void validate() const {
     auto fail = [](const char* what) { throw std::invalid_argument(what); };
     if (fixed_box_length < 0.0) fail("fixed_box_length must be >= 0");
+    if (sorting_frequency > 0 && environment_kind != ABS_ENV_UNIFORM_GRID)
+      fail("sorting requires the uniform_grid environment");
     if (!(simulation_time_step > 0.0)) fail("simulation_time_step must be > 0");
     if (repulsion_coefficient < 0.0) fail("repulsion_coefficient must be >= 0");
     if (!(max_displacement > 0.0)) fail("max_displacement must be > 0");
@@ -99,14 +104,14 @@ class UniformGrid {
   explicit UniformGrid(Simulation& sim) : sim_(sim) {}
   void update();
   double largest_agent_diameter() const { return info().first[4]; }
-  double max_query_radius() const { return box_length(); }
+  double max_query_radius() const;  // unbounded for the brute-force environment
   double box_length() const { return info().first[3]; }
   Vec3 origin() const {
     const auto g = info().first;
     return {g[0], g[1], g[2]};
   }
   std::array<std::uint32_t, 3> dims() const { return info().second; }
-  const char* name() const { return "uniform_grid"; }
+  const char* name() const;
   // box_index_of for every agent (storage order of agents())
   std::vector<std::uint64_t> cell_ids();
   // for_each_neighbor at the force radius 0.5 (d + dmax) for every agent,
@@ -136,6 +141,7 @@ class Simulation {
     cfg.model = params_.model;
     for (int i = 0; i < 8; ++i) cfg.model_params[i] = params_.model_params[i];
     cfg.record_forces = params_.record_forces ? 1 : 0;
+    cfg.environment = params_.environment_kind;
     check(abs_gpu_create(&cfg, device, &ctx_), nullptr);
   }
   ~Simulation() { abs_gpu_destroy(ctx_); }
@@ -241,6 +247,15 @@ class Simulation {
 inline void UniformGrid::update() {
   sim_.flush();
   check(abs_gpu_env_update(sim_.native()), sim_.native());
+}
+
+inline double UniformGrid::max_query_radius() const {
+  return sim_.params().environment_kind == ABS_ENV_BRUTE_FORCE ? std::numeric_limits<double>::infinity()
+                                                               : box_length();
+}
+
+inline const char* UniformGrid::name() const {
+  return sim_.params().environment_kind == ABS_ENV_BRUTE_FORCE ? "brute_force" : "uniform_grid";
 }
 
 inline std::pair<std::array<double, 5>, std::array<std::uint32_t, 3>> UniformGrid::info() const {

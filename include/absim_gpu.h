@@ -79,6 +79,12 @@ extern "C" {
                                      radius (<= box length, e.g. fixed_box_length), mp[1] speed; same-tag
                                      neighbours only */
 
+/* environment kinds (params.hpp:9 EnvironmentKind; simulation.cpp:40-53 make_environment) */
+#define ABS_ENV_UNIFORM_GRID 0  /* UniformGrid: the B200 cell table */
+#define ABS_ENV_BRUTE_FORCE 1   /* BruteForceEnvironment (environment.hpp:53-80): every agent is a
+                                   candidate, no maximum query radius; O(N^2) comparison baseline.
+                                   Sorting (params.cpp:52-55) and cell ids need the grid. */
+
 typedef struct abs_gpu_ctx abs_gpu_ctx;
 
 /* SimulationParams (params.hpp:17-52), hot-path subset + device knobs */
@@ -99,6 +105,8 @@ typedef struct {
   int32_t record_forces;         /* keep Agent::last_force (parity); 0 skips the 24 B/agent write */
   int32_t bins_per_box;          /* internal sub-bins per box edge along y and z: 0 auto, 1..4 */
   int32_t bins_per_box_x;        /* internal sub-bins per box edge along x: 0 auto, 1..4 */
+  int32_t environment;           /* ABS_ENV_* (SimulationParams::environment_kind), default grid */
+  int32_t reserved;
 } abs_gpu_config;
 
 /* SimulationReport counters (report.hpp:32-40) */
@@ -226,7 +234,8 @@ int abs_gpu_run_frames(abs_gpu_ctx* ctx, const abs_frame* frames, uint64_t count
 int abs_gpu_env_update(abs_gpu_ctx* ctx);
 /* grid[0..2] origin, grid[3] box length, grid[4] largest diameter */
 int abs_gpu_grid_info(abs_gpu_ctx* ctx, double* grid, uint32_t* dims);
-/* reference box index per agent (download order); requires abs_gpu_env_update */
+/* reference box index per agent (download order); requires abs_gpu_env_update;
+ * ABS_ERR_STATE under ABS_ENV_BRUTE_FORCE (no grid) */
 int abs_gpu_cell_ids(abs_gpu_ctx* ctx, uint64_t* out);
 /* CSR of sorted neighbour uids per agent (download order) within the force
  * query radius; offsets has n+1 entries. *total receives the number of uids;

@@ -57,6 +57,8 @@ typedef struct {
   int32_t model; /* 0 none, 1 volume grow/divide, 2 drive, 3 grow, 4 SIR,
                     5 models::GrowDivide, 6 models::Cohere */
   double mp[8];
+  int32_t env; /* EnvironmentKind; the port restates the uniform grid only (0) */
+  int32_t pad;
 } orc_params;
 
 typedef struct {
@@ -126,6 +128,10 @@ static void init_slot(orc_sim* s, uint64_t i, uint64_t uid, double x, double y, 
 
 orc_sim* orc_create(const orc_params* p, uint64_t n, const double* x, const double* y,
                     const double* z, const double* d, const uint8_t* mask) {
+  if (p->env != 0) {
+    fail("the port restates the uniform grid environment only");
+    return NULL;
+  }
   orc_sim* s = calloc(1, sizeof *s);
   s->p = *p;
   reserve(s, n);

@@ -43,6 +43,8 @@ class _Params(C.Structure):
         ("detect_static", C.c_int32),
         ("model", C.c_int32),
         ("mp", C.c_double * 8),
+        ("env", C.c_int32),
+        ("pad", C.c_int32),
     ]
 
 
@@ -62,6 +64,7 @@ class OracleParams:
     detect_static: bool = False
     model: int = MODEL_NONE
     mp: list = field(default_factory=lambda: [0.0] * 8)
+    env: int = 0  # EnvironmentKind (params.hpp:9): 0 uniform grid, 1 brute force, 2 kd-tree (reference only)
 
     def to_c(self) -> _Params:
         p = _Params()
@@ -76,6 +79,7 @@ class OracleParams:
         p.sorting_frequency = self.sorting_frequency
         p.detect_static = 1 if self.detect_static else 0
         p.model = self.model
+        p.env = self.env
         mp = list(self.mp) + [0.0] * (8 - len(self.mp))
         for i in range(8):
             p.mp[i] = float(mp[i])

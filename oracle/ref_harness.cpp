@@ -40,6 +40,8 @@ struct RefParams {
   std::int32_t detect_static;
   std::int32_t model;  // 0 none, 1 volume grow/divide (c2), 2 drive (c3), 3 grow (ref Grow)
   double mp[8];
+  std::int32_t env;  // EnvironmentKind: 0 uniform grid, 1 brute force, 2 kd-tree
+  std::int32_t pad;
 };
 
 // BASELINE configs[1]: volume growth + division (see absim_models.h).
@@ -102,6 +104,8 @@ SimulationParams to_params(const RefParams& r) {
   p.fixed_box_length = r.fixed_box;
   p.sorting_frequency = r.sorting_frequency;
   p.detect_static_agents = r.detect_static != 0;
+  p.environment_kind = r.env == 1 ? EnvironmentKind::kBruteForce
+                                  : (r.env == 2 ? EnvironmentKind::kKdTree : EnvironmentKind::kUniformGrid);
   return p;
 }
 
@@ -280,7 +284,15 @@ int ref_env_update(void* h, double* grid, std::uint32_t* dims, std::uint64_t* in
   return guarded([&] {
     Simulation& s = *static_cast<Ref*>(h)->sim;
     s.environment().update();
-    auto& g = dynamic_cast<UniformGrid&>(s.environment());
+    auto* gp = dynamic_cast<UniformGrid*>(&s.environment());
+    if (!gp) {  // brute-force / kd-tree: no grid tuple, only the largest diameter
+      grid[0] = grid[1] = grid[2] = grid[3] = 0.0;
+      grid[4] = s.environment().largest_agent_diameter();
+      dims[0] = dims[1] = dims[2] = 0;
+      if (indexed) *indexed = 0;
+      return;
+    }
+    auto& g = *gp;
     grid[0] = g.origin().x;
     grid[1] = g.origin().y;
     grid[2] = g.origin().z;

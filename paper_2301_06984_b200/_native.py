@@ -25,6 +25,7 @@ ABS_ERR_STATE = 8
 MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3, 4
 MODEL_GROW_DIVIDE, MODEL_COHERE = 5, 6  # the reference's own models::GrowDivide / models::Cohere
 FLAG_GHOST = 128
+ENV_UNIFORM_GRID, ENV_BRUTE_FORCE = 0, 1  # EnvironmentKind (params.hpp:9)
 
 # every symbol include/absim_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -56,6 +57,8 @@ class Config(C.Structure):
         ("record_forces", C.c_int32),
         ("bins_per_box", C.c_int32),
         ("bins_per_box_x", C.c_int32),
+        ("environment", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 

@@ -120,7 +120,7 @@ __device__ void reset_reduction(DevGrid* g) {
 }
 
 // uniform_grid.cpp:155-237 sizing; one thread.
-__global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, unsigned int bins_yz,
+__global__ void k_finalize(DevGrid* g, double fixed_box, int brute, unsigned int bins_x, unsigned int bins_yz,
                            unsigned int row_block_shift, unsigned long long bins_cap,
                            unsigned long long capacity, unsigned long long uid_cap, int may_add,
                            unsigned long long iteration) {
@@ -154,6 +154,13 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, unsigned int bins_x, un
     if (err == kErrNone) {
       if (g->ov_on) {
         g->box = g->ov_grid[3];
+      } else if (brute) {
+        // BruteForceEnvironment (environment.hpp:53-80): no grid. One box
+        // larger than the bounding box holds every agent, so the box walk
+        // visits all of them with the exact d2 <= r^2 test.
+        double ext = 0.0;
+        for (int k = 0; k < 3; ++k) ext = fmax(ext, hi[k] - lo[k]);
+        g->box = 2.0 * ext + dm + 1.0;
       } else if (fixed_box > 0.0) {
         if (dm > fixed_box) err = kErrFixedBox;
         g->box = fixed_box;
@@ -840,7 +847,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
       force_smem + (WALK == 2 ? 0 : (WALK == 1 ? kMaxRows + kMaxRows / 2 : 2 * kMaxRows)) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
-  if (MODEL == ABS_MODEL_COHERE && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
+  if (MODEL == ABS_MODEL_COHERE && !a.brute && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
     // uniform_grid.cpp:176-181: the query radius must not exceed the box
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       gw->err = kErrQueryRadius;
@@ -2122,6 +2129,9 @@ bool uses_ext(const abs_gpu_config& cfg) {
   return cfg.model == ABS_MODEL_GROW_DIVIDE || cfg.model == ABS_MODEL_COHERE;
 }
 
+// BruteForceEnvironment (environment.hpp:53-80) instead of the grid.
+int brute_env(const abs_gpu_ctx* c) { return c->cfg.environment == ABS_ENV_BRUTE_FORCE ? 1 : 0; }
+
 int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   const unsigned long long b = (work + kThreads - 1) / kThreads;
   const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 8;
@@ -2277,6 +2287,7 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
   a.model = c->cfg.model;
   a.detect_static = c->cfg.detect_static_agents;
   a.record_forces = c->cfg.record_forces;
+  a.brute = brute_env(c);
   return a;
 }
 
@@ -2304,12 +2315,12 @@ unsigned int row_block_shift() {
 // diameter spread (config 4) 2x2 sub-bins in y/z and 3 along x cut the
 // candidates ~2x (c4 @ 2^24: 2x2x2 7.77 ms, 3 along x 7.50 ms, 2x3x3 8.55 ms).
 unsigned int bins_yz(const abs_gpu_ctx* c) {
-  if (c->cfg.model == ABS_MODEL_SIR) return 1u;
+  if (c->cfg.model == ABS_MODEL_SIR || brute_env(c)) return 1u;
   const int b = c->cfg.bins_per_box;
   return b <= 0 ? c->auto_bins : static_cast<unsigned int>(std::min(b, 4));
 }
 unsigned int bins_x(const abs_gpu_ctx* c) {  // auto: 3 along x with 2x2 in y/z (c4 sweep)
-  if (c->cfg.model == ABS_MODEL_SIR) return 1u;
+  if (c->cfg.model == ABS_MODEL_SIR || brute_env(c)) return 1u;
   const int b = c->cfg.bins_per_box_x;
   return b <= 0 ? (c->auto_bins == 2u ? 3u : c->auto_bins) : static_cast<unsigned int>(std::min(b, 4));
 }
@@ -2341,7 +2352,8 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   }
   const Pd* pos = cur_pos(c);
   k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, bins_x(c), bins_yz(c), row_block_shift(),
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c),
+                                      row_block_shift(),
                                       c->bins_cap, c->cap,
                                       c->uid_cap, may_add, iteration);
   k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
@@ -2662,6 +2674,13 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
   if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
   if (cfg->model < 0 || cfg->model > 6) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->environment != ABS_ENV_UNIFORM_GRID && cfg->environment != ABS_ENV_BRUTE_FORCE)
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown environment kind");
+  // params.cpp:52-55
+  if (cfg->sorting_frequency > 0 && cfg->environment != ABS_ENV_UNIFORM_GRID)
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "sorting requires the uniform_grid environment");
+  if (cfg->model == ABS_MODEL_SIR && cfg->environment != ABS_ENV_UNIFORM_GRID)
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "the periodic SIR model runs on the uniform grid");
   if (cfg->model == ABS_MODEL_GROW_DIVIDE && !(cfg->model_params[2] > 0.0))
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "GrowDivide needs an initial diameter > 0");
   if (cfg->model == ABS_MODEL_COHERE && !(cfg->model_params[0] > 0.0))
@@ -2905,8 +2924,8 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     c->grid_valid = false;
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 1, 1, row_block_shift(), ~0ull, ~0ull, ~0ull,
-                                      0, iteration);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull, ~0ull,
+                                      ~0ull, 0, iteration);
   k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, exact_order ? 0 : 1);
   c->launches += 1;
   const int nxt = c->cur ^ 1;
@@ -3495,6 +3514,7 @@ int abs_gpu_grid_info(abs_gpu_ctx* c, double* grid, uint32_t* dims) {
 }
 
 int abs_gpu_cell_ids(abs_gpu_ctx* c, uint64_t* out) {
+  if (c && brute_env(c)) return set_err(c, ABS_ERR_STATE, "the brute_force environment has no cells");
   if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
   if (!c->grid_valid) return set_err(c, ABS_ERR_STATE, "cell ids require abs_gpu_env_update");
   DevGrid h{};

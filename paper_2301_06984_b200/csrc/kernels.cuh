@@ -98,7 +98,7 @@ struct StepArgs {
   int model;
   int detect_static;
   int record_forces;
-  int pad;
+  int brute;  // BruteForceEnvironment: no maximum query radius
 };
 
 // Order-preserving double <-> u64 map for atomicMin/atomicMax.

@@ -20,6 +20,7 @@ path.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import time
 from dataclasses import dataclass, field
 
@@ -40,6 +41,9 @@ def peak_rss_bytes() -> int:
     return 0
 
 
+ENVIRONMENTS = {"uniform_grid": N.ENV_UNIFORM_GRID, "brute_force": N.ENV_BRUTE_FORCE}
+
+
 @dataclass
 class SimulationParams:
     seed: int = 42
@@ -57,6 +61,8 @@ class SimulationParams:
     record_forces: bool = True
     bins_per_box: int = 0      # sub-bins per box edge along y, z (0 = auto)
     bins_per_box_x: int = 0    # sub-bins per box edge along x (0 = auto)
+    # EnvironmentKind (params.hpp:9): "uniform_grid" or "brute_force"
+    environment: str = "uniform_grid"
 
     def validate(self):
         """SimulationParams::validate (params.cpp:44-72), hot-path subset."""
@@ -70,6 +76,10 @@ class SimulationParams:
             raise ValueError("max_displacement must be > 0")
         if self.force_threshold < 0.0:
             raise ValueError("force_threshold must be >= 0")
+        if self.environment not in ENVIRONMENTS:
+            raise ValueError(f"unknown environment kind {self.environment!r}")
+        if self.sorting_frequency > 0 and self.environment != "uniform_grid":
+            raise ValueError("sorting requires the uniform_grid environment")  # params.cpp:52-55
 
     def to_c(self) -> N.Config:
         c = N.Config()
@@ -90,6 +100,7 @@ class SimulationParams:
         c.record_forces = 1 if self.record_forces else 0
         c.bins_per_box = self.bins_per_box
         c.bins_per_box_x = self.bins_per_box_x
+        c.environment = ENVIRONMENTS[self.environment]
         return c
 
 
@@ -126,13 +137,16 @@ def _p(a, ct):
 
 
 class UniformGrid:
-    """Environment contract over the device grid (uniform_grid.hpp:26-94)."""
+    """Environment contract over the device grid (uniform_grid.hpp:26-94).
+    With SimulationParams(environment="brute_force") it is the
+    BruteForceEnvironment (environment.hpp:53-80): every agent is a
+    candidate, max_query_radius is unbounded and there are no cell ids."""
 
     def __init__(self, sim: "Simulation"):
         self._sim = sim
 
     def name(self) -> str:
-        return "uniform_grid"
+        return self._sim.params.environment
 
     def update(self) -> None:
         N.check(N.load().abs_gpu_env_update(self._sim._ctx), self._sim._ctx)
@@ -151,6 +165,8 @@ class UniformGrid:
         return float(self._info()[0][3])
 
     def max_query_radius(self) -> float:
+        if self._sim.params.environment != "uniform_grid":
+            return math.inf
         return self.box_length()
 
     def origin(self) -> np.ndarray:
