@@ -227,6 +227,7 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, int brute, unsigned int
   reset_reduction(g);
   g->work = 0;
   g->sir[0] = g->sir[1] = g->sir[2] = 0;
+  g->mark_n = 0;
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
@@ -417,18 +418,41 @@ __global__ void k_zero_u32(unsigned int* __restrict__ a, const unsigned long lon
 // Phase 1 of run_staticness_update (simulation.cpp:351-373), scatter form:
 // every disturber (moved|grew) or fresh agent flags the agents within its
 // radius 0.5 (d_a + dmax). Racing stores write the same value (1).
+// The marking agents are listed first (one atomic per warp), so the walks
+// run on full warps: only ~10 % of config 3's agents move, scattered over
+// storage, and a per-agent grid would leave ~90 % of the lanes idle.
+__global__ void __launch_bounds__(kThreads) k_mark_list(Soa S, DevGrid* g, unsigned int* __restrict__ list) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long b = blockIdx.x * (unsigned long long)blockDim.x; b < n; b += stride) {
+    const unsigned long long i = b + threadIdx.x;  // warp-uniform trip count
+    bool act = false;
+    if (i < n) act = S.flags[i] & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED);
+    const unsigned int ballot = __ballot_sync(0xffffffffu, act);
+    if (!ballot) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&g->mark_n, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (act) list[base + __popc(ballot & ((1u << lane) - 1u))] = static_cast<unsigned int>(i);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_mark(Soa S, const DevGrid* g,
                                                    const unsigned int* __restrict__ start,
                                                    unsigned char* __restrict__ nv,
-                                                   unsigned char* __restrict__ nn) {
+                                                   unsigned char* __restrict__ nn,
+                                                   const unsigned int* __restrict__ list) {
   if (g->err) return;
   __shared__ QGrid Q;
   if (threadIdx.x == 0) Q = make_qgrid(*g);
   __syncthreads();
-  const unsigned long long n = g->n;
+  const unsigned long long m = g->mark_n;
   const double dmax = g->dmax;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < m;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = list[k];
     const unsigned char f = S.flags[i];
     const bool disturbs = f & (ABS_FLAG_MOVED | ABS_FLAG_GREW);
     const bool fresh = f & ABS_FLAG_NEWLY_ADDED;
@@ -2541,8 +2565,10 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
   const StepArgs a = step_args(c, iteration);
   Soa& S = c->S[c->cur];
   if (c->cfg.detect_static_agents && iteration > 0) {
-    k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn);
-    ++c->launches;
+    // c->rank is free between the re-bin's scatter and the next k_key
+    k_mark_list<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->rank);
+    k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn, c->rank);
+    c->launches += 2;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {
