@@ -55,9 +55,10 @@ constexpr unsigned long long kInfOrdHi = 0x000FFFFFFFFFFFFFull;  // ord_enc(-inf
 constexpr unsigned long long kZeroOrd = 0x8000000000000000ull;   // ord_enc(+0.0)
 
 // ---------------------------------------------------------------- reduce
-__global__ void __launch_bounds__(kThreads) k_reduce(const Pd* __restrict__ pos, DevGrid* g) {
-  if (g->err) return;
-  const unsigned long long n = g->n;
+// Block part of the bounds reduction: per-block min/max/dmax folded into the
+// grid record with order-preserving u64 atomics (bit-exact, order free).
+__device__ __forceinline__ void reduce_bounds_block(const Pd* __restrict__ pos, DevGrid* g, bool skip) {
+  const unsigned long long n = skip ? 0ull : g->n;
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   double dm = 0.0;
   unsigned int bad = 0;
@@ -112,6 +113,11 @@ __global__ void __launch_bounds__(kThreads) k_reduce(const Pd* __restrict__ pos,
   }
 }
 
+__global__ void __launch_bounds__(kThreads) k_reduce(const Pd* __restrict__ pos, DevGrid* g) {
+  if (g->err) return;
+  reduce_bounds_block(pos, g, false);
+}
+
 __device__ void reset_reduction(DevGrid* g) {
   g->red[0] = g->red[1] = g->red[2] = kInfOrdLo;
   g->red[3] = g->red[4] = g->red[5] = kInfOrdHi;
@@ -120,11 +126,22 @@ __device__ void reset_reduction(DevGrid* g) {
 }
 
 // uniform_grid.cpp:155-237 sizing; one thread.
-__global__ void k_finalize(DevGrid* g, double fixed_box, int brute, unsigned int bins_x, unsigned int bins_yz,
-                           unsigned int row_block_shift, unsigned long long bins_cap,
-                           unsigned long long capacity, unsigned long long uid_cap, int may_add,
-                           unsigned long long iteration) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+struct FinArgs {
+  double fixed_box;
+  int brute;
+  unsigned int bins_x, bins_yz, row_block_shift;
+  unsigned long long bins_cap, capacity, uid_cap;
+  int may_add;
+  unsigned long long iteration;
+};
+
+__device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
+  const double fixed_box = fa.fixed_box;
+  const int brute = fa.brute;
+  const unsigned int bins_x = fa.bins_x, bins_yz = fa.bins_yz, row_block_shift = fa.row_block_shift;
+  const unsigned long long bins_cap = fa.bins_cap, capacity = fa.capacity, uid_cap = fa.uid_cap;
+  const int may_add = fa.may_add;
+  const unsigned long long iteration = fa.iteration;
   if (g->err) {
     reset_reduction(g);
     return;
@@ -138,14 +155,14 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, int brute, unsigned int
     g->dmax = 0.0;
   } else {
     double lo[3], hi[3];
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = ord_dec(g->red[k]);
-      hi[k] = ord_dec(g->red[3 + k]);
+    for (int k = 0; k < 3; ++k) {  // L2 reads: the other blocks' atomics
+      lo[k] = ord_dec(__ldcg(&g->red[k]));
+      hi[k] = ord_dec(__ldcg(&g->red[3 + k]));
     }
-    double dm = ord_dec(g->red[6]);
+    double dm = ord_dec(__ldcg(&g->red[6]));
     for (int k = 0; k < 3; ++k)
       if (!isfinite(lo[k]) || !isfinite(hi[k])) err = kErrNonFinite;
-    if (g->nonfinite) err = kErrNonFinite;
+    if (__ldcg(&g->nonfinite)) err = kErrNonFinite;
     if (g->ov_on) {  // multi-domain: grid of all ranks
       for (int k = 0; k < 3; ++k) lo[k] = g->ov_grid[k];
       dm = g->ov_grid[4];
@@ -231,6 +248,28 @@ __global__ void k_finalize(DevGrid* g, double fixed_box, int brute, unsigned int
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
+  }
+}
+
+__global__ void k_finalize(DevGrid* g, FinArgs fa) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  finalize_grid(g, fa);
+}
+
+// Environment update pass 1 in one launch: bounds reduction, then the last
+// block to finish sizes the grid (uniform_grid.cpp:155-237).
+__global__ void __launch_bounds__(kThreads) k_reduce_finalize(const Pd* __restrict__ pos, DevGrid* g, FinArgs fa) {
+  const bool skip = g->err != 0;  // still counted, so the last block resets the reduction
+  reduce_bounds_block(pos, g, skip);
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&g->fin_count, 1ull) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    finalize_grid(g, fa);
+    g->fin_count = 0;
   }
 }
 
@@ -352,6 +391,81 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(T* __restrict__ data,
     run += v[q];
   }
   if (base + kScanTile >= len && threadIdx.x == kThreads - 1) data[len] = run;
+}
+
+// Single-pass exclusive scan of the u32 cell table (decoupled look-back):
+// tiles are taken in order from a ticket counter, each publishes its
+// aggregate, then its inclusive prefix, as one 64-bit word
+// [epoch:24 | flag:2 | value:38] (flag 1 aggregate, 2 inclusive prefix).
+// The epoch (per scan launch) makes the previous scan's words stale without a
+// reset pass; the two tickets alternate by epoch parity and tile 0 clears the
+// one the next scan will use. Same result as k_scan_tiles/partials/apply:
+// data[i] = sum(data[0..i)), data[len] = total.
+__global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restrict__ data,
+                                                           const unsigned long long* len_ptr,
+                                                           unsigned long long* __restrict__ state,
+                                                           unsigned int epoch, const int* err) {
+  unsigned long long* tickets = state;  // [0], [1]
+  if (err && *err) {  // skipped: keep the ticket pair consistent for the next scan
+    if (blockIdx.x == 0 && threadIdx.x == 0) tickets[(epoch + 1) & 1u] = 0;
+    return;
+  }
+  const unsigned long long len = *len_ptr;
+  const unsigned long long ntiles = (len + kScanTile - 1) / kScanTile;
+  unsigned long long* tile_state = state + 2;
+  __shared__ unsigned long long s_tile;
+  __shared__ unsigned long long s_prefix;
+  __shared__ unsigned int tot;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&tickets[epoch & 1u], 1ull);
+  __syncthreads();
+  const unsigned long long t = s_tile;
+  if (t >= ntiles) {
+    if (len == 0 && t == 0 && threadIdx.x == 0) {
+      data[0] = 0;
+      tickets[(epoch + 1) & 1u] = 0;
+    }
+    return;
+  }
+  if (t == 0 && threadIdx.x == 0) tickets[(epoch + 1) & 1u] = 0;
+  const unsigned long long base = t * kScanTile;
+  constexpr int per = kScanTile / kThreads;
+  unsigned int v[per];
+  unsigned int sum = 0;
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    const unsigned long long i = base + threadIdx.x * per + q;
+    v[q] = i < len ? data[i] : 0u;
+    sum += v[q];
+  }
+  unsigned int run = block_excl_scan(sum, &tot);
+  const unsigned long long tag = static_cast<unsigned long long>(epoch & 0xFFFFFFu) << 40;
+  constexpr unsigned long long kAgg = 1ull << 38, kInc = 2ull << 38, kVal = (1ull << 38) - 1;
+  if (threadIdx.x == 0) {
+    unsigned long long prefix = 0;
+    if (t == 0) {
+      atomicExch(&tile_state[0], tag | kInc | tot);
+    } else {
+      atomicExch(&tile_state[t], tag | kAgg | tot);
+      for (long long p = static_cast<long long>(t) - 1; p >= 0;) {
+        const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&tile_state[p]);
+        if ((w & ~((1ull << 40) - 1)) != tag || !(w & (kAgg | kInc))) continue;  // not published yet
+        prefix += w & kVal;
+        if (w & kInc) break;
+        --p;
+      }
+      atomicExch(&tile_state[t], tag | kInc | (prefix + tot));
+    }
+    s_prefix = prefix;
+  }
+  __syncthreads();
+  run += static_cast<unsigned int>(s_prefix);
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    const unsigned long long i = base + threadIdx.x * per + q;
+    if (i < len) data[i] = run;
+    run += v[q];
+  }
+  if (t == ntiles - 1 && threadIdx.x == kThreads - 1) data[len] = run;
 }
 
 // ---------------------------------------------------------------- scatter
@@ -2084,6 +2198,8 @@ struct abs_gpu_ctx {
   unsigned int* key = nullptr;
   unsigned int* rank = nullptr;
   unsigned int* tiles = nullptr;  // scan tile sums (u32)
+  unsigned long long* scan_state = nullptr;  // single-pass cell-table scan (k_scan_onepass)
+  unsigned int scan_epoch = 0;
   unsigned long long* tiles64 = nullptr;
   unsigned char* nv = nullptr;
   unsigned char* nn = nullptr;
@@ -2280,12 +2396,38 @@ int ensure_bins(abs_gpu_ctx* c, unsigned long long want) {
   unsigned long long nb = std::max<unsigned long long>(2 * want, 4096);  // growing domains: few retries
   cudaFree(c->start);
   cudaFree(c->tiles);
+  cudaFree(c->scan_state);
   CK(dalloc(&c->start, nb + 1));
   CK(cudaMemsetAsync(c->start, 0, (nb + 1) * 4, c->stream));
   CK(dalloc(&c->tiles, nb / kScanTile + 2));
+  // single-pass scan: per-tile (epoch, flag, value) words + two tile tickets
+  CK(dalloc(&c->scan_state, (nb + 1) / kScanTile + 4));
+  CK(cudaMemsetAsync(c->scan_state, 0, ((nb + 1) / kScanTile + 4) * 8, c->stream));
   c->bins_cap = nb;
   c->grid_valid = false;
   return ABS_OK;
+}
+
+// The cell table's scan in one launch (k_scan_onepass).
+template <typename T>
+void launch_scan(abs_gpu_ctx* c, T* data, const unsigned long long* len_dev, unsigned long long len_cap,
+                 T* tiles, const int* err);
+
+bool env_flag(const char* name, bool dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::strcmp(e, "0") != 0 : dflt;
+}
+
+void launch_scan_cells(abs_gpu_ctx* c, const unsigned long long* len_dev, unsigned long long len_cap,
+                       const int* err) {
+  static const bool onepass = env_flag("ABSIM_ONEPASS", true);
+  if (!onepass) {
+    launch_scan<unsigned int>(c, c->start, len_dev, len_cap, c->tiles, err);
+    return;
+  }
+  const unsigned int blocks = static_cast<unsigned int>(std::max<unsigned long long>(1, (len_cap + kScanTile - 1) / kScanTile));
+  k_scan_onepass<<<blocks, kThreads, 0, c->stream>>>(c->start, len_dev, c->scan_state, ++c->scan_epoch, err);
+  ++c->launches;
 }
 
 template <typename T>
@@ -2375,14 +2517,19 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
     ++c->launches;
   }
   const Pd* pos = cur_pos(c);
-  k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c),
-                                      row_block_shift(),
-                                      c->bins_cap, c->cap,
-                                      c->uid_cap, may_add, iteration);
+  const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
+                   c->bins_cap, c->cap, c->uid_cap, may_add, iteration};
+  static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
+  if (fused) {
+    k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa);
+  } else {
+    k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
+    k_finalize<<<1, 32, 0, c->stream>>>(c->g, fa);
+    ++c->launches;
+  }
   k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
-  c->launches += 3;
-  launch_scan<unsigned int>(c, c->start, nbins_dev, c->bins_cap, c->tiles, &c->g->err);
+  c->launches += 2;
+  launch_scan_cells(c, nbins_dev, c->bins_cap, &c->g->err);
   const int nxt = c->cur ^ 1;
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
@@ -2768,7 +2915,8 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[0]);
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
-  cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->nv); cudaFree(c->nn); cudaFree(c->st_parent);
+  cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
+  cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
   if (c->ingest_part) cudaFreeHost(c->ingest_part);
   if (c->hgrid) cudaFreeHost(c->hgrid);
@@ -2950,14 +3098,14 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     c->grid_valid = false;
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
-  k_finalize<<<1, 32, 0, c->stream>>>(c->g, c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull, ~0ull,
-                                      ~0ull, 0, iteration);
+  k_finalize<<<1, 32, 0, c->stream>>>(c->g, FinArgs{c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull,
+                                                     ~0ull, ~0ull, 0, iteration});
   k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, exact_order ? 0 : 1);
   c->launches += 1;
   const int nxt = c->cur ^ 1;
   // counting path (device-selected): Morton key + atomic slot, scan, scatter
   k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
-  launch_scan<unsigned int>(c, c->start, &c->g->sort_len, c->bins_cap, c->tiles, &c->g->err);
+  launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
   k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
                                                                c->key, c->rank, c->g, c->cap,
                                                                c->cfg.model == ABS_MODEL_PROLIFERATION,
