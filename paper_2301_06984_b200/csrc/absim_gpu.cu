@@ -1443,22 +1443,36 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
       const unsigned int cx = box_coord(me.x, 0.0, box, D0), cy = box_coord(me.y, 0.0, box, D1),
                          cz = box_coord(me.z, 0.0, box, D2);
       unsigned int k = 0;
-      for (int dz = -1; dz <= 1; ++dz) {
-        const unsigned int bz = (cz + D2 + dz) % D2;
-        for (int dy = -1; dy <= 1; ++dy) {
-          const unsigned int by = (cy + D1 + dy) % D1;
-          const unsigned int row = D0 * row_of(by, bz, ysh, D2);
-          for (int dx = -1; dx <= 1; ++dx) {
-            const unsigned int bx = (cx + D0 + dx) % D0;
-            const unsigned int j1 = __ldg(start + row + bx + 1);
-            for (unsigned int j = __ldg(start + row + bx); j < j1; ++j) {
-              if (j == i || S.beh[j] != ABS_SIR_I) continue;
-              const Pd q = load_pd(S.pd + j);
-              const double ex = abs_min_image(me.x - q.x, L), ey = abs_min_image(me.y - q.y, L),
-                           ez = abs_min_image(me.z - q.z, L);
-              if ((ex * ex + ey * ey) + ez * ez <= r2) ++k;
-            }
-          }
+      // The 27 wrapped boxes as x-contiguous windows: one per (y, z) row, or
+      // two where the x range wraps (dims >= 3, so the three boxes differ).
+      // All 18 cell-table reads are issued before any candidate is touched.
+      auto wrap = [](int v, int d) { return v < 0 ? v + d : (v >= d ? v - d : v); };
+      const int xa = static_cast<int>(cx) - 1, xb = static_cast<int>(cx) + 2;  // [xa, xb)
+      const bool split = xa < 0 || xb > static_cast<int>(D0);
+      // first window [x0a, x1a), second [x0b, x1b) (empty unless split)
+      const unsigned int x0a = split ? (xa < 0 ? 0u : static_cast<unsigned int>(xa)) : static_cast<unsigned int>(xa);
+      const unsigned int x1a = split ? (xa < 0 ? static_cast<unsigned int>(xb) : D0) : static_cast<unsigned int>(xb);
+      const unsigned int x0b = split ? (xa < 0 ? D0 - 1u : 0u) : 0u;
+      const unsigned int x1b = split ? (xa < 0 ? D0 : static_cast<unsigned int>(xb) - D0) : 0u;
+      unsigned int lo[18], hi[18];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) {
+        const unsigned int bz = static_cast<unsigned int>(wrap(static_cast<int>(cz) + q / 3 - 1, static_cast<int>(D2)));
+        const unsigned int by = static_cast<unsigned int>(wrap(static_cast<int>(cy) + q % 3 - 1, static_cast<int>(D1)));
+        const unsigned int row = D0 * row_of(by, bz, ysh, D2);
+        lo[2 * q] = __ldg(start + row + x0a);
+        hi[2 * q] = __ldg(start + row + x1a);
+        lo[2 * q + 1] = split ? __ldg(start + row + x0b) : 0u;
+        hi[2 * q + 1] = split ? __ldg(start + row + x1b) : 0u;
+      }
+#pragma unroll 1
+      for (int w = 0; w < 18; ++w) {
+        for (unsigned int j = lo[w]; j < hi[w]; ++j) {
+          if (j == i || S.beh[j] != ABS_SIR_I) continue;
+          const Pd q = load_pd(S.pd + j);
+          const double ex = abs_min_image(me.x - q.x, L), ey = abs_min_image(me.y - q.y, L),
+                       ez = abs_min_image(me.z - q.z, L);
+          if ((ex * ex + ey * ey) + ez * ez <= r2) ++k;
         }
       }
       if (k > 0 && abs_rng_word(a.seed, S.uid[i], ABS_RNG_SIR_INFECT(a.iteration)) < abs_sir_threshold(prob, k)) {
