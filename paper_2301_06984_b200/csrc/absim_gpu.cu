@@ -245,6 +245,7 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
   g->work = 0;
   g->sir[0] = g->sir[1] = g->sir[2] = 0;
   g->mark_n = 0;
+  g->work_n = 0;
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
@@ -958,6 +959,58 @@ __device__ __forceinline__ void flush_counters(unsigned long long n_eval, unsign
   }
 }
 
+// Static detection pre-pass (simulation.cpp:375-384 + 465-468): an agent
+// that is static this iteration and has no behaviour to run is settled here
+// exactly as agent_step would settle it (flags = static, no force, no move,
+// stale partners and last_force kept, marks cleared); ghosts likewise. The
+// rest is listed (one atomic per warp) for the force sweep, so warps of
+// config 3 (90 % static) run full instead of mostly idle.
+__global__ void __launch_bounds__(kThreads) k_static_pass(Soa S, Pd* __restrict__ out, DevGrid* g,
+                                                          unsigned char* __restrict__ nv,
+                                                          unsigned char* __restrict__ nn, int model_on,
+                                                          unsigned int* __restrict__ work) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  unsigned long long skips = 0;
+  for (unsigned long long b = blockIdx.x * (unsigned long long)blockDim.x; b < n; b += stride) {
+    const unsigned long long i = b + threadIdx.x;  // warp-uniform trip count
+    bool listed = false;
+    if (i < n) {
+      const unsigned char fl = S.flags[i];
+      const bool ghost = fl & kFlagGhost;
+      const bool settle = ghost || ((!model_on || !S.beh[i]) &&
+                                    !(fl & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED |
+                                            ABS_FLAG_NEIGHBOR_VIOLATION | ABS_FLAG_NEW_NEIGHBOR)) &&
+                                    !nv[i] && !nn[i] && S.partners[i] <= 1u);
+      if (settle) {
+        const Pd me = load_pd(S.pd + i);
+        reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
+        reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
+        nv[i] = 0;
+        nn[i] = 0;
+        if (!ghost) {
+          S.flags[i] = ABS_FLAG_STATIC;
+          ++skips;
+        }
+      } else {
+        listed = true;
+      }
+    }
+    const unsigned int ballot = __ballot_sync(0xffffffffu, listed);
+    if (ballot) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&g->work_n, (unsigned long long)__popc(ballot));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (listed) work[base + __popc(ballot & ((1u << lane) - 1u))] = static_cast<unsigned int>(i);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) skips += __shfl_xor_sync(0xffffffffu, skips, off);
+  if (lane == 0 && skips) atomicAdd(&g->skips, skips);
+}
+
 // Global-gather force kernel: one agent per thread, candidates fetched from
 // HBM/L2 through the per-lane flat window stream. Used for small tiles'
 // overflow and as the reference implementation of the tiled kernel below.
@@ -972,7 +1025,8 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-            unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
+            unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag,
+            const unsigned int* __restrict__ work) {
   if (gp->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
@@ -993,7 +1047,9 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
     }
     return;
   }
-  const unsigned long long n = gp->n;
+  // work != nullptr: only the agents k_static_pass listed (the rest were
+  // settled there as static); otherwise every agent in storage order
+  const unsigned long long n = work ? gp->work_n : gp->n;
   const double dmax = gp->dmax;
   // bins are the reference boxes
   const bool box_mode = WALK == 2 || (Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1);
@@ -1007,9 +1063,10 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
   for (unsigned long long chunk = warp_id;; chunk += warps_total) {
     const unsigned long long base = chunk * 32ull;
     if (base >= n) break;
-    const unsigned long long i = base + lane;
+    const bool live = base + lane < n;
+    const unsigned long long i = work ? (live ? work[base + lane] : 0ull) : base + lane;
     Daughter dg{false, 0, 0, 0, 0, 0, 0};
-    if (i < n) {
+    if (live) {
       const Pd me = load_pd(S.pd + i);
       const unsigned int self = static_cast<unsigned int>(i);
       // behaviour-side exact radius query (models::Cohere)
@@ -2579,6 +2636,12 @@ bool use_tile_kernel() {
 
 constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
 
+// ABSIM_STATIC_PREPASS=0: static agents settled inside the force sweep (A/B)
+bool static_prepass() {
+  static const bool v = env_flag("ABSIM_STATIC_PREPASS", true);
+  return v;
+}
+
 constexpr int kForceSmemBox = kMaxContacts * kForceThreads * 4;  // contact lists only
 constexpr int kForceSmemF32 = (kMaxRows + kMaxRows / 2 + kMaxContacts) * kForceThreads * 4;
 static_assert(kMaxRows % 2 == 0, "16-bit bound array packs two rows per word");
@@ -2591,8 +2654,17 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, WALK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, WALK>, smem);
   }
+  const unsigned int* work = nullptr;
+  if (STATIC && a.iteration != 0 && static_prepass()) {  // iteration 0: nobody is static (simulation.cpp:335-349)
+    // c->rank is free after k_mark (it listed the marking agents there)
+    k_static_pass<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->nv, c->nn,
+                                                                       MODEL != ABS_MODEL_NONE, c->rank);
+    ++c->launches;
+    work = c->rank;
+  }
   k_force<MODEL, STATIC, RECORD, WALK><<<blocks, kForceThreads, smem, c->stream>>>(
-      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
+      S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
+      c->st_tag, work);
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
