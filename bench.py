@@ -115,7 +115,7 @@ def _dist():
 
 CPU_SAMPLE = {"c1": 131_072, "c2": None, "c3": 1 << 21, "c4": 1 << 22, "c5": 1 << 21, "rclust": 1 << 18,
               "rprolif": 4096}
-CPU_STEPS = {"c1": 800, "c2": 60, "c3": 20, "c4": 30, "c5": 10, "rclust": 10, "rprolif": 18}
+CPU_STEPS = {"c1": 800, "c2": 60, "c3": 80, "c4": 30, "c5": 10, "rclust": 10, "rprolif": 18}
 REF_BUILDERS = {"ref_clustering": "clustering", "ref_proliferation": "proliferation"}
 
 
