@@ -259,8 +259,18 @@ __global__ void k_finalize(DevGrid* g, FinArgs fa) {
 
 // Environment update pass 1 in one launch: bounds reduction, then the last
 // block to finish sizes the grid (uniform_grid.cpp:155-237).
-__global__ void __launch_bounds__(kThreads) k_reduce_finalize(const Pd* __restrict__ pos, DevGrid* g, FinArgs fa) {
+// zero_start != nullptr: also clears the previous iteration's cell table
+// (entries [0, nbins_prev]; every entry beyond is zero already), which the
+// last block's finalize may resize only after every block has counted in.
+__global__ void __launch_bounds__(kThreads) k_reduce_finalize(const Pd* __restrict__ pos, DevGrid* g, FinArgs fa,
+                                                              unsigned int* __restrict__ zero_start) {
   const bool skip = g->err != 0;  // still counted, so the last block resets the reduction
+  if (zero_start && !skip) {
+    const unsigned long long len = g->nbins + 1;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+      zero_start[i] = 0u;
+  }
   reduce_bounds_block(pos, g, skip);
   __shared__ bool last;
   __threadfence();
@@ -2583,16 +2593,16 @@ void launch_commit(abs_gpu_ctx* c);
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
   const int nb = grid_blocks(c, c->cap);
   const unsigned long long* nbins_dev = &c->g->nbins;
-  if (c->grid_valid) {  // previous cell table still holds scanned offsets
+  static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
+  if (c->grid_valid && !fused) {  // previous cell table still holds scanned offsets
     k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, nbins_dev, 1, &c->g->err);
     ++c->launches;
   }
   const Pd* pos = cur_pos(c);
   const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
                    c->bins_cap, c->cap, c->uid_cap, may_add, iteration};
-  static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
   if (fused) {
-    k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa);
+    k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa, c->grid_valid ? c->start : nullptr);
   } else {
     k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
     k_finalize<<<1, 32, 0, c->stream>>>(c->g, fa);
