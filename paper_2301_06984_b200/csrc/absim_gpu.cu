@@ -2020,12 +2020,20 @@ __device__ __forceinline__ unsigned long long morton_code_of(const DevGrid& G, d
 // by Morton code when the code space fits the cell table (the in-box order is
 // unobservable there: the iteration's re-bin re-orders by cell right after),
 // else the exact radix path. mode == 0 always for abs_gpu_sort.
-__global__ void k_sort_mode(DevGrid* g, unsigned long long table_cap, int allow_counting) {
+// allow_counting: 0 exact radix path, 1 counting path if the code space
+// fits the cell table, 2 counting path required (the host launched only it:
+// if it does not fit, flag a retry so the host re-runs with the radix path).
+__global__ void k_sort_mode(DevGrid* g, unsigned long long table_cap, int allow_counting,
+                            unsigned long long iteration) {
   const unsigned int maxdim = max(g->dims[0], max(g->dims[1], g->dims[2]));
   unsigned int axis_bits = 0;
   while ((1u << axis_bits) < maxdim) ++axis_bits;
   const unsigned int code_bits = (g->dims[2] == 1 ? 2u : 3u) * axis_bits;
   const bool fits = code_bits < 40 && (1ull << code_bits) <= table_cap;
+  if (allow_counting == 2 && !fits && !g->err) {
+    g->err = kErrSortRetry;
+    g->failed_iteration = iteration;
+  }
   g->sort_mode = (allow_counting && fits && !g->err) ? 1u : 0u;
   g->sort_len = g->sort_mode ? (1ull << code_bits) : 0ull;
   if (g->sort_mode) g->sort_passes = 0;
@@ -2280,6 +2288,8 @@ struct abs_gpu_ctx {
   unsigned int* rank = nullptr;
   unsigned int* tiles = nullptr;  // scan tile sums (u32)
   unsigned long long* scan_state = nullptr;  // single-pass cell-table scan (k_scan_onepass)
+  unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
+  unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
   unsigned int scan_epoch = 0;
   unsigned long long* tiles64 = nullptr;
   unsigned char* nv = nullptr;
@@ -3196,18 +3206,42 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
   k_finalize<<<1, 32, 0, c->stream>>>(c->g, FinArgs{c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull,
                                                      ~0ull, ~0ull, 0, iteration});
-  k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, exact_order ? 0 : 1);
+  // Path choice: the counting sort needs the Morton code space of this grid
+  // to fit the cell table. The host guesses from the last grid it read (dims
+  // change slowly) and launches only that path; the device checks the guess
+  // (k_sort_mode) and a wrong counting guess rolls the iteration back to be
+  // re-run with the exact path (kErrSortRetry). Without a guess both paths
+  // are launched and the device picks.
+  int mode_arg = exact_order ? 0 : 1;
+  bool launch_counting = !exact_order, launch_radix = true;
+  if (!exact_order && c->sort_guess_dims[0]) {
+    unsigned int maxdim = std::max(c->sort_guess_dims[0], std::max(c->sort_guess_dims[1], c->sort_guess_dims[2]));
+    unsigned int axis_bits = 0;
+    while ((1u << axis_bits) < maxdim) ++axis_bits;
+    const unsigned int code_bits = (c->sort_guess_dims[2] == 1 ? 2u : 3u) * (axis_bits + 1);  // one bit of slack
+    const bool guess = code_bits < 40 && (1ull << code_bits) <= c->bins_cap && iteration != c->sort_radix_iteration;
+    mode_arg = guess ? 2 : 0;
+    launch_counting = guess;
+    launch_radix = !guess;
+  }
+  k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, mode_arg, iteration);
   c->launches += 1;
   const int nxt = c->cur ^ 1;
-  // counting path (device-selected): Morton key + atomic slot, scan, scatter
-  k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
-  launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
-  k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
-                                                               c->key, c->rank, c->g, c->cap,
-                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                                               c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
-  k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, nullptr);
-  c->launches += 3;
+  if (launch_counting) {  // Morton key + atomic slot, scan, scatter
+    k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+    launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
+    k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
+                                                                 c->key, c->rank, c->g, c->cap,
+                                                                 c->cfg.model == ABS_MODEL_PROLIFERATION,
+                                                                 c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, nullptr);
+    c->launches += 3;
+  }
+  if (!launch_radix) {
+    c->cur = nxt;
+    c->pos_in_new = false;
+    return ABS_OK;
+  }
   // exact path (device-selected otherwise): radix passes + gather
   const unsigned int blocks = static_cast<unsigned int>((c->cap + kSortChunk - 1) / kSortChunk);
   unsigned long long* k1 = c->sort_k[0];
@@ -3269,6 +3303,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     int rc = read_grid(c, &h);
     if (rc) return rc;
     if (h.err == kErrNone) {
+      if (h.n) std::memcpy(c->sort_guess_dims, h.dims, sizeof c->sort_guess_dims);
       c->iteration += todo;
       done += todo;
       if (deferred && todo) c->pending_commit = true;
@@ -3286,6 +3321,11 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
       rc = ensure_bins(c, h.needed_bins);
       if (rc) return rc;
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+    } else if (h.err == kErrSortRetry) {  // re-run that iteration's sort on the exact path
+      c->sort_radix_iteration = fi;
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
       rc = clear_dev_err(c);
       if (rc) return rc;

@@ -47,6 +47,7 @@ enum DevErr : int {
   kErrBinsRetry = 4,  // internal: grow the bin table and re-run the iteration
   kErrCapRetry = 5,   // internal: grow agent capacity and re-run the iteration
   kErrQueryRadius = 6,  // a behaviour's query radius exceeds the box (uniform_grid.cpp:176-181)
+  kErrSortRetry = 7,    // internal: the host's counting-sort guess did not fit; re-run with the exact path
 };
 
 // Grid + bookkeeping living in device memory (one per context).
