@@ -3219,7 +3219,9 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     unsigned int axis_bits = 0;
     while ((1u << axis_bits) < maxdim) ++axis_bits;
     const unsigned int code_bits = (c->sort_guess_dims[2] == 1 ? 2u : 3u) * (axis_bits + 1);  // one bit of slack
-    const bool guess = code_bits < 40 && (1ull << code_bits) <= c->bins_cap && iteration != c->sort_radix_iteration;
+    static const bool force_counting = env_flag("ABSIM_SORT_GUESS_COUNTING", false);  // test hook: always guess counting
+    const bool guess = (force_counting || (code_bits < 40 && (1ull << code_bits) <= c->bins_cap)) &&
+                       iteration != c->sort_radix_iteration;
     mode_arg = guess ? 2 : 0;
     launch_counting = guess;
     launch_radix = !guess;
@@ -3326,6 +3328,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       if (rc) return rc;
     } else if (h.err == kErrSortRetry) {  // re-run that iteration's sort on the exact path
       c->sort_radix_iteration = fi;
+      if (env_flag("ABSIM_SORT_GUESS_COUNTING", false)) std::fprintf(stderr, "absim: sort retry at iteration %llu\n", fi);
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
       rc = clear_dev_err(c);
       if (rc) return rc;
