@@ -492,6 +492,17 @@ struct Soa {
   unsigned long long* rngc;   // Agent::rng_counter (agent.hpp:145)
 };
 
+// Counting-sort scatter: agent i moves to slot start[key[i]] + rank[i] of
+// the destination buffers. kScatterBatch agents per thread are loaded before
+// any store, so each thread keeps several independent loads in flight (the
+// kernel is load-latency bound otherwise). partners are not carried when
+// the force sweep of the same iteration rewrites every one of them
+// (carry_partners = 0: no static detection, no SIR), beh only when a model
+// reads it.
+#ifndef ABS_SCATTER_BATCH
+#define ABS_SCATTER_BATCH 2  // c4 step 30.25 / 29.45 / 29.52 ms at 1 / 2 / 4; c3 0.98 / 0.96 / 0.99
+#endif
+constexpr int kScatterBatch = ABS_SCATTER_BATCH;
 __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos, Soa src, Soa dst,
                                                       float4* __restrict__ pf,
                                                       const unsigned int* __restrict__ start,
@@ -499,33 +510,57 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
                                                       const unsigned int* __restrict__ rank,
                                                       const DevGrid* g, unsigned long long cap,
                                                       int carry_vol, int carry_force, int write_pf,
-                                                      int only_sort_mode = -1, int carry_ext = 0) {
+                                                      int only_sort_mode = -1, int carry_ext = 0,
+                                                      int carry_partners = 1, int carry_beh = 1) {
   if (g->err) return;
   if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned int j = __ldg(start + key[i]) + rank[i];
-    ABS_ASSERT(j < n);
-    const Pd p = load_pd(pos + i);
-    reinterpret_cast<double2*>(dst.pd + j)[0] = make_double2(p.x, p.y);
-    reinterpret_cast<double2*>(dst.pd + j)[1] = make_double2(p.z, p.d);
-    if (write_pf)
-      pf[j] = make_float4(static_cast<float>(p.x - g->origin[0]), static_cast<float>(p.y - g->origin[1]),
-                          static_cast<float>(p.z - g->origin[2]), static_cast<float>(p.d));
-    dst.uid[j] = src.uid[i];
-    dst.flags[j] = src.flags[i];
-    dst.partners[j] = src.partners[i];
-    dst.beh[j] = src.beh[i];
-    if (carry_vol) dst.vol[j] = src.vol[i];
-    if (carry_force) {
-      dst.force[j] = src.force[i];
-      dst.force[cap + j] = src.force[cap + i];
-      dst.force[2 * cap + j] = src.force[2 * cap + i];
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const double ox = g->origin[0], oy = g->origin[1], oz = g->origin[2];
+  for (unsigned long long i0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i0 < n;
+       i0 += stride * kScatterBatch) {
+    unsigned int j[kScatterBatch];
+    Pd p[kScatterBatch];
+    unsigned long long u[kScatterBatch];
+    unsigned int pa[kScatterBatch];
+    unsigned char fl[kScatterBatch], bh[kScatterBatch];
+#pragma unroll
+    for (int b = 0; b < kScatterBatch; ++b) {
+      const unsigned long long i = i0 + b * stride;
+      if (i < n) {
+        j[b] = __ldg(start + key[i]) + rank[i];
+        p[b] = load_pd(pos + i);
+        u[b] = src.uid[i];
+        fl[b] = src.flags[i];
+        if (carry_partners) pa[b] = src.partners[i];
+        if (carry_beh) bh[b] = src.beh[i];
+      }
     }
-    if (carry_ext) {
-      dst.tag[j] = src.tag[i];
-      dst.rngc[j] = src.rngc[i];
+#pragma unroll
+    for (int b = 0; b < kScatterBatch; ++b) {
+      const unsigned long long i = i0 + b * stride;
+      if (i >= n) break;
+      const unsigned int jj = j[b];
+      ABS_ASSERT(jj < n);
+      reinterpret_cast<double2*>(dst.pd + jj)[0] = make_double2(p[b].x, p[b].y);
+      reinterpret_cast<double2*>(dst.pd + jj)[1] = make_double2(p[b].z, p[b].d);
+      if (write_pf)
+        pf[jj] = make_float4(static_cast<float>(p[b].x - ox), static_cast<float>(p[b].y - oy),
+                             static_cast<float>(p[b].z - oz), static_cast<float>(p[b].d));
+      dst.uid[jj] = u[b];
+      dst.flags[jj] = fl[b];
+      if (carry_partners) dst.partners[jj] = pa[b];
+      if (carry_beh) dst.beh[jj] = bh[b];
+      if (carry_vol) dst.vol[jj] = src.vol[i];
+      if (carry_force) {
+        dst.force[jj] = src.force[i];
+        dst.force[cap + jj] = src.force[cap + i];
+        dst.force[2 * cap + jj] = src.force[2 * cap + i];
+      }
+      if (carry_ext) {
+        dst.tag[jj] = src.tag[i];
+        dst.rngc[jj] = src.rngc[i];
+      }
     }
   }
 }
@@ -2600,7 +2635,7 @@ bool uses_f32_walk(const abs_gpu_ctx* c) {
 void launch_commit(abs_gpu_ctx* c);
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
-void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add) {
+void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add, bool in_step = false) {
   const int nb = grid_blocks(c, c->cap);
   const unsigned long long* nbins_dev = &c->g->nbins;
   static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
@@ -2622,9 +2657,13 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->launches += 2;
   launch_scan_cells(c, nbins_dev, c->bins_cap, &c->g->err);
   const int nxt = c->cur ^ 1;
+  // inside an iteration without static detection (and not SIR, whose
+  // partners hold infection times) k_force rewrites every agent's partners
+  const bool carry_partners = !in_step || c->cfg.detect_static_agents || c->cfg.model == ABS_MODEL_SIR;
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                            c->cfg.record_forces, uses_f32_walk(c), -1, uses_ext(c->cfg));
+                                            c->cfg.record_forces, uses_f32_walk(c), -1, uses_ext(c->cfg),
+                                            carry_partners ? 1 : 0, c->cfg.model != ABS_MODEL_NONE ? 1 : 0);
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2786,7 +2825,7 @@ void phase_mark(abs_gpu_ctx* c) {
 }
 
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
-  launch_env_update(c, iteration, adds_agents(c->cfg));
+  launch_env_update(c, iteration, adds_agents(c->cfg), true);
   phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
     const int nb = grid_blocks(c, c->cap);
