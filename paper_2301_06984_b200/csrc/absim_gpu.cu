@@ -292,16 +292,33 @@ __global__ void __launch_bounds__(kThreads) k_key(const Pd* __restrict__ pos, co
   if (g->err) return;
   const DevGrid G = *g;
   const unsigned long long n = G.n;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const Pd p = load_pd(pos + i);
-    const unsigned int bx = bin_coord(p.x, G.origin[0], G, 0);
-    const unsigned int by = bin_coord(p.y, G.origin[1], G, 1);
-    const unsigned int bz = bin_coord(p.z, G.origin[2], G, 2);
-    const unsigned int b = bx + G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
-    ABS_ASSERT(b < G.nbins);
-    key[i] = b;
-    rank[i] = atomicAdd(count + b, 1u);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  // two agents per thread: their loads and slot atomics overlap
+  for (unsigned long long i0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i0 < n; i0 += 2 * stride) {
+    unsigned int b[2], r[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned long long i = i0 + q * stride;
+      if (i < n) {
+        const Pd p = load_pd(pos + i);
+        const unsigned int bx = bin_coord(p.x, G.origin[0], G, 0);
+        const unsigned int by = bin_coord(p.y, G.origin[1], G, 1);
+        const unsigned int bz = bin_coord(p.z, G.origin[2], G, 2);
+        b[q] = bx + G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
+        ABS_ASSERT(b[q] < G.nbins);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (i0 + q * stride < n) r[q] = atomicAdd(count + b[q], 1u);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned long long i = i0 + q * stride;
+      if (i < n) {
+        key[i] = b[q];
+        rank[i] = r[q];
+      }
+    }
   }
 }
 
