@@ -1169,6 +1169,149 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
   flush_counters(n_eval, n_skip, gw);
 }
 
+// ------------------------------------------------------------ split force step
+// Config-4 path (no behaviours, no static detection, fp32-classified walk)
+// as two kernels: k_force_a walks the candidates (evaluation count + contact
+// superset, exactly pass A of agent_step) and writes each agent's contacts to
+// a global list; k_force_b runs pairwise_repulsion on them and integrates
+// (pass B + apply_pending). The walk kernel carries no fp64 force state, so it
+// keeps more warps resident; agents with more than kSplitContacts contacts are
+// listed and re-run through k_force (work list) instead.
+#ifndef ABS_SPLIT_MIN_BLOCKS
+#define ABS_SPLIT_MIN_BLOCKS 6
+#endif
+constexpr int kSplitContacts = 16;
+constexpr unsigned char kSplitOverflow = 0xFF;
+
+__global__ void __launch_bounds__(kForceThreads, ABS_SPLIT_MIN_BLOCKS)
+    k_force_a(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, DevGrid* g,
+              const unsigned int* __restrict__ start, unsigned int* __restrict__ cl, unsigned char* __restrict__ cn,
+              unsigned long long cap, unsigned int* __restrict__ overflow) {
+  if (g->err) return;
+  __shared__ QGrid Q;
+  extern __shared__ __align__(16) unsigned int force_smem[];
+  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
+  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
+  const int lane = threadIdx.x & 31;
+  unsigned long long n_eval = 0;
+  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
+    const unsigned long long base = chunk * 32ull;
+    if (base >= n) break;
+    const unsigned long long i = base + lane;
+    bool over = false;
+    if (i < n) {
+      const Pd me = load_pd(S.pd + i);
+      if (S.flags[i] & kFlagGhost) {  // candidate only (agent_step's ghost branch)
+        reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
+        reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
+        cn[i] = 0;
+      } else {
+        const double r = 0.5 * (me.d + dmax);
+        const float hme = 0.5f * static_cast<float>(me.d) + Q.slack;
+        unsigned int evals = 0, nov = 0;
+        for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, r,
+                                 r * r, [&](unsigned int j, float df2, float qd, bool in) {
+                                   evals += in;
+                                   const float hp = __fmaf_rn(0.5f, qd, hme);
+                                   const bool ct = in && df2 < hp * hp * 1.0000005f;
+                                   if (ct && nov < kSplitContacts) cl[nov * cap + i] = j;
+                                   nov += ct;
+                                 });
+        over = nov > kSplitContacts;
+        if (!over) n_eval += evals;  // an overflowing agent is counted by the full sweep
+        cn[i] = over ? kSplitOverflow : static_cast<unsigned char>(nov);
+      }
+    }
+    const unsigned int ballot = __ballot_sync(0xffffffffu, over);
+    if (ballot) {  // rare: listed for the full kernel
+      unsigned long long b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&g->work_n, (unsigned long long)__popc(ballot));
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (over) overflow[b0 + __popc(ballot & ((1u << lane) - 1u))] = static_cast<unsigned int>(i);
+    }
+  }
+  flush_counters(n_eval, 0ull, g);
+}
+
+template <bool RECORD>
+__global__ void __launch_bounds__(kThreads) k_force_b(Soa S, Pd* __restrict__ out, const DevGrid* g, StepArgs a,
+                                                      const unsigned int* __restrict__ cl,
+                                                      const unsigned char* __restrict__ cn, unsigned long long cap) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned char c = cn[i];
+    if (c == kSplitOverflow) continue;
+    unsigned char fl = S.flags[i];
+    if (fl & kFlagGhost) continue;
+    const Pd me = load_pd(S.pd + i);
+    const double k = a.k;
+    unsigned int contributors = 0;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    for (unsigned int s = 0; s < c; ++s) {
+      const unsigned int j = cl[s * cap + i];
+      const Pd q = load_pd(S.pd + j);
+      const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+      // pairwise_repulsion (mechanics.cpp:10-27), as agent_step's pass B
+      const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+      const double overlap = 0.5 * (me.d + q.d) - dist;
+      if (overlap <= 0.0) continue;
+      double f0, f1, f2;
+      if (dist > 0.0) {
+        const double sc = k * overlap / dist;
+        f0 = dx * sc;
+        f1 = dy * sc;
+        f2 = dz * sc;
+      } else {
+        coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
+      }
+      if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
+        ++contributors;
+        fx += f0;
+        fy += f1;
+        fz += f2;
+      }
+    }
+    double tx = 0.0, ty = 0.0, tz = 0.0;
+    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
+      tx = fx * a.dt;
+      ty = fy * a.dt;
+      tz = fz * a.dt;
+    }
+    // apply_pending (agent.hpp:115-133)
+    Pd np = me;
+    const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
+    if (disp > 0.0) {
+      if (disp > a.max_disp) {
+        const double sc = a.max_disp / disp;
+        tx *= sc;
+        ty *= sc;
+        tz *= sc;
+      }
+      np.x = me.x + tx;
+      np.y = me.y + ty;
+      np.z = me.z + tz;
+      fl |= ABS_FLAG_MOVED;
+    }
+    if (RECORD) {
+      S.force[i] = fx;
+      S.force[cap + i] = fy;
+      S.force[2 * cap + i] = fz;
+    }
+    S.partners[i] = contributors;
+    reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
+    reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
+    S.flags[i] = fl;
+  }
+}
+
 // Group-cooperative force kernel: LPA lanes per agent (for_each_neighbor_group).
 // A warp runs 32 / LPA consecutive agents (cell order) at a time; candidate
 // loads of a group are consecutive records of one bin row, so a warp load
@@ -2342,6 +2485,10 @@ struct abs_gpu_ctx {
   unsigned long long* scan_state = nullptr;  // single-pass cell-table scan (k_scan_onepass)
   unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
   unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
+  // split force step (k_force_a / k_force_b): per-agent contact lists
+  unsigned int* split_cl = nullptr;
+  unsigned char* split_cn = nullptr;
+  unsigned long long split_cap = 0;
   unsigned int scan_epoch = 0;
   unsigned long long* tiles64 = nullptr;
   unsigned char* nv = nullptr;
@@ -2722,6 +2869,63 @@ constexpr int kForceSmemBox = kMaxContacts * kForceThreads * 4;  // contact list
 constexpr int kForceSmemF32 = (kMaxRows + kMaxRows / 2 + kMaxContacts) * kForceThreads * 4;
 static_assert(kMaxRows % 2 == 0, "16-bit bound array packs two rows per word");
 
+// ABSIM_SPLIT_FORCE=1 runs config 4's force sweep as k_force_a + k_force_b.
+// Off by default: 70 registers and 7 resident CTAs for the walk (28 warps/SM
+// against 20) did not move it (c4 @ 2^26: 25.35 ms split vs 25.0-25.45 single).
+bool split_force() {
+  static const bool v = env_flag("ABSIM_SPLIT_FORCE", false);
+  return v;
+}
+
+template <int MODEL, bool STATIC, bool RECORD, int WALK>
+void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a);
+
+// k_force_a -> k_force_b -> k_force over the overflow list.
+int launch_split(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
+  if (c->split_cap != c->cap) {
+    cudaFree(c->split_cl);
+    cudaFree(c->split_cn);
+    c->split_cl = nullptr;
+    c->split_cn = nullptr;
+    c->split_cap = 0;
+    if (dalloc(&c->split_cl, kSplitContacts * c->cap) != cudaSuccess || dalloc(&c->split_cn, c->cap) != cudaSuccess) {
+      cudaGetLastError();
+      return ABS_ERR_CUDA;  // caller falls back to the single-kernel sweep
+    }
+    c->split_cap = c->cap;
+  }
+  static int blocks = 0;
+  constexpr int smem = (kMaxRows + kMaxRows / 2) * kForceThreads * 4;
+  if (!blocks) blocks = force_blocks(c, k_force_a, smem);
+  k_force_a<<<blocks, kForceThreads, smem, c->stream>>>(S, c->pf, c->newpd, c->g, c->start, c->split_cl, c->split_cn,
+                                                         c->cap, c->rank);
+  const int nb = grid_blocks(c, c->cap);
+  if (c->cfg.record_forces)
+    k_force_b<true><<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, a, c->split_cl, c->split_cn, c->cap);
+  else
+    k_force_b<false><<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, a, c->split_cl, c->split_cn, c->cap);
+  c->launches += 2;
+  // agents with more contacts than the list holds: the full sweep (c->rank lists them)
+  static int blocks_f = 0;
+  if (!blocks_f) {
+    cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kForceSmemF32);
+    cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kForceSmemF32);
+    blocks_f = c->sms;
+  }
+  if (c->cfg.record_forces)
+    k_force<ABS_MODEL_NONE, false, true, 1><<<blocks_f, kForceThreads, kForceSmemF32, c->stream>>>(
+        S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol,
+        c->div_mark, c->st_tag, c->rank);
+  else
+    k_force<ABS_MODEL_NONE, false, false, 1><<<blocks_f, kForceThreads, kForceSmemF32, c->stream>>>(
+        S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol,
+        c->div_mark, c->st_tag, c->rank);
+  ++c->launches;
+  return ABS_OK;
+}
+
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   static int blocks = 0;  // per template instance
@@ -2793,6 +2997,9 @@ void launch_group(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
 template <int MODEL, bool STATIC>
 void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
   const bool box_mode = bins_x(c) == 1u && bins_yz(c) == 1u;
+  if (MODEL == ABS_MODEL_NONE && !STATIC && !box_mode && use_f32_walk() && split_force() && !use_tile_kernel()) {
+    if (launch_split(c, S, a) == ABS_OK) return;
+  }
   if (MODEL == ABS_MODEL_COHERE) {  // its behaviour query lives in the gather kernel
     if (c->cfg.record_forces) launch_gather<MODEL, STATIC, true>(c, S, a);
     else launch_gather<MODEL, STATIC, false>(c, S, a);
@@ -3078,6 +3285,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
+  cudaFree(c->split_cl); cudaFree(c->split_cn);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
   if (c->ingest_part) cudaFreeHost(c->ingest_part);
