@@ -3928,8 +3928,22 @@ int abs_gpu_download(abs_gpu_ctx* c, uint64_t* n_out, uint64_t* uid, double* x, 
 // the D2H of frame f overlaps frame f+1. Each frame is exactly
 // abs_gpu_upload (uids 0..n-1) + abs_gpu_set_iteration + abs_gpu_simulate +
 // abs_gpu_download (x, y, z).
+static int run_frames_impl(abs_gpu_ctx* c, const abs_frame* frames, uint64_t count, uint64_t iterations,
+                           uint64_t first_iteration);
+
 int abs_gpu_run_frames(abs_gpu_ctx* c, const abs_frame* frames, uint64_t count, uint64_t iterations,
                        uint64_t first_iteration) {
+  const int rc = run_frames_impl(c, frames, count, iterations, first_iteration);
+  if (rc && c) {  // never return with copies into or out of caller memory still in flight
+    if (c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c->d2h) cudaStreamSynchronize(c->d2h);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+  }
+  return rc;
+}
+
+static int run_frames_impl(abs_gpu_ctx* c, const abs_frame* frames, uint64_t count, uint64_t iterations,
+                           uint64_t first_iteration) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (count && !frames) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "null frames");
   if (c->defer_commit && adds_agents(c->cfg))
