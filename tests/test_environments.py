@@ -108,3 +108,20 @@ def test_gpu_brute_force_equals_grid(engine):
     assert np.array_equal(a["partners"], b["partners"])
     for k in ("x", "y", "z"):
         assert_close(a[k], b[k], 1e-9, 1.0, k)
+
+
+@pytest.mark.gpu
+def test_gpu_brute_force_static_known_answer(engine):
+    """test_scheduler.cpp:464-488 under the brute-force environment: a settled
+    3x3x3 lattice costs 108 evaluations, then all 27 agents are skipped."""
+    E = engine
+    g = np.arange(3) * 10.0
+    x, y, z = (a.ravel() for a in np.meshgrid(g, g, g, indexing="ij"))
+    sim = E.Simulation(E.SimulationParams(detect_static_agents=True, environment="brute_force"))
+    sim.add_agents(x, y, z, np.full(27, 10.0))
+    sim.simulate(1)
+    r = sim.report()
+    assert r.force_evaluations == 108 and r.force_skips == 0
+    sim.simulate(1)
+    r = sim.report()
+    assert r.force_evaluations == 108 and r.force_skips == 27

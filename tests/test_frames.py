@@ -70,3 +70,30 @@ def test_frames_output_capacity_error(engine):
     outs = [tuple(np.zeros(100) for _ in range(3))]
     with pytest.raises(E.AbsimError):
         sim.run_frames([(wl.x, wl.y, wl.z, wl.d)], outs)
+
+
+def test_frames_with_divisions(engine):
+    """A model that adds agents inside a frame (models::GrowDivide): outputs
+    grow past the input count and still equal the sequential API."""
+    E = engine
+    wl = CF.ref_proliferation(216)
+    prm = {**wl.params, "record_forces": False}
+    seq = E.Simulation(E.SimulationParams(**prm))
+    seq.add_agents(wl.x, wl.y, wl.z, wl.d)
+    seq.set_iteration(0)
+    seq.simulate(7)
+    a = seq.agents()
+    i = np.argsort(a["uid"])
+    sim = E.Simulation(E.SimulationParams(**prm))
+    cap = 8 * wl.n
+    outs = [tuple(np.zeros(cap) for _ in range(3)) for _ in range(2)]
+    uids = [np.zeros(cap, np.uint64) for _ in range(2)]
+    counts = sim.run_frames([(wl.x, wl.y, wl.z, wl.d)] * 2, outs, iterations=7, first_iteration=0, uids=uids)
+    assert counts[0] > wl.n
+    # frame 0 starts at iteration 0 like the sequential run
+    n = counts[0]
+    assert n == len(a["uid"])
+    j = np.argsort(uids[0][:n])
+    assert np.array_equal(uids[0][:n][j], a["uid"][i])
+    for k, o in zip("xyz", outs[0]):
+        assert_close(o[:n][j], a[k][i], 1e-9, 1.0, f"divisions {k}")
