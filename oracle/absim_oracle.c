@@ -3,7 +3,7 @@
  * bench.py's cpu_baseline leg. Never linked into the product.
  *
  * Pinned against (a) the unmodified reference compiled by oracle/Makefile
- * (oracle/_ref/libabsim_ref.so; tests/test_oracle_vs_reference.py compares
+ * (oracle/_ref/libabsim_ref.so; tests/test_oracle.py compares
  * every output bit-for-bit) and (b) the golden fixtures in tests/golden/.
  *
  * Semantics follow the reference with ONE worker and ONE domain (the only
