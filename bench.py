@@ -448,6 +448,7 @@ def run_gpu(args):
     step_bytes = wl.bytes_per_agent_iteration * agent_its / max(1, world)
     step_achieved = step_bytes / (ms / 1e3) / 1e9
     traffic = None
+    issue = None
     tp = os.path.join(ROOT, "profiles", "force_traffic.json")
     if os.path.exists(tp):
         try:
@@ -455,6 +456,8 @@ def run_gpu(args):
                 tt = json.load(f)
             if tt.get("config") == args.config and tt.get("agents") == n_agents:
                 traffic = tt.get("dram_bytes_per_launch")
+                issue = {k: tt[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
+                                            "warp_instructions_per_agent") if k in tt}
         except Exception:
             pass
     line = {
@@ -467,7 +470,10 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else "k_force", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
-                     "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms},
+                     "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms,
+                     # the binding limit is instruction issue / load latency, not HBM: the same
+                     # capture's issue-slot utilisation (profiles/force_traffic.json)
+                     "ncu_issue": issue},
         "step_roofline": {"bytes_per_agent_iteration": wl.bytes_per_agent_iteration,
                           "achieved": step_achieved, "frac": step_achieved / hbm, "unit": "GB/s"},
         "clocks": clk.summary(),
