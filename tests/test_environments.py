@@ -125,3 +125,16 @@ def test_gpu_brute_force_static_known_answer(engine):
     sim.simulate(1)
     r = sim.report()
     assert r.force_evaluations == 108 and r.force_skips == 27
+
+
+@pytest.mark.gpu
+def test_gpu_brute_force_edge_cases(engine):
+    E = engine
+    sim = E.Simulation(E.SimulationParams(environment="brute_force"))
+    sim.simulate(3)  # empty population
+    assert sim.report().final_agent_count == 0
+    sim.add_agents([0.0, 1e6], [0.0, 0.0], [0.0, 0.0], [10.0, 10.0])  # far apart: no grid budget in brute force
+    sim.simulate(2)
+    assert sim.report().force_evaluations == 0
+    a = by_uid(sim.agents())
+    assert a["x"].tolist() == [0.0, 1e6]

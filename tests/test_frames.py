@@ -97,3 +97,17 @@ def test_frames_with_divisions(engine):
     assert np.array_equal(uids[0][:n][j], a["uid"][i])
     for k, o in zip("xyz", outs[0]):
         assert_close(o[:n][j], a[k][i], 1e-9, 1.0, f"divisions {k}")
+
+
+def test_frames_edge_cases(engine):
+    """Empty frames and a one-agent frame (uniform_grid.cpp:66-72: N = 0 gives
+    dims {1,1,1}); a lone agent has no neighbours and does not move."""
+    E = engine
+    sim = E.Simulation(E.SimulationParams(simulation_time_step=0.01))
+    e = np.zeros(0)
+    one = (np.array([1.0]), np.array([2.0]), np.array([3.0]), np.array([10.0]))
+    outs = [tuple(np.zeros(4) for _ in range(3)) for _ in range(3)]
+    counts = sim.run_frames([(e, e, e, e), one, (e, e, e, e)], outs, iterations=2)
+    assert counts == [0, 1, 0]
+    assert (outs[1][0][0], outs[1][1][0], outs[1][2][0]) == (1.0, 2.0, 3.0)
+    assert sim.report().force_evaluations == 0
