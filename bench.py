@@ -351,7 +351,7 @@ def run_gpu(args):
     sim.simulate(args.warmup)
     sim.synchronize()
     r0 = sim.report()
-    sim.reset_timers(True)
+    sim.reset_timers(False)  # the headline window records no per-iteration phase events
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -363,8 +363,20 @@ def run_gpu(args):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     r1 = sim.report()
+    # the dominant kernel's average launch time: a few more iterations with the
+    # per-launch CUDA events on (they cost launch-bound configs ~10-15 %)
+    kr = max(1, min(args.steps, 5))
+    sim.reset_timers(True)
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    sim.simulate(kr)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_r = e2.elapsed_time(e3)
     force_ms, force_launches = sim.force_kernel_time()
     sim.reset_timers(False)
+    r2 = sim.report()
     agent_its = None
     # agent count per step (constant unless the model adds agents)
     if r1.agents_added == r0.agents_added:
@@ -392,7 +404,7 @@ def run_gpu(args):
         outp = [torch.empty(wl.n, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
         # a host-driven loop continues the step numbering after each upload
         # (set_iteration), so periodic work (sorting_frequency) keeps its cadence
-        it = args.warmup + args.steps
+        it = sim.iteration
         ext = None
         if wl.tags is not None:  # per-agent tags / stream counters travel with the state
             ext = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy() for a in (wl.tags, wl.rng_counters)]
@@ -438,7 +450,7 @@ def run_gpu(args):
                    "sequential": seq}
 
     hbm, peak_src = _peaks()
-    n_agents = r1.final_agent_count
+    n_agents = (r1.final_agent_count + r2.final_agent_count) // 2  # during the kernel-event pass
     avg_force_ms = force_ms / max(1, force_launches)
     sir = wl.params.get("model") == E.MODEL_SIR
     # k_force: read {x,y,z,d} 32 B + write {x,y,z} 24 B per agent;
@@ -470,7 +482,8 @@ def run_gpu(args):
         "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else "k_force", "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
-                     "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms,
+                     "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms_r,
+                     "timing": f"CUDA events around each launch over {kr} further iterations",
                      # the binding limit is instruction issue / load latency, not HBM: the same
                      # capture's issue-slot utilisation (profiles/force_traffic.json)
                      "ncu_issue": issue},
