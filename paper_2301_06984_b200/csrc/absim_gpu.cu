@@ -1999,6 +1999,8 @@ __global__ void k_grid_reset(DevGrid* g, unsigned long long n, unsigned long lon
 }
 static_assert(offsetof(DevGrid, ov_on) % 8 == 0 && sizeof(DevGrid) % 8 == 0, "grid record layout");
 
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
 // Zero `bytes` bytes on the compute engine (16-byte stores + tail).
 __global__ void k_zero_bytes(unsigned char* __restrict__ p, unsigned long long bytes) {
   const unsigned long long n16 = bytes / 16;
@@ -2485,6 +2487,10 @@ struct abs_gpu_ctx {
   unsigned long long* scan_state = nullptr;  // single-pass cell-table scan (k_scan_onepass)
   unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
   unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
+  // per-iteration CUDA graphs (abs_gpu_simulate): [0] plain, [1] with the Morton sort
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int graph_failures = 0;
+  bool graphs_off = false;
   // split force step (k_force_a / k_force_b): per-agent contact lists
   unsigned int* split_cl = nullptr;
   unsigned char* split_cn = nullptr;
@@ -3296,6 +3302,8 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
     for (cudaEvent_t e : {c->in_ready[b], c->in_free[b], c->out_ready[b], c->out_free[b]})
       if (e) cudaEventDestroy(e);
   }
+  for (cudaGraphExec_t e : c->gexec)
+    if (e) cudaGraphExecDestroy(e);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   free_sort_scratch(c);
@@ -3458,7 +3466,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     CK(dalloc(&c->sort_hist, hlen + 1));
     CK(dalloc(&c->sort_tiles, hlen / kScanTile + 2));
     CK(dalloc(&c->sort_hlen, 1));
-    CK(cudaMemcpyAsync(c->sort_hlen, &hlen, 8, cudaMemcpyHostToDevice, c->stream));
+    k_set_u64<<<1, 1, 0, c->stream>>>(c->sort_hlen, hlen);  // a kernel: capturable in a graph
     c->sort_cap = c->cap;
   }
   const Pd* pos = cur_pos(c);
@@ -3535,6 +3543,13 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   return ABS_OK;
 }
 
+// Graph replay of iterations: ABSIM_GRAPHS=0 disables; never while the
+// per-launch timing events are on.
+bool use_graphs(const abs_gpu_ctx* c) {
+  static const bool on = env_flag("ABSIM_GRAPHS", true);
+  return on && !c->graphs_off && !c->timing;
+}
+
 int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
@@ -3555,13 +3570,59 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     for (unsigned long long t = 0; t < todo; ++t) {
       snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
       const unsigned long long it = c->iteration + t;
-      phase_mark(c);  // iteration start
-      if (c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0) {
-        const int rc = launch_sort(c, it, false);
+      const bool sorts =
+          c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0;
+      auto enqueue = [&]() -> int {
+        phase_mark(c);  // iteration start
+        if (sorts) {
+          const int rc = launch_sort(c, it, false);
+          if (rc) return rc;
+        }
+        phase_mark(c);  // after sort
+        launch_iteration(c, it);
+        return ABS_OK;
+      };
+      // One CUDA graph per iteration (cached executable, parameters updated in
+      // place): the launch-bound small configs lose the inter-kernel gaps.
+      // Any capture problem (e.g. a first-use allocation) falls back to
+      // direct launches for this iteration.
+      if (use_graphs(c)) {
+        const Snap sn = snaps.back();
+        const unsigned long long launches0 = c->launches;
+        const unsigned int epoch0 = c->scan_epoch;
+        bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        int rc = ok ? enqueue() : ABS_OK;
+        cudaGraph_t graph = nullptr;
+        if (ok) ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && graph && rc == ABS_OK;
+        if (ok) {
+          const int slot = sorts ? 1 : 0;
+          if (c->gexec[slot]) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(c->gexec[slot], graph, &info) != cudaSuccess) {
+              cudaGetLastError();
+              cudaGraphExecDestroy(c->gexec[slot]);
+              c->gexec[slot] = nullptr;
+            }
+          }
+          if (!c->gexec[slot] && cudaGraphInstantiate(&c->gexec[slot], graph, 0) != cudaSuccess) {
+            c->gexec[slot] = nullptr;
+            ok = false;
+          }
+          if (ok) ok = cudaGraphLaunch(c->gexec[slot], c->stream) == cudaSuccess;
+        }
+        if (graph) cudaGraphDestroy(graph);
+        if (ok) continue;
+        cudaGetLastError();  // clear the capture error; replay this iteration directly
+        c->cur = sn.cur;
+        c->pos_in_new = sn.pos_in_new;
+        c->grid_valid = sn.grid_valid;
+        c->launches = launches0;
+        c->scan_epoch = epoch0;
+        if (++c->graph_failures >= 4) c->graphs_off = true;
         if (rc) return rc;
       }
-      phase_mark(c);  // after sort
-      launch_iteration(c, it);
+      const int rc = enqueue();
+      if (rc) return rc;
     }
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return set_err(c, ABS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
