@@ -2000,6 +2000,7 @@ __global__ void k_grid_reset(DevGrid* g, unsigned long long n, unsigned long lon
 static_assert(offsetof(DevGrid, ov_on) % 8 == 0 && sizeof(DevGrid) % 8 == 0, "grid record layout");
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+__global__ void k_reset_reduction(DevGrid* g) { reset_reduction(g); }
 
 // Zero `bytes` bytes on the compute engine (16-byte stores + tail).
 __global__ void k_zero_bytes(unsigned char* __restrict__ p, unsigned long long bytes) {
@@ -2492,6 +2493,8 @@ struct abs_gpu_ctx {
   int graph_failures = 0;
   bool graphs_off = false;
   // split force step (k_force_a / k_force_b): per-agent contact lists
+  unsigned long long* xcounts = nullptr;   // abs_gpu_export_layers counts (device)
+  unsigned long long* hxcounts = nullptr;  // and their page-locked host copy
   unsigned int* split_cl = nullptr;
   unsigned char* split_cn = nullptr;
   unsigned long long split_cap = 0;
@@ -3291,7 +3294,8 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->split_cl); cudaFree(c->split_cn);
+  cudaFree(c->split_cl); cudaFree(c->split_cn); cudaFree(c->xcounts);
+  if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
   if (c->ingest_part) cudaFreeHost(c->ingest_part);
@@ -3794,11 +3798,8 @@ int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
     const unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
     std::memcpy(&out7[k], &b, 8);
   }
-  const unsigned long long reset[7] = {kInfOrdLo, kInfOrdLo, kInfOrdLo, kInfOrdHi, kInfOrdHi, kInfOrdHi, kZeroOrd};
-  CK(cudaMemcpyAsync(c->g->red, reset, sizeof reset, cudaMemcpyHostToDevice, c->stream));
-  const unsigned int zero = 0;
-  CK(cudaMemcpyAsync(&c->g->nonfinite, &zero, 4, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  k_reset_reduction<<<1, 1, 0, c->stream>>>(c->g);  // a kernel: no pageable copy
+  ++c->launches;
   if (h.nonfinite) return set_err(c, ABS_ERR_NONFINITE, "agent positions are not finite");
   return ABS_OK;
 }
@@ -3843,19 +3844,21 @@ int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* di
   int rc = read_grid(c, &h);
   if (rc) return rc;
   const unsigned long long n = h.n;
-  unsigned long long* counts = nullptr;
-  CK(dalloc(&counts, 2));
-  CK(cudaMemsetAsync(counts, 0, 16, c->stream));
+  if (!c->xcounts) {  // persistent: no allocation (and its device sync) per exchange
+    CK(dalloc(&c->xcounts, 2));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hxcounts), 16, cudaHostAllocDefault));
+  }
+  unsigned long long* counts = c->xcounts;
+  k_zero_bytes<<<1, 32, 0, c->stream>>>(reinterpret_cast<unsigned char*>(counts), 16);
   if (n) {
     k_export<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(
         cur_pos(c), c->S[c->cur], c->cap, n, grid[2], grid[3], dims[2], lo, hi, halo, periodic,
         static_cast<Rec*>(out_lo), static_cast<Rec*>(out_hi), cap, counts, halo == 0 ? c->rank : nullptr);
     ++c->launches;
   }
-  unsigned long long hc[2] = {0, 0};
-  CK(cudaMemcpyAsync(hc, counts, 16, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hxcounts, counts, 16, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(counts);
+  const unsigned long long hc[2] = {c->hxcounts[0], c->hxcounts[1]};
   if (n_lo) *n_lo = hc[0];
   if (n_hi) *n_hi = hc[1];
   if (hc[0] > cap || hc[1] > cap) return set_err(c, ABS_ERR_CAPACITY, "export buffer too small");
