@@ -3809,24 +3809,24 @@ static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
   unsigned int* keep = c->rank;  // scratch: rank[] is rewritten by the next k_key
   unsigned int* idx = c->key;
   CK(cudaMemcpyAsync(idx, keep, n * 4, cudaMemcpyDeviceToDevice, c->stream));
-  unsigned long long* len = nullptr;
-  CK(dalloc(&len, 1));
-  CK(cudaMemcpyAsync(len, &n, 8, cudaMemcpyHostToDevice, c->stream));
-  unsigned int* tiles = nullptr;
-  CK(dalloc(&tiles, n / kScanTile + 2));
+  if (!c->xcounts) {
+    CK(dalloc(&c->xcounts, 2));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hxcounts), 16, cudaHostAllocDefault));
+  }
+  unsigned long long* len = c->xcounts + 1;  // persistent scratch (no allocation per call)
+  k_set_u64<<<1, 1, 0, c->stream>>>(len, n);
+  // tiles64 holds (cap + kScanTile) / kScanTile + 2 u64 words: room for the u32 tile sums of n <= cap
+  unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
   launch_scan<unsigned int>(c, idx, len, n, tiles, nullptr);  // idx[n] = survivors
   const int nxt = c->cur ^ 1;
   k_compact<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur], c->S[nxt].pd, c->S[nxt], keep,
                                                            idx, n, c->cap);
   ++c->launches;
-  unsigned int kept = 0;
-  CK(cudaMemcpyAsync(&kept, idx + n, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->hxcounts, idx + n, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(len);
-  cudaFree(tiles);
-  const unsigned long long nn = kept;
-  CK(cudaMemcpyAsync(&c->g->n, &nn, 8, cudaMemcpyHostToDevice, c->stream));
-  if (c->grid_valid) CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+  const unsigned long long nn = *reinterpret_cast<const unsigned int*>(c->hxcounts);
+  k_set_u64<<<1, 1, 0, c->stream>>>(&c->g->n, nn);
+  if (c->grid_valid) dzero(c, c->start, (c->bins_cap + 1) * 4);
   CK(cudaStreamSynchronize(c->stream));
   c->cur = nxt;
   c->pos_in_new = false;
