@@ -2419,6 +2419,39 @@ __global__ void k_remove_plan(const unsigned long long* __restrict__ slots, unsi
   }
 }
 
+// O(removed) compaction: storage order is free (the next
+// re-bin re-sorts by cell), so the survivors beyond the new end move into
+// the holes below it. idx = exclusive scan of keep; hole k of [0, new_n) is
+// the k-th removed slot there; survivor i >= new_n fills hole idx[i] - idx[new_n].
+__global__ void k_hole_list(const unsigned int* __restrict__ keep, const unsigned int* __restrict__ idx,
+                            unsigned long long new_n, unsigned int* __restrict__ holes) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < new_n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    if (!keep[i]) holes[i - idx[i]] = static_cast<unsigned int>(i);
+}
+
+__global__ void k_swap_move(Pd* pos, Soa S, const unsigned int* __restrict__ keep, const unsigned int* __restrict__ idx,
+                            const unsigned int* __restrict__ holes, unsigned long long new_n, unsigned long long n,
+                            unsigned long long cap) {
+  const unsigned int base = idx[new_n];
+  for (unsigned long long i = new_n + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    const unsigned long long dst = holes[idx[i] - base];
+    pos[dst] = load_pd(pos + i);
+    S.uid[dst] = S.uid[i];
+    S.flags[dst] = S.flags[i];
+    S.partners[dst] = S.partners[i];
+    S.beh[dst] = S.beh[i];
+    S.vol[dst] = S.vol[i];
+    S.force[dst] = S.force[i];
+    S.force[cap + dst] = S.force[cap + i];
+    S.force[2 * cap + dst] = S.force[2 * cap + i];
+    S.tag[dst] = S.tag[i];
+    S.rngc[dst] = S.rngc[i];
+  }
+}
+
 __global__ void k_remove_move(const Pd* pos_in, Pd* pos, Soa S, const unsigned long long* __restrict__ slots,
                               unsigned long long r, unsigned long long new_size,
                               const unsigned int* __restrict__ hole_rank, const unsigned int* __restrict__ to_right,
@@ -2493,6 +2526,8 @@ struct abs_gpu_ctx {
   int graph_failures = 0;
   bool graphs_off = false;
   // split force step (k_force_a / k_force_b): per-agent contact lists
+  unsigned int* holes = nullptr;           // compact_population: removed slots below the new end
+  unsigned long long holes_cap = 0;
   unsigned long long* xcounts = nullptr;   // abs_gpu_export_layers counts (device)
   unsigned long long* hxcounts = nullptr;  // and their page-locked host copy
   unsigned int* split_cl = nullptr;
@@ -3294,7 +3329,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->split_cl); cudaFree(c->split_cn); cudaFree(c->xcounts);
+  cudaFree(c->split_cl); cudaFree(c->split_cn); cudaFree(c->xcounts); cudaFree(c->holes);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -3818,18 +3853,25 @@ static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
   // tiles64 holds (cap + kScanTile) / kScanTile + 2 u64 words: room for the u32 tile sums of n <= cap
   unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
   launch_scan<unsigned int>(c, idx, len, n, tiles, nullptr);  // idx[n] = survivors
-  const int nxt = c->cur ^ 1;
-  k_compact<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur], c->S[nxt].pd, c->S[nxt], keep,
-                                                           idx, n, c->cap);
-  ++c->launches;
   CK(cudaMemcpyAsync(c->hxcounts, idx + n, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const unsigned long long nn = *reinterpret_cast<const unsigned int*>(c->hxcounts);
+  if (nn < n) {
+    if (c->holes_cap < c->cap) {
+      cudaFree(c->holes);
+      c->holes = nullptr;
+      c->holes_cap = 0;
+      CK(dalloc(&c->holes, c->cap));
+      c->holes_cap = c->cap;
+    }
+    k_hole_list<<<grid_blocks(c, nn), kThreads, 0, c->stream>>>(keep, idx, nn, c->holes);
+    k_swap_move<<<grid_blocks(c, n - nn), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur], keep,
+                                                                     idx, c->holes, nn, n, c->cap);
+    c->launches += 2;
+  }
   k_set_u64<<<1, 1, 0, c->stream>>>(&c->g->n, nn);
   if (c->grid_valid) dzero(c, c->start, (c->bins_cap + 1) * 4);
   CK(cudaStreamSynchronize(c->stream));
-  c->cur = nxt;
-  c->pos_in_new = false;
   c->grid_valid = false;
   c->n = nn;
   return ABS_OK;
