@@ -2115,26 +2115,6 @@ __global__ void k_keep_ghostless(const Soa S, unsigned long long n, unsigned int
 
 // Order-preserving stream compaction of the population by keep[] (exclusive
 // scan in `dst_index`): survivors move to S[dst] / dst_pos.
-__global__ void k_compact(const Pd* __restrict__ pos, Soa src, Pd* __restrict__ dst_pos, Soa dst,
-                          const unsigned int* __restrict__ keep, const unsigned int* __restrict__ dst_index,
-                          unsigned long long n, unsigned long long cap) {
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (!keep[i]) continue;
-    const unsigned long long j = dst_index[i];
-    dst_pos[j] = load_pd(pos + i);
-    dst.uid[j] = src.uid[i];
-    dst.flags[j] = src.flags[i];
-    dst.partners[j] = src.partners[i];
-    dst.beh[j] = src.beh[i];
-    dst.vol[j] = src.vol[i];
-    dst.force[j] = src.force[i];
-    dst.force[cap + j] = src.force[cap + i];
-    dst.force[2 * cap + j] = src.force[2 * cap + i];
-    dst.tag[j] = src.tag[i];
-    dst.rngc[j] = src.rngc[i];
-  }
-}
 
 // ------------------------------------------------------------ parity helpers
 __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* out) {
