@@ -2113,9 +2113,6 @@ __global__ void k_keep_ghostless(const Soa S, unsigned long long n, unsigned int
     keep[i] = (S.flags[i] & ABS_FLAG_GHOST) ? 0u : 1u;
 }
 
-// Order-preserving stream compaction of the population by keep[] (exclusive
-// scan in `dst_index`): survivors move to S[dst] / dst_pos.
-
 // ------------------------------------------------------------ parity helpers
 __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigned long long* out) {
   const DevGrid G = *g;
