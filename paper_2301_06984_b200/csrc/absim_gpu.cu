@@ -3242,6 +3242,10 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   // params.cpp:52-55
   if (cfg->sorting_frequency > 0 && cfg->environment != ABS_ENV_UNIFORM_GRID)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "sorting requires the uniform_grid environment");
+  if ((cfg->model == ABS_MODEL_PROLIFERATION || cfg->model == ABS_MODEL_GROW_DIVIDE) && cfg->sorting_frequency > 0)
+    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT,
+                   "a model that adds agents cannot be combined with Morton sorting: daughter uids would follow "
+                   "the reference's reordered storage, which the device does not track");
   if (cfg->model == ABS_MODEL_SIR && cfg->environment != ABS_ENV_UNIFORM_GRID)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "the periodic SIR model runs on the uniform grid");
   if (cfg->model == ABS_MODEL_GROW_DIVIDE && !(cfg->model_params[2] > 0.0))
@@ -4247,8 +4251,18 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
   return ABS_OK;
 }
 
+// Models that add agents number daughters uid_count + the parent's rank in
+// the reference's storage order (commit.cpp:186-222, one worker: creation
+// order). The device ranks parents by uid, which is that order as long as
+// storage was never reordered by a Morton sort or a removal; after either,
+// the reference's numbering follows an order the device does not track.
+const char* kReorderWithAdditions =
+    "a model that adds agents cannot be combined with Morton sorting or removals: daughter uids would "
+    "follow the reference's reordered storage, which the device does not track";
+
 int abs_gpu_sort(abs_gpu_ctx* c) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  if (adds_agents(c->cfg)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, kReorderWithAdditions);
   cudaSetDevice(c->device);
   DevGrid h{};
   int rc = read_grid(c, &h);
@@ -4270,6 +4284,7 @@ int abs_gpu_sort(abs_gpu_ctx* c) {
 int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (r == 0) return ABS_OK;
+  if (adds_agents(c->cfg)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, kReorderWithAdditions);
   DevGrid h{};
   int rc = read_grid(c, &h);
   if (rc) return rc;

@@ -89,3 +89,57 @@ def test_cohere_radius_exceeds_box(engine):
     sim.add_agents(wl.x, wl.y, wl.z, wl.d)
     with pytest.raises(ValueError, match="query radius"):
         sim.simulate(1)
+
+
+@pytest.mark.parametrize("graphs", ["1", "0"])
+def test_growdivide_static_combined(engine, oracle_mod, graphs):
+    """Divisions + static detection together, replayed through CUDA graphs or
+    launched directly: capacity and cell-table growth mid-run (device
+    rollbacks), behaviour agents listed past the static pre-pass."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = f"""
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {root!r} + "/tests")
+import paper_2301_06984_b200 as E
+from oracle import oracle as O
+from paper_2301_06984_b200 import configs as CF
+from test_reference_models import _compare
+wl = CF.ref_proliferation(216)
+prm = dict(wl.params, detect_static_agents=True)
+sim = E.Simulation(E.SimulationParams(**prm))
+sim.add_agents(wl.x, wl.y, wl.z, wl.d)
+sim.set_agent_ext(wl.tags, wl.rng_counters)
+p = O.OracleParams(seed=prm["seed"], model=prm["model"], mp=prm["model_params"], detect_static=True,
+                   fixed_box=prm.get("fixed_box_length", 0.0))
+orc = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+orc.set_tags(wl.tags)
+orc.set_rng_counters(wl.rng_counters)
+for chunk in range(4):
+    sim.simulate(4)
+    orc.simulate(4)
+    _compare(sim, orc, f"after {{4 * (chunk + 1)}}")
+    assert sim.report().force_skips == orc.counts()["force_skips"]
+assert sim.report().final_agent_count > 216
+print("OK")
+"""
+    env = dict(os.environ, ABSIM_GRAPHS=graphs)
+    r = subprocess.run([sys.executable, "-c", script], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]
+
+
+def test_additions_reject_reordering(engine):
+    """Daughter uids follow the reference's storage order (commit.cpp:186-222);
+    after a Morton sort or a removal that order is not tracked on the device,
+    so those combinations are refused instead of numbering daughters wrongly."""
+    E = engine
+    wl = CF.ref_proliferation(216)
+    with pytest.raises(ValueError, match="Morton sorting"):
+        E.Simulation(E.SimulationParams(**{**wl.params, "sorting_frequency": 3}))
+    sim = _gpu(E, wl)
+    with pytest.raises(ValueError, match="cannot be combined"):
+        sim.sort()
+    with pytest.raises(ValueError, match="cannot be combined"):
+        sim.remove_agents([0])
