@@ -468,22 +468,31 @@ __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restr
   unsigned int run = block_excl_scan(sum, &tot);
   const unsigned long long tag = static_cast<unsigned long long>(epoch & 0xFFFFFFu) << 40;
   constexpr unsigned long long kAgg = 1ull << 38, kInc = 2ull << 38, kVal = (1ull << 38) - 1;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0 looks back over 32 predecessors at a time
+    const int lane = threadIdx.x;
     unsigned long long prefix = 0;
     if (t == 0) {
-      atomicExch(&tile_state[0], tag | kInc | tot);
+      if (lane == 0) atomicExch(&tile_state[0], tag | kInc | tot);
     } else {
-      atomicExch(&tile_state[t], tag | kAgg | tot);
-      for (long long p = static_cast<long long>(t) - 1; p >= 0;) {
-        const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(&tile_state[p]);
-        if ((w & ~((1ull << 40) - 1)) != tag || !(w & (kAgg | kInc))) continue;  // not published yet
-        prefix += w & kVal;
-        if (w & kInc) break;
-        --p;
+      if (lane == 0) atomicExch(&tile_state[t], tag | kAgg | tot);
+      for (long long base = static_cast<long long>(t) - 1;;) {
+        const long long p = base - lane;  // lane 0 = nearest predecessor
+        const unsigned long long w =
+            p >= 0 ? *reinterpret_cast<volatile unsigned long long*>(&tile_state[p]) : (tag | kInc);  // before tile 0: 0
+        const bool ready = (w & ~((1ull << 40) - 1)) == tag && (w & (kAgg | kInc));
+        if (!__all_sync(0xffffffffu, ready)) continue;  // some predecessor not published yet
+        const unsigned int inc = __ballot_sync(0xffffffffu, (w & kInc) != 0);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive prefix, else the whole window
+        unsigned long long v = lane <= stop ? (w & kVal) : 0ull;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        prefix += v;
+        if (inc) break;
+        base -= 32;
       }
-      atomicExch(&tile_state[t], tag | kInc | (prefix + tot));
+      if (lane == 0) atomicExch(&tile_state[t], tag | kInc | (prefix + tot));
     }
-    s_prefix = prefix;
+    if (lane == 0) s_prefix = prefix;
   }
   __syncthreads();
   run += static_cast<unsigned int>(s_prefix);
