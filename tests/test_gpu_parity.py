@@ -13,7 +13,7 @@ import math
 import numpy as np
 import pytest
 
-from _util import assert_close, by_uid
+from _util import assert_close, by_uid, contact_cases
 from paper_2301_06984_b200 import configs as CF
 
 pytestmark = pytest.mark.gpu
@@ -328,6 +328,33 @@ def test_single_agent_and_degenerate_volume(engine):
     f0 = np.array([b["fx"][0], b["fy"][0], b["fz"][0]])
     f1 = np.array([b["fx"][1], b["fy"][1], b["fz"][1]])
     assert abs(np.linalg.norm(f0) - 20.0) < 1e-12 and np.array_equal(f0, -f1)
+
+
+@pytest.mark.parametrize("static", [False, True])
+def test_contact_boundaries_match_oracle(engine, oracle_mod, static):
+    """Exact decision boundaries (coincident, touching, d2 == r^2, box faces)
+    against the oracle: cell ids and neighbour sets bit-exact, forces and
+    positions within 1e-9, partner counts and evaluation totals exact."""
+    x, y, z, d = contact_cases()
+    prm = dict(seed=3, simulation_time_step=0.01, detect_static_agents=static)
+    sim = engine.Simulation(engine.SimulationParams(**prm))
+    sim.add_agents(x, y, z, d)
+    orc = oracle_mod.PortSim(_oparams(oracle_mod, prm), x, y, z, d)
+    compare_env(sim, orc, "contacts t=0")
+    env = sim.environment()
+    assert env.box_length() == 14.0
+    for step in range(4):
+        teacher_force(sim, orc)
+        compare_env(sim, orc, f"contacts tf step {step}")
+        e0 = orc.counts()["force_evaluations"]
+        sim.simulate(1)
+        orc.simulate(1)
+        compare_state(sim.agents(), orc.dump(), what=f"contacts step {step}")
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"] - e0
+    # the touching pairs stay put with zero force, the coincident ones separate
+    g = by_uid(sim.agents())
+    f = np.sqrt(g["fx"] ** 2 + g["fy"] ** 2 + g["fz"] ** 2)
+    assert np.all(f[8:16] == 0.0) and np.all(f[0:8] > 0.0)
 
 
 def test_errors(engine):

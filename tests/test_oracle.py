@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2301_06984_b200 import configs as CF
-from _util import by_uid
+from _util import by_uid, contact_cases
 
 FIELDS = ["uid", "x", "y", "z", "d", "fx", "fy", "fz", "partners", "flags", "volume"]
 
@@ -61,6 +61,37 @@ def test_port_bitwise_equals_reference(oracle_mod, have_ref, case):
     ref.simulate(steps)
     port.simulate(steps)
     _bitwise(ref, port)
+
+
+@pytest.mark.parametrize("static", [False, True])
+def test_port_contact_boundaries_equal_reference(oracle_mod, have_ref, static):
+    """Exact decision boundaries (coincident centres, touching pairs,
+    d2 == r^2, agents on box faces; tests/_util.py:contact_cases): the port
+    reproduces the reference bit for bit, so the GPU test of the same cases
+    (test_gpu_parity.py) is pinned to the reference through it."""
+    O = oracle_mod
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    x, y, z, d = contact_cases()
+    p = O.OracleParams(seed=3, dt=0.01, detect_static=static, model=0, mp=[0.0] * 8,
+                       sorting_frequency=0, threshold=0.0, fixed_box=0.0)
+    ref = O.RefSim(p, x, y, z, d)
+    port = O.PortSim(p, x, y, z, d)
+    g1, g2 = ref.env_update(), port.env_update()
+    for k in ("origin", "box", "dmax", "dims", "indexed"):
+        assert np.array_equal(np.asarray(g1[k]), np.asarray(g2[k])), k
+    assert np.array_equal(ref.cell_ids(), port.cell_ids())
+    o1, u1 = ref.neighbors()
+    o2, u2 = port.neighbors()
+    assert np.array_equal(o1, o2) and np.array_equal(u1, u2)
+    ref.simulate(4)
+    port.simulate(4)
+    _bitwise(ref, port)
+    c = port.counts()
+    if static:  # the zero-force pairs (touching, d2 == r^2, past r) settle and are skipped
+        assert c["force_skips"] > 0
+    else:  # 44 evaluations per step: 2 per pair, 1 for the past-r pair (only its d = 14 side sees it)
+        assert c["force_evaluations"] == 4 * 44 and c["force_skips"] == 0
 
 
 def test_port_sort_equals_reference(oracle_mod, have_ref):
