@@ -473,6 +473,32 @@ def test_removal_large_unordered(engine, oracle_mod):
         sim.remove_agents([int(sim.agents()["uid"][0])] * 2)
 
 
+@pytest.mark.parametrize("k,max_disp,threshold", [(5.0, 0.5, 0.0), (2.0, 3.0, 4.0), (0.5, 0.05, 1.0)])
+def test_mechanics_parameters(engine, oracle_mod, k, max_disp, threshold):
+    """Non-default repulsion_coefficient, max_displacement (the clamp of
+    agent.hpp:115-133 active for most agents at dt 0.1) and force_threshold
+    (simulation.cpp:485-487: forces at or below it do not move the agent)
+    against the oracle, teacher-forced one step at a time."""
+    wl = CF.c1_relaxation(3000, seed=11)
+    prm = dict(seed=11, simulation_time_step=0.1, repulsion_coefficient=k,
+               max_displacement=max_disp, force_threshold=threshold)
+    sim = engine.Simulation(engine.SimulationParams(**prm))
+    sim.add_agents(wl.x, wl.y, wl.z, wl.d)
+    op = oracle_mod.OracleParams(seed=11, dt=0.1, k=k, max_disp=max_disp, threshold=threshold)
+    orc = oracle_mod.PortSim(op, wl.x, wl.y, wl.z, wl.d)
+    x0 = by_uid(orc.dump())
+    for step in range(3):
+        teacher_force(sim, orc)
+        e0 = orc.counts()["force_evaluations"]
+        sim.simulate(1)
+        orc.simulate(1)
+        compare_state(sim.agents(), orc.dump(), what=f"k={k} max={max_disp} thr={threshold} step {step}")
+        assert sim.report().force_evaluations == orc.counts()["force_evaluations"] - e0
+    g = by_uid(sim.agents())
+    moved = np.sqrt((g["x"] - x0["x"]) ** 2 + (g["y"] - x0["y"]) ** 2 + (g["z"] - x0["z"]) ** 2)
+    assert moved.max() <= 3 * max_disp * (1 + 1e-12)
+
+
 def test_grid_growth_retry(engine, oracle_mod):
     """Agents spreading far beyond the initial grid force a bin-table regrow
     (device-side retry) without changing results."""

@@ -94,6 +94,22 @@ def test_port_contact_boundaries_equal_reference(oracle_mod, have_ref, static):
         assert c["force_evaluations"] == 4 * 44 and c["force_skips"] == 0
 
 
+@pytest.mark.parametrize("k,max_disp,threshold", [(5.0, 0.5, 0.0), (2.0, 3.0, 4.0), (0.5, 0.05, 1.0)])
+def test_port_mechanics_parameters_equal_reference(oracle_mod, have_ref, k, max_disp, threshold):
+    """repulsion_coefficient / max_displacement / force_threshold away from
+    their defaults (params.hpp:17-52): port == reference bit for bit."""
+    O = oracle_mod
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    wl = CF.c1_relaxation(3000, seed=11)
+    p = O.OracleParams(seed=11, dt=0.1, k=k, max_disp=max_disp, threshold=threshold)
+    ref = O.RefSim(p, wl.x, wl.y, wl.z, wl.d)
+    port = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+    ref.simulate(3)
+    port.simulate(3)
+    _bitwise(ref, port)
+
+
 def test_port_sort_equals_reference(oracle_mod, have_ref):
     O = oracle_mod
     if not have_ref:
