@@ -41,6 +41,12 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+# initial population of each config at its default size (what the GPU arm's
+# config reports as agents_per_gpu), without generating it
+FULL_AGENTS = {"c1": 131_072, "c2": 16 ** 3, "c3": 1 << 23, "c4": 1 << 26, "c5": 10_000_000,
+               "rclust": 1 << 22, "rprolif": 32768}
+
+
 def _workload(name, n=None, seed=0):
     from paper_2301_06984_b200 import configs as CF
     if name == "c1":
@@ -178,6 +184,7 @@ def run_reference(args):
     brute = args.env != "uniform_grid"
     sim, kind, cores, wl = _ref_sim(args.config, BRUTE_SAMPLE if brute else CPU_SAMPLE[args.config], threads,
                                     args.env)
+    full_n = int(args.n or FULL_AGENTS.get(args.config, wl.n))
     for _ in range(args.warmup):
         sim.simulate(1)
     agent_its = 0
@@ -190,7 +197,11 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": wl.name, "sample_agents": wl.n, "environment": args.env},
+            "data": "synthetic",
+            # the same workload keys as the GPU arm's line, plus the bounded sample actually timed
+            "config": {"workload": wl.name, "agents_per_gpu": full_n, "global_agents": full_n * args.gpus,
+                       "parallelism": "single" if args.gpus == 1 else f"reference on rank 0 of {args.gpus}",
+                       "environment": args.env, "sample_agents": wl.n},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": f"{wl.name} shape at {wl.n} agents, {args.steps} timed iterations"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
