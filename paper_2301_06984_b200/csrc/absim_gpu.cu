@@ -32,13 +32,9 @@ using namespace absgpu;
 
 namespace {
 
-#ifndef ABS_FORCE_MIN_BLOCKS
-#define ABS_FORCE_MIN_BLOCKS 4
-#endif
 #ifndef ABS_FORCE_MIN_BLOCKS_F32
 #define ABS_FORCE_MIN_BLOCKS_F32 5
 #endif
-constexpr int kForceMinBlocks = ABS_FORCE_MIN_BLOCKS;
 #ifndef ABS_PASSB
 #define ABS_PASSB 1  // 2 or 4 measured slower (c4 @ 2^24: 6.27 / 6.38 / 6.56 ms)
 #endif
@@ -714,16 +710,10 @@ struct NoQuery {
 // index). `walk(r, r2, visit)` enumerates every candidate j != i with exact
 // fp64 d2 <= r2 in a fixed order; `fetch(j)` returns candidate j's Pd;
 // `uid_of(j)` its uid. `ovl` is this thread's column of the contact list.
-// LPA > 1: the LPA lanes of an aligned group run this together for the same
-// agent — every lane walks its share of the candidates (the walk deals them
-// out), the partial forces / partner counts are combined with a butterfly
-// (commutative pairwise adds: every lane ends with the same bits, and the
-// result is a fixed function of the storage order), and only the group's
-// leader lane writes agent state. All other decisions are group-uniform.
 // F32: `walk` is the fp32-classified walker (visit(j, df2, qd) for exactly
 // the candidates with fp64 d2 <= r^2); the contact record test is then the
 // conservative fp32 superset df2 < (h + slack)^2 (pass B decides exactly).
-template <int MODEL, bool STATIC, bool RECORD, int LPA = 1, bool F32 = false, class OvlT, class Walk, class Fetch,
+template <int MODEL, bool STATIC, bool RECORD, bool F32 = false, class OvlT, class Walk, class Fetch,
           class UidOf, class Query = NoQuery>
 __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, unsigned long long i, const Pd& me,
                                                double dmax, unsigned char* __restrict__ nv,
@@ -733,12 +723,11 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
                                                Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f,
                                                const Query& query = Query{}) {
   Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u};
-  const bool leader = LPA == 1 || (threadIdx.x & (LPA - 1)) == 0;
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
   dg.parent = my_uid;
   if (fl & kFlagGhost) {  // halo copy of another rank's agent: candidate only
-    if (leader) {
+    {
       if (STATIC) {
         nv[i] = 0;
         nn[i] = 0;
@@ -749,8 +738,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     return dg;
   }
   // --- staticness phase 2 (simulation.cpp:375-384) -----------------------
-  // (the nv / nn resets and the volume update are written at the end, by the
-  // leader, after every lane of the group has read them)
+  // (the nv / nn resets and the volume update are written at the end)
   if (STATIC) {
     if (a.iteration == 0) {
       fl = 0;  // :335-349 everyone participates, flags wiped
@@ -780,7 +768,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         dg.z = me.z + dir[2] * half;
         dg.d = abs_diameter_of_volume(v);
         dg.vol = v;
-        dg.divides = leader;
+        dg.divides = true;
       }
       new_vol = v;
       vol_changed = true;
@@ -810,7 +798,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         dg.d = a.mp[2];
         dg.vol = 0.0;
         dg.tag = S.tag[i];  // daughter.set_tag(a.tag())
-        dg.divides = leader;
+        dg.divides = true;
         tg += a.mp[2] - me.d;
       } else {
         tg += a.mp[0];
@@ -852,7 +840,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
   unsigned int contributors = 0;
   double fx = 0.0, fy = 0.0, fz = 0.0;
   if (STATIC && (fl & ABS_FLAG_STATIC)) {
-    if (leader) ++n_skip;
+    ++n_skip;
   } else {
     const double r = 0.5 * (me.d + dmax);
     unsigned int evals = 0, nov = 0;
@@ -904,7 +892,6 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     };
     auto contact = [&](unsigned int j) { contact_q(j, fetch(j)); };
     bool overflow = nov > kMaxContacts;
-    if (LPA > 1) overflow = (__ballot_sync(group_mask<LPA>(), overflow) & group_mask<LPA>()) != 0u;
 #if defined(ABS_ABLATE) && ABS_ABLATE >= 2
     if (nov > 1000000u) overflow = false;  // timing ablation: no pass B
     else nov = 0;
@@ -935,16 +922,6 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         if (d2 < h * h * (1.0 + 0x1.0p-50)) contact(j);
       });
     }
-    if (LPA > 1) {
-      const unsigned int gm = group_mask<LPA>();
-#pragma unroll
-      for (int off = LPA / 2; off; off >>= 1) {
-        fx += __shfl_xor_sync(gm, fx, off, LPA);
-        fy += __shfl_xor_sync(gm, fy, off, LPA);
-        fz += __shfl_xor_sync(gm, fz, off, LPA);
-        contributors += __shfl_xor_sync(gm, contributors, off, LPA);
-      }
-    }
     wrote_partners = true;
     if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
       tx += fx * a.dt;
@@ -972,7 +949,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     np.d = nd > 1e-9 ? nd : 1e-9;
     if (tg > 0.0) fl |= ABS_FLAG_GREW;
   }
-  if (leader) {
+  {
     if (STATIC && a.iteration != 0) {
       nv[i] = 0;
       nn[i] = 0;
@@ -1082,17 +1059,14 @@ __global__ void __launch_bounds__(kThreads) k_static_pass(Soa S, Pd* __restrict_
   if (lane == 0 && skips) atomicAdd(&g->skips, skips);
 }
 
-// Global-gather force kernel: one agent per thread, candidates fetched from
-// HBM/L2 through the per-lane flat window stream. Used for small tiles'
-// overflow and as the reference implementation of the tiled kernel below.
+// Force sweep: one agent per thread, candidates fetched from HBM/L2.
 // Resident CTAs per SM the register budget is sized for (c4 @ 2^24 sweep:
 // fp32 walk 5 -> 6.27 ms vs 2 -> 6.96 ms; box mode c3 4 -> 0.68 vs 2 -> 0.77).
-// WALK: 0 flat fp64 walk, 1 fp32-classified flat walk, 2 box-lockstep walk
-// (bins == boxes, decided on the host; 0/1 also fall back to it when the
-// device grid has no sub-bins).
+// WALK: 1 fp32-classified flat window walk (sub-binned grids; falls back to
+// the box walk when the device grid has no sub-bins), 2 box-lockstep walk
+// (bins == boxes, decided on the host).
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
-__global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
-                                                           : (WALK == 1 ? kForceMinBlocksF32 : kForceMinBlocks))
+__global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox : kForceMinBlocksF32)
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
@@ -1103,11 +1077,10 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
   extern __shared__ __align__(16) unsigned int force_smem[];
   constexpr bool F32 = WALK == 1;
   auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
-  auto wj1 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
   // fp32 walk: 16-bit stream bounds, so its contact lists start after 1.5 row arrays
   auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
   auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(
-      force_smem + (WALK == 2 ? 0 : (WALK == 1 ? kMaxRows + kMaxRows / 2 : 2 * kMaxRows)) * kForceThreads);
+      force_smem + (WALK == 2 ? 0 : kMaxRows + kMaxRows / 2) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
   if (MODEL == ABS_MODEL_COHERE && !a.brute && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
@@ -1146,7 +1119,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
                           [&](unsigned int j, const Pd& q, double, double, double, double) { v(j, q); });
       };
       if (F32 && !box_mode) {
-        dg = agent_step<MODEL, STATIC, RECORD, 1, true>(
+        dg = agent_step<MODEL, STATIC, RECORD, true>(
             S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
             [&](double r, double r2, auto&& visit) {
               for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wb16, self, me.x, me.y, me.z, r, r2, visit);
@@ -1157,526 +1130,16 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
           [&](double r, double r2, auto&& visit) {
-            if (box_mode) {
-              for_each_neighbor_box(Q, S.pd, start, self, me.x, me.y, me.z, r2,
-                                    [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                                      visit(j, q, d2);
-                                    });
-            } else {
-              for_each_neighbor_flat(Q, S.pd, pf, start, wj0, wj1, self, me.x, me.y, me.z, r, r2,
-                                     [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                                       visit(j, q, d2);
-                                     });
-            }
+            for_each_neighbor_box(Q, S.pd, start, self, me.x, me.y, me.z, r2,
+                                  [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                                    visit(j, q, d2);
+                                  });
           },
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, 0.0f,
           query);
     }
     if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
       stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
-  }
-  flush_counters(n_eval, n_skip, gw);
-}
-
-// ------------------------------------------------------------ split force step
-// Config-4 path (no behaviours, no static detection, fp32-classified walk)
-// as two kernels: k_force_a walks the candidates (evaluation count + contact
-// superset, exactly pass A of agent_step) and writes each agent's contacts to
-// a global list; k_force_b runs pairwise_repulsion on them and integrates
-// (pass B + apply_pending). The walk kernel carries no fp64 force state, so it
-// keeps more warps resident; agents with more than kSplitContacts contacts are
-// listed and re-run through k_force (work list) instead.
-#ifndef ABS_SPLIT_MIN_BLOCKS
-#define ABS_SPLIT_MIN_BLOCKS 6
-#endif
-constexpr int kSplitContacts = 16;
-constexpr unsigned char kSplitOverflow = 0xFF;
-
-__global__ void __launch_bounds__(kForceThreads, ABS_SPLIT_MIN_BLOCKS)
-    k_force_a(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, DevGrid* g,
-              const unsigned int* __restrict__ start, unsigned int* __restrict__ cl, unsigned char* __restrict__ cn,
-              unsigned long long cap, unsigned int* __restrict__ overflow) {
-  if (g->err) return;
-  __shared__ QGrid Q;
-  extern __shared__ __align__(16) unsigned int force_smem[];
-  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
-  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
-  if (threadIdx.x == 0) Q = make_qgrid(*g);
-  __syncthreads();
-  const unsigned long long n = g->n;
-  const double dmax = g->dmax;
-  const int lane = threadIdx.x & 31;
-  unsigned long long n_eval = 0;
-  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
-  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
-    const unsigned long long base = chunk * 32ull;
-    if (base >= n) break;
-    const unsigned long long i = base + lane;
-    bool over = false;
-    if (i < n) {
-      const Pd me = load_pd(S.pd + i);
-      if (S.flags[i] & kFlagGhost) {  // candidate only (agent_step's ghost branch)
-        reinterpret_cast<double2*>(out + i)[0] = make_double2(me.x, me.y);
-        reinterpret_cast<double2*>(out + i)[1] = make_double2(me.z, me.d);
-        cn[i] = 0;
-      } else {
-        const double r = 0.5 * (me.d + dmax);
-        const float hme = 0.5f * static_cast<float>(me.d) + Q.slack;
-        unsigned int evals = 0, nov = 0;
-        for_each_neighbor_flat32(Q, S.pd, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, r,
-                                 r * r, [&](unsigned int j, float df2, float qd, bool in) {
-                                   evals += in;
-                                   const float hp = __fmaf_rn(0.5f, qd, hme);
-                                   const bool ct = in && df2 < hp * hp * 1.0000005f;
-                                   if (ct && nov < kSplitContacts) cl[nov * cap + i] = j;
-                                   nov += ct;
-                                 });
-        over = nov > kSplitContacts;
-        if (!over) n_eval += evals;  // an overflowing agent is counted by the full sweep
-        cn[i] = over ? kSplitOverflow : static_cast<unsigned char>(nov);
-      }
-    }
-    const unsigned int ballot = __ballot_sync(0xffffffffu, over);
-    if (ballot) {  // rare: listed for the full kernel
-      unsigned long long b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&g->work_n, (unsigned long long)__popc(ballot));
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if (over) overflow[b0 + __popc(ballot & ((1u << lane) - 1u))] = static_cast<unsigned int>(i);
-    }
-  }
-  flush_counters(n_eval, 0ull, g);
-}
-
-template <bool RECORD>
-__global__ void __launch_bounds__(kThreads) k_force_b(Soa S, Pd* __restrict__ out, const DevGrid* g, StepArgs a,
-                                                      const unsigned int* __restrict__ cl,
-                                                      const unsigned char* __restrict__ cn, unsigned long long cap) {
-  if (g->err) return;
-  const unsigned long long n = g->n;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned char c = cn[i];
-    if (c == kSplitOverflow) continue;
-    unsigned char fl = S.flags[i];
-    if (fl & kFlagGhost) continue;
-    const Pd me = load_pd(S.pd + i);
-    const double k = a.k;
-    unsigned int contributors = 0;
-    double fx = 0.0, fy = 0.0, fz = 0.0;
-    for (unsigned int s = 0; s < c; ++s) {
-      const unsigned int j = cl[s * cap + i];
-      const Pd q = load_pd(S.pd + j);
-      const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-      // pairwise_repulsion (mechanics.cpp:10-27), as agent_step's pass B
-      const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
-      const double overlap = 0.5 * (me.d + q.d) - dist;
-      if (overlap <= 0.0) continue;
-      double f0, f1, f2;
-      if (dist > 0.0) {
-        const double sc = k * overlap / dist;
-        f0 = dx * sc;
-        f1 = dy * sc;
-        f2 = dz * sc;
-      } else {
-        coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
-      }
-      if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
-        ++contributors;
-        fx += f0;
-        fy += f1;
-        fz += f2;
-      }
-    }
-    double tx = 0.0, ty = 0.0, tz = 0.0;
-    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
-      tx = fx * a.dt;
-      ty = fy * a.dt;
-      tz = fz * a.dt;
-    }
-    // apply_pending (agent.hpp:115-133)
-    Pd np = me;
-    const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
-    if (disp > 0.0) {
-      if (disp > a.max_disp) {
-        const double sc = a.max_disp / disp;
-        tx *= sc;
-        ty *= sc;
-        tz *= sc;
-      }
-      np.x = me.x + tx;
-      np.y = me.y + ty;
-      np.z = me.z + tz;
-      fl |= ABS_FLAG_MOVED;
-    }
-    if (RECORD) {
-      S.force[i] = fx;
-      S.force[cap + i] = fy;
-      S.force[2 * cap + i] = fz;
-    }
-    S.partners[i] = contributors;
-    reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
-    reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
-    S.flags[i] = fl;
-  }
-}
-
-// Group-cooperative force kernel: LPA lanes per agent (for_each_neighbor_group).
-// A warp runs 32 / LPA consecutive agents (cell order) at a time; candidate
-// loads of a group are consecutive records of one bin row, so a warp load
-// touches ~32/LPA row segments instead of 32 unrelated lines (the per-lane
-// kernel above is L1-wavefront bound on exactly that). Persistent warps
-// sweep the agent array in a static warp-strided order, as in k_force.
-template <int MODEL, bool STATIC, bool RECORD, int LPA>
-__global__ void __launch_bounds__(kForceThreads, kForceMinBlocks)
-    k_force_g(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
-              unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
-              unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-              unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
-  if (gp->err) return;
-  __shared__ QGrid Q;
-  __shared__ unsigned int rows[kForceThreads / LPA][kGroupRowWords];
-  __shared__ unsigned int ovl[kMaxContacts][kForceThreads];
-  if (threadIdx.x == 0) Q = make_qgrid(*gp);
-  __syncthreads();
-  const unsigned long long n = gp->n;
-  const double dmax = gp->dmax;
-  constexpr int G = 32 / LPA;  // agents per warp per sweep step
-  unsigned long long n_eval = 0, n_skip = 0;
-  const int lane = threadIdx.x & 31;
-  unsigned int* my_rows = rows[threadIdx.x / LPA];
-  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
-  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
-    const unsigned long long base = chunk * G;
-    if (base >= n) break;
-    const unsigned long long i = base + lane / LPA;
-    Daughter dg{false, 0, 0, 0, 0, 0, 0};
-    if (i < n) {  // group-uniform
-      const Pd me = load_pd(S.pd + i);
-      const unsigned int self = static_cast<unsigned int>(i);
-      dg = agent_step<MODEL, STATIC, RECORD, LPA>(
-          S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
-          [&](double r, double r2, auto&& visit) {
-            for_each_neighbor_group<LPA>(Q, S.pd, start, my_rows, self, me.x, me.y, me.z, r, r2,
-                                         [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                                           visit(j, q, d2);
-                                         });
-          },
-          [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
-    }
-    if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
-      stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
-  }
-  flush_counters(n_eval, n_skip, gw);
-}
-
-// ------------------------------------------------------------ tiled force
-// One persistent CTA per SM walks tiles of kTB^3 reference boxes. For each
-// tile it stages the tile's halo — exactly the reference's 3x3x3-box
-// neighbourhood of every box in the tile (uniform_grid.cpp:199-201) — into
-// shared memory with one TMA bulk copy (cp.async.bulk) per bin row (a row
-// of the cell-ordered arrays is one contiguous byte range), builds a local
-// cell table, and then runs the same per-agent step as k_force with every
-// candidate read from shared memory. Tiles whose halo exceeds the staging
-// capacity fall back to the global walk.
-constexpr int kTileThreads = 512;
-constexpr int kTB = 4;                        // tile edge in reference boxes
-constexpr int kTileCap = 4096;                // staged agents per tile
-constexpr int kTileWinRows = 24;              // stored windows per query
-constexpr int kTileMaxHaloRows = 144;         // ((kTB + 2) * 2)^2 for B <= 2
-constexpr int kTileMaxHaloX = (kTB + 2) * 2 + 1;
-constexpr int kTileMaxCoreRows = (kTB * 2) * (kTB * 2);
-
-struct TileSmem {
-  Pd sp[kTileCap];
-  unsigned int lst[kTileMaxHaloRows][kTileMaxHaloX];  // local start of each halo bin (+ end)
-  unsigned int lrow[kTileMaxHaloRows + 1];            // local start of each halo row
-  unsigned int rowg0[kTileMaxHaloRows];               // global index of each row's first agent
-  unsigned int qpre[kTileMaxCoreRows + 1];            // query prefix over core rows
-  unsigned short qrow[kTileMaxCoreRows];              // halo row of each core row
-  unsigned short qoff[kTileMaxCoreRows];              // local bin offset of the core x range
-  unsigned short wj0[kTileWinRows][kTileThreads];
-  unsigned short wj1[kTileWinRows][kTileThreads];
-  unsigned short ovl[kMaxContacts][kTileThreads];
-  unsigned int ovl32[1];
-  unsigned long long bar;
-  int hx0, hx1, hy0, hy1, hz0, hz1, nhx, nhy, nrows, ncore, total, overflow;
-};
-
-__device__ __forceinline__ unsigned int smem_u32(const void* p) {
-  return static_cast<unsigned int>(__cvta_generic_to_shared(p));
-}
-
-template <int MODEL, bool STATIC, bool RECORD>
-__global__ void __launch_bounds__(kTileThreads, 1)
-    k_force_tile(Soa S, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
-                 unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
-                 unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
-                 unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag) {
-  if (gp->err) return;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileSmem& T = *reinterpret_cast<TileSmem*>(smem_raw);
-  __shared__ QGrid Q;
-  __shared__ DevGrid G;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    G = *gp;
-    Q = make_qgrid(G);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const double dmax = G.dmax;
-  const unsigned int Bx = G.B[0], By = G.B[1], Bz = G.B[2];
-  const unsigned int ntx = (G.dims[0] + kTB - 1) / kTB, nty = (G.dims[1] + kTB - 1) / kTB,
-                     ntz = (G.dims[2] + kTB - 1) / kTB;
-  const unsigned long long ntiles = (unsigned long long)ntx * nty * ntz;
-  unsigned long long n_eval = 0, n_skip = 0;
-  unsigned int phase = 0;
-  for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // ---- tile geometry (boxes -> bins) ---------------------------------
-    if (tid == 0) {
-      const unsigned int tx = tile % ntx, ty = (tile / ntx) % nty, tz = tile / ((unsigned long long)ntx * nty);
-      const int bx0 = tx * kTB, by0 = ty * kTB, bz0 = tz * kTB;
-      T.hx0 = max(bx0 - 1, 0) * Bx;
-      T.hx1 = min(bx0 + kTB + 1, (int)G.dims[0]) * Bx;
-      T.hy0 = max(by0 - 1, 0) * By;
-      T.hy1 = min(by0 + kTB + 1, (int)G.dims[1]) * By;
-      T.hz0 = max(bz0 - 1, 0) * Bz;
-      T.hz1 = min(bz0 + kTB + 1, (int)G.dims[2]) * Bz;
-      T.nhx = T.hx1 - T.hx0;
-      T.nhy = T.hy1 - T.hy0;
-      T.nrows = T.nhy * (T.hz1 - T.hz0);
-      // core rows/bins
-      const int cy0 = by0 * By, cy1 = min(by0 + kTB, (int)G.dims[1]) * By;
-      const int cz0 = bz0 * Bz, cz1 = min(bz0 + kTB, (int)G.dims[2]) * Bz;
-      int nc = 0;
-      for (int bz = cz0; bz < cz1; ++bz)
-        for (int by = cy0; by < cy1; ++by) {
-          T.qrow[nc] = static_cast<unsigned short>((bz - T.hz0) * T.nhy + (by - T.hy0));
-          ++nc;
-        }
-      T.ncore = nc;
-      T.qoff[0] = static_cast<unsigned short>(bx0 * Bx - T.hx0);
-      T.qoff[1] = static_cast<unsigned short>(min(bx0 + kTB, (int)G.dims[0]) * Bx - T.hx0);
-    }
-    __syncthreads();
-    const int nrows = T.nrows, nhx = T.nhx, nhy = T.nhy;
-    // ---- halo cell table: global bin starts -> local offsets ------------
-    for (int idx = tid; idx < nrows * (nhx + 1); idx += kTileThreads) {
-      const int r = idx / (nhx + 1), e = idx % (nhx + 1);
-      const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-      const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
-      T.lst[r][e] = __ldg(start + row + T.hx0 + e);
-    }
-    __syncthreads();
-    if (tid < 32) {  // row lengths -> exclusive scan (one warp)
-      unsigned int carry = 0;
-      for (int r0 = 0; r0 < nrows; r0 += 32) {
-        const int r = r0 + tid;
-        const unsigned int len = r < nrows ? T.lst[r][nhx] - T.lst[r][0] : 0;
-        const unsigned int inc = warp_incl_scan(len);
-        if (r < nrows) {
-          T.lrow[r] = carry + inc - len;
-          T.rowg0[r] = T.lst[r][0];
-        }
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      if (tid == 0) {
-        T.lrow[nrows] = carry;
-        T.total = carry;
-        T.overflow = carry > kTileCap;
-      }
-    }
-    __syncthreads();
-    const bool overflow = T.overflow;
-    if (!overflow) {
-      for (int idx = tid; idx < nrows * (nhx + 1); idx += kTileThreads) {
-        const int r = idx / (nhx + 1), e = idx % (nhx + 1);
-        T.lst[r][e] = T.lst[r][e] - T.rowg0[r] + T.lrow[r];
-      }
-      // ---- TMA: one bulk copy per non-empty halo row ------------------
-      if (tid == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&T.bar)),
-                     "r"(T.total * (unsigned int)sizeof(Pd))
-                     : "memory");
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncthreads();
-      for (int r = tid; r < nrows; r += kTileThreads) {
-        const unsigned int len = T.lrow[r + 1] - T.lrow[r];
-        if (len) {
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(&T.sp[T.lrow[r]])),
-              "l"(S.pd + T.rowg0[r]), "r"(len * (unsigned int)sizeof(Pd)), "r"(smem_u32(&T.bar))
-              : "memory");
-        }
-      }
-    }
-    // query prefix over core rows (local ranges)
-    if (tid < 32) {
-      unsigned int carry = 0;
-      for (int c0 = 0; c0 < T.ncore; c0 += 32) {
-        const int cr = c0 + tid;
-        unsigned int len = 0;
-        if (cr < T.ncore) {
-          const int r = T.qrow[cr];
-          len = overflow ? 0 : T.lst[r][T.qoff[1]] - T.lst[r][T.qoff[0]];
-          if (overflow) {  // global indices: recompute from start[]
-            const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-            const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
-            len = __ldg(start + row + T.hx0 + T.qoff[1]) - __ldg(start + row + T.hx0 + T.qoff[0]);
-          }
-        }
-        const unsigned int inc = warp_incl_scan(len);
-        if (cr < T.ncore) T.qpre[cr] = carry + inc - len;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      if (tid == 0) T.qpre[T.ncore] = carry;
-    }
-    __syncthreads();
-    if (!overflow) {  // wait for the staged halo
-      const unsigned int bar = smem_u32(&T.bar);
-      unsigned int done = 0;
-      while (!done) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(bar), "r"(phase)
-            : "memory");
-      }
-      phase ^= 1u;
-    }
-    // ---- queries ---------------------------------------------------------
-    const unsigned int nq = T.qpre[T.ncore];
-    for (unsigned int q0 = 0; q0 < nq; q0 += kTileThreads) {
-      const unsigned int q = q0 + tid;
-      Daughter dg{false, 0, 0, 0, 0, 0, 0};
-      if (q < nq) {
-        int lo = 0, hi = T.ncore - 1;  // core row holding query q
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (T.qpre[mid] <= q) lo = mid;
-          else hi = mid - 1;
-        }
-        const int r = T.qrow[lo];
-        const unsigned int off = q - T.qpre[lo];
-        unsigned long long gi;
-        unsigned int li = 0;
-        if (!overflow) {
-          li = T.lst[r][T.qoff[0]] + off;
-          gi = T.rowg0[r] + (li - T.lrow[r]);
-        } else {
-          const unsigned int by = T.hy0 + r % nhy, bz = T.hz0 + r / nhy;
-          const unsigned int row = G.bd[0] * row_of(by, bz, G.ysh, G.bd[2]);
-          gi = __ldg(start + row + T.hx0 + T.qoff[0]) + off;
-        }
-        const Pd me = overflow ? load_pd(S.pd + gi) : T.sp[li];
-        if (!overflow) {
-          dg = agent_step<MODEL, STATIC, RECORD>(
-              S, out, gi, me, dmax, nv, nn, a, cap, &T.ovl[0][tid], kTileThreads, n_eval, n_skip,
-              [&](double rr, double r2, auto&& visit) {
-                const float fx = static_cast<float>(me.x - Q.ox);
-                const float fy = static_cast<float>(me.y - Q.oy);
-                const float fz = static_cast<float>(me.z - Q.oz);
-                const float rf = static_cast<float>(rr) * 1.000001f + Q.slack;
-                const float rf2 = rf * rf;
-                int bl[3], bh[3];
-                box_bin_range(Q, me.x, me.y, me.z, bl, bh);
-                const int z0 = max(fbin(fz - rf, Q.inv_s[2], Q.bd[2]), max(T.hz0, bl[2]));
-                const int z1 = min(fbin(fz + rf, Q.inv_s[2], Q.bd[2]), min(T.hz1 - 1, bh[2]));
-                const int y0 = max(fbin(fy - rf, Q.inv_s[1], Q.bd[1]), max(T.hy0, bl[1]));
-                const int y1 = min(fbin(fy + rf, Q.inv_s[1], Q.bd[1]), min(T.hy1 - 1, bh[1]));
-                int nw = 0;
-                for (int bz = z0; bz <= z1; ++bz) {
-                  const float zl = static_cast<float>(bz) * Q.s[2];
-                  const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + Q.s[2])), 0.0f);
-                  for (int by = y0; by <= y1; ++by) {
-                    const float yl = static_cast<float>(by) * Q.s[1];
-                    const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + Q.s[1])), 0.0f);
-                    const float rem = rf2 - (gy * gy + gz * gz);
-                    if (rem < 0.0f) continue;
-                    const float w = sqrtf(rem);
-                    const int x0 = max(fbin(fx - w, Q.inv_s[0], Q.bd[0]), max(T.hx0, bl[0])) - T.hx0;
-                    const int x1 = min(fbin(fx + w, Q.inv_s[0], Q.bd[0]), min(T.hx1 - 1, bh[0])) - T.hx0;
-                    const int hr = (bz - T.hz0) * nhy + (by - T.hy0);
-                    const unsigned int j0 = T.lst[hr][x0], j1 = T.lst[hr][x1 + 1];
-                    if (j1 <= j0) continue;
-                    if (nw < kTileWinRows) {
-                      T.wj0[nw][tid] = static_cast<unsigned short>(j0);
-                      T.wj1[nw][tid] = static_cast<unsigned short>(j1);
-                      ++nw;
-                    } else {
-                      for (unsigned int j = j0; j < j1; ++j) {
-                        if (j == li) continue;
-                        const Pd c = T.sp[j];
-                        const double dx = me.x - c.x, dy = me.y - c.y, dz = me.z - c.z;
-                        const double d2 = (dx * dx + dy * dy) + dz * dz;
-                        if (d2 <= r2) visit(j, c, d2);
-                      }
-                    }
-                  }
-                }
-                if (nw == 0) return;
-                int k = 0;
-                unsigned int j = T.wj0[0][tid], je = T.wj1[0][tid];
-                while (k < nw) {
-                  unsigned int idx[kBatch];
-#pragma unroll
-                  for (int u = 0; u < kBatch; ++u) {
-                    idx[u] = li;
-                    if (k < nw) {
-                      idx[u] = j;
-                      if (++j == je && ++k < nw) {
-                        j = T.wj0[k][tid];
-                        je = T.wj1[k][tid];
-                      }
-                    }
-                  }
-                  Pd c[kBatch];
-#pragma unroll
-                  for (int u = 0; u < kBatch; ++u) c[u] = T.sp[idx[u]];
-#pragma unroll
-                  for (int u = 0; u < kBatch; ++u) {
-                    if (idx[u] != li) {
-                      const double dx = me.x - c[u].x, dy = me.y - c[u].y, dz = me.z - c[u].z;
-                      const double d2 = (dx * dx + dy * dy) + dz * dz;
-                      if (d2 <= r2) visit(idx[u], c[u], d2);
-                    }
-                  }
-                }
-              },
-              [&](unsigned int j) { return T.sp[j]; },
-              [&](unsigned int j) {  // local -> global index of a staged agent
-                int lo2 = 0, hi2 = nrows - 1;
-                while (lo2 < hi2) {
-                  const int mid = (lo2 + hi2 + 1) >> 1;
-                  if (T.lrow[mid] <= j) lo2 = mid;
-                  else hi2 = mid - 1;
-                }
-                return S.uid[T.rowg0[lo2] + (j - T.lrow[lo2])];
-              });
-        } else {
-          const unsigned int self = static_cast<unsigned int>(gi);
-          // overflow tile: the staging area is free, carve a u32 contact list
-          unsigned int* ovl32 = reinterpret_cast<unsigned int*>(T.sp) + tid;
-          dg = agent_step<MODEL, STATIC, RECORD>(
-              S, out, gi, me, dmax, nv, nn, a, cap, ovl32, kTileThreads, n_eval, n_skip,
-              [&](double rr, double r2, auto&& visit) {
-                for_each_neighbor(Q, S.pd, start, self, me.x, me.y, me.z, rr, r2,
-                                  [&](unsigned int j, const Pd& c, double, double, double, double d2) {
-                                    visit(j, c, d2);
-                                  });
-              },
-              [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; });
-        }
-      }
-      if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
-        stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
-    }
-    __syncthreads();  // smem reused by the next tile
   }
   flush_counters(n_eval, n_skip, gw);
 }
@@ -2511,14 +1974,10 @@ struct abs_gpu_ctx {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   int graph_failures = 0;
   bool graphs_off = false;
-  // split force step (k_force_a / k_force_b): per-agent contact lists
   unsigned int* holes = nullptr;           // compact_population: removed slots below the new end
   unsigned long long holes_cap = 0;
   unsigned long long* xcounts = nullptr;   // abs_gpu_export_layers counts (device)
   unsigned long long* hxcounts = nullptr;  // and their page-locked host copy
-  unsigned int* split_cl = nullptr;
-  unsigned char* split_cn = nullptr;
-  unsigned long long split_cap = 0;
   unsigned int scan_epoch = 0;
   unsigned long long* tiles64 = nullptr;
   unsigned char* nv = nullptr;
@@ -2811,19 +2270,10 @@ unsigned int bins_x(const abs_gpu_ctx* c) {  // auto: 3 along x with 2x2 in y/z 
   return b <= 0 ? (c->auto_bins == 2u ? 3u : c->auto_bins) : static_cast<unsigned int>(std::min(b, 4));
 }
 
-// ABSIM_F32=0 disables the fp32-classified candidate walk (A/B switch).
-bool use_f32_walk() {
-  static const int v = [] {
-    const char* e = std::getenv("ABSIM_F32");
-    return (e && std::strcmp(e, "0") == 0) ? 0 : 1;
-  }();
-  return v != 0;
-}
-
 // The fp32 copy `pf` is written by the re-bin only when the force kernel's
 // fp32-classified walk will read it (sub-binned grids; not SIR, not box mode).
 bool uses_f32_walk(const abs_gpu_ctx* c) {
-  return use_f32_walk() && c->cfg.model != ABS_MODEL_SIR && !(bins_x(c) == 1u && bins_yz(c) == 1u);
+  return c->cfg.model != ABS_MODEL_SIR && !(bins_x(c) == 1u && bins_yz(c) == 1u);
 }
 
 void launch_commit(abs_gpu_ctx* c);
@@ -2864,30 +2314,6 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->grid_valid = true;
 }
 
-template <int MODEL, bool STATIC, bool RECORD>
-void launch_tile(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  static bool configured = false;  // per template instance
-  const int smem = static_cast<int>(sizeof(TileSmem));
-  if (!configured) {
-    cudaFuncSetAttribute(k_force_tile<MODEL, STATIC, RECORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  k_force_tile<MODEL, STATIC, RECORD><<<c->sms, kTileThreads, smem, c->stream>>>(
-      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
-}
-
-// ABSIM_FORCE_KERNEL=tile selects the TMA-staged tile kernel; the default
-// is the per-lane gather kernel (faster on the measured configs so far,
-// see DESIGN.md §Kernels).
-bool use_tile_kernel() {
-  static const int v = [] {
-    const char* e = std::getenv("ABSIM_FORCE_KERNEL");
-    return (e && std::strcmp(e, "tile") == 0) ? 1 : 0;
-  }();
-  return v != 0;
-}
-
-constexpr int kForceSmem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4;
 
 // ABSIM_STATIC_PREPASS=0: static agents settled inside the force sweep (A/B)
 bool static_prepass() {
@@ -2899,67 +2325,10 @@ constexpr int kForceSmemBox = kMaxContacts * kForceThreads * 4;  // contact list
 constexpr int kForceSmemF32 = (kMaxRows + kMaxRows / 2 + kMaxContacts) * kForceThreads * 4;
 static_assert(kMaxRows % 2 == 0, "16-bit bound array packs two rows per word");
 
-// ABSIM_SPLIT_FORCE=1 runs config 4's force sweep as k_force_a + k_force_b.
-// Off by default: 70 registers and 7 resident CTAs for the walk (28 warps/SM
-// against 20) did not move it (c4 @ 2^26: 25.35 ms split vs 25.0-25.45 single).
-bool split_force() {
-  static const bool v = env_flag("ABSIM_SPLIT_FORCE", false);
-  return v;
-}
-
-template <int MODEL, bool STATIC, bool RECORD, int WALK>
-void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a);
-
-// k_force_a -> k_force_b -> k_force over the overflow list.
-int launch_split(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  if (c->split_cap != c->cap) {
-    cudaFree(c->split_cl);
-    cudaFree(c->split_cn);
-    c->split_cl = nullptr;
-    c->split_cn = nullptr;
-    c->split_cap = 0;
-    if (dalloc(&c->split_cl, kSplitContacts * c->cap) != cudaSuccess || dalloc(&c->split_cn, c->cap) != cudaSuccess) {
-      cudaGetLastError();
-      return ABS_ERR_CUDA;  // caller falls back to the single-kernel sweep
-    }
-    c->split_cap = c->cap;
-  }
-  static int blocks = 0;
-  constexpr int smem = (kMaxRows + kMaxRows / 2) * kForceThreads * 4;
-  if (!blocks) blocks = force_blocks(c, k_force_a, smem);
-  k_force_a<<<blocks, kForceThreads, smem, c->stream>>>(S, c->pf, c->newpd, c->g, c->start, c->split_cl, c->split_cn,
-                                                         c->cap, c->rank);
-  const int nb = grid_blocks(c, c->cap);
-  if (c->cfg.record_forces)
-    k_force_b<true><<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, a, c->split_cl, c->split_cn, c->cap);
-  else
-    k_force_b<false><<<nb, kThreads, 0, c->stream>>>(S, c->newpd, c->g, a, c->split_cl, c->split_cn, c->cap);
-  c->launches += 2;
-  // agents with more contacts than the list holds: the full sweep (c->rank lists them)
-  static int blocks_f = 0;
-  if (!blocks_f) {
-    cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kForceSmemF32);
-    cudaFuncSetAttribute(k_force<ABS_MODEL_NONE, false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kForceSmemF32);
-    blocks_f = c->sms;
-  }
-  if (c->cfg.record_forces)
-    k_force<ABS_MODEL_NONE, false, true, 1><<<blocks_f, kForceThreads, kForceSmemF32, c->stream>>>(
-        S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol,
-        c->div_mark, c->st_tag, c->rank);
-  else
-    k_force<ABS_MODEL_NONE, false, false, 1><<<blocks_f, kForceThreads, kForceSmemF32, c->stream>>>(
-        S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol,
-        c->div_mark, c->st_tag, c->rank);
-  ++c->launches;
-  return ABS_OK;
-}
-
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   static int blocks = 0;  // per template instance
-  constexpr int smem = WALK == 2 ? kForceSmemBox : (WALK == 1 ? kForceSmemF32 : kForceSmem);
+  constexpr int smem = WALK == 2 ? kForceSmemBox : kForceSmemF32;
   if (!blocks) {
     cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, WALK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, WALK>, smem);
@@ -2980,69 +2349,15 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
 template <int MODEL, bool STATIC, bool RECORD>
 void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   if (bins_x(c) == 1u && bins_yz(c) == 1u) launch_gather_f<MODEL, STATIC, RECORD, 2>(c, S, a);
-  else if (use_f32_walk()) launch_gather_f<MODEL, STATIC, RECORD, 1>(c, S, a);
-  else launch_gather_f<MODEL, STATIC, RECORD, 0>(c, S, a);
-}
-
-// Lanes per agent of the group kernel: ABSIM_LPA in {1 (per-lane k_force), 2,
-// 4, 8, 16, 32}; default 1 (measured fastest on c4).
-// Box mode (bins == boxes) keeps the lockstep walk.
-#ifndef ABS_GROUP_KERNEL
-#define ABS_GROUP_KERNEL 0  // -DABS_GROUP_KERNEL=1 builds the LPA > 1 variants
-#endif
-int lanes_per_agent() {
-  static const int v = [] {
-    const char* e = std::getenv("ABSIM_LPA");
-    const int x = e ? std::atoi(e) : 1;
-    return (ABS_GROUP_KERNEL && (x == 2 || x == 4 || x == 8 || x == 16 || x == 32)) ? x : 1;
-  }();
-  return v;
-}
-
-template <int MODEL, bool STATIC, bool RECORD, int LPA>
-void launch_group_l(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  static int blocks = 0;  // per template instance: resident CTAs
-  if (!blocks) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force_g<MODEL, STATIC, RECORD, LPA>, kForceThreads, 0);
-    blocks = c->sms * std::max(per_sm, 1);
-  }
-  k_force_g<MODEL, STATIC, RECORD, LPA><<<blocks, kForceThreads, 0, c->stream>>>(
-      S, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark, c->st_tag);
-}
-
-template <int MODEL, bool STATIC, bool RECORD>
-void launch_group(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-#if ABS_GROUP_KERNEL
-  switch (lanes_per_agent()) {
-    case 2: launch_group_l<MODEL, STATIC, RECORD, 2>(c, S, a); break;
-    case 4: launch_group_l<MODEL, STATIC, RECORD, 4>(c, S, a); break;
-    case 16: launch_group_l<MODEL, STATIC, RECORD, 16>(c, S, a); break;
-    case 32: launch_group_l<MODEL, STATIC, RECORD, 32>(c, S, a); break;
-    default: launch_group_l<MODEL, STATIC, RECORD, 8>(c, S, a); break;
-  }
-#endif
+  else launch_gather_f<MODEL, STATIC, RECORD, 1>(c, S, a);
 }
 
 template <int MODEL, bool STATIC>
 void launch_force_t(abs_gpu_ctx* c, int, Soa& S, const StepArgs& a) {
   const bool box_mode = bins_x(c) == 1u && bins_yz(c) == 1u;
-  if (MODEL == ABS_MODEL_NONE && !STATIC && !box_mode && use_f32_walk() && split_force() && !use_tile_kernel()) {
-    if (launch_split(c, S, a) == ABS_OK) return;
-  }
   if (MODEL == ABS_MODEL_COHERE) {  // its behaviour query lives in the gather kernel
     if (c->cfg.record_forces) launch_gather<MODEL, STATIC, true>(c, S, a);
     else launch_gather<MODEL, STATIC, false>(c, S, a);
-    return;
-  }
-  if (!use_tile_kernel() && !box_mode && lanes_per_agent() > 1) {
-    if (c->cfg.record_forces) launch_group<MODEL, STATIC, true>(c, S, a);
-    else launch_group<MODEL, STATIC, false>(c, S, a);
-    return;
-  }
-  if (use_tile_kernel()) {
-    if (c->cfg.record_forces) launch_tile<MODEL, STATIC, true>(c, S, a);
-    else launch_tile<MODEL, STATIC, false>(c, S, a);
     return;
   }
   if (c->cfg.record_forces) launch_gather<MODEL, STATIC, true>(c, S, a);
@@ -3319,7 +2634,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->split_cl); cudaFree(c->split_cn); cudaFree(c->xcounts); cudaFree(c->holes);
+  cudaFree(c->xcounts); cudaFree(c->holes);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);

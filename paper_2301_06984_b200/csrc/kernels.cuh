@@ -289,9 +289,6 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
 constexpr int kMaxRows = ABS_MAX_ROWS;
 constexpr int kMaxContacts = ABS_MAX_CONTACTS;  // recorded possible contacts per agent (pass B)
 constexpr int kForceThreads = 128;
-#ifndef ABS_PREFILTER
-#define ABS_PREFILTER 0
-#endif
 #ifndef ABS_BATCH
 #define ABS_BATCH 4
 #endif
@@ -333,116 +330,7 @@ __device__ __forceinline__ void for_each_neighbor_box(const QGrid& g, const Pd* 
 }
 
 
-template <class F>
-__device__ __forceinline__ void for_each_neighbor_flat(const QGrid& g, const Pd* __restrict__ pd,
-                                                       const float4* __restrict__ pf,
-                                                       const unsigned int* __restrict__ start,
-                                                       unsigned int (*wj0)[kForceThreads],
-                                                       unsigned int (*wj1)[kForceThreads],
-                                                       unsigned int self, double cx, double cy,
-                                                       double cz, double r, double r2, F&& visit) {
-  const int t = threadIdx.x;
-  const float fx = static_cast<float>(cx - g.ox);
-  const float fy = static_cast<float>(cy - g.oy);
-  const float fz = static_cast<float>(cz - g.oz);
-  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
-  const float rf2 = rf * rf;
-  int bl[3], bh[3];
-  box_bin_range(g, cx, cy, cz, bl, bh);
-  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
-  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
-  int nw = 0;
-  for (int bz = z0; bz <= z1; ++bz) {
-    const float zl = static_cast<float>(bz) * g.s[2];
-    const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
-    for (int by = y0; by <= y1; ++by) {
-      const float yl = static_cast<float>(by) * g.s[1];
-      const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
-      const float rem = rf2 - (gy * gy + gz * gz);
-      if (rem < 0.0f) continue;
-      const float w = sqrtf(rem);
-      const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
-      const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
-      const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
-      ABS_ASSERT(x0 >= 0 && x1 + 1 <= (int)g.bd[0] && by >= 0 && bz >= 0 && by < (int)g.bd[1] && bz < (int)g.bd[2]);
-      const unsigned int j0 = __ldg(start + row + x0);
-      const unsigned int j1 = __ldg(start + row + x1 + 1);
-      ABS_ASSERT(j0 <= j1);
-      if (j1 <= j0) continue;
-      if (nw < kMaxRows) {
-        wj0[nw][t] = j0;
-        wj1[nw][t] = j1;
-        ++nw;
-      } else {
-        for (unsigned int j = j0; j < j1; ++j) {  // overflow rows: nested walk
-          if (j == self) continue;
-          const Pd q = load_pd(pd + j);
-          const double dx = cx - q.x, dy = cy - q.y, dz = cz - q.z;
-          const double d2 = (dx * dx + dy * dy) + dz * dz;
-          if (d2 <= r2) visit(j, q, dx, dy, dz, d2);
-        }
-      }
-    }
-  }
-  if (nw == 0) return;
-  int k = 0;
-  unsigned int j = wj0[0][t], je = wj1[0][t];
-  // kBatch candidates per lane per round: their loads are independent and in
-  // flight together; the exact tests are independent fp64 chains.
-  while (k < nw) {
-    unsigned int idx[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      idx[u] = self;  // sentinel: skipped below
-      if (k < nw) {
-        idx[u] = j;
-        if (++j == je && ++k < nw) {
-          j = wj0[k][t];
-          je = wj1[k][t];
-        }
-      }
-    }
-#if ABS_PREFILTER
-    // conservative fp32 reject on the float4 copy (|error| < slack), then the
-    // exact fp64 test only for the survivors
-    float4 qf[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pf + idx[u]);
-    bool pass[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const float ex = fx - qf[u].x, ey = fy - qf[u].y, ez = fz - qf[u].z;
-      pass[u] = idx[u] != self && __fmaf_rn(ez, ez, __fmaf_rn(ey, ey, ex * ex)) <= rf2;
-    }
-    Pd q[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u)
-      if (pass[u]) q[u] = load_pd(pd + idx[u]);
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      if (pass[u]) {
-        const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
-        const double d2 = (dx * dx + dy * dy) + dz * dz;
-        if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
-      }
-    }
-#else
-    Pd q[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + idx[u]);
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      if (idx[u] != self) {
-        const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
-        const double d2 = (dx * dx + dy * dy) + dz * dz;
-        if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
-      }
-    }
-#endif
-  }
-}
-
-// fp32-classified variant of for_each_neighbor_flat. Candidates are read
+// Flat-stream, fp32-classified walk used by the force kernel. Candidates are read
 // from `pf` (float4 {x, y, z, d} relative to the grid origin, 16 B) and
 // classified against the exact fp64 test with a proven margin: the fp32
 // distance differs from the fp64 one by less than `g.slack` (rounding of two
@@ -610,117 +498,6 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) visit(idx[u], df2[u], qf[u].w, in[u]);
-  }
-}
-
-// Group-cooperative variant: the LPA lanes of a group (aligned lane block)
-// share ONE agent. The agent's candidate stream — exactly the rows and order
-// of for_each_neighbor — is dealt round-robin to the group's lanes (lane l
-// gets flat positions l, l + LPA, ...), so one group load is LPA consecutive
-// records of a row (coalesced) instead of LPA unrelated ones. Rows are
-// enumerated in chunks of 32: lane l computes rows [l*R, (l+1)*R) of the
-// chunk, a group scan of the row lengths gives each row's flat offset, and
-// `rj0`/`rpre` (this group's shared-memory slice, 2*32+1 words) hold them for
-// the walk. Each lane visits its candidates in increasing flat order.
-constexpr int kGroupRows = 32;
-constexpr int kGroupRowWords = 2 * kGroupRows + 1;
-
-template <int LPA>
-__device__ __forceinline__ unsigned int group_mask() {
-  return LPA == 32 ? 0xffffffffu : (((1u << LPA) - 1u) << ((threadIdx.x & 31) & ~(LPA - 1)));
-}
-
-template <int LPA, class F>
-__device__ __forceinline__ void for_each_neighbor_group(const QGrid& g, const Pd* __restrict__ pd,
-                                                        const unsigned int* __restrict__ start,
-                                                        unsigned int* __restrict__ rows, unsigned int self,
-                                                        double cx, double cy, double cz, double r, double r2,
-                                                        F&& visit) {
-  constexpr int R = kGroupRows / LPA;
-  const unsigned int mask = group_mask<LPA>();
-  const int l = threadIdx.x & (LPA - 1);
-  unsigned int* rj0 = rows;
-  unsigned int* rpre = rows + kGroupRows;
-  const float fx = static_cast<float>(cx - g.ox);
-  const float fy = static_cast<float>(cy - g.oy);
-  const float fz = static_cast<float>(cz - g.oz);
-  const float rf = static_cast<float>(r) * 1.000001f + g.slack;
-  const float rf2 = rf * rf;
-  int bl[3], bh[3];
-  box_bin_range(g, cx, cy, cz, bl, bh);
-  const int z0 = max(fbin(fz - rf, g.inv_s[2], g.bd[2]), bl[2]), z1 = min(fbin(fz + rf, g.inv_s[2], g.bd[2]), bh[2]);
-  const int y0 = max(fbin(fy - rf, g.inv_s[1], g.bd[1]), bl[1]), y1 = min(fbin(fy + rf, g.inv_s[1], g.bd[1]), bh[1]);
-  const int ny = y1 - y0 + 1;
-  const int nq = (z1 >= z0 && ny > 0) ? (z1 - z0 + 1) * ny : 0;
-  for (int qb = 0; qb < nq; qb += kGroupRows) {
-    unsigned int j0[R], len[R], tot = 0;
-#pragma unroll
-    for (int m = 0; m < R; ++m) {
-      const int q = qb + l * R + m;
-      j0[m] = 0;
-      len[m] = 0;
-      if (q < nq) {
-        const int bz = z0 + q / ny, by = y0 + q % ny;
-        const float zl = static_cast<float>(bz) * g.s[2];
-        const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
-        const float yl = static_cast<float>(by) * g.s[1];
-        const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
-        const float rem = rf2 - (gy * gy + gz * gz);
-        if (rem >= 0.0f) {
-          const float w = sqrtf(rem);
-          const int x0 = max(fbin(fx - w, g.inv_s[0], g.bd[0]), bl[0]);
-          const int x1 = min(fbin(fx + w, g.inv_s[0], g.bd[0]), bh[0]);
-          const unsigned int row =
-              g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
-          const unsigned int a0 = __ldg(start + row + x0);
-          const unsigned int a1 = __ldg(start + row + x1 + 1);
-          j0[m] = a0;
-          len[m] = a1 > a0 ? a1 - a0 : 0u;
-        }
-      }
-      tot += len[m];
-    }
-    unsigned int inc = tot;
-#pragma unroll
-    for (int off = 1; off < LPA; off <<= 1) {
-      const unsigned int v = __shfl_up_sync(mask, inc, off, LPA);
-      if (l >= off) inc += v;
-    }
-    const unsigned int total = __shfl_sync(mask, inc, LPA - 1, LPA);
-    unsigned int run = inc - tot;
-#pragma unroll
-    for (int m = 0; m < R; ++m) {
-      rj0[l * R + m] = j0[m];
-      rpre[l * R + m] = run;
-      run += len[m];
-    }
-    if (l == LPA - 1) rpre[kGroupRows] = total;
-    __syncwarp(mask);
-    int k = 0;
-    for (unsigned int p0 = 0; p0 < total; p0 += LPA * kBatch) {
-      unsigned int idx[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const unsigned int p = p0 + u * LPA + l;
-        idx[u] = self;  // sentinel: skipped below
-        if (p < total) {
-          while (rpre[k + 1] <= p) ++k;
-          idx[u] = rj0[k] + (p - rpre[k]);
-        }
-      }
-      Pd q[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + idx[u]);
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        if (idx[u] != self) {
-          const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
-          const double d2 = (dx * dx + dy * dy) + dz * dz;
-          if (d2 <= r2) visit(idx[u], q[u], dx, dy, dz, d2);
-        }
-      }
-    }
-    __syncwarp(mask);  // the next chunk overwrites rj0 / rpre
   }
 }
 
