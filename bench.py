@@ -386,6 +386,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     ms_r = e2.elapsed_time(e3)
     force_ms, force_launches = sim.force_kernel_time()
+    lists = sim.list_stats()
     sim.reset_timers(False)
     r2 = sim.report()
     agent_its = None
@@ -490,7 +491,8 @@ def run_gpu(args):
         "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
                    "parallelism": f"replicas{world}" if world > 1 else "single", "environment": args.env,
                    "bins_per_box": [args.bins_x, args.bins, args.bins], "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
-        "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else "k_force", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else ("k_force_list" if lists["list_steps"] else "k_force"),
+                     "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
                      "avg_launch_ms": avg_force_ms, "force_share_of_step": force_ms / ms_r,
@@ -503,6 +505,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "gpu_launches": int(r1.kernel_launches - r0.kernel_launches),
         "force_evaluations_per_agent_step": (r1.force_evaluations - r0.force_evaluations) / max(1, agent_its / world),
+        "lists": lists,
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:

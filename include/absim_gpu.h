@@ -106,7 +106,11 @@ typedef struct {
   int32_t bins_per_box;          /* internal sub-bins per box edge along y and z: 0 auto, 1..4 */
   int32_t bins_per_box_x;        /* internal sub-bins per box edge along x: 0 auto, 1..4 */
   int32_t environment;           /* ABS_ENV_* (SimulationParams::environment_kind), default grid */
-  int32_t reserved;
+  int32_t neighbor_list;         /* 0 auto: per-agent candidate lists between environment rebuilds when
+                                    the diameters are constant (no behaviours, no static detection, one
+                                    domain); -1 off (re-bin + cell-table walk every iteration). The
+                                    visited neighbour sets are identical either way */
+  double neighbor_skin;          /* list skin (absolute length); 0 = 0.15 x the largest diameter */
 } abs_gpu_config;
 
 /* SimulationReport counters (report.hpp:32-40) */
@@ -264,6 +268,18 @@ int abs_gpu_force_kernel_time(abs_gpu_ctx* ctx, double* total_ms, uint64_t* laun
  * rolled-back attempt counts as one). */
 int abs_gpu_phase_times(abs_gpu_ctx* ctx, double* out4, double* per_iteration_ms, uint64_t cap, uint64_t* n);
 int abs_gpu_reset_timers(abs_gpu_ctx* ctx, int enable);
+/* Parity hook: with enable != 0 every iteration records each agent's force
+ * evaluations (run_forces' ++evals, simulation.cpp:473) — the size of its
+ * neighbour set at the force radius; static agents record 0.
+ * abs_gpu_download_evaluations copies the last iteration's counts in
+ * download (storage) order. */
+int abs_gpu_record_evaluations(abs_gpu_ctx* ctx, int enable);
+int abs_gpu_download_evaluations(abs_gpu_ctx* ctx, uint32_t* out, uint64_t cap);
+/* Neighbour-list statistics: out4 = {list builds, list
+ * steps (iterations served from the lists), build launches timed, largest
+ * candidate count of the last build}; *build_ms = CUDA-event time of the
+ * timed builds (abs_gpu_reset_timers(ctx, 1)). Counts since creation. */
+int abs_gpu_list_stats(abs_gpu_ctx* ctx, uint64_t* out4, double* build_ms);
 
 #ifdef __cplusplus
 }

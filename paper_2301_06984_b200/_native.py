@@ -38,6 +38,7 @@ EXPORTS = [
     "abs_gpu_stream", "abs_gpu_set_stream", "abs_gpu_force_kernel_time", "abs_gpu_reset_timers",
     "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
     "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times", "abs_gpu_run_frames",
+    "abs_gpu_list_stats", "abs_gpu_record_evaluations", "abs_gpu_download_evaluations",
 ]
 
 
@@ -58,7 +59,8 @@ class Config(C.Structure):
         ("bins_per_box", C.c_int32),
         ("bins_per_box_x", C.c_int32),
         ("environment", C.c_int32),
-        ("reserved", C.c_int32),
+        ("neighbor_list", C.c_int32),
+        ("neighbor_skin", C.c_double),
     ]
 
 
@@ -146,6 +148,9 @@ def load():
         "abs_gpu_set_stream": (C.c_int, [_CTX, C.c_void_p]),
         "abs_gpu_force_kernel_time": (C.c_int, [_CTX, _D, _U64]),
         "abs_gpu_reset_timers": (C.c_int, [_CTX, C.c_int]),
+        "abs_gpu_list_stats": (C.c_int, [_CTX, _U64, _D]),
+        "abs_gpu_record_evaluations": (C.c_int, [_CTX, C.c_int]),
+        "abs_gpu_download_evaluations": (C.c_int, [_CTX, _U32, C.c_uint64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -129,6 +129,8 @@ struct FinArgs {
   unsigned long long bins_cap, capacity, uid_cap;
   int may_add;
   unsigned long long iteration;
+  int list_mode;  // 0 no neighbour lists, 1 list step (check coverage), 2 list (re)build step
+  double skin;    // list skin (absolute)
 };
 
 __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
@@ -236,6 +238,23 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
       }
       g->margin = 1e-9 * mag;
     }
+  }
+  // Neighbour lists. A list built at step t0 holds every j
+  // with |p_i - p_j| <= r_i + skin at t0. At a later step, any j with
+  // |p_i - p_j| <= r_i was within r_i + D_i + D_j at t0, where D is the
+  // displacement since t0 <= list_acc (per-step maxima + rounding margin);
+  // so the lists still cover the query while 2 list_acc <= skin and the
+  // radii have not grown (constant diameters, dmax <= list_dmax).
+  if (fa.list_mode == 2) {
+    g->list_acc = 0.0;
+    g->list_dmax = g->dmax;
+    g->step_disp = 0u;
+    g->list_need = 0u;
+  } else if (fa.list_mode == 1 && err == kErrNone) {
+    const double acc = g->list_acc + static_cast<double>(__uint_as_float(g->step_disp)) + g->margin + 1e-12;
+    g->list_acc = acc;
+    g->step_disp = 0u;
+    if (2.0 * acc > fa.skin || g->dmax > g->list_dmax) err = kErrListRebuild;
   }
   reset_reduction(g);
   g->work = 0;
@@ -867,6 +886,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       });
     }
     n_eval += evals;
+    if (a.evc) a.evc[i] = evals;
     const double k = a.k;
     auto contact_q = [&](unsigned int j, const Pd& q) {
       const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
@@ -1142,6 +1162,189 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
       stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
   }
   flush_counters(n_eval, n_skip, gw);
+}
+
+// ------------------------------------------------------------ neighbour lists
+// Between two environment rebuilds the mechanical step reads per-agent
+// candidate lists instead of walking the cell table. The
+// reference's neighbour set of agent i is {j != i : d2 <= r_i^2} with
+// r_i = 0.5 (d_i + dmax) (simulation.cpp:469, uniform_grid.cpp:172-230) and
+// does not depend on the grid, so any superset of it tested with the
+// reference's exact fp64 d2 <= r^2 visits exactly the same agents. A list
+// built with radius r_i + skin stays such a superset while every agent has
+// moved less than skin / 2 since the build (checked on the device by
+// finalize_grid before every list step; a failed check re-runs the
+// iteration as a rebuild).
+//
+// k_list_build: after the re-bin, every agent's candidates within r + skin
+// (fp32 superset, no 3x3x3 box clamp) into list[k * stride + i] — column k
+// of all agents is contiguous, so the list sweep's index loads coalesce.
+#ifndef ABS_LIST_MIN_BLOCKS
+#define ABS_LIST_MIN_BLOCKS 6
+#endif
+constexpr int kListSmem = (kMaxRows + kMaxRows / 2) * kForceThreads * 4;
+
+__global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
+    k_list_build(const float4* __restrict__ pf, DevGrid* g, const unsigned int* __restrict__ start,
+                 unsigned int* __restrict__ list, unsigned char* __restrict__ cnt, unsigned long long stride,
+                 unsigned int kmax, double skin, unsigned long long iteration) {
+  if (g->err) return;
+  __shared__ QGrid Q;
+  extern __shared__ __align__(16) unsigned int force_smem[];
+  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
+  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
+  const int lane = threadIdx.x & 31;
+  unsigned int most = 0;
+  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
+    const unsigned long long base = chunk * 32ull;
+    if (base >= n) break;
+    const unsigned long long i = base + lane;
+    if (i < n) {
+      const float4 me = __ldg(pf + i);
+      // pf.w is the diameter rounded to fp32 (relative error 2^-24); the
+      // 2e-6 inflation of rf covers it and the rounding of R
+      const double R = 0.5 * (static_cast<double>(me.w) + dmax) + skin;
+      const float rf = static_cast<float>(R) * 1.000002f + Q.slack + 1e-6f;
+      unsigned int c = 0;
+      unsigned int* col = list + i;
+      for_each_candidate32(Q, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, rf,
+                           [&](unsigned int j) {
+                             if (c < kmax) col[c * stride] = j;
+                             ++c;
+                           });
+      cnt[i] = static_cast<unsigned char>(c < kmax ? c : kmax);
+      most = c > most ? c : most;
+    }
+  }
+  most = __reduce_max_sync(0xffffffffu, most);
+  if (lane == 0 && most) {
+    atomicMax(&g->list_need, most);
+    if (most > kmax && atomicCAS(&g->err, 0, static_cast<int>(kErrListOverflow)) == 0) g->failed_iteration = iteration;
+  }
+}
+
+// k_force_list: run_forces + apply_pending (simulation.cpp:463-500,
+// mechanics.cpp:10-27, agent.hpp:115-133) over the list — for every listed
+// j the reference's exact d2 <= r^2 (a force evaluation), then
+// pairwise_repulsion with the reference's operations; a pair whose d2 is at
+// least h^2 (1 + 2^-50) has dist >= h, i.e. overlap <= 0, and skips the
+// sqrt. Positions are read from `pin` and written to `pout` (ping-pong). The
+// step's largest displacement is folded into g->step_disp for the coverage
+// check of the next step.
+#ifndef ABS_LIST_FORCE_MIN_BLOCKS
+#define ABS_LIST_FORCE_MIN_BLOCKS 3
+#endif
+template <bool RECORD>
+__global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
+    k_force_list(const Pd* __restrict__ pin, Pd* __restrict__ pout, Soa S, DevGrid* g,
+                 const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt,
+                 unsigned long long stride, StepArgs a, unsigned long long cap) {
+  if (g->err) return;
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
+  const double k = a.k;
+  unsigned long long n_eval = 0;
+  float moved = 0.0f;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const Pd me = load_pd(pin + i);
+    const unsigned int c = cnt[i];
+    const double r = 0.5 * (me.d + dmax);
+    const double r2 = r * r;
+    const unsigned int* col = list + i;
+    unsigned int evals = 0, contributors = 0;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    for (unsigned int s = 0; s < c; s += kBatch) {
+      unsigned int jj[kBatch];
+      Pd q[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) jj[u] = __ldg(col + static_cast<unsigned long long>(min(s + u, c - 1)) * stride);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pin + jj[u]);
+      // radius test for the batch; pairs that may overlap are re-read and
+      // handled afterwards, so no record stays live across the fp64
+      // sqrt/division slow paths
+      unsigned int contact = 0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const double dx = me.x - q[u].x, dy = me.y - q[u].y, dz = me.z - q[u].z;
+        const double d2 = (dx * dx + dy * dy) + dz * dz;
+        const bool in = s + u < c && d2 <= r2;
+        evals += in;
+        const double h = 0.5 * (me.d + q[u].d);
+        contact |= (in && d2 < h * h * (1.0 + 0x1.0p-50)) ? (1u << u) : 0u;
+      }
+      while (contact) {
+        const int u = __ffs(contact) - 1;
+        contact &= contact - 1;
+        const unsigned int j = jj[u];
+        const Pd qq = load_pd(pin + j);
+        const double dx = me.x - qq.x, dy = me.y - qq.y, dz = me.z - qq.z;
+        // pairwise_repulsion (mechanics.cpp:10-27)
+        const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+        const double overlap = 0.5 * (me.d + qq.d) - dist;
+        if (overlap <= 0.0) continue;
+        double f0, f1, f2;
+        if (dist > 0.0) {
+          const double sc = k * overlap / dist;
+          f0 = dx * sc;
+          f1 = dy * sc;
+          f2 = dz * sc;
+        } else {
+          coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
+        }
+        if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
+          ++contributors;
+          fx += f0;
+          fy += f1;
+          fz += f2;
+        }
+      }
+    }
+    n_eval += evals;
+    if (a.evc) a.evc[i] = evals;
+    double tx = 0.0, ty = 0.0, tz = 0.0;
+    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
+      tx = fx * a.dt;
+      ty = fy * a.dt;
+      tz = fz * a.dt;
+    }
+    Pd np = me;
+    const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
+    if (disp > 0.0) {
+      double md = disp;
+      if (disp > a.max_disp) {
+        const double sc = a.max_disp / disp;
+        tx *= sc;
+        ty *= sc;
+        tz *= sc;
+        md = a.max_disp;
+      }
+      np.x = me.x + tx;
+      np.y = me.y + ty;
+      np.z = me.z + tz;
+      const unsigned char fl = S.flags[i];
+      if (!(fl & ABS_FLAG_MOVED)) S.flags[i] = fl | ABS_FLAG_MOVED;
+      moved = fmaxf(moved, __double2float_ru(md * (1.0 + 0x1.0p-40)));
+    }
+    if (RECORD) {
+      S.force[i] = fx;
+      S.force[cap + i] = fy;
+      S.force[2 * cap + i] = fz;
+    }
+    S.partners[i] = contributors;
+    reinterpret_cast<double2*>(pout + i)[0] = make_double2(np.x, np.y);
+    reinterpret_cast<double2*>(pout + i)[1] = make_double2(np.z, np.d);
+  }
+  const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
+  if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
+  flush_counters(n_eval, 0ull, g);
 }
 
 // ------------------------------------------------------------ config 5: SIR
@@ -1971,7 +2174,26 @@ struct abs_gpu_ctx {
   unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
   unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
   // per-iteration CUDA graphs (abs_gpu_simulate): [0] plain, [1] with the Morton sort
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  // slot = (sort ? 1 : 0) + 2 * iteration kind (0 re-bin + walk, 1 list step, 2 list rebuild)
+  cudaGraphExec_t gexec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // neighbour lists
+  unsigned int* nl = nullptr;           // [kmax][stride] candidate storage indices
+  unsigned char* nl_cnt = nullptr;      // [stride] candidates per agent
+  unsigned long long nl_stride = 0;
+  unsigned int nl_kmax = 0;
+  bool list_valid = false;              // lists match the current storage order
+  bool list_off = false;                // lists disabled for this context (candidate count > 255)
+  bool ov_on = false;                   // host mirror of the multi-domain grid override
+  double host_dmax = 0.0;               // largest diameter of the last upload (auto skin)
+  double build_ms = 0.0;
+  unsigned long long build_launches = 0;
+  std::vector<cudaEvent_t> bev;  // pairs around k_list_build (timing on)
+  size_t bev_used = 0;
+  unsigned long long list_builds = 0, list_steps = 0;
+  // per-agent force evaluations of the last iteration (abs_gpu_record_evaluations)
+  unsigned int* evc = nullptr;
+  unsigned long long evc_cap = 0;
+  bool rec_evals = false;
   int graph_failures = 0;
   bool graphs_off = false;
   unsigned int* holes = nullptr;           // compact_population: removed slots below the new end
@@ -2097,6 +2319,7 @@ Pd* cur_pos(abs_gpu_ctx* c) { return c->pos_in_new ? c->newpd : c->S[c->cur].pd;
 // (Re)allocate agent-sized buffers preserving the first `keep` agents.
 int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long keep) {
   if (want <= c->cap) return ABS_OK;
+  c->list_valid = false;
   unsigned long long ncap = std::max<unsigned long long>(want, 1024);
   Soa S2[2]{};
   for (int b = 0; b < 2; ++b) CK(alloc_soa(S2[b], ncap));
@@ -2144,6 +2367,14 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   CK(dalloc(&c->st_vol, ncap));
   CK(dalloc(&c->st_tag, ncap));
   c->cap = ncap;
+  if (c->rec_evals) {
+    cudaFree(c->evc);
+    c->evc = nullptr;
+    c->evc_cap = 0;
+    CK(dalloc(&c->evc, ncap));
+    CK(cudaMemsetAsync(c->evc, 0, ncap * sizeof(unsigned int), c->stream));
+    c->evc_cap = ncap;
+  }
   return ABS_OK;
 }
 
@@ -2233,6 +2464,7 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
   a.detect_static = c->cfg.detect_static_agents;
   a.record_forces = c->cfg.record_forces;
   a.brute = brute_env(c);
+  a.evc = c->rec_evals ? c->evc : nullptr;
   return a;
 }
 
@@ -2279,7 +2511,8 @@ bool uses_f32_walk(const abs_gpu_ctx* c) {
 void launch_commit(abs_gpu_ctx* c);
 
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
-void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add, bool in_step = false) {
+void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add, bool in_step = false,
+                       int list_mode = 0, double skin = 0.0) {
   const int nb = grid_blocks(c, c->cap);
   const unsigned long long* nbins_dev = &c->g->nbins;
   static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
@@ -2289,7 +2522,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   }
   const Pd* pos = cur_pos(c);
   const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
-                   c->bins_cap, c->cap, c->uid_cap, may_add, iteration};
+                   c->bins_cap, c->cap, c->uid_cap, may_add, iteration, list_mode, skin};
   if (fused) {
     k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa, c->grid_valid ? c->start : nullptr);
   } else {
@@ -2306,12 +2539,14 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   const bool carry_partners = !in_step || c->cfg.detect_static_agents || c->cfg.model == ABS_MODEL_SIR;
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                            c->cfg.record_forces, uses_f32_walk(c), -1, uses_ext(c->cfg),
-                                            carry_partners ? 1 : 0, c->cfg.model != ABS_MODEL_NONE ? 1 : 0);
+                                            c->cfg.record_forces, uses_f32_walk(c) || list_mode == 2, -1,
+                                            uses_ext(c->cfg), carry_partners ? 1 : 0,
+                                            c->cfg.model != ABS_MODEL_NONE ? 1 : 0);
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
   c->grid_valid = true;
+  c->list_valid = false;  // storage re-ordered (a list build follows in list mode 2)
 }
 
 
@@ -2393,7 +2628,117 @@ void phase_mark(abs_gpu_ctx* c) {
   cudaEventRecord(c->pev[c->pev_used++], c->stream);
 }
 
-void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration) {
+// Neighbour lists serve the mechanical step when the
+// diameters are constant and one context owns the whole population: no
+// behaviours, no static detection, no ghosts or grid override, the grid
+// environment. ABSIM_NLIST=0 turns them off (A/B switch).
+bool list_mode_ok(const abs_gpu_ctx* c) {
+  static const bool on = env_flag("ABSIM_NLIST", true);
+  return on && !c->list_off && c->cfg.neighbor_list >= 0 && c->cfg.model == ABS_MODEL_NONE &&
+         !c->cfg.detect_static_agents && !brute_env(c) && !c->defer_commit && c->ghosts == 0 && !c->ov_on;
+}
+
+double list_skin(const abs_gpu_ctx* c) {
+  if (c->cfg.neighbor_skin > 0.0) return c->cfg.neighbor_skin;
+  return 0.15 * (c->host_dmax > 0.0 ? c->host_dmax : 1.0);
+}
+
+constexpr unsigned int kListKmaxInit = 64;
+constexpr unsigned int kListKmaxMax = 255;  // u8 counts
+
+// List storage for the current population: [kmax][stride] u32 + u8 counts.
+int ensure_lists(abs_gpu_ctx* c, unsigned int kmax) {
+  const unsigned long long stride = std::max<unsigned long long>(32, (c->n + 31) / 32 * 32);
+  if (c->nl && stride <= c->nl_stride && kmax <= c->nl_kmax) return ABS_OK;
+  const unsigned long long ns = std::max(stride, c->nl_stride);
+  const unsigned int kk = std::max(kmax, c->nl_kmax);
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(c->nl);
+  cudaFree(c->nl_cnt);
+  c->nl = nullptr;
+  c->nl_cnt = nullptr;
+  c->nl_stride = 0;
+  c->nl_kmax = 0;
+  c->list_valid = false;
+  CK(dalloc(&c->nl, ns * kk));
+  CK(dalloc(&c->nl_cnt, ns));
+  c->nl_stride = ns;
+  c->nl_kmax = kk;
+  return ABS_OK;
+}
+
+cudaEvent_t* event_pair(abs_gpu_ctx* c, std::vector<cudaEvent_t>& v, size_t& used) {
+  if (used + 2 > v.size()) {
+    for (int q = 0; q < 256; ++q) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      v.push_back(e);
+    }
+  }
+  used += 2;
+  return &v[used - 2];
+}
+
+// One list iteration. kind 2: re-bin (the environment update), build the
+// lists, force sweep over them; kind 1: bounds reduction + grid sizing +
+// coverage check (finalize_grid), force sweep over the existing lists.
+void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind) {
+  const StepArgs a = step_args(c, iteration);
+  const double skin = list_skin(c);
+  Pd* pin;
+  Pd* pout;
+  if (kind == 2) {
+    launch_env_update(c, iteration, 0, true, 2, skin);
+    static int blocks = 0;
+    if (!blocks) {
+      cudaFuncSetAttribute(k_list_build, cudaFuncAttributeMaxDynamicSharedMemorySize, kListSmem);
+      blocks = force_blocks(c, k_list_build, kListSmem);
+    }
+    cudaEvent_t* ev = c->timing ? event_pair(c, c->bev, c->bev_used) : nullptr;
+    if (ev) cudaEventRecord(ev[0], c->stream);
+    k_list_build<<<blocks, kForceThreads, kListSmem, c->stream>>>(c->pf, c->g, c->start, c->nl, c->nl_cnt,
+                                                                  c->nl_stride, c->nl_kmax, skin, iteration);
+    if (ev) cudaEventRecord(ev[1], c->stream);
+    ++c->launches;
+    c->list_valid = true;
+    pin = c->S[c->cur].pd;
+    pout = c->newpd;
+    c->pos_in_new = true;
+  } else {
+    const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
+                     c->bins_cap, c->cap, c->uid_cap, 0, iteration, 1, skin};
+    pin = cur_pos(c);
+    k_reduce_finalize<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pin, c->g, fa,
+                                                                          c->grid_valid ? c->start : nullptr);
+    ++c->launches;
+    c->grid_valid = false;
+    pout = c->pos_in_new ? c->S[c->cur].pd : c->newpd;
+    c->pos_in_new = !c->pos_in_new;
+  }
+  phase_mark(c);  // after environment update
+  cudaEvent_t* ev = c->timing ? event_pair(c, c->ev, c->ev_used) : nullptr;
+  if (ev) cudaEventRecord(ev[0], c->stream);
+  const int nb = grid_blocks(c, c->cap);
+  if (c->cfg.record_forces)
+    k_force_list<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, c->S[c->cur], c->g, c->nl, c->nl_cnt, c->nl_stride,
+                                                      a, c->cap);
+  else
+    k_force_list<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
+                                                       c->nl_stride, a, c->cap);
+  if (ev) cudaEventRecord(ev[1], c->stream);
+  ++c->launches;
+  phase_mark(c);  // after agent ops
+  phase_mark(c);  // no commit
+}
+
+void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0) {
+  if (c->rec_evals && c->evc) {  // static / ghost agents evaluate nothing this iteration
+    cudaMemsetAsync(c->evc, 0, c->evc_cap * sizeof(unsigned int), c->stream);
+  }
+  if (kind) {
+    launch_list_iteration(c, iteration, kind);
+    return;
+  }
   launch_env_update(c, iteration, adds_agents(c->cfg), true);
   phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
@@ -2634,7 +2979,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_soa(c->S[1]);
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
-  cudaFree(c->xcounts); cudaFree(c->holes);
+  cudaFree(c->xcounts); cudaFree(c->holes); cudaFree(c->nl); cudaFree(c->nl_cnt); cudaFree(c->evc);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -2653,6 +2998,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   free_sort_scratch(c);
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ABS_OK;
@@ -2743,7 +3089,9 @@ static int upload_finish(abs_gpu_ctx* c, unsigned long long n, int ib) {
       mx = c->ingest_part[2 * b + 1] > mx ? c->ingest_part[2 * b + 1] : mx;
     }
     c->auto_bins = (mx > 0.0 && sum / static_cast<double>(n) > 0.75 * mx) ? 1u : 2u;
+    c->host_dmax = mx;
   }
+  c->list_valid = false;
   if (bad) {
     c->n = 0;
     CK(cudaMemsetAsync(&c->g->n, 0, 8, c->stream));
@@ -2799,6 +3147,7 @@ constexpr unsigned long long kSortChunk = 4096;
 // the device runs sort_passes, gather into the other state buffer. Callable
 // inside the iteration loop (sorting_frequency, simulation.cpp:246-247).
 static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_order) {
+  if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
   if (c->sort_cap != c->cap) {
     free_sort_scratch(c);
     const unsigned long long blocks = (c->cap + kSortChunk - 1) / kSortChunk;
@@ -2908,16 +3257,36 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   // rolled back to the failed iteration (no kernel touched state after it).
   unsigned long long done = 0;
   const unsigned long long chunk = 32;
+  // neighbour lists: storage for this population, allocated
+  // outside any graph capture
+  if (list_mode_ok(c) && iterations >= 2) {
+    if (ensure_lists(c, c->nl_kmax ? c->nl_kmax : kListKmaxInit) != ABS_OK) {
+      cudaGetLastError();
+      c->list_off = true;  // no room for the lists: re-bin + walk every iteration
+    }
+  }
   while (done < iterations) {
     const unsigned long long todo = std::min<unsigned long long>(chunk, iterations - done);
-    struct Snap { int cur; bool pos_in_new; bool grid_valid; };
+    struct Snap { int cur; bool pos_in_new; bool grid_valid; bool list_valid; };
     std::vector<Snap> snaps;
     snaps.reserve(todo);
+    std::vector<int> kinds;
+    kinds.reserve(todo);
     for (unsigned long long t = 0; t < todo; ++t) {
-      snaps.push_back({c->cur, c->pos_in_new, c->grid_valid});
+      snaps.push_back({c->cur, c->pos_in_new, c->grid_valid, c->list_valid});
       const unsigned long long it = c->iteration + t;
       const bool sorts =
           c->cfg.sorting_frequency > 0 && it % static_cast<unsigned long long>(c->cfg.sorting_frequency) == 0;
+      // iteration kind: 0 re-bin + cell-table walk, 1 list step, 2 list
+      // rebuild (a build pays off only if at least one more iteration of
+      // this call can use the lists; a sort re-orders storage)
+      const unsigned long long remaining = iterations - done - t;
+      int kind = 0;
+      if (list_mode_ok(c) && c->nl) {
+        if (c->list_valid && !sorts) kind = 1;
+        else if (remaining >= 2) kind = 2;
+      }
+      kinds.push_back(kind);
       auto enqueue = [&]() -> int {
         phase_mark(c);  // iteration start
         if (sorts) {
@@ -2925,7 +3294,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
           if (rc) return rc;
         }
         phase_mark(c);  // after sort
-        launch_iteration(c, it);
+        launch_iteration(c, it, kind);
         return ABS_OK;
       };
       // One CUDA graph per iteration (cached executable, parameters updated in
@@ -2941,7 +3310,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
         cudaGraph_t graph = nullptr;
         if (ok) ok = cudaStreamEndCapture(c->stream, &graph) == cudaSuccess && graph && rc == ABS_OK;
         if (ok) {
-          const int slot = sorts ? 1 : 0;
+          const int slot = (sorts ? 1 : 0) + 2 * kind;
           if (c->gexec[slot]) {
             cudaGraphExecUpdateResultInfo info;
             if (cudaGraphExecUpdate(c->gexec[slot], graph, &info) != cudaSuccess) {
@@ -2962,6 +3331,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
         c->cur = sn.cur;
         c->pos_in_new = sn.pos_in_new;
         c->grid_valid = sn.grid_valid;
+        c->list_valid = sn.list_valid;
         c->launches = launches0;
         c->scan_epoch = epoch0;
         if (++c->graph_failures >= 4) c->graphs_off = true;
@@ -2975,7 +3345,14 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     DevGrid h{};
     int rc = read_grid(c, &h);
     if (rc) return rc;
+    auto count_kinds = [&](unsigned long long upto) {
+      for (unsigned long long q = 0; q < upto && q < kinds.size(); ++q) {
+        c->list_builds += kinds[q] == 2;
+        c->list_steps += kinds[q] != 0;
+      }
+    };
     if (h.err == kErrNone) {
+      count_kinds(todo);
       if (h.n) std::memcpy(c->sort_guess_dims, h.dims, sizeof c->sort_guess_dims);
       // Auto sub-bins (bins_yz): a crowded grid (config 2 once its cells have
       // grown: ~14 agents per box, 106 evaluations per agent) needs the row
@@ -2996,6 +3373,8 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     c->cur = snaps[off].cur;
     c->pos_in_new = snaps[off].pos_in_new;
     c->grid_valid = false;  // finalize may have left a partially filled count table
+    c->list_valid = snaps[off].list_valid;
+    count_kinds(off);
     c->iteration = fi;
     done += off;
     if (h.err == kErrBinsRetry) {
@@ -3009,6 +3388,20 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       c->sort_radix_iteration = fi;
       if (env_flag("ABSIM_SORT_GUESS_COUNTING", false)) std::fprintf(stderr, "absim: sort retry at iteration %llu\n", fi);
       CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+    } else if (h.err == kErrListRebuild) {  // the lists no longer cover r: rebuild at this iteration
+      c->list_valid = false;
+      rc = clear_dev_err(c);
+      if (rc) return rc;
+    } else if (h.err == kErrListOverflow) {  // more candidates than the list holds: grow, rebuild
+      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
+      c->list_valid = false;
+      const unsigned int need = h.list_need;
+      if (need > kListKmaxMax || ensure_lists(c, std::min(kListKmaxMax, need + need / 4 + 8)) != ABS_OK) {
+        cudaGetLastError();
+        c->list_off = true;
+      }
       rc = clear_dev_err(c);
       if (rc) return rc;
     } else if (h.err == kErrCapRetry) {
@@ -3118,6 +3511,7 @@ int abs_gpu_set_grid_override(abs_gpu_ctx* c, const double* grid, const uint32_t
     if (!(grid[3] > 0.0) || !dims[0] || !dims[1] || !dims[2])
       return set_err(c, ABS_ERR_INVALID_ARGUMENT, "bad grid override");
   }
+  c->ov_on = ov.on != 0;
   CK(cudaMemcpyAsync(&c->g->ov_on, &ov.on, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->g->ov_grid, ov.g, sizeof ov.g, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->g->ov_dims, ov.d, sizeof ov.d, cudaMemcpyHostToDevice, c->stream));
@@ -3146,6 +3540,7 @@ int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
 
 // Keep only agents with keep[i] (already filled for the current population).
 static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
+  if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
   unsigned int* keep = c->rank;  // scratch: rank[] is rewritten by the next k_key
   unsigned int* idx = c->key;
   CK(cudaMemcpyAsync(idx, keep, n * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -3214,6 +3609,7 @@ int abs_gpu_export_layers(abs_gpu_ctx* c, const double* grid, const uint32_t* di
 }
 
 int abs_gpu_import(abs_gpu_ctx* c, const void* records, uint64_t count, int as_ghost) {
+  if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
   if (!c || (count && !records)) return ABS_ERR_INVALID_ARGUMENT;
   if (!count) return ABS_OK;
   cudaSetDevice(c->device);
@@ -3606,6 +4002,7 @@ int abs_gpu_sort(abs_gpu_ctx* c) {
 }
 
 int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
+  if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (r == 0) return ABS_OK;
   if (adds_agents(c->cfg)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, kReorderWithAdditions);
@@ -3726,10 +4123,61 @@ int abs_gpu_phase_times(abs_gpu_ctx* c, double* out4, double* per_iteration_ms, 
   return ABS_OK;
 }
 
+int abs_gpu_record_evaluations(abs_gpu_ctx* c, int enable) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  c->rec_evals = enable != 0;
+  if (c->rec_evals && c->evc_cap < c->cap) {
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->evc);
+    c->evc = nullptr;
+    c->evc_cap = 0;
+    CK(dalloc(&c->evc, c->cap));
+    CK(cudaMemsetAsync(c->evc, 0, c->cap * sizeof(unsigned int), c->stream));
+    c->evc_cap = c->cap;
+  }
+  return ABS_OK;
+}
+
+int abs_gpu_download_evaluations(abs_gpu_ctx* c, uint32_t* out, uint64_t cap) {
+  if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
+  if (!c->evc) return set_err(c, ABS_ERR_STATE, "evaluation recording is off (abs_gpu_record_evaluations)");
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (cap < h.n) return set_err(c, ABS_ERR_CAPACITY, "output holds fewer entries than agents");
+  CK(cudaMemcpy(out, c->evc, h.n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+  return ABS_OK;
+}
+
+int abs_gpu_list_stats(abs_gpu_ctx* c, uint64_t* out4, double* build_ms) {
+  if (!c) return ABS_ERR_INVALID_ARGUMENT;
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t q = 0; q + 1 < c->bev_used; q += 2) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->bev[q], c->bev[q + 1]));
+    c->build_ms += ms;
+    ++c->build_launches;
+  }
+  c->bev_used = 0;
+  unsigned int need = 0;
+  CK(cudaMemcpy(&need, &c->g->list_need, sizeof need, cudaMemcpyDeviceToHost));
+  if (out4) {
+    out4[0] = c->list_builds;
+    out4[1] = c->list_steps;
+    out4[2] = c->build_launches;
+    out4[3] = need;
+  }
+  if (build_ms) *build_ms = c->build_ms;
+  return ABS_OK;
+}
+
 int abs_gpu_reset_timers(abs_gpu_ctx* c, int enable) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   CK(cudaStreamSynchronize(c->stream));
   c->ev_used = 0;
+  c->bev_used = 0;
+  c->build_ms = 0.0;
+  c->build_launches = 0;
   c->force_ms = 0.0;
   c->force_launches = 0;
   c->pev_used = 0;

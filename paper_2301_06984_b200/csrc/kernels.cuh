@@ -48,6 +48,8 @@ enum DevErr : int {
   kErrCapRetry = 5,   // internal: grow agent capacity and re-run the iteration
   kErrQueryRadius = 6,  // a behaviour's query radius exceeds the box (uniform_grid.cpp:176-181)
   kErrSortRetry = 7,    // internal: the host's counting-sort guess did not fit; re-run with the exact path
+  kErrListRebuild = 8,  // internal: the neighbour lists no longer cover the query radius; re-run as a rebuild
+  kErrListOverflow = 9, // internal: an agent has more list candidates than the list holds; grow and re-run
 };
 
 // Grid + bookkeeping living in device memory (one per context).
@@ -92,6 +94,11 @@ struct DevGrid {
   unsigned long long sort_len;  // counting mode: Morton code space (cell-table entries used)
   unsigned int sort_mode;       // 1 counting sort by code (in-box order free), 0 exact radix path
   unsigned int pad3;
+  // --- neighbour lists ---
+  double list_acc;              // sum over steps since the last build of the largest displacement (+ margin)
+  double list_dmax;             // largest diameter when the lists were built
+  unsigned int step_disp;       // float bits of this step's largest displacement (atomicMax)
+  unsigned int list_need;       // largest candidate count seen by the last build
 };
 
 struct StepArgs {
@@ -103,6 +110,7 @@ struct StepArgs {
   int detect_static;
   int record_forces;
   int brute;  // BruteForceEnvironment: no maximum query radius
+  unsigned int* evc;  // per-agent force evaluations of the step (parity hook; nullptr = off)
 };
 
 // Order-preserving double <-> u64 map for atomicMin/atomicMax.
@@ -498,6 +506,102 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) visit(idx[u], df2[u], qf[u].w, in[u]);
+  }
+}
+
+// Candidate walk of the neighbour-list build: every agent j != self whose
+// fp32 squared distance (relative coordinates from `pf`) is <= rf2 — a
+// conservative superset of the exact fp64 ball of radius R when
+// rf >= R * (1 + 1e-6) + slack. Rows cover the whole ball, clamped to the
+// grid only (NOT to the reference's 3x3x3 boxes: R = r + skin may exceed the
+// box, and the list must hold every agent that can come within r before the
+// next rebuild). Same two-phase row windows as for_each_neighbor_flat32.
+template <class F>
+__device__ __forceinline__ void for_each_candidate32(const QGrid& g, const float4* __restrict__ pf,
+                                                     const unsigned int* __restrict__ start,
+                                                     unsigned int (*wj0)[kForceThreads],
+                                                     unsigned short (*wj1)[kForceThreads], unsigned int self,
+                                                     float fx, float fy, float fz, float rf, F&& visit) {
+  const int t = threadIdx.x;
+  const float rf2 = rf * rf;
+  const int z0 = fbin(fz - rf, g.inv_s[2], g.bd[2]), z1 = fbin(fz + rf, g.inv_s[2], g.bd[2]);
+  const int y0 = fbin(fy - rf, g.inv_s[1], g.bd[1]), y1 = fbin(fy + rf, g.inv_s[1], g.bd[1]);
+  auto test = [&](unsigned int j, const float4& qf, bool valid) {
+    const float ex = fx - qf.x, ey = fy - qf.y, ez = fz - qf.z;
+    const float df2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
+    if (valid && j != self && df2 <= rf2) visit(j);
+  };
+  int nr = 0;
+  for (int bz = z0; bz <= z1; ++bz) {
+    const float zl = static_cast<float>(bz) * g.s[2];
+    const float gz = fmaxf(fmaxf(zl - fz, fz - (zl + g.s[2])), 0.0f);
+    for (int by = y0; by <= y1; ++by) {
+      const float yl = static_cast<float>(by) * g.s[1];
+      const float gy = fmaxf(fmaxf(yl - fy, fy - (yl + g.s[1])), 0.0f);
+      const float rem = rf2 - (gy * gy + gz * gz);
+      if (rem < 0.0f) continue;
+      const float w = cull_sqrt(rem);
+      const int x0 = fbin(fx - w, g.inv_s[0], g.bd[0]);
+      const int x1 = fbin(fx + w, g.inv_s[0], g.bd[0]);
+      const unsigned int row = g.bd[0] * row_of(static_cast<unsigned int>(by), static_cast<unsigned int>(bz), g.ysh, g.bd[2]);
+      if (nr < kMaxRows) {
+        wj0[nr][t] = row + x0;
+        wj1[nr][t] = static_cast<unsigned short>(x1 + 1 - x0);
+        ++nr;
+      } else {  // overflow rows: direct walk
+        const unsigned int j1 = __ldg(start + row + x1 + 1);
+        for (unsigned int j = __ldg(start + row + x0); j < j1; ++j) test(j, __ldg(pf + j), true);
+      }
+    }
+  }
+  constexpr int kRowBatch = 4;
+  int nw = 0;
+  unsigned int total = 0;
+  for (int r0 = 0; r0 < nr; r0 += kRowBatch) {
+    unsigned int lo[kRowBatch], hi[kRowBatch];
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      const int q = min(r0 + u, nr - 1);
+      const unsigned int b0 = wj0[q][t];
+      lo[u] = __ldg(start + b0);
+      hi[u] = __ldg(start + b0 + wj1[q][t]);
+    }
+#pragma unroll
+    for (int u = 0; u < kRowBatch; ++u) {
+      if (r0 + u < nr && hi[u] > lo[u]) {
+        if (total + (hi[u] - lo[u]) > 0xFFFFu) {
+          for (unsigned int j = lo[u]; j < hi[u]; ++j) test(j, __ldg(pf + j), true);
+          continue;
+        }
+        wj0[nw][t] = lo[u] - total;
+        total += hi[u] - lo[u];
+        wj1[nw][t] = static_cast<unsigned short>(total);
+        ++nw;
+      }
+    }
+  }
+  if (nw == 0) return;
+  int k = 0;
+  unsigned int off = wj0[0][t], bnd = wj1[0][t];
+  for (unsigned int p = 0; p < total;) {
+    unsigned int idx[kBatch];
+    bool val[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      val[u] = p < total;
+      idx[u] = val[u] ? p + off : self;
+      ++p;
+      if (p == bnd) {
+        k = min(k + 1, nw - 1);
+        off = wj0[k][t];
+        bnd = wj1[k][t];
+      }
+    }
+    float4 qf[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pf + idx[u]);
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) test(idx[u], qf[u], val[u]);
   }
 }
 

@@ -63,6 +63,11 @@ class SimulationParams:
     bins_per_box_x: int = 0    # sub-bins per box edge along x (0 = auto)
     # EnvironmentKind (params.hpp:9): "uniform_grid" or "brute_force"
     environment: str = "uniform_grid"
+    # per-agent candidate lists between environment rebuilds:
+    # True = auto (used when the path allows it), False = re-bin every step;
+    # neighbor_skin 0 = 0.15 x the largest diameter
+    neighbor_list: bool = True
+    neighbor_skin: float = 0.0
 
     def validate(self):
         """SimulationParams::validate (params.cpp:44-72), hot-path subset."""
@@ -101,6 +106,8 @@ class SimulationParams:
         c.bins_per_box = self.bins_per_box
         c.bins_per_box_x = self.bins_per_box_x
         c.environment = ENVIRONMENTS[self.environment]
+        c.neighbor_list = 0 if self.neighbor_list else -1
+        c.neighbor_skin = float(self.neighbor_skin)
         return c
 
 
@@ -429,6 +436,25 @@ class Simulation:
     # -- timing of the dominant kernel --------------------------------------
     def reset_timers(self, enable: bool = True):
         N.check(N.load().abs_gpu_reset_timers(self._ctx, 1 if enable else 0), self._ctx)
+
+    def list_stats(self) -> dict:
+        """Neighbour-list counters (abs_gpu_list_stats): builds, list steps,
+        timed build launches + their CUDA-event ms, largest candidate count."""
+        out = np.zeros(4, np.uint64)
+        ms = C.c_double(0)
+        N.check(N.load().abs_gpu_list_stats(self._ctx, _p(out, C.c_uint64), C.byref(ms)), self._ctx)
+        return {"builds": int(out[0]), "list_steps": int(out[1]), "build_launches": int(out[2]),
+                "max_candidates": int(out[3]), "build_ms": ms.value}
+
+    def record_evaluations(self, enable: bool = True):
+        """Record every agent's force evaluations per iteration (parity hook)."""
+        N.check(N.load().abs_gpu_record_evaluations(self._ctx, 1 if enable else 0), self._ctx)
+
+    def evaluations(self) -> np.ndarray:
+        """Per-agent force evaluations of the last iteration, download order."""
+        out = np.zeros(max(1, self.agent_count()), np.uint32)
+        N.check(N.load().abs_gpu_download_evaluations(self._ctx, _p(out, C.c_uint32), len(out)), self._ctx)
+        return out[:self.agent_count()]
 
     def force_kernel_time(self):
         ms = C.c_double(0)
