@@ -250,6 +250,13 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
     g->list_dmax = g->dmax;
     g->step_disp = 0u;
     g->list_need = 0u;
+    double ext = 1.0;
+    for (int k = 0; k < 3; ++k) {
+      g->lorigin[k] = g->origin[k];
+      ext = fmax(ext, static_cast<double>(g->dims[k]) * g->box);
+    }
+    // relative coordinates stay within ext + skin / 2 while the lists are valid
+    g->lslack = static_cast<float>(16.0 * (ext + fa.skin + 1.0) * 0x1.0p-24 + 1e-5);
   } else if (fa.list_mode == 1 && err == kErrNone) {
     const double acc = g->list_acc + static_cast<double>(__uint_as_float(g->step_disp)) + g->margin + 1e-12;
     g->list_acc = acc;
@@ -1176,13 +1183,23 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
 // finalize_grid before every list step; a failed check re-runs the
 // iteration as a rebuild).
 //
+// Candidates are classified in fp32 against float4 copies relative to the
+// build origin (`pf`, rewritten by every list step) with the proven margin of
+// for_each_neighbor_flat32 (slack from the build extent + skin); only the
+// margin band reads the fp64 record. Possible contacts go to a per-lane
+// shared-memory list and pairwise_repulsion runs on them afterwards with all
+// lanes busy (the fp64 sqrt/division would otherwise run at ~8 of 32 lanes).
+//
 // k_list_build: after the re-bin, every agent's candidates within r + skin
-// (fp32 superset, no 3x3x3 box clamp) into list[k * stride + i] — column k
-// of all agents is contiguous, so the list sweep's index loads coalesce.
+// (fp32 superset, no 3x3x3 box clamp: r + skin may exceed the box) are staged
+// per lane in shared memory and written out as list[k * stride + i] — column
+// k of all agents is contiguous, so both the write-out and the list sweep's
+// index loads coalesce.
 #ifndef ABS_LIST_MIN_BLOCKS
-#define ABS_LIST_MIN_BLOCKS 6
+#define ABS_LIST_MIN_BLOCKS 5
 #endif
-constexpr int kListSmem = (kMaxRows + kMaxRows / 2) * kForceThreads * 4;
+constexpr int kListStage = 64;  // candidates staged per lane before the coalesced write-out
+constexpr int kListSmem = (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads * 4;
 
 __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
     k_list_build(const float4* __restrict__ pf, DevGrid* g, const unsigned int* __restrict__ start,
@@ -1193,11 +1210,13 @@ __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned int force_smem[];
   auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
   auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  auto stage = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + (kMaxRows + kMaxRows / 2) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*g);
   __syncthreads();
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
   const int lane = threadIdx.x & 31;
+  const unsigned int kst = kmax < kListStage ? kmax : kListStage;
   unsigned int most = 0;
   const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
   const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1205,22 +1224,28 @@ __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
     const unsigned long long base = chunk * 32ull;
     if (base >= n) break;
     const unsigned long long i = base + lane;
+    unsigned int c = 0;
     if (i < n) {
       const float4 me = __ldg(pf + i);
       // pf.w is the diameter rounded to fp32 (relative error 2^-24); the
       // 2e-6 inflation of rf covers it and the rounding of R
       const double R = 0.5 * (static_cast<double>(me.w) + dmax) + skin;
       const float rf = static_cast<float>(R) * 1.000002f + Q.slack + 1e-6f;
-      unsigned int c = 0;
       unsigned int* col = list + i;
       for_each_candidate32(Q, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, rf,
                            [&](unsigned int j) {
-                             if (c < kmax) col[c * stride] = j;
+                             if (c < kst) stage[c][threadIdx.x] = j;
+                             else if (c < kmax) col[c * stride] = j;
                              ++c;
                            });
       cnt[i] = static_cast<unsigned char>(c < kmax ? c : kmax);
-      most = c > most ? c : most;
     }
+    // coalesced write-out of the staged columns: entry k of the warp's 32 agents
+    const unsigned int cs = c < kst ? c : kst;
+    const unsigned int wmax = __reduce_max_sync(0xffffffffu, cs);
+    for (unsigned int k = 0; k < wmax; ++k)
+      if (k < cs) list[k * stride + i] = stage[k][threadIdx.x];
+    most = c > most ? c : most;
   }
   most = __reduce_max_sync(0xffffffffu, most);
   if (lane == 0 && most) {
@@ -1230,25 +1255,34 @@ __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
 }
 
 // k_force_list: run_forces + apply_pending (simulation.cpp:463-500,
-// mechanics.cpp:10-27, agent.hpp:115-133) over the list — for every listed
-// j the reference's exact d2 <= r^2 (a force evaluation), then
-// pairwise_repulsion with the reference's operations; a pair whose d2 is at
-// least h^2 (1 + 2^-50) has dist >= h, i.e. overlap <= 0, and skips the
-// sqrt. Positions are read from `pin` and written to `pout` (ping-pong). The
+// mechanics.cpp:10-27, agent.hpp:115-133) over the list. Pass A classifies
+// every listed j (the reference's exact d2 <= r^2 decides: fp32 outside the
+// margin band, fp64 inside it) and records possible contacts; pass B runs
+// pairwise_repulsion on them with the reference's operations. Positions are
+// read from `pin`/`pfin` and written to `pout`/`pfout` (ping-pong). The
 // step's largest displacement is folded into g->step_disp for the coverage
 // check of the next step.
 #ifndef ABS_LIST_FORCE_MIN_BLOCKS
 #define ABS_LIST_FORCE_MIN_BLOCKS 3
 #endif
+constexpr int kListContacts = 16;
+constexpr int kListForceSmem = kListContacts * kThreads * 4;
+
 template <bool RECORD>
 __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
-    k_force_list(const Pd* __restrict__ pin, Pd* __restrict__ pout, Soa S, DevGrid* g,
-                 const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt,
-                 unsigned long long stride, StepArgs a, unsigned long long cap) {
+    k_force_list(const Pd* __restrict__ pin, const float4* __restrict__ pfin, Pd* __restrict__ pout,
+                 float4* __restrict__ pfout, Soa S, DevGrid* g, const unsigned int* __restrict__ list,
+                 const unsigned char* __restrict__ cnt, unsigned long long stride, StepArgs a,
+                 unsigned long long cap) {
   if (g->err) return;
+  extern __shared__ __align__(16) unsigned int force_smem[];
+  auto ovl = reinterpret_cast<unsigned int (*)[kThreads]>(force_smem);
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
   const double k = a.k;
+  const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
+  const float slack = g->lslack;
+  const double sl = static_cast<double>(slack);
   unsigned long long n_eval = 0;
   float moved = 0.0f;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
@@ -1257,63 +1291,84 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
     const unsigned int c = cnt[i];
     const double r = 0.5 * (me.d + dmax);
     const double r2 = r * r;
+    // fp32 classification thresholds (for_each_neighbor_flat32)
+    const double rin = r - sl;
+    const float rin2 = rin > 0.0 ? __double2float_rd(rin * rin * (1.0 - 0x1.0p-40)) : -1.0f;
+    const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
+    const float fx = static_cast<float>(me.x - lox), fy = static_cast<float>(me.y - loy),
+                fz = static_cast<float>(me.z - loz);
+    const float hme = 0.5f * static_cast<float>(me.d) + slack;
     const unsigned int* col = list + i;
-    unsigned int evals = 0, contributors = 0;
-    double fx = 0.0, fy = 0.0, fz = 0.0;
+    unsigned int evals = 0, nov = 0;
     for (unsigned int s = 0; s < c; s += kBatch) {
       unsigned int jj[kBatch];
-      Pd q[kBatch];
+      float4 qf[kBatch];
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) jj[u] = __ldg(col + static_cast<unsigned long long>(min(s + u, c - 1)) * stride);
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pin + jj[u]);
-      // radius test for the batch; pairs that may overlap are re-read and
-      // handled afterwards, so no record stays live across the fp64
-      // sqrt/division slow paths
-      unsigned int contact = 0;
+      for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
 #pragma unroll
       for (int u = 0; u < kBatch; ++u) {
-        const double dx = me.x - q[u].x, dy = me.y - q[u].y, dz = me.z - q[u].z;
-        const double d2 = (dx * dx + dy * dy) + dz * dz;
-        const bool in = s + u < c && d2 <= r2;
+        const float ex = fx - qf[u].x, ey = fy - qf[u].y, ez = fz - qf[u].z;
+        const float df2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
+        bool in = s + u < c && df2 <= rout2;
+        if (in && df2 > rin2) {  // margin band: the reference's exact fp64 test
+          const Pd q = load_pd(pin + jj[u]);
+          const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+          in = (dx * dx + dy * dy) + dz * dz <= r2;
+        }
         evals += in;
-        const double h = 0.5 * (me.d + q[u].d);
-        contact |= (in && d2 < h * h * (1.0 + 0x1.0p-50)) ? (1u << u) : 0u;
-      }
-      while (contact) {
-        const int u = __ffs(contact) - 1;
-        contact &= contact - 1;
-        const unsigned int j = jj[u];
-        const Pd qq = load_pd(pin + j);
-        const double dx = me.x - qq.x, dy = me.y - qq.y, dz = me.z - qq.z;
-        // pairwise_repulsion (mechanics.cpp:10-27)
-        const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
-        const double overlap = 0.5 * (me.d + qq.d) - dist;
-        if (overlap <= 0.0) continue;
-        double f0, f1, f2;
-        if (dist > 0.0) {
-          const double sc = k * overlap / dist;
-          f0 = dx * sc;
-          f1 = dy * sc;
-          f2 = dz * sc;
-        } else {
-          coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
-        }
-        if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
-          ++contributors;
-          fx += f0;
-          fy += f1;
-          fz += f2;
-        }
+        // contact superset: df2 < (0.5 (d_i + d_j) + slack)^2 (1 + 5e-7)
+        const float hp = __fmaf_rn(0.5f, qf[u].w, hme);
+        const bool ct = in && df2 < hp * hp * 1.0000005f;
+        if (ct && nov < kListContacts) ovl[nov][threadIdx.x] = jj[u];
+        nov += ct;
       }
     }
     n_eval += evals;
     if (a.evc) a.evc[i] = evals;
+    unsigned int contributors = 0;
+    double fx64 = 0.0, fy64 = 0.0, fz64 = 0.0;
+    auto contact = [&](unsigned int j) {
+      const Pd q = load_pd(pin + j);
+      const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+      // pairwise_repulsion (mechanics.cpp:10-27)
+      const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
+      const double overlap = 0.5 * (me.d + q.d) - dist;
+      if (overlap <= 0.0) return;
+      double f0, f1, f2;
+      if (dist > 0.0) {
+        const double sc = k * overlap / dist;
+        f0 = dx * sc;
+        f1 = dy * sc;
+        f2 = dz * sc;
+      } else {
+        coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
+      }
+      if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
+        ++contributors;
+        fx64 += f0;
+        fy64 += f1;
+        fz64 += f2;
+      }
+    };
+    if (nov <= kListContacts) {
+      for (unsigned int q = 0; q < nov; ++q) contact(ovl[q][threadIdx.x]);
+    } else {  // more possible contacts than the shared list holds: re-scan (rare)
+      for (unsigned int s = 0; s < c; ++s) {
+        const unsigned int j = __ldg(col + static_cast<unsigned long long>(s) * stride);
+        const Pd q = load_pd(pin + j);
+        const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+        const double d2 = (dx * dx + dy * dy) + dz * dz;
+        const double h = 0.5 * (me.d + q.d);
+        if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact(j);
+      }
+    }
     double tx = 0.0, ty = 0.0, tz = 0.0;
-    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
-      tx = fx * a.dt;
-      ty = fy * a.dt;
-      tz = fz * a.dt;
+    if ((fx64 * fx64 + fy64 * fy64) + fz64 * fz64 > a.threshold2) {
+      tx = fx64 * a.dt;
+      ty = fy64 * a.dt;
+      tz = fz64 * a.dt;
     }
     Pd np = me;
     const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
@@ -1334,13 +1389,15 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
       moved = fmaxf(moved, __double2float_ru(md * (1.0 + 0x1.0p-40)));
     }
     if (RECORD) {
-      S.force[i] = fx;
-      S.force[cap + i] = fy;
-      S.force[2 * cap + i] = fz;
+      S.force[i] = fx64;
+      S.force[cap + i] = fy64;
+      S.force[2 * cap + i] = fz64;
     }
     S.partners[i] = contributors;
     reinterpret_cast<double2*>(pout + i)[0] = make_double2(np.x, np.y);
     reinterpret_cast<double2*>(pout + i)[1] = make_double2(np.z, np.d);
+    pfout[i] = make_float4(static_cast<float>(np.x - lox), static_cast<float>(np.y - loy),
+                           static_cast<float>(np.z - loz), static_cast<float>(np.d));
   }
   const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
   if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
@@ -2178,6 +2235,8 @@ struct abs_gpu_ctx {
   cudaGraphExec_t gexec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // neighbour lists
   unsigned int* nl = nullptr;           // [kmax][stride] candidate storage indices
+  float4* pf2 = nullptr;                // fp32 copy paired with newpd (pf is paired with S[cur].pd)
+  unsigned long long pf2_cap = 0;
   unsigned char* nl_cnt = nullptr;      // [stride] candidates per agent
   unsigned long long nl_stride = 0;
   unsigned int nl_kmax = 0;
@@ -2185,6 +2244,9 @@ struct abs_gpu_ctx {
   bool list_off = false;                // lists disabled for this context (candidate count > 255)
   bool ov_on = false;                   // host mirror of the multi-domain grid override
   double host_dmax = 0.0;               // largest diameter of the last upload (auto skin)
+  // host prediction of the device coverage check: accumulated displacement
+  // the next list step will see, and the last step's largest displacement
+  double pred_acc = 0.0, pred_rate = 0.0;
   double build_ms = 0.0;
   unsigned long long build_launches = 0;
   std::vector<cudaEvent_t> bev;  // pairs around k_list_build (timing on)
@@ -2355,6 +2417,9 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag);
   cudaFree(c->pf);
   c->pf = nullptr;
+  cudaFree(c->pf2);
+  c->pf2 = nullptr;
+  c->pf2_cap = 0;
   CK(dalloc(&c->pf, ncap));
   CK(dalloc(&c->key, ncap));
   CK(dalloc(&c->rank, ncap));
@@ -2649,6 +2714,15 @@ constexpr unsigned int kListKmaxMax = 255;  // u8 counts
 // List storage for the current population: [kmax][stride] u32 + u8 counts.
 int ensure_lists(abs_gpu_ctx* c, unsigned int kmax) {
   const unsigned long long stride = std::max<unsigned long long>(32, (c->n + 31) / 32 * 32);
+  if (c->pf2_cap < c->cap) {
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(c->pf2);
+    c->pf2 = nullptr;
+    c->pf2_cap = 0;
+    c->list_valid = false;
+    CK(dalloc(&c->pf2, c->cap));
+    c->pf2_cap = c->cap;
+  }
   if (c->nl && stride <= c->nl_stride && kmax <= c->nl_kmax) return ABS_OK;
   const unsigned long long ns = std::max(stride, c->nl_stride);
   const unsigned int kk = std::max(kmax, c->nl_kmax);
@@ -2682,11 +2756,15 @@ cudaEvent_t* event_pair(abs_gpu_ctx* c, std::vector<cudaEvent_t>& v, size_t& use
 // One list iteration. kind 2: re-bin (the environment update), build the
 // lists, force sweep over them; kind 1: bounds reduction + grid sizing +
 // coverage check (finalize_grid), force sweep over the existing lists.
+// Positions and their fp32 copies travel in pairs: (S[cur].pd, pf) and
+// (newpd, pf2).
 void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind) {
   const StepArgs a = step_args(c, iteration);
   const double skin = list_skin(c);
   Pd* pin;
   Pd* pout;
+  float4* fin;
+  float4* fout;
   if (kind == 2) {
     launch_env_update(c, iteration, 0, true, 2, skin);
     static int blocks = 0;
@@ -2702,29 +2780,40 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     ++c->launches;
     c->list_valid = true;
     pin = c->S[c->cur].pd;
+    fin = c->pf;
     pout = c->newpd;
+    fout = c->pf2;
     c->pos_in_new = true;
   } else {
     const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
                      c->bins_cap, c->cap, c->uid_cap, 0, iteration, 1, skin};
-    pin = cur_pos(c);
+    const bool from_new = c->pos_in_new;
+    pin = from_new ? c->newpd : c->S[c->cur].pd;
+    fin = from_new ? c->pf2 : c->pf;
+    pout = from_new ? c->S[c->cur].pd : c->newpd;
+    fout = from_new ? c->pf : c->pf2;
     k_reduce_finalize<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pin, c->g, fa,
                                                                           c->grid_valid ? c->start : nullptr);
     ++c->launches;
     c->grid_valid = false;
-    pout = c->pos_in_new ? c->S[c->cur].pd : c->newpd;
-    c->pos_in_new = !c->pos_in_new;
+    c->pos_in_new = !from_new;
   }
   phase_mark(c);  // after environment update
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_force_list<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kListForceSmem);
+    cudaFuncSetAttribute(k_force_list<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kListForceSmem);
+    configured = true;
+  }
   cudaEvent_t* ev = c->timing ? event_pair(c, c->ev, c->ev_used) : nullptr;
   if (ev) cudaEventRecord(ev[0], c->stream);
   const int nb = grid_blocks(c, c->cap);
   if (c->cfg.record_forces)
-    k_force_list<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, c->S[c->cur], c->g, c->nl, c->nl_cnt, c->nl_stride,
-                                                      a, c->cap);
+    k_force_list<true><<<nb, kThreads, kListForceSmem, c->stream>>>(pin, fin, pout, fout, c->S[c->cur], c->g, c->nl,
+                                                                    c->nl_cnt, c->nl_stride, a, c->cap);
   else
-    k_force_list<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
-                                                       c->nl_stride, a, c->cap);
+    k_force_list<false><<<nb, kThreads, kListForceSmem, c->stream>>>(pin, fin, pout, fout, c->S[c->cur], c->g,
+                                                                     c->nl, c->nl_cnt, c->nl_stride, a, c->cap);
   if (ev) cudaEventRecord(ev[1], c->stream);
   ++c->launches;
   phase_mark(c);  // after agent ops
@@ -2980,6 +3069,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
   cudaFree(c->xcounts); cudaFree(c->holes); cudaFree(c->nl); cudaFree(c->nl_cnt); cudaFree(c->evc);
+  cudaFree(c->pf2);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -3281,10 +3371,20 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       // rebuild (a build pays off only if at least one more iteration of
       // this call can use the lists; a sort re-orders storage)
       const unsigned long long remaining = iterations - done - t;
+      // The host predicts the device's coverage check from the last observed
+      // displacement rate and schedules the rebuild itself, so a rejected list
+      // step (rolled back with the rest of its chunk) stays the exception.
       int kind = 0;
       if (list_mode_ok(c) && c->nl) {
-        if (c->list_valid && !sorts) kind = 1;
-        else if (remaining >= 2) kind = 2;
+        const double skin = list_skin(c);
+        const bool usable = c->list_valid && !sorts;
+        if (usable && (2.0 * c->pred_acc <= skin || remaining < 2)) {
+          kind = 1;
+          c->pred_acc += c->pred_rate;
+        } else if (remaining >= 2) {
+          kind = 2;
+          c->pred_acc = c->pred_rate;
+        }
       }
       kinds.push_back(kind);
       auto enqueue = [&]() -> int {
@@ -3345,6 +3445,13 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     DevGrid h{};
     int rc = read_grid(c, &h);
     if (rc) return rc;
+    {  // the prediction restarts from the device's own numbers
+      float rate = 0.0f;
+      std::memcpy(&rate, &h.step_disp, sizeof rate);
+      const double margin = h.margin + 1e-12;
+      c->pred_acc = h.list_acc + static_cast<double>(rate) + margin;
+      if (rate > 0.0f) c->pred_rate = static_cast<double>(rate) + margin;
+    }
     auto count_kinds = [&](unsigned long long upto) {
       for (unsigned long long q = 0; q < upto && q < kinds.size(); ++q) {
         c->list_builds += kinds[q] == 2;

@@ -99,6 +99,9 @@ struct DevGrid {
   double list_dmax;             // largest diameter when the lists were built
   unsigned int step_disp;       // float bits of this step's largest displacement (atomicMax)
   unsigned int list_need;       // largest candidate count seen by the last build
+  double lorigin[3];            // grid origin at the build: list steps classify in fp32 relative to it
+  float lslack;                 // fp32 classification slack of the list steps (build extent + skin)
+  unsigned int pad4;
 };
 
 struct StepArgs {
