@@ -250,6 +250,7 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
     g->list_dmax = g->dmax;
     g->step_disp = 0u;
     g->list_need = 0u;
+    g->list_incomplete = 0u;
     double ext = 1.0;
     for (int k = 0; k < 3; ++k) {
       g->lorigin[k] = g->origin[k];
@@ -261,7 +262,7 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
     const double acc = g->list_acc + static_cast<double>(__uint_as_float(g->step_disp)) + g->margin + 1e-12;
     g->list_acc = acc;
     g->step_disp = 0u;
-    if (2.0 * acc > fa.skin || g->dmax > g->list_dmax) err = kErrListRebuild;
+    if (2.0 * acc > fa.skin || g->dmax > g->list_dmax || g->list_incomplete) err = kErrListRebuild;
   }
   reset_reduction(g);
   g->work = 0;
@@ -1192,19 +1193,20 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
 //
 // k_list_build: after the re-bin, every agent's candidates within r + skin
 // (fp32 superset, no 3x3x3 box clamp: r + skin may exceed the box) are staged
-// per lane in shared memory and written out as list[k * stride + i] — column
-// k of all agents is contiguous, so both the write-out and the list sweep's
-// index loads coalesce.
+// per lane in shared memory and written out warp-blocked: entry k of agent i
+// lives at list[(i / 32) * kmax * 32 + k * 32 + i % 32], so a warp's list is
+// one contiguous kmax x 128 B block — the write-out and the list sweep's index
+// loads are full-line, sequential accesses.
 #ifndef ABS_LIST_MIN_BLOCKS
 #define ABS_LIST_MIN_BLOCKS 5
 #endif
 constexpr int kListStage = 64;  // candidates staged per lane before the coalesced write-out
+constexpr unsigned char kListOverflow = 255;  // count sentinel: the agent's candidates did not fit
 constexpr int kListSmem = (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads * 4;
 
 __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
     k_list_build(const float4* __restrict__ pf, DevGrid* g, const unsigned int* __restrict__ start,
-                 unsigned int* __restrict__ list, unsigned char* __restrict__ cnt, unsigned long long stride,
-                 unsigned int kmax, double skin, unsigned long long iteration) {
+                 unsigned int* __restrict__ list, unsigned char* __restrict__ cnt, unsigned int kmax, double skin) {
   if (g->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
@@ -1231,106 +1233,187 @@ __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
       // 2e-6 inflation of rf covers it and the rounding of R
       const double R = 0.5 * (static_cast<double>(me.w) + dmax) + skin;
       const float rf = static_cast<float>(R) * 1.000002f + Q.slack + 1e-6f;
-      unsigned int* col = list + i;
+      unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
       for_each_candidate32(Q, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, rf,
                            [&](unsigned int j) {
                              if (c < kst) stage[c][threadIdx.x] = j;
-                             else if (c < kmax) col[c * stride] = j;
+                             else if (c < kmax) col[c * 32] = j;
                              ++c;
                            });
-      cnt[i] = static_cast<unsigned char>(c < kmax ? c : kmax);
+      // more candidates than a list holds: the sentinel sends this agent to
+      // the exact cell-table walk in this (rebuild) step, and the next
+      // step's check rejects the lists so the host grows them
+      cnt[i] = static_cast<unsigned char>(c <= kmax ? c : kListOverflow);
     }
     // coalesced write-out of the staged columns: entry k of the warp's 32 agents
     const unsigned int cs = c < kst ? c : kst;
     const unsigned int wmax = __reduce_max_sync(0xffffffffu, cs);
+    unsigned int* wcol = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
     for (unsigned int k = 0; k < wmax; ++k)
-      if (k < cs) list[k * stride + i] = stage[k][threadIdx.x];
+      if (k < cs) wcol[k * 32] = stage[k][threadIdx.x];
     most = c > most ? c : most;
   }
   most = __reduce_max_sync(0xffffffffu, most);
   if (lane == 0 && most) {
     atomicMax(&g->list_need, most);
-    if (most > kmax && atomicCAS(&g->err, 0, static_cast<int>(kErrListOverflow)) == 0) g->failed_iteration = iteration;
+    if (most > kmax) g->list_incomplete = 1u;
   }
 }
 
-// k_force_list: run_forces + apply_pending (simulation.cpp:463-500,
-// mechanics.cpp:10-27, agent.hpp:115-133) over the list. Pass A classifies
-// every listed j (the reference's exact d2 <= r^2 decides: fp32 outside the
-// margin band, fp64 inside it) and records possible contacts; pass B runs
-// pairwise_repulsion on them with the reference's operations. Positions are
-// read from `pin`/`pfin` and written to `pout`/`pfout` (ping-pong). The
-// step's largest displacement is folded into g->step_disp for the coverage
-// check of the next step.
-#ifndef ABS_LIST_FORCE_MIN_BLOCKS
-#define ABS_LIST_FORCE_MIN_BLOCKS 3
+// The list step is two kernels, so the latency-bound candidate scan keeps
+// many warps resident (it holds no fp64 force state):
+// k_list_scan: every listed j through the reference's exact d2 <= r^2 (fp32
+// outside the margin band, fp64 inside it) — a force evaluation — and the
+// possible contacts into a warp-blocked per-agent contact list;
+// k_list_forces: pairwise_repulsion (mechanics.cpp:10-27) on the contacts,
+// the force sum, apply_pending (agent.hpp:115-133) and the step's largest
+// displacement (folded into g->step_disp for the next coverage check).
+// Positions are read from `pin`/`pfin` and written to `pout`/`pfout`.
+#ifndef ABS_LIST_SCAN_MIN_BLOCKS
+#define ABS_LIST_SCAN_MIN_BLOCKS 4
 #endif
-constexpr int kListContacts = 16;
-constexpr int kListForceSmem = kListContacts * kThreads * 4;
+constexpr int kListContacts = 16;                 // contacts recorded per agent (more: re-scan)
+constexpr unsigned char kContactOverflow = 255;  // contact count sentinel
+
+// Exact cell-table walk of one agent whose candidates did not fit its list
+// (rebuild step only): evaluations << 32 | possible contacts, recorded in ct.
+// Out of line: rare, and its fp64 state would cap the scan's occupancy.
+__device__ __noinline__ unsigned long long scan_walk(const QGrid& Q, const Pd* __restrict__ pin,
+                                                     const unsigned int* __restrict__ start, unsigned int i,
+                                                     double r, unsigned int* ct) {
+  const Pd me = load_pd(pin + i);
+  unsigned int evals = 0, nov = 0;
+  for_each_neighbor(Q, pin, start, i, me.x, me.y, me.z, r, r * r,
+                    [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                      ++evals;
+                      const double h = 0.5 * (me.d + q.d);
+                      if (d2 < h * h * (1.0 + 0x1.0p-50)) {
+                        if (nov < kListContacts) ct[nov * 32] = j;
+                        ++nov;
+                      }
+                    });
+  return (static_cast<unsigned long long>(evals) << 32) | nov;
+}
+
+__global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
+    k_list_scan(const Pd* __restrict__ pin, const float4* __restrict__ pfin, DevGrid* g,
+                const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
+                unsigned int* __restrict__ contacts, unsigned char* __restrict__ ncontacts,
+                unsigned int* __restrict__ evc, const unsigned int* __restrict__ start) {
+  if (g->err) return;
+  __shared__ QGrid Q;  // the build's grid: only read for overflow agents, in the rebuild step itself
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
+  const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
+  const float slack = g->lslack;
+  const double sl = static_cast<double>(slack);
+  const int lane = threadIdx.x & 31;
+  unsigned long long n_eval = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  // warp-uniform sweep: every lane of a warp stays in the loops below, so the
+  // band branch and the candidate loop bound are warp-wide decisions
+  for (unsigned long long b0 = blockIdx.x * (unsigned long long)blockDim.x + (threadIdx.x & ~31u); b0 < n;
+       b0 += stride) {
+    const unsigned long long i = b0 + lane;
+    const bool live = i < n;
+    const unsigned int c = live ? cnt[i] : 0u;
+    const float4 mf = __ldg(pfin + (live ? i : b0));
+    const double d = live ? pin[i].d : 1.0;
+    const double r = 0.5 * (d + dmax);
+    const double r2 = r * r;
+    const double rin = r - sl;
+    const float rin2 = rin > 0.0 ? __double2float_rd(rin * rin * (1.0 - 0x1.0p-40)) : -1.0f;
+    const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
+    const float hme = 0.5f * mf.w + slack;
+    const unsigned long long wbase = (b0 >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
+    unsigned int* ct = contacts + (b0 >> 5) * (kListContacts * 32) + lane;
+    unsigned int evals = 0, nov = 0;
+    const bool walk = c == kListOverflow;  // candidates did not fit: exact cell-table walk (rebuild step only)
+    const unsigned int cl = walk ? 0u : c;
+    const unsigned int cmax = __reduce_max_sync(0xffffffffu, cl);
+    if (__any_sync(0xffffffffu, walk) && walk) {
+      const unsigned long long en = scan_walk(Q, pin, start, static_cast<unsigned int>(i), r, ct);
+      evals = static_cast<unsigned int>(en >> 32);
+      nov = static_cast<unsigned int>(en);
+    }
+    const unsigned int* col = list + wbase;
+    unsigned int nj[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) nj[u] = u < static_cast<int>(cl) ? __ldg(col + u * 32) : 0u;
+    for (unsigned int s = 0; s < cmax; s += kBatch) {
+      unsigned int jj[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) jj[u] = nj[u];
+      float4 qf[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
+      col += kBatch * 32;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) nj[u] = s + kBatch + u < cl ? __ldg(col + u * 32) : 0u;
+      float df2[kBatch];
+      unsigned int in = 0, band = 0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const float ex = mf.x - qf[u].x, ey = mf.y - qf[u].y, ez = mf.z - qf[u].z;
+        df2[u] = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
+        const bool v = s + u < cl && df2[u] <= rout2;
+        in |= v ? (1u << u) : 0u;
+        band |= (v && df2[u] > rin2) ? (1u << u) : 0u;
+      }
+      if (__any_sync(0xffffffffu, band != 0u) && band) {  // margin band: the reference's exact fp64 test
+        const Pd me = load_pd(pin + i);
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          if (band & (1u << u)) {
+            const Pd q = load_pd(pin + jj[u]);
+            const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+            if (!((dx * dx + dy * dy) + dz * dz <= r2)) in &= ~(1u << u);
+          }
+        }
+      }
+      evals += __popc(in);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        // contact superset: df2 < (0.5 (d_i + d_j) + slack)^2 (1 + 5e-7)
+        const float hp = __fmaf_rn(0.5f, qf[u].w, hme);
+        if ((in & (1u << u)) && df2[u] < hp * hp * 1.0000005f) {
+          if (nov < kListContacts) ct[nov * 32] = jj[u];
+          ++nov;
+        }
+      }
+    }
+    if (!live) continue;
+    n_eval += evals;
+    if (evc) evc[i] = evals;
+    ncontacts[i] = nov <= kListContacts ? static_cast<unsigned char>(nov) : kContactOverflow;
+  }
+  flush_counters(n_eval, 0ull, g);
+}
 
 template <bool RECORD>
-__global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
-    k_force_list(const Pd* __restrict__ pin, const float4* __restrict__ pfin, Pd* __restrict__ pout,
-                 float4* __restrict__ pfout, Soa S, DevGrid* g, const unsigned int* __restrict__ list,
-                 const unsigned char* __restrict__ cnt, unsigned long long stride, StepArgs a,
-                 unsigned long long cap) {
+__global__ void __launch_bounds__(kThreads, 3)
+    k_list_forces(const Pd* __restrict__ pin, Pd* __restrict__ pout, float4* __restrict__ pfout, Soa S, DevGrid* g,
+                  const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
+                  const unsigned int* __restrict__ contacts, const unsigned char* __restrict__ ncontacts,
+                  StepArgs a, unsigned long long cap, const unsigned int* __restrict__ start) {
   if (g->err) return;
-  extern __shared__ __align__(16) unsigned int force_smem[];
-  auto ovl = reinterpret_cast<unsigned int (*)[kThreads]>(force_smem);
+  __shared__ QGrid Q;
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
   const double k = a.k;
   const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
-  const float slack = g->lslack;
-  const double sl = static_cast<double>(slack);
-  unsigned long long n_eval = 0;
   float moved = 0.0f;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd me = load_pd(pin + i);
-    const unsigned int c = cnt[i];
-    const double r = 0.5 * (me.d + dmax);
-    const double r2 = r * r;
-    // fp32 classification thresholds (for_each_neighbor_flat32)
-    const double rin = r - sl;
-    const float rin2 = rin > 0.0 ? __double2float_rd(rin * rin * (1.0 - 0x1.0p-40)) : -1.0f;
-    const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
-    const float fx = static_cast<float>(me.x - lox), fy = static_cast<float>(me.y - loy),
-                fz = static_cast<float>(me.z - loz);
-    const float hme = 0.5f * static_cast<float>(me.d) + slack;
-    const unsigned int* col = list + i;
-    unsigned int evals = 0, nov = 0;
-    for (unsigned int s = 0; s < c; s += kBatch) {
-      unsigned int jj[kBatch];
-      float4 qf[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) jj[u] = __ldg(col + static_cast<unsigned long long>(min(s + u, c - 1)) * stride);
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const float ex = fx - qf[u].x, ey = fy - qf[u].y, ez = fz - qf[u].z;
-        const float df2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
-        bool in = s + u < c && df2 <= rout2;
-        if (in && df2 > rin2) {  // margin band: the reference's exact fp64 test
-          const Pd q = load_pd(pin + jj[u]);
-          const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-          in = (dx * dx + dy * dy) + dz * dz <= r2;
-        }
-        evals += in;
-        // contact superset: df2 < (0.5 (d_i + d_j) + slack)^2 (1 + 5e-7)
-        const float hp = __fmaf_rn(0.5f, qf[u].w, hme);
-        const bool ct = in && df2 < hp * hp * 1.0000005f;
-        if (ct && nov < kListContacts) ovl[nov][threadIdx.x] = jj[u];
-        nov += ct;
-      }
-    }
-    n_eval += evals;
-    if (a.evc) a.evc[i] = evals;
+    const unsigned int nc = ncontacts[i];
     unsigned int contributors = 0;
-    double fx64 = 0.0, fy64 = 0.0, fz64 = 0.0;
-    auto contact = [&](unsigned int j) {
-      const Pd q = load_pd(pin + j);
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    auto contact_q = [&](unsigned int j, const Pd& q) {
       const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
       // pairwise_repulsion (mechanics.cpp:10-27)
       const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
@@ -1347,28 +1430,52 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
       }
       if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
         ++contributors;
-        fx64 += f0;
-        fy64 += f1;
-        fz64 += f2;
+        fx += f0;
+        fy += f1;
+        fz += f2;
       }
     };
-    if (nov <= kListContacts) {
-      for (unsigned int q = 0; q < nov; ++q) contact(ovl[q][threadIdx.x]);
-    } else {  // more possible contacts than the shared list holds: re-scan (rare)
-      for (unsigned int s = 0; s < c; ++s) {
-        const unsigned int j = __ldg(col + static_cast<unsigned long long>(s) * stride);
-        const Pd q = load_pd(pin + j);
-        const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-        const double d2 = (dx * dx + dy * dy) + dz * dz;
-        const double h = 0.5 * (me.d + q.d);
-        if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact(j);
+    if (nc != kContactOverflow) {
+      const unsigned int* ct = contacts + (i >> 5) * (kListContacts * 32) + (i & 31);
+      unsigned int q = 0;
+      for (; q + 2 <= nc; q += 2) {  // two records in flight
+        const unsigned int j0 = __ldg(ct + q * 32), j1 = __ldg(ct + (q + 1) * 32);
+        const Pd q0 = load_pd(pin + j0);
+        const Pd q1 = load_pd(pin + j1);
+        contact_q(j0, q0);
+        contact_q(j1, q1);
+      }
+      if (q < nc) {
+        const unsigned int j0 = __ldg(ct + q * 32);
+        contact_q(j0, load_pd(pin + j0));
+      }
+    } else {  // more possible contacts than recorded: the list (or the rebuild step's walk) again
+      const double r = 0.5 * (me.d + dmax);
+      const double r2 = r * r;
+      const unsigned int c = cnt[i];
+      if (c == kListOverflow) {
+        for_each_neighbor(Q, pin, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r2,
+                          [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                            const double h = 0.5 * (me.d + q.d);
+                            if (d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+                          });
+      } else {
+        const unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + (i & 31);
+        for (unsigned int s2 = 0; s2 < c; ++s2) {
+          const unsigned int j = __ldg(col + static_cast<unsigned long long>(s2) * 32);
+          const Pd q = load_pd(pin + j);
+          const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          const double h = 0.5 * (me.d + q.d);
+          if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+        }
       }
     }
     double tx = 0.0, ty = 0.0, tz = 0.0;
-    if ((fx64 * fx64 + fy64 * fy64) + fz64 * fz64 > a.threshold2) {
-      tx = fx64 * a.dt;
-      ty = fy64 * a.dt;
-      tz = fz64 * a.dt;
+    if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
+      tx = fx * a.dt;
+      ty = fy * a.dt;
+      tz = fz * a.dt;
     }
     Pd np = me;
     const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
@@ -1389,9 +1496,9 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
       moved = fmaxf(moved, __double2float_ru(md * (1.0 + 0x1.0p-40)));
     }
     if (RECORD) {
-      S.force[i] = fx64;
-      S.force[cap + i] = fy64;
-      S.force[2 * cap + i] = fz64;
+      S.force[i] = fx;
+      S.force[cap + i] = fy;
+      S.force[2 * cap + i] = fz;
     }
     S.partners[i] = contributors;
     reinterpret_cast<double2*>(pout + i)[0] = make_double2(np.x, np.y);
@@ -1401,7 +1508,6 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_FORCE_MIN_BLOCKS)
   }
   const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
   if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
-  flush_counters(n_eval, 0ull, g);
 }
 
 // ------------------------------------------------------------ config 5: SIR
@@ -2238,6 +2344,8 @@ struct abs_gpu_ctx {
   float4* pf2 = nullptr;                // fp32 copy paired with newpd (pf is paired with S[cur].pd)
   unsigned long long pf2_cap = 0;
   unsigned char* nl_cnt = nullptr;      // [stride] candidates per agent
+  unsigned int* nl_ct = nullptr;        // warp-blocked [16][32] possible contacts per agent (list step)
+  unsigned char* nl_nct = nullptr;      // contacts per agent
   unsigned long long nl_stride = 0;
   unsigned int nl_kmax = 0;
   bool list_valid = false;              // lists match the current storage order
@@ -2417,7 +2525,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag);
   cudaFree(c->pf);
   c->pf = nullptr;
-  cudaFree(c->pf2);
+  cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct);
   c->pf2 = nullptr;
   c->pf2_cap = 0;
   CK(dalloc(&c->pf, ncap));
@@ -2709,7 +2817,7 @@ double list_skin(const abs_gpu_ctx* c) {
 }
 
 constexpr unsigned int kListKmaxInit = 64;
-constexpr unsigned int kListKmaxMax = 255;  // u8 counts
+constexpr unsigned int kListKmaxMax = 254;  // u8 counts (255 = overflow sentinel)
 
 // List storage for the current population: [kmax][stride] u32 + u8 counts.
 int ensure_lists(abs_gpu_ctx* c, unsigned int kmax) {
@@ -2729,13 +2837,19 @@ int ensure_lists(abs_gpu_ctx* c, unsigned int kmax) {
   CK(cudaStreamSynchronize(c->stream));
   cudaFree(c->nl);
   cudaFree(c->nl_cnt);
+  cudaFree(c->nl_ct);
+  cudaFree(c->nl_nct);
   c->nl = nullptr;
   c->nl_cnt = nullptr;
+  c->nl_ct = nullptr;
+  c->nl_nct = nullptr;
   c->nl_stride = 0;
   c->nl_kmax = 0;
   c->list_valid = false;
   CK(dalloc(&c->nl, ns * kk));
   CK(dalloc(&c->nl_cnt, ns));
+  CK(dalloc(&c->nl_ct, ns * kListContacts));
+  CK(dalloc(&c->nl_nct, ns));
   c->nl_stride = ns;
   c->nl_kmax = kk;
   return ABS_OK;
@@ -2775,7 +2889,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     cudaEvent_t* ev = c->timing ? event_pair(c, c->bev, c->bev_used) : nullptr;
     if (ev) cudaEventRecord(ev[0], c->stream);
     k_list_build<<<blocks, kForceThreads, kListSmem, c->stream>>>(c->pf, c->g, c->start, c->nl, c->nl_cnt,
-                                                                  c->nl_stride, c->nl_kmax, skin, iteration);
+                                                                  c->nl_kmax, skin);
     if (ev) cudaEventRecord(ev[1], c->stream);
     ++c->launches;
     c->list_valid = true;
@@ -2799,23 +2913,25 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     c->pos_in_new = !from_new;
   }
   phase_mark(c);  // after environment update
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_force_list<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kListForceSmem);
-    cudaFuncSetAttribute(k_force_list<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kListForceSmem);
-    configured = true;
+  static int scan_blocks = 0;
+  if (!scan_blocks) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_list_scan, kThreads, 0);
+    scan_blocks = c->sms * std::max(per_sm, 1);
   }
   cudaEvent_t* ev = c->timing ? event_pair(c, c->ev, c->ev_used) : nullptr;
   if (ev) cudaEventRecord(ev[0], c->stream);
+  k_list_scan<<<scan_blocks, kThreads, 0, c->stream>>>(pin, fin, c->g, c->nl, c->nl_cnt, c->nl_kmax, c->nl_ct,
+                                                       c->nl_nct, a.evc, c->start);
   const int nb = grid_blocks(c, c->cap);
   if (c->cfg.record_forces)
-    k_force_list<true><<<nb, kThreads, kListForceSmem, c->stream>>>(pin, fin, pout, fout, c->S[c->cur], c->g, c->nl,
-                                                                    c->nl_cnt, c->nl_stride, a, c->cap);
+    k_list_forces<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
+                                                        c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
   else
-    k_force_list<false><<<nb, kThreads, kListForceSmem, c->stream>>>(pin, fin, pout, fout, c->S[c->cur], c->g,
-                                                                     c->nl, c->nl_cnt, c->nl_stride, a, c->cap);
+    k_list_forces<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
+                                                         c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
   if (ev) cudaEventRecord(ev[1], c->stream);
-  ++c->launches;
+  c->launches += 2;
   phase_mark(c);  // after agent ops
   phase_mark(c);  // no commit
 }
@@ -3460,6 +3576,14 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     };
     if (h.err == kErrNone) {
       count_kinds(todo);
+      if (h.list_incomplete && c->list_valid) {  // the last build overflowed: grow, rebuild next
+        c->list_valid = false;
+        const unsigned int need = h.list_need;
+        if (need > kListKmaxMax || ensure_lists(c, std::min(kListKmaxMax, need + need / 4 + 8)) != ABS_OK) {
+          cudaGetLastError();
+          c->list_off = true;
+        }
+      }
       if (h.n) std::memcpy(c->sort_guess_dims, h.dims, sizeof c->sort_guess_dims);
       // Auto sub-bins (bins_yz): a crowded grid (config 2 once its cells have
       // grown: ~14 agents per box, 106 evaluations per agent) needs the row
@@ -3499,15 +3623,12 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       if (rc) return rc;
     } else if (h.err == kErrListRebuild) {  // the lists no longer cover r: rebuild at this iteration
       c->list_valid = false;
-      rc = clear_dev_err(c);
-      if (rc) return rc;
-    } else if (h.err == kErrListOverflow) {  // more candidates than the list holds: grow, rebuild
-      CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
-      c->list_valid = false;
       const unsigned int need = h.list_need;
-      if (need > kListKmaxMax || ensure_lists(c, std::min(kListKmaxMax, need + need / 4 + 8)) != ABS_OK) {
-        cudaGetLastError();
-        c->list_off = true;
+      if (h.list_incomplete) {  // the last build overflowed: grow the lists first
+        if (need > kListKmaxMax || ensure_lists(c, std::min(kListKmaxMax, need + need / 4 + 8)) != ABS_OK) {
+          cudaGetLastError();
+          c->list_off = true;
+        }
       }
       rc = clear_dev_err(c);
       if (rc) return rc;

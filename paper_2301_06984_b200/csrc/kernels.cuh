@@ -49,7 +49,6 @@ enum DevErr : int {
   kErrQueryRadius = 6,  // a behaviour's query radius exceeds the box (uniform_grid.cpp:176-181)
   kErrSortRetry = 7,    // internal: the host's counting-sort guess did not fit; re-run with the exact path
   kErrListRebuild = 8,  // internal: the neighbour lists no longer cover the query radius; re-run as a rebuild
-  kErrListOverflow = 9, // internal: an agent has more list candidates than the list holds; grow and re-run
 };
 
 // Grid + bookkeeping living in device memory (one per context).
@@ -101,7 +100,7 @@ struct DevGrid {
   unsigned int list_need;       // largest candidate count seen by the last build
   double lorigin[3];            // grid origin at the build: list steps classify in fp32 relative to it
   float lslack;                 // fp32 classification slack of the list steps (build extent + skin)
-  unsigned int pad4;
+  unsigned int list_incomplete; // the last build met more candidates than a list holds (those agents walk)
 };
 
 struct StepArgs {

@@ -81,10 +81,10 @@ def test_list_step_per_agent_evaluations(engine, oracle_mod):
     more list step with per-agent recording)."""
     O = oracle_mod
     wl = CF.c4_large_uniform(8192, seed=9)
-    p = dict(wl.params, sorting_frequency=0)
+    p = dict(wl.params, sorting_frequency=0, neighbor_skin=8.0)  # wide: the lists surely cover step 4
     sim = engine.Simulation(engine.SimulationParams(**p))
     sim.add_agents(wl.x, wl.y, wl.z, wl.d)
-    sim.simulate(6)
+    sim.simulate(3)
     pre = sim.agents()
     steps0 = sim.list_stats()["list_steps"]
     sim.record_evaluations(True)
@@ -93,7 +93,7 @@ def test_list_step_per_agent_evaluations(engine, oracle_mod):
     ev = dict(zip(sim.agents()["uid"].tolist(), sim.evaluations().tolist()))
     orc = O.PortSim(_oparams(O, p), pre["x"], pre["y"], pre["z"], pre["d"])
     st = {k: pre[k] for k in ("uid", "x", "y", "z", "d", "flags", "partners", "volume")}
-    orc.load(st, int(pre["uid"].max()) + 1, 6)
+    orc.load(st, int(pre["uid"].max()) + 1, 3)
     orc.env_update()
     off, nb = orc.neighbors()
     od = orc.dump()
