@@ -1191,12 +1191,74 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
 // shared-memory list and pairwise_repulsion runs on them afterwards with all
 // lanes busy (the fp64 sqrt/division would otherwise run at ~8 of 32 lanes).
 //
-// Lists are warp-blocked: entry k of agent i lives at
-// list[(i / 32) * kmax * 32 + k * 32 + i % 32], so a warp's list is one
-// contiguous kmax x 128 B block — the build's write-out and the list sweep's
-// index loads are full-line, sequential accesses.
+// k_list_build: after the re-bin, every agent's candidates within r + skin
+// (fp32 superset, no 3x3x3 box clamp: r + skin may exceed the box) are staged
+// per lane in shared memory and written out warp-blocked: entry k of agent i
+// lives at list[(i / 32) * kmax * 32 + k * 32 + i % 32], so a warp's list is
+// one contiguous kmax x 128 B block — the write-out and the list sweep's index
+// loads are full-line, sequential accesses.
+#ifndef ABS_LIST_MIN_BLOCKS
+#define ABS_LIST_MIN_BLOCKS 5
+#endif
 constexpr int kListStage = 64;  // candidates staged per lane before the coalesced write-out
 constexpr unsigned char kListOverflow = 255;  // count sentinel: the agent's candidates did not fit
+constexpr int kListSmem = (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads * 4;
+
+__global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
+    k_list_build(const float4* __restrict__ pf, DevGrid* g, const unsigned int* __restrict__ start,
+                 unsigned int* __restrict__ list, unsigned char* __restrict__ cnt, unsigned int kmax, double skin) {
+  if (g->err) return;
+  __shared__ QGrid Q;
+  extern __shared__ __align__(16) unsigned int force_smem[];
+  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
+  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
+  auto stage = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + (kMaxRows + kMaxRows / 2) * kForceThreads);
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
+  const unsigned long long n = g->n;
+  const double dmax = g->dmax;
+  const int lane = threadIdx.x & 31;
+  const unsigned int kst = kmax < kListStage ? kmax : kListStage;
+  unsigned int most = 0;
+  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
+    const unsigned long long base = chunk * 32ull;
+    if (base >= n) break;
+    const unsigned long long i = base + lane;
+    unsigned int c = 0;
+    if (i < n) {
+      const float4 me = __ldg(pf + i);
+      // pf.w is the diameter rounded to fp32 (relative error 2^-24); the
+      // 2e-6 inflation of rf covers it and the rounding of R
+      const double R = 0.5 * (static_cast<double>(me.w) + dmax) + skin;
+      const float rf = static_cast<float>(R) * 1.000002f + Q.slack + 1e-6f;
+      unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
+      for_each_candidate32(Q, pf, start, wj0, wb16, static_cast<unsigned int>(i), me.x, me.y, me.z, rf,
+                           [&](unsigned int j) {
+                             if (c < kst) stage[c][threadIdx.x] = j;
+                             else if (c < kmax) col[c * 32] = j;
+                             ++c;
+                           });
+      // more candidates than a list holds: the sentinel sends this agent to
+      // the exact cell-table walk in this (rebuild) step, and the next
+      // step's check rejects the lists so the host grows them
+      cnt[i] = static_cast<unsigned char>(c <= kmax ? c : kListOverflow);
+    }
+    // coalesced write-out of the staged columns: entry k of the warp's 32 agents
+    const unsigned int cs = c < kst ? c : kst;
+    const unsigned int wmax = __reduce_max_sync(0xffffffffu, cs);
+    unsigned int* wcol = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
+    for (unsigned int k = 0; k < wmax; ++k)
+      if (k < cs) wcol[k * 32] = stage[k][threadIdx.x];
+    most = c > most ? c : most;
+  }
+  most = __reduce_max_sync(0xffffffffu, most);
+  if (lane == 0 && most) {
+    atomicMax(&g->list_need, most);
+    if (most > kmax) g->list_incomplete = 1u;
+  }
+}
 
 // The list step is two kernels, so the latency-bound candidate scan keeps
 // many warps resident (it holds no fp64 force state):
@@ -1213,12 +1275,35 @@ constexpr unsigned char kListOverflow = 255;  // count sentinel: the agent's can
 constexpr int kListContacts = 16;                 // contacts recorded per agent (more: re-scan)
 constexpr unsigned char kContactOverflow = 255;  // contact count sentinel
 
+// Exact cell-table walk of one agent whose candidates did not fit its list
+// (rebuild step only): evaluations << 32 | possible contacts, recorded in ct.
+// Out of line: rare, and its fp64 state would cap the scan's occupancy.
+__device__ __noinline__ unsigned long long scan_walk(const QGrid& Q, const Pd* __restrict__ pin,
+                                                     const unsigned int* __restrict__ start, unsigned int i,
+                                                     double r, unsigned int* ct) {
+  const Pd me = load_pd(pin + i);
+  unsigned int evals = 0, nov = 0;
+  for_each_neighbor(Q, pin, start, i, me.x, me.y, me.z, r, r * r,
+                    [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                      ++evals;
+                      const double h = 0.5 * (me.d + q.d);
+                      if (d2 < h * h * (1.0 + 0x1.0p-50)) {
+                        if (nov < kListContacts) ct[nov * 32] = j;
+                        ++nov;
+                      }
+                    });
+  return (static_cast<unsigned long long>(evals) << 32) | nov;
+}
+
 __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
     k_list_scan(const Pd* __restrict__ pin, const float4* __restrict__ pfin, DevGrid* g,
                 const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
                 unsigned int* __restrict__ contacts, unsigned char* __restrict__ ncontacts,
-                unsigned int* __restrict__ evc) {
+                unsigned int* __restrict__ evc, const unsigned int* __restrict__ start) {
   if (g->err) return;
+  __shared__ QGrid Q;  // the build's grid: only read for overflow agents, in the rebuild step itself
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
   const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
@@ -1245,9 +1330,14 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
     const unsigned long long wbase = (b0 >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
     unsigned int* ct = contacts + (b0 >> 5) * (kListContacts * 32) + lane;
     unsigned int evals = 0, nov = 0;
-    // (a list step never sees an incomplete list: finalize_grid rejects it)
-    const unsigned int cl = c;
+    const bool walk = c == kListOverflow;  // candidates did not fit: exact cell-table walk (rebuild step only)
+    const unsigned int cl = walk ? 0u : c;
     const unsigned int cmax = __reduce_max_sync(0xffffffffu, cl);
+    if (__any_sync(0xffffffffu, walk) && walk) {
+      const unsigned long long en = scan_walk(Q, pin, start, static_cast<unsigned int>(i), r, ct);
+      evals = static_cast<unsigned int>(en >> 32);
+      nov = static_cast<unsigned int>(en);
+    }
     const unsigned int* col = list + wbase;
     unsigned int nj[kBatch];
 #pragma unroll
@@ -1307,8 +1397,11 @@ __global__ void __launch_bounds__(kThreads, 3)
     k_list_forces(const Pd* __restrict__ pin, Pd* __restrict__ pout, float4* __restrict__ pfout, Soa S, DevGrid* g,
                   const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
                   const unsigned int* __restrict__ contacts, const unsigned char* __restrict__ ncontacts,
-                  StepArgs a, unsigned long long cap) {
+                  StepArgs a, unsigned long long cap, const unsigned int* __restrict__ start) {
   if (g->err) return;
+  __shared__ QGrid Q;
+  if (threadIdx.x == 0) Q = make_qgrid(*g);
+  __syncthreads();
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
   const double k = a.k;
@@ -1356,18 +1449,26 @@ __global__ void __launch_bounds__(kThreads, 3)
         const unsigned int j0 = __ldg(ct + q * 32);
         contact_q(j0, load_pd(pin + j0));
       }
-    } else {  // more possible contacts than recorded: re-scan the list (rare)
+    } else {  // more possible contacts than recorded: the list (or the rebuild step's walk) again
       const double r = 0.5 * (me.d + dmax);
       const double r2 = r * r;
       const unsigned int c = cnt[i];
-      const unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + (i & 31);
-      for (unsigned int s2 = 0; s2 < c; ++s2) {
-        const unsigned int j = __ldg(col + static_cast<unsigned long long>(s2) * 32);
-        const Pd q = load_pd(pin + j);
-        const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-        const double d2 = (dx * dx + dy * dy) + dz * dz;
-        const double h = 0.5 * (me.d + q.d);
-        if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+      if (c == kListOverflow) {
+        for_each_neighbor(Q, pin, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r2,
+                          [&](unsigned int j, const Pd& q, double, double, double, double d2) {
+                            const double h = 0.5 * (me.d + q.d);
+                            if (d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+                          });
+      } else {
+        const unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + (i & 31);
+        for (unsigned int s2 = 0; s2 < c; ++s2) {
+          const unsigned int j = __ldg(col + static_cast<unsigned long long>(s2) * 32);
+          const Pd q = load_pd(pin + j);
+          const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          const double h = 0.5 * (me.d + q.d);
+          if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+        }
       }
     }
     double tx = 0.0, ty = 0.0, tz = 0.0;
@@ -1407,172 +1508,6 @@ __global__ void __launch_bounds__(kThreads, 3)
   }
   const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
   if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
-}
-
-// k_force_build: the rebuild step in one sweep. Each agent walks its
-// candidates within r + skin once (for_each_candidate32, fp32 superset); every
-// candidate inside that ball goes to its list (staged in shared memory,
-// written out warp-blocked), and the same stream runs the
-// step's run_forces pass A (the reference's exact d2 <= r^2: fp32 outside the
-// margin band, fp64 inside it) with the possible contacts recorded for pass B
-// (pairwise_repulsion on the contacts, apply_pending). One sweep instead of a
-// build followed by a list step.
-#ifndef ABS_FORCE_BUILD_MIN_BLOCKS
-#define ABS_FORCE_BUILD_MIN_BLOCKS 4
-#endif
-constexpr int kForceBuildSmem = (kMaxRows + kMaxRows / 2 + kListStage + kListContacts) * kForceThreads * 4;
-
-template <bool RECORD>
-__global__ void __launch_bounds__(kForceThreads, ABS_FORCE_BUILD_MIN_BLOCKS)
-    k_force_build(const Pd* __restrict__ pin, const float4* __restrict__ pf, Pd* __restrict__ pout,
-                  float4* __restrict__ pfout, Soa S, DevGrid* g, const unsigned int* __restrict__ start,
-                  unsigned int* __restrict__ list, unsigned char* __restrict__ cnt, unsigned int kmax, double skin,
-                  StepArgs a, unsigned long long cap) {
-  if (g->err) return;
-  __shared__ QGrid Q;
-  extern __shared__ __align__(16) unsigned int force_smem[];
-  auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
-  auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
-  auto stage = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem + (kMaxRows + kMaxRows / 2) * kForceThreads);
-  auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(
-      force_smem + (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads);
-  if (threadIdx.x == 0) Q = make_qgrid(*g);
-  __syncthreads();
-  const unsigned long long n = g->n;
-  const double dmax = g->dmax;
-  const double k = a.k;
-  const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
-  const double sl = static_cast<double>(Q.slack);
-  const int lane = threadIdx.x & 31;
-  const unsigned int kst = kmax < kListStage ? kmax : kListStage;
-  unsigned int most = 0;
-  unsigned long long n_eval = 0;
-  float moved = 0.0f;
-  const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
-  const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  for (unsigned long long chunk = warp_id;; chunk += warps_total) {
-    const unsigned long long base = chunk * 32ull;
-    if (base >= n) break;
-    const unsigned long long i = base + lane;
-    unsigned int c = 0;
-    if (i < n) {
-      const Pd me = load_pd(pin + i);
-      const float4 mf = __ldg(pf + i);
-      const double r = 0.5 * (me.d + dmax);
-      const double r2 = r * r;
-      const double rin = r - sl;
-      const float rin2 = rin > 0.0 ? __double2float_rd(rin * rin * (1.0 - 0x1.0p-40)) : -1.0f;
-      const float rout2 = __double2float_ru((r + sl) * (r + sl) * (1.0 + 0x1.0p-40));
-      const float rf = static_cast<float>(r + skin) * 1.000002f + Q.slack + 1e-6f;
-      const float hme = 0.5f * mf.w + Q.slack;
-      unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
-      unsigned int evals = 0, nov = 0;
-      for_each_candidate32(Q, pf, start, wj0, wb16, static_cast<unsigned int>(i), mf.x, mf.y, mf.z, rf,
-                           [&](unsigned int j, float df2, float qd) {
-                             if (c < kst) stage[c][threadIdx.x] = j;
-                             else if (c < kmax) col[c * 32] = j;
-                             ++c;
-                             bool in = df2 <= rout2;
-                             if (in && df2 > rin2) {  // margin band: the reference's exact fp64 test
-                               const Pd q = load_pd(pin + j);
-                               const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-                               in = (dx * dx + dy * dy) + dz * dz <= r2;
-                             }
-                             evals += in;
-                             const float hp = __fmaf_rn(0.5f, qd, hme);
-                             const bool ct = in && df2 < hp * hp * 1.0000005f;
-                             if (ct && nov < kListContacts) ovl[nov][threadIdx.x] = j;
-                             nov += ct;
-                           });
-      cnt[i] = static_cast<unsigned char>(c <= kmax ? c : kListOverflow);
-      n_eval += evals;
-      if (a.evc) a.evc[i] = evals;
-      unsigned int contributors = 0;
-      double fx = 0.0, fy = 0.0, fz = 0.0;
-      auto contact_q = [&](unsigned int j, const Pd& q) {
-        const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-        // pairwise_repulsion (mechanics.cpp:10-27)
-        const double dist = sqrt((dx * dx + dy * dy) + dz * dz);
-        const double overlap = 0.5 * (me.d + q.d) - dist;
-        if (overlap <= 0.0) return;
-        double f0, f1, f2;
-        if (dist > 0.0) {
-          const double sc = k * overlap / dist;
-          f0 = dx * sc;
-          f1 = dy * sc;
-          f2 = dz * sc;
-        } else {
-          coincident_force(S.uid[i], S.uid[j], k * overlap, &f0, &f1, &f2);
-        }
-        if ((f0 * f0 + f1 * f1) + f2 * f2 > 0.0) {
-          ++contributors;
-          fx += f0;
-          fy += f1;
-          fz += f2;
-        }
-      };
-      if (nov <= kListContacts) {
-        for (unsigned int q = 0; q < nov; ++q) {
-          const unsigned int j = ovl[q][threadIdx.x];
-          contact_q(j, load_pd(pin + j));
-        }
-      } else {  // more possible contacts than recorded: the exact walk again (rare)
-        for_each_neighbor(Q, pin, start, static_cast<unsigned int>(i), me.x, me.y, me.z, r, r2,
-                          [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                            const double h = 0.5 * (me.d + q.d);
-                            if (d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
-                          });
-      }
-      double tx = 0.0, ty = 0.0, tz = 0.0;
-      if ((fx * fx + fy * fy) + fz * fz > a.threshold2) {
-        tx = fx * a.dt;
-        ty = fy * a.dt;
-        tz = fz * a.dt;
-      }
-      Pd np = me;
-      const double disp = sqrt((tx * tx + ty * ty) + tz * tz);
-      if (disp > 0.0) {
-        double md = disp;
-        if (disp > a.max_disp) {
-          const double sc = a.max_disp / disp;
-          tx *= sc;
-          ty *= sc;
-          tz *= sc;
-          md = a.max_disp;
-        }
-        np.x = me.x + tx;
-        np.y = me.y + ty;
-        np.z = me.z + tz;
-        const unsigned char fl = S.flags[i];
-        if (!(fl & ABS_FLAG_MOVED)) S.flags[i] = fl | ABS_FLAG_MOVED;
-        moved = fmaxf(moved, __double2float_ru(md * (1.0 + 0x1.0p-40)));
-      }
-      if (RECORD) {
-        S.force[i] = fx;
-        S.force[cap + i] = fy;
-        S.force[2 * cap + i] = fz;
-      }
-      S.partners[i] = contributors;
-      reinterpret_cast<double2*>(pout + i)[0] = make_double2(np.x, np.y);
-      reinterpret_cast<double2*>(pout + i)[1] = make_double2(np.z, np.d);
-      pfout[i] = make_float4(static_cast<float>(np.x - lox), static_cast<float>(np.y - loy),
-                             static_cast<float>(np.z - loz), static_cast<float>(np.d));
-    }
-    const unsigned int cs = c < kst ? c : kst;
-    const unsigned int wmax = __reduce_max_sync(0xffffffffu, cs);
-    unsigned int* wcol = list + (base >> 5) * (static_cast<unsigned long long>(kmax) * 32) + lane;
-    for (unsigned int q = 0; q < wmax; ++q)
-      if (q < cs) wcol[q * 32] = stage[q][threadIdx.x];
-    most = c > most ? c : most;
-  }
-  most = __reduce_max_sync(0xffffffffu, most);
-  const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
-  if (lane == 0) {
-    if (most) atomicMax(&g->list_need, most);
-    if (most > kmax) g->list_incomplete = 1u;
-    if (mb) atomicMax(&g->step_disp, mb);
-  }
-  flush_counters(n_eval, 0ull, g);
 }
 
 // ------------------------------------------------------------ config 5: SIR
@@ -2422,7 +2357,7 @@ struct abs_gpu_ctx {
   double pred_acc = 0.0, pred_rate = 0.0;
   double build_ms = 0.0;
   unsigned long long build_launches = 0;
-  std::vector<cudaEvent_t> bev;  // pairs around k_force_build (timing on)
+  std::vector<cudaEvent_t> bev;  // pairs around k_list_build (timing on)
   size_t bev_used = 0;
   unsigned long long list_builds = 0, list_steps = 0;
   // per-agent force evaluations of the last iteration (abs_gpu_record_evaluations)
@@ -2946,31 +2881,23 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
   float4* fout;
   if (kind == 2) {
     launch_env_update(c, iteration, 0, true, 2, skin);
-    phase_mark(c);  // after environment update
-    // the step's forces run inside the build sweep (k_force_build)
     static int blocks = 0;
     if (!blocks) {
-      cudaFuncSetAttribute(k_force_build<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kForceBuildSmem);
-      cudaFuncSetAttribute(k_force_build<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kForceBuildSmem);
-      blocks = force_blocks(c, k_force_build<false>, kForceBuildSmem);
+      cudaFuncSetAttribute(k_list_build, cudaFuncAttributeMaxDynamicSharedMemorySize, kListSmem);
+      blocks = force_blocks(c, k_list_build, kListSmem);
     }
     cudaEvent_t* ev = c->timing ? event_pair(c, c->bev, c->bev_used) : nullptr;
     if (ev) cudaEventRecord(ev[0], c->stream);
-    if (c->cfg.record_forces)
-      k_force_build<true><<<blocks, kForceThreads, kForceBuildSmem, c->stream>>>(
-          c->S[c->cur].pd, c->pf, c->newpd, c->pf2, c->S[c->cur], c->g, c->start, c->nl, c->nl_cnt, c->nl_kmax, skin,
-          a, c->cap);
-    else
-      k_force_build<false><<<blocks, kForceThreads, kForceBuildSmem, c->stream>>>(
-          c->S[c->cur].pd, c->pf, c->newpd, c->pf2, c->S[c->cur], c->g, c->start, c->nl, c->nl_cnt, c->nl_kmax, skin,
-          a, c->cap);
+    k_list_build<<<blocks, kForceThreads, kListSmem, c->stream>>>(c->pf, c->g, c->start, c->nl, c->nl_cnt,
+                                                                  c->nl_kmax, skin);
     if (ev) cudaEventRecord(ev[1], c->stream);
     ++c->launches;
     c->list_valid = true;
+    pin = c->S[c->cur].pd;
+    fin = c->pf;
+    pout = c->newpd;
+    fout = c->pf2;
     c->pos_in_new = true;
-    phase_mark(c);  // after agent ops
-    phase_mark(c);  // no commit
-    return;
   } else {
     const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
                      c->bins_cap, c->cap, c->uid_cap, 0, iteration, 1, skin};
@@ -2995,22 +2922,14 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
   cudaEvent_t* ev = c->timing ? event_pair(c, c->ev, c->ev_used) : nullptr;
   if (ev) cudaEventRecord(ev[0], c->stream);
   k_list_scan<<<scan_blocks, kThreads, 0, c->stream>>>(pin, fin, c->g, c->nl, c->nl_cnt, c->nl_kmax, c->nl_ct,
-                                                       c->nl_nct, a.evc);
-  // persistent grid (resident CTAs only): the sweep advances front to back, so
-  // the contacts' records stay in L2 between neighbouring warps
-  static int force_nb = 0;
-  if (!force_nb) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_list_forces<false>, kThreads, 0);
-    force_nb = c->sms * std::max(per_sm, 1);
-  }
-  const int nb = force_nb;
+                                                       c->nl_nct, a.evc, c->start);
+  const int nb = grid_blocks(c, c->cap);
   if (c->cfg.record_forces)
     k_list_forces<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
-                                                        c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap);
+                                                        c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
   else
     k_list_forces<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
-                                                         c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap);
+                                                         c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
   if (ev) cudaEventRecord(ev[1], c->stream);
   c->launches += 2;
   phase_mark(c);  // after agent ops

@@ -511,9 +511,8 @@ __device__ __forceinline__ void for_each_neighbor_flat32(const QGrid& g, const P
   }
 }
 
-// Candidate walk of the neighbour-list build: visit(j, df2, d_j) for every
-// agent j != self whose fp32 squared distance df2 (relative coordinates from
-// `pf`) is <= rf2 — a
+// Candidate walk of the neighbour-list build: every agent j != self whose
+// fp32 squared distance (relative coordinates from `pf`) is <= rf2 — a
 // conservative superset of the exact fp64 ball of radius R when
 // rf >= R * (1 + 1e-6) + slack. Rows cover the whole ball, clamped to the
 // grid only (NOT to the reference's 3x3x3 boxes: R = r + skin may exceed the
@@ -532,7 +531,7 @@ __device__ __forceinline__ void for_each_candidate32(const QGrid& g, const float
   auto test = [&](unsigned int j, const float4& qf, bool valid) {
     const float ex = fx - qf.x, ey = fy - qf.y, ez = fz - qf.z;
     const float df2 = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
-    if (valid && j != self && df2 <= rf2) visit(j, df2, qf.w);
+    if (valid && j != self && df2 <= rf2) visit(j);
   };
   int nr = 0;
   for (int bz = z0; bz <= z1; ++bz) {
