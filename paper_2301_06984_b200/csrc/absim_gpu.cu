@@ -129,7 +129,8 @@ struct FinArgs {
   unsigned long long bins_cap, capacity, uid_cap;
   int may_add;
   unsigned long long iteration;
-  int list_mode;  // 0 no neighbour lists, 1 list step (check coverage), 2 list (re)build step
+  int list_mode;  // 0 no neighbour lists, 1 list step (check coverage), 2 list (re)build step,
+                  // 3 re-binning step with displacement tracking (list policy)
   double skin;    // list skin (absolute)
 };
 
@@ -258,6 +259,8 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
     }
     // relative coordinates stay within ext + skin / 2 while the lists are valid
     g->lslack = static_cast<float>(16.0 * (ext + fa.skin + 1.0) * 0x1.0p-24 + 1e-5);
+  } else if (fa.list_mode == 3) {  // re-binning step whose displacement the list policy tracks
+    g->step_disp = 0u;
   } else if (fa.list_mode == 1 && err == kErrNone) {
     const double acc = g->list_acc + static_cast<double>(__uint_as_float(g->step_disp)) + g->margin + 1e-12;
     g->list_acc = acc;
@@ -708,6 +711,7 @@ struct Daughter {
   unsigned long long parent;
   double x, y, z, d, vol;
   unsigned int tag;
+  float moved;  // length of this step's translation (0 if none)
 };
 
 // RandomStream::unit_vector (random.hpp:47-52) on an agent's own stream:
@@ -749,7 +753,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
                                                unsigned long long& n_eval, unsigned long long& n_skip,
                                                Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f,
                                                const Query& query = Query{}) {
-  Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u};
+  Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
   dg.parent = my_uid;
@@ -971,6 +975,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     np.y = me.y + ty;
     np.z = me.z + tz;
     fl |= ABS_FLAG_MOVED;
+    if (a.track_disp) dg.moved = __double2float_ru((disp < a.max_disp ? disp : a.max_disp) * (1.0 + 0x1.0p-40));
   }
   if (tg != 0.0) {
     const double nd = me.d + tg;
@@ -1130,6 +1135,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
   // the resident warps cover a contiguous window of the agent array (cell
   // order) that advances front to back, with no shared counter to contend on.
   const int lane = threadIdx.x & 31;
+  float moved = 0.0f;
   const unsigned long long warps_total = (unsigned long long)gridDim.x * (blockDim.x >> 5);
   const unsigned long long warp_id = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   for (unsigned long long chunk = warp_id;; chunk += warps_total) {
@@ -1137,7 +1143,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
     if (base >= n) break;
     const bool live = base + lane < n;
     const unsigned long long i = work ? (live ? work[base + lane] : 0ull) : base + lane;
-    Daughter dg{false, 0, 0, 0, 0, 0, 0};
+    Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
     if (live) {
       const Pd me = load_pd(S.pd + i);
       const unsigned int self = static_cast<unsigned int>(i);
@@ -1168,6 +1174,11 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
     }
     if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
       stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
+    moved = fmaxf(moved, dg.moved);
+  }
+  if (a.track_disp) {  // the step's largest displacement (neighbour-list policy)
+    const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
+    if (lane == 0 && mb) atomicMax(&gw->step_disp, mb);
   }
   flush_counters(n_eval, n_skip, gw);
 }
@@ -2337,8 +2348,9 @@ struct abs_gpu_ctx {
   unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
   unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
   // per-iteration CUDA graphs (abs_gpu_simulate): [0] plain, [1] with the Morton sort
-  // slot = (sort ? 1 : 0) + 2 * iteration kind (0 re-bin + walk, 1 list step, 2 list rebuild)
-  cudaGraphExec_t gexec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // slot = (sort ? 1 : 0) + 2 * iteration kind (0 re-bin + walk, 1 list step, 2 list rebuild,
+  // 3 re-bin + walk tracking the displacement for the list policy)
+  cudaGraphExec_t gexec[8] = {};
   // neighbour lists
   unsigned int* nl = nullptr;           // [kmax][stride] candidate storage indices
   float4* pf2 = nullptr;                // fp32 copy paired with newpd (pf is paired with S[cur].pd)
@@ -2355,6 +2367,7 @@ struct abs_gpu_ctx {
   // host prediction of the device coverage check: accumulated displacement
   // the next list step will see, and the last step's largest displacement
   double pred_acc = 0.0, pred_rate = 0.0;
+  bool track_now = false;               // this iteration tracks its largest displacement (kind 3)
   double build_ms = 0.0;
   unsigned long long build_launches = 0;
   std::vector<cudaEvent_t> bev;  // pairs around k_list_build (timing on)
@@ -2638,6 +2651,7 @@ StepArgs step_args(const abs_gpu_ctx* c, unsigned long long iteration) {
   a.record_forces = c->cfg.record_forces;
   a.brute = brute_env(c);
   a.evc = c->rec_evals ? c->evc : nullptr;
+  a.track_disp = c->track_now ? 1 : 0;
   return a;
 }
 
@@ -2813,10 +2827,11 @@ bool list_mode_ok(const abs_gpu_ctx* c) {
 
 double list_skin(const abs_gpu_ctx* c) {
   if (c->cfg.neighbor_skin > 0.0) return c->cfg.neighbor_skin;
-  return 0.15 * (c->host_dmax > 0.0 ? c->host_dmax : 1.0);
+  return 0.2 * (c->host_dmax > 0.0 ? c->host_dmax : 1.0);
 }
 
 constexpr unsigned int kListKmaxInit = 64;
+constexpr double kListMinSteps = 4.0;  // a build must serve >= this many steps (c4: build iteration ~3x a list step)
 constexpr unsigned int kListKmaxMax = 254;  // u8 counts (255 = overflow sentinel)
 
 // List storage for the current population: [kmax][stride] u32 + u8 counts.
@@ -2940,11 +2955,12 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
   if (c->rec_evals && c->evc) {  // static / ghost agents evaluate nothing this iteration
     cudaMemsetAsync(c->evc, 0, c->evc_cap * sizeof(unsigned int), c->stream);
   }
-  if (kind) {
+  if (kind == 1 || kind == 2) {
     launch_list_iteration(c, iteration, kind);
     return;
   }
-  launch_env_update(c, iteration, adds_agents(c->cfg), true);
+  c->track_now = kind == 3;  // re-binning step whose displacement the list policy tracks
+  launch_env_update(c, iteration, adds_agents(c->cfg), true, kind == 3 ? 3 : 0);
   phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
     const int nb = grid_blocks(c, c->cap);
@@ -3472,7 +3488,9 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     }
   }
   while (done < iterations) {
-    const unsigned long long todo = std::min<unsigned long long>(chunk, iterations - done);
+    // while the list policy is re-binning, re-read the displacement rate every 8 iterations
+    const unsigned long long todo = std::min<unsigned long long>(
+        list_mode_ok(c) && c->nl && !c->list_valid ? 8 : chunk, iterations - done);
     struct Snap { int cur; bool pos_in_new; bool grid_valid; bool list_valid; };
     std::vector<Snap> snaps;
     snaps.reserve(todo);
@@ -3490,16 +3508,23 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       // The host predicts the device's coverage check from the last observed
       // displacement rate and schedules the rebuild itself, so a rejected list
       // step (rolled back with the rest of its chunk) stays the exception.
+      // A build pays off only if the lists then serve several steps: at the
+      // current rate a fresh list lasts skin / (2 rate) steps; below
+      // kListMinSteps the iteration re-bins and walks (tracking the rate).
       int kind = 0;
       if (list_mode_ok(c) && c->nl) {
         const double skin = list_skin(c);
         const bool usable = c->list_valid && !sorts;
+        const bool pays = c->pred_rate <= 0.0 || skin >= 2.0 * kListMinSteps * c->pred_rate;
         if (usable && (2.0 * c->pred_acc <= skin || remaining < 2)) {
           kind = 1;
           c->pred_acc += c->pred_rate;
-        } else if (remaining >= 2) {
+        } else if (remaining >= 2 && pays) {
           kind = 2;
           c->pred_acc = c->pred_rate;
+        } else {
+          kind = 3;
+          c->list_valid = false;
         }
       }
       kinds.push_back(kind);
@@ -3571,7 +3596,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     auto count_kinds = [&](unsigned long long upto) {
       for (unsigned long long q = 0; q < upto && q < kinds.size(); ++q) {
         c->list_builds += kinds[q] == 2;
-        c->list_steps += kinds[q] != 0;
+        c->list_steps += kinds[q] == 1 || kinds[q] == 2;
       }
     };
     if (h.err == kErrNone) {

@@ -113,6 +113,7 @@ struct StepArgs {
   int record_forces;
   int brute;  // BruteForceEnvironment: no maximum query radius
   unsigned int* evc;  // per-agent force evaluations of the step (parity hook; nullptr = off)
+  int track_disp;     // fold the step's largest displacement into DevGrid::step_disp (list policy)
 };
 
 // Order-preserving double <-> u64 map for atomicMin/atomicMax.
