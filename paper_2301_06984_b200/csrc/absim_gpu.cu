@@ -617,10 +617,13 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
   }
 }
 
+// Zero a[0 .. *len_ptr (+1)), clamped to the allocation (cap entries); skipped
+// once the iteration has failed (the host clears the table before a re-run).
 __global__ void k_zero_u32(unsigned int* __restrict__ a, const unsigned long long* len_ptr, int plus_one,
-                           const int* err) {
+                           const int* err, unsigned long long cap) {
   if (err && *err) return;
-  const unsigned long long len = *len_ptr + (plus_one ? 1 : 0);
+  unsigned long long len = *len_ptr + (plus_one ? 1 : 0);
+  len = len < cap ? len : cap;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < len;
        i += (unsigned long long)gridDim.x * blockDim.x)
     a[i] = 0;
@@ -2614,6 +2617,18 @@ bool env_flag(const char* name, bool dflt) {
   return e ? std::strcmp(e, "0") != 0 : dflt;
 }
 
+// ABSIM_SYNC_CHECK=1 (debugging): synchronise after the marked launches and
+// report the first one that faulted (direct launches only; graphs are off).
+void sync_check(abs_gpu_ctx* c, const char* what) {
+  static const bool on = env_flag("ABSIM_SYNC_CHECK", false);
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "absim: %s failed: %s (iteration %llu)\n", what, cudaGetErrorString(e), c->iteration);
+    std::abort();
+  }
+}
+
 void launch_scan_cells(abs_gpu_ctx* c, const unsigned long long* len_dev, unsigned long long len_cap,
                        const int* err) {
   static const bool onepass = env_flag("ABSIM_ONEPASS", true);
@@ -2704,7 +2719,8 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   const unsigned long long* nbins_dev = &c->g->nbins;
   static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
   if (c->grid_valid && !fused) {  // previous cell table still holds scanned offsets
-    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, nbins_dev, 1, &c->g->err);
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, nbins_dev, 1, &c->g->err, c->bins_cap + 1);
+    sync_check(c, "k_zero_u32");
     ++c->launches;
   }
   const Pd* pos = cur_pos(c);
@@ -2712,12 +2728,16 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
                    c->bins_cap, c->cap, c->uid_cap, may_add, iteration, list_mode, skin};
   if (fused) {
     k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa, c->grid_valid ? c->start : nullptr);
+    sync_check(c, "k_reduce_finalize");
   } else {
     k_reduce<<<nb, kThreads, 0, c->stream>>>(pos, c->g);
+    sync_check(c, "k_reduce");
     k_finalize<<<1, 32, 0, c->stream>>>(c->g, fa);
+    sync_check(c, "k_finalize");
     ++c->launches;
   }
   k_key<<<nb, kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+  sync_check(c, "k_key");
   c->launches += 2;
   launch_scan_cells(c, nbins_dev, c->bins_cap, &c->g->err);
   const int nxt = c->cur ^ 1;
@@ -2729,6 +2749,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
                                             c->cfg.record_forces, uses_f32_walk(c) || list_mode == 2, -1,
                                             uses_ext(c->cfg), carry_partners ? 1 : 0,
                                             c->cfg.model != ABS_MODEL_NONE ? 1 : 0);
+                                        sync_check(c, "k_scatter");
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
@@ -2760,12 +2781,14 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
     // c->rank is free after k_mark (it listed the marking agents there)
     k_static_pass<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->nv, c->nn,
                                                                        MODEL != ABS_MODEL_NONE, c->rank);
+                                                                   sync_check(c, "k_static_pass");
     ++c->launches;
     work = c->rank;
   }
   k_force<MODEL, STATIC, RECORD, WALK><<<blocks, kForceThreads, smem, c->stream>>>(
       S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
       c->st_tag, work);
+  sync_check(c, "k_force");
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
@@ -3385,14 +3408,18 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     c->sort_cap = c->cap;
   }
   const Pd* pos = cur_pos(c);
+  sync_check(c, "k_set_u64");
   if (c->grid_valid) {  // the sort leaves no valid cell table behind
-    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->nbins, 1, nullptr);
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->nbins, 1, &c->g->err, c->bins_cap + 1);
+    sync_check(c, "k_zero_u32");
     ++c->launches;
     c->grid_valid = false;
   }
   k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
+  sync_check(c, "k_reduce");
   k_finalize<<<1, 32, 0, c->stream>>>(c->g, FinArgs{c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull,
                                                      ~0ull, ~0ull, 0, iteration});
+                                                 sync_check(c, "k_finalize");
   // Path choice: the counting sort needs the Morton code space of this grid
   // to fit the cell table. The host guesses from the last grid it read (dims
   // change slowly) and launches only that path; the device checks the guess
@@ -3414,16 +3441,20 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     launch_radix = !guess;
   }
   k_sort_mode<<<1, 1, 0, c->stream>>>(c->g, c->bins_cap, mode_arg, iteration);
+  sync_check(c, "k_sort_mode");
   c->launches += 1;
   const int nxt = c->cur ^ 1;
   if (launch_counting) {  // Morton key + atomic slot, scan, scatter
     k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+    sync_check(c, "k_mkey");
     launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
     k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
                                                                  c->key, c->rank, c->g, c->cap,
                                                                  c->cfg.model == ABS_MODEL_PROLIFERATION,
                                                                  c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
-    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, nullptr);
+                                                             sync_check(c, "k_scatter");
+    k_zero_u32<<<grid_blocks(c, c->bins_cap), kThreads, 0, c->stream>>>(c->start, &c->g->sort_len, 1, &c->g->err, c->bins_cap + 1);
+    sync_check(c, "k_zero_u32");
     c->launches += 3;
   }
   if (!launch_radix) {
@@ -3438,13 +3469,16 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   unsigned int* i1 = c->sort_i[0];
   unsigned int* i2 = c->sort_i[1];
   k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
+  sync_check(c, "k_sort_keys");
   c->launches += 3;
   for (int shift = 0; shift < 64; shift += 8) {
     k_radix_hist<<<blocks, kThreads, 0, c->stream>>>(k1, i1, c->g, shift, c->sort_hist, kSortChunk);
+    sync_check(c, "k_radix_hist");
     launch_scan<unsigned int>(c, c->sort_hist, c->sort_hlen, 256ull * blocks, c->sort_tiles, nullptr);
     // one warp per chunk (stable by construction): 32-thread blocks keep the
     // SM full of independent chunk walkers
     k_radix_scatter<<<blocks, 32, 0, c->stream>>>(k1, i1, k2, i2, c->g, shift, c->sort_hist, kSortChunk);
+    sync_check(c, "k_radix_scatter");
     c->launches += 2;
     std::swap(k1, k2);
     std::swap(i1, i2);
@@ -3452,6 +3486,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
                                                               c->cfg.record_forces, 0, uses_ext(c->cfg));
+                                                          sync_check(c, "k_gather");
   ++c->launches;
   c->cur = nxt;
   c->pos_in_new = false;
