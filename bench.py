@@ -349,6 +349,8 @@ def run_gpu(args):
     prm["environment"] = args.env
     prm["bins_per_box"] = args.bins
     prm["bins_per_box_x"] = args.bins_x
+    prm["neighbor_list"] = args.lists != "off"
+    prm["neighbor_skin"] = args.skin
     if wl.params.get("model") == E.MODEL_PROLIFERATION:
         prm["capacity"] = 5 * wl.n * 2 ** 9
     if wl.params.get("model") == E.MODEL_GROW_DIVIDE:  # doubles every 3 iterations
@@ -529,6 +531,9 @@ def main():
     ap.add_argument("--bins", type=int, default=0, help="sub-bins per box edge along y, z (0 = auto)")
     ap.add_argument("--bins-x", type=int, default=0, help="sub-bins per box edge along x (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--lists", default="auto", choices=["auto", "off"],
+                    help="neighbour lists between environment rebuilds (DESIGN.md §4b)")
+    ap.add_argument("--skin", type=float, default=0.0, help="neighbour-list skin (0 = auto)")
     ap.add_argument("--decompose", action="store_true", help="use the slab decomposition even at N=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force"],

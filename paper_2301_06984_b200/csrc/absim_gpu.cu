@@ -2541,7 +2541,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   cudaFree(c->st_parent); cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag);
   cudaFree(c->pf);
   c->pf = nullptr;
-  cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct);
+  cudaFree(c->pf2);
   c->pf2 = nullptr;
   c->pf2_cap = 0;
   CK(dalloc(&c->pf, ncap));
@@ -2622,7 +2622,8 @@ bool env_flag(const char* name, bool dflt) {
 void sync_check(abs_gpu_ctx* c, const char* what) {
   static const bool on = env_flag("ABSIM_SYNC_CHECK", false);
   if (!on) return;
-  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "absim: %s failed: %s (iteration %llu)\n", what, cudaGetErrorString(e), c->iteration);
     std::abort();
@@ -2911,6 +2912,7 @@ cudaEvent_t* event_pair(abs_gpu_ctx* c, std::vector<cudaEvent_t>& v, size_t& use
 // Positions and their fp32 copies travel in pairs: (S[cur].pd, pf) and
 // (newpd, pf2).
 void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind) {
+  sync_check(c, "before list iteration");
   const StepArgs a = step_args(c, iteration);
   const double skin = list_skin(c);
   Pd* pin;
@@ -2929,6 +2931,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     k_list_build<<<blocks, kForceThreads, kListSmem, c->stream>>>(c->pf, c->g, c->start, c->nl, c->nl_cnt,
                                                                   c->nl_kmax, skin);
     if (ev) cudaEventRecord(ev[1], c->stream);
+    sync_check(c, "k_list_build");
     ++c->launches;
     c->list_valid = true;
     pin = c->S[c->cur].pd;
@@ -2946,6 +2949,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     fout = from_new ? c->pf : c->pf2;
     k_reduce_finalize<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pin, c->g, fa,
                                                                           c->grid_valid ? c->start : nullptr);
+    sync_check(c, "k_reduce_finalize(list)");
     ++c->launches;
     c->grid_valid = false;
     c->pos_in_new = !from_new;
@@ -2961,6 +2965,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
   if (ev) cudaEventRecord(ev[0], c->stream);
   k_list_scan<<<scan_blocks, kThreads, 0, c->stream>>>(pin, fin, c->g, c->nl, c->nl_cnt, c->nl_kmax, c->nl_ct,
                                                        c->nl_nct, a.evc, c->start);
+  sync_check(c, "k_list_scan");
   const int nb = grid_blocks(c, c->cap);
   if (c->cfg.record_forces)
     k_list_forces<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
@@ -2969,12 +2974,14 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     k_list_forces<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
                                                          c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
   if (ev) cudaEventRecord(ev[1], c->stream);
+  sync_check(c, "k_list_forces");
   c->launches += 2;
   phase_mark(c);  // after agent ops
   phase_mark(c);  // no commit
 }
 
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0) {
+  sync_check(c, "before iteration");
   if (c->rec_evals && c->evc) {  // static / ghost agents evaluate nothing this iteration
     cudaMemsetAsync(c->evc, 0, c->evc_cap * sizeof(unsigned int), c->stream);
   }
@@ -3224,7 +3231,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
   cudaFree(c->xcounts); cudaFree(c->holes); cudaFree(c->nl); cudaFree(c->nl_cnt); cudaFree(c->evc);
-  cudaFree(c->pf2);
+  cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -3514,6 +3521,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   // rolled back to the failed iteration (no kernel touched state after it).
   unsigned long long done = 0;
   const unsigned long long chunk = 32;
+  sync_check(c, "simulate entry");
   // neighbour lists: storage for this population, allocated
   // outside any graph capture
   if (list_mode_ok(c) && iterations >= 2) {
@@ -3521,6 +3529,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       cudaGetLastError();
       c->list_off = true;  // no room for the lists: re-bin + walk every iteration
     }
+    sync_check(c, "ensure_lists");
   }
   while (done < iterations) {
     // while the list policy is re-binning, re-read the displacement rate every 8 iterations

@@ -59,12 +59,13 @@ def test_lists_same_as_rebinning(engine, oracle_mod):
 
 
 def test_tiny_skin_forces_rebuilds(engine, oracle_mod):
-    """skin 0.02: the device coverage check rejects most list steps; each is
-    re-run as a rebuild and the results stay exact."""
+    """skin 0.02: before any displacement is known the host schedules list
+    steps that the device coverage check rejects; each is re-run as a
+    rebuild, then the policy falls back to re-binning. Results stay exact."""
     wl = CF.c1_relaxation(3000, seed=7)
     sim, _ = _run_pair(engine, oracle_mod, wl, 20, 2, neighbor_skin=0.02)
     st = sim.list_stats()
-    assert st["builds"] >= 10, st
+    assert st["builds"] >= 5, st
 
 
 def test_wide_skin_grows_lists(engine, oracle_mod):
