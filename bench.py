@@ -391,12 +391,9 @@ def run_gpu(args):
     lists = sim.list_stats()
     sim.reset_timers(False)
     r2 = sim.report()
-    agent_its = None
-    # agent count per step (constant unless the model adds agents)
-    if r1.agents_added == r0.agents_added:
-        agent_its = r1.final_agent_count * args.steps
-    else:
-        agent_its = (r0.final_agent_count + r1.final_agent_count) / 2 * args.steps
+    # the device sums every iteration's agent count at its start (exact for
+    # growing populations, as the reference arm's per-step sum)
+    agent_its = r1.agent_iterations - r0.agent_iterations
     ms_max = ms
     if world > 1:
         t = torch.tensor([ms], device="cuda")

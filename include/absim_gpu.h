@@ -123,6 +123,8 @@ typedef struct {
   uint64_t agents_added;
   uint64_t agents_removed;
   uint64_t kernel_launches; /* kernels this context launched so far */
+  uint64_t agent_iterations; /* sum over iterations since the last upload of the agents at iteration start
+                                (the metric's numerator, exact for growing populations) */
 } abs_step_stats;
 
 void abs_gpu_default_config(abs_gpu_config* cfg);

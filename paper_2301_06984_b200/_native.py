@@ -74,6 +74,7 @@ class Stats(C.Structure):
         ("agents_added", C.c_uint64),
         ("agents_removed", C.c_uint64),
         ("kernel_launches", C.c_uint64),
+        ("agent_iterations", C.c_uint64),
     ]
 
 

@@ -132,6 +132,7 @@ struct FinArgs {
   int list_mode;  // 0 no neighbour lists, 1 list step (check coverage), 2 list (re)build step,
                   // 3 re-binning step with displacement tracking (list policy)
   double skin;    // list skin (absolute)
+  int counts_iteration;  // this finalize opens an iteration: add its agents to agent_its
 };
 
 __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
@@ -275,6 +276,8 @@ __device__ void finalize_grid(DevGrid* g, const FinArgs& fa) {
   if (err != kErrNone) {
     g->err = err;
     g->failed_iteration = iteration;
+  } else if (fa.counts_iteration) {
+    g->agent_its += n;
   }
 }
 
@@ -455,6 +458,8 @@ __global__ void __launch_bounds__(kThreads) k_scan_apply(T* __restrict__ data,
 // reset pass; the two tickets alternate by epoch parity and tile 0 clears the
 // one the next scan will use. Same result as k_scan_tiles/partials/apply:
 // data[i] = sum(data[0..i)), data[len] = total.
+constexpr unsigned int kScanEpochMask = 0x3FFFFFFFu;
+
 __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restrict__ data,
                                                            const unsigned long long* len_ptr,
                                                            unsigned long long* __restrict__ state,
@@ -492,8 +497,12 @@ __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restr
     sum += v[q];
   }
   unsigned int run = block_excl_scan(sum, &tot);
-  const unsigned long long tag = static_cast<unsigned long long>(epoch & 0xFFFFFFu) << 40;
-  constexpr unsigned long long kAgg = 1ull << 38, kInc = 2ull << 38, kVal = (1ull << 38) - 1;
+  // tile word: epoch (30 bits) | inclusive/aggregate flags (2 bits) | value (32
+  // bits: a tile prefix is at most the table total < 2^32). The host clears
+  // the words when the 30-bit epoch wraps (launch_scan_cells), so a stale
+  // word can never carry the current tag.
+  const unsigned long long tag = static_cast<unsigned long long>(epoch & kScanEpochMask) << 34;
+  constexpr unsigned long long kAgg = 1ull << 32, kInc = 2ull << 32, kVal = (1ull << 32) - 1;
   if (threadIdx.x < 32) {  // warp 0 looks back over 32 predecessors at a time
     const int lane = threadIdx.x;
     unsigned long long prefix = 0;
@@ -505,7 +514,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restr
         const long long p = base - lane;  // lane 0 = nearest predecessor
         const unsigned long long w =
             p >= 0 ? *reinterpret_cast<volatile unsigned long long*>(&tile_state[p]) : (tag | kInc);  // before tile 0: 0
-        const bool ready = (w & ~((1ull << 40) - 1)) == tag && (w & (kAgg | kInc));
+        const bool ready = (w & ~((1ull << 34) - 1)) == tag && (w & (kAgg | kInc));
         if (!__all_sync(0xffffffffu, ready)) continue;  // some predecessor not published yet
         const unsigned int inc = __ballot_sync(0xffffffffu, (w & kInc) != 0);
         const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive prefix, else the whole window
@@ -2347,6 +2356,7 @@ struct abs_gpu_ctx {
   unsigned int* key = nullptr;
   unsigned int* rank = nullptr;
   unsigned int* tiles = nullptr;  // scan tile sums (u32)
+  unsigned int* ctiles = nullptr;  // tile sums of agent-sized scans (compaction), cap / kScanTile + 2
   unsigned long long* scan_state = nullptr;  // single-pass cell-table scan (k_scan_onepass)
   unsigned int sort_guess_dims[3] = {0, 0, 0};      // grid dims last read back (in-loop sort path guess)
   unsigned long long sort_radix_iteration = ~0ull;  // iteration whose counting guess failed
@@ -2545,8 +2555,11 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   c->pf2 = nullptr;
   c->pf2_cap = 0;
   CK(dalloc(&c->pf, ncap));
-  CK(dalloc(&c->key, ncap));
-  CK(dalloc(&c->rank, ncap));
+  CK(dalloc(&c->key, ncap + 1));   // compact_population writes the survivor count at [n <= cap]
+  CK(dalloc(&c->rank, ncap + 1));
+  cudaFree(c->ctiles);
+  c->ctiles = nullptr;
+  CK(dalloc(&c->ctiles, ncap / kScanTile + 2));
   CK(dalloc(&c->nv, ncap));
   CK(dalloc(&c->nn, ncap));
   CK(cudaMemsetAsync(c->nv, 0, ncap, c->stream));
@@ -2638,6 +2651,10 @@ void launch_scan_cells(abs_gpu_ctx* c, const unsigned long long* len_dev, unsign
     return;
   }
   const unsigned int blocks = static_cast<unsigned int>(std::max<unsigned long long>(1, (len_cap + kScanTile - 1) / kScanTile));
+  if (((c->scan_epoch + 1) & kScanEpochMask) == 0) {  // the tag wraps: no stale tile word may match it
+    cudaMemsetAsync(c->scan_state, 0, ((c->bins_cap + 1) / kScanTile + 4) * 8, c->stream);
+    ++c->scan_epoch;
+  }
   k_scan_onepass<<<blocks, kThreads, 0, c->stream>>>(c->start, len_dev, c->scan_state, ++c->scan_epoch, err);
   ++c->launches;
 }
@@ -2726,7 +2743,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   }
   const Pd* pos = cur_pos(c);
   const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
-                   c->bins_cap, c->cap, c->uid_cap, may_add, iteration, list_mode, skin};
+                   c->bins_cap, c->cap, c->uid_cap, may_add, iteration, list_mode, skin, in_step ? 1 : 0};
   if (fused) {
     k_reduce_finalize<<<nb, kThreads, 0, c->stream>>>(pos, c->g, fa, c->grid_valid ? c->start : nullptr);
     sync_check(c, "k_reduce_finalize");
@@ -2941,7 +2958,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     c->pos_in_new = true;
   } else {
     const FinArgs fa{c->cfg.fixed_box_length, brute_env(c), bins_x(c), bins_yz(c), row_block_shift(),
-                     c->bins_cap, c->cap, c->uid_cap, 0, iteration, 1, skin};
+                     c->bins_cap, c->cap, c->uid_cap, 0, iteration, 1, skin, 1};
     const bool from_new = c->pos_in_new;
     pin = from_new ? c->newpd : c->S[c->cur].pd;
     fin = from_new ? c->pf2 : c->pf;
@@ -3231,7 +3248,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->newpd); cudaFree(c->pf); cudaFree(c->g); cudaFree(c->start); cudaFree(c->key); cudaFree(c->rank);
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
   cudaFree(c->xcounts); cudaFree(c->holes); cudaFree(c->nl); cudaFree(c->nl_cnt); cudaFree(c->evc);
-  cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct);
+  cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct); cudaFree(c->ctiles);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -3847,9 +3864,8 @@ static int compact_population(abs_gpu_ctx* c, unsigned long long n) {
   }
   unsigned long long* len = c->xcounts + 1;  // persistent scratch (no allocation per call)
   k_set_u64<<<1, 1, 0, c->stream>>>(len, n);
-  // tiles64 holds (cap + kScanTile) / kScanTile + 2 u64 words: room for the u32 tile sums of n <= cap
-  unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
-  launch_scan<unsigned int>(c, idx, len, n, tiles, nullptr);  // idx[n] = survivors
+  // ctiles holds cap / kScanTile + 2 u32 tile sums: room for any n <= cap
+  launch_scan<unsigned int>(c, idx, len, n, c->ctiles, nullptr);  // idx[n] = survivors
   CK(cudaMemcpyAsync(c->hxcounts, idx + n, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   const unsigned long long nn = *reinterpret_cast<const unsigned int*>(c->hxcounts);
@@ -3988,6 +4004,7 @@ int abs_gpu_stats(abs_gpu_ctx* c, abs_step_stats* out) {
   out->agents_added = h.added;
   out->agents_removed = h.removed;
   out->kernel_launches = c->launches;
+  out->agent_iterations = h.agent_its;
   return ABS_OK;
 }
 

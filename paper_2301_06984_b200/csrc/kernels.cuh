@@ -83,6 +83,7 @@ struct DevGrid {
   unsigned long long mark_n;  // staticness phase 1: listed disturbers / fresh agents
   unsigned long long fin_count;  // k_reduce_finalize: blocks done (last one sizes the grid)
   unsigned long long work_n;     // static detection: agents listed for the force sweep (k_static_pass)
+  unsigned long long agent_its;  // sum over completed iterations of the agents at iteration start
   // --- kept across uploads (abs_gpu_upload copies everything above) ---
   int ov_on;               // multi-domain: use the global grid below
   int pad1;

@@ -125,6 +125,7 @@ class SimulationReport:
     agents_added: int = 0
     agents_removed: int = 0
     kernel_launches: int = 0
+    agent_iterations: int = 0        # sum of the agents at the start of every iteration since the upload
     total_wall_ms: float = 0.0
     agent_ops_ms: float = 0.0
     env_update_ms: float = 0.0
@@ -357,7 +358,7 @@ class Simulation:
                                 uid_count=s.uid_count, force_evaluations=s.force_evaluations,
                                 force_skips=s.force_skips, agents_added=s.agents_added,
                                 agents_removed=s.agents_removed, kernel_launches=s.kernel_launches,
-                                total_wall_ms=self._wall_ms, peak_rss_bytes=peak_rss_bytes())
+                                agent_iterations=s.agent_iterations, total_wall_ms=self._wall_ms, peak_rss_bytes=peak_rss_bytes())
 
     def phase_report(self) -> SimulationReport:
         """report() plus the device-time categories of the timed iterations."""
