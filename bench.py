@@ -174,17 +174,31 @@ def cpu_baseline(wl_name, steps=None, threads=None, env="uniform_grid"):
                       f"(same density and distributions), {wall:.1f} s of CPU wall time"}
 
 
+def _workload_config(args, wl_name, n, world):
+    """The workload keys of a bench line, identical for the GPU and reference arms."""
+    return {"workload": wl_name, "agents_per_gpu": int(n), "global_agents": int(n) * world,
+            "parallelism": "single" if world == 1 else f"replicas{world}", "environment": args.env,
+            "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"}
+
+
 def run_reference(args):
-    """--impl reference: each step is one iteration of the unmodified
-    reference on the bounded sample, on all host cores; rank 0 only."""
+    """--impl reference: each step is one iteration of the unmodified reference
+    (oracle/_ref, all host cores) on the SAME population the GPU arm simulates
+    at N=1 (config.agents_per_gpu equal: c4 = 2^26 agents, ~8 s per iteration
+    on 16 cores, so the driver's 5 + 20 iterations take ~4 min; the population
+    build is untimed). Under torchrun (N>1) rank 0 alone runs one GPU's share.
+    --ref-sample N times a smaller sample of the same shape instead."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     threads = os.cpu_count()
     brute = args.env != "uniform_grid"
-    sim, kind, cores, wl = _ref_sim(args.config, BRUTE_SAMPLE if brute else CPU_SAMPLE[args.config], threads,
-                                    args.env)
-    full_n = int(args.n or FULL_AGENTS.get(args.config, wl.n))
+    n = BRUTE_SAMPLE if brute else (args.ref_sample or args.n or FULL_AGENTS[args.config])
+    if args.config == "c2":
+        n = None  # the proliferation run starts from its 16^3 lattice
+    t_build = time.perf_counter()
+    sim, kind, cores, wl = _ref_sim(args.config, n, threads, args.env)
+    t_build = time.perf_counter() - t_build
     for _ in range(args.warmup):
         sim.simulate(1)
     agent_its = 0
@@ -198,13 +212,16 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            # the same workload keys as the GPU arm's line, plus the bounded sample actually timed
-            "config": {"workload": wl.name, "agents_per_gpu": full_n, "global_agents": full_n * args.gpus,
-                       "parallelism": "single" if args.gpus == 1 else f"reference on rank 0 of {args.gpus}",
-                       "environment": args.env, "sample_agents": wl.n},
+            # the GPU arm's workload keys, with the population this run actually timed
+            "config": _workload_config(args, wl.name, wl.n, 1),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": f"{wl.name} shape at {wl.n} agents, {args.steps} timed iterations"},
+                             "sample": f"{wl.name} at {wl.n} agents (the GPU arm's N=1 population"
+                                       f"{'' if wl.n == FULL_AGENTS.get(args.config, wl.n) else ': a bounded sample'}), "
+                                       f"{args.steps} timed iterations after {args.warmup} warm-up; "
+                                       f"population built in {t_build:.1f} s (untimed)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if args.gpus > 1:
+        line["config"]["note"] = f"reference on rank 0 of {args.gpus}: one GPU's share of the weak-scaling run"
     print(json.dumps(line))
 
 
@@ -487,9 +504,8 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl.name, "agents_per_gpu": wl.n, "global_agents": int(wl.n * world),
-                   "parallelism": f"replicas{world}" if world > 1 else "single", "environment": args.env,
-                   "bins_per_box": [args.bins_x, args.bins, args.bins], "l2": "inputs (2.5 GB state at c4) >> 126 MB L2, no flush"},
+        "config": _workload_config(args, wl.name, wl.n, world),
+        "device_knobs": {"bins_per_box": [args.bins_x, args.bins, args.bins], "lists": args.lists, "skin": args.skin},
         "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else ("k_force_list" if lists["list_steps"] else "k_force"),
                      "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
@@ -531,6 +547,8 @@ def main():
     ap.add_argument("--lists", default="auto", choices=["auto", "off"],
                     help="neighbour lists between environment rebuilds (DESIGN.md §4b)")
     ap.add_argument("--skin", type=float, default=0.0, help="neighbour-list skin (0 = auto)")
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="--impl reference: time a bounded sample of this many agents instead of the full population")
     ap.add_argument("--decompose", action="store_true", help="use the slab decomposition even at N=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force"],
