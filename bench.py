@@ -140,8 +140,8 @@ def _ref_sim(wl_name, sample_n, threads, env="uniform_grid"):
                        sorting_frequency=prm.get("sorting_frequency", 0), threads=threads, domains=0,
                        fixed_box=prm.get("fixed_box_length", 0.0), env=ENV_IDS[env])
     try:
-        if prm.get("model", 0) == 4:  # SIR: the reference has no periodic boundaries
-            raise FileNotFoundError("no reference path for config 5")
+        if prm.get("model", 0) == 4:  # SIR: periodic cube as ghost images over the reference engine
+            return O.RefSirSim(p, wl.x, wl.y, wl.z), "reference", threads, wl
         if wl.name in REF_BUILDERS:  # the reference's own population builder and models
             return O.RefSim.builtin(p, REF_BUILDERS[wl.name], wl.n), "reference", threads, wl
         return O.RefSim(p, wl.x, wl.y, wl.z, wl.d, wl.mask), "reference", threads, wl

@@ -263,6 +263,16 @@ class RefSim(_Sim):
             cls._lib = d
         return cls._lib
 
+    def neighbor_counts(self, threads: int = 0) -> np.ndarray:
+        """Per-agent force-query neighbour counts (storage order), multithreaded;
+        call after env_update()."""
+        lib = self.lib().cdll
+        lib.ref_neighbor_counts.argtypes = [C.c_void_p, _U32, C.c_int]
+        out = np.zeros(self.counts()["agents"], np.uint32)
+        if lib.ref_neighbor_counts(self.h, _ptr(out, C.c_uint32), threads or os.cpu_count()) != 0:
+            raise RuntimeError(lib.ref_last_error().decode())
+        return out
+
     @classmethod
     def builtin(cls, params: OracleParams, name: str, n: int) -> "RefSim":
         self = cls.__new__(cls)
@@ -353,6 +363,69 @@ class PortSim(_Sim):
     def set_rng_counters(self, c):
         v = np.ascontiguousarray(c, np.uint64)
         self._check(self.lib()["orc_set_rng_counters"](self.h, _ptr(v, C.c_uint64)))
+
+
+class RefSirSim:
+    """Config 5 (SIR, periodic cube) through the UNMODIFIED reference engine:
+    ghost images at the faces + public agent / standalone operations
+    (ref_harness.cpp, RefSir). Same interface as PortSim's SIR subset."""
+
+    def __init__(self, params: OracleParams, x, y, z):
+        lib = RefSim.lib().cdll
+        lib.ref_sir_create.restype = C.c_void_p
+        lib.ref_sir_create.argtypes = [C.c_void_p, C.c_uint64, _D, _D, _D]
+        lib.ref_sir_destroy.argtypes = [C.c_void_p]
+        lib.ref_sir_simulate.argtypes = [C.c_void_p, C.c_uint64]
+        lib.ref_sir_counts.restype = C.c_int64
+        lib.ref_sir_counts.argtypes = [C.c_void_p, _U64, C.c_uint64]
+        lib.ref_sir_dump.argtypes = [C.c_void_p, _U64, _D, _D, _D, _U8, _U32]
+        lib.ref_sir_agents.restype = C.c_uint64
+        lib.ref_sir_agents.argtypes = [C.c_void_p]
+        self.lib = lib
+        x, y, z = (np.ascontiguousarray(a, dtype=np.float64) for a in (x, y, z))
+        self._p = params.to_c()
+        self.h = lib.ref_sir_create(C.byref(self._p), len(x), _ptr(x, C.c_double), _ptr(y, C.c_double),
+                                    _ptr(z, C.c_double))
+        if not self.h:
+            raise RuntimeError(lib.ref_last_error().decode())
+        self.iterations = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ref_sir_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def simulate(self, iterations: int):
+        if self.lib.ref_sir_simulate(self.h, iterations) != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        self.iterations += iterations
+
+    def count_history(self) -> np.ndarray:
+        out = np.zeros((max(self.iterations, 1), 3), np.uint64)
+        n = self.lib.ref_sir_counts(self.h, _ptr(out, C.c_uint64), self.iterations)
+        return out[:n]
+
+    def sir_counts(self):
+        return [int(v) for v in self.count_history()[-1]]
+
+    def agents(self) -> int:
+        return int(self.lib.ref_sir_agents(self.h))
+
+    def counts(self) -> dict:
+        return {"agents": self.agents(), "iterations": self.iterations}
+
+    def dump(self) -> dict:
+        n = self.agents()
+        out = {"uid": np.zeros(n, np.uint64), "x": np.zeros(n), "y": np.zeros(n), "z": np.zeros(n),
+               "state": np.zeros(n, np.uint8), "t": np.zeros(n, np.uint32)}
+        if self.lib.ref_sir_dump(self.h, _ptr(out["uid"], C.c_uint64), _ptr(out["x"], C.c_double),
+                                 _ptr(out["y"], C.c_double), _ptr(out["z"], C.c_double),
+                                 _ptr(out["state"], C.c_uint8), _ptr(out["t"], C.c_uint32)) != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return out
 
 
 def morton_encode3(x: int, y: int, z: int) -> int:

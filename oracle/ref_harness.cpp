@@ -17,6 +17,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "absim/models.hpp"
@@ -347,6 +348,36 @@ std::int64_t ref_neighbors(void* h, std::uint64_t* offsets, std::uint64_t* uids,
   return rc == 0 ? total : -1;
 }
 
+// Force-query neighbour COUNTS per agent (storage order), i.e. the force
+// evaluations run_forces performs for a non-static agent (simulation.cpp:469-
+// 475), for populations too large for ref_neighbors' uid lists. Queries run
+// concurrently on `threads` std::threads, as the reference's own workers do
+// (for_each_neighbor is read-only between updates).
+int ref_neighbor_counts(void* h, std::uint32_t* counts, int threads) {
+  return guarded([&] {
+    Simulation& s = *static_cast<Ref*>(h)->sim;
+    Environment& env = s.environment();
+    const double dmax = env.largest_agent_diameter();
+    std::vector<std::pair<Agent*, AgentHandle>> all;
+    s.resource_manager().for_each_agent([&](Agent& a, AgentHandle hd) { all.push_back({&a, hd}); });
+    const std::size_t n = all.size();
+    const int T = std::max(1, threads);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) {
+      pool.emplace_back([&, t] {
+        for (std::size_t i = t; i < n; i += T) {
+          std::uint32_t c = 0;
+          LambdaVisitor v([&](Agent&, double) { ++c; });
+          const double r = 0.5 * (all[i].first->diameter() + dmax);
+          env.for_each_neighbor(all[i].second, all[i].first->position(), r * r, v);
+          counts[i] = c;
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
 // env update + sort_and_balance (sort_balance.cpp:22-148) on the current state.
 int ref_sort(void* h, std::uint64_t* moved) {
   return guarded([&] {
@@ -357,5 +388,189 @@ int ref_sort(void* h, std::uint64_t* moved) {
     if (moved) *moved = o.agents_moved;
   });
 }
+
+// ---- config 5 (SIR on a periodic cube) through the reference engine -------
+// The reference has no periodic boundaries, so the periodic
+// cube is realised with ghost images: before every iteration each agent
+// within r (+ margin) of a face gets translated copies (x +- L per axis, up
+// to 7 per corner agent) as extra agents of the reference Simulation. The
+// reference's own grid and AgentContext::for_each_neighbor (inclusive
+// d2 <= r^2, simulation.hpp:41-44) then find every neighbour the
+// minimum-image convention of absim_models.h finds (L > 4 r: one image of a
+// pair at most is within r). Everything else runs through public hooks:
+//   agent op "sir"    (add_agent_operation, simulation.hpp:111): real agents
+//                     update their state from the START-of-iteration states
+//                     (double-buffered in the harness, keyed by uid) and
+//                     translate by the random-walk step; ghosts remove_self
+//   repulsion k = 0   the engine's forces op still runs, contributing nothing
+//   post ops          (add_standalone_operation, Phase::kPost, after the
+//                     commit removed the old ghosts): wrap positions into
+//                     [0, L) with Agent::set_position, publish the new
+//                     states, count S/I/R, add the next iteration's ghosts.
+// Decisions and draws use absim_models.h (the shared definitions), so the
+// result is comparable bit for bit with the C port and the kernels; the only
+// arithmetic difference is the ghost position x + L (computed here) against
+// the port's wrapped difference (x_i - x_j) - L, which can move d2 by an ulp
+// (a decision flips only if d2 is within ~1e-15 of r^2).
+struct RefSir {
+  std::unique_ptr<Simulation> sim;
+  double L, r, step, prob;
+  std::uint64_t rec;
+  std::uint64_t seed;
+  std::uint64_t n_real;
+  std::vector<std::int64_t> ghost_of;  // by uid: real uid of a ghost, -1 for a real agent
+  std::vector<std::uint8_t> st_old, st_new;
+  std::vector<std::uint32_t> t_old, t_new;
+  std::vector<std::uint64_t> counts;  // 3 per completed iteration
+
+  void ensure(std::uint64_t uid) {
+    if (uid >= ghost_of.size()) {
+      const std::size_t m = std::max<std::size_t>(uid + 1, ghost_of.size() * 2);
+      ghost_of.resize(m, -1);
+      st_old.resize(m, 0);
+      st_new.resize(m, 0);
+      t_old.resize(m, 0);
+      t_new.resize(m, 0);
+    }
+  }
+
+  void add_ghosts() {
+    std::vector<std::pair<Vec3, std::uint64_t>> img;
+    const double m = r * 1.01 + 1e-9;  // superset: a spare image is never within r
+    sim->resource_manager().for_each_agent([&](Agent& a, AgentHandle) {
+      if (ghost_of[a.uid()] >= 0) return;
+      const double p[3] = {a.position().x, a.position().y, a.position().z};
+      int lo[3], hi[3];
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = p[k] >= L - m ? -1 : 0;
+        hi[k] = p[k] < m ? 1 : 0;
+      }
+      for (int ox = lo[0]; ox <= hi[0]; ++ox)
+        for (int oy = lo[1]; oy <= hi[1]; ++oy)
+          for (int oz = lo[2]; oz <= hi[2]; ++oz) {
+            if (!ox && !oy && !oz) continue;
+            const Vec3 q{ox ? p[0] + ox * L : p[0], oy ? p[1] + oy * L : p[1], oz ? p[2] + oz * L : p[2]};
+            img.push_back({q, a.uid()});
+          }
+    });
+    for (auto& [q, real] : img) {
+      Agent& g = sim->add_agent(q, 1.0);
+      ensure(g.uid());
+      ghost_of[g.uid()] = static_cast<std::int64_t>(real);
+    }
+  }
+};
+
+void* ref_sir_create(const RefParams* rp, std::uint64_t n, const double* x, const double* y, const double* z) {
+  RefSir* r = nullptr;
+  const int rc = guarded([&] {
+    auto h = std::make_unique<RefSir>();
+    h->L = rp->mp[0];
+    h->r = rp->mp[1];
+    h->step = rp->mp[2];
+    h->rec = static_cast<std::uint64_t>(rp->mp[3]);
+    h->prob = rp->mp[4];
+    h->seed = rp->seed;
+    h->n_real = n;
+    if (!(h->L > 4.0 * h->r)) throw std::invalid_argument("ghost images need L > 4 r");
+    RefParams q = *rp;
+    q.k = 0.0;           // no mechanics: the forces op contributes nothing
+    q.fixed_box = h->r;  // boxes of the infection radius (point agents, d = 1 <= r)
+    q.sorting_frequency = 0;
+    q.detect_static = 0;
+    h->sim = std::make_unique<Simulation>(to_params(q));
+    h->ensure(n);
+    for (std::uint64_t i = 0; i < n; ++i) {
+      Agent& a = h->sim->add_agent({x[i], y[i], z[i]}, 1.0);
+      const std::uint64_t u = a.uid();
+      h->ensure(u);
+      h->st_old[u] = abs_u01(abs_rng_word(rp->seed, u, ABS_RNG_SIR_INIT)) < 0.01 ? ABS_SIR_I : ABS_SIR_S;
+      h->t_old[u] = 0;
+    }
+    RefSir* self = h.get();
+    self->add_ghosts();
+    self->sim->add_agent_operation("sir", 1, [self](Agent& a, AgentContext& ctx) {
+      const std::uint64_t u = a.uid();
+      if (self->ghost_of[u] >= 0) {  // an image of the previous iteration
+        ctx.remove_self();
+        return;
+      }
+      std::uint8_t st = self->st_old[u];
+      std::uint32_t ti = self->t_old[u];
+      const std::uint64_t it = ctx.iteration();
+      if (st == ABS_SIR_I && it - ti >= self->rec) st = ABS_SIR_R;
+      if (st == ABS_SIR_S) {
+        unsigned int k = 0;
+        ctx.for_each_neighbor(self->r, [&](Agent& b, double) {
+          const std::int64_t g = self->ghost_of[b.uid()];
+          const std::uint64_t real = g >= 0 ? static_cast<std::uint64_t>(g) : b.uid();
+          if (self->st_old[real] == ABS_SIR_I) ++k;
+        });
+        if (k > 0 && abs_rng_word(self->seed, u, ABS_RNG_SIR_INFECT(it)) < abs_sir_threshold(self->prob, k)) {
+          st = ABS_SIR_I;
+          ti = static_cast<std::uint32_t>(it);
+        }
+      }
+      self->st_new[u] = st;
+      self->t_new[u] = ti;
+      double dir[3];
+      abs_unit_vector(self->seed, u, ABS_RNG_SIR_WALK(it), dir);
+      a.translate({dir[0] * self->step, dir[1] * self->step, dir[2] * self->step});
+    });
+    self->sim->add_standalone_operation("sir_publish", Phase::kPost, 1, [self](Simulation& s) {
+      std::uint64_t c[3] = {0, 0, 0};
+      s.resource_manager().for_each_agent([&](Agent& a, AgentHandle) {
+        const std::uint64_t u = a.uid();
+        if (self->ghost_of[u] >= 0) return;
+        const Vec3& p = a.position();
+        a.set_position({abs_wrap(p.x, self->L), abs_wrap(p.y, self->L), abs_wrap(p.z, self->L)});
+        self->st_old[u] = self->st_new[u];
+        self->t_old[u] = self->t_new[u];
+        ++c[self->st_old[u]];
+      });
+      self->counts.insert(self->counts.end(), c, c + 3);
+      self->add_ghosts();
+    });
+    r = h.release();
+  });
+  return rc == 0 ? r : nullptr;
+}
+
+void ref_sir_destroy(void* h) { delete static_cast<RefSir*>(h); }
+
+int ref_sir_simulate(void* h, std::uint64_t iterations) {
+  return guarded([&] { static_cast<RefSir*>(h)->sim->simulate(iterations); });
+}
+
+// S/I/R counts after each completed iteration: out[3 * t + s], t < cap.
+std::int64_t ref_sir_counts(void* h, std::uint64_t* out, std::uint64_t cap) {
+  const RefSir& r = *static_cast<RefSir*>(h);
+  const std::uint64_t its = r.counts.size() / 3;
+  for (std::uint64_t t = 0; t < its && t < cap; ++t)
+    for (int k = 0; k < 3; ++k) out[3 * t + k] = r.counts[3 * t + k];
+  return static_cast<std::int64_t>(its);
+}
+
+// Real agents (ghosts excluded) in storage order: uid, position, state, infection iteration.
+int ref_sir_dump(void* h, std::uint64_t* uid, double* x, double* y, double* z, std::uint8_t* state,
+                 std::uint32_t* t_inf) {
+  return guarded([&] {
+    RefSir& r = *static_cast<RefSir*>(h);
+    std::uint64_t i = 0;
+    r.sim->resource_manager().for_each_agent([&](Agent& a, AgentHandle) {
+      const std::uint64_t u = a.uid();
+      if (r.ghost_of[u] >= 0) return;
+      uid[i] = u;
+      x[i] = a.position().x;
+      y[i] = a.position().y;
+      z[i] = a.position().z;
+      state[i] = r.st_old[u];
+      t_inf[i] = r.t_old[u];
+      ++i;
+    });
+  });
+}
+
+std::uint64_t ref_sir_agents(void* h) { return static_cast<RefSir*>(h)->n_real; }
 
 }  // extern "C"

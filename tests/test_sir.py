@@ -1,7 +1,9 @@
 """Config 5 (SIR on a periodic cube, absim_models.h). The reference has no
-periodic boundaries, so this model is pinned between the C
-oracle and the GPU only: bit-exact positions, states, infection iterations
-and S/I/R counts per step."""
+periodic boundaries; the unmodified reference engine runs the
+model with ghost images at the faces through its public hooks
+(oracle/ref_harness.cpp, RefSir), which pins the C port bit for bit
+(positions, states, infection iterations, S/I/R counts per step); the GPU
+is then checked against the port."""
 import numpy as np
 import pytest
 
@@ -12,6 +14,35 @@ from paper_2301_06984_b200 import configs as CF
 def _oparams(O, wl):
     prm = wl.params
     return O.OracleParams(seed=prm["seed"], model=prm["model"], mp=prm["model_params"])
+
+
+@pytest.mark.parametrize("n,steps,threads", [(3000, 45, 1), (12000, 30, 4)])
+def test_sir_port_equals_reference(oracle_mod, have_ref, n, steps, threads):
+    """The port's SIR restatement against the reference engine (ghost images):
+    identical per-step S/I/R counts, states, infection iterations and
+    positions; the step count crosses the recovery time (20)."""
+    if not have_ref:
+        pytest.skip("reference build (oracle/_ref) not present")
+    O = oracle_mod
+    wl = CF.c5_sir(n, seed=5)
+    p = _oparams(O, wl)
+    port = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+    p.threads = threads
+    ref = O.RefSirSim(p, wl.x, wl.y, wl.z)
+    hist = []
+    for _ in range(steps):
+        port.simulate(1)
+        hist.append(port.sir_counts())
+    ref.simulate(steps)
+    assert np.array_equal(ref.count_history(), np.array(hist, np.uint64))
+    r = by_uid(ref.dump())
+    o = port.dump()
+    o["state"], o["t"] = port.sir_state()
+    o = by_uid({k: o[k] for k in ("uid", "x", "y", "z", "state", "t")})
+    assert np.array_equal(r["uid"], o["uid"])
+    for k in ("x", "y", "z", "state", "t"):
+        assert np.array_equal(r[k], o[k]), k
+    assert hist[-1][2] > 0 and hist[-1][1] > 0
 
 
 def test_sir_oracle_invariants(oracle_mod):
