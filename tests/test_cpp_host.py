@@ -18,6 +18,46 @@ def _compile():
                     "-labsim_gpu", f"-Wl,-rpath,{LIBDIR}", "-o", OUT], check=True)
 
 
+BRIDGE_SRC = os.path.join(ROOT, "tests", "cpp", "gpu_step_clustering.cpp")
+BRIDGE_OUT = os.path.join(ROOT, "tests", "cpp", "_build", "gpu_step_clustering")
+REF_INC = "/root/reference/proj/include"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref")
+
+
+def compile_bridge():
+    """integration/gpu_step.hpp against the reference's public headers and the
+    unmodified reference library (oracle/_ref). Needs /root/reference, so it
+    is built in the build container (__graft_entry__.build) and the binary
+    travels with the snapshot."""
+    if not os.path.isdir(REF_INC):
+        return os.path.exists(BRIDGE_OUT)
+    os.makedirs(os.path.dirname(BRIDGE_OUT), exist_ok=True)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-Werror", "-ffp-contract=off", f"-I{REF_INC}",
+                    f"-I{ROOT}/include", f"-I{ROOT}/integration", BRIDGE_SRC, f"-L{LIBDIR}", "-labsim_gpu",
+                    f"-L{REF_LIB}", "-labsim_ref", f"-Wl,-rpath,{LIBDIR}", f"-Wl,-rpath,{REF_LIB}", "-pthread",
+                    "-o", BRIDGE_OUT], check=True)
+    return True
+
+
+def test_bridge_compiles(engine, oracle_mod):
+    if not os.path.isdir(REF_INC):
+        pytest.skip("reference headers not present (build container only)")
+    assert compile_bridge()
+
+
+@pytest.mark.gpu
+def test_bridge_runs_reference_clustering(engine):
+    """The reference's own Simulation + build_clustering population, its hot
+    path forwarded to the B200 through integration/gpu_step.hpp, against the
+    same population advanced by the unmodified reference."""
+    if not compile_bridge():
+        pytest.skip("bridge binary not built (needs /root/reference at build time)")
+    r = subprocess.run([BRIDGE_OUT, "20000", "20"], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout
+
+
 def test_cpp_host_compiles(engine):
     _compile()
     assert os.path.exists(OUT)
