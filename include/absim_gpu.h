@@ -13,16 +13,16 @@
  *                           = Environment::update → [staticness] → behaviours
  *                             → run_forces → run_integration → run_commit
  *   abs_gpu_stats           Simulation::report() counters                   report.hpp:32-40
- *   abs_gpu_download        ResourceManager::for_each_agent + Agent getters resource_manager.hpp:346, agent.hpp:31-110
+ *   abs_gpu_download        ResourceManager::for_each_agent + Agent getters resource_manager.hpp:70, agent.hpp:31-110
  *   abs_gpu_run_frames      add_agent -> simulate -> read agents, repeated over
  *                           independent host frames with copy/compute overlap simulation.hpp:107-121
- *   abs_gpu_env_update      Environment::update (UniformGrid::update)       environment.hpp:38, uniform_grid.cpp:155-266
+ *   abs_gpu_env_update      Environment::update (UniformGrid::update)       environment.hpp:40, uniform_grid.cpp:59-170
  *   abs_gpu_grid_info       UniformGrid::{origin, box_length, dims, largest_agent_diameter}  uniform_grid.hpp:40-49
- *   abs_gpu_cell_ids        UniformGrid::box_index_of (per agent)           uniform_grid.cpp:124-133
+ *   abs_gpu_cell_ids        UniformGrid::box_index_of (per agent)           uniform_grid.cpp:28-37
  *   abs_gpu_neighbors       Environment::for_each_neighbor (batched; force
- *                           query radius 0.5 (d + dmax), simulation.cpp:469) uniform_grid.cpp:268-326
+ *                           query radius 0.5 (d + dmax), simulation.cpp:469) uniform_grid.cpp:172-230
  *   abs_gpu_sort            sort_and_balance (one domain)                   sort_balance.cpp:22-148
- *   abs_gpu_remove          CommitBuffer removals / remove_agents_parallel  commit.cpp:86-178
+ *   abs_gpu_remove          CommitBuffer removals / remove_agents_parallel  commit.cpp:14-106
  *   abs_gpu_set_defer_commit / abs_gpu_division_marks / abs_gpu_commit
  *                           CommitBuffer::commit additions, split so ranks
  *                           agree on daughter uids                          commit.cpp:186-222, simulation.cpp:64-91
@@ -50,9 +50,9 @@ extern "C" {
 #define ABS_OK 0
 #define ABS_ERR_INVALID_ARGUMENT 1  /* std::invalid_argument in the reference */
 #define ABS_ERR_CUDA 2
-#define ABS_ERR_NONFINITE 3          /* "agent positions are not finite"  uniform_grid.cpp:208-212 */
-#define ABS_ERR_FIXED_BOX 4          /* fixed box < largest diameter     uniform_grid.cpp:214-221 */
-#define ABS_ERR_BOX_BUDGET 5         /* > 2^31 boxes                      uniform_grid.cpp:235-237 */
+#define ABS_ERR_NONFINITE 3          /* "agent positions are not finite"  uniform_grid.cpp:112-116 */
+#define ABS_ERR_FIXED_BOX 4          /* fixed box < largest diameter     uniform_grid.cpp:118-125 */
+#define ABS_ERR_BOX_BUDGET 5         /* > 2^31 boxes                      uniform_grid.cpp:139-141 */
 #define ABS_ERR_CAPACITY 6           /* device agent capacity exhausted */
 #define ABS_ERR_NO_DEVICE 7
 #define ABS_ERR_STATE 8              /* std::logic_error in the reference */
@@ -177,7 +177,7 @@ int abs_gpu_commit(abs_gpu_ctx* ctx, const uint32_t* global_marks_device, uint64
  * instead of the local bounds; grid == NULL restores the local grid. */
 int abs_gpu_set_grid_override(abs_gpu_ctx* ctx, const double* grid, const uint32_t* dims);
 /* Local bounds of the current population: out[0..2] min xyz, out[3..5]
- * max xyz, out[6] largest diameter (uniform_grid.cpp:170-206 pass 1). */
+ * max xyz, out[6] largest diameter (uniform_grid.cpp:74-110 pass 1). */
 int abs_gpu_local_bounds(abs_gpu_ctx* ctx, double* out7);
 
 /* Device-resident multi-domain exchange. Agents travel as

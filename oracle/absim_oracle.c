@@ -8,14 +8,14 @@
  *
  * Semantics follow the reference with ONE worker and ONE domain (the only
  * bitwise-deterministic mode, test_scheduler.cpp:196-212):
- *   grid build        uniform_grid.cpp:155-266 (pass 1, sizing, LIFO chains)
- *   box_index_of      uniform_grid.cpp:124-133
- *   for_each_neighbor uniform_grid.cpp:268-326 (z,y,x boxes; chain order)
+ *   grid build        uniform_grid.cpp:59-170 (pass 1, sizing, LIFO chains)
+ *   box_index_of      uniform_grid.cpp:28-37
+ *   for_each_neighbor uniform_grid.cpp:172-230 (z,y,x boxes; chain order)
  *   pairwise force    mechanics.cpp:10-27
  *   run_forces        simulation.cpp:463-489
  *   integration       agent.hpp:115-133, simulation.cpp:491-500
  *   staticness        simulation.cpp:334-386, flags agent.hpp:61-101
- *   commit            commit.cpp:86-178 (5-step removal), :236-297 (appends),
+ *   commit            commit.cpp:14-106 (5-step removal), :236-297 (appends),
  *                     mark_new_agent_neighbors simulation.cpp:510-530
  *   morton / offsets  morton.cpp:11-186
  *   sort_and_balance  sort_balance.cpp:22-148 (single domain)
@@ -186,7 +186,7 @@ void orc_destroy(orc_sim* s) {
 
 /* ---- uniform grid ------------------------------------------------------ */
 
-/* uniform_grid.cpp:124-133 */
+/* uniform_grid.cpp:28-37 */
 static uint64_t box_index_of(const orc_sim* s, double px, double py, double pz) {
   const double p[3] = {px, py, pz};
   uint64_t c[3];
@@ -200,7 +200,7 @@ static uint64_t box_index_of(const orc_sim* s, double px, double py, double pz) 
   return c[0] + s->dims[0] * (c[1] + (uint64_t)s->dims[1] * c[2]);
 }
 
-/* std::min / std::max argument order (b < a ? b : a), uniform_grid.cpp:191-194 */
+/* std::min / std::max argument order (b < a ? b : a), uniform_grid.cpp:95-96, 106-107 */
 static double smin(double a, double b) { return b < a ? b : a; }
 static double smax(double a, double b) { return a < b ? b : a; }
 
@@ -215,7 +215,7 @@ int orc_set_grid_override(orc_sim* s, const double* grid, const uint32_t* dims) 
   return 0;
 }
 
-/* uniform_grid.cpp:155-266 with one worker */
+/* uniform_grid.cpp:59-170 with one worker */
 int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) {
   s->indexed = s->n;
   if (s->n == 0) {
@@ -293,7 +293,7 @@ int orc_env_update(orc_sim* s, double* grid, uint32_t* dims, uint64_t* indexed) 
 
 typedef void (*visit_fn)(orc_sim* s, void* ctx, uint64_t j, double d2);
 
-/* uniform_grid.cpp:268-326; query == ORC_NIL means no exclusion */
+/* uniform_grid.cpp:172-230; query == ORC_NIL means no exclusion */
 static int for_each_neighbor(orc_sim* s, uint64_t query, double cx, double cy, double cz,
                              double r2, visit_fn fn, void* ctx) {
   if (s->indexed == 0) return 0;
@@ -666,7 +666,7 @@ int orc_rng_counters(const orc_sim* s, uint64_t* out) {
   return 0;
 }
 
-/* commit.cpp:86-178 (five steps, slot semantics independent of workers) */
+/* commit.cpp:14-106 (five steps, slot semantics independent of workers) */
 int orc_remove(orc_sim* s, const uint32_t* removed, uint32_t r) {
   if (r == 0) return 0;
   if (r > s->n) return fail("more removals than agents");
@@ -694,7 +694,7 @@ int orc_remove(orc_sim* s, const uint32_t* removed, uint32_t r) {
   return 0;
 }
 
-/* commit.cpp:236-297 with one staging slot */
+/* commit.cpp:186-222 with one staging slot */
 static int run_commit(orc_sim* s) {
   if (s->nstage == 0) return 0;
   if (s->p.detect_static && mark_new_agent_neighbors(s)) return -1;

@@ -169,7 +169,7 @@ class AbsimError(RuntimeError):
 
 def check(rc: int, ctx=None):
     """Map a status code to the reference's exception kinds (params.cpp:44-72,
-    uniform_grid.cpp:208-237): invalid_argument -> ValueError, others ->
+    uniform_grid.cpp:112-141): invalid_argument -> ValueError, others ->
     RuntimeError subclasses carrying the code."""
     if rc == ABS_OK:
         return

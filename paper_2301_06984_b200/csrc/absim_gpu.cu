@@ -2,15 +2,15 @@
 // mechanical-step engine. One iteration (Simulation::simulate body,
 // simulation.cpp:232-303) is:
 //
-//   k_reduce     bbox + largest diameter          uniform_grid.cpp:170-206
-//   k_finalize   box length, origin, dims, checks  uniform_grid.cpp:208-237
+//   k_reduce     bbox + largest diameter          uniform_grid.cpp:74-110
+//   k_finalize   box length, origin, dims, checks  uniform_grid.cpp:112-141
 //   k_key        bin of each agent + per-bin count (atomic slot = rank)
 //   scan         exclusive scan of bin counts -> cell table `start`
 //   k_scatter    permute state into cell order (coalesced SoA writes)
 //   k_mark       [static] disturbers flag neighbours  simulation.cpp:351-373
 //   k_force      behaviours + static skip + 27-box radius query + pairwise
 //                repulsion + force sum + integration     simulation.cpp:388-500
-//   commit       [additions] daughter uid ranks + append  commit.cpp:236-297
+//   commit       [additions] daughter uid ranks + append  commit.cpp:186-222
 //
 // Every kernel is a grid-stride loop over a device-resident agent count, so an
 // iteration needs no host synchronisation (counts change on the device).
@@ -121,7 +121,7 @@ __device__ void reset_reduction(DevGrid* g) {
   g->nonfinite = 0;
 }
 
-// uniform_grid.cpp:155-237 sizing; one thread.
+// uniform_grid.cpp:59-141 sizing; one thread.
 struct FinArgs {
   double fixed_box;
   int brute;
@@ -287,7 +287,7 @@ __global__ void k_finalize(DevGrid* g, FinArgs fa) {
 }
 
 // Environment update pass 1 in one launch: bounds reduction, then the last
-// block to finish sizes the grid (uniform_grid.cpp:155-237).
+// block to finish sizes the grid (uniform_grid.cpp:59-141).
 // zero_start != nullptr: also clears the previous iteration's cell table
 // (entries [0, nbins_prev]; every entry beyond is zero already), which the
 // last block's finalize may resize only after every block has counted in.
@@ -1698,7 +1698,7 @@ __global__ void k_mark_new(Soa S, const Pd* __restrict__ live, const DevGrid* g,
 // Daughters get uid = uid_count + rank of the parent among this iteration's
 // dividers in parent-uid order (= the reference's one-worker storage order
 // while storage order equals uid order, resource_manager.hpp:44-46), and are
-// appended at n + rank (commit.cpp:258-292: appends never move survivors).
+// appended at n + rank (commit.cpp:196-220: appends never move survivors).
 __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
                          const unsigned long long* __restrict__ st_parent,
                          const Pd* __restrict__ st_pd, const double* __restrict__ st_vol,
@@ -2244,7 +2244,7 @@ __global__ void k_find_slots(const unsigned long long* __restrict__ uid, const D
 }
 
 // ------------------------------------------------------------ removal
-// remove_agents_parallel (commit.cpp:86-178): holes left of the split are
+// remove_agents_parallel (commit.cpp:14-106): holes left of the split are
 // filled, in removal-list order, by surviving tail agents in index order.
 __global__ void k_remove_plan(const unsigned long long* __restrict__ slots, unsigned long long r,
                               unsigned long long new_size, unsigned int* __restrict__ to_right,

@@ -145,7 +145,7 @@ __device__ __forceinline__ int clamp_bin(double v, double s, unsigned int nb) {
   return static_cast<int>(t);
 }
 
-// Reference box coordinate (uniform_grid.cpp:124-133): floor((p-o)/box) clamped.
+// Reference box coordinate (uniform_grid.cpp:28-37): floor((p-o)/box) clamped.
 __device__ __forceinline__ unsigned int box_coord(double p, double o, double box, unsigned int dim) {
   const double rel = (p - o) / box;
   long long i = static_cast<long long>(floor(rel));
@@ -308,7 +308,7 @@ constexpr int kBatch = ABS_BATCH;
 
 // Box-lockstep variant (requires bins == reference boxes). Every lane walks
 // the 3x3x3 reference boxes around ITS box as 9 contiguous x-runs
-// (uniform_grid.cpp:199-201 without the per-lane trimming), so the lanes of a
+// (uniform_grid.cpp:198-200 without the per-lane trimming), so the lanes of a
 // warp whose agents share a box fetch the same candidate at the same time:
 // their loads coalesce into one broadcast instead of one L1 line per lane.
 template <class F>

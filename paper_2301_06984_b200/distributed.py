@@ -7,7 +7,7 @@ exchange (NCCL on GPUs, gloo for the CPU tests). Per iteration:
 
 1. **Global grid.** Each rank reduces the bounds of its owned agents; an
    all-reduce(MAX) over [-lo, hi, dmax] (7 doubles, exact) gives every rank
-   the single-domain grid (uniform_grid.cpp:170-237): origin, box length,
+   the single-domain grid (uniform_grid.cpp:74-141): origin, box length,
    dims. Cell ids and box geometry therefore match the one-process
    reference bit for bit.
 2. **Ownership by box layer.** Rank r owns the agents whose reference box z
@@ -86,7 +86,7 @@ class GlobalGrid:
 
 
 def global_grid(bounds7: np.ndarray, fixed_box_length: float = 0.0) -> GlobalGrid:
-    """uniform_grid.cpp:208-237 on all-reduced bounds (same IEEE ops)."""
+    """uniform_grid.cpp:112-141 on all-reduced bounds (same IEEE ops)."""
     lo, hi, dmax = bounds7[:3], bounds7[3:6], float(bounds7[6])
     if not (np.isfinite(lo).all() and np.isfinite(hi).all()):
         raise RuntimeError("agent positions are not finite")
@@ -103,7 +103,7 @@ def global_grid(bounds7: np.ndarray, fixed_box_length: float = 0.0) -> GlobalGri
 
 
 def box_layer(z: np.ndarray, g: GlobalGrid) -> np.ndarray:
-    """Reference box z-coordinate (uniform_grid.cpp:124-133)."""
+    """Reference box z-coordinate (uniform_grid.cpp:28-37)."""
     rel = (z - g.origin[2]) / g.box
     return np.clip(np.floor(rel), 0, g.dims[2] - 1).astype(np.int64)
 

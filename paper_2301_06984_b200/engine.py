@@ -390,6 +390,19 @@ class Simulation:
             _p(out["volume"], C.c_double)), self._ctx)
         return out
 
+    def fields(self, *names) -> dict:
+        """Download a subset of agents() (uid, x, y, z, d, partners, flags), device storage order."""
+        n = self.agent_count()
+        dt = {"uid": np.uint64, "partners": np.uint32, "flags": np.uint8}
+        out = {k: np.zeros(n, dt.get(k, np.float64)) for k in names}
+        nn = C.c_uint64(0)
+        g = lambda k, ct: _p(out[k], ct) if k in out else None  # noqa: E731
+        N.check(N.load().abs_gpu_download(
+            self._ctx, C.byref(nn), g("uid", C.c_uint64), g("x", C.c_double), g("y", C.c_double),
+            g("z", C.c_double), g("d", C.c_double), None, None, None, g("partners", C.c_uint32),
+            g("flags", C.c_uint8), None), self._ctx)
+        return out
+
     def positions(self, x, y, z) -> int:
         """Download positions into caller-owned float64 arrays (e.g. pinned);
         returns the agent count (device storage order)."""

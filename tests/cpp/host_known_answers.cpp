@@ -91,7 +91,7 @@ int main() {
       CHECK(std::fabs(a.last_force.x - expect) <= 1e-12 && a.last_force.y == 0.0 && a.last_force.z == 0.0);
     }
   }
-  {  // test_grid.cpp:163-181, :203-215 — floor/clamp, inclusive radius
+  {  // test_grid.cpp:68-86, :108-120 — floor/clamp, inclusive radius
     std::printf("grid\n");
     SimulationParams p;
     p.fixed_box_length = 20.0;
@@ -120,7 +120,7 @@ int main() {
     CHECK(pairs == 2);
     CHECK(std::string(two.environment().name()) == "uniform_grid");
   }
-  {  // errors: params.cpp:44-72, uniform_grid.cpp:214-221
+  {  // errors: params.cpp:44-72, uniform_grid.cpp:118-125
     std::printf("errors\n");
     SimulationParams p;
     p.simulation_time_step = 0.0;

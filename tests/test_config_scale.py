@@ -58,9 +58,14 @@ def test_c2_through_division_bursts(engine, oracle_mod):
 def _ref_counts_and_cells(O, st):
     """Reference engine on a downloaded state (agents created in uid order):
     per-uid box_index_of and force-query neighbour counts."""
-    o = np.argsort(st["uid"], kind="stable")
-    assert np.array_equal(st["uid"][o], np.arange(len(o), dtype=np.uint64))
-    ref = O.RefSim(O.OracleParams(seed=0, dt=0.01), st["x"][o], st["y"][o], st["z"][o], st["d"][o])
+    n = len(st["uid"])
+    u = st["uid"].astype(np.int64)
+    arrs = {}
+    for k in ("x", "y", "z", "d"):  # scatter into uid order (a permutation of 0..n-1)
+        a = np.empty(n)
+        a[u] = st[k]
+        arrs[k] = a
+    ref = O.RefSim(O.OracleParams(seed=0, dt=0.01), arrs["x"], arrs["y"], arrs["z"], arrs["d"])
     grid = ref.env_update()
     cells = ref.cell_ids()
     counts = ref.neighbor_counts()
@@ -72,7 +77,7 @@ def _gpu_cells(sim):
     env = sim.environment()
     env.update()
     ids = env.cell_ids()
-    uid = sim.agents()["uid"]
+    uid = sim.fields("uid")["uid"]
     out = np.empty(len(uid), np.uint64)
     out[uid.astype(np.int64)] = ids
     return env, out
@@ -89,7 +94,7 @@ def test_c4_full_scale_sort_iterations(engine, oracle_mod, have_ref):
     for target in (0, 10):
         if target:
             sim.simulate(target - sim.iteration)
-        pre = sim.agents()
+        pre = sim.fields("uid", "x", "y", "z", "d")
         env, gcells = _gpu_cells(sim)
         grid, rcells, rcounts = _ref_counts_and_cells(O, pre)
         assert np.array_equal(env.origin(), grid["origin"]) and env.box_length() == grid["box"], target
@@ -100,7 +105,7 @@ def test_c4_full_scale_sort_iterations(engine, oracle_mod, have_ref):
         sim.simulate(1)  # the sort iteration itself (sorting_frequency 10)
         sim.record_evaluations(False)
         ev = sim.evaluations()
-        uid = sim.agents()["uid"].astype(np.int64)
+        uid = sim.fields("uid")["uid"].astype(np.int64)
         gev = np.empty(n, np.uint32)
         gev[uid] = ev
         assert np.array_equal(gev, rcounts), f"per-agent evaluations at iteration {target}"

@@ -269,7 +269,7 @@ def test_static_on_off_same_trajectory(engine):
 
 
 def test_grid_known_answers(engine):
-    """test_grid.cpp:163-181 floor/clamp; :203-215 inclusive radius; :309-322 box = dmax."""
+    """test_grid.cpp:68-86 floor/clamp; :108-120 inclusive radius; :214-227 box = dmax."""
     sim = engine.Simulation(engine.SimulationParams(fixed_box_length=20.0))
     sim.add_agents([0.0, 100.0, 19.999, 100.0], [0.0, 100.0, 20.0, 100.0], [0.0, 100.0, 39.9, 100.0],
                    [10.0] * 4)
@@ -308,7 +308,7 @@ def test_single_agent_and_degenerate_volume(engine):
     assert sim.report().force_evaluations == 0
     a = sim.agents()
     assert (a["x"][0], a["y"][0], a["z"][0]) == (5.0, 5.0, 5.0)
-    # three coincident agents (test_grid.cpp:183-194) and the coincident-centre
+    # three coincident agents (test_acceptance.cpp:154-170 instance 7) and the coincident-centre
     # force of magnitude k * overlap (test_mechanics.cpp:55-72)
     sim = engine.Simulation(engine.SimulationParams(simulation_time_step=0.01))
     sim.add_agents([3.0] * 3, [3.0] * 3, [3.0] * 3, [10.0] * 3)
@@ -454,7 +454,7 @@ def test_removal_worked_example(engine):
 
 
 def test_removal_large_unordered(engine, oracle_mod):
-    """remove_agents_parallel survivor order (commit.cpp:86-178) for a large
+    """remove_agents_parallel survivor order (commit.cpp:14-106) for a large
     unordered removal list; slots are looked up on the device."""
     rng = np.random.default_rng(5)
     n = 20000

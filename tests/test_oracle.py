@@ -248,7 +248,7 @@ def test_static_front_known_answer(oracle_mod, have_ref):
 
 
 def test_grid_floor_clamp_known_answer(oracle_mod):
-    """test_grid.cpp:163-181: (19.999,20,39.9) -> (0,1,1); far corner clamps."""
+    """test_grid.cpp:68-86: (19.999,20,39.9) -> (0,1,1); far corner clamps."""
     O = oracle_mod
     x = np.array([0.0, 100.0, 19.999, 100.0])
     y = np.array([0.0, 100.0, 20.0, 100.0])
