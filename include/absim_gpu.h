@@ -198,6 +198,43 @@ int abs_gpu_import(abs_gpu_ctx* ctx, const void* records, uint64_t count, int as
 /* Remove every ghost agent (order-preserving compaction). */
 int abs_gpu_drop_ghosts(abs_gpu_ctx* ctx);
 
+/* Multi-GPU slab decomposition driven by the library: one
+ * context per GPU / rank; per iteration a device all-reduce of the bounds
+ * gives the single-domain grid, an all-reduced z-layer histogram gives
+ * equal-count slab edges (sort_balance.cpp:61-77 analogue), one export pass
+ * and one exchange move emigrants (owned) and boundary layers (ghosts) to the
+ * neighbouring slabs, then the iteration runs and the ghosts are dropped.
+ * Transport: the built-in NCCL one (abs_gpu_comm_init, unique id from
+ * abs_gpu_nccl_unique_id on one rank, shared by the caller), or callbacks.
+ * All device pointers; counts are host values; `stream` is the context's
+ * CUDA stream (cudaStream_t). Callbacks return 0 on success. */
+#define ABS_DT_F64_MAX 0 /* element-wise MAX of doubles */
+#define ABS_DT_U64_SUM 1
+#define ABS_DT_U32_SUM 2
+typedef struct {
+  void* user;
+  int (*allreduce)(void* user, void* dev, uint64_t count, int dtype, void* stream);
+  /* send n_lo / n_hi to the lo / hi neighbour slab, return what they send here */
+  int (*counts)(void* user, uint64_t n_lo, uint64_t n_hi, uint64_t* got_lo, uint64_t* got_hi, void* stream);
+  /* ABS_RECORD_BYTES-byte records: send_lo[n_lo] -> lo peer, send_hi[n_hi] -> hi peer;
+     receive got_lo records from the lo peer into recv_lo, got_hi from the hi peer into recv_hi */
+  int (*records)(void* user, const void* send_lo, uint64_t n_lo, const void* send_hi, uint64_t n_hi, void* recv_lo,
+                 uint64_t got_lo, void* recv_hi, uint64_t got_hi, void* stream);
+} abs_gpu_transport;
+int abs_gpu_nccl_unique_id(void* id_128_bytes);
+int abs_gpu_comm_init(abs_gpu_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+int abs_gpu_comm_set_transport(abs_gpu_ctx* ctx, const abs_gpu_transport* transport, int rank, int nranks);
+/* Reserve exchange records per direction (grown automatically otherwise). */
+int abs_gpu_comm_reserve(abs_gpu_ctx* ctx, uint64_t records);
+/* `iterations` decomposed iterations (the population is this rank's slab;
+ * uids global, uid_count the global count). */
+int abs_gpu_simulate_decomposed(abs_gpu_ctx* ctx, uint64_t iterations);
+/* Slab edges of the last iteration (nranks + 1 z-layers) and the owned agents. */
+int abs_gpu_decomp_info(abs_gpu_ctx* ctx, int64_t* layer_bounds, uint64_t* owned);
+/* Stream-ordered copy between any two pointers (host or device), then a
+ * synchronisation of `stream` (for transport callbacks staging through host memory). */
+int abs_gpu_memcpy(void* dst, const void* src, uint64_t bytes, void* stream);
+
 /* Config 5 (SIR): S/I/R counts after the last iteration, and the per-agent
  * state (0 S, 1 I, 2 R) + infection iteration in download order. */
 int abs_gpu_sir_counts(abs_gpu_ctx* ctx, uint64_t* out3);

@@ -39,7 +39,22 @@ EXPORTS = [
     "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
     "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times", "abs_gpu_run_frames",
     "abs_gpu_list_stats", "abs_gpu_record_evaluations", "abs_gpu_download_evaluations",
+    "abs_gpu_nccl_unique_id", "abs_gpu_comm_init", "abs_gpu_comm_set_transport", "abs_gpu_comm_reserve",
+    "abs_gpu_simulate_decomposed", "abs_gpu_decomp_info", "abs_gpu_memcpy",
 ]
+
+DT_F64_MAX, DT_U64_SUM, DT_U32_SUM = 0, 1, 2
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p)
+COUNTS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                        C.c_void_p)
+RECORDS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
+                         C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+class Transport(C.Structure):
+    """abs_gpu_transport: caller-side collectives of the slab decomposition."""
+    _fields_ = [("user", C.c_void_p), ("allreduce", ALLREDUCE_FN), ("counts", COUNTS_FN), ("records", RECORDS_FN)]
 
 
 class Config(C.Structure):
@@ -152,6 +167,13 @@ def load():
         "abs_gpu_list_stats": (C.c_int, [_CTX, _U64, _D]),
         "abs_gpu_record_evaluations": (C.c_int, [_CTX, C.c_int]),
         "abs_gpu_download_evaluations": (C.c_int, [_CTX, _U32, C.c_uint64]),
+        "abs_gpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
+        "abs_gpu_comm_init": (C.c_int, [_CTX, C.c_void_p, C.c_int, C.c_int]),
+        "abs_gpu_comm_set_transport": (C.c_int, [_CTX, C.POINTER(Transport), C.c_int, C.c_int]),
+        "abs_gpu_comm_reserve": (C.c_int, [_CTX, C.c_uint64]),
+        "abs_gpu_simulate_decomposed": (C.c_int, [_CTX, C.c_uint64]),
+        "abs_gpu_decomp_info": (C.c_int, [_CTX, C.POINTER(C.c_int64), _U64]),
+        "abs_gpu_memcpy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

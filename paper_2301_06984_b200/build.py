@@ -24,6 +24,7 @@ FLAGS = [
     "--fmad=false",
     "-Xcompiler", "-fPIC", "-shared",
     "-I" + os.path.join(ROOT, "include"),
+    "-ldl",  # NCCL is dlopen-ed by the multi-GPU driver (decomp.cuh)
 ]
 
 

@@ -1329,7 +1329,6 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
   __syncthreads();
   const unsigned long long n = g->n;
   const double dmax = g->dmax;
-  const double lox = g->lorigin[0], loy = g->lorigin[1], loz = g->lorigin[2];
   const float slack = g->lslack;
   const double sl = static_cast<double>(slack);
   const int lane = threadIdx.x & 31;
@@ -2381,6 +2380,7 @@ struct abs_gpu_ctx {
   // the next list step will see, and the last step's largest displacement
   double pred_acc = 0.0, pred_rate = 0.0;
   bool track_now = false;               // this iteration tracks its largest displacement (kind 3)
+  struct abs_gpu_decomp* decomp = nullptr;  // multi-GPU slab decomposition (decomp.cuh)
   double build_ms = 0.0;
   unsigned long long build_launches = 0;
   std::vector<cudaEvent_t> bev;  // pairs around k_list_build (timing on)
@@ -3127,6 +3127,9 @@ int map_dev_err(abs_gpu_ctx* c, const DevGrid& h) {
       return set_err(c, ABS_ERR_FIXED_BOX, "operation 'environment update' failed at iteration " +
                                                std::to_string(h.failed_iteration) +
                                                ": fixed box length is smaller than the largest agent diameter");
+    case kErrSlabs:
+      return set_err(c, ABS_ERR_STATE, "slab decomposition at iteration " + std::to_string(h.failed_iteration) +
+                                           ": fewer than 3 z box layers per rank");
     case kErrQueryRadius:
       return set_err(c, ABS_ERR_INVALID_ARGUMENT, "operation 'behaviours' failed at iteration " +
                                                       std::to_string(h.failed_iteration) +
@@ -3238,6 +3241,7 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
 }
 
 static void free_sort_scratch(abs_gpu_ctx* c);
+void decomp_destroy(abs_gpu_ctx* c);  // decomp.cuh
 
 int abs_gpu_destroy(abs_gpu_ctx* c) {
   if (!c) return ABS_OK;
@@ -3269,6 +3273,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   for (cudaEvent_t e : c->pev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  decomp_destroy(c);
   delete c;
   return ABS_OK;
 }
@@ -4502,3 +4507,5 @@ int abs_gpu_reset_timers(abs_gpu_ctx* c, int enable) {
 }
 
 }  // extern "C"
+
+#include "decomp.cuh"

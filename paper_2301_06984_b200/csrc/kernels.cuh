@@ -49,6 +49,7 @@ enum DevErr : int {
   kErrQueryRadius = 6,  // a behaviour's query radius exceeds the box (uniform_grid.cpp:176-181)
   kErrSortRetry = 7,    // internal: the host's counting-sort guess did not fit; re-run with the exact path
   kErrListRebuild = 8,  // internal: the neighbour lists no longer cover the query radius; re-run as a rebuild
+  kErrSlabs = 9,        // slab decomposition: fewer than 3 z-layers per rank
 };
 
 // Grid + bookkeeping living in device memory (one per context).

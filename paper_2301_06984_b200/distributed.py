@@ -112,6 +112,37 @@ def layer_bounds(dims_z: int, world: int) -> np.ndarray:
     return np.array([(r * dims_z) // world for r in range(world + 1)], np.int64)
 
 
+HIST_BINS, MIN_LAYERS = 4096, 3  # decomp.cuh kHistBins / kMinLayers
+
+
+def balanced_bounds(layer_counts: np.ndarray, world: int, min_layers: int = MIN_LAYERS) -> np.ndarray:
+    """Slab edges with equal agent counts (the host mirror of decomp.cuh's
+    k_layer_bounds, integer for integer): layers coarsened into <= 4096 bins,
+    edge r = first bin edge whose prefix exceeds r * total / world, every
+    slab >= min_layers layers (the analogue of sort_balance.cpp:61-77)."""
+    D = len(layer_counts)
+    if D < world * min_layers:
+        raise RuntimeError("fewer than 3 z box layers per rank")
+    cz = (D + HIST_BINS - 1) // HIST_BINS
+    nb = (D + cz - 1) // cz
+    hist = np.zeros(nb, np.int64)
+    np.add.at(hist, np.arange(D) // cz, np.asarray(layer_counts, np.int64))
+    total = int(hist.sum())
+    lb = np.zeros(world + 1, np.int64)
+    lb[world] = D
+    run, b = 0, 0
+    for r in range(1, world):
+        target = (total * r) // world
+        while b < nb and run + int(hist[b]) <= target:
+            run += int(hist[b])
+            b += 1
+        e = b * cz if total else (D * r) // world
+        lo_ok = int(lb[r - 1]) + min_layers
+        hi_ok = D - (world - r) * min_layers
+        lb[r] = min(max(e, lo_ok), hi_ok)
+    return lb
+
+
 class SlabDecomposition:
     """Drives one rank. `engine` implements load/set_grid_override/step/dump/
     counters (see GpuRankEngine / tests' OracleRankEngine)."""
@@ -267,7 +298,8 @@ def sir_grid(L: float, r: float) -> GlobalGrid:
     return GlobalGrid(np.zeros(3), L / D, r, np.array([D, D, D], np.int64))
 
 
-def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, mask=None, grid=None):
+def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, mask=None, grid=None,
+                      balanced=False):
     """The owned slice of a population for `rank` (box layers of the initial
     grid, or of `grid` when given — e.g. the periodic grid of config 5)."""
     n = len(x)
@@ -282,65 +314,64 @@ def initial_partition(x, y, z, d, world: int, rank: int, fixed_box_length=0.0, m
         g = global_grid(b, fixed_box_length)
     else:
         g = grid
-    L = layer_bounds(int(g.dims[2]), world)
     lay = box_layer(st["z"], g)
+    if balanced:  # the device driver's equal-count edges (DeviceSlabDecomposition)
+        L = balanced_bounds(np.bincount(lay, minlength=int(g.dims[2])), world)
+    else:
+        L = layer_bounds(int(g.dims[2]), world)
     return _take(st, np.nonzero((lay >= L[rank]) & (lay < L[rank + 1]))[0])
 
 
 class DeviceSlabDecomposition:
-    """The same decomposition with a device-resident population: agents stay
-    in the rank's HBM; per iteration only the 7-double bounds, migrants and
-    the two boundary layers (packed 96-byte records, ABS_RECORD_BYTES) move.
-    transport="nccl": CUDA tensors straight through torch.distributed (NCCL
-    over NVLink); transport="host": staged through host tensors (gloo) — used
-    to test several ranks sharing one GPU."""
+    """The library's own slab decomposition (csrc/decomp.cuh,
+    abs_gpu_simulate_decomposed): agents stay in the rank's HBM; per
+    iteration a device all-reduce of the bounds gives the single-domain grid,
+    an all-reduced z-layer histogram gives equal-count slab edges
+    (balanced_bounds), and one export pass + one exchange move emigrants
+    (owned records) and boundary layers (ghosts, ABS_RECORD_BYTES each).
+    transport="nccl": the library's NCCL communicator (abs_gpu_comm_init; rank
+    0 draws the unique id, torch.distributed shares it). transport="host": the
+    same driver with collectives supplied here through torch.distributed
+    (gloo, staged through host memory) — used to test several ranks sharing
+    one GPU."""
 
     RECORD = 96
 
     def __init__(self, sim, dist, rank: int, world: int, fixed_box_length: float = 0.0,
                  transport: str = "nccl", cap: int = 1 << 20):
+        import ctypes as C
+
         import torch
+
+        from . import _native as N
         self.sim, self.dist, self.rank, self.world = sim, dist, rank, world
-        self.fixed_box_length = fixed_box_length
         self.transport = transport
         self.torch = torch
         self.dev = torch.device("cuda", torch.cuda.current_device())
-        self._alloc(cap)
         self._r0 = sim.report()
         self.iteration = 0
-        # additions (config 2): daughters are committed only after the ranks
-        # have summed their division marks, so uids match the single domain
-        from ._native import MODEL_GROW_DIVIDE, MODEL_PROLIFERATION, MODEL_SIR
-        self.additions = sim.params.model in (MODEL_PROLIFERATION, MODEL_GROW_DIVIDE)
-        self._marks = None
-        if self.additions:
-            sim.set_defer_commit(True)
-        # config 5: the periodic cube's fixed grid (abs_gpu_create: box L / D,
-        # D = max(3, floor(L / r))); slabs form a ring of z layers
+        from ._native import MODEL_SIR
         self.periodic = sim.params.model == MODEL_SIR
-        if self.periodic:
-            self._fixed = sir_grid(float(sim.params.model_params[0]), float(sim.params.model_params[1]))
-        # NCCL: the first P2P batch must not be a communicator's first call
+        if fixed_box_length != sim.params.fixed_box_length:
+            raise ValueError("fixed_box_length is the context's (SimulationParams.fixed_box_length)")
+        lib = N.load()
+        if transport == "nccl":
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                N.check(lib.abs_gpu_nccl_unique_id(uid.data_ptr()))
+            box = uid.to(self.dev) if dist.get_backend() == "nccl" else uid
+            dist.broadcast(box, 0)
+            uid = box.cpu()
+            N.check(lib.abs_gpu_comm_init(sim._ctx, uid.data_ptr(), rank, world), sim._ctx)
+        else:
+            self._tr = N.Transport(None, N.ALLREDUCE_FN(self._cb_allreduce), N.COUNTS_FN(self._cb_counts),
+                                   N.RECORDS_FN(self._cb_records))
+            N.check(lib.abs_gpu_comm_set_transport(sim._ctx, C.byref(self._tr), rank, world), sim._ctx)
+        N.check(lib.abs_gpu_comm_reserve(sim._ctx, cap), sim._ctx)
         self.dist.barrier()
 
-    def _alloc(self, cap):
-        t = self.torch
-        self.cap = cap
-        self.buf = {k: t.empty(cap * self.RECORD, dtype=t.uint8, device=self.dev)
-                    for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
-
-    # -- collectives -----------------------------------------------------------
-    def _coll_tensor(self, a):
-        t = self.torch.from_numpy(np.ascontiguousarray(a))
-        return t.to(self.dev) if self.transport == "nccl" else t
-
-    def _allreduce(self, a, op):
-        t = self._coll_tensor(a)
-        self.dist.all_reduce(t, op=op)
-        return t.cpu().numpy()
-
+    # -- host transport (torch.distributed, staged through host memory) ------------
     def _peers(self):
-        """(lo peer, hi peer); None at an open slab end. Periodic: a ring."""
         r, w = self.rank, self.world
         if w == 1:
             return None, None
@@ -348,13 +379,30 @@ class DeviceSlabDecomposition:
             return (r - 1) % w, (r + 1) % w
         return (r - 1 if r > 0 else None), (r + 1 if r < w - 1 else None)
 
+    def _copy(self, dst, src, nbytes, stream):
+        from . import _native as N
+        return N.load().abs_gpu_memcpy(dst, src, nbytes, stream)
+
+    def _cb_allreduce(self, user, dev, count, dtype, stream):
+        try:
+            t = self.torch
+            from . import _native as N
+            dt = {N.DT_F64_MAX: t.float64, N.DT_U64_SUM: t.int64, N.DT_U32_SUM: t.int32}[dtype]
+            host = t.empty(count, dtype=dt)
+            nbytes = count * host.element_size()
+            if self._copy(host.data_ptr(), dev, nbytes, stream):
+                return 1
+            self.dist.all_reduce(host, op=self.dist.ReduceOp.MAX if dtype == N.DT_F64_MAX else self.dist.ReduceOp.SUM)
+            return 1 if self._copy(dev, host.data_ptr(), nbytes, stream) else 0
+        except Exception:  # a callback must not raise through C
+            import traceback
+            traceback.print_exc()
+            return 1
+
     def _p2p(self, sends, recvs):
-        """One batched round of point-to-point transfers (a single NCCL group,
-        so paired sends/receives cannot deadlock). sends/recvs: lists of
-        (tensor, peer, tag). Messages to one peer are posted lo-side first and
-        received hi-side first on every rank, so at world 2 on a ring (both
-        peers the same rank) the in-order matching of NCCL pairs each message
-        with the right buffer; the tags do the same for gloo."""
+        """One batched round (paired sends/receives cannot deadlock). Messages
+        to one peer are posted lo-side first and received hi-side first, with
+        direction tags, so a two-rank ring (both peers the same rank) matches."""
         d = self.dist
         ops = [d.P2POp(d.isend, t, p, tag=tag) for t, p, tag in sends]
         ops += [d.P2POp(d.irecv, t, p, tag=tag) for t, p, tag in recvs]
@@ -362,125 +410,82 @@ class DeviceSlabDecomposition:
             for w in d.batch_isend_irecv(ops):
                 w.wait()
 
-    def _exchange(self, n_lo: int, n_hi: int):
-        """Send send_lo[:n_lo] to the lo peer and send_hi[:n_hi] to the hi peer;
-        returns the received record counts (from lo peer, from hi peer) into
-        recv_lo / recv_hi. Tag 1: travels to the receiver's hi side, tag 0: to
-        its lo side."""
-        t = self.torch
-        lo_p, hi_p = self._peers()
-        sends, recvs, cnt = [], [], {}
-        if lo_p is not None:
-            sends.append((self._coll_tensor(np.array([n_lo], np.int64)), lo_p, 1))
-        if hi_p is not None:
-            sends.append((self._coll_tensor(np.array([n_hi], np.int64)), hi_p, 0))
-        if hi_p is not None:
-            cnt["hi"] = self._coll_tensor(np.zeros(1, np.int64))
-            recvs.append((cnt["hi"], hi_p, 1))
-        if lo_p is not None:
-            cnt["lo"] = self._coll_tensor(np.zeros(1, np.int64))
-            recvs.append((cnt["lo"], lo_p, 0))
-        self._p2p(sends, recvs)
-        got = {k: int(v.cpu().item()) for k, v in cnt.items()}
-        need = max([n_lo if lo_p is not None else 0, n_hi if hi_p is not None else 0] + list(got.values()) + [0])
-        if need > self.cap:
-            raise RuntimeError("halo larger than the exchange buffers")
-        staged = []
+    def _cb_counts(self, user, n_lo, n_hi, got_lo, got_hi, stream):
+        try:
+            t = self.torch
+            lo_p, hi_p = self._peers()
+            sends, recvs, cnt = [], [], {}
+            if lo_p is not None:
+                sends.append((t.tensor([n_lo], dtype=t.int64), lo_p, 1))
+            if hi_p is not None:
+                sends.append((t.tensor([n_hi], dtype=t.int64), hi_p, 0))
+            if hi_p is not None:
+                cnt["hi"] = t.zeros(1, dtype=t.int64)
+                recvs.append((cnt["hi"], hi_p, 1))
+            if lo_p is not None:
+                cnt["lo"] = t.zeros(1, dtype=t.int64)
+                recvs.append((cnt["lo"], lo_p, 0))
+            self._p2p(sends, recvs)
+            got_lo[0] = int(cnt["lo"].item()) if "lo" in cnt else 0
+            got_hi[0] = int(cnt["hi"].item()) if "hi" in cnt else 0
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
 
-        def buf(key, nbytes, incoming):
-            if self.transport == "nccl":
-                return self.buf[key][:nbytes]
-            if not incoming:
-                return self.buf[key][:nbytes].cpu()
-            host = t.empty(nbytes, dtype=t.uint8)
-            staged.append((key, host))
-            return host
-        sends, recvs = [], []
-        if lo_p is not None and n_lo:
-            sends.append((buf("send_lo", n_lo * self.RECORD, False), lo_p, 1))
-        if hi_p is not None and n_hi:
-            sends.append((buf("send_hi", n_hi * self.RECORD, False), hi_p, 0))
-        if got.get("hi", 0):
-            recvs.append((buf("recv_hi", got["hi"] * self.RECORD, True), hi_p, 1))
-        if got.get("lo", 0):
-            recvs.append((buf("recv_lo", got["lo"] * self.RECORD, True), lo_p, 0))
-        self._p2p(sends, recvs)
-        for key, host in staged:
-            self.buf[key][:host.numel()].copy_(host.to(self.dev))
-        # the engine consumes the buffers on its own CUDA stream: make the
-        # received bytes (NCCL / staging copies on torch's stream) visible first
-        t.cuda.current_stream().synchronize()
-        return got.get("lo", 0), got.get("hi", 0)
+    def _cb_records(self, user, send_lo, n_lo, send_hi, n_hi, recv_lo, got_lo, recv_hi, got_hi, stream):
+        try:
+            t = self.torch
+            R = self.RECORD
+            lo_p, hi_p = self._peers()
+            sends, recvs, land = [], [], []
+            for ptr, cnt_, peer, tag in ((send_lo, n_lo, lo_p, 1), (send_hi, n_hi, hi_p, 0)):
+                if peer is not None and cnt_:
+                    host = t.empty(cnt_ * R, dtype=t.uint8)
+                    if self._copy(host.data_ptr(), ptr, cnt_ * R, stream):
+                        return 1
+                    sends.append((host, peer, tag))
+            for ptr, cnt_, peer, tag in ((recv_hi, got_hi, hi_p, 1), (recv_lo, got_lo, lo_p, 0)):
+                if peer is not None and cnt_:
+                    host = t.empty(cnt_ * R, dtype=t.uint8)
+                    recvs.append((host, peer, tag))
+                    land.append((ptr, host))
+            self._p2p(sends, recvs)
+            for ptr, host in land:
+                if self._copy(ptr, host.data_ptr(), host.numel(), stream):
+                    return 1
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
 
-    # -- one iteration -------------------------------------------------------------
-    def _export(self, g, lo, hi, mode):
+    # -- driving ---------------------------------------------------------------------
+    def simulate(self, iterations: int):
         from . import _native as N
-        import ctypes as C
-        if self.periodic:
-            mode |= 2
-        grid, dims = g.as_override()
-        grid = np.ascontiguousarray(grid)
-        dims = np.ascontiguousarray(dims, np.uint32)
-        a, b = C.c_uint64(0), C.c_uint64(0)
-        rc = N.load().abs_gpu_export_layers(self.sim._ctx, grid.ctypes.data_as(C.POINTER(C.c_double)),
-                                            dims.ctypes.data_as(C.POINTER(C.c_uint32)), int(lo), int(hi), mode,
-                                            self.buf["send_lo"].data_ptr(), self.buf["send_hi"].data_ptr(),
-                                            self.cap, C.byref(a), C.byref(b))
-        N.check(rc, self.sim._ctx)
-        return int(a.value), int(b.value)
-
-    def _import(self, key, count, ghost):
-        from . import _native as N
-        if count:
-            N.check(N.load().abs_gpu_import(self.sim._ctx, self.buf[key].data_ptr(), count, 1 if ghost else 0),
-                    self.sim._ctx)
+        N.check(N.load().abs_gpu_simulate_decomposed(self.sim._ctx, iterations), self.sim._ctx)
+        self.iteration += iterations
 
     def step(self):
-        from . import _native as N
-        if self.periodic:  # fixed grid, already forced at context creation
-            g = self._fixed
-        else:
-            b = self.sim.local_bounds()
-            red = self._allreduce(np.concatenate([-b[:3], b[3:]]), self.dist.ReduceOp.MAX)
-            g = global_grid(np.concatenate([-red[:3], red[3:]]), self.fixed_box_length)
-        L = layer_bounds(int(g.dims[2]), self.world)
-        lo, hi = L[self.rank], L[self.rank + 1]
-        n_lo, n_hi = self._export(g, lo, hi, 0)            # migrants leave
-        got_lo, got_hi = self._exchange(n_lo, n_hi)
-        self._import("recv_lo", got_lo, False)
-        self._import("recv_hi", got_hi, False)
-        n_lo, n_hi = self._export(g, lo, hi, 1)            # boundary layers
-        got_lo, got_hi = self._exchange(n_lo, n_hi)
-        self._import("recv_lo", got_lo, True)
-        self._import("recv_hi", got_hi, True)
-        if not self.periodic:
-            grid, dims = g.as_override()
-            self.sim.set_grid_override(grid, dims)
-        self.sim.simulate(1)
-        if self.additions:
-            self._commit_additions()
-        N.check(N.load().abs_gpu_drop_ghosts(self.sim._ctx), self.sim._ctx)
-        self.iteration += 1
-        return g
+        self.simulate(1)
 
-    def _commit_additions(self):
-        """Sum the ranks' uid-indexed division marks (every uid divides on at
-        most one rank) and commit: daughter uid = uid_count + rank of the
-        parent among all dividers (commit.cpp:186-222)."""
-        t = self.torch
-        length = self.sim.division_marks()  # uid_count: identical on every rank
-        if self._marks is None or self._marks.numel() < max(length, 1):
-            self._marks = t.zeros(max(int(length * 1.5), 1024), dtype=t.int32, device=self.dev)
-        self.sim.division_marks(self._marks.data_ptr(), self._marks.numel())
-        view = self._marks[:length]
-        if self.transport == "nccl":
-            self.dist.all_reduce(view, op=self.dist.ReduceOp.SUM)
-        else:
-            host = view.cpu()
-            self.dist.all_reduce(host, op=self.dist.ReduceOp.SUM)
-            view.copy_(host.to(self.dev))
-        t.cuda.current_stream().synchronize()  # the engine reads the sum on its own stream
-        self.sim.commit(view.data_ptr(), length)
+    def info(self):
+        """(slab edges of the last iteration as z-layers, owned agents)."""
+        import ctypes as C
+
+        from . import _native as N
+        lb = (C.c_int64 * (self.world + 1))()
+        owned = C.c_uint64(0)
+        N.check(N.load().abs_gpu_decomp_info(self.sim._ctx, lb, C.byref(owned)), self.sim._ctx)
+        return np.array(lb[:], np.int64), int(owned.value)
+
+    def _allreduce(self, a, op):
+        t = self.torch.from_numpy(np.ascontiguousarray(a))
+        if self.dist.get_backend() == "nccl":
+            t = t.to(self.dev)
+        self.dist.all_reduce(t, op=op)
+        return t.cpu().numpy()
 
     def sir_counts(self):
         """Config 5: S/I/R over all ranks after the last iteration."""
@@ -494,7 +499,3 @@ class DeviceSlabDecomposition:
         tot = self._allreduce(np.array([r.force_evaluations - self._r0.force_evaluations,
                                         r.force_skips - self._r0.force_skips], np.int64), self.dist.ReduceOp.SUM)
         return int(tot[0]), int(tot[1])
-
-    def simulate(self, iterations: int):
-        for _ in range(iterations):
-            self.step()

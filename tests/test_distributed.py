@@ -120,6 +120,30 @@ def test_slab_decomposition_matches_single_domain(oracle_mod, world, case):
     assert (evals, skips) == (c["force_evaluations"], c["force_skips"])
 
 
+def test_balanced_slab_edges():
+    """Equal-count edges (decomp.cuh k_layer_bounds mirror): a dense middle
+    (the c3 spheroid's profile) gets thin slabs, the ends thick ones, and no
+    slab is thinner than 3 layers."""
+    prof = np.array([1] * 20 + [50] * 20 + [1] * 20)
+    lb = D.balanced_bounds(prof, 4)
+    assert lb[0] == 0 and lb[-1] == 60 and (np.diff(lb) >= 3).all()
+    share = [prof[lb[r]:lb[r + 1]].sum() for r in range(4)]
+    assert max(share) <= 1.25 * sum(share) / 4  # one 50-agent layer is 19 % of a share
+    assert list(D.balanced_bounds(np.zeros(12, np.int64), 4)) == [0, 3, 6, 9, 12]
+    with pytest.raises(RuntimeError):
+        D.balanced_bounds(np.ones(8), 3)
+    # c3 at 8 ranks: equal-count slabs keep the largest share within 5 % of the mean
+    wl = CF.c3_spheroid(60000, seed=0)
+    b = np.array([wl.x.min(), wl.y.min(), wl.z.min(), wl.x.max(), wl.y.max(), wl.z.max(), wl.d.max()])
+    g = D.global_grid(b)
+    counts = np.bincount(D.box_layer(wl.z, g), minlength=int(g.dims[2]))
+    lb = D.balanced_bounds(counts, 8)
+    share = np.array([counts[lb[r]:lb[r + 1]].sum() for r in range(8)])
+    eq = D.layer_bounds(int(g.dims[2]), 8)
+    share_eq = np.array([counts[eq[r]:eq[r + 1]].sum() for r in range(8)])
+    assert share.max() / share.mean() < share_eq.max() / share_eq.mean()
+
+
 def test_grid_and_layers_helpers():
     b = np.array([0.0, 0.0, 0.0, 100.0, 50.0, 95.0, 10.0])
     g = D.global_grid(b)
@@ -196,7 +220,7 @@ def _dev_worker(rank, world, port, case, outdir):
     sir = wl.params.get("model") == E.MODEL_SIR
     mask = wl.mask if wl.mask is not None else np.ones(wl.n, np.uint8)  # None = behaviour on every agent
     grid = D.sir_grid(wl.params["model_params"][0], wl.params["model_params"][1]) if sir else None
-    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=mask, grid=grid)
+    st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=mask, grid=grid, balanced=True)
     sim = E.Simulation(E.SimulationParams(**wl.params), device=0)
     sim.add_agents(st["x"], st["y"], st["z"], st["d"], behaviour_mask=None if sir else st["beh"], uid=st["uid"],
                    uid_count=wl.n)  # SIR: initial states from (seed, uid), as in one domain
