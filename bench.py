@@ -242,18 +242,40 @@ def _slab_workload(n_per, world, rank, seed=0):
     return x, y, z, d, uid, L
 
 
+def _decomposed_workload(args, world, rank):
+    """(x, y, z, d, mask, uid, uid_count, params, name, scaling, per-rank
+    nominal agents) of this rank's slab. c4 weak: 2^26 agents per GPU in one
+    cube; c4 strong: 2^26 in total; c3 (strong): the 2^23-agent spheroid split
+    into equal-count slabs (distributed.balanced_bounds, the device driver's
+    own edges)."""
+    import numpy as np
+    from paper_2301_06984_b200 import distributed as D
+    if args.config == "c3":
+        wl = _workload("c3", args.n, args.seed)
+        st = D.initial_partition(wl.x, wl.y, wl.z, wl.d, world, rank, mask=wl.mask, balanced=True)
+        prm = dict(wl.params)
+        return (st["x"], st["y"], st["z"], st["d"], st["beh"], st["uid"], wl.n, prm, wl.name, "strong",
+                wl.n / world)
+    strong = args.scaling == "strong"
+    total = args.n or (1 << 26)
+    n_per = total // world if strong else total
+    x, y, z, d, uid, L = _slab_workload(n_per, world, rank, args.seed)
+    prm = dict(seed=args.seed, simulation_time_step=0.01)
+    return (x, y, z, d, None, uid, n_per * world, prm, "c4_large_uniform", "strong" if strong else "weak", n_per)
+
+
 def run_decomposed(args, dist, world, rank, local):
-    """N GPUs: slab decomposition with the device-resident exchange over NCCL."""
+    """N GPUs: the library's slab decomposition (csrc/decomp.cuh) over NCCL."""
     import torch
 
     import paper_2301_06984_b200 as E
     from paper_2301_06984_b200 import distributed as D
-    n_per = args.n or (1 << 26)
-    x, y, z, d, uid, L = _slab_workload(n_per, world, rank, args.seed)
-    prm = dict(seed=args.seed, simulation_time_step=0.01, record_forces=False,
-               bins_per_box=args.bins, bins_per_box_x=args.bins_x, capacity=int(n_per * 1.3))
+    x, y, z, d, mask, uid, uid_count, prm, name, scaling, n_nominal = _decomposed_workload(args, world, rank)
+    n_per = len(x)
+    prm = dict(prm, record_forces=False, bins_per_box=args.bins, bins_per_box_x=args.bins_x,
+               capacity=int(max(n_per, n_nominal) * 1.3) + 1024)
     sim = E.Simulation(E.SimulationParams(**prm), device=local)
-    sim.add_agents(x, y, z, d, uid=uid, uid_count=n_per * world)
+    sim.add_agents(x, y, z, d, behaviour_mask=mask, uid=uid, uid_count=uid_count)
     dec = D.DeviceSlabDecomposition(sim, dist, rank, world, transport="nccl",
                                     cap=int(0.06 * n_per) + (1 << 20))
     dec.simulate(args.warmup)
@@ -276,7 +298,7 @@ def run_decomposed(args, dist, world, rank, local):
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    owned = torch.tensor([float(sim.agent_count())], device="cuda")
+    owned = torch.tensor([float(dec.info()[1])], device="cuda")
     dist.all_reduce(owned)
     total = float(owned.item())
     value = total * args.steps / (ms_max / 1e3)
@@ -298,20 +320,21 @@ def run_decomposed(args, dist, world, rank, local):
         n_e = 0
         it = args.warmup + args.steps
         for k in range(e2e_steps):
-            sim.add_agents(*pin[:4], uid=pin[4], uid_count=n_per * world)
+            sim.add_agents(*pin[:4], behaviour_mask=mask, uid=pin[4], uid_count=uid_count)
             sim.set_iteration(it + k)
             dec.simulate(1)
             n_e = sim.positions(*outp)
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device="cuda")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_per * world * e2e_steps / float(dt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": n_per * 40 * world, "d2h_bytes_per_step": n_e * 24 * world,
+        e2e = {"value": uid_count * e2e_steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": uid_count * 40, "d2h_bytes_per_step": n_e * 24 * world,
                "steps": e2e_steps, "timing": "wall clock between barriers, max over ranks",
                "path": "per rank: abs_gpu_upload (pinned) -> decomposed iteration -> abs_gpu_download (pinned)"}
     if rank == 0:
         hbm, peak_src = _peaks()
-        step_bytes = 128 * n_per * args.steps
+        bpa = 134 if args.config == "c3" else 128
+        step_bytes = bpa * (total / world) * args.steps
         # rank 0's k_force (owned agents + ghosts stepped as candidates only):
         # 56 B per owned agent per launch over its CUDA-event average
         avg_force_ms = force_ms / max(1, force_launches)
@@ -323,13 +346,13 @@ def run_decomposed(args, dist, world, rank, local):
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c4_large_uniform (weak scaling)", "agents_per_gpu": n_per,
-                       "global_agents": int(total), "cube_side": L,
-                       "parallelism": f"slab{world} (z box layers, NCCL halo + migration)",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{name} ({scaling} scaling)", "agents_per_gpu": int(n_nominal),
+                       "global_agents": int(total),
+                       "parallelism": f"slab{world} (equal-count z slabs, NCCL halo + migration, library-driven)",
                        "l2": "inputs >> 126 MB L2, no flush"},
             "roofline": roofline,
-            "step_roofline": {"bytes_per_agent_iteration": 128, "unit": "GB/s",
+            "step_roofline": {"bytes_per_agent_iteration": bpa, "unit": "GB/s",
                               "achieved_per_gpu": step_bytes / (ms_max / 1e3) / 1e9,
                               "frac": step_bytes / (ms_max / 1e3) / 1e9 / hbm},
             "clocks": clk.summary(),
@@ -348,8 +371,8 @@ def run_gpu(args):
     dist, world, rank, local = _dist() if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (None, 1, 0, 0)
     torch.cuda.set_device(local)
     if world > 1 or args.decompose:
-        if args.config != "c4":
-            raise SystemExit("multi-GPU bench runs config c4 (slab decomposition)")
+        if args.config not in ("c4", "c3"):
+            raise SystemExit("the multi-GPU bench decomposes configs c4 (weak or strong) and c3 (strong)")
         if dist is None:
             import torch.distributed as dist0
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -550,6 +573,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=0,
                     help="--impl reference: time a bounded sample of this many agents instead of the full population")
     ap.add_argument("--decompose", action="store_true", help="use the slab decomposition even at N=1")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="c4 under torchrun: 2^26 agents per GPU (weak) or in total (strong)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force"],
                     help="EnvironmentKind (params.hpp:9); brute_force = the O(N^2) comparison baseline")

@@ -3129,7 +3129,7 @@ int map_dev_err(abs_gpu_ctx* c, const DevGrid& h) {
                                                ": fixed box length is smaller than the largest agent diameter");
     case kErrSlabs:
       return set_err(c, ABS_ERR_STATE, "slab decomposition at iteration " + std::to_string(h.failed_iteration) +
-                                           ": fewer than 3 z box layers per rank");
+                                           ": fewer than 2 z box layers per rank");
     case kErrQueryRadius:
       return set_err(c, ABS_ERR_INVALID_ARGUMENT, "operation 'behaviours' failed at iteration " +
                                                       std::to_string(h.failed_iteration) +

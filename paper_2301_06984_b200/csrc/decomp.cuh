@@ -15,7 +15,7 @@
 //      to the neighbouring slab as owned records, the two boundary layers as
 //      ghost records; an emigrant that lands in the layer next to this slab
 //      stays here as a ghost (its new owner's boundary layer), the others
-//      leave. Slabs >= 3 layers and steps <= max_displacement (<= one box)
+//      leave. Slabs >= 2 layers and steps <= max_displacement (<= one box)
 //      guarantee no agent crosses a whole slab (checked on the device);
 //   4. the records are imported (owned or ghost), the iteration runs with
 //      ghosts as candidates only (ABS_FLAG_GHOST), additions are committed
@@ -35,7 +35,7 @@
 namespace {
 
 constexpr int kHistBins = 4096;   // layer histogram bins (layers are coarsened beyond)
-constexpr int kMinLayers = 3;     // slab thickness floor (no agent crosses a slab per step)
+constexpr int kMinLayers = 2;     // slab thickness floor (the device checks that no agent crosses a slab)
 
 struct NcclApi {
   void* h = nullptr;
@@ -147,19 +147,31 @@ __device__ __forceinline__ unsigned int layer_coarsening(unsigned int D) {
   return (D + kHistBins - 1) / kHistBins;
 }
 
-// Owned agents per (coarsened) z-layer of the override grid.
-__global__ void k_layer_hist(const Pd* __restrict__ pos, const unsigned char* __restrict__ flags,
-                             const DevGrid* g, unsigned long long n, unsigned long long* __restrict__ hist) {
-  if (g->err) return;
+// Owned agents per (coarsened) z-layer of the override grid. Storage is
+// cell-ordered, so neighbouring agents share a layer: counts gather in a
+// shared-memory histogram per block (warp-aggregated increments), and only
+// the non-zero bins reach global memory.
+__global__ void __launch_bounds__(kThreads) k_layer_hist(const Pd* __restrict__ pos,
+                                                         const unsigned char* __restrict__ flags, const DevGrid* g,
+                                                         unsigned long long n, unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int sh[kHistBins];
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) sh[b] = 0u;
+  __syncthreads();
+  const bool ok = !g->err;
   const unsigned int D = g->ov_dims[2];
   const unsigned int cz = layer_coarsening(D);
   const double oz = g->ov_grid[2], box = g->ov_grid[3];
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (flags[i] & ABS_FLAG_GHOST) continue;
-    const unsigned int layer = box_coord(pos[i].z, oz, box, D);
-    atomicAdd(hist + layer / cz, 1ull);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long b0 = blockIdx.x * (unsigned long long)blockDim.x; ok && b0 < n; b0 += stride) {
+    const unsigned long long i = b0 + threadIdx.x;  // warp-uniform trip count
+    int bin = -1;
+    if (i < n && !(flags[i] & ABS_FLAG_GHOST)) bin = static_cast<int>(box_coord(pos[i].z, oz, box, D) / cz);
+    const unsigned int peers = __match_any_sync(0xffffffffu, bin);
+    if (bin >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bin], __popc(peers));
   }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
+    if (sh[b]) atomicAdd(hist + b, static_cast<unsigned long long>(sh[b]));
 }
 
 // Slab edges L[0..W] (layer indices): equal shares of the agents, snapped to

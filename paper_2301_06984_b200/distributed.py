@@ -112,7 +112,7 @@ def layer_bounds(dims_z: int, world: int) -> np.ndarray:
     return np.array([(r * dims_z) // world for r in range(world + 1)], np.int64)
 
 
-HIST_BINS, MIN_LAYERS = 4096, 3  # decomp.cuh kHistBins / kMinLayers
+HIST_BINS, MIN_LAYERS = 4096, 2  # decomp.cuh kHistBins / kMinLayers
 
 
 def balanced_bounds(layer_counts: np.ndarray, world: int, min_layers: int = MIN_LAYERS) -> np.ndarray:
@@ -122,7 +122,7 @@ def balanced_bounds(layer_counts: np.ndarray, world: int, min_layers: int = MIN_
     slab >= min_layers layers (the analogue of sort_balance.cpp:61-77)."""
     D = len(layer_counts)
     if D < world * min_layers:
-        raise RuntimeError("fewer than 3 z box layers per rank")
+        raise RuntimeError("fewer than 2 z box layers per rank")
     cz = (D + HIST_BINS - 1) // HIST_BINS
     nb = (D + cz - 1) // cz
     hist = np.zeros(nb, np.int64)
