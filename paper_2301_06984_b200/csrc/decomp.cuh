@@ -208,7 +208,8 @@ __global__ void k_layer_bounds(DevGrid* g, const unsigned long long* __restrict_
 
 // One export pass (see the file header). Records carry the owned / ghost
 // role in pad0. counts: [0] records to lo, [1] records to hi, [2] agents
-// leaving this context, [3] agents that skipped a slab (error).
+// leaving this context, [3] agents that skipped a slab (error), [4] agents
+// turned into local ghosts (k_import_slab adds the imported ghosts in [5]).
 __global__ void k_export_slab(Pd* pos, Soa S, unsigned long long cap, unsigned long long n, const DevGrid* g,
                               const long long* __restrict__ lb, int rank, int world, int periodic,
                               Rec* __restrict__ out_lo, Rec* __restrict__ out_hi, unsigned long long out_cap,
@@ -270,6 +271,7 @@ __global__ void k_export_slab(Pd* pos, Soa S, unsigned long long cap, unsigned l
     emit(dest, i, p, fl, true);
     if (adjacent) {
       S.flags[i] = fl | ABS_FLAG_GHOST;  // its new owner's boundary layer: a candidate here
+      atomicAdd(counts + 4, 1ull);
     } else {
       keep[i] = 0u;
       atomicAdd(counts + 2, 1ull);
@@ -279,7 +281,8 @@ __global__ void k_export_slab(Pd* pos, Soa S, unsigned long long cap, unsigned l
 
 // Append records at `base`: owned ones as agents of this context, the rest as ghosts.
 __global__ void k_import_slab(const Rec* __restrict__ in, unsigned long long count, unsigned long long base,
-                              Pd* __restrict__ pos, Soa S, unsigned long long cap) {
+                              Pd* __restrict__ pos, Soa S, unsigned long long cap,
+                              unsigned long long* __restrict__ ghosts) {
   for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < count;
        k += (unsigned long long)gridDim.x * blockDim.x) {
     const Rec r = in[k];
@@ -291,6 +294,7 @@ __global__ void k_import_slab(const Rec* __restrict__ in, unsigned long long cou
     S.partners[j] = r.partners;
     S.flags[j] = r.pad0 ? static_cast<unsigned char>(r.flags & ~ABS_FLAG_GHOST)
                         : static_cast<unsigned char>(r.flags | ABS_FLAG_GHOST);
+    if (!r.pad0) atomicAdd(ghosts, 1ull);
     S.beh[j] = r.beh;
     S.tag[j] = r.tag;
     S.rngc[j] = r.rngc;
@@ -388,11 +392,11 @@ int decomp_setup(abs_gpu_ctx* c, int rank, int world) {
   CK(dalloc(&d->b7, 7));
   CK(dalloc(&d->hist, kHistBins));
   CK(dalloc(&d->lb, world + 1));
-  CK(dalloc(&d->xc, 4));
+  CK(dalloc(&d->xc, 6));
   CK(dalloc(&d->rcnt, 2));
   CK(dalloc(&d->owned, 1));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hlb), (world + 1) * sizeof(long long), cudaHostAllocDefault));
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hxc), 4 * sizeof(unsigned long long), cudaHostAllocDefault));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hxc), 6 * sizeof(unsigned long long), cudaHostAllocDefault));
   if (adds_agents(c->cfg)) {
     int rc = abs_gpu_set_defer_commit(c, 1);
     if (rc) return rc;
@@ -457,9 +461,8 @@ int decomp_step(abs_gpu_ctx* c) {
   const int W = d->world;
   void* stream = c->stream;
   DevGrid h{};
-  int rc = read_grid(c, &h);
-  if (rc) return rc;
-  unsigned long long n = h.n;
+  int rc = ABS_OK;
+  unsigned long long n = c->n;  // host mirror, current after every call that changes it
   if (!d->periodic) {  // 1. global grid (config 5 keeps its fixed periodic grid)
     k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
     k_bounds_out<<<1, 1, 0, c->stream>>>(c->g, d->b7);
@@ -469,6 +472,12 @@ int decomp_step(abs_gpu_ctx* c) {
     ++c->launches;
     c->ov_on = true;
   }
+  if (W == 1) {  // one slab: no neighbours, nothing to export or import
+    rc = abs_gpu_simulate(c, 1);
+    if (rc) return rc;
+    if (c->defer_commit && adds_agents(c->cfg)) return abs_gpu_commit(c, nullptr, 0);
+    return ABS_OK;
+  }
   // 2. equal-count slab edges
   CK(cudaMemsetAsync(d->hist, 0, kHistBins * sizeof(unsigned long long), c->stream));
   if (n) k_layer_hist<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur].flags, c->g, n, d->hist);
@@ -477,14 +486,14 @@ int decomp_step(abs_gpu_ctx* c) {
   k_layer_bounds<<<1, 1, 0, c->stream>>>(c->g, d->hist, W, d->lb, d->periodic ? 1 : 0, c->iteration);
   c->launches += 2;
   // 3. one export pass
-  CK(cudaMemsetAsync(d->xc, 0, 4 * sizeof(unsigned long long), c->stream));
+  CK(cudaMemsetAsync(d->xc, 0, 6 * sizeof(unsigned long long), c->stream));
   if (n) {
     k_export_slab<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(cur_pos(c), c->S[c->cur], c->cap, n, c->g, d->lb,
                                                                  d->rank, W, d->periodic ? 1 : 0, d->send[0],
                                                                  d->send[1], d->rec_cap, d->xc, c->rank);
     ++c->launches;
   }
-  CK(cudaMemcpyAsync(d->hxc, d->xc, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(d->hxc, d->xc, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(d->hlb, d->lb, (W + 1) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   rc = read_grid(c, &h);  // synchronises the stream
   if (rc) return rc;
@@ -527,9 +536,10 @@ int decomp_step(abs_gpu_ctx* c) {
     rc = ensure_capacity(c, std::max<unsigned long long>(c->cap, 2 * (n + arrive) + 1024), n);
     if (rc) return rc;
     if (got_lo) k_import_slab<<<grid_blocks(c, got_lo), kThreads, 0, c->stream>>>(d->recv[0], got_lo, n, cur_pos(c),
-                                                                                  c->S[c->cur], c->cap);
+                                                                                  c->S[c->cur], c->cap, d->xc + 5);
     if (got_hi) k_import_slab<<<grid_blocks(c, got_hi), kThreads, 0, c->stream>>>(d->recv[1], got_hi, n + got_lo,
-                                                                                  cur_pos(c), c->S[c->cur], c->cap);
+                                                                                  cur_pos(c), c->S[c->cur], c->cap,
+                                                                                  d->xc + 5);
     c->launches += 2;
     const unsigned long long nn = n + arrive;
     k_set_u64<<<1, 1, 0, c->stream>>>(&c->g->n, nn);
@@ -540,9 +550,12 @@ int decomp_step(abs_gpu_ctx* c) {
     if (c->grid_valid) dzero(c, c->start, (c->bins_cap + 1) * 4);
     c->grid_valid = false;
   }
-  c->ghosts = n;  // upper bound: drop_ghosts compacts them away after the step
+  c->ghosts = n;  // upper bound (abs_gpu_drop_ghosts' no-op test); refined below
   rc = abs_gpu_simulate(c, 1);
   if (rc) return rc;
+  CK(cudaMemcpyAsync(d->hxc + 5, d->xc + 5, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->ghosts = d->hxc[4] + d->hxc[5];  // local ghost conversions + imported ghosts
   if (c->defer_commit && adds_agents(c->cfg)) {  // daughters: uids ranked over all ranks
     unsigned long long len = 0;
     DevGrid hh{};
@@ -650,6 +663,10 @@ int abs_gpu_decomp_info(abs_gpu_ctx* c, int64_t* layer_bounds, uint64_t* owned) 
   DevGrid h{};
   int rc = read_grid(c, &h);
   if (rc) return rc;
+  if (d->world == 1) {  // one slab: every layer
+    d->hlb[0] = 0;
+    d->hlb[1] = h.ov_on ? h.ov_dims[2] : h.dims[2];
+  }
   if (layer_bounds)
     for (int r = 0; r <= d->world; ++r) layer_bounds[r] = d->hlb[r];
   if (owned) {
