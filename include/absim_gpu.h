@@ -65,6 +65,7 @@ extern "C" {
 #define ABS_FLAG_NEIGHBOR_VIOLATION 16u
 #define ABS_FLAG_NEW_NEIGHBOR 32u
 #define ABS_FLAG_GHOST 128u /* multi-domain halo copy: a candidate, never stepped */
+#define ABS_FLAG_REMOVED 64u /* internal: removal staged this iteration (never seen after the commit) */
 
 /* device behaviour models (BASELINE configs; models.hpp:69-83 for GROW) */
 #define ABS_MODEL_NONE 0
@@ -75,6 +76,10 @@ extern "C" {
 #define ABS_MODEL_GROW_DIVIDE 5   /* the reference's models::GrowDivide (models.hpp:15-37): mp[0] growth rate,
                                      mp[1] division threshold, mp[2] initial diameter; daughters from the
                                      agent's own RandomStream (tag copied, counter advanced by 2) */
+#define ABS_MODEL_GROW_DIVIDE_DIE 7 /* models::GrowDivide (mp[0..2] as above) whose agents also remove themselves
+                                     (AgentContext::remove_self, simulation.cpp:64-66) with probability mp[3]
+                                     per iteration: u01(rng_word(seed, uid, ABS_RNG_DEATH(it))) < mp[3]; the
+                                     commit applies removals (remove_agents_parallel) before additions */
 #define ABS_MODEL_COHERE 6        /* the reference's models::Cohere (models.hpp:42-64): mp[0] attraction
                                      radius (<= box length, e.g. fixed_box_length), mp[1] speed; same-tag
                                      neighbours only */

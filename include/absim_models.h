@@ -100,6 +100,8 @@ ABS_HD void abs_unit_vector(uint64_t seed, uint64_t stream, uint64_t base,
  *   grow(diameter_of_volume(V) - diameter)   [deferred, agent.hpp:40]
  */
 #define ABS_RNG_DIVISION_BASE(it) ((uint64_t)(it) << 8)
+/* ABS_MODEL_GROW_DIVIDE_DIE: the per-iteration removal draw (AgentContext::remove_self) */
+#define ABS_RNG_DEATH(it) (((uint64_t)(it) << 8) | 0xfdull)
 
 /* ---- config 3: outward drive of the outer shells (BASELINE configs[2]) --
  * delta = unit(p - centre) * (speed_max * u), u = abs_u01(rng_word(seed,

@@ -92,6 +92,9 @@ typedef struct {
   double *s_x, *s_y, *s_z, *s_d, *s_vol;
   uint8_t* s_beh;
   uint32_t* s_tag;
+  /* staged removals (AgentContext::remove_self, simulation.cpp:64-66): slots in loop order */
+  uint32_t* rem;
+  uint64_t nrem, rem_cap;
 } orc_sim;
 
 static void* xrealloc(void* p, size_t n) {
@@ -180,7 +183,7 @@ void orc_destroy(orc_sim* s) {
   free(s->partners); free(s->flags); free(s->beh); free(s->vol); free(s->succ);
   free(s->tag); free(s->rngc);
   free(s->head); free(s->count); free(s->s_uid); free(s->s_x); free(s->s_y);
-  free(s->s_z); free(s->s_d); free(s->s_vol); free(s->s_beh); free(s->s_tag);
+  free(s->s_z); free(s->s_d); free(s->s_vol); free(s->s_beh); free(s->s_tag); free(s->rem);
   free(s);
 }
 
@@ -586,7 +589,15 @@ static int run_behaviour(orc_sim* s, uint64_t i) {
       const double rem = cap - s->d[i];
       s->tg[i] += rem < p->mp[0] ? rem : p->mp[0];
     }
-  } else if (p->model == 5) { /* models::GrowDivide (models.hpp:15-37): mp rate, threshold, initial d */
+  } else if (p->model == 7 &&
+             abs_u01(abs_rng_word(p->seed, s->uid[i], ABS_RNG_DEATH(s->iteration))) < p->mp[3]) {
+    /* GrowDivide + remove_self (absim_gpu.h ABS_MODEL_GROW_DIVIDE_DIE): staged in loop order */
+    if (s->nrem == s->rem_cap) {
+      s->rem_cap = s->rem_cap ? 2 * s->rem_cap : 64;
+      s->rem = xrealloc(s->rem, s->rem_cap * sizeof *s->rem);
+    }
+    s->rem[s->nrem++] = (uint32_t)i;
+  } else if (p->model == 5 || p->model == 7) { /* models::GrowDivide (models.hpp:15-37): mp rate, threshold, initial d */
     if (s->d[i] >= p->mp[1]) {
       double dir[3];
       orc_unit_vector(p->seed, s->uid[i], &s->rngc[i], dir); /* ctx.random(), random.hpp:47-52 */
@@ -694,10 +705,18 @@ int orc_remove(orc_sim* s, const uint32_t* removed, uint32_t r) {
   return 0;
 }
 
-/* commit.cpp:186-222 with one staging slot */
+/* commit.cpp:164-225 with one staging slot: removals first (remove_agents_parallel
+ * over the slots in staging order), then the additions appended in creation order */
 static int run_commit(orc_sim* s) {
+  if (s->nrem == 0 && s->nstage == 0) return 0;
+  /* simulation.cpp:502-508: new-agent marking sees the pre-commit storage */
+  if (s->nstage && s->p.detect_static && mark_new_agent_neighbors(s)) return -1;
+  if (s->nrem) {
+    const uint64_t r = s->nrem;
+    s->nrem = 0;
+    if (orc_remove(s, s->rem, (uint32_t)r)) return -1;
+  }
   if (s->nstage == 0) return 0;
-  if (s->p.detect_static && mark_new_agent_neighbors(s)) return -1;
   reserve(s, s->n + s->nstage);
   for (uint64_t k = 0; k < s->nstage; ++k) {
     init_slot(s, s->n + k, s->s_uid[k], s->s_x[k], s->s_y[k], s->s_z[k], s->s_d[k],

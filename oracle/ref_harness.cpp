@@ -88,6 +88,26 @@ class Drive final : public BehaviorBase<Drive> {
   double vmax_;
 };
 
+// ABS_MODEL_GROW_DIVIDE_DIE (absim_gpu.h): the reference's own
+// models::GrowDivide, preceded by a removal draw that calls
+// AgentContext::remove_self (simulation.cpp:64-66).
+class GrowDivideDie final : public BehaviorBase<GrowDivideDie> {
+ public:
+  GrowDivideDie(double rate, double threshold, double initial, double p_remove)
+      : inner_(rate, threshold, initial), p_remove_(p_remove) {}
+  void run(Agent& a, AgentContext& ctx) override {
+    if (abs_u01(abs_rng_word(ctx.params().seed, a.uid(), ABS_RNG_DEATH(ctx.iteration()))) < p_remove_) {
+      ctx.remove_self();
+      return;
+    }
+    inner_.run(a, ctx);
+  }
+
+ private:
+  models::GrowDivide inner_;
+  double p_remove_;
+};
+
 struct Ref {
   std::unique_ptr<Simulation> sim;
   RefParams p;
@@ -164,6 +184,9 @@ void* ref_create(const RefParams* rp, std::uint64_t n, const double* x, const do
         a.add_behavior(rm.clone_behavior(proto, dom));
       } else if (rp->model == 6) {
         models::Cohere proto(rp->mp[0], rp->mp[1]);
+        a.add_behavior(rm.clone_behavior(proto, dom));
+      } else if (rp->model == 7) {
+        GrowDivideDie proto(rp->mp[0], rp->mp[1], rp->mp[2], rp->mp[3]);
         a.add_behavior(rm.clone_behavior(proto, dom));
       }
     }

@@ -24,6 +24,7 @@ ABS_ERR_STATE = 8
 
 MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3, 4
 MODEL_GROW_DIVIDE, MODEL_COHERE = 5, 6  # the reference's own models::GrowDivide / models::Cohere
+MODEL_GROW_DIVIDE_DIE = 7  # models::GrowDivide + AgentContext::remove_self with probability mp[3]
 FLAG_GHOST = 128
 ENV_UNIFORM_GRID, ENV_BRUTE_FORCE = 0, 1  # EnvironmentKind (params.hpp:9)
 

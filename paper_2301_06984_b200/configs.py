@@ -168,6 +168,19 @@ def ref_proliferation(n: int = 4096) -> Workload:
                     rng_counters=np.zeros(m, np.uint64))
 
 
+def ref_proliferation_die(n: int = 4096, p_remove: float = 0.02, sorting_frequency: int = 0) -> Workload:
+    """ref_proliferation with every cell also removing itself with probability
+    p_remove per iteration (ABS_MODEL_GROW_DIVIDE_DIE: models::GrowDivide +
+    AgentContext::remove_self): additions and removals in the same commits,
+    optionally with the Morton re-sort, so daughter uids and removal slots
+    follow the reference's reordered storage."""
+    wl = ref_proliferation(n)
+    wl.name = "ref_proliferation_die"
+    wl.params = dict(seed=42, model=N.MODEL_GROW_DIVIDE_DIE, model_params=[2.0, 14.0, 10.0, p_remove],
+                     sorting_frequency=sorting_frequency)
+    return wl
+
+
 def ref_clustering(n: int = 10_000, seed: int = 42) -> Workload:
     """The reference's own build_clustering (models.cpp:40-61): n cells of
     two interleaved types (tag = uid % 2) uniformly in a cube of side

@@ -551,6 +551,7 @@ struct Soa {
   double* force;  // [3][cap]
   unsigned int* tag;          // Agent::tag (agent.hpp:35-36)
   unsigned long long* rngc;   // Agent::rng_counter (agent.hpp:145)
+  unsigned int* skey;         // the agent's slot in the REFERENCE's storage order
 };
 
 // Counting-sort scatter: agent i moves to slot start[key[i]] + rank[i] of
@@ -622,6 +623,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
         dst.tag[jj] = src.tag[i];
         dst.rngc[jj] = src.rngc[i];
       }
+      dst.skey[jj] = src.skey[i];
     }
   }
 }
@@ -720,6 +722,7 @@ constexpr unsigned char kFlagGhost = 128u;  // ABS_FLAG_GHOST
 // Outputs of one agent's step that need warp-level cooperation afterwards.
 struct Daughter {
   bool divides;
+  bool dies;  // AgentContext::remove_self staged (ABS_MODEL_GROW_DIVIDE_DIE)
   unsigned long long parent;
   double x, y, z, d, vol;
   unsigned int tag;
@@ -765,10 +768,10 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
                                                unsigned long long& n_eval, unsigned long long& n_skip,
                                                Walk&& walk, Fetch&& fetch, UidOf&& uid_of, float slack = 0.0f,
                                                const Query& query = Query{}) {
-  Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
+  Daughter dg{false, false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
   unsigned char fl = S.flags[i];
   const unsigned long long my_uid = S.uid[i];
-  dg.parent = my_uid;
+  dg.parent = S.skey[i];  // daughters are numbered in the reference's storage order
   if (fl & kFlagGhost) {  // halo copy of another rank's agent: candidate only
     {
       if (STATIC) {
@@ -827,7 +830,11 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         const double rem = a.mp[1] - me.d;
         tg += rem < a.mp[0] ? rem : a.mp[0];
       }
-    } else if (MODEL == ABS_MODEL_GROW_DIVIDE) {  // models::GrowDivide (models.hpp:15-37)
+    } else if ((MODEL == ABS_MODEL_GROW_DIVIDE_DIE) &&
+               abs_u01(abs_rng_word(a.seed, my_uid, ABS_RNG_DEATH(a.iteration))) < a.mp[3]) {
+      dg.dies = true;  // ctx.remove_self(): committed after the iteration (simulation.cpp:64-66)
+    } else if (MODEL == ABS_MODEL_GROW_DIVIDE || MODEL == ABS_MODEL_GROW_DIVIDE_DIE) {
+      // models::GrowDivide (models.hpp:15-37)
       if (me.d >= a.mp[1]) {
         unsigned long long ctr = S.rngc[i];
         double dir[3];
@@ -1011,7 +1018,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     }
     reinterpret_cast<double2*>(out + i)[0] = make_double2(np.x, np.y);
     reinterpret_cast<double2*>(out + i)[1] = make_double2(np.z, np.d);
-    S.flags[i] = fl;
+    S.flags[i] = dg.dies ? static_cast<unsigned char>(fl | ABS_FLAG_REMOVED) : fl;
   }
   return dg;
 }
@@ -1116,7 +1123,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
             unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag,
-            const unsigned int* __restrict__ work) {
+            const unsigned int* __restrict__ work, unsigned int* __restrict__ rmark) {
   if (gp->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
@@ -1155,7 +1162,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
     if (base >= n) break;
     const bool live = base + lane < n;
     const unsigned long long i = work ? (live ? work[base + lane] : 0ull) : base + lane;
-    Daughter dg{false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
+    Daughter dg{false, false, 0, 0, 0, 0, 0, 0, 0u, 0.0f};
     if (live) {
       const Pd me = load_pd(S.pd + i);
       const unsigned int self = static_cast<unsigned int>(i);
@@ -1184,8 +1191,13 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, 0.0f,
           query);
     }
-    if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE)
+    if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE || MODEL == ABS_MODEL_GROW_DIVIDE_DIE)
       stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
+    if (MODEL == ABS_MODEL_GROW_DIVIDE_DIE) {  // removal staging: one atomic per warp
+      if (dg.dies) rmark[S.skey[i]] = 1u;
+      const unsigned int dead = __ballot_sync(0xffffffffu, dg.dies);
+      if (lane == 0 && dead) atomicAdd(&gw->removed_now, (unsigned long long)__popc(dead));
+    }
     moved = fmaxf(moved, dg.moved);
   }
   if (a.track_disp) {  // the step's largest displacement (neighbour-list policy)
@@ -1705,7 +1717,7 @@ __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
                          const unsigned int* __restrict__ div_rank, const unsigned int* __restrict__ div_rank_g,
                          unsigned long long cap, int record_forces) {
   if (g->err) return;
-  const unsigned long long staged = g->staged, n = g->n, uc = g->uid_count;
+  const unsigned long long staged = g->staged, n = g->n, uc = g->uid_count, nk = g->nkeys;
   for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < staged;
        k += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long parent = st_parent[k];
@@ -1715,6 +1727,7 @@ __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
     reinterpret_cast<double2*>(live + j)[0] = make_double2(p.x, p.y);
     reinterpret_cast<double2*>(live + j)[1] = make_double2(p.z, p.d);
     S.uid[j] = uc + rk;
+    S.skey[j] = static_cast<unsigned int>(nk + rk);  // appended after the reference's survivors, creation order
     S.flags[j] = ABS_FLAG_NEWLY_ADDED;
     S.partners[j] = 0;
     S.beh[j] = 1;
@@ -1731,6 +1744,7 @@ __global__ void k_commit_fin(DevGrid* g, const unsigned int* __restrict__ grank)
   if (threadIdx.x || blockIdx.x || g->err) return;
   const unsigned long long s = g->staged;
   g->n += s;
+  g->nkeys += grank[g->uid_count];
   g->uid_count += grank[g->uid_count];
   g->added += s;
   g->staged = 0;
@@ -1776,6 +1790,7 @@ __global__ void __launch_bounds__(kThreads) k_ingest(const double* __restrict__ 
     else if (uid_limit && S.uid[i] >= uid_limit) bad |= 2u;
     S.tag[i] = 0;   // set with abs_gpu_set_agent_ext
     S.rngc[i] = 0;
+    S.skey[i] = static_cast<unsigned int>(i);  // storage order of the reference = upload order
     if (set_vol) S.vol[i] = abs_volume_of_diameter(di);
     if (sir) {  // absim_models.h: 1 % initially infected, from the seed (or given states)
       const unsigned long long u = set_uid ? i : S.uid[i];
@@ -1854,6 +1869,7 @@ __global__ void k_grid_reset(DevGrid* g, unsigned long long n, unsigned long lon
     g->dims[0] = g->dims[1] = g->dims[2] = 1;
     g->B[0] = g->B[1] = g->B[2] = 1;
     g->n = n;
+    g->nkeys = n;
     g->uid_count = uid_count;
   }
 }
@@ -1944,7 +1960,7 @@ __global__ void k_export(const Pd* __restrict__ pos, Soa S, unsigned long long c
     r.pad0 = r.pad1 = 0;
     r.rngc = S.rngc[i];
     r.tag = S.tag[i];
-    r.pad3 = 0;
+    r.pad3 = S.skey[i];
     (dest ? out_hi : out_lo)[slot] = r;
   }
 }
@@ -1964,6 +1980,7 @@ __global__ void k_import(const Rec* __restrict__ in, unsigned long long count, u
     S.beh[j] = r.beh;
     S.tag[j] = r.tag;
     S.rngc[j] = r.rngc;
+    S.skey[j] = r.pad3;
   }
 }
 
@@ -2209,6 +2226,7 @@ __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const uns
       dst.force[cap + j] = src.force[cap + i];
       dst.force[2 * cap + j] = src.force[2 * cap + i];
     }
+    dst.skey[j] = static_cast<unsigned int>(j);  // sort_and_balance's new storage slot
     if (carry_ext) {
       dst.tag[j] = src.tag[i];
       dst.rngc[j] = src.rngc[i];
@@ -2242,19 +2260,6 @@ __global__ void k_find_slots(const unsigned long long* __restrict__ uid, const D
   if (hits) atomicAdd(found, hits);
 }
 
-// ------------------------------------------------------------ removal
-// remove_agents_parallel (commit.cpp:14-106): holes left of the split are
-// filled, in removal-list order, by surviving tail agents in index order.
-__global__ void k_remove_plan(const unsigned long long* __restrict__ slots, unsigned long long r,
-                              unsigned long long new_size, unsigned int* __restrict__ to_right,
-                              unsigned int* __restrict__ tail_alive) {
-  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
-       k += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long idx = slots[k];
-    if (idx < new_size) to_right[k] = 1;
-    else tail_alive[idx - new_size] = 0;
-  }
-}
 
 // O(removed) compaction: storage order is free (the next
 // re-bin re-sorts by cell), so the survivors beyond the new end move into
@@ -2286,43 +2291,125 @@ __global__ void k_swap_move(Pd* pos, Soa S, const unsigned int* __restrict__ kee
     S.force[2 * cap + dst] = S.force[2 * cap + i];
     S.tag[dst] = S.tag[i];
     S.rngc[dst] = S.rngc[i];
+    S.skey[dst] = S.skey[i];
   }
 }
 
-__global__ void k_remove_move(const Pd* pos_in, Pd* pos, Soa S, const unsigned long long* __restrict__ slots,
-                              unsigned long long r, unsigned long long new_size,
-                              const unsigned int* __restrict__ hole_rank, const unsigned int* __restrict__ to_right,
-                              const unsigned int* __restrict__ mover_rank, const unsigned int* __restrict__ tail_alive,
-                              unsigned int* __restrict__ hole_at, unsigned long long cap, int phase) {
-  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
-       k += (unsigned long long)gridDim.x * blockDim.x) {
-    if (phase == 0) {
-      if (to_right[k]) hole_at[hole_rank[k]] = static_cast<unsigned int>(slots[k]);
-    } else if (tail_alive[k]) {
-      const unsigned long long src = new_size + k;
-      const unsigned long long dst = hole_at[mover_rank[k]];
-      const Pd p = pos_in[src];
-      pos[dst] = p;
-      S.uid[dst] = S.uid[src];
-      S.flags[dst] = S.flags[src];
-      S.partners[dst] = S.partners[src];
-      S.beh[dst] = S.beh[src];
-      S.vol[dst] = S.vol[src];
-      S.force[dst] = S.force[src];
-      S.force[cap + dst] = S.force[cap + src];
-      S.force[2 * cap + dst] = S.force[2 * cap + src];
-      S.tag[dst] = S.tag[src];
-      S.rngc[dst] = S.rngc[src];
+
+
+// ------------------------------------------------------------ removal by storage key
+// remove_agents_parallel (commit.cpp:14-106) applied to the reference's
+// storage order, which the device carries as per-agent keys (Soa::skey): with
+// new_size = nkeys - r, the k-th hole (a removed key < new_size, in
+// removal-list order — for removals staged by the agent loop of one worker
+// that is key order) receives the k-th surviving key >= new_size in
+// ascending order; every other survivor keeps its key. The device's own
+// storage order is free (the next re-bin re-sorts by cell), so the removed
+// agents are then compacted out with O(removed) moves.
+//
+// rscan: the removal marks over keys [0, nkeys), exclusive-scanned in place
+// (rscan[nkeys] = r); a mark is rscan[k+1] - rscan[k].
+__global__ void k_rem_holes(const unsigned int* __restrict__ rscan, const DevGrid* g,
+                            unsigned int* __restrict__ hole_at) {
+  if (g->err) return;
+  const unsigned long long nk = g->nkeys;
+  const unsigned long long new_size = nk - rscan[nk];
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < new_size;
+       k += (unsigned long long)gridDim.x * blockDim.x)
+    if (rscan[k + 1] > rscan[k]) hole_at[rscan[k]] = static_cast<unsigned int>(k);
+}
+
+// New keys of the survivors; keep / idx = 1 for survivors (idx is scanned next).
+__global__ void k_rem_rekey(Soa S, const DevGrid* g, const unsigned int* __restrict__ rscan,
+                            const unsigned int* __restrict__ hole_at, unsigned int* __restrict__ keep,
+                            unsigned int* __restrict__ idx) {
+  if (g->err) return;
+  const unsigned long long n = g->n, nk = g->nkeys;
+  const unsigned long long new_size = nk - rscan[nk];
+  const unsigned int base = rscan[new_size];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const bool dead = S.flags[i] & ABS_FLAG_REMOVED;
+    keep[i] = idx[i] = dead ? 0u : 1u;
+    if (dead) continue;
+    const unsigned int key = S.skey[i];
+    if (key >= new_size) {  // a surviving tail agent: the mover rank picks its hole
+      const unsigned long long m = (key - new_size) - (rscan[key] - base);
+      S.skey[i] = hole_at[m];
     }
   }
 }
 
-
-__global__ void k_set_u32(unsigned int* a, unsigned long long n, unsigned int v) {
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+// Compaction with device-resident counts: idx = exclusive scan of keep over
+// [0, n), idx[n] = survivors.
+__global__ void k_hole_list_d(const unsigned int* __restrict__ keep, const unsigned int* __restrict__ idx,
+                              const DevGrid* g, unsigned int* __restrict__ holes) {
+  if (g->err) return;
+  const unsigned long long new_n = idx[g->n];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < new_n;
        i += (unsigned long long)gridDim.x * blockDim.x)
-    a[i] = v;
+    if (!keep[i]) holes[i - idx[i]] = static_cast<unsigned int>(i);
 }
+
+__global__ void k_swap_move_d(Pd* pos, Soa S, const unsigned int* __restrict__ keep,
+                              const unsigned int* __restrict__ idx, const unsigned int* __restrict__ holes,
+                              const DevGrid* g, unsigned long long cap) {
+  if (g->err) return;
+  const unsigned long long n = g->n, new_n = idx[n];
+  const unsigned int base = idx[new_n];
+  for (unsigned long long i = new_n + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    const unsigned long long dst = holes[idx[i] - base];
+    pos[dst] = load_pd(pos + i);
+    S.uid[dst] = S.uid[i];
+    S.flags[dst] = S.flags[i];
+    S.partners[dst] = S.partners[i];
+    S.beh[dst] = S.beh[i];
+    S.vol[dst] = S.vol[i];
+    S.force[dst] = S.force[i];
+    S.force[cap + dst] = S.force[cap + i];
+    S.force[2 * cap + dst] = S.force[2 * cap + i];
+    S.tag[dst] = S.tag[i];
+    S.rngc[dst] = S.rngc[i];
+    S.skey[dst] = S.skey[i];
+  }
+}
+
+__global__ void k_rem_fin(DevGrid* g, const unsigned int* __restrict__ idx, const unsigned int* __restrict__ rscan) {
+  if (threadIdx.x || blockIdx.x || g->err) return;
+  const unsigned long long n = g->n, nn = idx[n];
+  g->removed += n - nn;
+  g->nkeys -= rscan[g->nkeys];
+  g->n = nn;
+  g->removed_now = 0;
+}
+
+// abs_gpu_remove: the caller's list gives the hole order. to_right[k] = 1 for
+// list entries whose key lies below new_size; keys are marked for the
+// mover ranks and the agents flagged for the compaction.
+__global__ void k_api_mark(Soa S, const unsigned long long* __restrict__ slots, unsigned long long r,
+                           unsigned long long new_size, unsigned int* __restrict__ rmark,
+                           unsigned int* __restrict__ to_right, unsigned int* __restrict__ key_of) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
+       k += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = slots[k];
+    const unsigned int key = S.skey[i];
+    key_of[k] = key;
+    S.flags[i] |= ABS_FLAG_REMOVED;
+    rmark[key] = 1u;
+    to_right[k] = key < new_size ? 1u : 0u;
+  }
+}
+
+__global__ void k_api_holes(const unsigned int* __restrict__ to_right, const unsigned int* __restrict__ rank,
+                            const unsigned int* __restrict__ key_of, unsigned long long r,
+                            unsigned int* __restrict__ hole_at) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < r;
+       k += (unsigned long long)gridDim.x * blockDim.x)
+    if (to_right[k]) hole_at[rank[k]] = key_of[k];
+}
+
 
 }  // namespace
 
@@ -2406,6 +2493,8 @@ struct abs_gpu_ctx {
   unsigned int* st_tag = nullptr;    // staged daughters' tags
   unsigned int* div_mark = nullptr;  // uid_cap + 1: this context's dividing parents (then their local ranks)
   unsigned int* div_mark_g = nullptr;  // uid_cap + 1: all ranks' dividing parents (deferred commit only)
+  unsigned int* rmark = nullptr;     // uid_cap + 1: removal marks by reference storage key (then their scan)
+  unsigned int* hole_at = nullptr;   // uid_cap + 1: the reference's holes in removal order
   bool defer_commit = false;         // multi-domain additions: stop before the commit
   bool pending_commit = false;
   double* ingest_part = nullptr;     // mapped page-locked: per-block (sum d, max d) of the last upload
@@ -2459,11 +2548,17 @@ int set_err(abs_gpu_ctx* c, int code, const std::string& m) {
 
 // Models whose behaviour creates agents (daughter staging, uid-indexed marks).
 bool adds_agents(const abs_gpu_config& cfg) {
-  return cfg.model == ABS_MODEL_PROLIFERATION || cfg.model == ABS_MODEL_GROW_DIVIDE;
+  return cfg.model == ABS_MODEL_PROLIFERATION || cfg.model == ABS_MODEL_GROW_DIVIDE ||
+         cfg.model == ABS_MODEL_GROW_DIVIDE_DIE;
 }
+// Models whose behaviour removes agents (AgentContext::remove_self).
+bool removes_agents(const abs_gpu_config& cfg) { return cfg.model == ABS_MODEL_GROW_DIVIDE_DIE; }
+// Storage keys must follow the reference's order exactly (daughter numbering,
+// removal slots): Morton sorts then take the exact (radix) path.
+bool keys_exact(const abs_gpu_config& cfg) { return adds_agents(cfg) || removes_agents(cfg); }
 // Models that read Agent::tag / rng_counter.
 bool uses_ext(const abs_gpu_config& cfg) {
-  return cfg.model == ABS_MODEL_GROW_DIVIDE || cfg.model == ABS_MODEL_COHERE;
+  return cfg.model == ABS_MODEL_GROW_DIVIDE || cfg.model == ABS_MODEL_COHERE || cfg.model == ABS_MODEL_GROW_DIVIDE_DIE;
 }
 
 // BruteForceEnvironment (environment.hpp:53-80) instead of the grid.
@@ -2492,7 +2587,7 @@ cudaError_t dalloc(T** p, unsigned long long count) {
 
 void free_soa(Soa& s) {
   cudaFree(s.pd); cudaFree(s.uid); cudaFree(s.flags); cudaFree(s.partners);
-  cudaFree(s.vol); cudaFree(s.beh); cudaFree(s.force); cudaFree(s.tag); cudaFree(s.rngc);
+  cudaFree(s.vol); cudaFree(s.beh); cudaFree(s.force); cudaFree(s.tag); cudaFree(s.rngc); cudaFree(s.skey);
   s = Soa{};
 }
 
@@ -2507,6 +2602,7 @@ cudaError_t alloc_soa(Soa& s, unsigned long long cap) {
   if ((e = dalloc(&s.force, 3 * cap))) return e;
   if ((e = dalloc(&s.tag, cap))) return e;
   if ((e = dalloc(&s.rngc, cap))) return e;
+  if ((e = dalloc(&s.skey, cap))) return e;
   return cudaSuccess;
 }
 
@@ -2532,6 +2628,7 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
     CK(cudaMemcpyAsync(dst.beh, src.beh, keep, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(dst.tag, src.tag, keep * 4, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(dst.rngc, src.rngc, keep * 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst.skey, src.skey, keep * 4, cudaMemcpyDeviceToDevice, c->stream));
     for (int q = 0; q < 3; ++q)
       CK(cudaMemcpyAsync(dst.force + q * ncap, src.force + q * c->cap, keep * 8, cudaMemcpyDeviceToDevice,
                          c->stream));
@@ -2569,6 +2666,11 @@ int ensure_capacity(abs_gpu_ctx* c, unsigned long long want, unsigned long long 
   CK(dalloc(&c->st_vol, ncap));
   CK(dalloc(&c->st_tag, ncap));
   c->cap = ncap;
+  cudaFree(c->holes);  // the compaction scratch follows the capacity
+  c->holes = nullptr;
+  c->holes_cap = 0;
+  CK(dalloc(&c->holes, ncap));
+  c->holes_cap = ncap;
   if (c->rec_evals) {
     cudaFree(c->evc);
     c->evc = nullptr;
@@ -2590,10 +2692,17 @@ int ensure_uid_space(abs_gpu_ctx* c, unsigned long long want) {
   cudaFree(c->div_mark);
   cudaFree(c->div_mark_g);
   cudaFree(c->tiles64);
+  cudaFree(c->rmark);
+  cudaFree(c->hole_at);
   c->div_mark = nullptr;
   c->div_mark_g = nullptr;
+  c->rmark = nullptr;
+  c->hole_at = nullptr;
   CK(dalloc(&c->div_mark, ncap + 1));
   CK(cudaMemsetAsync(c->div_mark, 0, (ncap + 1) * 4, c->stream));
+  CK(dalloc(&c->rmark, ncap + 1));
+  CK(cudaMemsetAsync(c->rmark, 0, (ncap + 1) * 4, c->stream));
+  CK(dalloc(&c->hole_at, ncap + 1));
   if (c->defer_commit) {
     CK(dalloc(&c->div_mark_g, ncap + 1));
     CK(cudaMemsetAsync(c->div_mark_g, 0, (ncap + 1) * 4, c->stream));
@@ -2805,7 +2914,7 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   }
   k_force<MODEL, STATIC, RECORD, WALK><<<blocks, kForceThreads, smem, c->stream>>>(
       S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
-      c->st_tag, work);
+      c->st_tag, work, c->rmark);
   sync_check(c, "k_force");
 }
 
@@ -2840,6 +2949,7 @@ void launch_force(abs_gpu_ctx* c, int nb, Soa& S, const StepArgs& a) {
     case ABS_MODEL_GROW: launch_force_m<ABS_MODEL_GROW>(c, nb, S, a); break;
     case ABS_MODEL_GROW_DIVIDE: launch_force_m<ABS_MODEL_GROW_DIVIDE>(c, nb, S, a); break;
     case ABS_MODEL_COHERE: launch_force_m<ABS_MODEL_COHERE>(c, nb, S, a); break;
+    case ABS_MODEL_GROW_DIVIDE_DIE: launch_force_m<ABS_MODEL_GROW_DIVIDE_DIE>(c, nb, S, a); break;
     default: launch_force_m<ABS_MODEL_NONE>(c, nb, S, a); break;
   }
 }
@@ -3078,7 +3188,28 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
 // (multi-domain): div_mark_g holds every rank's dividers (the caller summed
 // the ranks' div_mark into it), giving global uid ranks, while this rank's
 // own div_mark gives the local append slots.
+// The removal half of CommitBuffer::commit (removals before additions,
+// commit.cpp:164-185) for agents the loop staged (ABS_FLAG_REMOVED + key marks).
+void launch_removals(abs_gpu_ctx* c, bool keys_in_list_order = false) {
+  const int nb = grid_blocks(c, c->cap);
+  Soa& S = c->S[c->cur];
+  unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
+  launch_scan<unsigned int>(c, c->rmark, &c->g->nkeys, c->uid_cap, tiles, &c->g->err);
+  if (!keys_in_list_order) {
+    k_rem_holes<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->rmark, c->g, c->hole_at);
+    ++c->launches;
+  }
+  k_rem_rekey<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->rmark, c->hole_at, c->key, c->rank);
+  launch_scan<unsigned int>(c, c->rank, &c->g->n, c->cap, c->ctiles, &c->g->err);
+  k_hole_list_d<<<nb, kThreads, 0, c->stream>>>(c->key, c->rank, c->g, c->holes);
+  k_swap_move_d<<<nb, kThreads, 0, c->stream>>>(cur_pos(c), S, c->key, c->rank, c->holes, c->g, c->cap);
+  k_rem_fin<<<1, 32, 0, c->stream>>>(c->g, c->rank, c->rmark);
+  k_zero_marks<<<grid_blocks(c, c->uid_cap), kThreads, 0, c->stream>>>(c->rmark, c->g);
+  c->launches += 5;
+}
+
 void launch_commit(abs_gpu_ctx* c) {
+  if (removes_agents(c->cfg)) launch_removals(c);
   const int nb = grid_blocks(c, c->cap);
   Soa& S = c->S[c->cur];
   const unsigned long long* uc = &c->g->uid_count;
@@ -3176,16 +3307,12 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "repulsion_coefficient must be >= 0");
   if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
   if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
-  if (cfg->model < 0 || cfg->model > 6) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
+  if (cfg->model < 0 || cfg->model > 7) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
   if (cfg->environment != ABS_ENV_UNIFORM_GRID && cfg->environment != ABS_ENV_BRUTE_FORCE)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown environment kind");
   // params.cpp:52-55
   if (cfg->sorting_frequency > 0 && cfg->environment != ABS_ENV_UNIFORM_GRID)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "sorting requires the uniform_grid environment");
-  if ((cfg->model == ABS_MODEL_PROLIFERATION || cfg->model == ABS_MODEL_GROW_DIVIDE) && cfg->sorting_frequency > 0)
-    return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT,
-                   "a model that adds agents cannot be combined with Morton sorting: daughter uids would follow "
-                   "the reference's reordered storage, which the device does not track");
   if (cfg->model == ABS_MODEL_SIR && cfg->environment != ABS_ENV_UNIFORM_GRID)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "the periodic SIR model runs on the uniform grid");
   if (cfg->model == ABS_MODEL_GROW_DIVIDE && !(cfg->model_params[2] > 0.0))
@@ -3256,6 +3383,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
+  cudaFree(c->rmark); cudaFree(c->hole_at);
   if (c->ingest_part) cudaFreeHost(c->ingest_part);
   if (c->hgrid) cudaFreeHost(c->hgrid);
   for (int b = 0; b < 2; ++b) {
@@ -3597,7 +3725,7 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       auto enqueue = [&]() -> int {
         phase_mark(c);  // iteration start
         if (sorts) {
-          const int rc = launch_sort(c, it, false);
+          const int rc = launch_sort(c, it, keys_exact(c->cfg));
           if (rc) return rc;
         }
         phase_mark(c);  // after sort
@@ -4290,18 +4418,8 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
   return ABS_OK;
 }
 
-// Models that add agents number daughters uid_count + the parent's rank in
-// the reference's storage order (commit.cpp:186-222, one worker: creation
-// order). The device ranks parents by uid, which is that order as long as
-// storage was never reordered by a Morton sort or a removal; after either,
-// the reference's numbering follows an order the device does not track.
-const char* kReorderWithAdditions =
-    "a model that adds agents cannot be combined with Morton sorting or removals: daughter uids would "
-    "follow the reference's reordered storage, which the device does not track";
-
 int abs_gpu_sort(abs_gpu_ctx* c) {
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
-  if (adds_agents(c->cfg)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, kReorderWithAdditions);
   cudaSetDevice(c->device);
   DevGrid h{};
   int rc = read_grid(c, &h);
@@ -4324,15 +4442,16 @@ int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
   if (!c) return ABS_ERR_INVALID_ARGUMENT;
   if (r == 0) return ABS_OK;
-  if (adds_agents(c->cfg)) return set_err(c, ABS_ERR_INVALID_ARGUMENT, kReorderWithAdditions);
+  cudaSetDevice(c->device);
   DevGrid h{};
   int rc = read_grid(c, &h);
   if (rc) return rc;
   const unsigned long long n = h.n;
   if (r > n) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "more removals than agents");
+  if (h.nkeys != n) return set_err(c, ABS_ERR_STATE, "removals need the whole population in one context");
   Soa& S = c->S[c->cur];
-  // the removal list sorted on the host (O(r log r)); duplicates are the
-  // reference's double-staging error (agent.hpp:136-141)
+  // the removal list sorted on the host (O(r log r)) for the uid lookup;
+  // duplicates are the reference's double-staging error (agent.hpp:136-141)
   std::vector<unsigned long long> perm(r);
   for (unsigned long long k = 0; k < r; ++k) perm[k] = k;
   std::sort(perm.begin(), perm.end(), [&](unsigned long long a, unsigned long long b) { return uids[a] < uids[b]; });
@@ -4340,8 +4459,15 @@ int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   for (unsigned long long k = 0; k < r; ++k) su[k] = uids[perm[k]];
   for (unsigned long long k = 1; k < r; ++k)
     if (su[k] == su[k - 1]) return set_err(c, ABS_ERR_STATE, "agent staged for removal twice");
-  unsigned long long *d_su, *d_perm, *d_found, *d_slots;
+  unsigned long long *d_su, *d_perm, *d_found, *d_slots, *len;
+  unsigned int *to_right, *key_of, *hrank, *tiles;
   CK(dalloc(&d_su, r)); CK(dalloc(&d_perm, r)); CK(dalloc(&d_found, 1)); CK(dalloc(&d_slots, r));
+  CK(dalloc(&len, 1)); CK(dalloc(&to_right, r + 1)); CK(dalloc(&key_of, r + 1)); CK(dalloc(&hrank, r + 1));
+  CK(dalloc(&tiles, r / kScanTile + 2));
+  auto release = [&] {
+    cudaFree(d_su); cudaFree(d_perm); cudaFree(d_found); cudaFree(d_slots); cudaFree(len);
+    cudaFree(to_right); cudaFree(key_of); cudaFree(hrank); cudaFree(tiles);
+  };
   CK(cudaMemcpyAsync(d_su, su.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(d_perm, perm.data(), r * 8, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemsetAsync(d_found, 0, 8, c->stream));
@@ -4350,48 +4476,29 @@ int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   unsigned long long found = 0;
   CK(cudaMemcpyAsync(&found, d_found, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(d_su); cudaFree(d_perm); cudaFree(d_found);
   if (found != r) {
-    cudaFree(d_slots);
+    release();
     return set_err(c, ABS_ERR_INVALID_ARGUMENT, "unknown uid");
   }
+  // holes in the caller's list order (the reference's removal vector), movers
+  // by key, then the same re-key + compaction as the loop-staged removals
   const unsigned long long new_size = n - r;
-  unsigned long long *dslots, *len;
-  unsigned int *to_right, *tail_alive, *hole_at, *tiles;
-  dslots = d_slots;
-  CK(dalloc(&len, 1));
-  CK(dalloc(&to_right, r + 1)); CK(dalloc(&tail_alive, r + 1)); CK(dalloc(&hole_at, r + 1));
-  CK(dalloc(&tiles, r / kScanTile + 2));
-  unsigned int* to_right_scan = nullptr;
-  unsigned int* tail_scan = nullptr;
-  CK(dalloc(&to_right_scan, r + 1)); CK(dalloc(&tail_scan, r + 1));
-  CK(cudaMemcpyAsync(len, &r, 8, cudaMemcpyHostToDevice, c->stream));
   const int nb = grid_blocks(c, r);
-  k_set_u32<<<nb, kThreads, 0, c->stream>>>(to_right, r + 1, 0u);
-  k_set_u32<<<nb, kThreads, 0, c->stream>>>(tail_alive, r + 1, 1u);
-  k_remove_plan<<<nb, kThreads, 0, c->stream>>>(dslots, r, new_size, to_right, tail_alive);
-  CK(cudaMemcpyAsync(to_right_scan, to_right, (r + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemcpyAsync(tail_scan, tail_alive, (r + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
-  launch_scan<unsigned int>(c, to_right_scan, len, r, tiles, nullptr);
-  launch_scan<unsigned int>(c, tail_scan, len, r, tiles, nullptr);
-  Pd* pos = cur_pos(c);
-  k_remove_move<<<nb, kThreads, 0, c->stream>>>(pos, pos, S, dslots, r, new_size, to_right_scan, to_right, tail_scan,
-                                                tail_alive, hole_at, c->cap, 0);
-  k_remove_move<<<nb, kThreads, 0, c->stream>>>(pos, pos, S, dslots, r, new_size, to_right_scan, to_right, tail_scan,
-                                                tail_alive, hole_at, c->cap, 1);
-  c->launches += 5;
-  h.n = new_size;
-  h.removed += r;
-  CK(cudaMemcpyAsync(&c->g->n, &h.n, 8, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(&c->g->removed, &h.removed, 8, cudaMemcpyHostToDevice, c->stream));
+  k_api_mark<<<nb, kThreads, 0, c->stream>>>(S, d_slots, r, new_size, c->rmark, to_right, key_of);
+  CK(cudaMemcpyAsync(hrank, to_right, r * 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemcpyAsync(len, &r, 8, cudaMemcpyHostToDevice, c->stream));
+  launch_scan<unsigned int>(c, hrank, len, r, tiles, nullptr);
+  k_api_holes<<<nb, kThreads, 0, c->stream>>>(to_right, hrank, key_of, r, c->hole_at);
+  c->launches += 2;
+  launch_removals(c, true);
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(dslots); cudaFree(len); cudaFree(to_right); cudaFree(tail_alive); cudaFree(hole_at);
-  cudaFree(tiles); cudaFree(to_right_scan); cudaFree(tail_scan);
+  release();
   if (c->grid_valid) {
     CK(cudaMemsetAsync(c->start, 0, (c->bins_cap + 1) * 4, c->stream));
     c->grid_valid = false;
   }
-  c->n = new_size;
+  rc = read_grid(c, &h);
+  if (rc) return rc;
   return ABS_OK;
 }
 

@@ -237,7 +237,7 @@ __global__ void k_export_slab(Pd* pos, Soa S, unsigned long long cap, unsigned l
     r.pad1 = 0;
     r.rngc = S.rngc[i];
     r.tag = S.tag[i];
-    r.pad3 = 0;
+    r.pad3 = S.skey[i];
     (dest ? out_hi : out_lo)[slot] = r;
   };
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
@@ -299,6 +299,17 @@ __global__ void k_import_slab(const Rec* __restrict__ in, unsigned long long cou
     S.tag[j] = r.tag;
     S.rngc[j] = r.rngc;
   }
+}
+
+// Multi-domain additions rank daughters by reference storage key over ALL
+// ranks; with no removals or sorts the reference's order is creation = uid
+// order, so the global keys are the uids.
+__global__ void k_keys_from_uids(Soa S, DevGrid* g) {
+  const unsigned long long n = g->n;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    S.skey[i] = static_cast<unsigned int>(S.uid[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) g->nkeys = g->uid_count;
 }
 
 __global__ void k_clear_ghosts(unsigned char* __restrict__ flags, unsigned long long n) {
@@ -397,9 +408,16 @@ int decomp_setup(abs_gpu_ctx* c, int rank, int world) {
   CK(dalloc(&d->owned, 1));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hlb), (world + 1) * sizeof(long long), cudaHostAllocDefault));
   CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hxc), 6 * sizeof(unsigned long long), cudaHostAllocDefault));
+  if (removes_agents(c->cfg))
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "models that remove agents run in one domain");
+  if (c->cfg.sorting_frequency > 0 && adds_agents(c->cfg))
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT,
+                   "multi-domain additions with Morton sorting: the reference's global storage order is not tracked");
   if (adds_agents(c->cfg)) {
     int rc = abs_gpu_set_defer_commit(c, 1);
     if (rc) return rc;
+    k_keys_from_uids<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(c->S[c->cur], c->g);
+    ++c->launches;
   }
   return decomp_records(c, 1 << 16);
 }

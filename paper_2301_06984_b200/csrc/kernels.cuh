@@ -85,6 +85,8 @@ struct DevGrid {
   unsigned long long fin_count;  // k_reduce_finalize: blocks done (last one sizes the grid)
   unsigned long long work_n;     // static detection: agents listed for the force sweep (k_static_pass)
   unsigned long long agent_its;  // sum over completed iterations of the agents at iteration start
+  unsigned long long nkeys;      // size of the reference's storage (the key space): keys are 0..nkeys-1
+  unsigned long long removed_now;  // removals staged this iteration (device-initiated)
   // --- kept across uploads (abs_gpu_upload copies everything above) ---
   int ov_on;               // multi-domain: use the global grid below
   int pad1;

@@ -325,3 +325,28 @@ def test_cohere_matches_reference_builder(oracle_mod, have_ref):
         ref.simulate(4)
         port.simulate(4)
         _same_state(ref, port, f"cohere after {4 * (chunk + 1)}")
+
+
+@pytest.mark.parametrize("model,sf", [(5, 3), (7, 0), (7, 3)])
+def test_reordered_storage_matches_reference(oracle_mod, have_ref, model, sf):
+    """Daughter uids and removal slots follow the reference's storage order
+    after Morton sorts (sorting_frequency) and removals (remove_self, commit:
+    removals before additions, commit.cpp:164-225): GrowDivide with sorts,
+    GrowDivide + removals, both together; port == unmodified reference."""
+    if not have_ref:
+        pytest.skip("reference build unavailable")
+    O = oracle_mod
+    wl = CF.ref_proliferation_die(216, p_remove=0.03, sorting_frequency=sf) if model == 7 else CF.ref_proliferation(216)
+    prm = dict(wl.params, sorting_frequency=sf)
+    p = O.OracleParams(seed=prm["seed"], model=prm["model"], mp=prm["model_params"], sorting_frequency=sf)
+    port = O.PortSim(p, wl.x, wl.y, wl.z, wl.d)
+    port.set_tags(wl.tags)
+    port.set_rng_counters(wl.rng_counters)
+    ref = O.RefSim(p, wl.x, wl.y, wl.z, wl.d)  # fresh agents: tags and stream counters 0, as the lattice's
+    assert not wl.tags.any() and not wl.rng_counters.any()
+    for chunk in range(5):
+        ref.simulate(5)
+        port.simulate(5)
+        _same_state(ref, port, f"model {model} sf {sf} after {5 * (chunk + 1)}")
+    c = ref.counts()
+    assert c["agents_added"] > 0 and (model != 7 or c["agents_removed"] > 0)

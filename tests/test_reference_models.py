@@ -130,16 +130,44 @@ print("OK")
     assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]
 
 
-def test_additions_reject_reordering(engine):
-    """Daughter uids follow the reference's storage order (commit.cpp:186-222);
-    after a Morton sort or a removal that order is not tracked on the device,
-    so those combinations are refused instead of numbering daughters wrongly."""
-    E = engine
+@pytest.mark.parametrize("model,sf", [(5, 3), (7, 0), (7, 4)])
+def test_additions_after_reordering(engine, oracle_mod, model, sf):
+    """Daughter uids follow the reference's storage order (commit.cpp:186-222)
+    after Morton sorts and removals: the device carries each agent's slot in
+    that order (Soa::skey) through every move, ranks dividing parents by it
+    and applies remove_agents_parallel (commit.cpp:14-106) to it. GrowDivide
+    with sorts, GrowDivide + remove_self, both together, against the port
+    (pinned to the reference in test_oracle.py)."""
+    O = oracle_mod
+    wl = CF.ref_proliferation_die(216, p_remove=0.03, sorting_frequency=sf) if model == 7 else CF.ref_proliferation(216)
+    wl.params = dict(wl.params, sorting_frequency=sf)
+    sim = _gpu(engine, wl)
+    orc = O.PortSim(O.OracleParams(seed=wl.params["seed"], model=wl.params["model"], mp=wl.params["model_params"],
+                                   sorting_frequency=sf), wl.x, wl.y, wl.z, wl.d)
+    for chunk in range(5):
+        sim.simulate(5)
+        orc.simulate(5)
+        _compare(sim, orc, f"model {model} sf {sf} after {5 * (chunk + 1)}")
+    r = sim.report()
+    assert r.agents_added > 0 and (model != 7 or r.agents_removed > 0)
+
+
+def test_api_removal_then_divisions(engine, oracle_mod):
+    """abs_gpu_remove in the caller's list order (the reference's removal
+    vector gives the hole order), then more GrowDivide iterations: survivors'
+    slots and the later daughters' uids match the port."""
+    O = oracle_mod
     wl = CF.ref_proliferation(216)
-    with pytest.raises(ValueError, match="Morton sorting"):
-        E.Simulation(E.SimulationParams(**{**wl.params, "sorting_frequency": 3}))
-    sim = _gpu(E, wl)
-    with pytest.raises(ValueError, match="cannot be combined"):
-        sim.sort()
-    with pytest.raises(ValueError, match="cannot be combined"):
-        sim.remove_agents([0])
+    sim = _gpu(engine, wl)
+    orc, _ = _oracle(O, wl)
+    sim.simulate(6)
+    orc.simulate(6)
+    d = orc.dump()
+    rng = np.random.default_rng(3)
+    slots = rng.choice(len(d["uid"]), size=40, replace=False).astype(np.uint32)
+    sim.remove_agents(d["uid"][slots])
+    orc.remove(slots)
+    for chunk in range(3):
+        sim.simulate(5)
+        orc.simulate(5)
+        _compare(sim, orc, f"after removal + {5 * (chunk + 1)}")
