@@ -113,9 +113,11 @@ typedef struct {
   int32_t environment;           /* ABS_ENV_* (SimulationParams::environment_kind), default grid */
   int32_t neighbor_list;         /* 0 auto: per-agent candidate lists between environment rebuilds when
                                     the diameters are constant (no behaviours, no static detection, one
-                                    domain); -1 off (re-bin + cell-table walk every iteration). The
-                                    visited neighbour sets are identical either way */
-  double neighbor_skin;          /* list skin (absolute length); 0 = 0.15 x the largest diameter */
+                                    domain) and the observed displacement rate lets a build serve >= 3 steps;
+                                    1 always (build whenever the lists do not cover the step); -1 off
+                                    (re-bin + cell-table walk every iteration). The visited neighbour
+                                    sets are identical either way */
+  double neighbor_skin;          /* list skin (absolute length); 0 = 0.2 x the largest diameter */
 } abs_gpu_config;
 
 /* SimulationReport counters (report.hpp:32-40) */
@@ -319,6 +321,16 @@ int abs_gpu_reset_timers(abs_gpu_ctx* ctx, int enable);
  * download (storage) order. */
 int abs_gpu_record_evaluations(abs_gpu_ctx* ctx, int enable);
 int abs_gpu_download_evaluations(abs_gpu_ctx* ctx, uint32_t* out, uint64_t cap);
+/* Each agent's slot in the REFERENCE's storage order (ResourceManager's agent
+ * vector, resource_manager.hpp:19-101), download order. The device keeps its
+ * own storage in cell order; the reference's order — which decides daughter
+ * uids (commit.cpp:186-222) and survivor slots (remove_agents_parallel,
+ * commit.cpp:14-106) — is carried as this key through uploads (slot = upload
+ * order), appends, removals and exact Morton sorts (abs_gpu_sort, and in-loop
+ * sorts of models that add or remove agents). Sorting a download by it gives
+ * the reference's for_each_agent order. Single-domain contexts only
+ * (decomposed contexts carry global keys). */
+int abs_gpu_download_storage_keys(abs_gpu_ctx* ctx, uint32_t* out, uint64_t cap);
 /* Neighbour-list statistics: out4 = {list builds, list
  * steps (iterations served from the lists), build launches timed, largest
  * candidate count of the last build}; *build_ms = CUDA-event time of the

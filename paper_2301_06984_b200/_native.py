@@ -40,6 +40,7 @@ EXPORTS = [
     "abs_gpu_set_defer_commit", "abs_gpu_division_marks", "abs_gpu_commit",
     "abs_gpu_set_agent_ext", "abs_gpu_download_ext", "abs_gpu_phase_times", "abs_gpu_run_frames",
     "abs_gpu_list_stats", "abs_gpu_record_evaluations", "abs_gpu_download_evaluations",
+    "abs_gpu_download_storage_keys",
     "abs_gpu_nccl_unique_id", "abs_gpu_comm_init", "abs_gpu_comm_set_transport", "abs_gpu_comm_reserve",
     "abs_gpu_simulate_decomposed", "abs_gpu_decomp_info", "abs_gpu_memcpy",
 ]
@@ -168,6 +169,7 @@ def load():
         "abs_gpu_list_stats": (C.c_int, [_CTX, _U64, _D]),
         "abs_gpu_record_evaluations": (C.c_int, [_CTX, C.c_int]),
         "abs_gpu_download_evaluations": (C.c_int, [_CTX, _U32, C.c_uint64]),
+        "abs_gpu_download_storage_keys": (C.c_int, [_CTX, _U32, C.c_uint64]),
         "abs_gpu_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "abs_gpu_comm_init": (C.c_int, [_CTX, C.c_void_p, C.c_int, C.c_int]),
         "abs_gpu_comm_set_transport": (C.c_int, [_CTX, C.POINTER(Transport), C.c_int, C.c_int]),

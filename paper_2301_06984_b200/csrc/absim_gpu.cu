@@ -1043,6 +1043,7 @@ __device__ __forceinline__ void stage_daughter(const Daughter& dg, DevGrid* gw,
     reinterpret_cast<double2*>(st_pd + slot)[1] = make_double2(dg.z, dg.d);
     st_vol[slot] = dg.vol;
     st_tag[slot] = dg.tag;
+    ABS_ASSERT(dg.parent < gw->nkeys);
     div_mark[dg.parent] = 1u;
   }
 }
@@ -1194,6 +1195,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
     if (MODEL == ABS_MODEL_PROLIFERATION || MODEL == ABS_MODEL_GROW_DIVIDE || MODEL == ABS_MODEL_GROW_DIVIDE_DIE)
       stage_daughter(dg, gw, st_parent, st_pd, st_vol, div_mark, st_tag);
     if (MODEL == ABS_MODEL_GROW_DIVIDE_DIE) {  // removal staging: one atomic per warp
+      ABS_ASSERT(!dg.dies || S.skey[i] < gp->nkeys);
       if (dg.dies) rmark[S.skey[i]] = 1u;
       const unsigned int dead = __ballot_sync(0xffffffffu, dg.dies);
       if (lane == 0 && dead) atomicAdd(&gw->removed_now, (unsigned long long)__popc(dead));
@@ -1722,6 +1724,7 @@ __global__ void k_append(Soa S, Pd* __restrict__ live, const DevGrid* g,
        k += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long parent = st_parent[k];
     const unsigned long long j = n + div_rank[parent];  // local append slot
+    ABS_ASSERT(j < cap);
     const unsigned int rk = div_rank_g[parent];         // rank among all dividers
     const Pd p = st_pd[k];
     reinterpret_cast<double2*>(live + j)[0] = make_double2(p.x, p.y);
@@ -2110,10 +2113,20 @@ __global__ void k_mkey(const Pd* __restrict__ pos, const DevGrid* g, unsigned in
 // code alone then gives curve order with descending index inside a box — the
 // reference's chain order (sort_balance.cpp:88-128) — without radix passes
 // over the index bits.
+//
+// "Storage index" is the REFERENCE's: the device keeps its own storage in cell
+// order, so with by_key the agent at device slot i is listed at its reference
+// slot skey[i] (a permutation of [0, n) in a single-domain context; checked
+// through nkeys == n). Without keys (decomposed contexts, whose keys are
+// global) the device order stands in.
 __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned long long* keyhi,
-                            unsigned int* __restrict__ idx) {
+                            unsigned int* __restrict__ idx, const unsigned int* __restrict__ skey, int by_key) {
   const DevGrid G = *g;
   if (G.sort_mode == 1u) return;  // in-loop counting sort selected (k_sort_mode)
+  // an earlier iteration of this chunk failed (to be re-run): its state moves
+  // were skipped, so the buffers the host already flipped to hold no valid keys
+  if (G.err) return;
+  const bool keyed = by_key && G.nkeys == G.n;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // passes over the used key bits, rounded up to even
     const unsigned int maxdim = max(G.dims[0], max(G.dims[1], G.dims[2]));
     unsigned int axis_bits = 0;
@@ -2122,9 +2135,11 @@ __global__ void k_sort_keys(const Pd* __restrict__ pos, DevGrid* g, unsigned lon
     unsigned int passes = (code_bits + 7u) / 8u;
     g->sort_passes = passes + (passes & 1u);
   }
-  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < G.n;
-       t += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long i = G.n - 1 - t;
+  for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < G.n;
+       q += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = keyed ? q : G.n - 1 - q;
+    ABS_ASSERT(!keyed || skey[i] < G.n);
+    const unsigned long long t = keyed ? G.n - 1 - skey[i] : q;
     const Pd p = load_pd(pos + i);
     const unsigned long long c0 = box_coord(p.x, G.origin[0], G.box, G.dims[0]);
     const unsigned long long c1 = box_coord(p.y, G.origin[1], G.box, G.dims[1]);
@@ -2333,8 +2348,10 @@ __global__ void k_rem_rekey(Soa S, const DevGrid* g, const unsigned int* __restr
     keep[i] = idx[i] = dead ? 0u : 1u;
     if (dead) continue;
     const unsigned int key = S.skey[i];
+    ABS_ASSERT(key < nk);
     if (key >= new_size) {  // a surviving tail agent: the mover rank picks its hole
       const unsigned long long m = (key - new_size) - (rscan[key] - base);
+      ABS_ASSERT(m < base);
       S.skey[i] = hole_at[m];
     }
   }
@@ -2361,6 +2378,7 @@ __global__ void k_swap_move_d(Pd* pos, Soa S, const unsigned int* __restrict__ k
        i += (unsigned long long)gridDim.x * blockDim.x) {
     if (!keep[i]) continue;
     const unsigned long long dst = holes[idx[i] - base];
+    ABS_ASSERT(dst < new_n);
     pos[dst] = load_pd(pos + i);
     S.uid[dst] = S.uid[i];
     S.flags[dst] = S.flags[i];
@@ -2982,7 +3000,19 @@ double list_skin(const abs_gpu_ctx* c) {
 }
 
 constexpr unsigned int kListKmaxInit = 64;
-constexpr double kListMinSteps = 4.0;  // a build must serve >= this many steps (c4: build iteration ~3x a list step)
+// A build must serve >= this many steps (the build iteration included) to pay
+// off. c4 at 2^26 (ncu launch list, profiles/r2_*): build iteration 46.6 ms
+// (re-bin 3.3 + k_list_build 28 + list step), list step 15.5 ms, re-bin + walk
+// 29.3 ms: two steps lose (31 ms/step), three win (25.9), four 23.3.
+// ABSIM_LIST_MIN_STEPS overrides (A/B switch).
+double list_min_steps() {
+  static const double v = [] {
+    const char* e = std::getenv("ABSIM_LIST_MIN_STEPS");
+    const double x = e ? std::atof(e) : 0.0;
+    return x > 0.0 ? x : 3.0;
+  }();
+  return v;
+}
 constexpr unsigned int kListKmaxMax = 254;  // u8 counts (255 = overflow sentinel)
 
 // List storage for the current population: [kmax][stride] u32 + u8 counts.
@@ -3107,6 +3137,32 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
   phase_mark(c);  // no commit
 }
 
+#ifdef ABS_DEBUG
+// Debug builds (direct launches, ABSIM_GRAPHS=0): the storage keys of a
+// single-domain context are a permutation of [0, n).
+void check_keys(abs_gpu_ctx* c, const char* where, unsigned long long iteration) {
+  static const bool on = env_flag("ABSIM_CHECK_KEYS", false);
+  if (!on) return;
+  DevGrid h{};
+  cudaStreamSynchronize(c->stream);
+  cudaMemcpy(&h, c->g, sizeof h, cudaMemcpyDeviceToHost);
+  if (h.err || h.nkeys != h.n) return;
+  std::vector<unsigned int> k(h.n);
+  if (h.n) cudaMemcpy(k.data(), c->S[c->cur].skey, h.n * 4, cudaMemcpyDeviceToHost);
+  std::vector<char> seen(h.n, 0);
+  for (unsigned long long i = 0; i < h.n; ++i) {
+    if (k[i] >= h.n || seen[k[i]]) {
+      std::fprintf(stderr, "absim: bad storage key %u at slot %llu of %llu (%s, iteration %llu, dup %d)\n", k[i], i,
+                   h.n, where, iteration, k[i] < h.n);
+      std::abort();
+    }
+    seen[k[i]] = 1;
+  }
+}
+#else
+inline void check_keys(abs_gpu_ctx*, const char*, unsigned long long) {}
+#endif
+
 void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0) {
   sync_check(c, "before iteration");
   if (c->rec_evals && c->evc) {  // static / ghost agents evaluate nothing this iteration
@@ -3117,7 +3173,9 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
     return;
   }
   c->track_now = kind == 3;  // re-binning step whose displacement the list policy tracks
+  check_keys(c, "iteration start (after the sort)", iteration);
   launch_env_update(c, iteration, adds_agents(c->cfg), true, kind == 3 ? 3 : 0);
+  check_keys(c, "after the re-bin", iteration);
   phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
     const int nb = grid_blocks(c, c->cap);
@@ -3178,6 +3236,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
       ++c->launches;
     }
     if (!c->defer_commit) launch_commit(c);
+    check_keys(c, "after the commit", iteration);
   }
   phase_mark(c);  // after commit
 }
@@ -3625,7 +3684,8 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   unsigned long long* k2 = c->sort_k[1];
   unsigned int* i1 = c->sort_i[0];
   unsigned int* i2 = c->sort_i[1];
-  k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1);
+  k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1, c->S[c->cur].skey,
+                                                                 exact_order ? 1 : 0);
   sync_check(c, "k_sort_keys");
   c->launches += 3;
   for (int shift = 0; shift < 64; shift += 8) {
@@ -3682,9 +3742,17 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     sync_check(c, "ensure_lists");
   }
   while (done < iterations) {
-    // while the list policy is re-binning, re-read the displacement rate every 8 iterations
+    // while the list policy is re-binning (a relaxing system's rate decays), re-read the
+    // displacement rate every 4 iterations
+    // (and while the rate is still unknown, a build + one list step to learn it:
+    // a whole chunk scheduled as list steps would be rolled back at the first
+    // failed coverage check)
+    const bool lists_on = list_mode_ok(c) && c->nl;
+    const bool rebinning = lists_on && c->pred_rate > 0.0 && c->cfg.neighbor_list <= 0 &&
+                           list_skin(c) < 2.0 * list_min_steps() * c->pred_rate;
     const unsigned long long todo = std::min<unsigned long long>(
-        list_mode_ok(c) && c->nl && !c->list_valid ? 8 : chunk, iterations - done);
+        lists_on && c->pred_rate <= 0.0 ? 2 : (rebinning ? 4 : (lists_on && !c->list_valid ? 8 : chunk)),
+        iterations - done);
     struct Snap { int cur; bool pos_in_new; bool grid_valid; bool list_valid; };
     std::vector<Snap> snaps;
     snaps.reserve(todo);
@@ -3704,12 +3772,13 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       // step (rolled back with the rest of its chunk) stays the exception.
       // A build pays off only if the lists then serve several steps: at the
       // current rate a fresh list lasts skin / (2 rate) steps; below
-      // kListMinSteps the iteration re-bins and walks (tracking the rate).
+      // list_min_steps() the iteration re-bins and walks (tracking the rate).
       int kind = 0;
       if (list_mode_ok(c) && c->nl) {
         const double skin = list_skin(c);
         const bool usable = c->list_valid && !sorts;
-        const bool pays = c->pred_rate <= 0.0 || skin >= 2.0 * kListMinSteps * c->pred_rate;
+        const bool pays = c->cfg.neighbor_list > 0 || c->pred_rate <= 0.0 ||
+                          skin >= 2.0 * list_min_steps() * c->pred_rate;
         if (usable && (2.0 * c->pred_acc <= skin || remaining < 2)) {
           kind = 1;
           c->pred_acc += c->pred_rate;
@@ -3780,6 +3849,15 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     DevGrid h{};
     int rc = read_grid(c, &h);
     if (rc) return rc;
+    static const bool trace = env_flag("ABSIM_LIST_TRACE", false);
+    if (trace) {  // debugging: the chunk's iteration kinds and the device's coverage numbers
+      float rate = 0.0f;
+      std::memcpy(&rate, &h.step_disp, sizeof rate);
+      std::fprintf(stderr, "absim: it %llu kinds", c->iteration);
+      for (int k : kinds) std::fprintf(stderr, " %d", k);
+      std::fprintf(stderr, " | err %d failed_it %llu rate %.4f acc %.4f pred_rate %.4f pred_acc %.4f need %u\n", h.err,
+                   h.failed_iteration, rate, h.list_acc, c->pred_rate, c->pred_acc, h.list_need);
+    }
     {  // the prediction restarts from the device's own numbers
       float rate = 0.0f;
       std::memcpy(&rate, &h.step_disp, sizeof rate);
@@ -4449,6 +4527,9 @@ int abs_gpu_remove(abs_gpu_ctx* c, const uint64_t* uids, uint64_t r) {
   const unsigned long long n = h.n;
   if (r > n) return set_err(c, ABS_ERR_INVALID_ARGUMENT, "more removals than agents");
   if (h.nkeys != n) return set_err(c, ABS_ERR_STATE, "removals need the whole population in one context");
+  // key-indexed removal marks and hole table (sized at upload only for models that add agents)
+  rc = ensure_uid_space(c, h.nkeys + 1);
+  if (rc) return rc;
   Soa& S = c->S[c->cur];
   // the removal list sorted on the host (O(r log r)) for the uid lookup;
   // duplicates are the reference's double-staging error (agent.hpp:136-141)
@@ -4572,6 +4653,17 @@ int abs_gpu_download_evaluations(abs_gpu_ctx* c, uint32_t* out, uint64_t cap) {
   if (rc) return rc;
   if (cap < h.n) return set_err(c, ABS_ERR_CAPACITY, "output holds fewer entries than agents");
   CK(cudaMemcpy(out, c->evc, h.n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
+  return ABS_OK;
+}
+
+int abs_gpu_download_storage_keys(abs_gpu_ctx* c, uint32_t* out, uint64_t cap) {
+  if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  DevGrid h{};
+  int rc = read_grid(c, &h);
+  if (rc) return rc;
+  if (cap < h.n) return set_err(c, ABS_ERR_CAPACITY, "output holds fewer entries than agents");
+  if (h.n) CK(cudaMemcpy(out, c->S[c->cur].skey, h.n * sizeof(unsigned int), cudaMemcpyDeviceToHost));
   return ABS_OK;
 }
 

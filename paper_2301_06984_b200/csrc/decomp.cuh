@@ -298,6 +298,7 @@ __global__ void k_import_slab(const Rec* __restrict__ in, unsigned long long cou
     S.beh[j] = r.beh;
     S.tag[j] = r.tag;
     S.rngc[j] = r.rngc;
+    S.skey[j] = r.pad3;  // the global storage key travels with the agent (k_export_slab)
   }
 }
 

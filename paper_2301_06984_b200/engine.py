@@ -64,9 +64,10 @@ class SimulationParams:
     # EnvironmentKind (params.hpp:9): "uniform_grid" or "brute_force"
     environment: str = "uniform_grid"
     # per-agent candidate lists between environment rebuilds:
-    # True = auto (used when the path allows it), False = re-bin every step;
-    # neighbor_skin 0 = 0.15 x the largest diameter
-    neighbor_list: bool = True
+    # True = auto (used when the path allows it and a build pays off), False =
+    # re-bin every step, "always" = build whenever the lists do not cover a step;
+    # neighbor_skin 0 = 0.2 x the largest diameter
+    neighbor_list: bool | str = True
     neighbor_skin: float = 0.0
 
     def validate(self):
@@ -106,7 +107,7 @@ class SimulationParams:
         c.bins_per_box = self.bins_per_box
         c.bins_per_box_x = self.bins_per_box_x
         c.environment = ENVIRONMENTS[self.environment]
-        c.neighbor_list = 0 if self.neighbor_list else -1
+        c.neighbor_list = 1 if self.neighbor_list == "always" else (0 if self.neighbor_list else -1)
         c.neighbor_skin = float(self.neighbor_skin)
         return c
 
@@ -468,6 +469,13 @@ class Simulation:
         """Per-agent force evaluations of the last iteration, download order."""
         out = np.zeros(max(1, self.agent_count()), np.uint32)
         N.check(N.load().abs_gpu_download_evaluations(self._ctx, _p(out, C.c_uint32), len(out)), self._ctx)
+        return out[:self.agent_count()]
+
+    def storage_keys(self) -> np.ndarray:
+        """Each agent's slot in the reference's storage order (download order);
+        agents()[k][np.argsort(storage_keys())] is the reference's for_each_agent order."""
+        out = np.zeros(max(1, self.agent_count()), np.uint32)
+        N.check(N.load().abs_gpu_download_storage_keys(self._ctx, _p(out, C.c_uint32), len(out)), self._ctx)
         return out[:self.agent_count()]
 
     def force_kernel_time(self):
