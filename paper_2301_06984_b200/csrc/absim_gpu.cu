@@ -1235,9 +1235,14 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
 // one contiguous kmax x 128 B block — the write-out and the list sweep's index
 // loads are full-line, sequential accesses.
 #ifndef ABS_LIST_MIN_BLOCKS
-#define ABS_LIST_MIN_BLOCKS 5
+#define ABS_LIST_MIN_BLOCKS 4
 #endif
-constexpr int kListStage = 64;  // candidates staged per lane before the coalesced write-out
+// c4 @ 2^26 k_list_build: 64 staged (3 CTAs/SM) 28.1 ms, 56 / 48 / 44 (4 CTAs) 23.6 / 23.7 / 23.3,
+// 32 (5 CTAs) 32.0, 16 (6 CTAs) 35.0: residency helps until the unstaged tail writes take over
+#ifndef ABS_LIST_STAGE
+#define ABS_LIST_STAGE 48
+#endif
+constexpr int kListStage = ABS_LIST_STAGE;  // candidates staged per lane before the coalesced write-out
 constexpr unsigned char kListOverflow = 255;  // count sentinel: the agent's candidates did not fit
 constexpr int kListSmem = (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads * 4;
 
@@ -1332,6 +1337,20 @@ __device__ __noinline__ unsigned long long scan_walk(const QGrid& Q, const Pd* _
   return (static_cast<unsigned long long>(evals) << 32) | nov;
 }
 
+// c4 @ 2^26 k_list_scan (batch, CTAs/SM): (4,4) 7.57 ms, (5,4) 7.25, (6,4) 7.33, (8,3) 7.69, (2,6) 10.1, (6,5) 11.1
+#ifndef ABS_SCAN_BATCH
+#define ABS_SCAN_BATCH 5
+#endif
+constexpr int kScanBatch = ABS_SCAN_BATCH;  // candidates in flight per lane
+// c4 @ 2^26 k_list_forces (batch, CTAs/SM): (2,3) 8.17 ms, (4,3) 8.31, (4,2) 9.9, (3,4) 7.30, (2,4) 6.78, (2,5) 7.79, (1,6) 10.3
+#ifndef ABS_LF_MIN_BLOCKS
+#define ABS_LF_MIN_BLOCKS 4
+#endif
+#ifndef ABS_LF_BATCH
+#define ABS_LF_BATCH 2
+#endif
+constexpr int kLfBatch = ABS_LF_BATCH;  // contact records in flight per lane
+
 __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
     k_list_scan(const Pd* __restrict__ pin, const float4* __restrict__ pfin, DevGrid* g,
                 const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
@@ -1375,23 +1394,23 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
       nov = static_cast<unsigned int>(en);
     }
     const unsigned int* col = list + wbase;
-    unsigned int nj[kBatch];
+    unsigned int nj[kScanBatch];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) nj[u] = u < static_cast<int>(cl) ? __ldg(col + u * 32) : 0u;
-    for (unsigned int s = 0; s < cmax; s += kBatch) {
-      unsigned int jj[kBatch];
+    for (int u = 0; u < kScanBatch; ++u) nj[u] = u < static_cast<int>(cl) ? __ldg(col + u * 32) : 0u;
+    for (unsigned int s = 0; s < cmax; s += kScanBatch) {
+      unsigned int jj[kScanBatch];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) jj[u] = nj[u];
-      float4 qf[kBatch];
+      for (int u = 0; u < kScanBatch; ++u) jj[u] = nj[u];
+      float4 qf[kScanBatch];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
-      col += kBatch * 32;
+      for (int u = 0; u < kScanBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
+      col += kScanBatch * 32;
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) nj[u] = s + kBatch + u < cl ? __ldg(col + u * 32) : 0u;
-      float df2[kBatch];
+      for (int u = 0; u < kScanBatch; ++u) nj[u] = s + kScanBatch + u < cl ? __ldg(col + u * 32) : 0u;
+      float df2[kScanBatch];
       unsigned int in = 0, band = 0;
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
+      for (int u = 0; u < kScanBatch; ++u) {
         const float ex = mf.x - qf[u].x, ey = mf.y - qf[u].y, ez = mf.z - qf[u].z;
         df2[u] = __fmaf_rn(ex, ex, __fmaf_rn(ey, ey, ez * ez));
         const bool v = s + u < cl && df2[u] <= rout2;
@@ -1401,7 +1420,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
       if (__any_sync(0xffffffffu, band != 0u) && band) {  // margin band: the reference's exact fp64 test
         const Pd me = load_pd(pin + i);
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
+        for (int u = 0; u < kScanBatch; ++u) {
           if (band & (1u << u)) {
             const Pd q = load_pd(pin + jj[u]);
             const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
@@ -1411,7 +1430,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
       }
       evals += __popc(in);
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
+      for (int u = 0; u < kScanBatch; ++u) {
         // contact superset: df2 < (0.5 (d_i + d_j) + slack)^2 (1 + 5e-7)
         const float hp = __fmaf_rn(0.5f, qf[u].w, hme);
         if ((in & (1u << u)) && df2[u] < hp * hp * 1.0000005f) {
@@ -1429,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
 }
 
 template <bool RECORD>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, ABS_LF_MIN_BLOCKS)
     k_list_forces(const Pd* __restrict__ pin, Pd* __restrict__ pout, float4* __restrict__ pfout, Soa S, DevGrid* g,
                   const unsigned int* __restrict__ list, const unsigned char* __restrict__ cnt, unsigned int kmax,
                   const unsigned int* __restrict__ contacts, const unsigned char* __restrict__ ncontacts,
@@ -1474,14 +1493,17 @@ __global__ void __launch_bounds__(kThreads, 3)
     if (nc != kContactOverflow) {
       const unsigned int* ct = contacts + (i >> 5) * (kListContacts * 32) + (i & 31);
       unsigned int q = 0;
-      for (; q + 2 <= nc; q += 2) {  // two records in flight
-        const unsigned int j0 = __ldg(ct + q * 32), j1 = __ldg(ct + (q + 1) * 32);
-        const Pd q0 = load_pd(pin + j0);
-        const Pd q1 = load_pd(pin + j1);
-        contact_q(j0, q0);
-        contact_q(j1, q1);
+      for (; q + kLfBatch <= nc; q += kLfBatch) {  // kLfBatch records in flight
+        unsigned int jb[kLfBatch];
+        Pd qb[kLfBatch];
+#pragma unroll
+        for (int u = 0; u < kLfBatch; ++u) jb[u] = __ldg(ct + (q + u) * 32);
+#pragma unroll
+        for (int u = 0; u < kLfBatch; ++u) qb[u] = load_pd(pin + jb[u]);
+#pragma unroll
+        for (int u = 0; u < kLfBatch; ++u) contact_q(jb[u], qb[u]);
       }
-      if (q < nc) {
+      for (; q < nc; ++q) {
         const unsigned int j0 = __ldg(ct + q * 32);
         contact_q(j0, load_pd(pin + j0));
       }
