@@ -1243,6 +1243,19 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
 #define ABS_LIST_STAGE 48
 #endif
 constexpr int kListStage = ABS_LIST_STAGE;  // candidates staged per lane before the coalesced write-out
+// Streaming accesses of the list kernels (list / contact columns, the
+// integration outputs) are marked evict-first so they do not push the
+// gathered candidate records out of L2. ABS_CACHE_HINTS=0: plain accesses.
+#ifndef ABS_CACHE_HINTS
+#define ABS_CACHE_HINTS 1
+#endif
+#if ABS_CACHE_HINTS
+#define ABS_LDS(p) __ldcs(p)
+#define ABS_STS(p, v) __stcs((p), (v))
+#else
+#define ABS_LDS(p) __ldg(p)
+#define ABS_STS(p, v) (*(p) = (v))
+#endif
 constexpr unsigned char kListOverflow = 255;  // count sentinel: the agent's candidates did not fit
 constexpr int kListSmem = (kMaxRows + kMaxRows / 2 + kListStage) * kForceThreads * 4;
 
@@ -1396,7 +1409,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
     const unsigned int* col = list + wbase;
     unsigned int nj[kScanBatch];
 #pragma unroll
-    for (int u = 0; u < kScanBatch; ++u) nj[u] = u < static_cast<int>(cl) ? __ldg(col + u * 32) : 0u;
+    for (int u = 0; u < kScanBatch; ++u) nj[u] = u < static_cast<int>(cl) ? ABS_LDS(col + u * 32) : 0u;
     for (unsigned int s = 0; s < cmax; s += kScanBatch) {
       unsigned int jj[kScanBatch];
 #pragma unroll
@@ -1406,7 +1419,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
       for (int u = 0; u < kScanBatch; ++u) qf[u] = __ldg(pfin + jj[u]);
       col += kScanBatch * 32;
 #pragma unroll
-      for (int u = 0; u < kScanBatch; ++u) nj[u] = s + kScanBatch + u < cl ? __ldg(col + u * 32) : 0u;
+      for (int u = 0; u < kScanBatch; ++u) nj[u] = s + kScanBatch + u < cl ? ABS_LDS(col + u * 32) : 0u;
       float df2[kScanBatch];
       unsigned int in = 0, band = 0;
 #pragma unroll
@@ -1434,7 +1447,7 @@ __global__ void __launch_bounds__(kThreads, ABS_LIST_SCAN_MIN_BLOCKS)
         // contact superset: df2 < (0.5 (d_i + d_j) + slack)^2 (1 + 5e-7)
         const float hp = __fmaf_rn(0.5f, qf[u].w, hme);
         if ((in & (1u << u)) && df2[u] < hp * hp * 1.0000005f) {
-          if (nov < kListContacts) ct[nov * 32] = jj[u];
+          if (nov < kListContacts) ABS_STS(ct + nov * 32, jj[u]);
           ++nov;
         }
       }
@@ -1497,14 +1510,14 @@ __global__ void __launch_bounds__(kThreads, ABS_LF_MIN_BLOCKS)
         unsigned int jb[kLfBatch];
         Pd qb[kLfBatch];
 #pragma unroll
-        for (int u = 0; u < kLfBatch; ++u) jb[u] = __ldg(ct + (q + u) * 32);
+        for (int u = 0; u < kLfBatch; ++u) jb[u] = ABS_LDS(ct + (q + u) * 32);
 #pragma unroll
         for (int u = 0; u < kLfBatch; ++u) qb[u] = load_pd(pin + jb[u]);
 #pragma unroll
         for (int u = 0; u < kLfBatch; ++u) contact_q(jb[u], qb[u]);
       }
       for (; q < nc; ++q) {
-        const unsigned int j0 = __ldg(ct + q * 32);
+        const unsigned int j0 = ABS_LDS(ct + q * 32);
         contact_q(j0, load_pd(pin + j0));
       }
     } else {  // more possible contacts than recorded: the list (or the rebuild step's walk) again
@@ -1558,11 +1571,11 @@ __global__ void __launch_bounds__(kThreads, ABS_LF_MIN_BLOCKS)
       S.force[cap + i] = fy;
       S.force[2 * cap + i] = fz;
     }
-    S.partners[i] = contributors;
-    reinterpret_cast<double2*>(pout + i)[0] = make_double2(np.x, np.y);
-    reinterpret_cast<double2*>(pout + i)[1] = make_double2(np.z, np.d);
-    pfout[i] = make_float4(static_cast<float>(np.x - lox), static_cast<float>(np.y - loy),
-                           static_cast<float>(np.z - loz), static_cast<float>(np.d));
+    ABS_STS(S.partners + i, contributors);
+    ABS_STS(reinterpret_cast<double2*>(pout + i), make_double2(np.x, np.y));
+    ABS_STS(reinterpret_cast<double2*>(pout + i) + 1, make_double2(np.z, np.d));
+    ABS_STS(pfout + i, make_float4(static_cast<float>(np.x - lox), static_cast<float>(np.y - loy),
+                                   static_cast<float>(np.z - loz), static_cast<float>(np.d)));
   }
   const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
   if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
