@@ -513,14 +513,16 @@ def run_gpu(args):
     traffic = None
     issue = None
     tp = os.path.join(ROOT, "profiles", "force_traffic.json")
-    if os.path.exists(tp):
+    kernel_name = "k_sir" if sir else ("k_force_list" if lists["list_steps"] else "k_force")
+    if os.path.exists(tp):  # ncu --set full figures of the same workload, per kernel (profiles/r2/)
         try:
             with open(tp) as f:
-                tt = json.load(f)
-            if tt.get("config") == args.config and tt.get("agents") == n_agents:
-                traffic = tt.get("dram_bytes_per_launch")
-                issue = {k: tt[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
-                                            "warp_instructions_per_agent") if k in tt}
+                tt = json.load(f).get(args.config, {})
+            if tt.get("agents") == n_agents and kernel_name in tt:
+                tk = tt[kernel_name]
+                traffic = tk.get("dram_bytes_per_launch")
+                issue = {k: tk[k] for k in ("issue_active_pct", "warps_active_pct", "l1_hit_pct", "l2_hit_pct",
+                                            "warp_instructions_per_agent", "kernels") if k in tk}
         except Exception:
             pass
     line = {
@@ -529,7 +531,8 @@ def run_gpu(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _workload_config(args, wl.name, wl.n, world),
         "device_knobs": {"bins_per_box": [args.bins_x, args.bins, args.bins], "lists": args.lists, "skin": args.skin},
-        "roofline": {"bound": "hbm", "kernel": "k_sir" if sir else ("k_force_list" if lists["list_steps"] else "k_force"),
+        # k_force_list = the list step's force work, k_list_scan + k_list_forces, timed as one event pair
+        "roofline": {"bound": "hbm", "kernel": kernel_name,
                      "achieved": achieved, "peak": hbm,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "algorithmic_bytes_per_launch": force_bytes,
