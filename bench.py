@@ -170,8 +170,8 @@ def cpu_baseline(wl_name, steps=None, threads=None, env="uniform_grid"):
         sim.simulate(1)
     wall = time.perf_counter() - t0
     return {"value": agent_its / wall, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{wl.name} shape at {wl.n} agents x {steps} iterations "
-                      f"(same density and distributions), {wall:.1f} s of CPU wall time"}
+            "sample": f"{wl.name} shape from {wl.n} agents x {steps} iterations "
+                      f"({agent_its} agent-iterations, same density and distributions), {wall:.1f} s of CPU wall time"}
 
 
 def _workload_config(args, wl_name, n, world):
@@ -550,7 +550,10 @@ def run_gpu(args):
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(args.config, env=args.env)
+        # c2 grows from its 16^3 lattice: the reference runs the same iterations as the GPU arm
+        # (warm-up + timed steps; 200 iterations reach ~2.1 M agents, ~10 s on 16 cores)
+        c2_steps = (args.warmup + args.steps) if args.config == "c2" else None
+        line["cpu_baseline"] = cpu_baseline(args.config, steps=c2_steps, env=args.env)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

@@ -16,7 +16,7 @@ for r in rows[1:]:
     name=re.split(r"[(<]", re.sub(r"^void ","",r[ki]).replace("<unnamed>::",""))[0]
     t=float(r[vi].replace(",",""))/1e6
     if t>0.2: d.setdefault(name,[]).append(t)
-print("$v", " ".join("%s=%.2f(x%d)"%(k.replace("k_",""),statistics.median(v),len(v)) for k,v in d.items() if k in ("k_list_build","k_list_scan","k_list_forces","k_force")))
+print("$v", " ".join("%s=%.2f(x%d)"%(k.replace("k_",""),statistics.median(v),len(v)) for k,v in d.items() if k.startswith("k_list") or k=="k_force"))
 PY
   rm -f gpurun_out/${TAG}_$v.csv
 done
