@@ -898,12 +898,19 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
     // contact superset threshold: (0.5 (d_a + d_b) + slack)^2 (1 + 5e-7), the
     // half diameter of this agent and the slack folded in once
     const float hme = 0.5f * dif + slack;
+    // contacts beyond the shared-memory list spill to a per-thread array (local
+    // memory, touched only by the few lanes that need it): the alternative, a
+    // second walk by that lane, stalls its whole warp (c1: ~1 % of the agents
+    // hold more than 16 contacts, i.e. a quarter of the warps walked twice)
+    unsigned int ovf[kSpillContacts];
     if constexpr (F32) {
       walk(r, r * r, [&](unsigned int j, float df2, float qd, bool in) {
         evals += in;
         const float hp = __fmaf_rn(0.5f, qd, hme);
         const bool ct = in && df2 < hp * hp * 1.0000005f;
         if (ct && nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+        if (__builtin_expect(ct && nov >= kMaxContacts, 0))
+          if (nov < kMaxContacts + kSpillContacts) ovf[nov - kMaxContacts] = j;
         nov += ct;
       });
     } else {
@@ -912,6 +919,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
         const double h = 0.5 * (me.d + q.d);
         if (d2 < h * h * (1.0 + 0x1.0p-50)) {
           if (nov < kMaxContacts) ovl[nov * ovl_stride] = static_cast<OvlT>(j);
+          else if (nov < kMaxContacts + kSpillContacts) ovf[nov - kMaxContacts] = j;
           ++nov;
         }
       });
@@ -942,7 +950,7 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       }
     };
     auto contact = [&](unsigned int j) { contact_q(j, fetch(j)); };
-    bool overflow = nov > kMaxContacts;
+    bool overflow = nov > kMaxContacts + kSpillContacts;
 #if defined(ABS_ABLATE) && ABS_ABLATE >= 2
     if (nov > 1000000u) overflow = false;  // timing ablation: no pass B
     else nov = 0;
@@ -951,7 +959,8 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
       // contact records fetched kPassB at a time (independent loads in
       // flight), applied in list order
       unsigned int c = 0;
-      for (; c + kPassB <= nov; c += kPassB) {
+      const unsigned int nsh = nov < kMaxContacts ? nov : kMaxContacts;  // in shared memory; the rest spilled
+      for (; c + kPassB <= nsh; c += kPassB) {
         unsigned int jj[kPassB];
         Pd qq[kPassB];
 #pragma unroll
@@ -961,7 +970,8 @@ __device__ __forceinline__ Daughter agent_step(Soa& S, Pd* __restrict__ out, uns
 #pragma unroll
         for (int u = 0; u < kPassB; ++u) contact_q(jj[u], qq[u]);
       }
-      for (; c < nov; ++c) contact(ovl[c * ovl_stride]);
+      for (; c < nsh; ++c) contact(ovl[c * ovl_stride]);
+      for (; c < nov; ++c) contact(ovf[c - kMaxContacts]);
     } else if constexpr (F32) {  // more contacts than the list holds: re-walk (rare)
       walk(r, r * r, [&](unsigned int j, float df2, float qd, bool in) {
         const float hp = __fmaf_rn(0.5f, qd, hme);
@@ -1327,7 +1337,11 @@ __global__ void __launch_bounds__(kForceThreads, ABS_LIST_MIN_BLOCKS)
 #ifndef ABS_LIST_SCAN_MIN_BLOCKS
 #define ABS_LIST_SCAN_MIN_BLOCKS 4
 #endif
-constexpr int kListContacts = 16;                 // contacts recorded per agent (more: re-scan)
+// Contacts recorded per agent (more: the force pass re-scans the agent's
+// list, one lane, ~25 us of serial loads — at 16, ~1 % of c1's agents (mean 9
+// contacts) did, and their warps were the whole kernel's tail: k_list_forces
+// 35 us for 131,072 agents with the SMs 39 % active).
+constexpr int kListContacts = 24;
 constexpr unsigned char kContactOverflow = 255;  // contact count sentinel
 
 // Exact cell-table walk of one agent whose candidates did not fit its list
@@ -1532,13 +1546,22 @@ __global__ void __launch_bounds__(kThreads, ABS_LF_MIN_BLOCKS)
                           });
       } else {
         const unsigned int* col = list + (i >> 5) * (static_cast<unsigned long long>(kmax) * 32) + (i & 31);
-        for (unsigned int s2 = 0; s2 < c; ++s2) {
-          const unsigned int j = __ldg(col + static_cast<unsigned long long>(s2) * 32);
-          const Pd q = load_pd(pin + j);
-          const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
-          const double d2 = (dx * dx + dy * dy) + dz * dz;
-          const double h = 0.5 * (me.d + q.d);
-          if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(j, q);
+        for (unsigned int s2 = 0; s2 < c; s2 += 4) {  // four records in flight
+          unsigned int jb[4];
+          Pd qb[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) jb[u] = __ldg(col + static_cast<unsigned long long>(min(s2 + u, c - 1)) * 32);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) qb[u] = load_pd(pin + jb[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (s2 + u >= c) break;
+            const Pd& q = qb[u];
+            const double dx = me.x - q.x, dy = me.y - q.y, dz = me.z - q.z;
+            const double d2 = (dx * dx + dy * dy) + dz * dz;
+            const double h = 0.5 * (me.d + q.d);
+            if (d2 <= r2 && d2 < h * h * (1.0 + 0x1.0p-50)) contact_q(jb[u], q);
+          }
         }
       }
     }
@@ -1577,8 +1600,16 @@ __global__ void __launch_bounds__(kThreads, ABS_LF_MIN_BLOCKS)
     ABS_STS(pfout + i, make_float4(static_cast<float>(np.x - lox), static_cast<float>(np.y - loy),
                                    static_cast<float>(np.z - loz), static_cast<float>(np.d)));
   }
+  // one same-address atomic per block, not per warp
+  __shared__ unsigned int smoved[kThreads / 32];
   const unsigned int mb = __reduce_max_sync(0xffffffffu, __float_as_uint(moved));
-  if ((threadIdx.x & 31) == 0 && mb) atomicMax(&g->step_disp, mb);
+  if ((threadIdx.x & 31) == 0) smoved[threadIdx.x >> 5] = mb;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int m = 0;
+    for (int q = 0; q < kThreads / 32; ++q) m = max(m, smoved[q]);
+    if (m) atomicMax(&g->step_disp, m);
+  }
 }
 
 // ------------------------------------------------------------ config 5: SIR
@@ -2623,6 +2654,19 @@ int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
 }
 
+// Grid of an agent-sized grid-stride kernel, from the host's mirror of the
+// agent count (exact between chunks; a population that grows inside a chunk
+// only makes the resident threads loop). Small populations get fewer blocks:
+// an empty block still pays its start-up and, in the reductions, its
+// same-address atomics (c1: k_reduce_finalize 12.7 us with 1028 blocks).
+int agent_blocks(const abs_gpu_ctx* c, unsigned int per_thread = 1) {
+  const unsigned long long n = c->n ? std::min(c->n, c->cap) : c->cap;
+  const unsigned long long per_block = static_cast<unsigned long long>(kThreads) * per_thread;
+  const unsigned long long b = (n + per_block - 1) / per_block;
+  const unsigned long long lim = static_cast<unsigned long long>(c->sms) * 8;
+  return static_cast<int>(std::max<unsigned long long>(1, std::min(b, lim)));
+}
+
 template <class K>
 int force_blocks(const abs_gpu_ctx* c, K kernel, int smem = (2 * kMaxRows + kMaxContacts) * kForceThreads * 4) {
   int per_sm = 0;  // persistent: the resident CTAs only
@@ -2895,7 +2939,7 @@ void launch_commit(abs_gpu_ctx* c);
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add, bool in_step = false,
                        int list_mode = 0, double skin = 0.0) {
-  const int nb = grid_blocks(c, c->cap);
+  const int nb = agent_blocks(c);
   const unsigned long long* nbins_dev = &c->g->nbins;
   static const bool fused = env_flag("ABSIM_FUSED_FINALIZE", true);
   if (c->grid_valid && !fused) {  // previous cell table still holds scanned offsets
@@ -2959,7 +3003,7 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   const unsigned int* work = nullptr;
   if (STATIC && a.iteration != 0 && static_prepass()) {  // iteration 0: nobody is static (simulation.cpp:335-349)
     // c->rank is free after k_mark (it listed the marking agents there)
-    k_static_pass<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->nv, c->nn,
+    k_static_pass<<<agent_blocks(c), kThreads, 0, c->stream>>>(S, c->newpd, c->g, c->nv, c->nn,
                                                                        MODEL != ABS_MODEL_NONE, c->rank);
                                                                    sync_check(c, "k_static_pass");
     ++c->launches;
@@ -3139,7 +3183,7 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
     fin = from_new ? c->pf2 : c->pf;
     pout = from_new ? c->S[c->cur].pd : c->newpd;
     fout = from_new ? c->pf : c->pf2;
-    k_reduce_finalize<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pin, c->g, fa,
+    k_reduce_finalize<<<agent_blocks(c, 4), kThreads, 0, c->stream>>>(pin, c->g, fa,
                                                                           c->grid_valid ? c->start : nullptr);
     sync_check(c, "k_reduce_finalize(list)");
     ++c->launches;
@@ -3158,13 +3202,13 @@ void launch_list_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kin
   k_list_scan<<<scan_blocks, kThreads, 0, c->stream>>>(pin, fin, c->g, c->nl, c->nl_cnt, c->nl_kmax, c->nl_ct,
                                                        c->nl_nct, a.evc, c->start);
   sync_check(c, "k_list_scan");
-  const int nb = grid_blocks(c, c->cap);
-  if (c->cfg.record_forces)
-    k_list_forces<true><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
-                                                        c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
-  else
-    k_list_forces<false><<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt,
-                                                         c->nl_kmax, c->nl_ct, c->nl_nct, a, c->cap, c->start);
+  const int nb = agent_blocks(c);
+  auto forces = [&](auto kernel) {
+    kernel<<<nb, kThreads, 0, c->stream>>>(pin, pout, fout, c->S[c->cur], c->g, c->nl, c->nl_cnt, c->nl_kmax,
+                                           c->nl_ct, c->nl_nct, a, c->cap, c->start);
+  };
+  if (c->cfg.record_forces) forces(k_list_forces<true>);
+  else forces(k_list_forces<false>);
   if (ev) cudaEventRecord(ev[1], c->stream);
   sync_check(c, "k_list_forces");
   c->launches += 2;
@@ -3213,7 +3257,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
   check_keys(c, "after the re-bin", iteration);
   phase_mark(c);  // after environment update
   if (c->cfg.model == ABS_MODEL_SIR) {
-    const int nb = grid_blocks(c, c->cap);
+    const int nb = agent_blocks(c);
     const StepArgs a = step_args(c, iteration);
     Soa& S = c->S[c->cur];
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -3238,7 +3282,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
     phase_mark(c);  // no commit
     return;
   }
-  const int nb = grid_blocks(c, c->cap);
+  const int nb = agent_blocks(c);
   const StepArgs a = step_args(c, iteration);
   Soa& S = c->S[c->cur];
   if (c->cfg.detect_static_agents && iteration > 0) {
@@ -3285,7 +3329,7 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
 // The removal half of CommitBuffer::commit (removals before additions,
 // commit.cpp:164-185) for agents the loop staged (ABS_FLAG_REMOVED + key marks).
 void launch_removals(abs_gpu_ctx* c, bool keys_in_list_order = false) {
-  const int nb = grid_blocks(c, c->cap);
+  const int nb = agent_blocks(c);
   Soa& S = c->S[c->cur];
   unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
   launch_scan<unsigned int>(c, c->rmark, &c->g->nkeys, c->uid_cap, tiles, &c->g->err);
@@ -3304,7 +3348,7 @@ void launch_removals(abs_gpu_ctx* c, bool keys_in_list_order = false) {
 
 void launch_commit(abs_gpu_ctx* c) {
   if (removes_agents(c->cfg)) launch_removals(c);
-  const int nb = grid_blocks(c, c->cap);
+  const int nb = agent_blocks(c);
   Soa& S = c->S[c->cur];
   const unsigned long long* uc = &c->g->uid_count;
   unsigned int* tiles = reinterpret_cast<unsigned int*>(c->tiles64);
@@ -3666,7 +3710,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     ++c->launches;
     c->grid_valid = false;
   }
-  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g);
+  k_reduce<<<agent_blocks(c, 4), kThreads, 0, c->stream>>>(pos, c->g);
   sync_check(c, "k_reduce");
   k_finalize<<<1, 32, 0, c->stream>>>(c->g, FinArgs{c->cfg.fixed_box_length, 0, 1, 1, row_block_shift(), ~0ull,
                                                      ~0ull, ~0ull, 0, iteration});
@@ -3696,10 +3740,10 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   c->launches += 1;
   const int nxt = c->cur ^ 1;
   if (launch_counting) {  // Morton key + atomic slot, scan, scatter
-    k_mkey<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
+    k_mkey<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
     sync_check(c, "k_mkey");
     launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
-    k_scatter<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
+    k_scatter<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
                                                                  c->key, c->rank, c->g, c->cap,
                                                                  c->cfg.model == ABS_MODEL_PROLIFERATION,
                                                                  c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
@@ -3719,7 +3763,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
   unsigned long long* k2 = c->sort_k[1];
   unsigned int* i1 = c->sort_i[0];
   unsigned int* i2 = c->sort_i[1];
-  k_sort_keys<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->g, k1, i1, c->S[c->cur].skey,
+  k_sort_keys<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->g, k1, i1, c->S[c->cur].skey,
                                                                  exact_order ? 1 : 0);
   sync_check(c, "k_sort_keys");
   c->launches += 3;
@@ -3735,7 +3779,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     std::swap(k1, k2);
     std::swap(i1, i2);
   }
-  k_gather<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
+  k_gather<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], i1, c->g, c->cap,
                                                               c->cfg.model == ABS_MODEL_PROLIFERATION,
                                                               c->cfg.record_forces, 0, uses_ext(c->cfg));
                                                           sync_check(c, "k_gather");
@@ -4082,7 +4126,7 @@ int abs_gpu_set_grid_override(abs_gpu_ctx* c, const double* grid, const uint32_t
 int abs_gpu_local_bounds(abs_gpu_ctx* c, double* out7) {
   if (!c || !out7) return ABS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
-  k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
+  k_reduce<<<agent_blocks(c, 4), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
   ++c->launches;
   DevGrid h{};
   int rc = read_grid(c, &h);

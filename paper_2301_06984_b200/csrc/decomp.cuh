@@ -417,7 +417,7 @@ int decomp_setup(abs_gpu_ctx* c, int rank, int world) {
   if (adds_agents(c->cfg)) {
     int rc = abs_gpu_set_defer_commit(c, 1);
     if (rc) return rc;
-    k_keys_from_uids<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(c->S[c->cur], c->g);
+    k_keys_from_uids<<<agent_blocks(c), kThreads, 0, c->stream>>>(c->S[c->cur], c->g);
     ++c->launches;
   }
   return decomp_records(c, 1 << 16);
@@ -483,7 +483,7 @@ int decomp_step(abs_gpu_ctx* c) {
   int rc = ABS_OK;
   unsigned long long n = c->n;  // host mirror, current after every call that changes it
   if (!d->periodic) {  // 1. global grid (config 5 keeps its fixed periodic grid)
-    k_reduce<<<grid_blocks(c, c->cap), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
+    k_reduce<<<agent_blocks(c, 4), kThreads, 0, c->stream>>>(cur_pos(c), c->g);
     k_bounds_out<<<1, 1, 0, c->stream>>>(c->g, d->b7);
     c->launches += 2;
     if (W > 1 && d->tr.allreduce(d->tr.user, d->b7, 7, ABS_DT_F64_MAX, stream)) return tr_fail(c, "bounds all-reduce");

@@ -303,6 +303,10 @@ __device__ __forceinline__ void for_each_neighbor(const QGrid& g, const Pd* __re
 #endif
 constexpr int kMaxRows = ABS_MAX_ROWS;
 constexpr int kMaxContacts = ABS_MAX_CONTACTS;  // recorded possible contacts per agent (pass B)
+#ifndef ABS_SPILL_CONTACTS
+#define ABS_SPILL_CONTACTS 48
+#endif
+constexpr int kSpillContacts = ABS_SPILL_CONTACTS;  // further contacts kept per thread before a second walk
 constexpr int kForceThreads = 128;
 #ifndef ABS_BATCH
 #define ABS_BATCH 4
