@@ -125,7 +125,7 @@ CPU_STEPS = {"c1": 800, "c2": 60, "c3": 80, "c4": 30, "c5": 10, "rclust": 10, "r
 REF_BUILDERS = {"ref_clustering": "clustering", "ref_proliferation": "proliferation"}
 
 
-ENV_IDS = {"uniform_grid": 0, "brute_force": 1}
+ENV_IDS = {"uniform_grid": 0, "brute_force": 1, "kdtree": 2}
 
 
 def _ref_sim(wl_name, sample_n, threads, env="uniform_grid"):
@@ -160,7 +160,7 @@ BRUTE_SAMPLE, BRUTE_STEPS = 16384, 4  # O(N^2) reference: a smaller bounded samp
 def cpu_baseline(wl_name, steps=None, threads=None, env="uniform_grid"):
     """Reference CPU throughput on a bounded sample (population built untimed)."""
     threads = threads or os.cpu_count()
-    brute = env != "uniform_grid"
+    brute = env == "brute_force"
     steps = steps or (BRUTE_STEPS if brute else CPU_STEPS[wl_name])
     sim, kind, cores, wl = _ref_sim(wl_name, BRUTE_SAMPLE if brute else CPU_SAMPLE[wl_name], threads, env)
     agent_its = 0
@@ -192,7 +192,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count()
-    brute = args.env != "uniform_grid"
+    brute = args.env == "brute_force"
     n = BRUTE_SAMPLE if brute else (args.ref_sample or args.n or FULL_AGENTS[args.config])
     if args.config == "c2":
         n = None  # the proliferation run starts from its 16^3 lattice
@@ -582,8 +582,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="c4 under torchrun: 2^26 agents per GPU (weak) or in total (strong)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force"],
-                    help="EnvironmentKind (params.hpp:9); brute_force = the O(N^2) comparison baseline")
+    ap.add_argument("--env", default="uniform_grid", choices=["uniform_grid", "brute_force", "kdtree"],
+                    help="EnvironmentKind (params.hpp:9); brute_force / kdtree = the comparison baselines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

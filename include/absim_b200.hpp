@@ -62,7 +62,7 @@ struct SimulationParams {
   int model = ABS_MODEL_NONE;
   std::array<double, 8> model_params{};
   bool record_forces = true;
-  // EnvironmentKind (params.hpp:9): ABS_ENV_UNIFORM_GRID or ABS_ENV_BRUTE_FORCE
+  // EnvironmentKind (params.hpp:9): ABS_ENV_UNIFORM_GRID, ABS_ENV_BRUTE_FORCE or ABS_ENV_KD_TREE
   int environment_kind = ABS_ENV_UNIFORM_GRID;
 
   // SimulationParams::validate (params.cpp:44-72), hot-path fields
@@ -250,12 +250,13 @@ inline void UniformGrid::update() {
 }
 
 inline double UniformGrid::max_query_radius() const {
-  return sim_.params().environment_kind == ABS_ENV_BRUTE_FORCE ? std::numeric_limits<double>::infinity()
-                                                               : box_length();
+  return sim_.params().environment_kind != ABS_ENV_UNIFORM_GRID ? std::numeric_limits<double>::infinity()
+                                                                : box_length();
 }
 
 inline const char* UniformGrid::name() const {
-  return sim_.params().environment_kind == ABS_ENV_BRUTE_FORCE ? "brute_force" : "uniform_grid";
+  const int k = sim_.params().environment_kind;
+  return k == ABS_ENV_BRUTE_FORCE ? "brute_force" : (k == ABS_ENV_KD_TREE ? "kdtree" : "uniform_grid");
 }
 
 inline std::pair<std::array<double, 5>, std::array<std::uint32_t, 3>> UniformGrid::info() const {

@@ -89,6 +89,11 @@ extern "C" {
 #define ABS_ENV_BRUTE_FORCE 1   /* BruteForceEnvironment (environment.hpp:53-80): every agent is a
                                    candidate, no maximum query radius; O(N^2) comparison baseline.
                                    Sorting (params.cpp:52-55) and cell ids need the grid. */
+#define ABS_ENV_KD_TREE 2       /* KdTreeEnvironment (kdtree_env.cpp:8-86): a balanced kd-tree over the
+                                   agent array, rebuilt every environment update (median splits along the
+                                   widest axis, leaves of 32); the force query descends it with the exact
+                                   d2 <= r^2 at the leaves. Same query contract as brute force (no maximum
+                                   radius); the paper's grid-vs-tree comparison baseline. */
 
 typedef struct abs_gpu_ctx abs_gpu_ctx;
 

@@ -47,8 +47,9 @@ class GpuStep {
     c.fixed_box_length = p.fixed_box_length;
     c.sorting_frequency = p.sorting_frequency;  // Morton sort cadence, simulation.cpp:246-247
     c.detect_static_agents = p.detect_static_agents ? 1 : 0;
-    c.environment = p.environment_kind == absim::EnvironmentKind::kBruteForce ? ABS_ENV_BRUTE_FORCE
-                                                                                : ABS_ENV_UNIFORM_GRID;
+    c.environment = p.environment_kind == absim::EnvironmentKind::kBruteForce
+                        ? ABS_ENV_BRUTE_FORCE
+                        : (p.environment_kind == absim::EnvironmentKind::kKdTree ? ABS_ENV_KD_TREE : ABS_ENV_UNIFORM_GRID);
     c.model = m.model;
     for (int q = 0; q < 8; ++q) c.model_params[q] = m.params[q];
     c.record_forces = 1;

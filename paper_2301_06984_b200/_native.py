@@ -26,7 +26,7 @@ MODEL_NONE, MODEL_PROLIFERATION, MODEL_DRIVE, MODEL_GROW, MODEL_SIR = 0, 1, 2, 3
 MODEL_GROW_DIVIDE, MODEL_COHERE = 5, 6  # the reference's own models::GrowDivide / models::Cohere
 MODEL_GROW_DIVIDE_DIE = 7  # models::GrowDivide + AgentContext::remove_self with probability mp[3]
 FLAG_GHOST = 128
-ENV_UNIFORM_GRID, ENV_BRUTE_FORCE = 0, 1  # EnvironmentKind (params.hpp:9)
+ENV_UNIFORM_GRID, ENV_BRUTE_FORCE, ENV_KD_TREE = 0, 1, 2  # EnvironmentKind (params.hpp:9)
 
 # every symbol include/absim_gpu.h declares (checked by tests/test_abi.py)
 EXPORTS = [

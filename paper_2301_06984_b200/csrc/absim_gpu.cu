@@ -1129,21 +1129,21 @@ __global__ void __launch_bounds__(kThreads) k_static_pass(Soa S, Pd* __restrict_
 // the box walk when the device grid has no sub-bins), 2 box-lockstep walk
 // (bins == boxes, decided on the host).
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
-__global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox : kForceMinBlocksF32)
+__global__ void __launch_bounds__(kForceThreads, WALK >= 2 ? kForceMinBlocksBox : kForceMinBlocksF32)
     k_force(Soa S, const float4* __restrict__ pf, Pd* __restrict__ out, const DevGrid* gp, DevGrid* gw, const unsigned int* __restrict__ start,
             unsigned char* __restrict__ nv, unsigned char* __restrict__ nn, StepArgs a, unsigned long long cap,
             unsigned long long* __restrict__ st_parent, Pd* __restrict__ st_pd, double* __restrict__ st_vol,
             unsigned int* __restrict__ div_mark, unsigned int* __restrict__ st_tag,
-            const unsigned int* __restrict__ work, unsigned int* __restrict__ rmark) {
+            const unsigned int* __restrict__ work, unsigned int* __restrict__ rmark, KdView kd) {
   if (gp->err) return;
   __shared__ QGrid Q;
   extern __shared__ __align__(16) unsigned int force_smem[];
-  constexpr bool F32 = WALK == 1;
+  constexpr bool F32 = WALK == 1;  // 2: box-lockstep walk, 3: kd-tree query (ABS_ENV_KD_TREE)
   auto wj0 = reinterpret_cast<unsigned int (*)[kForceThreads]>(force_smem);
   // fp32 walk: 16-bit stream bounds, so its contact lists start after 1.5 row arrays
   auto wb16 = reinterpret_cast<unsigned short (*)[kForceThreads]>(force_smem + kMaxRows * kForceThreads);
   auto ovl = reinterpret_cast<unsigned int (*)[kForceThreads]>(
-      force_smem + (WALK == 2 ? 0 : kMaxRows + kMaxRows / 2) * kForceThreads);
+      force_smem + (WALK >= 2 ? 0 : kMaxRows + kMaxRows / 2) * kForceThreads);
   if (threadIdx.x == 0) Q = make_qgrid(*gp);
   __syncthreads();
   if (MODEL == ABS_MODEL_COHERE && !a.brute && a.mp[0] * a.mp[0] > Q.box * Q.box * (1.0 + 1e-12)) {
@@ -1159,7 +1159,7 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
   const unsigned long long n = work ? gp->work_n : gp->n;
   const double dmax = gp->dmax;
   // bins are the reference boxes
-  const bool box_mode = WALK == 2 || (Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1);
+  const bool box_mode = WALK >= 2 || (Q.B[0] == 1 && Q.B[1] == 1 && Q.B[2] == 1);
   unsigned long long n_eval = 0, n_skip = 0;
   // Persistent warps sweep 32-agent chunks in a static warp-strided order:
   // the resident warps cover a contiguous window of the agent array (cell
@@ -1194,10 +1194,9 @@ __global__ void __launch_bounds__(kForceThreads, WALK == 2 ? kForceMinBlocksBox 
       dg = agent_step<MODEL, STATIC, RECORD>(
           S, out, i, me, dmax, nv, nn, a, cap, &ovl[0][threadIdx.x], kForceThreads, n_eval, n_skip,
           [&](double r, double r2, auto&& visit) {
-            for_each_neighbor_box(Q, S.pd, start, self, me.x, me.y, me.z, r2,
-                                  [&](unsigned int j, const Pd& q, double, double, double, double d2) {
-                                    visit(j, q, d2);
-                                  });
+            auto v6 = [&](unsigned int j, const Pd& q, double, double, double, double d2) { visit(j, q, d2); };
+            if constexpr (WALK == 3) for_each_neighbor_kd(kd, S.pd, self, me.x, me.y, me.z, r, r2, v6);
+            else for_each_neighbor_box(Q, S.pd, start, self, me.x, me.y, me.z, r2, v6);
           },
           [&](unsigned int j) { return load_pd(S.pd + j); }, [&](unsigned int j) { return S.uid[j]; }, 0.0f,
           query);
@@ -2073,7 +2072,7 @@ __global__ void k_cell_ids(const Pd* __restrict__ pos, const DevGrid* g, unsigne
 }
 
 __global__ void k_nbr_count(const Pd* __restrict__ pd, const DevGrid* g,
-                            const unsigned int* __restrict__ start, unsigned long long* cnt) {
+                            const unsigned int* __restrict__ start, unsigned long long* cnt, KdView kd) {
   const DevGrid G = *g;
   const QGrid Q = make_qgrid(G);
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
@@ -2081,15 +2080,16 @@ __global__ void k_nbr_count(const Pd* __restrict__ pd, const DevGrid* g,
     const Pd me = load_pd(pd + i);
     const double r = 0.5 * (me.d + G.dmax);
     unsigned long long c = 0;
-    for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
-                      [&](unsigned int, const Pd&, double, double, double, double) { ++c; });
+    auto count = [&](unsigned int, const Pd&, double, double, double, double) { ++c; };
+    if (kd.n) for_each_neighbor_kd(kd, pd, (unsigned int)i, me.x, me.y, me.z, r, r * r, count);
+    else for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r, count);
     cnt[i] = c;
   }
 }
 
 __global__ void k_nbr_fill(const Pd* __restrict__ pd, const unsigned long long* __restrict__ uid,
                            const DevGrid* g, const unsigned int* __restrict__ start,
-                           const unsigned long long* __restrict__ off, unsigned long long* out) {
+                           const unsigned long long* __restrict__ off, unsigned long long* out, KdView kd) {
   const DevGrid G = *g;
   const QGrid Q = make_qgrid(G);
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < G.n;
@@ -2097,8 +2097,9 @@ __global__ void k_nbr_fill(const Pd* __restrict__ pd, const unsigned long long* 
     const Pd me = load_pd(pd + i);
     const double r = 0.5 * (me.d + G.dmax);
     unsigned long long w = off[i];
-    for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r,
-                      [&](unsigned int j, const Pd&, double, double, double, double) { out[w++] = uid[j]; });
+    auto put = [&](unsigned int j, const Pd&, double, double, double, double) { out[w++] = uid[j]; };
+    if (kd.n) for_each_neighbor_kd(kd, pd, (unsigned int)i, me.x, me.y, me.z, r, r * r, put);
+    else for_each_neighbor(Q, pd, start, (unsigned int)i, me.x, me.y, me.z, r, r * r, put);
     // insertion sort of this agent's uid list
     const unsigned long long b = off[i], e = off[i + 1];
     for (unsigned long long p = b + 1; p < e; ++p) {
@@ -2287,7 +2288,7 @@ __global__ void k_radix_scatter(const unsigned long long* __restrict__ key, cons
 
 __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const unsigned int* __restrict__ perm,
                          const DevGrid* g, unsigned long long cap, int carry_vol, int carry_force,
-                         int only_sort_mode = -1, int carry_ext = 1) {
+                         int only_sort_mode = -1, int carry_ext = 1, int renumber_keys = 1) {
   if (g->err) return;
   if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
@@ -2307,7 +2308,8 @@ __global__ void k_gather(const Pd* __restrict__ pos, Soa src, Soa dst, const uns
       dst.force[cap + j] = src.force[cap + i];
       dst.force[2 * cap + j] = src.force[2 * cap + i];
     }
-    dst.skey[j] = static_cast<unsigned int>(j);  // sort_and_balance's new storage slot
+    // sort_and_balance's new storage slot; a gather that is not the reference's sort carries the key
+    dst.skey[j] = renumber_keys ? static_cast<unsigned int>(j) : src.skey[i];
     if (carry_ext) {
       dst.tag[j] = src.tag[i];
       dst.rngc[j] = src.rngc[i];
@@ -2518,6 +2520,13 @@ struct abs_gpu_ctx {
   int cur = 0;
   Pd* newpd = nullptr;
   float4* pf = nullptr;  // fp32 copy of pd relative to the grid origin (candidate classification)
+  // kd-tree environment (kdtree.cuh): per-node split axis and bounds, heap order
+  unsigned char* kd_axis = nullptr;
+  double* kd_lmax = nullptr;
+  double* kd_rmin = nullptr;
+  unsigned long long* kd_bbox = nullptr;
+  unsigned long long kd_nodes_cap = 0, kd_n = 0;
+  bool kd_valid = false;
   bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
   bool grid_valid = false; // `start` holds a scanned cell table for S[cur]
 
@@ -2646,7 +2655,17 @@ bool uses_ext(const abs_gpu_config& cfg) {
 }
 
 // BruteForceEnvironment (environment.hpp:53-80) instead of the grid.
-int brute_env(const abs_gpu_ctx* c) { return c->cfg.environment == ABS_ENV_BRUTE_FORCE ? 1 : 0; }
+// The kd-tree environment keeps the brute-force single box underneath (static
+// marking, new-agent marking and behaviour queries walk it) and answers the
+// force query through the tree.
+bool kd_env(const abs_gpu_ctx* c) { return c->cfg.environment == ABS_ENV_KD_TREE; }
+int brute_env(const abs_gpu_ctx* c) {
+  return c->cfg.environment == ABS_ENV_BRUTE_FORCE || c->cfg.environment == ABS_ENV_KD_TREE ? 1 : 0;
+}
+KdView kd_view(const abs_gpu_ctx* c) {
+  if (!kd_env(c) || !c->kd_valid || !c->grid_valid) return KdView{nullptr, nullptr, nullptr, 0u};
+  return KdView{c->kd_axis, c->kd_lmax, c->kd_rmin, static_cast<unsigned int>(c->kd_n)};
+}
 
 int grid_blocks(const abs_gpu_ctx* c, unsigned long long work) {
   const unsigned long long b = (work + kThreads - 1) / kThreads;
@@ -2936,6 +2955,38 @@ bool uses_f32_walk(const abs_gpu_ctx* c) {
 
 void launch_commit(abs_gpu_ctx* c);
 
+constexpr unsigned long long kSortChunk = 4096;
+
+// Radix-sort scratch of the Morton sort and the kd-tree build, sized by the capacity.
+int ensure_sort_scratch(abs_gpu_ctx* c) {
+  if (c->sort_cap == c->cap) return ABS_OK;
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(c->sort_k[b]);
+    cudaFree(c->sort_i[b]);
+    c->sort_k[b] = nullptr;
+    c->sort_i[b] = nullptr;
+  }
+  cudaFree(c->sort_hist); cudaFree(c->sort_tiles); cudaFree(c->sort_hlen);
+  c->sort_hist = nullptr;
+  c->sort_tiles = nullptr;
+  c->sort_hlen = nullptr;
+  c->sort_cap = 0;
+  const unsigned long long blocks = (c->cap + kSortChunk - 1) / kSortChunk;
+  for (int b = 0; b < 2; ++b) {
+    CK(dalloc(&c->sort_k[b], c->cap));
+    CK(dalloc(&c->sort_i[b], c->cap));
+  }
+  const unsigned long long hlen = 256ull * blocks;
+  CK(dalloc(&c->sort_hist, hlen + 1));
+  CK(dalloc(&c->sort_tiles, hlen / kScanTile + 2));
+  CK(dalloc(&c->sort_hlen, 1));
+  k_set_u64<<<1, 1, 0, c->stream>>>(c->sort_hlen, hlen);  // a kernel: capturable in a graph
+  c->sort_cap = c->cap;
+  return ABS_OK;
+}
+
+#include "kdtree.cuh"
+
 // Environment::update: reduce, size, bin, scan, scatter into S[cur^1].
 void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add, bool in_step = false,
                        int list_mode = 0, double skin = 0.0) {
@@ -2979,6 +3030,7 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->pos_in_new = false;
   c->grid_valid = true;
   c->list_valid = false;  // storage re-ordered (a list build follows in list mode 2)
+  if (kd_env(c) && kd_build(c) != ABS_OK) c->kd_valid = false;  // KdTreeEnvironment::update on top of the single box
 }
 
 
@@ -2995,7 +3047,7 @@ static_assert(kMaxRows % 2 == 0, "16-bit bound array packs two rows per word");
 template <int MODEL, bool STATIC, bool RECORD, int WALK>
 void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   static int blocks = 0;  // per template instance
-  constexpr int smem = WALK == 2 ? kForceSmemBox : kForceSmemF32;
+  constexpr int smem = WALK >= 2 ? kForceSmemBox : kForceSmemF32;
   if (!blocks) {
     cudaFuncSetAttribute(k_force<MODEL, STATIC, RECORD, WALK>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     blocks = force_blocks(c, k_force<MODEL, STATIC, RECORD, WALK>, smem);
@@ -3011,13 +3063,14 @@ void launch_gather_f(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
   }
   k_force<MODEL, STATIC, RECORD, WALK><<<blocks, kForceThreads, smem, c->stream>>>(
       S, c->pf, c->newpd, c->g, c->g, c->start, c->nv, c->nn, a, c->cap, c->st_parent, c->st_pd, c->st_vol, c->div_mark,
-      c->st_tag, work, c->rmark);
+      c->st_tag, work, c->rmark, kd_view(c));
   sync_check(c, "k_force");
 }
 
 template <int MODEL, bool STATIC, bool RECORD>
 void launch_gather(abs_gpu_ctx* c, Soa& S, const StepArgs& a) {
-  if (bins_x(c) == 1u && bins_yz(c) == 1u) launch_gather_f<MODEL, STATIC, RECORD, 2>(c, S, a);
+  if (kd_env(c)) launch_gather_f<MODEL, STATIC, RECORD, 3>(c, S, a);
+  else if (bins_x(c) == 1u && bins_yz(c) == 1u) launch_gather_f<MODEL, STATIC, RECORD, 2>(c, S, a);
   else launch_gather_f<MODEL, STATIC, RECORD, 1>(c, S, a);
 }
 
@@ -3446,7 +3499,8 @@ int abs_gpu_create(const abs_gpu_config* cfg, int device, abs_gpu_ctx** out) {
   if (!(cfg->max_displacement > 0.0)) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "max_displacement must be > 0");
   if (cfg->force_threshold < 0.0) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "force_threshold must be >= 0");
   if (cfg->model < 0 || cfg->model > 7) return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown model");
-  if (cfg->environment != ABS_ENV_UNIFORM_GRID && cfg->environment != ABS_ENV_BRUTE_FORCE)
+  if (cfg->environment != ABS_ENV_UNIFORM_GRID && cfg->environment != ABS_ENV_BRUTE_FORCE &&
+      cfg->environment != ABS_ENV_KD_TREE)
     return set_err(nullptr, ABS_ERR_INVALID_ARGUMENT, "unknown environment kind");
   // params.cpp:52-55
   if (cfg->sorting_frequency > 0 && cfg->environment != ABS_ENV_UNIFORM_GRID)
@@ -3518,6 +3572,7 @@ int abs_gpu_destroy(abs_gpu_ctx* c) {
   cudaFree(c->tiles); cudaFree(c->tiles64); cudaFree(c->scan_state); cudaFree(c->nv); cudaFree(c->nn);
   cudaFree(c->xcounts); cudaFree(c->holes); cudaFree(c->nl); cudaFree(c->nl_cnt); cudaFree(c->evc);
   cudaFree(c->pf2); cudaFree(c->nl_ct); cudaFree(c->nl_nct); cudaFree(c->ctiles);
+  cudaFree(c->kd_axis); cudaFree(c->kd_lmax); cudaFree(c->kd_rmin); cudaFree(c->kd_bbox);
   if (c->hxcounts) cudaFreeHost(c->hxcounts);
   cudaFree(c->st_parent);
   cudaFree(c->st_pd); cudaFree(c->st_vol); cudaFree(c->st_tag); cudaFree(c->div_mark); cudaFree(c->div_mark_g);
@@ -3679,8 +3734,6 @@ static void free_sort_scratch(abs_gpu_ctx* c) {
   c->sort_cap = 0;
 }
 
-constexpr unsigned long long kSortChunk = 4096;
-
 // sort_and_balance (sort_balance.cpp:22-148) on the device, stream-ordered and
 // without host synchronisation: grid of the current state (no re-binning),
 // Morton-code keys in descending index order, 8 8-bit LSD pass slots of which
@@ -3688,19 +3741,9 @@ constexpr unsigned long long kSortChunk = 4096;
 // inside the iteration loop (sorting_frequency, simulation.cpp:246-247).
 static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_order) {
   if (c) c->list_valid = false;  // storage order changes (neighbour lists index it)
-  if (c->sort_cap != c->cap) {
-    free_sort_scratch(c);
-    const unsigned long long blocks = (c->cap + kSortChunk - 1) / kSortChunk;
-    for (int b = 0; b < 2; ++b) {
-      CK(dalloc(&c->sort_k[b], c->cap));
-      CK(dalloc(&c->sort_i[b], c->cap));
-    }
-    const unsigned long long hlen = 256ull * blocks;
-    CK(dalloc(&c->sort_hist, hlen + 1));
-    CK(dalloc(&c->sort_tiles, hlen / kScanTile + 2));
-    CK(dalloc(&c->sort_hlen, 1));
-    k_set_u64<<<1, 1, 0, c->stream>>>(c->sort_hlen, hlen);  // a kernel: capturable in a graph
-    c->sort_cap = c->cap;
+  {
+    const int rc = ensure_sort_scratch(c);
+    if (rc) return rc;
   }
   const Pd* pos = cur_pos(c);
   sync_check(c, "k_set_u64");
@@ -3795,7 +3838,7 @@ constexpr double kCrowdedAgentsPerBox = 6.0;  // c1 2.9, c3 ~1, c4 ~10 (sub-binn
 // per-launch timing events are on.
 bool use_graphs(const abs_gpu_ctx* c) {
   static const bool on = env_flag("ABSIM_GRAPHS", true);
-  return on && !c->graphs_off && !c->timing;
+  return on && !c->graphs_off && !c->timing && !kd_env(c);  // the kd build sizes its launches on the host
 }
 
 int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
@@ -3809,7 +3852,8 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
   // Launch in chunks; a chunk whose finalize asked for more bins/capacity is
   // rolled back to the failed iteration (no kernel touched state after it).
   unsigned long long done = 0;
-  const unsigned long long chunk = 32;
+  // (the kd-tree build reads the agent count on the host: one iteration per chunk)
+  const unsigned long long chunk = kd_env(c) ? 1 : 32;
   sync_check(c, "simulate entry");
   // neighbour lists: storage for this population, allocated
   // outside any graph capture
@@ -4526,7 +4570,7 @@ int abs_gpu_grid_info(abs_gpu_ctx* c, double* grid, uint32_t* dims) {
 }
 
 int abs_gpu_cell_ids(abs_gpu_ctx* c, uint64_t* out) {
-  if (c && brute_env(c)) return set_err(c, ABS_ERR_STATE, "the brute_force environment has no cells");
+  if (c && brute_env(c)) return set_err(c, ABS_ERR_STATE, "the brute_force and kd_tree environments have no cells");
   if (!c || !out) return ABS_ERR_INVALID_ARGUMENT;
   if (!c->grid_valid) return set_err(c, ABS_ERR_STATE, "cell ids require abs_gpu_env_update");
   DevGrid h{};
@@ -4555,7 +4599,7 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
   CK(dalloc(&t64, (n + 1) / kScanTile + 2));
   CK(cudaMemcpyAsync(len, &n, 8, cudaMemcpyHostToDevice, c->stream));
   const Pd* pd = c->S[c->cur].pd;
-  k_nbr_count<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->g, c->start, cnt);
+  k_nbr_count<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->g, c->start, cnt, kd_view(c));
   ++c->launches;
   launch_scan<unsigned long long>(c, cnt, len, n + 1, t64, nullptr);
   CK(cudaMemcpyAsync(offsets, cnt, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -4567,7 +4611,8 @@ int abs_gpu_neighbors(abs_gpu_ctx* c, uint64_t* offsets, uint64_t* uids, uint64_
     return uids ? set_err(c, ABS_ERR_CAPACITY, "neighbour buffer too small") : ABS_OK;
   }
   CK(dalloc(&out, tot));
-  k_nbr_fill<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->S[c->cur].uid, c->g, c->start, cnt, out);
+  k_nbr_fill<<<grid_blocks(c, n), kThreads, 0, c->stream>>>(pd, c->S[c->cur].uid, c->g, c->start, cnt, out,
+                                                           kd_view(c));
   ++c->launches;
   CK(cudaMemcpyAsync(uids, out, tot * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));

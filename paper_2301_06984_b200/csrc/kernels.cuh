@@ -349,6 +349,73 @@ __device__ __forceinline__ void for_each_neighbor_box(const QGrid& g, const Pd* 
 }
 
 
+// ------------------------------------------------------------ kd-tree environment
+// KdTreeEnvironment (kdtree_env.cpp:8-86) on the device: a balanced kd-tree
+// over the agent array itself. The array is permuted so that every node owns
+// a contiguous range [begin, end), split at its midpoint index along the
+// widest axis of the range's bounding box (kdtree_env.cpp:31-50); ranges are
+// implicit (they follow from n by the midpoint rule), nodes are addressed in
+// heap order (children 2 id + 1, 2 id + 2) and store their split axis and the
+// two bounds left_max >= every left coordinate, right_min <= every right
+// coordinate. A range of <= kKdLeaf agents is a leaf (kLeafSize). The query
+// (kdtree_env.cpp:55-84) descends with an explicit stack and applies the
+// exact fp64 d2 <= r^2 to every agent of a reached leaf — the brute-force
+// query contract, no maximum radius.
+constexpr unsigned int kKdLeaf = 32;
+struct KdView {
+  const unsigned char* axis;
+  const double* lmax;
+  const double* rmin;
+  unsigned int n;  // 0: no tree
+};
+
+template <class F>
+__device__ __forceinline__ void for_each_neighbor_kd(const KdView& t, const Pd* __restrict__ pd, unsigned int self,
+                                                     double cx, double cy, double cz, double r, double r2,
+                                                     F&& visit) {
+  if (t.n == 0) return;
+  unsigned int sid[40], sb[40], se[40];
+  int top = 1;
+  sid[0] = 0;
+  sb[0] = 0;
+  se[0] = t.n;
+  const double rr = r * (1.0 + 1e-12);  // pruning is conservative; membership is decided by d2 <= r2
+  while (top > 0) {
+    --top;
+    const unsigned int id = sid[top], b = sb[top], e = se[top];
+    if (e - b <= kKdLeaf) {
+      for (unsigned int j = b; j < e; j += kBatch) {
+        Pd q[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) q[u] = load_pd(pd + min(j + u, e - 1));
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const unsigned int jj = j + u;
+          const double dx = cx - q[u].x, dy = cy - q[u].y, dz = cz - q[u].z;
+          const double d2 = (dx * dx + dy * dy) + dz * dz;
+          if (jj < e && jj != self && d2 <= r2) visit(jj, q[u], dx, dy, dz, d2);
+        }
+      }
+      continue;
+    }
+    const unsigned int mid = b + (e - b) / 2;
+    const unsigned int ax = t.axis[id];
+    const double c = ax == 0 ? cx : (ax == 1 ? cy : cz);
+    if (__ldg(t.rmin + id) - c <= rr) {  // right child (kdtree_env.cpp:82)
+      sid[top] = 2 * id + 2;
+      sb[top] = mid;
+      se[top] = e;
+      ++top;
+    }
+    if (c - __ldg(t.lmax + id) <= rr) {  // left child (kdtree_env.cpp:81)
+      sid[top] = 2 * id + 1;
+      sb[top] = b;
+      se[top] = mid;
+      ++top;
+    }
+  }
+}
+
 // Flat-stream, fp32-classified walk used by the force kernel. Candidates are read
 // from `pf` (float4 {x, y, z, d} relative to the grid origin, 16 B) and
 // classified against the exact fp64 test with a proven margin: the fp32

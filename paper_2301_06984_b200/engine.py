@@ -41,7 +41,7 @@ def peak_rss_bytes() -> int:
     return 0
 
 
-ENVIRONMENTS = {"uniform_grid": N.ENV_UNIFORM_GRID, "brute_force": N.ENV_BRUTE_FORCE}
+ENVIRONMENTS = {"uniform_grid": N.ENV_UNIFORM_GRID, "brute_force": N.ENV_BRUTE_FORCE, "kdtree": N.ENV_KD_TREE, "kd_tree": N.ENV_KD_TREE}
 
 
 @dataclass
@@ -61,7 +61,7 @@ class SimulationParams:
     record_forces: bool = True
     bins_per_box: int = 0      # sub-bins per box edge along y, z (0 = auto)
     bins_per_box_x: int = 0    # sub-bins per box edge along x (0 = auto)
-    # EnvironmentKind (params.hpp:9): "uniform_grid" or "brute_force"
+    # EnvironmentKind (params.hpp:9): "uniform_grid", "brute_force" or "kdtree" (params.cpp:7-30 names)
     environment: str = "uniform_grid"
     # per-agent candidate lists between environment rebuilds:
     # True = auto (used when the path allows it and a build pays off), False =
