@@ -3900,8 +3900,14 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
       if (list_mode_ok(c) && c->nl) {
         const double skin = list_skin(c);
         const bool usable = c->list_valid && !sorts;
-        const bool pays = c->cfg.neighbor_list > 0 || c->pred_rate <= 0.0 ||
-                          skin >= 2.0 * list_min_steps() * c->pred_rate;
+        // life of a list built now: until the displacement check fails or the next Morton sort
+        // (builds at iterations 8 or 9 of a 10-iteration sort period do not pay: walk instead)
+        double life = c->pred_rate > 0.0 ? skin / (2.0 * c->pred_rate) : 1e18;
+        if (c->cfg.sorting_frequency > 0) {
+          const unsigned long long sf = static_cast<unsigned long long>(c->cfg.sorting_frequency);
+          life = std::min(life, static_cast<double>(sf - it % sf));
+        }
+        const bool pays = c->cfg.neighbor_list > 0 || c->pred_rate <= 0.0 || life >= list_min_steps();
         if (usable && (2.0 * c->pred_acc <= skin || remaining < 2)) {
           kind = 1;
           c->pred_acc += c->pred_rate;
