@@ -2527,6 +2527,7 @@ struct abs_gpu_ctx {
   unsigned long long* kd_bbox = nullptr;
   unsigned long long kd_nodes_cap = 0, kd_n = 0;
   bool kd_valid = false;
+  bool kd_failed = false;  // the last build could not allocate its node arrays
   bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
   bool grid_valid = false; // `start` holds a scanned cell table for S[cur]
 
@@ -3030,7 +3031,10 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   c->pos_in_new = false;
   c->grid_valid = true;
   c->list_valid = false;  // storage re-ordered (a list build follows in list mode 2)
-  if (kd_env(c) && kd_build(c) != ABS_OK) c->kd_valid = false;  // KdTreeEnvironment::update on top of the single box
+  if (kd_env(c) && kd_build(c) != ABS_OK) {  // KdTreeEnvironment::update on top of the single box
+    c->kd_valid = false;
+    c->kd_failed = true;  // reported by the caller (an empty tree would silently find no neighbours)
+  }
 }
 
 
@@ -3975,6 +3979,11 @@ int abs_gpu_simulate(abs_gpu_ctx* c, uint64_t iterations) {
     }
     cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) return set_err(c, ABS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(le));
+    if (c->kd_failed) {
+      c->kd_failed = false;
+      cudaStreamSynchronize(c->stream);
+      return set_err(c, ABS_ERR_CAPACITY, "kd-tree environment: the tree build failed (device memory)");
+    }
     DevGrid h{};
     int rc = read_grid(c, &h);
     if (rc) return rc;
@@ -4539,6 +4548,11 @@ int abs_gpu_env_update(abs_gpu_ctx* c) {
     const int cur0 = c->cur;
     const bool pin0 = c->pos_in_new;
     launch_env_update(c, c->iteration, 0);
+    if (c->kd_failed) {
+      c->kd_failed = false;
+      cudaStreamSynchronize(c->stream);
+      return set_err(c, ABS_ERR_CAPACITY, "kd-tree environment: the tree build failed (device memory)");
+    }
     DevGrid h{};
     int rc = read_grid(c, &h);
     if (rc) return rc;

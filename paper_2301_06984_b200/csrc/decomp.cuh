@@ -411,6 +411,8 @@ int decomp_setup(abs_gpu_ctx* c, int rank, int world) {
   CK(cudaHostAlloc(reinterpret_cast<void**>(&d->hxc), 6 * sizeof(unsigned long long), cudaHostAllocDefault));
   if (removes_agents(c->cfg))
     return set_err(c, ABS_ERR_INVALID_ARGUMENT, "models that remove agents run in one domain");
+  if (c->cfg.environment != ABS_ENV_UNIFORM_GRID)
+    return set_err(c, ABS_ERR_INVALID_ARGUMENT, "the slab decomposition needs the uniform_grid environment");
   if (c->cfg.sorting_frequency > 0 && adds_agents(c->cfg))
     return set_err(c, ABS_ERR_INVALID_ARGUMENT,
                    "multi-domain additions with Morton sorting: the reference's global storage order is not tracked");
