@@ -26,9 +26,20 @@
  *   abs_gpu_set_defer_commit / abs_gpu_division_marks / abs_gpu_commit
  *                           CommitBuffer::commit additions, split so ranks
  *                           agree on daughter uids                          commit.cpp:186-222, simulation.cpp:64-91
+ *   abs_gpu_download_storage_keys
+ *                           each agent's slot in ResourceManager's agent
+ *                           vector (the order for_each_agent walks and that
+ *                           decides daughter uids and survivor slots)        resource_manager.hpp:19-101
+ *   abs_gpu_create with environment = ABS_ENV_BRUTE_FORCE / ABS_ENV_KD_TREE
+ *                           make_environment(kBruteForce / kKdTree)          simulation.cpp:40-53, environment.hpp:53-80,
+ *                                                                            kdtree_env.cpp:8-86
+ *   abs_gpu_comm_init / abs_gpu_comm_set_transport / abs_gpu_simulate_decomposed / abs_gpu_decomp_info
+ *                           the reference's per-domain partition of one
+ *                           address space (ResourceManager domains, box-aligned
+ *                           shares) as one z slab per GPU                    resource_manager.hpp:95, sort_balance.cpp:61-77
  *   abs_gpu_export_layers / abs_gpu_import / abs_gpu_drop_ghosts / abs_gpu_set_grid_override
- *                           multi-domain slab exchange (no reference
- *                           counterpart: the reference is one process)
+ *                           the same slab exchange step by step, for hosts
+ *                           that bring their own transport
  *
  * Conventions: int status (ABS_OK == 0), no exceptions across the ABI, one
  * host thread per context, device memory owned by the context, host buffers
