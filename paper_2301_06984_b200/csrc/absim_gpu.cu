@@ -1627,6 +1627,8 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
   const unsigned long long rec = static_cast<unsigned long long>(a.mp[3]);
   const double box = g->box, r2 = r * r;
   const unsigned int D0 = g->dims[0], D1 = g->dims[1], D2 = g->dims[2], ysh = g->ysh;
+  __shared__ unsigned int woff[18][kThreads];
+  __shared__ unsigned short wbnd[18][kThreads];
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const Pd me = load_pd(S.pd + i);
@@ -1666,14 +1668,55 @@ __global__ void __launch_bounds__(kThreads) k_sir(Soa S, Pd* __restrict__ out, c
         lo[2 * q + 1] = split ? __ldg(start + row + x0b) : 0u;
         hi[2 * q + 1] = split ? __ldg(start + row + x1b) : 0u;
       }
-#pragma unroll 1
+      auto infected_within = [&](unsigned int j) {
+        const Pd q = load_pd(S.pd + j);
+        const double ex = abs_min_image(me.x - q.x, L), ey = abs_min_image(me.y - q.y, L),
+                     ez = abs_min_image(me.z - q.z, L);
+        return (ex * ex + ey * ey) + ez * ez <= r2;
+      };
+      // The non-empty windows become ONE candidate stream per lane (offset,
+      // cumulative bound in shared memory), walked four states at a time: a
+      // warp then runs for its longest stream, not for the sum over windows of
+      // the longest window (the nested loop ran at 16 of 32 lanes active).
+      unsigned int total = 0;
+      int nw = 0;
+#pragma unroll
       for (int w = 0; w < 18; ++w) {
-        for (unsigned int j = lo[w]; j < hi[w]; ++j) {
-          if (j == i || S.beh[j] != ABS_SIR_I) continue;
-          const Pd q = load_pd(S.pd + j);
-          const double ex = abs_min_image(me.x - q.x, L), ey = abs_min_image(me.y - q.y, L),
-                       ez = abs_min_image(me.z - q.z, L);
-          if ((ex * ex + ey * ey) + ez * ez <= r2) ++k;
+        if (hi[w] > lo[w]) {
+          woff[nw][threadIdx.x] = lo[w] - total;
+          total += hi[w] - lo[w];
+          wbnd[nw][threadIdx.x] = static_cast<unsigned short>(total);
+          ++nw;
+        }
+      }
+      if (total > 0xFFFFu) {  // stream bounds would not fit 16 bits: nested walk
+#pragma unroll
+        for (int w = 0; w < 18; ++w)
+          for (unsigned int j = lo[w]; j < hi[w]; ++j)
+            if (j != i && S.beh[j] == ABS_SIR_I && infected_within(j)) ++k;
+      } else if (nw > 0) {
+        int wk = 0;
+        unsigned int off = woff[0][threadIdx.x], bnd = wbnd[0][threadIdx.x];
+        for (unsigned int p = 0; p < total;) {
+          unsigned int idx[4];
+          bool val[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            val[u] = p < total;
+            idx[u] = val[u] ? p + off : static_cast<unsigned int>(i);
+            ++p;
+            if (p == bnd) {
+              wk = min(wk + 1, nw - 1);
+              off = woff[wk][threadIdx.x];
+              bnd = wbnd[wk][threadIdx.x];
+            }
+          }
+          unsigned char sj[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sj[u] = S.beh[idx[u]];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (val[u] && idx[u] != i && sj[u] == ABS_SIR_I && infected_within(idx[u])) ++k;
         }
       }
       if (k > 0 && abs_rng_word(a.seed, S.uid[i], ABS_RNG_SIR_INFECT(a.iteration)) < abs_sir_threshold(prob, k)) {
