@@ -488,13 +488,24 @@ __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restr
   if (t == 0 && threadIdx.x == 0) tickets[(epoch + 1) & 1u] = 0;
   const unsigned long long base = t * kScanTile;
   constexpr int per = kScanTile / kThreads;
+  static_assert(per == 8, "the full-tile path moves two uint4 per thread");
   unsigned int v[per];
   unsigned int sum = 0;
+  const bool full = base + kScanTile <= len;  // whole tile in range: 128-bit accesses (the table is 256-B aligned)
+  if (full) {
+    const uint4* src = reinterpret_cast<const uint4*>(data + base) + threadIdx.x * 2;
+    const uint4 a = src[0], b = src[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 #pragma unroll
-  for (int q = 0; q < per; ++q) {
-    const unsigned long long i = base + threadIdx.x * per + q;
-    v[q] = i < len ? data[i] : 0u;
-    sum += v[q];
+    for (int q = 0; q < per; ++q) sum += v[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+      const unsigned long long i = base + threadIdx.x * per + q;
+      v[q] = i < len ? data[i] : 0u;
+      sum += v[q];
+    }
   }
   unsigned int run = block_excl_scan(sum, &tot);
   // tile word: epoch (30 bits) | inclusive/aggregate flags (2 bits) | value (32
@@ -531,11 +542,23 @@ __global__ void __launch_bounds__(kThreads) k_scan_onepass(unsigned int* __restr
   }
   __syncthreads();
   run += static_cast<unsigned int>(s_prefix);
+  if (full) {
+    unsigned int o[per];
 #pragma unroll
-  for (int q = 0; q < per; ++q) {
-    const unsigned long long i = base + threadIdx.x * per + q;
-    if (i < len) data[i] = run;
-    run += v[q];
+    for (int q = 0; q < per; ++q) {
+      o[q] = run;
+      run += v[q];
+    }
+    uint4* dst = reinterpret_cast<uint4*>(data + base) + threadIdx.x * 2;
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+      const unsigned long long i = base + threadIdx.x * per + q;
+      if (i < len) data[i] = run;
+      run += v[q];
+    }
   }
   if (t == ntiles - 1 && threadIdx.x == kThreads - 1) data[len] = run;
 }
