@@ -596,14 +596,18 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
                                                       const DevGrid* g, unsigned long long cap,
                                                       int carry_vol, int carry_force, int write_pf,
                                                       int only_sort_mode = -1, int carry_ext = 0,
-                                                      int carry_partners = 1, int carry_beh = 1) {
+                                                      int carry_partners = 1, int carry_beh = 1,
+                                                      unsigned int* __restrict__ mark_list = nullptr,
+                                                      unsigned long long* __restrict__ mark_n = nullptr) {
   if (g->err) return;
   if (only_sort_mode >= 0 && static_cast<int>(g->sort_mode) != only_sort_mode) return;
   const unsigned long long n = g->n;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   const double ox = g->origin[0], oy = g->origin[1], oz = g->origin[2];
-  for (unsigned long long i0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i0 < n;
-       i0 += stride * kScatterBatch) {
+  // block-uniform trip count (the tail is handled per element): the mark-list
+  // ballots below need whole warps
+  for (unsigned long long b0 = blockIdx.x * (unsigned long long)blockDim.x; b0 < n; b0 += stride * kScatterBatch) {
+    const unsigned long long i0 = b0 + threadIdx.x;
     unsigned int j[kScatterBatch];
     Pd p[kScatterBatch];
     unsigned long long u[kScatterBatch];
@@ -647,6 +651,23 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
         dst.rngc[jj] = src.rngc[i];
       }
       dst.skey[jj] = src.skey[i];
+    }
+    // static detection: the agents that moved, grew or were added last
+    // iteration mark their neighbours (k_mark); they are listed here, by their
+    // new slot, instead of in a pass of their own over every agent's flags
+    if (mark_list) {
+#pragma unroll
+      for (int b = 0; b < kScatterBatch; ++b) {
+        const unsigned long long i = i0 + b * stride;
+        const bool act = i < n && (fl[b] & (ABS_FLAG_MOVED | ABS_FLAG_GREW | ABS_FLAG_NEWLY_ADDED));
+        const unsigned int ballot = __ballot_sync(0xffffffffu, act);
+        if (!ballot) continue;
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(mark_n, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act) mark_list[base + __popc(ballot & ((1u << lane) - 1u))] = j[b];
+      }
     }
   }
 }
@@ -2592,6 +2613,7 @@ struct abs_gpu_ctx {
   double* kd_rmin = nullptr;
   unsigned long long* kd_bbox = nullptr;
   unsigned long long kd_nodes_cap = 0, kd_n = 0;
+  bool marks_listed = false;  // this iteration's k_scatter wrote the static-detection mark list (c->holes)
   bool kd_valid = false;
   bool kd_failed = false;  // the last build could not allocate its node arrays
   bool pos_in_new = true;  // current positions live in newpd (else S[cur].pd)
@@ -3086,11 +3108,15 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   // inside an iteration without static detection (and not SIR, whose
   // partners hold infection times) k_force rewrites every agent's partners
   const bool carry_partners = !in_step || c->cfg.detect_static_agents || c->cfg.model == ABS_MODEL_SIR;
+  // static detection inside an iteration: the scatter also lists the agents whose neighbours k_mark
+  // marks (c->holes is free during the iteration; the kd gather would re-order the slots, so not there)
+  c->marks_listed = in_step && c->cfg.detect_static_agents && iteration > 0 && !kd_env(c);
   k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
                                             c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
                                             c->cfg.record_forces, uses_f32_walk(c) || list_mode == 2, -1,
                                             uses_ext(c->cfg), carry_partners ? 1 : 0,
-                                            c->cfg.model != ABS_MODEL_NONE ? 1 : 0);
+                                            c->cfg.model != ABS_MODEL_NONE ? 1 : 0,
+                                            c->marks_listed ? c->holes : nullptr, &c->g->mark_n);
                                         sync_check(c, "k_scatter");
   ++c->launches;
   c->cur = nxt;
@@ -3410,9 +3436,14 @@ void launch_iteration(abs_gpu_ctx* c, unsigned long long iteration, int kind = 0
   Soa& S = c->S[c->cur];
   if (c->cfg.detect_static_agents && iteration > 0) {
     // c->rank is free between the re-bin's scatter and the next k_key
-    k_mark_list<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->rank);
-    k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn, c->rank);
-    c->launches += 2;
+    if (c->marks_listed) {  // listed by the re-bin's scatter
+      k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn, c->holes);
+      c->launches += 1;
+    } else {
+      k_mark_list<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->rank);
+      k_mark<<<nb, kThreads, 0, c->stream>>>(S, c->g, c->start, c->nv, c->nn, c->rank);
+      c->launches += 2;
+    }
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing) {
