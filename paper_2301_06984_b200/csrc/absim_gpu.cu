@@ -588,6 +588,7 @@ struct Soa {
 #define ABS_SCATTER_BATCH 2  // c4 step 30.25 / 29.45 / 29.52 ms at 1 / 2 / 4; c3 0.98 / 0.96 / 0.99
 #endif
 constexpr int kScatterBatch = ABS_SCATTER_BATCH;
+template <bool MARK>  // MARK: also list the static-detection marking agents (block-uniform loop for the ballots)
 __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos, Soa src, Soa dst,
                                                       float4* __restrict__ pf,
                                                       const unsigned int* __restrict__ start,
@@ -604,10 +605,11 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
   const unsigned long long n = g->n;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   const double ox = g->origin[0], oy = g->origin[1], oz = g->origin[2];
-  // block-uniform trip count (the tail is handled per element): the mark-list
-  // ballots below need whole warps
-  for (unsigned long long b0 = blockIdx.x * (unsigned long long)blockDim.x; b0 < n; b0 += stride * kScatterBatch) {
-    const unsigned long long i0 = b0 + threadIdx.x;
+  // MARK: block-uniform trip count (the tail is handled per element), the
+  // mark-list ballots below need whole warps
+  for (unsigned long long b0 = blockIdx.x * (unsigned long long)blockDim.x + (MARK ? 0u : threadIdx.x); b0 < n;
+       b0 += stride * kScatterBatch) {
+    const unsigned long long i0 = b0 + (MARK ? threadIdx.x : 0u);
     unsigned int j[kScatterBatch];
     Pd p[kScatterBatch];
     unsigned long long u[kScatterBatch];
@@ -655,7 +657,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const Pd* __restrict__ pos
     // static detection: the agents that moved, grew or were added last
     // iteration mark their neighbours (k_mark); they are listed here, by their
     // new slot, instead of in a pass of their own over every agent's flags
-    if (mark_list) {
+    if constexpr (MARK) {
 #pragma unroll
       for (int b = 0; b < kScatterBatch; ++b) {
         const unsigned long long i = i0 + b * stride;
@@ -3111,12 +3113,15 @@ void launch_env_update(abs_gpu_ctx* c, unsigned long long iteration, int may_add
   // static detection inside an iteration: the scatter also lists the agents whose neighbours k_mark
   // marks (c->holes is free during the iteration; the kd gather would re-order the slots, so not there)
   c->marks_listed = in_step && c->cfg.detect_static_agents && iteration > 0 && !kd_env(c);
-  k_scatter<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g,
-                                            c->cap, c->cfg.model == ABS_MODEL_PROLIFERATION,
-                                            c->cfg.record_forces, uses_f32_walk(c) || list_mode == 2, -1,
-                                            uses_ext(c->cfg), carry_partners ? 1 : 0,
-                                            c->cfg.model != ABS_MODEL_NONE ? 1 : 0,
-                                            c->marks_listed ? c->holes : nullptr, &c->g->mark_n);
+  auto scatter = [&](auto kernel) {
+    kernel<<<nb, kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start, c->key, c->rank, c->g, c->cap,
+                                           c->cfg.model == ABS_MODEL_PROLIFERATION, c->cfg.record_forces,
+                                           uses_f32_walk(c) || list_mode == 2, -1, uses_ext(c->cfg),
+                                           carry_partners ? 1 : 0, c->cfg.model != ABS_MODEL_NONE ? 1 : 0, c->holes,
+                                           &c->g->mark_n);
+  };
+  if (c->marks_listed) scatter(k_scatter<true>);
+  else scatter(k_scatter<false>);
                                         sync_check(c, "k_scatter");
   ++c->launches;
   c->cur = nxt;
@@ -3887,7 +3892,7 @@ static int launch_sort(abs_gpu_ctx* c, unsigned long long iteration, bool exact_
     k_mkey<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->g, c->start, c->key, c->rank);
     sync_check(c, "k_mkey");
     launch_scan_cells(c, &c->g->sort_len, c->bins_cap, &c->g->err);
-    k_scatter<<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
+    k_scatter<false><<<agent_blocks(c), kThreads, 0, c->stream>>>(pos, c->S[c->cur], c->S[nxt], c->pf, c->start,
                                                                  c->key, c->rank, c->g, c->cap,
                                                                  c->cfg.model == ABS_MODEL_PROLIFERATION,
                                                                  c->cfg.record_forces, 0, 1, uses_ext(c->cfg));
